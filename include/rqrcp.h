@@ -1,0 +1,160 @@
+/*
+ * rqrcp.h -- C ABI of the B200-native randomized QR with column pivoting
+ * (RQRCP) hot path.  Xiao, Gu, Langou, "Fast Parallel Randomized QR with
+ * Column Pivoting Algorithms for Reliable Low-rank Matrix Approximations",
+ * HiPC 2017 (arXiv 1804.05138).  Citations: P:n = line n of the paper text
+ * (PAPER.md), S:n = line n of the desk-scale SPEC.md.
+ *
+ * What rqrcp_factor computes: the partial QRCP
+ *       A Pi = Q [R11 R12; 0 R22] ~= Q1 [R11 R12]
+ * by Alg. 2: Omega ~ N(0,1)^{(b+p) x m}, B = Omega A
+ * (P:144); per panel of width bb = min(b, k-i): partial QRCP of
+ * the sample B(:, i:n) for bb pivots, the same swaps on A and Pi
+ * (P:148), Householder QR of the panel A(i:m, i:i+bb) with compact-WY
+ * T, the trailing update A22 <- Q~^T A22 = A22 - V T^T V^T A22, and the
+ * sample update of Eq. (4): B <- [R^12 - R^11 R11^{-1} R12; R^22].
+ *
+ * Conventions (all identical to LAPACK dgeqp3's):
+ *   - matrices are column-major fp64; every pointer to matrix data is a
+ *     DEVICE pointer on the context's device unless the name says _host;
+ *   - on return A holds V below the diagonal of its first rank columns
+ *     (unit diagonal implicit), R11 (upper triangle of A(0:k,0:k)) and R12
+ *     (A(0:k, k:n)) in pivoted column order, and the trailing R22 by-product;
+ *   - jpvt (int64, 0-based): column j of A Pi is column jpvt[j] of
+ *     the input;  tau[k]: Householder scalars, H_j = I - tau_j v_j v_j^T,
+ *     Q = H_0 H_1 ... H_{k-1};
+ *   - Householder sign convention = LAPACK dlarfg (reading R-G7);
+ *   - Omega is drawn from Philox4x32-10 (key = seed) + Box-Muller with the
+ *     counter mapping of DESIGN.md "Generator mapping" (reading R-G8).
+ *
+ * Ownership: the caller owns A, jpvt, tau (and every buffer it passes); the
+ * context owns its workspace (sized at create time) and, for nranks > 1, its
+ * NCCL communicator.  No allocation happens inside rqrcp_factor.  A context
+ * is not thread-safe; use one per (device, rank).
+ *
+ * Errors: every function returns 0 on success, a negative value -i when its
+ * i-th argument is invalid (LAPACK "info" style), or a positive RQRCP_E_*
+ * code; rqrcp_last_error(ctx) gives a human-readable message.  A positive
+ * RQRCP_W_* code is a warning: outputs are valid.
+ */
+#ifndef RQRCP_H
+#define RQRCP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RQRCP_OK 0
+#define RQRCP_E_CUDA 1          /* a CUDA runtime call failed */
+#define RQRCP_E_NCCL 2          /* an NCCL call failed */
+#define RQRCP_E_WORKSPACE 3     /* size exceeds the create-time maxima, or out of memory */
+#define RQRCP_E_NONFINITE 4     /* NaN/Inf in the sample (hence in A) */
+#define RQRCP_E_UNSUPPORTED 5   /* feature not built (e.g. nranks > 1 without NCCL) */
+#define RQRCP_W_RANK_DEFICIENT 16 /* early stop (reading R-G12): *rank_out < k */
+
+typedef struct rqrcp_ctx rqrcp_ctx;
+
+typedef struct rqrcp_config {
+    int device;            /* CUDA device ordinal */
+    void *stream;          /* cudaStream_t to run on; NULL -> a context-owned stream */
+    int nranks;            /* GPUs in the 1D column-block-cyclic layout (1 = single GPU) */
+    int rank;              /* this process's rank in [0, nranks) */
+    uint8_t nccl_uid[128]; /* ncclUniqueId bytes from rank 0 (ignored if nranks == 1) */
+    int64_t max_m;         /* workspace maxima: rqrcp_factor fails with RQRCP_E_WORKSPACE */
+    int64_t max_n;         /*   when m > max_m, n > max_n, b > max_b or p > max_p     */
+    int max_b;
+    int max_p;
+} rqrcp_config;
+
+/* Per-phase device times of the last rqrcp_factor (CUDA events, ms). */
+typedef struct rqrcp_timings {
+    double total_ms;
+    double omega_ms;        /* S0: Philox Omega */
+    double sketch_ms;       /* S1: B = Omega A */
+    double sample_qrcp_ms;  /* S2 */
+    double swap_ms;         /* S3 */
+    double panel_ms;        /* S4 (panel QR + T) */
+    double trailing_ms;     /* S5 (W = V^T A22, W2 = -T^T W, A22 += V W2) */
+    double sample_update_ms;/* S6 */
+    double comm_ms;         /* NCCL collectives (nranks > 1) */
+    int64_t panels;
+    int64_t kernel_launches;/* kernels this library launched in the call */
+} rqrcp_timings;
+
+/* Create a context: allocates every workspace buffer for the maxima in cfg
+ * (and the NCCL communicator when nranks > 1).  *ctx is NULL on failure.
+ * Returns 0, -1 (ctx null), -2 (cfg null or invalid field), or RQRCP_E_*. */
+int rqrcp_create(rqrcp_ctx **ctx, const rqrcp_config *cfg);
+
+/* Factor A in place (Alg. 2).
+ *   A      device, column-major m x n (single GPU) or this rank's shard of the
+ *          global columns {j : floor(j/b) mod nranks == rank}, m x n_loc
+ *          (multi-GPU), leading dimension lda >= max(1, m); overwritten.
+ *   m, n   global sizes, 1 <= m, n;  k target rank, 1 <= k <= min(m, n)
+ *   b      panel width >= 1;  p oversampling >= 0 with b + p <= m
+ *   seed   Philox key for Omega (never invalid)
+ *   jpvt   device int64[n] (output);  tau device double[k] (output)
+ *   rank_out host int64 (output): achieved rank (== k unless the warning)
+ * Synchronous: returns after the work on the context's stream completed.
+ * Argument codes: -1 ctx, -2 A, -3 lda, -4 m, -5 n, -6 k, -7 b, -8 p,
+ * -10 jpvt, -11 tau, -12 rank_out.  Returns RQRCP_W_RANK_DEFICIENT when the
+ * sample's column norms all fall below 1e3*eps*||Omega A||_F before k pivots
+ * (outputs valid for the first *rank_out columns, tau = 0 beyond). */
+int rqrcp_factor(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
+                 uint64_t seed, int64_t *jpvt, double *tau, int64_t *rank_out);
+
+/* Same computation with HOST buffers (the end-to-end path): copies A_host
+ * (m x n, lda) to a context-owned device buffer, factors, and copies the
+ * factored A, jpvt and tau back (A_out_host may equal A_host).  Single GPU
+ * only.  Pinned host memory gives full PCIe bandwidth.  Codes as
+ * rqrcp_factor, plus RQRCP_E_WORKSPACE if m*n exceeds max_m*max_n. */
+int rqrcp_factor_host(rqrcp_ctx *ctx, const double *A_host, int64_t lda, int64_t m, int64_t n, int64_t k,
+                      int b, int p, uint64_t seed, double *A_out_host, int64_t *jpvt_host, double *tau_host,
+                      int64_t *rank_out);
+
+/* Testing API: rqrcp_factor with optional hooks.
+ *   omega_in   device l x m (ld = l) sketch to use instead of the Philox draw, or NULL
+ *   omega_out  device l x m (ld = l) receives the Omega used, or NULL
+ *   gaps_out   device double[k]: per pivot step, relative gap (best - runner-up)/best
+ *              of the squared sample norms (diagnoses ties), or NULL */
+int rqrcp_factor_ex(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
+                    uint64_t seed, int64_t *jpvt, double *tau, int64_t *rank_out, const double *omega_in,
+                    double *omega_out, double *gaps_out);
+
+/* Testing/bench API: rows [row0, row0+rows) x cols [col0, col0+cols) of the
+ * N(0,1) matrix (seed, stream) with the Omega generator, into out (device,
+ * column-major, ld >= rows).  Stream 0 is Omega itself. */
+int rqrcp_fill_gaussian(rqrcp_ctx *ctx, uint64_t seed, uint32_t stream, int64_t rows, int64_t cols, int64_t row0,
+                        int64_t col0, double *out, int64_t ld);
+
+/* Testing API: raw Philox4x32-10 words.  ctr (device uint32[4*count]),
+ * key (host, 2 words), out (device uint32[4*count]). */
+int rqrcp_philox_words(rqrcp_ctx *ctx, const uint32_t *ctr, const uint32_t *key, uint32_t *out, int64_t count);
+
+/* Algorithmic flop counts: out[0] sketch 2lmn, out[1]
+ * Householder QR sum_j 4(m-j)(n-j), out[2] sample QRCP, out[3] sample
+ * update.  Host only; needs no context.  Returns 0 or a negative code. */
+int rqrcp_flops(int64_t m, int64_t n, int64_t k, int b, int p, double out[4]);
+
+/* Per-phase timings of the last rqrcp_factor on ctx. */
+int rqrcp_get_timings(const rqrcp_ctx *ctx, rqrcp_timings *out);
+
+/* Enable (1) / disable (0) per-phase CUDA-event timing (default 1). */
+int rqrcp_set_timing(rqrcp_ctx *ctx, int enabled);
+
+/* Destroy: frees workspace and the communicator.  NULL is a no-op. */
+int rqrcp_destroy(rqrcp_ctx *ctx);
+
+/* Message for the last non-zero return on ctx (static string if ctx NULL). */
+const char *rqrcp_last_error(const rqrcp_ctx *ctx);
+
+/* Library version string. */
+const char *rqrcp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RQRCP_H */

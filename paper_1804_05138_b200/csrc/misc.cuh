@@ -1,0 +1,151 @@
+// misc.cuh -- S3 swap (K5), S6 sample update (K8), and the sample's
+// Frobenius norm for the rank-stop threshold (reading R-G12).
+#pragma once
+#include "common.cuh"
+
+namespace rq {
+
+// ---------------------------------------------------------------------------
+// ||B||_F^2 of the initial sample, deterministic two-level sum; sets
+// stop_tol2 = (1e3 eps)^2 ||B||_F^2 and status = 4 if non-finite.
+// ---------------------------------------------------------------------------
+__global__ void sumsq_partial_kernel(const double *B, int64_t rows, int64_t cols, int64_t ldb, double *part) {
+    __shared__ double red[32];
+    const int64_t total = rows * cols;
+    double s = 0.0;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e % rows, c = e / rows;
+        const double v = B[r + c * ldb];
+        s += v * v;
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+        t = warp_sum(t);
+        if (threadIdx.x == 0) part[blockIdx.x] = t;
+    }
+}
+
+__global__ void sumsq_final_kernel(const double *part, int nparts, double *stop_tol2, int *status) {
+    if (threadIdx.x != 0) return;
+    double s = 0.0;
+    for (int q = 0; q < nparts; ++q) s += part[q];
+    const double eps = 0x1p-52;
+    *stop_tol2 = (1e3 * eps) * (1e3 * eps) * s;
+    if (!isfinite(s)) *status = 4;
+}
+
+// ---------------------------------------------------------------------------
+// S3 swap ("Swap (j1..jb) and (i:i+b-1) columns in A, Pi"): the bb_eff
+// transpositions j <-> piv[j], applied in order (reading R-G5), restricted
+// to the <= 2 bb positions they touch, give a list of (dst, src) column moves
+// (one CTA, tiny); jpvt is permuted there too.  The A columns (full height
+// m, so earlier R12 rows move with them, LAPACK semantics) are then moved
+// through a staging buffer by two grid kernels.
+// ---------------------------------------------------------------------------
+__global__ void swap_plan_kernel(const int64_t *piv, const int *bb_eff, int64_t *jpvt /* + i */, int64_t *dst,
+                                 int64_t *src, int *npairs) {
+    __shared__ int64_t pos[2 * 128 + 2], cur[2 * 128 + 2];
+    __shared__ int64_t jv[2 * 128 + 2];
+    if (threadIdx.x != 0) return;
+    const int nb = *bb_eff;
+    int nt = 0;
+    auto find = [&](int64_t p) {
+        for (int e = 0; e < nt; ++e)
+            if (pos[e] == p) return e;
+        pos[nt] = p; cur[nt] = p; jv[nt] = jpvt[p];
+        return nt++;
+    };
+    for (int j = 0; j < nb; ++j) {
+        const int64_t s = piv[j];
+        if (s == j) continue;
+        const int a = find(j), b = find(s);
+        int64_t t = cur[a]; cur[a] = cur[b]; cur[b] = t;
+        t = jv[a]; jv[a] = jv[b]; jv[b] = t;
+    }
+    int np = 0;
+    for (int e = 0; e < nt; ++e) {
+        jpvt[pos[e]] = jv[e];
+        if (cur[e] != pos[e]) { dst[np] = pos[e]; src[np] = cur[e]; ++np; }
+    }
+    *npairs = np;
+}
+
+__global__ void swap_gather_kernel(const double *A /* + i*lda */, int64_t lda, int64_t m, const int64_t *src,
+                                   const int *npairs, double *stage, int64_t lds) {
+    const int np = *npairs;
+    const int64_t total = (int64_t)np * m;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e % m, q = e / m;
+        stage[r + q * lds] = A[r + src[q] * lda];
+    }
+}
+
+__global__ void swap_scatter_kernel(double *A, int64_t lda, int64_t m, const int64_t *dst, const int *npairs,
+                                    const double *stage, int64_t lds) {
+    const int np = *npairs;
+    const int64_t total = (int64_t)np * m;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e % m, q = e / m;
+        A[r + dst[q] * lda] = stage[r + q * lds];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// S6 sample update, Eq. (4) (readings R-G1..G3, R-G20):
+//   Omega-hat11 = R-hat11 R11^{-1}   (b x b upper triangular)
+//   B_next(0:bb, c) = R-hat12(:, c) - Omega-hat11 R12(:, c)
+//   B_next(bb:l, c) = R-hat22(:, c);  rows l..lpad-1 = 0
+// R-hat12/22 are read from the physical sample columns perm[bb + c].
+// Skipped (no-op) when the panel ended early (bb_eff < bb).
+// ---------------------------------------------------------------------------
+__global__ void omhat_kernel(const double *rhat11, const double *A /* &A[i + i lda] */, int64_t lda, int bb,
+                             int bbpad, const int *bb_eff, double *omhat) {
+    // one thread per row r: row-vector triangular solve  x^T R11 = rhat11(r, :)
+    if (*bb_eff != bb) return;
+    for (int r = threadIdx.x; r < bbpad; r += blockDim.x) {
+        for (int c = 0; c < bbpad; ++c) {
+            double v = 0.0;
+            if (r < bb && c < bb && c >= r) {
+                double s = rhat11[r + (int64_t)c * bbpad];
+                for (int q = r; q < c; ++q) s -= omhat[r + (int64_t)q * bbpad] * A[q + (int64_t)c * lda];
+                v = s / A[c + (int64_t)c * lda];
+            }
+            omhat[r + (int64_t)c * bbpad] = v;
+        }
+    }
+}
+
+constexpr int SU_COLS = 16;
+__global__ void __launch_bounds__(256) sample_update_kernel(const double *Bold, int64_t ldb, const int64_t *perm,
+                                                            const double *omhat, int bbpad,
+                                                            const double *R12 /* &A[i + (i+bb) lda] */, int64_t lda,
+                                                            int bb, int l, int lpad, int64_t npp, const int *bb_eff,
+                                                            double *Bnew, int64_t ldn) {
+    if (*bb_eff != bb) return;
+    __shared__ double r12[128 * SU_COLS];
+    const int64_t c0 = (int64_t)blockIdx.x * SU_COLS;
+    const int ncols = (int)min((int64_t)SU_COLS, npp - c0);
+    for (int e = threadIdx.x; e < bb * ncols; e += blockDim.x) {
+        const int q = e % bb, c = e / bb;
+        r12[q + c * 128] = R12[q + (c0 + c) * lda];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < lpad * ncols; e += blockDim.x) {
+        const int r = e % lpad, c = e / lpad;
+        const int64_t src = perm[bb + c0 + c];
+        double v = 0.0;
+        if (r < bb) {
+            double s = 0.0;
+            for (int q = r; q < bb; ++q) s += omhat[r + (int64_t)q * bbpad] * r12[q + c * 128];
+            v = Bold[r + src * ldb] - s;
+        } else if (r < l) {
+            v = Bold[r + src * ldb];
+        }
+        Bnew[r + (c0 + c) * ldn] = v;
+    }
+}
+
+}  // namespace rq

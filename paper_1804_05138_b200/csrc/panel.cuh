@@ -1,0 +1,160 @@
+// panel.cuh -- S4 (kernel K6): unpivoted Householder QR of the panel
+// A(i:m, i:i+bb) (Alg. 2 line P:149, PDGEQRF at P:760) with the compact-WY
+// factor T built in the same pass (PDLARFT): H_0 ... H_{bb-1} =
+// I - V T V^T, T upper triangular, T(j,j) = tau_j,
+// T(0:j, j) = -tau_j T(0:j, 0:j) (V(:,0:j)^T v_j).
+//
+// One persistent cooperative kernel, CTA g owns a contiguous block of panel
+// rows; one grid barrier per column.  At step j each CTA writes the partial
+// Gram row  g_c = sum_{r > j, r owned} A(r, c) A(r, j)  for every panel
+// column c (c > j: the dot products v_j^T a_c up to scaling; c = j: ||x||^2
+// below the diagonal; c < j: V(:,c)^T x, which gives T's column j), and the
+// owner of row j publishes that row.  After the barrier every CTA sums the G
+// partials in fixed order (identical bits everywhere), forms beta, tau,
+// v = x/(alpha - beta) (dlarfg, reading R-G7) and w_c = tau (a_jc + g_c/(alpha-beta)),
+// and updates its own rows: a_rc -= w_c v_r.  Columns bb_eff..bb-1 of the
+// panel (rank stop, R-G12) still receive the reflectors.
+// Outputs: V below the diagonal and R11 on/above it, in place; tau; the
+// explicit V (Vfull, m' x bbpad: unit diagonal, zeros above, K-contiguous for
+// W = V^T A22) and its transpose Vt (bbpad x m', for A22 += V W2); Tneg = -T.
+#pragma once
+#include "common.cuh"
+
+namespace rq {
+
+constexpr int PN_THREADS = 256;
+constexpr int PN_WARPS = PN_THREADS / 32;
+constexpr int PN_MAXB = 128;
+constexpr int PN_MAXROWS = 512;  // rows per CTA held in shared memory as x
+
+struct PanelArgs {
+    double *A;          // &A[i + i*lda]
+    int64_t lda;
+    int64_t mp;         // m' rows
+    int bb;             // planned panel width (columns present)
+    int bbpad;
+    const int *bb_eff;
+    double *tau;        // tau + i
+    double *vfull;      // mp x bbpad, ld ldv
+    int64_t ldv;
+    double *vt;         // bbpad x mp, ld bbpad
+    double *tneg;       // bbpad x bbpad
+    double *part;       // [2][G][bbpad] partial Gram rows
+    double *rowj;       // [2][bbpad] published row j
+    unsigned *bar;
+};
+
+__global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
+    __shared__ double w[PN_MAXB];
+    __shared__ double xs[PN_MAXROWS];
+    __shared__ double s_scal, s_tau, s_beta;
+    const int G = gridDim.x, g = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int bb = a.bb;
+    const int bbe = *a.bb_eff;
+    const int64_t mp = a.mp;
+    const int64_t rpb = (mp + G - 1) / G;
+    const int64_t r_lo = min(mp, (int64_t)g * rpb), r_hi = min(mp, r_lo + rpb);
+    const int nrows = (int)(r_hi - r_lo);
+    double *A = a.A;
+    const int64_t lda = a.lda;
+
+    for (int j = 0; j < bbe; ++j) {
+        const int par = j & 1;
+        // ---- partial Gram row over own rows r > j -----------------------
+        const int64_t rs = max(r_lo, (int64_t)j + 1);
+        for (int c = warp; c < bb; c += PN_WARPS) {
+            double s = 0.0;
+            for (int64_t r = rs + lane; r < r_hi; r += 32) s += A[r + c * lda] * A[r + (int64_t)j * lda];
+            s = warp_sum(s);
+            if (lane == 0) a.part[((int64_t)par * G + g) * a.bbpad + c] = s;
+        }
+        if (j >= r_lo && j < r_hi)
+            for (int c = tid; c < bb; c += PN_THREADS) a.rowj[par * a.bbpad + c] = A[j + c * lda];
+        grid_barrier(a.bar, G);
+        // ---- fixed-order sums -> reflector, w_c (every CTA) ---------------
+        for (int c = tid; c < bb; c += PN_THREADS) {
+            double s = 0.0;
+            for (int q = 0; q < G; ++q) s += ld_cg(a.part + ((int64_t)par * G + q) * a.bbpad + c);
+            w[c] = s;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const double alpha = ld_cg(a.rowj + par * a.bbpad + j);
+            const double xn2 = w[j];
+            double tau = 0.0, beta = alpha, scal = 0.0;
+            if (xn2 != 0.0) {
+                const double nrm = sqrt(alpha * alpha + xn2);
+                beta = (alpha >= 0.0) ? -nrm : nrm;
+                tau = (beta - alpha) / beta;
+                scal = 1.0 / (alpha - beta);
+            }
+            s_tau = tau; s_beta = beta; s_scal = scal;
+            if (g == 0) a.tau[j] = tau;
+        }
+        __syncthreads();
+        const double tau = s_tau, scal = s_scal;
+        // T column j (CTA 0): y_c = v_c^T v_j = A(j,c) + scal * g_c  (c < j)
+        if (g == 0) {
+            // y into w[0..j) is safe: w[c] for c < j is not used by the update
+            for (int c = tid; c < j; c += PN_THREADS) w[c] = ld_cg(a.rowj + par * a.bbpad + c) + scal * w[c];
+            __syncthreads();
+            for (int r = tid; r < a.bbpad; r += PN_THREADS) {
+                double t = 0.0;
+                if (r < j) {
+                    // T(0:j,j) = -tau T(0:j,0:j) y, tneg = -T:
+                    // tneg(r,j) = tau (T y)_r = -tau sum_c tneg(r,c) y_c
+                    double acc = 0.0;
+                    for (int c = r; c < j; ++c) acc += a.tneg[r + (int64_t)c * a.bbpad] * w[c];
+                    t = -tau * acc;
+                } else if (r == j) {
+                    t = -tau;
+                }
+                a.tneg[r + (int64_t)j * a.bbpad] = t;
+            }
+            __syncthreads();
+        }
+        // w_c = tau * (a_jc + scal g_c) for c > j
+        for (int c = j + 1 + tid; c < bb; c += PN_THREADS) w[c] = tau * (ld_cg(a.rowj + par * a.bbpad + c) + scal * w[c]);
+        // own rows: x_r (old column j) into shared memory
+        for (int r = tid; r < nrows; r += PN_THREADS) xs[r] = A[r_lo + r + (int64_t)j * lda];
+        __syncthreads();
+        // ---- update own rows ---------------------------------------------
+        if (tau != 0.0) {
+            for (int c = j + 1 + warp; c < bb; c += PN_WARPS) {
+                const double wc = w[c];
+                for (int64_t r = r_lo + lane; r < r_hi; r += 32) {
+                    if (r > j) A[r + c * lda] -= wc * (scal * xs[r - r_lo]);
+                    else if (r == j) A[r + c * lda] -= wc;
+                }
+            }
+            for (int64_t r = r_lo + tid; r < r_hi; r += PN_THREADS) {
+                if (r > j) A[r + (int64_t)j * lda] = scal * xs[r - r_lo];
+                else if (r == j) A[r + (int64_t)j * lda] = s_beta;
+            }
+        }
+        __syncthreads();
+    }
+    // ---- explicit V / V^T, zero tail of tau / T (rank stop) -------------
+    for (int64_t r = r_lo + warp; r < r_hi; r += PN_WARPS)
+        for (int c = lane; c < a.bbpad; c += 32) {
+            double v = 0.0;
+            if (c < bbe) v = (r > c) ? A[r + (int64_t)c * lda] : (r == c ? 1.0 : 0.0);
+            a.vt[c + r * a.bbpad] = v;
+        }
+    for (int c = warp; c < a.bbpad; c += PN_WARPS)
+        for (int64_t r = r_lo + lane; r < r_hi; r += 32) {
+            double v = 0.0;
+            if (c < bbe) v = (r > c) ? A[r + (int64_t)c * lda] : (r == c ? 1.0 : 0.0);
+            a.vfull[r + c * a.ldv] = v;
+        }
+    if (g == 0) {
+        for (int c = bbe + tid; c < bb; c += PN_THREADS) a.tau[c] = 0.0;
+        for (int e = tid; e < a.bbpad * a.bbpad; e += PN_THREADS) {
+            const int r = e % a.bbpad, c = e / a.bbpad;
+            if (c >= bbe || r > c) a.tneg[e] = 0.0;
+        }
+    }
+}
+
+}  // namespace rq

@@ -1,0 +1,669 @@
+// rqrcp.cu -- the C ABI (include/rqrcp.h) and the host driver of the RQRCP
+// hot path (Alg. 2).  The driver only enqueues kernels on the
+// context's stream (no host synchronisation inside the panel loop; pivots
+// stay on the device) and synchronises once at the end for the status.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "rqrcp.h"
+#include "common.cuh"
+#include "gemm_dmma.cuh"
+#include "misc.cuh"
+#include "panel.cuh"
+#include "philox.cuh"
+#include "sample_qrcp.cuh"
+
+using namespace rq;
+
+static inline int64_t rup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+enum Phase { PH_OMEGA, PH_SKETCH, PH_SQRCP, PH_SWAP, PH_PANEL, PH_TRAIL, PH_SUPD, PH_COMM, PH_N };
+
+struct rqrcp_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int nranks = 1, rank = 0;
+    int64_t max_m = 0, max_n = 0;
+    int max_b = 0, max_p = 0;
+    int lpad_max = 0, bpad_max = 0;
+    int64_t ldo = 0;  // leading dim of Omega^T and Vfull (= round8(max_m))
+    int num_sms = 0;
+    std::string err;
+    // workspace
+    double *omt = nullptr;     // Omega^T  ldo x lpad_max
+    double *bs[2] = {nullptr, nullptr};  // samples lpad_max x max_n
+    double *vfull = nullptr;   // ldo x bpad_max
+    double *vt = nullptr;      // bpad_max x max_m
+    double *w = nullptr, *w2 = nullptr;  // bpad_max x max_n
+    double *tneg = nullptr, *rhat11 = nullptr, *omhat = nullptr;  // bpad_max^2
+    double *vhat = nullptr;    // lpad_max x bpad_max
+    double *tauhat = nullptr;
+    double *splitk = nullptr;
+    int64_t splitk_elems = 0;
+    double *sq_r = nullptr, *sq_r0 = nullptr;
+    int *sq_lpos = nullptr;
+    unsigned char *sq_active = nullptr;
+    double *slot_val = nullptr, *slot_data = nullptr;
+    int64_t *slot_pos = nullptr, *slot_col = nullptr;
+    double *pn_part = nullptr, *pn_rowj = nullptr;
+    double *swap_stage = nullptr;
+    int64_t *swap_dst = nullptr, *swap_src = nullptr;
+    int *swap_np = nullptr;
+    int64_t *perm = nullptr, *piv = nullptr;
+    double *sumsq_part = nullptr;
+    // device scalars: [0] status [1] bb_eff [2] done [3] rank
+    int *iscal = nullptr;
+    double *stop_tol2 = nullptr;
+    unsigned *bars = nullptr;  // [0..1] sample qrcp, [2..3] panel
+    // host-path buffer (lazily allocated)
+    double *a_dev = nullptr;
+    int64_t a_dev_elems = 0;
+    int64_t *jpvt_dev = nullptr;
+    double *tau_dev = nullptr;
+    // cooperative limits
+    int sq_max_grid = 0, pn_max_grid = 0;
+    // timing
+    bool timing = true;
+    cudaEvent_t ev[2 * 4096 + 8];
+    int nev = 0;
+    int open_phase = -1, open_ev = -1;
+    std::vector<int> rec_phase, rec_s, rec_e;
+    rqrcp_timings last{};
+    int64_t launches = 0;
+};
+
+static const char *g_static_err = "no context";
+
+#define CK(call)                                                                      \
+    do {                                                                              \
+        cudaError_t e_ = (call);                                                      \
+        if (e_ != cudaSuccess) {                                                      \
+            ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);            \
+            return RQRCP_E_CUDA;                                                      \
+        }                                                                             \
+    } while (0)
+
+#define CKL()                                                                         \
+    do {                                                                              \
+        cudaError_t e_ = cudaGetLastError();                                          \
+        if (e_ != cudaSuccess) {                                                      \
+            ctx->err = std::string("kernel launch: ") + cudaGetErrorString(e_);       \
+            return RQRCP_E_CUDA;                                                      \
+        }                                                                             \
+        ctx->launches++;                                                              \
+    } while (0)
+
+static int grid_for(int64_t total, int threads, int num_sms) {
+    int64_t g = (total + threads - 1) / threads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)num_sms * 8));
+}
+
+// ---------------------------------------------------------------------------
+// GEMM dispatch: C = X^T Y (see gemm_dmma.cuh), M small (skinny) or large.
+// ---------------------------------------------------------------------------
+template <int MT, int NT, int WM, int WN, int BK, int ST, int EPI>
+static int launch_tn_cfg(rqrcp_ctx *ctx, GemmArgs g, int splits) {
+    constexpr int BM = 8 * MT * WM, BN = 8 * NT * WN;
+    const size_t smem = (size_t)ST * BK * (BM + BN) * sizeof(double);
+    auto kern = gemm_tn_kernel<MT, NT, WM, WN, BK, ST, EPI>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
+    }
+    dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM), (unsigned)splits);
+    kern<<<grid, WM * WN * 32, smem, ctx->stream>>>(g);
+    CKL();
+    return 0;
+}
+
+template <int MT, int NT, int WM, int WN>
+static int launch_skinny(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const double *X, int64_t ldx,
+                         const double *Y, int64_t ldy, double *C, int64_t ldc) {
+    constexpr int BK = 32, ST = 3;
+    constexpr int BM = 8 * MT * WM, BN = 8 * NT * WN;
+    const int64_t tiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM);
+    int64_t splits = std::max<int64_t>(1, (2 * (int64_t)ctx->num_sms + tiles - 1) / tiles);
+    splits = std::min<int64_t>(splits, std::max<int64_t>(1, K / 256));
+    while (splits > 1 && splits * M * N > ctx->splitk_elems) --splits;
+    int64_t kps = rup((K + splits - 1) / splits, BK);
+    splits = (K + kps - 1) / kps;
+    GemmArgs g{M, N, K, X, ldx, Y, ldy, C, ldc, kps, M * N};
+    if (splits <= 1) {
+        g.k_per_split = rup(std::max<int64_t>(K, 1), BK);
+        return launch_tn_cfg<MT, NT, WM, WN, BK, ST, EPI_STORE>(ctx, g, 1);
+    }
+    g.C = ctx->splitk;
+    int rc = launch_tn_cfg<MT, NT, WM, WN, BK, ST, EPI_PARTIAL>(ctx, g, (int)splits);
+    if (rc) return rc;
+    splitk_reduce_kernel<<<grid_for(M * N, 256, ctx->num_sms), 256, 0, ctx->stream>>>(ctx->splitk, M, N, (int)splits,
+                                                                                      M * N, C, ldc);
+    CKL();
+    return 0;
+}
+
+// C (M x N) = X^T Y with M <= 144 rows (sample rows l_pad or panel width).
+static int gemm_skinny(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const double *X, int64_t ldx,
+                       const double *Y, int64_t ldy, double *C, int64_t ldc) {
+    if (M <= 32) return launch_skinny<4, 2, 1, 4>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc);
+    if (M <= 40) return launch_skinny<5, 2, 1, 4>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc);
+    if (M <= 64) return launch_skinny<4, 4, 2, 2>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc);
+    if (M <= 80) return launch_skinny<5, 4, 2, 2>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc);
+    if (M <= 128) return launch_skinny<4, 4, 4, 2>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc);
+    if (M <= 144) return launch_skinny<6, 4, 3, 2>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc);
+    return launch_skinny<4, 4, 4, 2>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc);  // grid.y tiles M
+}
+
+// A22 (rows x cols, lda) += V W2 as (A22^T)(cols x rows) += W2^T Vt.
+static int gemm_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, const double *w2, int64_t ldw,
+                       const double *vt, int64_t ldvt, double *A22, int64_t lda) {
+    if (rows <= 0 || cols <= 0) return 0;
+    GemmArgs g{cols, rows, K, w2, ldw, vt, ldvt, A22, lda, rup(K, 32), 0};
+    return launch_tn_cfg<4, 4, 2, 4, 32, 2, EPI_ACCUM_T>(ctx, g, 1);
+}
+
+// ---------------------------------------------------------------------------
+// timing helpers
+// ---------------------------------------------------------------------------
+static constexpr int kMaxEv = 2 * 4096 + 8;
+static void ph_begin(rqrcp_ctx *ctx, int phase) {
+    ctx->open_phase = -1;
+    if (!ctx->timing || ctx->nev + 3 > kMaxEv) return;
+    ctx->open_phase = phase;
+    ctx->open_ev = ctx->nev;
+    cudaEventRecord(ctx->ev[ctx->nev++], ctx->stream);
+}
+static void ph_end(rqrcp_ctx *ctx) {
+    if (ctx->open_phase < 0) return;
+    ctx->rec_phase.push_back(ctx->open_phase);
+    ctx->rec_s.push_back(ctx->open_ev);
+    ctx->rec_e.push_back(ctx->nev);
+    cudaEventRecord(ctx->ev[ctx->nev++], ctx->stream);
+    ctx->open_phase = -1;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" const char *rqrcp_version(void) { return "rqrcp-b200 0.1 (sm_100a, fp64 DMMA)"; }
+
+extern "C" const char *rqrcp_last_error(const rqrcp_ctx *ctx) { return ctx ? ctx->err.c_str() : g_static_err; }
+
+extern "C" int rqrcp_flops(int64_t m, int64_t n, int64_t k, int b, int p, double out[4]) {
+    if (m < 1) return -1;
+    if (n < 1) return -2;
+    if (k < 1 || k > std::min(m, n)) return -3;
+    if (b < 1) return -4;
+    if (p < 0 || (int64_t)b + p > m) return -5;
+    if (!out) return -6;
+    const double l = (double)b + p;
+    out[0] = 2.0 * l * (double)m * (double)n;
+    double qr = 0.0, sq = 0.0, su = 0.0;
+    for (int64_t j = 0; j < k; ++j) qr += 4.0 * (double)(m - j) * (double)(n - j);
+    for (int64_t i = 0; i < k; i += b) {
+        const int64_t bb = std::min<int64_t>(b, k - i);
+        for (int64_t j = 0; j < bb; ++j) sq += 4.0 * (l - j) * (double)(n - i - j);
+        su += 2.0 * (double)bb * bb * (double)(n - i - bb);
+    }
+    out[1] = qr;
+    out[2] = sq;
+    out[3] = su;
+    return 0;
+}
+
+static int free_all(rqrcp_ctx *ctx) {
+    void *ptrs[] = {ctx->omt,     ctx->bs[0],   ctx->bs[1],     ctx->vfull,     ctx->vt,        ctx->w,
+                    ctx->w2,      ctx->tneg,    ctx->rhat11,    ctx->omhat,     ctx->vhat,      ctx->tauhat,
+                    ctx->splitk,  ctx->sq_r,    ctx->sq_r0,     ctx->sq_lpos,   ctx->sq_active, ctx->slot_val,
+                    ctx->slot_data, ctx->slot_pos, ctx->slot_col, ctx->pn_part, ctx->pn_rowj,   ctx->swap_stage,
+                    ctx->swap_dst, ctx->swap_src, ctx->swap_np, ctx->perm,     ctx->piv,       ctx->sumsq_part,
+                    ctx->iscal,   ctx->stop_tol2, ctx->bars,    ctx->a_dev,     ctx->jpvt_dev,  ctx->tau_dev};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    return 0;
+}
+
+extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
+    if (!out) return -1;
+    *out = nullptr;
+    if (!cfg || cfg->max_m < 1 || cfg->max_n < 1 || cfg->max_b < 1 || cfg->max_b > 128 || cfg->max_p < 0 ||
+        cfg->max_b + cfg->max_p > SQ_MAXL || cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks)
+        return -2;
+    if (cfg->nranks > 1) return RQRCP_E_UNSUPPORTED;
+    rqrcp_ctx *ctx = new rqrcp_ctx();
+    ctx->device = cfg->device;
+    ctx->nranks = cfg->nranks;
+    ctx->rank = cfg->rank;
+    ctx->max_m = cfg->max_m;
+    ctx->max_n = cfg->max_n;
+    ctx->max_b = cfg->max_b;
+    ctx->max_p = cfg->max_p;
+    auto fail = [&](int code) {
+        free_all(ctx);
+        int rc = code;
+        delete ctx;
+        return rc;
+    };
+#define CKC(call)                                                                 \
+    do {                                                                          \
+        cudaError_t e_ = (call);                                                  \
+        if (e_ != cudaSuccess) {                                                  \
+            fprintf(stderr, "rqrcp_create: %s: %s\n", #call, cudaGetErrorString(e_)); \
+            return fail(e_ == cudaErrorMemoryAllocation ? RQRCP_E_WORKSPACE : RQRCP_E_CUDA); \
+        }                                                                         \
+    } while (0)
+    CKC(cudaSetDevice(ctx->device));
+    CKC(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    if (cfg->stream) {
+        ctx->stream = (cudaStream_t)cfg->stream;
+    } else {
+        CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->own_stream = true;
+    }
+    ctx->lpad_max = (int)rup(cfg->max_b + cfg->max_p, 8);
+    ctx->bpad_max = (int)rup(cfg->max_b, 8);
+    ctx->ldo = rup(cfg->max_m, 8);
+    const int64_t lp = ctx->lpad_max, bp = ctx->bpad_max, mm = cfg->max_m, nn = cfg->max_n;
+    const int G = ctx->num_sms;
+    auto dalloc = [&](double **p, int64_t n) { return cudaMalloc((void **)p, sizeof(double) * std::max<int64_t>(n, 1)); };
+    CKC(dalloc(&ctx->omt, ctx->ldo * lp));
+    CKC(dalloc(&ctx->bs[0], lp * nn));
+    CKC(dalloc(&ctx->bs[1], lp * nn));
+    CKC(dalloc(&ctx->vfull, ctx->ldo * bp));
+    CKC(dalloc(&ctx->vt, bp * mm));
+    CKC(dalloc(&ctx->w, bp * nn));
+    CKC(dalloc(&ctx->w2, bp * nn));
+    CKC(dalloc(&ctx->tneg, bp * bp));
+    CKC(dalloc(&ctx->rhat11, bp * bp));
+    CKC(dalloc(&ctx->omhat, bp * bp));
+    CKC(dalloc(&ctx->vhat, lp * bp));
+    CKC(dalloc(&ctx->tauhat, bp));
+    ctx->splitk_elems = std::max<int64_t>(4 << 20, 0);
+    CKC(dalloc(&ctx->splitk, ctx->splitk_elems));
+    CKC(dalloc(&ctx->sq_r, nn));
+    CKC(dalloc(&ctx->sq_r0, nn));
+    CKC(cudaMalloc((void **)&ctx->sq_lpos, sizeof(int) * nn));
+    CKC(cudaMalloc((void **)&ctx->sq_active, nn));
+    CKC(dalloc(&ctx->slot_val, 2 * 2 * G));
+    CKC(dalloc(&ctx->slot_data, 2 * G * lp));
+    CKC(cudaMalloc((void **)&ctx->slot_pos, sizeof(int64_t) * 2 * G));
+    CKC(cudaMalloc((void **)&ctx->slot_col, sizeof(int64_t) * 2 * G));
+    CKC(dalloc(&ctx->pn_part, 2 * G * bp));
+    CKC(dalloc(&ctx->pn_rowj, 2 * bp));
+    CKC(dalloc(&ctx->swap_stage, 2 * bp * mm));
+    CKC(cudaMalloc((void **)&ctx->swap_dst, sizeof(int64_t) * 2 * bp));
+    CKC(cudaMalloc((void **)&ctx->swap_src, sizeof(int64_t) * 2 * bp));
+    CKC(cudaMalloc((void **)&ctx->swap_np, sizeof(int)));
+    CKC(cudaMalloc((void **)&ctx->perm, sizeof(int64_t) * nn));
+    CKC(cudaMalloc((void **)&ctx->piv, sizeof(int64_t) * bp));
+    CKC(dalloc(&ctx->sumsq_part, 4 * G));
+    CKC(cudaMalloc((void **)&ctx->iscal, sizeof(int) * 8));
+    CKC(dalloc(&ctx->stop_tol2, 1));
+    CKC(cudaMalloc((void **)&ctx->bars, sizeof(unsigned) * 8));
+    CKC(cudaMemset(ctx->bars, 0, sizeof(unsigned) * 8));
+    CKC(cudaMemset(ctx->tneg, 0, sizeof(double) * bp * bp));
+    int occ = 0;
+    CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sample_qrcp_kernel, SQ_THREADS, 0));
+    ctx->sq_max_grid = std::max(1, occ) * G;
+    CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, panel_qr_kernel, PN_THREADS, 0));
+    ctx->pn_max_grid = std::max(1, occ) * G;
+    for (auto &e : ctx->ev) CKC(cudaEventCreate(&e));
+#undef CKC
+    *out = ctx;
+    return 0;
+}
+
+extern "C" int rqrcp_destroy(rqrcp_ctx *ctx) {
+    if (!ctx) return 0;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    free_all(ctx);
+    for (auto &e : ctx->ev) cudaEventDestroy(e);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return 0;
+}
+
+extern "C" int rqrcp_set_timing(rqrcp_ctx *ctx, int enabled) {
+    if (!ctx) return -1;
+    ctx->timing = enabled != 0;
+    return 0;
+}
+
+extern "C" int rqrcp_get_timings(const rqrcp_ctx *ctx, rqrcp_timings *out) {
+    if (!ctx) return -1;
+    if (!out) return -2;
+    *out = ctx->last;
+    return 0;
+}
+
+static int coop_launch(rqrcp_ctx *ctx, const void *func, int grid, int threads, void **args) {
+    cudaError_t e = cudaLaunchCooperativeKernel(func, dim3(grid), dim3(threads), args, 0, ctx->stream);
+    if (e != cudaSuccess) {
+        ctx->err = std::string("cooperative launch: ") + cudaGetErrorString(e);
+        return RQRCP_E_CUDA;
+    }
+    ctx->launches++;
+    return 0;
+}
+
+__global__ void iota_kernel(int64_t *x, int64_t n) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        x[e] = e;
+}
+
+static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
+                       uint64_t seed, int64_t *jpvt, double *tau, int64_t *rank_out, const double *omega_in,
+                       double *omega_out, double *gaps_out) {
+    if (!ctx) return -1;
+    if (!A) return -2;
+    if (lda < std::max<int64_t>(1, m)) return -3;
+    if (m < 1) return -4;
+    if (n < 1) return -5;
+    if (k < 1 || k > std::min(m, n)) return -6;
+    if (b < 1) return -7;
+    if (p < 0 || (int64_t)b + p > m) return -8;
+    if (!jpvt) return -10;
+    if (!tau) return -11;
+    if (!rank_out) return -12;
+    if (m > ctx->max_m || n > ctx->max_n || b > ctx->max_b || p > ctx->max_p) {
+        ctx->err = "problem exceeds the create-time workspace maxima";
+        return RQRCP_E_WORKSPACE;
+    }
+    CK(cudaSetDevice(ctx->device));
+    ctx->launches = 0;
+    ctx->nev = 0;
+    ctx->rec_phase.clear();
+    ctx->rec_s.clear();
+    ctx->rec_e.clear();
+    ctx->open_phase = -1;
+    const int l = b + p;
+    const int lpad = (int)rup(l, 8);
+    const int G = ctx->num_sms;
+    cudaStream_t st = ctx->stream;
+    const int ev_t0 = ctx->nev;
+    if (ctx->timing) cudaEventRecord(ctx->ev[ctx->nev++], st);
+    ph_begin(ctx, PH_OMEGA);
+    CK(cudaMemsetAsync(ctx->iscal, 0, sizeof(int) * 8, st));
+    // ---- S0: Omega^T -----------------------------------------------------
+    if (omega_in) {
+        omega_t_from_kernel<<<grid_for((int64_t)lpad * m, 256, G), 256, 0, st>>>(omega_in, l, lpad, m, ctx->omt,
+                                                                                 ctx->ldo);
+    } else {
+        omega_t_kernel<<<grid_for((int64_t)lpad / 2 * m, 256, G), 256, 0, st>>>(seed, l, lpad, m, ctx->omt, ctx->ldo);
+    }
+    CKL();
+    if (omega_out) {
+        omega_from_t_kernel<<<grid_for((int64_t)l * m, 256, G), 256, 0, st>>>(ctx->omt, ctx->ldo, l, m, omega_out);
+        CKL();
+    }
+    ph_end(ctx);
+    // ---- S1: sketch B = Omega A -------------------------------------------
+    ph_begin(ctx, PH_SKETCH);
+    int cur = 0;
+    int rc = gemm_skinny(ctx, lpad, n, m, ctx->omt, ctx->ldo, A, lda, ctx->bs[cur], lpad);
+    if (rc) return rc;
+    sumsq_partial_kernel<<<4 * G, 256, 0, st>>>(ctx->bs[cur], lpad, n, lpad, ctx->sumsq_part);
+    CKL();
+    sumsq_final_kernel<<<1, 32, 0, st>>>(ctx->sumsq_part, 4 * G, ctx->stop_tol2, ctx->iscal + 0);
+    CKL();
+    ph_end(ctx);
+
+    int *status = ctx->iscal + 0, *bb_eff = ctx->iscal + 1, *done = ctx->iscal + 2, *rankd = ctx->iscal + 3;
+    // Pi = I_n
+    iota_kernel<<<grid_for(n, 256, G), 256, 0, st>>>(jpvt, n);
+    CKL();
+    CK(cudaMemsetAsync(tau, 0, sizeof(double) * k, st));
+
+    int panels = 0;
+    for (int64_t i = 0; i < k; i += b) {
+        const int bb = (int)std::min<int64_t>(b, k - i);
+        const int bbpad = (int)rup(bb, 8);
+        const int64_t mp = m - i, np = n - i, npp = np - bb;
+        ++panels;
+        // ---- S2: sample QRCP ---------------------------------------------
+        ph_begin(ctx, PH_SQRCP);
+        {
+            SqArgs a{};
+            a.B = ctx->bs[cur];
+            a.ldb = lpad;
+            a.l = l;
+            a.lpad = lpad;
+            a.nn = np;
+            a.bb = bb;
+            a.stop_tol2 = ctx->stop_tol2;
+            a.r = ctx->sq_r;
+            a.r0 = ctx->sq_r0;
+            a.lpos = ctx->sq_lpos;
+            a.active = ctx->sq_active;
+            a.slot_val = ctx->slot_val;
+            a.slot_pos = ctx->slot_pos;
+            a.slot_col = ctx->slot_col;
+            a.slot_data = ctx->slot_data;
+            a.piv = ctx->piv;
+            a.tauhat = ctx->tauhat;
+            a.vhat = ctx->vhat;
+            a.rhat11 = ctx->rhat11;
+            a.bbpad = bbpad;
+            a.perm = ctx->perm;
+            a.bb_eff = bb_eff;
+            a.done = done;
+            a.rank = rankd;
+            a.status = status;
+            a.gaps = gaps_out ? gaps_out + i : nullptr;
+            a.bar = ctx->bars;
+            int grid = (int)std::min<int64_t>((np + 31) / 32, std::min(ctx->sq_max_grid, G));
+            grid = std::max(grid, 1);
+            void *args[] = {&a};
+            rc = coop_launch(ctx, (const void *)sample_qrcp_kernel, grid, SQ_THREADS, args);
+            if (rc) return rc;
+        }
+        ph_end(ctx);
+        // ---- S3: swaps on A and Pi -----------------------------------------
+        ph_begin(ctx, PH_SWAP);
+        swap_plan_kernel<<<1, 32, 0, st>>>(ctx->piv, bb_eff, jpvt + i, ctx->swap_dst, ctx->swap_src, ctx->swap_np);
+        CKL();
+        {
+            const int64_t lds = ctx->max_m;
+            const int gg = grid_for(2 * (int64_t)bb * m, 256, G);
+            swap_gather_kernel<<<gg, 256, 0, st>>>(A + i * lda, lda, m, ctx->swap_src, ctx->swap_np, ctx->swap_stage,
+                                                    lds);
+            CKL();
+            swap_scatter_kernel<<<gg, 256, 0, st>>>(A + i * lda, lda, m, ctx->swap_dst, ctx->swap_np,
+                                                     ctx->swap_stage, lds);
+            CKL();
+        }
+        ph_end(ctx);
+        // ---- S4: panel QR + T ----------------------------------------------
+        ph_begin(ctx, PH_PANEL);
+        {
+            PanelArgs a{};
+            a.A = A + i + i * lda;
+            a.lda = lda;
+            a.mp = mp;
+            a.bb = bb;
+            a.bbpad = bbpad;
+            a.bb_eff = bb_eff;
+            a.tau = tau + i;
+            a.vfull = ctx->vfull;
+            a.ldv = ctx->ldo;
+            a.vt = ctx->vt;
+            a.tneg = ctx->tneg;
+            a.part = ctx->pn_part;
+            a.rowj = ctx->pn_rowj;
+            a.bar = ctx->bars + 2;
+            int64_t want = std::max<int64_t>((mp + PN_MAXROWS - 1) / PN_MAXROWS, std::min<int64_t>(G, (mp + 63) / 64));
+            int grid = (int)std::min<int64_t>(want, ctx->pn_max_grid);
+            if ((mp + grid - 1) / grid > PN_MAXROWS) {
+                ctx->err = "panel too tall for the cooperative grid";
+                return RQRCP_E_WORKSPACE;
+            }
+            void *args[] = {&a};
+            rc = coop_launch(ctx, (const void *)panel_qr_kernel, grid, PN_THREADS, args);
+            if (rc) return rc;
+        }
+        ph_end(ctx);
+        // ---- S5: trailing update A22 -= V T^T V^T A22 ------------------------
+        ph_begin(ctx, PH_TRAIL);
+        if (npp > 0) {
+            double *A22 = A + i + (i + bb) * lda;
+            rc = gemm_skinny(ctx, bbpad, npp, mp, ctx->vfull, ctx->ldo, A22, lda, ctx->w, bbpad);
+            if (rc) return rc;
+            rc = gemm_skinny(ctx, bbpad, npp, bbpad, ctx->tneg, bbpad, ctx->w, bbpad, ctx->w2, bbpad);
+            if (rc) return rc;
+            rc = gemm_update(ctx, mp, npp, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda);
+            if (rc) return rc;
+        }
+        ph_end(ctx);
+        // ---- S6: sample update (Eq. (4)); skipped after the last panel (R-G9)
+        if (i + bb < k && npp > 0) {
+            ph_begin(ctx, PH_SUPD);
+            omhat_kernel<<<1, 128, 0, st>>>(ctx->rhat11, A + i + i * lda, lda, bb, bbpad, bb_eff, ctx->omhat);
+            CKL();
+            sample_update_kernel<<<(unsigned)((npp + SU_COLS - 1) / SU_COLS), 256, 0, st>>>(
+                ctx->bs[cur], lpad, ctx->perm, ctx->omhat, bbpad, A + i + (i + bb) * lda, lda, bb, l, lpad, npp,
+                bb_eff, ctx->bs[cur ^ 1], lpad);
+            CKL();
+            ph_end(ctx);
+            cur ^= 1;
+        }
+    }
+    // ---- status ----------------------------------------------------------
+    int hs[4];
+    CK(cudaMemcpyAsync(hs, ctx->iscal, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
+    const int ev_t1 = ctx->nev;
+    if (ctx->timing) cudaEventRecord(ctx->ev[ctx->nev++], st);
+    CK(cudaStreamSynchronize(st));
+    // timings
+    rqrcp_timings t{};
+    if (ctx->timing) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ctx->ev[ev_t0], ctx->ev[ev_t1]);
+        t.total_ms = ms;
+        double acc[PH_N] = {0};
+        for (size_t q = 0; q < ctx->rec_phase.size(); ++q) {
+            float x = 0;
+            cudaEventElapsedTime(&x, ctx->ev[ctx->rec_s[q]], ctx->ev[ctx->rec_e[q]]);
+            acc[ctx->rec_phase[q]] += x;
+        }
+        t.omega_ms = acc[PH_OMEGA];
+        t.sketch_ms = acc[PH_SKETCH];
+        t.sample_qrcp_ms = acc[PH_SQRCP];
+        t.swap_ms = acc[PH_SWAP];
+        t.panel_ms = acc[PH_PANEL];
+        t.trailing_ms = acc[PH_TRAIL];
+        t.sample_update_ms = acc[PH_SUPD];
+        t.comm_ms = acc[PH_COMM];
+    }
+    t.panels = panels;
+    t.kernel_launches = ctx->launches;
+    ctx->last = t;
+    *rank_out = hs[3];
+    if (hs[0] == 4) {
+        ctx->err = "non-finite values in the sample (A contains NaN/Inf)";
+        return RQRCP_E_NONFINITE;
+    }
+    if (hs[3] < k) {
+        ctx->err = "rank-deficient: early stop";
+        return RQRCP_W_RANK_DEFICIENT;
+    }
+    return 0;
+}
+
+extern "C" int rqrcp_factor(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
+                            uint64_t seed, int64_t *jpvt, double *tau, int64_t *rank_out) {
+    return factor_impl(ctx, A, lda, m, n, k, b, p, seed, jpvt, tau, rank_out, nullptr, nullptr, nullptr);
+}
+
+extern "C" int rqrcp_factor_ex(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
+                               uint64_t seed, int64_t *jpvt, double *tau, int64_t *rank_out, const double *omega_in,
+                               double *omega_out, double *gaps_out) {
+    return factor_impl(ctx, A, lda, m, n, k, b, p, seed, jpvt, tau, rank_out, omega_in, omega_out, gaps_out);
+}
+
+extern "C" int rqrcp_factor_host(rqrcp_ctx *ctx, const double *A_host, int64_t lda, int64_t m, int64_t n, int64_t k,
+                                 int b, int p, uint64_t seed, double *A_out_host, int64_t *jpvt_host,
+                                 double *tau_host, int64_t *rank_out) {
+    if (!ctx) return -1;
+    if (!A_host) return -2;
+    if (lda < std::max<int64_t>(1, m)) return -3;
+    if (m < 1) return -4;
+    if (n < 1) return -5;
+    if (k < 1 || k > std::min(m, n)) return -6;
+    if (!A_out_host) return -10;
+    if (!jpvt_host) return -11;
+    if (!tau_host) return -12;
+    if (!rank_out) return -13;
+    if (m > ctx->max_m || n > ctx->max_n) {
+        ctx->err = "problem exceeds the create-time workspace maxima";
+        return RQRCP_E_WORKSPACE;
+    }
+    CK(cudaSetDevice(ctx->device));
+    const int64_t need = m * n;
+    if (ctx->a_dev_elems < need) {
+        if (ctx->a_dev) cudaFree(ctx->a_dev);
+        if (ctx->jpvt_dev) cudaFree(ctx->jpvt_dev);
+        if (ctx->tau_dev) cudaFree(ctx->tau_dev);
+        ctx->a_dev = nullptr;
+        ctx->a_dev_elems = 0;
+        CK(cudaMalloc((void **)&ctx->a_dev, sizeof(double) * need));
+        CK(cudaMalloc((void **)&ctx->jpvt_dev, sizeof(int64_t) * ctx->max_n));
+        CK(cudaMalloc((void **)&ctx->tau_dev, sizeof(double) * std::min(ctx->max_m, ctx->max_n)));
+        ctx->a_dev_elems = need;
+    }
+    CK(cudaMemcpy2DAsync(ctx->a_dev, sizeof(double) * m, A_host, sizeof(double) * lda, sizeof(double) * m, n,
+                         cudaMemcpyHostToDevice, ctx->stream));
+    int64_t rk = 0;
+    int rc = factor_impl(ctx, ctx->a_dev, m, m, n, k, b, p, seed, ctx->jpvt_dev, ctx->tau_dev, &rk, nullptr, nullptr,
+                         nullptr);
+    *rank_out = rk;
+    if (rc != 0 && rc != RQRCP_W_RANK_DEFICIENT) return rc;
+    CK(cudaMemcpy2DAsync(A_out_host, sizeof(double) * lda, ctx->a_dev, sizeof(double) * m, sizeof(double) * m, n,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(jpvt_host, ctx->jpvt_dev, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(tau_host, ctx->tau_dev, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return rc;
+}
+
+extern "C" int rqrcp_fill_gaussian(rqrcp_ctx *ctx, uint64_t seed, uint32_t stream, int64_t rows, int64_t cols,
+                                   int64_t row0, int64_t col0, double *out, int64_t ld) {
+    if (!ctx) return -1;
+    if (rows < 0) return -4;
+    if (cols < 0) return -5;
+    if (row0 < 0) return -6;
+    if (col0 < 0) return -7;
+    if (!out && rows * cols > 0) return -8;
+    if (ld < std::max<int64_t>(1, rows)) return -9;
+    if (rows * cols == 0) return 0;
+    CK(cudaSetDevice(ctx->device));
+    const int64_t npairs = ((row0 + rows - 1) >> 1) - (row0 >> 1) + 1;
+    gaussian_fill_kernel<<<grid_for(npairs * cols, 256, ctx->num_sms), 256, 0, ctx->stream>>>(seed, stream, rows, cols,
+                                                                                               row0, col0, out, ld);
+    CKL();
+    CK(cudaStreamSynchronize(ctx->stream));
+    return 0;
+}
+
+extern "C" int rqrcp_philox_words(rqrcp_ctx *ctx, const uint32_t *ctr, const uint32_t *key, uint32_t *out,
+                                  int64_t count) {
+    if (!ctx) return -1;
+    if (!ctr) return -2;
+    if (!key) return -3;
+    if (!out) return -4;
+    if (count < 0) return -5;
+    if (count == 0) return 0;
+    CK(cudaSetDevice(ctx->device));
+    philox_words_kernel<<<(unsigned)((count + 255) / 256), 256, 0, ctx->stream>>>(ctr, make_uint2(key[0], key[1]), out,
+                                                                                  count);
+    CKL();
+    CK(cudaStreamSynchronize(ctx->stream));
+    return 0;
+}

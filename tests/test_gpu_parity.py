@@ -1,0 +1,212 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Acceptance (BASELINE.json north_star): identical pivot sequences; |diag R|
+within 1e-10 relative; ||A Pi - Q1 [R11 R12]||_F/||A||_F (and ||R22||_F/||A||_F)
+within 1e-12 of the oracle's.  Inputs are seeded synthetic matrices from
+inputs/ with the recipes of BASELINE.json's configs, at sizes the oracle
+finishes in seconds (several GEMM / sample-QRCP / panel tiles and ragged tails).
+"""
+import numpy as np
+import pytest
+import torch
+
+import inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+DIAG_RTOL = 1e-10
+RES_ATOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_1804_05138_b200 as rq
+    c = rq.RQRCP(max_m=4200, max_n=4200, max_b=128, max_p=32)
+    yield c
+    c.close()
+
+
+def to_dev(A):
+    return inputs.fortran(torch.as_tensor(np.asarray(A))).cuda()
+
+
+def gpu_factor(ctx, A, k, b, p, seed, **kw):
+    Ad = to_dev(A)
+    jpvt, tau, rank = ctx.factor(Ad, k, b, p, seed=seed, **kw)
+    torch.cuda.synchronize()
+    return dict(A=Ad.cpu().numpy(), jpvt=jpvt.cpu().numpy(), tau=tau.cpu().numpy(), rank=rank)
+
+
+def full_R(F, k):
+    R = F.copy()
+    for j in range(k):
+        R[j + 1:, j] = 0.0
+    return R
+
+
+def trunc_residual(A, res, k, probes=None):
+    """||A Pi - Q1 [R11 R12]||_F / ||A||_F (exact when probes is None)."""
+    Api = A[:, res["jpvt"]]
+    Rt = np.triu(res["A"][:k, :])
+    Rfull = np.zeros_like(res["A"])
+    Rfull[:k] = Rt
+    if probes is None:
+        return np.linalg.norm(Api - oracle.apply_q(res["A"], res["tau"][:k], Rfull)) / np.linalg.norm(A)
+    X = probes
+    return (np.linalg.norm(Api @ X - oracle.apply_q(res["A"], res["tau"][:k], Rfull @ X))
+            / np.linalg.norm(A @ X))
+
+
+def compare(A, g, o, k, probes=None):
+    assert g["rank"] == o["rank"] == k
+    # identical pivot sequences (the whole permutation: same transpositions)
+    if not np.array_equal(g["jpvt"], o["jpvt"]):
+        bad = int(np.nonzero(g["jpvt"] != o["jpvt"])[0][0])
+        pytest.fail(f"pivots differ first at {bad}; oracle gap there {o['gaps'][min(bad, k - 1)]:.3e}")
+    dg = np.abs(np.diag(g["A"])[:k])
+    do = np.abs(np.diag(o["A"])[:k])
+    assert np.max(np.abs(dg - do) / do) <= DIAG_RTOL
+    nA = np.linalg.norm(A)
+    r22g = np.linalg.norm(full_R(g["A"], k)[k:, k:]) / nA
+    r22o = np.linalg.norm(full_R(o["A"], k)[k:, k:]) / nA
+    assert abs(r22g - r22o) <= RES_ATOL
+    rg = trunc_residual(A, g, k, probes)
+    ro = trunc_residual(A, o, k, probes)
+    assert abs(rg - ro) <= RES_ATOL
+    return rg
+
+
+CASES = [
+    # name, kind, m, n, k, b, p, seed
+    ("C1", "svd_exp", 512, 512, 64, 32, 8, 1001),
+    ("ragged", "iid", 700, 523, 100, 32, 8, 11),
+    ("tall", "svd_poly", 1500, 700, 200, 64, 10, 12),
+    ("wide", "graded", 600, 1900, 130, 32, 5, 13),
+    ("lowrank", "lowrank", 1024, 1024, 160, 64, 10, 14),
+    ("b1p0", "iid", 40, 30, 5, 1, 0, 15),
+    ("kfull", "iid", 256, 256, 256, 32, 8, 16),
+    ("b128", "graded", 900, 1100, 256, 128, 16, 17),
+    ("odd", "iid", 333, 301, 77, 13, 3, 18),
+]
+
+
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", CASES, ids=[c[0] for c in CASES])
+def test_factor_parity(ctx, name, kind, m, n, k, b, p, seed):
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    o = oracle.rqrcp(A, k, b, p, seed=seed)
+    g = gpu_factor(ctx, A, k, b, p, seed)
+    compare(A, g, o, k)
+
+
+def test_C2_full_size(ctx):
+    """configs[1] (the bench workload) at its full size: 4096^2, k=512, b=64, p=10."""
+    c = inputs.CONFIGS["C2"]
+    A = inputs.config_matrix("C2").numpy()
+    o = oracle.rqrcp(A, c["k"], c["b"], c["p"], seed=c["seed"])
+    g = gpu_factor(ctx, A, c["k"], c["b"], c["p"], c["seed"])
+    X = np.random.default_rng(0).standard_normal((c["n"], 8))
+    compare(A, g, o, c["k"], probes=X)
+
+
+def test_philox_words_bitwise(ctx):
+    rng = np.random.default_rng(1)
+    ctr = rng.integers(0, 2 ** 32, size=(257, 4), dtype=np.uint64)
+    key = (0x12345678, 0x9ABCDEF0)
+    got = ctx.philox_words(torch.tensor(ctr.astype(np.int64)).cuda(), key).cpu().numpy()
+    for i in range(ctr.shape[0]):
+        assert tuple(int(x) for x in got[i]) == oracle.philox4x32_10(ctr[i], key)
+
+
+def test_omega_normals(ctx):
+    """Device Philox + Box-Muller vs the oracle's: a few ulp (libm differences)."""
+    out = inputs.fortran(torch.empty(37, 61, dtype=torch.float64)).cuda()
+    ctx.fill_gaussian(out, 4242, 0, row0=3, col0=100)
+    ref = oracle.normal(4242, 0, 37, 61, row0=3, col0=100)
+    got = out.cpu().numpy()
+    assert np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-3)) < 16 * np.finfo(float).eps
+
+
+def test_omega_out_matches_oracle(ctx):
+    A = inputs.iid(5, 300, 200).numpy()
+    om = torch.empty(40 * 300, dtype=torch.float64, device="cuda")
+    gpu_factor(ctx, A, 40, 32, 8, 77, omega_out=om)
+    got = om.cpu().numpy().reshape(300, 40).T
+    ref = oracle.omega(77, 40, 300)
+    assert np.max(np.abs(got - ref)) < 1e-14
+
+
+def test_omega_in(ctx):
+    """Injected Omega (testing hook) = the oracle's explicit-Omega mode."""
+    A = inputs.iid(6, 400, 350).numpy()
+    om = np.random.default_rng(3).standard_normal((24, 400))
+    o = oracle.rqrcp(A, 60, 16, 8, omega=om)
+    g = gpu_factor(ctx, A, 60, 16, 8, 0, omega=torch.tensor(om.ravel(order="F")).cuda())
+    compare(A, g, o, 60)
+
+
+def test_deterministic(ctx):
+    A = inputs.iid(7, 800, 700).numpy()
+    g1 = gpu_factor(ctx, A, 128, 64, 10, 3)
+    g2 = gpu_factor(ctx, A, 128, 64, 10, 3)
+    assert np.array_equal(g1["A"], g2["A"]) and np.array_equal(g1["jpvt"], g2["jpvt"])
+
+
+def test_rank_deficient(ctx):
+    rng = np.random.default_rng(42)
+    A = rng.standard_normal((120, 25)) @ rng.standard_normal((25, 100))
+    o = oracle.rqrcp(A, 60, 16, 8, seed=1)
+    g = gpu_factor(ctx, A, 60, 16, 8, 1)
+    assert g["rank"] == o["rank"] == 25
+    assert np.array_equal(g["jpvt"], o["jpvt"])
+    assert np.all(g["tau"][25:] == 0.0)
+
+
+def test_zero_matrix(ctx):
+    g = gpu_factor(ctx, np.zeros((50, 40)), 10, 4, 2, 1)
+    assert g["rank"] == 0 and np.array_equal(g["jpvt"], np.arange(40))
+
+
+def test_nonfinite(ctx):
+    import paper_1804_05138_b200 as rq
+    A = np.ones((64, 48))
+    A[5, 7] = np.nan
+    with pytest.raises(rq.RqrcpError) as e:
+        gpu_factor(ctx, A, 8, 4, 2, 1)
+    assert e.value.code == rq.RQRCP_E_NONFINITE
+
+
+def test_argument_errors(ctx):
+    import ctypes
+
+    import paper_1804_05138_b200 as rq
+    L = rq.lib()
+    A = torch.zeros(10, 8, dtype=torch.float64, device="cuda").t().contiguous().t()
+    jp = torch.zeros(8, dtype=torch.int64, device="cuda")
+    ta = torch.zeros(8, dtype=torch.float64, device="cuda")
+    r = ctypes.c_int64()
+    h = ctx._h
+    call = lambda *a: L.rqrcp_factor(*a)
+    assert call(None, A.data_ptr(), 10, 10, 8, 4, 2, 2, 0, jp.data_ptr(), ta.data_ptr(), ctypes.byref(r)) == -1
+    assert call(h, None, 10, 10, 8, 4, 2, 2, 0, jp.data_ptr(), ta.data_ptr(), ctypes.byref(r)) == -2
+    assert call(h, A.data_ptr(), 9, 10, 8, 4, 2, 2, 0, jp.data_ptr(), ta.data_ptr(), ctypes.byref(r)) == -3
+    assert call(h, A.data_ptr(), 10, 0, 8, 4, 2, 2, 0, jp.data_ptr(), ta.data_ptr(), ctypes.byref(r)) == -4
+    assert call(h, A.data_ptr(), 10, 10, 0, 4, 2, 2, 0, jp.data_ptr(), ta.data_ptr(), ctypes.byref(r)) == -5
+    assert call(h, A.data_ptr(), 10, 10, 8, 9, 2, 2, 0, jp.data_ptr(), ta.data_ptr(), ctypes.byref(r)) == -6
+    assert call(h, A.data_ptr(), 10, 10, 8, 4, 0, 2, 0, jp.data_ptr(), ta.data_ptr(), ctypes.byref(r)) == -7
+    assert call(h, A.data_ptr(), 10, 10, 8, 4, 4, 7, 0, jp.data_ptr(), ta.data_ptr(), ctypes.byref(r)) == -8
+    assert call(h, A.data_ptr(), 10, 10, 8, 4, 2, 2, 0, None, ta.data_ptr(), ctypes.byref(r)) == -10
+    assert call(h, A.data_ptr(), 10, 10, 8, 4, 2, 2, 0, jp.data_ptr(), None, ctypes.byref(r)) == -11
+    assert call(h, A.data_ptr(), 10, 10, 8, 4, 2, 2, 0, jp.data_ptr(), ta.data_ptr(), None) == -12
+    big = L.rqrcp_factor(h, A.data_ptr(), 5000, 5000, 8, 4, 2, 2, 0, jp.data_ptr(), ta.data_ptr(), ctypes.byref(r))
+    assert big == rq.RQRCP_E_WORKSPACE
+
+
+def test_factor_host_equals_device(ctx):
+    A = inputs.iid(8, 640, 512).numpy()
+    g = gpu_factor(ctx, A, 96, 32, 8, 5)
+    Ah = inputs.fortran(torch.as_tensor(A)).pin_memory()
+    jp, ta, rank = ctx.factor_host(Ah, 96, 32, 8, seed=5)
+    assert rank == 96
+    assert np.array_equal(Ah.numpy(), g["A"])
+    assert np.array_equal(jp.numpy(), g["jpvt"])
