@@ -110,11 +110,12 @@ def haar(seed: int, stream: int, n: int, device="cpu") -> torch.Tensor:
 
 
 def svd_matrix(seed: int, m: int, n: int, sigma: torch.Tensor, device="cpu") -> torch.Tensor:
-    """A = U diag(sigma) V^T with U, V Haar (streams 1, 2); square only."""
-    assert m == n
-    u = haar(seed, STREAM_GU, m, device=device)
-    v = haar(seed, STREAM_GV, n, device=device)
-    return fortran((u * sigma.to(device).view(1, -1)) @ v.t())
+    """A = U diag(sigma) V^T with U, V the first min(m, n) columns of Haar
+    m x m / n x n orthogonal matrices (streams 1, 2)."""
+    r = min(m, n)
+    u = haar(seed, STREAM_GU, m, device=device)[:, :r]
+    v = haar(seed, STREAM_GV, n, device=device)[:, :r]
+    return fortran((u * sigma[:r].to(device).view(1, -1)) @ v.t())
 
 
 def iid(seed: int, m: int, n: int, device="cpu") -> torch.Tensor:

@@ -38,58 +38,33 @@ __global__ void sumsq_final_kernel(const double *part, int nparts, double *stop_
 }
 
 // ---------------------------------------------------------------------------
-// S3 swap ("Swap (j1..jb) and (i:i+b-1) columns in A, Pi"): the bb_eff
-// transpositions j <-> piv[j], applied in order (reading R-G5), restricted
-// to the <= 2 bb positions they touch, give a list of (dst, src) column moves
-// (one CTA, tiny); jpvt is permuted there too.  The A columns (full height
-// m, so earlier R12 rows move with them, LAPACK semantics) are then moved
-// through a staging buffer by two grid kernels.
+// S3 swap ("Swap (j1..jb) and (i:i+b-1) columns in A, Pi"): the
+// sample QRCP kernel turns its bb_eff transpositions (applied in order,
+// reading R-G5) into a list of (dst, src) column moves over the <= 2 bb
+// positions they touch.  Whole columns move (full height m, so earlier R12
+// rows move with them: LAPACK semantics), through a staging buffer, and
+// jpvt with them.
 // ---------------------------------------------------------------------------
-__global__ void swap_plan_kernel(const int64_t *piv, const int *bb_eff, int64_t *jpvt /* + i */, int64_t *dst,
-                                 int64_t *src, int *npairs) {
-    __shared__ int64_t pos[2 * 128 + 2], cur[2 * 128 + 2];
-    __shared__ int64_t jv[2 * 128 + 2];
-    if (threadIdx.x != 0) return;
-    const int nb = *bb_eff;
-    int nt = 0;
-    auto find = [&](int64_t p) {
-        for (int e = 0; e < nt; ++e)
-            if (pos[e] == p) return e;
-        pos[nt] = p; cur[nt] = p; jv[nt] = jpvt[p];
-        return nt++;
-    };
-    for (int j = 0; j < nb; ++j) {
-        const int64_t s = piv[j];
-        if (s == j) continue;
-        const int a = find(j), b = find(s);
-        int64_t t = cur[a]; cur[a] = cur[b]; cur[b] = t;
-        t = jv[a]; jv[a] = jv[b]; jv[b] = t;
-    }
-    int np = 0;
-    for (int e = 0; e < nt; ++e) {
-        jpvt[pos[e]] = jv[e];
-        if (cur[e] != pos[e]) { dst[np] = pos[e]; src[np] = cur[e]; ++np; }
-    }
-    *npairs = np;
-}
-
-__global__ void swap_gather_kernel(const double *A /* + i*lda */, int64_t lda, int64_t m, const int64_t *src,
-                                   const int *npairs, double *stage, int64_t lds) {
+__global__ void swap_gather_kernel(const double *A /* + i*lda */, int64_t lda, int64_t m, const int64_t *jpvt,
+                                   const int64_t *src, const int *npairs, double *stage, int64_t lds,
+                                   int64_t *jstage) {
     const int np = *npairs;
     const int64_t total = (int64_t)np * m;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = e % m, q = e / m;
         stage[r + q * lds] = A[r + src[q] * lda];
+        if (r == 0) jstage[q] = jpvt[src[q]];
     }
 }
 
-__global__ void swap_scatter_kernel(double *A, int64_t lda, int64_t m, const int64_t *dst, const int *npairs,
-                                    const double *stage, int64_t lds) {
+__global__ void swap_scatter_kernel(double *A, int64_t lda, int64_t m, int64_t *jpvt, const int64_t *dst,
+                                    const int *npairs, const double *stage, int64_t lds, const int64_t *jstage) {
     const int np = *npairs;
     const int64_t total = (int64_t)np * m;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = e % m, q = e / m;
         A[r + dst[q] * lda] = stage[r + q * lds];
+        if (r == 0) jpvt[dst[q]] = jstage[q];
     }
 }
 
@@ -101,20 +76,27 @@ __global__ void swap_scatter_kernel(double *A, int64_t lda, int64_t m, const int
 // R-hat12/22 are read from the physical sample columns perm[bb + c].
 // Skipped (no-op) when the panel ended early (bb_eff < bb).
 // ---------------------------------------------------------------------------
+// Omega-hat11 = R-hat11 R11^{-1}: x^T R11 = rhat11(r, :) for every row r, one
+// thread per row, the solution kept in shared memory (upper triangular).
 __global__ void omhat_kernel(const double *rhat11, const double *A /* &A[i + i lda] */, int64_t lda, int bb,
                              int bbpad, const int *bb_eff, double *omhat) {
-    // one thread per row r: row-vector triangular solve  x^T R11 = rhat11(r, :)
+    extern __shared__ double oh[];  // bbpad x bbpad, oh[r + c*bbpad]
     if (*bb_eff != bb) return;
-    for (int r = threadIdx.x; r < bbpad; r += blockDim.x) {
-        for (int c = 0; c < bbpad; ++c) {
-            double v = 0.0;
-            if (r < bb && c < bb && c >= r) {
-                double s = rhat11[r + (int64_t)c * bbpad];
-                for (int q = r; q < c; ++q) s -= omhat[r + (int64_t)q * bbpad] * A[q + (int64_t)c * lda];
-                v = s / A[c + (int64_t)c * lda];
-            }
-            omhat[r + (int64_t)c * bbpad] = v;
+    __shared__ double dinv[128];
+    for (int c = threadIdx.x; c < bb; c += blockDim.x) dinv[c] = 1.0 / A[c + (int64_t)c * lda];
+    __syncthreads();
+    for (int c = 0; c < bb; ++c) {
+        // column c of A's R11 is read by every thread: broadcast via L1
+        for (int r = threadIdx.x; r <= c; r += blockDim.x) {
+            double s = rhat11[r + (int64_t)c * bbpad];
+            for (int q = r; q < c; ++q) s -= oh[r + q * bbpad] * __ldg(A + q + (int64_t)c * lda);
+            oh[r + c * bbpad] = s * dinv[c];
         }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < bbpad * bbpad; e += blockDim.x) {
+        const int r = e % bbpad, c = e / bbpad;
+        omhat[e] = (r <= c && c < bb) ? oh[e] : 0.0;
     }
 }
 

@@ -4,16 +4,18 @@
 // I - V T V^T, T upper triangular, T(j,j) = tau_j,
 // T(0:j, j) = -tau_j T(0:j, 0:j) (V(:,0:j)^T v_j).
 //
-// One persistent cooperative kernel, CTA g owns a contiguous block of panel
-// rows; one grid barrier per column.  At step j each CTA writes the partial
-// Gram row  g_c = sum_{r > j, r owned} A(r, c) A(r, j)  for every panel
-// column c (c > j: the dot products v_j^T a_c up to scaling; c = j: ||x||^2
+// One persistent cooperative kernel; CTA g owns a contiguous block of panel
+// rows, cached in shared memory when it fits (the panel is then read from
+// and written to HBM exactly once); one grid barrier per column.  At step j
+// each CTA writes the partial Gram row  g_c = sum_{r > j, r owned} A(r,c) A(r,j)
+// for every panel column c (c > j: v_j^T a_c up to scaling; c = j: ||x||^2
 // below the diagonal; c < j: V(:,c)^T x, which gives T's column j), and the
-// owner of row j publishes that row.  After the barrier every CTA sums the G
-// partials in fixed order (identical bits everywhere), forms beta, tau,
-// v = x/(alpha - beta) (dlarfg, reading R-G7) and w_c = tau (a_jc + g_c/(alpha-beta)),
-// and updates its own rows: a_rc -= w_c v_r.  Columns bb_eff..bb-1 of the
-// panel (rank stop, R-G12) still receive the reflectors.
+// owner of row j publishes that row.  After the barrier every CTA reduces
+// the G partials (warp per column, fixed butterfly: identical bits in every
+// CTA), forms beta, tau, v = x/(alpha - beta) (dlarfg, reading R-G7) and
+// w_c = tau (a_jc + g_c/(alpha - beta)), and updates its own rows:
+// a_rc -= w_c v_r.  Columns bb_eff..bb-1 of the panel (rank stop, R-G12)
+// still receive the reflectors.
 // Outputs: V below the diagonal and R11 on/above it, in place; tau; the
 // explicit V (Vfull, m' x bbpad: unit diagonal, zeros above, K-contiguous for
 // W = V^T A22) and its transpose Vt (bbpad x m', for A22 += V W2); Tneg = -T.
@@ -25,7 +27,7 @@ namespace rq {
 constexpr int PN_THREADS = 256;
 constexpr int PN_WARPS = PN_THREADS / 32;
 constexpr int PN_MAXB = 128;
-constexpr int PN_MAXROWS = 512;  // rows per CTA held in shared memory as x
+constexpr int PN_MAXROWS = 1024;  // rows per CTA (x staging buffer)
 
 struct PanelArgs {
     double *A;          // &A[i + i*lda]
@@ -33,18 +35,20 @@ struct PanelArgs {
     int64_t mp;         // m' rows
     int bb;             // planned panel width (columns present)
     int bbpad;
+    int use_smem;       // cache own rows (rows x bb) in dynamic shared memory
     const int *bb_eff;
     double *tau;        // tau + i
     double *vfull;      // mp x bbpad, ld ldv
     int64_t ldv;
     double *vt;         // bbpad x mp, ld bbpad
     double *tneg;       // bbpad x bbpad
-    double *part;       // [2][G][bbpad] partial Gram rows
+    double *part;       // [2][bbpad][G] partial Gram rows (column-major over CTAs)
     double *rowj;       // [2][bbpad] published row j
     unsigned *bar;
 };
 
 __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
+    extern __shared__ __align__(16) double pn_dyn[];
     __shared__ double w[PN_MAXB];
     __shared__ double xs[PN_MAXROWS];
     __shared__ double s_scal, s_tau, s_beta;
@@ -56,27 +60,43 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
     const int64_t rpb = (mp + G - 1) / G;
     const int64_t r_lo = min(mp, (int64_t)g * rpb), r_hi = min(mp, r_lo + rpb);
     const int nrows = (int)(r_hi - r_lo);
-    double *A = a.A;
     const int64_t lda = a.lda;
+
+    // P(r, c) = A(r_lo + r, c): shared-memory copy or the panel itself
+    double *P;
+    int64_t ldp;
+    if (a.use_smem) {
+        P = pn_dyn;
+        ldp = nrows;
+        for (int c = warp; c < bb; c += PN_WARPS)
+            for (int r = lane; r < nrows; r += 32) P[r + (int64_t)c * ldp] = a.A[r_lo + r + c * lda];
+        __syncthreads();
+    } else {
+        P = a.A + r_lo;
+        ldp = lda;
+    }
 
     for (int j = 0; j < bbe; ++j) {
         const int par = j & 1;
+        const int rj = (int)(j - r_lo);  // local index of row j (may be out of range)
         // ---- partial Gram row over own rows r > j -----------------------
-        const int64_t rs = max(r_lo, (int64_t)j + 1);
+        const int rs = max(0, rj + 1);
         for (int c = warp; c < bb; c += PN_WARPS) {
             double s = 0.0;
-            for (int64_t r = rs + lane; r < r_hi; r += 32) s += A[r + c * lda] * A[r + (int64_t)j * lda];
+            for (int r = rs + lane; r < nrows; r += 32) s += P[r + (int64_t)c * ldp] * P[r + (int64_t)j * ldp];
             s = warp_sum(s);
-            if (lane == 0) a.part[((int64_t)par * G + g) * a.bbpad + c] = s;
+            if (lane == 0) a.part[((int64_t)par * a.bbpad + c) * G + g] = s;
         }
-        if (j >= r_lo && j < r_hi)
-            for (int c = tid; c < bb; c += PN_THREADS) a.rowj[par * a.bbpad + c] = A[j + c * lda];
+        if (rj >= 0 && rj < nrows)
+            for (int c = tid; c < bb; c += PN_THREADS) a.rowj[par * a.bbpad + c] = P[rj + (int64_t)c * ldp];
         grid_barrier(a.bar, G);
-        // ---- fixed-order sums -> reflector, w_c (every CTA) ---------------
-        for (int c = tid; c < bb; c += PN_THREADS) {
+        // ---- reduce the G partials (warp per column, fixed order) ----------
+        for (int c = warp; c < bb; c += PN_WARPS) {
+            const double *pc = a.part + ((int64_t)par * a.bbpad + c) * G;
             double s = 0.0;
-            for (int q = 0; q < G; ++q) s += ld_cg(a.part + ((int64_t)par * G + q) * a.bbpad + c);
-            w[c] = s;
+            for (int q = lane; q < G; q += 32) s += ld_cg(pc + q);
+            s = warp_sum(s);
+            if (lane == 0) w[c] = s;
         }
         __syncthreads();
         if (tid == 0) {
@@ -96,63 +116,68 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
         const double tau = s_tau, scal = s_scal;
         // T column j (CTA 0): y_c = v_c^T v_j = A(j,c) + scal * g_c  (c < j)
         if (g == 0) {
-            // y into w[0..j) is safe: w[c] for c < j is not used by the update
             for (int c = tid; c < j; c += PN_THREADS) w[c] = ld_cg(a.rowj + par * a.bbpad + c) + scal * w[c];
             __syncthreads();
-            for (int r = tid; r < a.bbpad; r += PN_THREADS) {
+            for (int rr = tid; rr < a.bbpad; rr += PN_THREADS) {
                 double t = 0.0;
-                if (r < j) {
-                    // T(0:j,j) = -tau T(0:j,0:j) y, tneg = -T:
-                    // tneg(r,j) = tau (T y)_r = -tau sum_c tneg(r,c) y_c
+                if (rr < j) {
+                    // T(0:j,j) = -tau T(0:j,0:j) y with tneg = -T:
+                    // tneg(r,j) = -tau sum_c tneg(r,c) y_c
                     double acc = 0.0;
-                    for (int c = r; c < j; ++c) acc += a.tneg[r + (int64_t)c * a.bbpad] * w[c];
+                    for (int c = rr; c < j; ++c) acc += a.tneg[rr + (int64_t)c * a.bbpad] * w[c];
                     t = -tau * acc;
-                } else if (r == j) {
+                } else if (rr == j) {
                     t = -tau;
                 }
-                a.tneg[r + (int64_t)j * a.bbpad] = t;
+                a.tneg[rr + (int64_t)j * a.bbpad] = t;
             }
             __syncthreads();
         }
         // w_c = tau * (a_jc + scal g_c) for c > j
         for (int c = j + 1 + tid; c < bb; c += PN_THREADS) w[c] = tau * (ld_cg(a.rowj + par * a.bbpad + c) + scal * w[c]);
-        // own rows: x_r (old column j) into shared memory
-        for (int r = tid; r < nrows; r += PN_THREADS) xs[r] = A[r_lo + r + (int64_t)j * lda];
+        for (int r = tid; r < nrows; r += PN_THREADS) xs[r] = P[r + (int64_t)j * ldp];
         __syncthreads();
         // ---- update own rows ---------------------------------------------
         if (tau != 0.0) {
             for (int c = j + 1 + warp; c < bb; c += PN_WARPS) {
                 const double wc = w[c];
-                for (int64_t r = r_lo + lane; r < r_hi; r += 32) {
-                    if (r > j) A[r + c * lda] -= wc * (scal * xs[r - r_lo]);
-                    else if (r == j) A[r + c * lda] -= wc;
+                for (int r = lane; r < nrows; r += 32) {
+                    if (r > rj) P[r + (int64_t)c * ldp] -= wc * (scal * xs[r]);
+                    else if (r == rj) P[r + (int64_t)c * ldp] -= wc;
                 }
             }
-            for (int64_t r = r_lo + tid; r < r_hi; r += PN_THREADS) {
-                if (r > j) A[r + (int64_t)j * lda] = scal * xs[r - r_lo];
-                else if (r == j) A[r + (int64_t)j * lda] = s_beta;
+            for (int r = tid; r < nrows; r += PN_THREADS) {
+                if (r > rj) P[r + (int64_t)j * ldp] = scal * xs[r];
+                else if (r == rj) P[r + (int64_t)j * ldp] = s_beta;
             }
         }
         __syncthreads();
     }
-    // ---- explicit V / V^T, zero tail of tau / T (rank stop) -------------
-    for (int64_t r = r_lo + warp; r < r_hi; r += PN_WARPS)
+    // ---- write back, explicit V / V^T, zero tails (rank stop) -----------
+    if (a.use_smem) {
+        for (int c = warp; c < bb; c += PN_WARPS)
+            for (int r = lane; r < nrows; r += 32) a.A[r_lo + r + c * lda] = P[r + (int64_t)c * ldp];
+    }
+    for (int r = warp; r < nrows; r += PN_WARPS) {
+        const int64_t gr = r_lo + r;
         for (int c = lane; c < a.bbpad; c += 32) {
             double v = 0.0;
-            if (c < bbe) v = (r > c) ? A[r + (int64_t)c * lda] : (r == c ? 1.0 : 0.0);
-            a.vt[c + r * a.bbpad] = v;
+            if (c < bbe) v = (gr > c) ? P[r + (int64_t)c * ldp] : (gr == c ? 1.0 : 0.0);
+            a.vt[c + gr * a.bbpad] = v;
         }
+    }
     for (int c = warp; c < a.bbpad; c += PN_WARPS)
-        for (int64_t r = r_lo + lane; r < r_hi; r += 32) {
+        for (int r = lane; r < nrows; r += 32) {
+            const int64_t gr = r_lo + r;
             double v = 0.0;
-            if (c < bbe) v = (r > c) ? A[r + (int64_t)c * lda] : (r == c ? 1.0 : 0.0);
-            a.vfull[r + c * a.ldv] = v;
+            if (c < bbe) v = (gr > c) ? P[r + (int64_t)c * ldp] : (gr == c ? 1.0 : 0.0);
+            a.vfull[gr + c * a.ldv] = v;
         }
     if (g == 0) {
         for (int c = bbe + tid; c < bb; c += PN_THREADS) a.tau[c] = 0.0;
         for (int e = tid; e < a.bbpad * a.bbpad; e += PN_THREADS) {
-            const int r = e % a.bbpad, c = e / a.bbpad;
-            if (c >= bbe || r > c) a.tneg[e] = 0.0;
+            const int rr = e % a.bbpad, c = e / a.bbpad;
+            if (c >= bbe || rr > c) a.tneg[e] = 0.0;
         }
     }
 }

@@ -49,12 +49,12 @@ struct rqrcp_ctx {
     int64_t splitk_elems = 0;
     double *sq_r = nullptr, *sq_r0 = nullptr;
     int *sq_lpos = nullptr;
-    unsigned char *sq_active = nullptr;
+    int *sq_active = nullptr;
     double *slot_val = nullptr, *slot_data = nullptr;
     int64_t *slot_pos = nullptr, *slot_col = nullptr;
     double *pn_part = nullptr, *pn_rowj = nullptr;
     double *swap_stage = nullptr;
-    int64_t *swap_dst = nullptr, *swap_src = nullptr;
+    int64_t *swap_dst = nullptr, *swap_src = nullptr, *swap_jstage = nullptr;
     int *swap_np = nullptr;
     int64_t *perm = nullptr, *piv = nullptr;
     double *sumsq_part = nullptr;
@@ -99,6 +99,8 @@ static const char *g_static_err = "no context";
         }                                                                             \
         ctx->launches++;                                                              \
     } while (0)
+
+static constexpr int kDynSmemMax = 200 * 1024;  // dynamic shared memory cap for cached kernels
 
 static int grid_for(int64_t total, int threads, int num_sms) {
     int64_t g = (total + threads - 1) / threads;
@@ -223,7 +225,7 @@ static int free_all(rqrcp_ctx *ctx) {
                     ctx->w2,      ctx->tneg,    ctx->rhat11,    ctx->omhat,     ctx->vhat,      ctx->tauhat,
                     ctx->splitk,  ctx->sq_r,    ctx->sq_r0,     ctx->sq_lpos,   ctx->sq_active, ctx->slot_val,
                     ctx->slot_data, ctx->slot_pos, ctx->slot_col, ctx->pn_part, ctx->pn_rowj,   ctx->swap_stage,
-                    ctx->swap_dst, ctx->swap_src, ctx->swap_np, ctx->perm,     ctx->piv,       ctx->sumsq_part,
+                    ctx->swap_dst, ctx->swap_src, ctx->swap_jstage, ctx->swap_np, ctx->perm,     ctx->piv,       ctx->sumsq_part,
                     ctx->iscal,   ctx->stop_tol2, ctx->bars,    ctx->a_dev,     ctx->jpvt_dev,  ctx->tau_dev};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -290,7 +292,7 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(dalloc(&ctx->sq_r, nn));
     CKC(dalloc(&ctx->sq_r0, nn));
     CKC(cudaMalloc((void **)&ctx->sq_lpos, sizeof(int) * nn));
-    CKC(cudaMalloc((void **)&ctx->sq_active, nn));
+    CKC(cudaMalloc((void **)&ctx->sq_active, sizeof(int) * nn));
     CKC(dalloc(&ctx->slot_val, 2 * 2 * G));
     CKC(dalloc(&ctx->slot_data, 2 * G * lp));
     CKC(cudaMalloc((void **)&ctx->slot_pos, sizeof(int64_t) * 2 * G));
@@ -300,6 +302,7 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(dalloc(&ctx->swap_stage, 2 * bp * mm));
     CKC(cudaMalloc((void **)&ctx->swap_dst, sizeof(int64_t) * 2 * bp));
     CKC(cudaMalloc((void **)&ctx->swap_src, sizeof(int64_t) * 2 * bp));
+    CKC(cudaMalloc((void **)&ctx->swap_jstage, sizeof(int64_t) * 2 * bp));
     CKC(cudaMalloc((void **)&ctx->swap_np, sizeof(int)));
     CKC(cudaMalloc((void **)&ctx->perm, sizeof(int64_t) * nn));
     CKC(cudaMalloc((void **)&ctx->piv, sizeof(int64_t) * bp));
@@ -309,11 +312,9 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(cudaMalloc((void **)&ctx->bars, sizeof(unsigned) * 8));
     CKC(cudaMemset(ctx->bars, 0, sizeof(unsigned) * 8));
     CKC(cudaMemset(ctx->tneg, 0, sizeof(double) * bp * bp));
-    int occ = 0;
-    CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sample_qrcp_kernel, SQ_THREADS, 0));
-    ctx->sq_max_grid = std::max(1, occ) * G;
-    CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, panel_qr_kernel, PN_THREADS, 0));
-    ctx->pn_max_grid = std::max(1, occ) * G;
+    CKC(cudaFuncSetAttribute(sample_qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
+    CKC(cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
+    CKC(cudaFuncSetAttribute(omhat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 128 * 8));
     for (auto &e : ctx->ev) CKC(cudaEventCreate(&e));
 #undef CKC
     *out = ctx;
@@ -344,8 +345,14 @@ extern "C" int rqrcp_get_timings(const rqrcp_ctx *ctx, rqrcp_timings *out) {
     return 0;
 }
 
-static int coop_launch(rqrcp_ctx *ctx, const void *func, int grid, int threads, void **args) {
-    cudaError_t e = cudaLaunchCooperativeKernel(func, dim3(grid), dim3(threads), args, 0, ctx->stream);
+static int coop_launch(rqrcp_ctx *ctx, const void *func, int grid, int threads, void **args, size_t smem) {
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, func, threads, smem);
+    if (e == cudaSuccess && grid > occ * ctx->num_sms) {
+        ctx->err = "cooperative grid exceeds co-residency";
+        return RQRCP_E_WORKSPACE;
+    }
+    e = cudaLaunchCooperativeKernel(func, dim3(grid), dim3(threads), args, smem, ctx->stream);
     if (e != cudaSuccess) {
         ctx->err = std::string("cooperative launch: ") + cudaGetErrorString(e);
         return RQRCP_E_CUDA;
@@ -459,25 +466,28 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.status = status;
             a.gaps = gaps_out ? gaps_out + i : nullptr;
             a.bar = ctx->bars;
-            int grid = (int)std::min<int64_t>((np + 31) / 32, std::min(ctx->sq_max_grid, G));
-            grid = std::max(grid, 1);
+            a.swap_dst = ctx->swap_dst;
+            a.swap_src = ctx->swap_src;
+            a.swap_np = ctx->swap_np;
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(G, (np + 7) / 8));
+            const int64_t cpb = (np + grid - 1) / grid;
+            const size_t smem = sq_smem_bytes(cpb, lpad);
+            a.use_smem = smem <= (size_t)kDynSmemMax;
             void *args[] = {&a};
-            rc = coop_launch(ctx, (const void *)sample_qrcp_kernel, grid, SQ_THREADS, args);
+            rc = coop_launch(ctx, (const void *)sample_qrcp_kernel, grid, SQ_THREADS, args, a.use_smem ? smem : 0);
             if (rc) return rc;
         }
         ph_end(ctx);
         // ---- S3: swaps on A and Pi -----------------------------------------
         ph_begin(ctx, PH_SWAP);
-        swap_plan_kernel<<<1, 32, 0, st>>>(ctx->piv, bb_eff, jpvt + i, ctx->swap_dst, ctx->swap_src, ctx->swap_np);
-        CKL();
         {
             const int64_t lds = ctx->max_m;
             const int gg = grid_for(2 * (int64_t)bb * m, 256, G);
-            swap_gather_kernel<<<gg, 256, 0, st>>>(A + i * lda, lda, m, ctx->swap_src, ctx->swap_np, ctx->swap_stage,
-                                                    lds);
+            swap_gather_kernel<<<gg, 256, 0, st>>>(A + i * lda, lda, m, jpvt + i, ctx->swap_src, ctx->swap_np,
+                                                    ctx->swap_stage, lds, ctx->swap_jstage);
             CKL();
-            swap_scatter_kernel<<<gg, 256, 0, st>>>(A + i * lda, lda, m, ctx->swap_dst, ctx->swap_np,
-                                                     ctx->swap_stage, lds);
+            swap_scatter_kernel<<<gg, 256, 0, st>>>(A + i * lda, lda, m, jpvt + i, ctx->swap_dst, ctx->swap_np,
+                                                     ctx->swap_stage, lds, ctx->swap_jstage);
             CKL();
         }
         ph_end(ctx);
@@ -499,14 +509,17 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.part = ctx->pn_part;
             a.rowj = ctx->pn_rowj;
             a.bar = ctx->bars + 2;
-            int64_t want = std::max<int64_t>((mp + PN_MAXROWS - 1) / PN_MAXROWS, std::min<int64_t>(G, (mp + 63) / 64));
-            int grid = (int)std::min<int64_t>(want, ctx->pn_max_grid);
-            if ((mp + grid - 1) / grid > PN_MAXROWS) {
+            const int grid = (int)std::max<int64_t>((mp + PN_MAXROWS - 1) / PN_MAXROWS,
+                                                    std::min<int64_t>(G, (mp + 31) / 32));
+            const int64_t rpb = (mp + grid - 1) / grid;
+            if (rpb > PN_MAXROWS) {
                 ctx->err = "panel too tall for the cooperative grid";
                 return RQRCP_E_WORKSPACE;
             }
+            const size_t smem = (size_t)rpb * bb * sizeof(double);
+            a.use_smem = smem <= (size_t)kDynSmemMax;
             void *args[] = {&a};
-            rc = coop_launch(ctx, (const void *)panel_qr_kernel, grid, PN_THREADS, args);
+            rc = coop_launch(ctx, (const void *)panel_qr_kernel, grid, PN_THREADS, args, a.use_smem ? smem : 0);
             if (rc) return rc;
         }
         ph_end(ctx);
@@ -525,7 +538,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         // ---- S6: sample update (Eq. (4)); skipped after the last panel (R-G9)
         if (i + bb < k && npp > 0) {
             ph_begin(ctx, PH_SUPD);
-            omhat_kernel<<<1, 128, 0, st>>>(ctx->rhat11, A + i + i * lda, lda, bb, bbpad, bb_eff, ctx->omhat);
+            omhat_kernel<<<1, 128, (size_t)bbpad * bbpad * sizeof(double), st>>>(ctx->rhat11, A + i + i * lda, lda, bb, bbpad, bb_eff, ctx->omhat);
             CKL();
             sample_update_kernel<<<(unsigned)((npp + SU_COLS - 1) / SU_COLS), 256, 0, st>>>(
                 ctx->bs[cur], lpad, ctx->perm, ctx->omhat, bbpad, A + i + (i + bb) * lda, lda, bb, l, lpad, npp,
