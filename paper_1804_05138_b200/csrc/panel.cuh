@@ -1,8 +1,9 @@
 // panel.cuh -- S4 (kernel K6): unpivoted Householder QR of the panel
 // A(i:m, i:i+bb) (Alg. 2 line P:149, PDGEQRF at P:760) with the compact-WY
-// factor T built in the same pass (PDLARFT): H_0 ... H_{bb-1} =
-// I - V T V^T, T upper triangular, T(j,j) = tau_j,
-// T(0:j, j) = -tau_j T(0:j, 0:j) (V(:,0:j)^T v_j).
+// inputs of the compact-WY factor T (PDLARFT) gathered in the same
+// pass: H_0 ... H_{bb-1} = I - V T V^T with T(j,j) = tau_j,
+// T(0:j, j) = -tau_j T(0:j, 0:j) (V(:,0:j)^T v_j); the V^T v_j columns are
+// recorded here and T itself is built by tri_kernel (tri.cuh).
 //
 // One persistent cooperative kernel; CTA g owns a contiguous block of panel
 // rows, cached in shared memory when it fits (the panel is then read from
@@ -18,7 +19,7 @@
 // still receive the reflectors.
 // Outputs: V below the diagonal and R11 on/above it, in place; tau; the
 // explicit V (Vfull, m' x bbpad: unit diagonal, zeros above, K-contiguous for
-// W = V^T A22) and its transpose Vt (bbpad x m', for A22 += V W2); Tneg = -T.
+// W = V^T A22) and its transpose Vt (bbpad x m', for A22 += V W2); ybuf.
 #pragma once
 #include "common.cuh"
 
@@ -41,10 +42,10 @@ struct PanelArgs {
     double *vfull;      // mp x bbpad, ld ldv
     int64_t ldv;
     double *vt;         // bbpad x mp, ld bbpad
-    double *tneg;       // bbpad x bbpad
+    double *ybuf;       // bbpad x bbpad: y(c, j) = v_c^T v_j for c < j (strict upper of V^T V)
     double *part;       // [2][bbpad][G] partial Gram rows (column-major over CTAs)
     double *rowj;       // [2][bbpad] published row j
-    unsigned *bar;
+    unsigned *bar;      // per-launch barrier counter (zeroed by the host)
 };
 
 __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
@@ -61,6 +62,7 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
     const int64_t r_lo = min(mp, (int64_t)g * rpb), r_hi = min(mp, r_lo + rpb);
     const int nrows = (int)(r_hi - r_lo);
     const int64_t lda = a.lda;
+    unsigned epoch = 0;
 
     // P(r, c) = A(r_lo + r, c): shared-memory copy or the panel itself
     double *P;
@@ -89,14 +91,28 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
         }
         if (rj >= 0 && rj < nrows)
             for (int c = tid; c < bb; c += PN_THREADS) a.rowj[par * a.bbpad + c] = P[rj + (int64_t)c * ldp];
-        grid_barrier(a.bar, G);
+        grid_barrier(a.bar, G, epoch);
         // ---- reduce the G partials (warp per column, fixed order) ----------
-        for (int c = warp; c < bb; c += PN_WARPS) {
-            const double *pc = a.part + ((int64_t)par * a.bbpad + c) * G;
-            double s = 0.0;
-            for (int q = lane; q < G; q += 32) s += ld_cg(pc + q);
-            s = warp_sum(s);
-            if (lane == 0) w[c] = s;
+        // (loads of up to 4 columns x 5 partials per lane issued before any add)
+        for (int c0 = warp; c0 < bb; c0 += 4 * PN_WARPS) {
+            double v[4][5];
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                const int c = c0 + cc * PN_WARPS;
+                const double *pc = a.part + ((int64_t)par * a.bbpad + c) * G;
+#pragma unroll
+                for (int u = 0; u < 5; ++u) {
+                    const int q = lane + 32 * u;
+                    v[cc][u] = (c < bb && q < G) ? ld_cg(pc + q) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                double s = v[cc][0] + v[cc][1] + v[cc][2] + v[cc][3] + v[cc][4];
+                s = warp_sum(s);
+                const int c = c0 + cc * PN_WARPS;
+                if (lane == 0 && c < bb) w[c] = s;
+            }
         }
         __syncthreads();
         if (tid == 0) {
@@ -114,25 +130,11 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
         }
         __syncthreads();
         const double tau = s_tau, scal = s_scal;
-        // T column j (CTA 0): y_c = v_c^T v_j = A(j,c) + scal * g_c  (c < j)
-        if (g == 0) {
-            for (int c = tid; c < j; c += PN_THREADS) w[c] = ld_cg(a.rowj + par * a.bbpad + c) + scal * w[c];
-            __syncthreads();
-            for (int rr = tid; rr < a.bbpad; rr += PN_THREADS) {
-                double t = 0.0;
-                if (rr < j) {
-                    // T(0:j,j) = -tau T(0:j,0:j) y with tneg = -T:
-                    // tneg(r,j) = -tau sum_c tneg(r,c) y_c
-                    double acc = 0.0;
-                    for (int c = rr; c < j; ++c) acc += a.tneg[rr + (int64_t)c * a.bbpad] * w[c];
-                    t = -tau * acc;
-                } else if (rr == j) {
-                    t = -tau;
-                }
-                a.tneg[rr + (int64_t)j * a.bbpad] = t;
-            }
-            __syncthreads();
-        }
+        // CTA 0 records y_c = v_c^T v_j = A(j,c) + scal g_c (c < j): column j of
+        // strict_upper(V^T V), from which tri_kernel builds T off the critical path
+        if (g == 0)
+            for (int c = tid; c < j; c += PN_THREADS)
+                a.ybuf[c + (int64_t)j * a.bbpad] = ld_cg(a.rowj + par * a.bbpad + c) + scal * w[c];
         // w_c = tau * (a_jc + scal g_c) for c > j
         for (int c = j + 1 + tid; c < bb; c += PN_THREADS) w[c] = tau * (ld_cg(a.rowj + par * a.bbpad + c) + scal * w[c]);
         for (int r = tid; r < nrows; r += PN_THREADS) xs[r] = P[r + (int64_t)j * ldp];
@@ -173,13 +175,8 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
             if (c < bbe) v = (gr > c) ? P[r + (int64_t)c * ldp] : (gr == c ? 1.0 : 0.0);
             a.vfull[gr + c * a.ldv] = v;
         }
-    if (g == 0) {
+    if (g == 0)
         for (int c = bbe + tid; c < bb; c += PN_THREADS) a.tau[c] = 0.0;
-        for (int e = tid; e < a.bbpad * a.bbpad; e += PN_THREADS) {
-            const int rr = e % a.bbpad, c = e / a.bbpad;
-            if (c >= bbe || rr > c) a.tneg[e] = 0.0;
-        }
-    }
 }
 
 }  // namespace rq

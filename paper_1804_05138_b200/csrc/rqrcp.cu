@@ -18,6 +18,7 @@
 #include "panel.cuh"
 #include "philox.cuh"
 #include "sample_qrcp.cuh"
+#include "tri.cuh"
 
 using namespace rq;
 
@@ -28,6 +29,8 @@ enum Phase { PH_OMEGA, PH_SKETCH, PH_SQRCP, PH_SWAP, PH_PANEL, PH_TRAIL, PH_SUPD
 struct rqrcp_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // concurrent small kernels (tri_kernel)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool own_stream = false;
     int nranks = 1, rank = 0;
     int64_t max_m = 0, max_n = 0;
@@ -42,7 +45,7 @@ struct rqrcp_ctx {
     double *vfull = nullptr;   // ldo x bpad_max
     double *vt = nullptr;      // bpad_max x max_m
     double *w = nullptr, *w2 = nullptr;  // bpad_max x max_n
-    double *tneg = nullptr, *rhat11 = nullptr, *omhat = nullptr;  // bpad_max^2
+    double *tneg = nullptr, *rhat11 = nullptr, *omhat = nullptr, *ybuf = nullptr;  // bpad_max^2
     double *vhat = nullptr;    // lpad_max x bpad_max
     double *tauhat = nullptr;
     double *splitk = nullptr;
@@ -61,7 +64,8 @@ struct rqrcp_ctx {
     // device scalars: [0] status [1] bb_eff [2] done [3] rank
     int *iscal = nullptr;
     double *stop_tol2 = nullptr;
-    unsigned *bars = nullptr;  // [0..1] sample qrcp, [2..3] panel
+    unsigned *bars = nullptr;  // one grid-barrier counter per cooperative launch
+    int64_t nbars = 0;
     // host-path buffer (lazily allocated)
     double *a_dev = nullptr;
     int64_t a_dev_elems = 0;
@@ -222,7 +226,7 @@ extern "C" int rqrcp_flops(int64_t m, int64_t n, int64_t k, int b, int p, double
 
 static int free_all(rqrcp_ctx *ctx) {
     void *ptrs[] = {ctx->omt,     ctx->bs[0],   ctx->bs[1],     ctx->vfull,     ctx->vt,        ctx->w,
-                    ctx->w2,      ctx->tneg,    ctx->rhat11,    ctx->omhat,     ctx->vhat,      ctx->tauhat,
+                    ctx->w2,      ctx->tneg, ctx->ybuf,   ctx->rhat11,    ctx->omhat,     ctx->vhat,      ctx->tauhat,
                     ctx->splitk,  ctx->sq_r,    ctx->sq_r0,     ctx->sq_lpos,   ctx->sq_active, ctx->slot_val,
                     ctx->slot_data, ctx->slot_pos, ctx->slot_col, ctx->pn_part, ctx->pn_rowj,   ctx->swap_stage,
                     ctx->swap_dst, ctx->swap_src, ctx->swap_jstage, ctx->swap_np, ctx->perm,     ctx->piv,       ctx->sumsq_part,
@@ -284,6 +288,7 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(dalloc(&ctx->w2, bp * nn));
     CKC(dalloc(&ctx->tneg, bp * bp));
     CKC(dalloc(&ctx->rhat11, bp * bp));
+    CKC(dalloc(&ctx->ybuf, bp * bp));
     CKC(dalloc(&ctx->omhat, bp * bp));
     CKC(dalloc(&ctx->vhat, lp * bp));
     CKC(dalloc(&ctx->tauhat, bp));
@@ -309,12 +314,16 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(dalloc(&ctx->sumsq_part, 4 * G));
     CKC(cudaMalloc((void **)&ctx->iscal, sizeof(int) * 8));
     CKC(dalloc(&ctx->stop_tol2, 1));
-    CKC(cudaMalloc((void **)&ctx->bars, sizeof(unsigned) * 8));
-    CKC(cudaMemset(ctx->bars, 0, sizeof(unsigned) * 8));
+    ctx->nbars = 2 * std::min(cfg->max_m, cfg->max_n) + 16;
+    CKC(cudaMalloc((void **)&ctx->bars, sizeof(unsigned) * ctx->nbars));
+    CKC(cudaMemset(ctx->bars, 0, sizeof(unsigned) * ctx->nbars));
     CKC(cudaMemset(ctx->tneg, 0, sizeof(double) * bp * bp));
     CKC(cudaFuncSetAttribute(sample_qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
     CKC(cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
-    CKC(cudaFuncSetAttribute(omhat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 128 * 8));
+    CKC(cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (128 * 128 + 64 * 64) * 8));
+    CKC(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
     for (auto &e : ctx->ev) CKC(cudaEventCreate(&e));
 #undef CKC
     *out = ctx;
@@ -327,6 +336,9 @@ extern "C" int rqrcp_destroy(rqrcp_ctx *ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     free_all(ctx);
     for (auto &e : ctx->ev) cudaEventDestroy(e);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return 0;
@@ -399,6 +411,8 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     if (ctx->timing) cudaEventRecord(ctx->ev[ctx->nev++], st);
     ph_begin(ctx, PH_OMEGA);
     CK(cudaMemsetAsync(ctx->iscal, 0, sizeof(int) * 8, st));
+    const int64_t npanels = (k + b - 1) / b;
+    CK(cudaMemsetAsync(ctx->bars, 0, sizeof(unsigned) * 2 * npanels, st));
     // ---- S0: Omega^T -----------------------------------------------------
     if (omega_in) {
         omega_t_from_kernel<<<grid_for((int64_t)lpad * m, 256, G), 256, 0, st>>>(omega_in, l, lpad, m, ctx->omt,
@@ -465,7 +479,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.rank = rankd;
             a.status = status;
             a.gaps = gaps_out ? gaps_out + i : nullptr;
-            a.bar = ctx->bars;
+            a.bar = ctx->bars + 2 * (panels - 1);
             a.swap_dst = ctx->swap_dst;
             a.swap_src = ctx->swap_src;
             a.swap_np = ctx->swap_np;
@@ -505,10 +519,10 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.vfull = ctx->vfull;
             a.ldv = ctx->ldo;
             a.vt = ctx->vt;
-            a.tneg = ctx->tneg;
+            a.ybuf = ctx->ybuf;
             a.part = ctx->pn_part;
             a.rowj = ctx->pn_rowj;
-            a.bar = ctx->bars + 2;
+            a.bar = ctx->bars + 2 * (panels - 1) + 1;
             const int grid = (int)std::max<int64_t>((mp + PN_MAXROWS - 1) / PN_MAXROWS,
                                                     std::min<int64_t>(G, (mp + 31) / 32));
             const int64_t rpb = (mp + grid - 1) / grid;
@@ -522,6 +536,19 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             rc = coop_launch(ctx, (const void *)panel_qr_kernel, grid, PN_THREADS, args, a.use_smem ? smem : 0);
             if (rc) return rc;
         }
+        // T and Omega-hat11 on the side stream, overlapping W = V^T A22
+        {
+            int nb = 8;
+            while (nb < bbpad) nb *= 2;
+            const size_t smem = ((size_t)nb * nb + (size_t)(nb / 2) * (nb / 2)) * sizeof(double);
+            CK(cudaEventRecord(ctx->ev_fork, st));
+            CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+            const int do_om = (i + bb < k && npp > 0) ? 1 : 0;
+            tri_kernel<<<2, TRI_THREADS, smem, ctx->side>>>(ctx->ybuf, tau + i, ctx->rhat11, A + i + i * lda, lda,
+                                                          bb, bbpad, nb, bb_eff, ctx->tneg, ctx->omhat, do_om);
+            CKL();
+            CK(cudaEventRecord(ctx->ev_join, ctx->side));
+        }
         ph_end(ctx);
         // ---- S5: trailing update A22 -= V T^T V^T A22 ------------------------
         ph_begin(ctx, PH_TRAIL);
@@ -529,17 +556,18 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             double *A22 = A + i + (i + bb) * lda;
             rc = gemm_skinny(ctx, bbpad, npp, mp, ctx->vfull, ctx->ldo, A22, lda, ctx->w, bbpad);
             if (rc) return rc;
+            CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
             rc = gemm_skinny(ctx, bbpad, npp, bbpad, ctx->tneg, bbpad, ctx->w, bbpad, ctx->w2, bbpad);
             if (rc) return rc;
             rc = gemm_update(ctx, mp, npp, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda);
             if (rc) return rc;
+        } else {
+            CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
         }
         ph_end(ctx);
         // ---- S6: sample update (Eq. (4)); skipped after the last panel (R-G9)
         if (i + bb < k && npp > 0) {
             ph_begin(ctx, PH_SUPD);
-            omhat_kernel<<<1, 128, (size_t)bbpad * bbpad * sizeof(double), st>>>(ctx->rhat11, A + i + i * lda, lda, bb, bbpad, bb_eff, ctx->omhat);
-            CKL();
             sample_update_kernel<<<(unsigned)((npp + SU_COLS - 1) / SU_COLS), 256, 0, st>>>(
                 ctx->bs[cur], lpad, ctx->perm, ctx->omhat, bbpad, A + i + (i + bb) * lda, lda, bb, l, lpad, npp,
                 bb_eff, ctx->bs[cur ^ 1], lpad);

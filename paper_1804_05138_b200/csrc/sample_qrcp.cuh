@@ -64,7 +64,7 @@ struct SqArgs {
     int *rank;            // in/out: accumulated rank
     const int *status;    // non-zero -> no-op
     double *gaps;         // [bb] or nullptr
-    unsigned *bar;
+    unsigned *bar;        // per-launch barrier counter (zeroed by the host)
 };
 
 RQ_DEV bool sq_better(double v, int64_t pos, double bv, int64_t bpos) {
@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
         return;
     }
     const double stop2 = *a.stop_tol2;
+    unsigned epoch = 0;
 
     // column storage (local index cl = c - c_lo) and per-column state
     double *cols;
@@ -199,22 +200,31 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
     };
 
     publish(0);
-    grid_barrier(a.bar, G);
+    grid_barrier(a.bar, G, epoch);
 
     int j = 0;
     for (; j < a.bb; ++j) {
         const int par = j & 1;
         // ---- 1. global winner (warp 0, parallel over slots) ---------------
         if (warp == 0) {
-            SqCand c{-1.0, -1.0, INT64_MAX, -1, -1};
-            for (int q = lane; q < G; q += 32) {
-                const int si = par * G + q;
-                const int64_t cq = *(volatile int64_t *)(a.slot_col + si);
-                if (cq < 0) continue;
-                SqCand d{*(volatile double *)(a.slot_val + 2 * si), *(volatile double *)(a.slot_val + 2 * si + 1),
-                         *(volatile int64_t *)(a.slot_pos + si), cq, q};
-                c = sq_combine(c, d);
+            // all slot loads first (G <= 160: at most 5 per lane), then combine
+            SqCand d[5];
+#pragma unroll
+            for (int u = 0; u < 5; ++u) {
+                const int q = lane + 32 * u;
+                d[u] = SqCand{-1.0, -1.0, INT64_MAX, -1, q};
+                if (q < G) {
+                    const int si = par * G + q;
+                    d[u].col = __ldcg(a.slot_col + si);
+                    d[u].v = __ldcg(a.slot_val + 2 * si);
+                    d[u].v2 = __ldcg(a.slot_val + 2 * si + 1);
+                    d[u].pos = __ldcg(a.slot_pos + si);
+                }
             }
+            SqCand c{-1.0, -1.0, INT64_MAX, -1, -1};
+#pragma unroll
+            for (int u = 0; u < 5; ++u)
+                if (d[u].col >= 0) c = sq_combine(c, d[u]);
             c = sq_warp_reduce(c);
             if (lane == 0) {
                 s_wpos = c.pos;
@@ -292,7 +302,7 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
         __syncthreads();
         // ---- 4. candidates for step j+1 -----------------------------------
         publish(par ^ 1);
-        grid_barrier(a.bar, G);
+        grid_barrier(a.bar, G, epoch);
     }
 
     // ---- results ------------------------------------------------------------

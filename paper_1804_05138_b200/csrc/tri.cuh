@@ -1,0 +1,160 @@
+// tri.cuh -- the two small b x b triangular computations of a panel, done
+// by block-recursive doubling so that no thread runs a b^2-long serial chain:
+//
+//  block 0: compact-WY T (PDLARFT) from Y = strict_upper(V^T V) and tau:
+//     base 8x8 blocks by the column recurrence T(0:j,j) = -tau_j T(0:j,0:j) y_j,
+//     then merges  T = [T1, -T1 Y12 T2; 0, T2]  for block sizes 8, 16, 32, 64.
+//     Written negated (Tneg = -T) for the W2 = -T^T W contraction.
+//  block 1: Omega-hat11 = R-hat11 R11^{-1} (Eq. (4), reading
+//     R-G20): R11^{-1} by the same doubling (inverse 8x8 blocks, then
+//     B <- -A^{-1} B D^{-1}), then the upper-triangular product.
+//
+// One CTA each, run on a side stream concurrently with W = V^T A22 (neither
+// result is needed before W2 = -T^T W / the sample update).  Entries beyond
+// the panel's effective width are zero (tau = 0, identity blocks).
+#pragma once
+#include "common.cuh"
+
+namespace rq {
+
+constexpr int TRI_THREADS = 256;
+
+// C(s x s) = A(s x s, upper) * B(s x s, upper)  (result upper); all in smem, ld given.
+RQ_DEV void tri_mul_uu(const double *A, int lda, const double *B, int ldb, double *C, int ldc, int s, double alpha) {
+    for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+        const int r = e % s, c = e / s;
+        double acc = 0.0;
+        if (r <= c)
+            for (int q = r; q <= c; ++q) acc += A[r + q * lda] * B[q + c * ldb];
+        C[r + c * ldc] = alpha * acc;
+    }
+}
+
+// C(s x s) = A(s x s, upper) * B(s x s, full); then D = C * E(upper) scaled.
+RQ_DEV void tri_mul_uf(const double *A, int lda, const double *B, int ldb, double *C, int ldc, int s) {
+    for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+        const int r = e % s, c = e / s;
+        double acc = 0.0;
+        for (int q = r; q < s; ++q) acc += A[r + q * lda] * B[q + c * ldb];
+        C[r + c * ldc] = acc;
+    }
+}
+RQ_DEV void tri_mul_fu(const double *A, int lda, const double *B, int ldb, double *C, int ldc, int s, double alpha) {
+    for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+        const int r = e % s, c = e / s;
+        double acc = 0.0;
+        for (int q = 0; q <= c; ++q) acc += A[r + q * lda] * B[q + c * ldb];
+        C[r + c * ldc] = alpha * acc;
+    }
+}
+
+// nb = power of two multiple of 8, >= bb
+__global__ void __launch_bounds__(TRI_THREADS) tri_kernel(const double *ybuf /* bbpad x bbpad */, const double *tau,
+                                                          const double *rhat11 /* bbpad x bbpad */,
+                                                          const double *R11 /* &A[i+i lda] */, int64_t lda, int bb,
+                                                          int bbpad, int nb, const int *bb_eff, double *tneg,
+                                                          double *omhat, int do_omhat) {
+    extern __shared__ __align__(16) double tsm[];
+    double *M = tsm;             // nb x nb
+    double *tmp = tsm + nb * nb; // (nb/2) x (nb/2)
+    const int ld = nb;
+    const int bbe = *bb_eff;
+    const int tid = threadIdx.x;
+    if (blockIdx.x == 0) {
+        // ---------------- T ----------------
+        for (int e = tid; e < nb * nb; e += blockDim.x) M[e] = 0.0;
+        __syncthreads();
+        // base: each thread owns one 8x8 diagonal block, column recurrence
+        if (tid < nb / 8) {
+            const int k0 = tid * 8;
+            for (int j = k0; j < k0 + 8; ++j) {
+                if (j >= bbe) continue;  // tau = 0 beyond the effective width: zero column
+                const double tj = tau[j];
+                for (int r = k0; r < j; ++r) {
+                    double acc = 0.0;
+                    for (int c = r; c < j; ++c) acc += M[r + c * ld] * ybuf[c + (int64_t)j * bbpad];
+                    M[r + j * ld] = -tj * acc;
+                }
+                M[j + j * ld] = tj;
+            }
+        }
+        __syncthreads();
+        for (int s = 8; s < nb; s *= 2) {
+            for (int k = 0; k < nb; k += 2 * s) {
+                // tmp = Y12 * T2 ; T12 = -T1 * tmp
+                for (int e = tid; e < s * s; e += blockDim.x) {
+                    const int r = e % s, c = e / s;
+                    double acc = 0.0;
+                    for (int q = 0; q <= c; ++q) {
+                        const int gr = k + r, gq = k + s + q;
+                        const double y = (gr < bbe && gq < bbe) ? ybuf[gr + (int64_t)gq * bbpad] : 0.0;
+                        acc += y * M[(k + s + q) + (k + s + c) * ld];
+                    }
+                    tmp[r + c * (nb / 2)] = acc;
+                }
+                __syncthreads();
+                tri_mul_uf(M + k + k * ld, ld, tmp, nb / 2, M + k + (k + s) * ld, ld, s);
+                __syncthreads();
+            }
+            // negate T12 blocks of this level
+            for (int k = 0; k < nb; k += 2 * s)
+                for (int e = tid; e < s * s; e += blockDim.x) {
+                    const int r = e % s, c = e / s;
+                    M[(k + r) + (k + s + c) * ld] = -M[(k + r) + (k + s + c) * ld];
+                }
+            __syncthreads();
+        }
+        for (int e = tid; e < bbpad * bbpad; e += blockDim.x) {
+            const int r = e % bbpad, c = e / bbpad;
+            tneg[e] = (r < nb && c < nb) ? -M[r + c * ld] : 0.0;
+        }
+    } else {
+        // ---------------- Omega-hat11 = R-hat11 R11^{-1} ----------------
+        if (!do_omhat || bbe != bb) return;
+        for (int e = tid; e < nb * nb; e += blockDim.x) {
+            const int r = e % nb, c = e / nb;
+            double v = 0.0;
+            if (r < bb && c < bb) v = (r <= c) ? R11[r + (int64_t)c * lda] : 0.0;
+            else if (r == c) v = 1.0;  // identity padding
+            M[e] = v;
+        }
+        __syncthreads();
+        // base: invert 8x8 diagonal blocks in place (thread per block column-by-column)
+        if (tid < nb / 8) {
+            const int k0 = tid * 8;
+            double inv[8][8];
+            for (int c = 0; c < 8; ++c)
+                for (int r = 0; r < 8; ++r) inv[r][c] = 0.0;
+            for (int c = 0; c < 8; ++c) {
+                // solve U x = e_c (back substitution), U = M[k0.., k0..]
+                for (int r = c; r >= 0; --r) {
+                    double s = (r == c) ? 1.0 : 0.0;
+                    for (int q = r + 1; q <= c; ++q) s -= M[(k0 + r) + (k0 + q) * ld] * inv[q][c];
+                    inv[r][c] = s / M[(k0 + r) + (k0 + r) * ld];
+                }
+            }
+            for (int c = 0; c < 8; ++c)
+                for (int r = 0; r < 8; ++r) M[(k0 + r) + (k0 + c) * ld] = (r <= c) ? inv[r][c] : 0.0;
+        }
+        __syncthreads();
+        for (int s = 8; s < nb; s *= 2) {
+            for (int k = 0; k < nb; k += 2 * s) {
+                // B <- -A^{-1} B D^{-1}:  tmp = A^{-1} B ; B = -tmp D^{-1}
+                tri_mul_uf(M + k + k * ld, ld, M + k + (k + s) * ld, ld, tmp, nb / 2, s);
+                __syncthreads();
+                tri_mul_fu(tmp, nb / 2, M + (k + s) + (k + s) * ld, ld, M + k + (k + s) * ld, ld, s, -1.0);
+                __syncthreads();
+            }
+        }
+        // Omega-hat = R-hat11 * R11^{-1} (upper x upper)
+        for (int e = tid; e < bbpad * bbpad; e += blockDim.x) {
+            const int r = e % bbpad, c = e / bbpad;
+            double acc = 0.0;
+            if (r <= c && c < bb)
+                for (int q = r; q <= c; ++q) acc += rhat11[r + (int64_t)q * bbpad] * M[q + c * ld];
+            omhat[e] = acc;
+        }
+    }
+}
+
+}  // namespace rq
