@@ -25,7 +25,7 @@
 
 namespace rq {
 
-enum GemmEpi { EPI_STORE = 0, EPI_PARTIAL = 1, EPI_ACCUM_T = 2 };
+enum GemmEpi { EPI_STORE = 0, EPI_PARTIAL = 1, EPI_ACCUM_T = 2, EPI_ACCUM_T_PRE = 3 };
 
 struct GemmArgs {
     int64_t M, N, K;
@@ -89,14 +89,31 @@ __global__ void __launch_bounds__(WM *WN * 32) gemm_tn_kernel(GemmArgs g) {
 #pragma unroll
         for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+    const int fr = lane >> 2;        // fragment row within an 8x8 tile
+    const int fk = (lane & 3) * 2;   // fragment k pair within a k8 block
+    // EPI_ACCUM_T_PRE: the C tile (A22^T) is loaded into registers before the
+    // K loop, so its HBM latency overlaps the DMMAs instead of the epilogue.
+    double cpre[EPI == EPI_ACCUM_T_PRE ? MT : 1][EPI == EPI_ACCUM_T_PRE ? NT : 1][2];
+    if (EPI == EPI_ACCUM_T_PRE) {
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+            const int64_t gm = m0 + wm * 8 * MT + i * 8 + fr;
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int64_t gn = n0 + wn * 8 * NT + j * 8 + fk + h;
+                    cpre[i][j][h] = (gm < g.M && gn < g.N) ? g.C[gn + gm * g.ldc] : 0.0;
+                }
+        }
+    }
+
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
         if (s < nk) load_stage(s, s);
         cp_async_commit();
     }
 
-    const int fr = lane >> 2;        // fragment row within an 8x8 tile
-    const int fk = (lane & 3) * 2;   // fragment k pair within a k8 block
     for (int64_t kt = 0; kt < nk; ++kt) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
@@ -118,13 +135,16 @@ __global__ void __launch_bounds__(WM *WN * 32) gemm_tn_kernel(GemmArgs g) {
 #pragma unroll
             for (int j = 0; j < NT; ++j)
                 b[j] = *reinterpret_cast<const double2 *>(yd + (kb * BN + wn * 8 * NT + j * 8 + fr) * 8 + fk);
+            // all even-k MMAs, then all odd-k ones: MT*NT independent
+            // accumulators between two dependent DMMAs (hides DMMA latency)
 #pragma unroll
             for (int i = 0; i < MT; ++i)
 #pragma unroll
-                for (int j = 0; j < NT; ++j) {
-                    dmma(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
-                    dmma(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
-                }
+                for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
         }
     }
     cp_async_wait<0>();
@@ -144,9 +164,11 @@ __global__ void __launch_bounds__(WM *WN * 32) gemm_tn_kernel(GemmArgs g) {
                     g.C[gm + gn * g.ldc] = acc[i][j][h];
                 } else if (EPI == EPI_PARTIAL) {
                     g.C[(int64_t)blockIdx.z * g.split_stride + gm + gn * g.M] = acc[i][j][h];
-                } else {  // EPI_ACCUM_T
+                } else if (EPI == EPI_ACCUM_T) {
                     double *c = g.C + gn + gm * g.ldc;
                     *c = *c + acc[i][j][h];
+                } else {  // EPI_ACCUM_T_PRE
+                    g.C[gn + gm * g.ldc] = cpre[i][j][h] + acc[i][j][h];
                 }
             }
         }

@@ -1,0 +1,222 @@
+// gemm_tma.cuh -- persistent FP64 DMMA contraction fed by TMA.
+//
+// Same product as gemm_dmma.cuh (C = X^T Y, both operands K-contiguous) but:
+//  * operands are staged by the Tensor Memory Accelerator: per k8 block one
+//    cp.async.bulk.tensor.2d of box {8 doubles, rows} lands a dense [rows][8]
+//    slab -- exactly the conflict-free fragment layout -- and signals an
+//    mbarrier with its byte count; out-of-range rows/columns are zero-filled
+//    by the TMA unit (ragged M, N, K tails need no predication);
+//  * the kernel is persistent (grid = #SMs): each CTA walks its tiles and
+//    their K chunks as ONE stage stream, so the loads of the next tile are in
+//    flight while the current tile finishes and stores its epilogue;
+//  * EPI_ACCUM_T_PRE issues the C-tile loads (A22) into registers when a tile
+//    starts, hiding HBM latency behind the tile's DMMAs.
+// One elected thread issues the TMA copies; a __syncthreads per stage guards
+// slot reuse (plus fence.proxy.async before the async-proxy overwrite).
+#pragma once
+#include <cuda.h>
+#include "common.cuh"
+#include "gemm_dmma.cuh"
+
+namespace rq {
+
+struct TmaGemmArgs {
+    int64_t M, N, K;       // product sizes
+    int64_t xk0, xm0;      // operand X element (k, m) -> tensor coords (xk0 + k, xm0 + m)
+    int64_t yk0, yn0;      // operand Y element (k, n) -> tensor coords (yk0 + k, yn0 + n)
+    double *C;
+    int64_t ldc;
+    int64_t k_per_split;   // multiple of BK
+    int splits;
+    int64_t split_stride;
+};
+
+RQ_DEV unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+RQ_DEV void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+RQ_DEV void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+RQ_DEV void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+RQ_DEV void tma_load_2d(void *dst, const CUtensorMap *tm, int c0, int c1, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int MT, int NT, int WM, int WN, int BK, int ST>
+constexpr size_t tma_gemm_smem() {
+    return 128 + (size_t)ST * BK * (8 * MT * WM + 8 * NT * WN) * sizeof(double) + ST * sizeof(uint64_t);
+}
+
+template <int MT, int NT, int WM, int WN, int BK, int ST, int EPI>
+__global__ void __launch_bounds__(WM *WN * 32, 1)
+    gemm_tma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY, TmaGemmArgs g) {
+    constexpr int BM = 8 * MT * WM;
+    constexpr int BN = 8 * NT * WN;
+    constexpr int KB = BK / 8;
+    constexpr int XS = KB * BM * 8;  // doubles per stage
+    constexpr int YS = KB * BN * 8;
+    constexpr unsigned STAGE_BYTES = (unsigned)((XS + YS) * sizeof(double));
+    // dynamic smem: [pad to 128 B][X stages][Y stages][ST mbarriers]
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    // align through the shared-window offset so the pointer stays a shared
+    // pointer (LDS, not generic LD) for the compiler
+    const unsigned pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
+    double *xs = reinterpret_cast<double *>(smem_raw + pad);
+    double *ys = xs + ST * XS;
+    uint64_t *full = reinterpret_cast<uint64_t *>(ys + ST * YS);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wm = warp / WN, wn = warp % WN;
+    const int fr = lane >> 2, fk = (lane & 3) * 2;
+    const int64_t tilesN = (g.N + BN - 1) / BN, tilesM = (g.M + BM - 1) / BM;
+    const int64_t ntiles = tilesN * tilesM * g.splits;
+
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    // tile t -> (split, m-tile, n-tile); n fastest so concurrent CTAs share X
+    struct It {
+        int64_t t;
+        int64_t kc, nk, m0, n0, kbeg;
+        int split;
+    };
+    auto set_tile = [&](It &it, int64_t t) {
+        it.t = t;
+        it.kc = 0;
+        if (t >= ntiles) return;
+        const int64_t per = tilesN * tilesM;
+        it.split = (int)(t / per);
+        const int64_t r = t % per;
+        it.m0 = (r / tilesN) * BM;
+        it.n0 = (r % tilesN) * BN;
+        it.kbeg = (int64_t)it.split * g.k_per_split;
+        const int64_t kend = min(g.K, it.kbeg + g.k_per_split);
+        it.nk = (kend > it.kbeg) ? (kend - it.kbeg + BK - 1) / BK : 0;
+    };
+    auto advance = [&](It &it) {
+        if (++it.kc >= it.nk) set_tile(it, it.t + gridDim.x);
+    };
+    auto issue = [&](const It &it, int slot) {
+        const int64_t k0 = it.kbeg + it.kc * BK;
+        mbar_expect_tx(&full[slot], STAGE_BYTES);
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) {
+            tma_load_2d(xs + slot * XS + kb * BM * 8, &tmX, (int)(g.xk0 + k0 + kb * 8), (int)(g.xm0 + it.m0), &full[slot]);
+            tma_load_2d(ys + slot * YS + kb * BN * 8, &tmY, (int)(g.yk0 + k0 + kb * 8), (int)(g.yn0 + it.n0), &full[slot]);
+        }
+    };
+
+    It P, Cn;
+    set_tile(P, blockIdx.x);
+    set_tile(Cn, blockIdx.x);
+    // skip tiles with no K work (cannot happen for K >= 1, kept for safety)
+    int64_t sp = 0, sc = 0;
+    if (tid == 0) {
+        for (int s = 0; s < ST - 1 && P.t < ntiles; ++s) {
+            issue(P, (int)(sp % ST));
+            ++sp;
+            advance(P);
+        }
+    }
+
+    double acc[MT][NT][2];
+    double cpre[EPI == EPI_ACCUM_T_PRE ? MT : 1][EPI == EPI_ACCUM_T_PRE ? NT : 1][2];
+    while (Cn.t < ntiles) {
+        const int slot = (int)(sc % ST);
+        mbar_wait(&full[slot], (unsigned)((sc / ST) & 1));
+        __syncthreads();  // everyone is past stage sc-1: its slot may be refilled
+        if (tid == 0 && P.t < ntiles) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            issue(P, (int)(sp % ST));
+            ++sp;
+            advance(P);
+        }
+        if (Cn.kc == 0) {
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+            if (EPI == EPI_ACCUM_T_PRE) {
+#pragma unroll
+                for (int i = 0; i < MT; ++i) {
+                    const int64_t gm = Cn.m0 + wm * 8 * MT + i * 8 + fr;
+#pragma unroll
+                    for (int j = 0; j < NT; ++j)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int64_t gn = Cn.n0 + wn * 8 * NT + j * 8 + fk + h;
+                            cpre[i][j][h] = (gm < g.M && gn < g.N) ? g.C[gn + gm * g.ldc] : 0.0;
+                        }
+                }
+            }
+        }
+        const double *xd = xs + slot * XS;
+        const double *yd = ys + slot * YS;
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) {
+            double2 a[MT], b[NT];
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+                a[i] = *reinterpret_cast<const double2 *>(xd + (kb * BM + wm * 8 * MT + i * 8 + fr) * 8 + fk);
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+                b[j] = *reinterpret_cast<const double2 *>(yd + (kb * BN + wn * 8 * NT + j * 8 + fr) * 8 + fk);
+            // all even-k MMAs, then all odd-k ones: MT*NT independent
+            // accumulators between two dependent DMMAs (hides DMMA latency)
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
+        }
+        if (Cn.kc == Cn.nk - 1) {
+            // epilogue of this tile (stores overlap the next tile's loads)
+#pragma unroll
+            for (int i = 0; i < MT; ++i) {
+                const int64_t gm = Cn.m0 + wm * 8 * MT + i * 8 + fr;
+                if (gm >= g.M) continue;
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int64_t gn = Cn.n0 + wn * 8 * NT + j * 8 + fk + h;
+                        if (gn >= g.N) continue;
+                        if (EPI == EPI_STORE) {
+                            g.C[gm + gn * g.ldc] = acc[i][j][h];
+                        } else if (EPI == EPI_PARTIAL) {
+                            g.C[(int64_t)Cn.split * g.split_stride + gm + gn * g.M] = acc[i][j][h];
+                        } else if (EPI == EPI_ACCUM_T_PRE) {
+                            g.C[gn + gm * g.ldc] = cpre[i][j][h] + acc[i][j][h];
+                        }
+                    }
+            }
+        }
+        ++sc;
+        advance(Cn);
+    }
+}
+
+}  // namespace rq

@@ -3,10 +3,12 @@
 // context's stream (no host synchronisation inside the panel loop; pivots
 // stay on the device) and synchronises once at the end for the status.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -14,6 +16,7 @@
 #include "rqrcp.h"
 #include "common.cuh"
 #include "gemm_dmma.cuh"
+#include "gemm_tma.cuh"
 #include "misc.cuh"
 #include "panel.cuh"
 #include "philox.cuh"
@@ -81,6 +84,7 @@ struct rqrcp_ctx {
     std::vector<int> rec_phase, rec_s, rec_e;
     rqrcp_timings last{};
     int64_t launches = 0;
+    bool debug_sync = false;  // RQRCP_DEBUG_SYNC=1: synchronise after every launch
 };
 
 static const char *g_static_err = "no context";
@@ -97,8 +101,10 @@ static const char *g_static_err = "no context";
 #define CKL()                                                                         \
     do {                                                                              \
         cudaError_t e_ = cudaGetLastError();                                          \
+        if (e_ == cudaSuccess && ctx->debug_sync) e_ = cudaStreamSynchronize(ctx->stream); \
         if (e_ != cudaSuccess) {                                                      \
-            ctx->err = std::string("kernel launch: ") + cudaGetErrorString(e_);       \
+            ctx->err = std::string("kernel launch #") + std::to_string(ctx->launches) + \
+                       " (line " + std::to_string(__LINE__) + "): " + cudaGetErrorString(e_); \
             return RQRCP_E_CUDA;                                                      \
         }                                                                             \
         ctx->launches++;                                                              \
@@ -173,6 +179,124 @@ static int gemm_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, co
     if (rows <= 0 || cols <= 0) return 0;
     GemmArgs g{cols, rows, K, w2, ldw, vt, ldvt, A22, lda, rup(K, 32), 0};
     return launch_tn_cfg<4, 4, 2, 4, 32, 2, EPI_ACCUM_T>(ctx, g, 1);
+}
+
+// ---------------------------------------------------------------------------
+// TMA-fed persistent DMMA kernels (gemm_tma.cuh).  Used when every operand's
+// row stride is a multiple of 16 bytes (TMA requirement); otherwise the
+// cp.async kernels above.
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+// 2-D map over a column-major matrix (dim0 = rows = K direction, contiguous),
+// box {8 doubles, box1 columns}; out-of-range elements read as zero.
+static bool make_tmap(CUtensorMap *m, const double *base, int64_t dim0, int64_t dim1, int64_t ld, int box1) {
+    auto enc = tma_encode_fn();
+    if (!enc || ((uintptr_t)base & 15) || ((ld * 8) & 15) || dim0 < 1 || dim1 < 1) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)dim0, (cuuint64_t)dim1};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+    cuuint32_t box[2] = {8, (cuuint32_t)box1};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// splits minimising ceil(T*S / grid) / S (persistent-grid wave quantisation)
+static int choose_splits(int64_t tiles, int64_t K, int grid, int64_t max_elems_per_split, int64_t partial_cap) {
+    int64_t smax = std::max<int64_t>(1, K / 512);
+    if (max_elems_per_split > 0) smax = std::min<int64_t>(smax, std::max<int64_t>(1, partial_cap / max_elems_per_split));
+    int best = 1;
+    double best_t = 1e30;
+    for (int64_t s = 1; s <= std::min<int64_t>(smax, 64); ++s) {
+        const double t = (double)((tiles * s + grid - 1) / grid) / (double)s + 0.002 * s;  // small per-split cost
+        if (t < best_t - 1e-12) { best_t = t; best = (int)s; }
+    }
+    return best;
+}
+
+template <int MT, int NT, int WM, int WN, int EPI>
+static int launch_tma_cfg(rqrcp_ctx *ctx, const double *X, int64_t xdim0, int64_t xdim1, int64_t ldx, const double *Y,
+                          int64_t ydim0, int64_t ydim1, int64_t ldy, TmaGemmArgs g, bool *done) {
+    constexpr int BK = 32;
+    constexpr int BM = 8 * MT * WM, BN = 8 * NT * WN;
+    constexpr int ST = (4 * BK * (BM + BN) * 8 <= 216 * 1024) ? 4 : 3;
+    *done = false;
+    // TMA needs the box's inner (K) start offset 16-byte aligned: even
+    // element coordinates for fp64 (an odd panel offset i falls back)
+    if ((g.xk0 | g.yk0) & 1) return 0;
+    CUtensorMap tx, ty;
+    if (!make_tmap(&tx, X, xdim0, xdim1, ldx, BM) || !make_tmap(&ty, Y, ydim0, ydim1, ldy, BN)) return 0;
+    const size_t smem = tma_gemm_smem<MT, NT, WM, WN, BK, ST>();
+    auto kern = gemm_tma_kernel<MT, NT, WM, WN, BK, ST, EPI>;
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const int64_t tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM) * g.splits;
+    const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);
+    kern<<<grid, WM * WN * 32, smem, ctx->stream>>>(tx, ty, g);
+    CKL();
+    *done = true;
+    return 0;
+}
+
+// C (M x N, ldc) = X^T Y, X = tensor (xdim0 x xdim1, ldx) from coords (xk0, xm0),
+// Y likewise; skinny M <= 144.  Returns 0 and sets *done when launched.
+template <int MT, int NT, int WM, int WN>
+static int tma_skinny_cfg(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const double *X, int64_t xdim0,
+                          int64_t xdim1, int64_t ldx, int64_t xk0, int64_t xm0, const double *Y, int64_t ydim0,
+                          int64_t ydim1, int64_t ldy, int64_t yk0, int64_t yn0, double *C, int64_t ldc, bool *done) {
+    constexpr int BM = 8 * MT * WM, BN = 8 * NT * WN;
+    const int64_t tiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM);
+    int splits = choose_splits(tiles, K, ctx->num_sms, M * N, ctx->splitk_elems);
+    int64_t kps = rup((K + splits - 1) / splits, 32);
+    splits = (int)((K + kps - 1) / kps);
+    TmaGemmArgs g{M, N, K, xk0, xm0, yk0, yn0, C, ldc, kps, splits, M * N};
+    if (splits <= 1) return launch_tma_cfg<MT, NT, WM, WN, EPI_STORE>(ctx, X, xdim0, xdim1, ldx, Y, ydim0, ydim1, ldy, g, done);
+    g.C = ctx->splitk;
+    int rc = launch_tma_cfg<MT, NT, WM, WN, EPI_PARTIAL>(ctx, X, xdim0, xdim1, ldx, Y, ydim0, ydim1, ldy, g, done);
+    if (rc || !*done) return rc;
+    splitk_reduce_kernel<<<grid_for(M * N, 256, ctx->num_sms), 256, 0, ctx->stream>>>(ctx->splitk, M, N, splits, M * N,
+                                                                                      C, ldc);
+    CKL();
+    return 0;
+}
+
+static int tma_skinny(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const double *X, int64_t xdim0, int64_t xdim1,
+                      int64_t ldx, int64_t xk0, int64_t xm0, const double *Y, int64_t ydim0, int64_t ydim1, int64_t ldy,
+                      int64_t yk0, int64_t yn0, double *C, int64_t ldc, bool *done) {
+    *done = false;
+    if (M <= 32) return tma_skinny_cfg<4, 4, 1, 8>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done);
+    if (M <= 40) return tma_skinny_cfg<5, 4, 1, 8>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done);
+    if (M <= 64) return tma_skinny_cfg<4, 4, 2, 4>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done);
+    if (M <= 80) return tma_skinny_cfg<5, 4, 2, 4>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done);
+    if (M <= 128) return tma_skinny_cfg<4, 4, 4, 2>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done);
+    if (M <= 144) return tma_skinny_cfg<6, 4, 3, 2>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done);
+    return 0;
+}
+
+// A22 (rows x cols, lda) += V W2  as  A22^T += W2^T Vt  (TMA operands W2, Vt).
+static int tma_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, const double *w2, int64_t ldw,
+                      const double *vt, int64_t ldvt, double *A22, int64_t lda, bool *done) {
+    *done = false;
+    if (rows <= 0 || cols <= 0) { *done = true; return 0; }
+    if ((lda & 1) || ((uintptr_t)A22 & 7)) return 0;
+    TmaGemmArgs g{cols, rows, K, 0, 0, 0, 0, A22, lda, rup(K, 32), 1, 0};
+    return launch_tma_cfg<4, 4, 2, 4, EPI_ACCUM_T_PRE>(ctx, w2, K, cols, ldw, vt, K, rows, ldvt, g, done);
 }
 
 // ---------------------------------------------------------------------------
@@ -251,6 +375,10 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     ctx->max_n = cfg->max_n;
     ctx->max_b = cfg->max_b;
     ctx->max_p = cfg->max_p;
+    {
+        const char *d = getenv("RQRCP_DEBUG_SYNC");
+        ctx->debug_sync = d && d[0] == '1';
+    }
     auto fail = [&](int code) {
         free_all(ctx);
         int rc = code;
@@ -429,7 +557,11 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     // ---- S1: sketch B = Omega A -------------------------------------------
     ph_begin(ctx, PH_SKETCH);
     int cur = 0;
-    int rc = gemm_skinny(ctx, lpad, n, m, ctx->omt, ctx->ldo, A, lda, ctx->bs[cur], lpad);
+    bool tdone = false;
+    int rc = tma_skinny(ctx, lpad, n, m, ctx->omt, m, lpad, ctx->ldo, 0, 0, A, m, n, lda, 0, 0, ctx->bs[cur], lpad,
+                        &tdone);
+    if (rc) return rc;
+    if (!tdone) rc = gemm_skinny(ctx, lpad, n, m, ctx->omt, ctx->ldo, A, lda, ctx->bs[cur], lpad);
     if (rc) return rc;
     sumsq_partial_kernel<<<4 * G, 256, 0, st>>>(ctx->bs[cur], lpad, n, lpad, ctx->sumsq_part);
     CKL();
@@ -554,12 +686,18 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         ph_begin(ctx, PH_TRAIL);
         if (npp > 0) {
             double *A22 = A + i + (i + bb) * lda;
-            rc = gemm_skinny(ctx, bbpad, npp, mp, ctx->vfull, ctx->ldo, A22, lda, ctx->w, bbpad);
+            // W = V^T A22: V = Vfull(0:m', 0:bbpad); A22 = A(i:m, i+bb:n) by TMA coordinates
+            rc = tma_skinny(ctx, bbpad, npp, mp, ctx->vfull, mp, bbpad, ctx->ldo, 0, 0, A, m, n, lda, i, i + bb,
+                            ctx->w, bbpad, &tdone);
+            if (rc) return rc;
+            if (!tdone) rc = gemm_skinny(ctx, bbpad, npp, mp, ctx->vfull, ctx->ldo, A22, lda, ctx->w, bbpad);
             if (rc) return rc;
             CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
             rc = gemm_skinny(ctx, bbpad, npp, bbpad, ctx->tneg, bbpad, ctx->w, bbpad, ctx->w2, bbpad);
             if (rc) return rc;
-            rc = gemm_update(ctx, mp, npp, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda);
+            rc = tma_update(ctx, mp, npp, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda, &tdone);
+            if (rc) return rc;
+            if (!tdone) rc = gemm_update(ctx, mp, npp, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda);
             if (rc) return rc;
         } else {
             CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));

@@ -1,0 +1,187 @@
+// tools/gemm_bench.cu -- timing harness for the DMMA contraction variants of
+// the trailing update (S5) at BASELINE shapes.  Not part of the library.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1804_05138_b200/csrc -o tools/gemm_bench tools/gemm_bench.cu
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cstdio>
+#include <cstdlib>
+#include <cmath>
+#include <vector>
+#include "gemm_dmma.cuh"
+#include "gemm_tma.cuh"
+using namespace rq;
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e)); exit(1); } } while (0)
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+static CUtensorMap make_map(const double *base, int64_t dim0, int64_t dim1, int64_t ld, int box1) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)dim0, (cuuint64_t)dim1};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+    cuuint32_t box[2] = {8, (cuuint32_t)box1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)base, dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { fprintf(stderr, "encode failed %d\n", (int)r); exit(1); }
+    return m;
+}
+
+__global__ void fill(double *p, int64_t n, uint64_t seed) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t x = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+        x ^= x >> 31; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 29;
+        p[i] = (double)(x >> 11) * 0x1p-53 - 0.5;
+    }
+}
+__global__ void maxdiff(const double *a, const double *b, int64_t n, double *out) {
+    double m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) m = fmax(m, fabs(a[i] - b[i]));
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(~0u, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long *)out, __double_as_longlong(m));
+}
+
+template <class F> float timeit(F f, int reps) {
+    f();
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) f();
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    return ms / reps;
+}
+
+template <int MT, int NT, int WM, int WN, int BK, int ST, int EPI>
+float run_cp(GemmArgs g, int splits, int reps) {
+    constexpr int BM = 8 * MT * WM, BN = 8 * NT * WN;
+    const size_t smem = (size_t)ST * BK * (BM + BN) * 8;
+    auto k = gemm_tn_kernel<MT, NT, WM, WN, BK, ST, EPI>;
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, splits);
+    return timeit([&] { k<<<grid, WM * WN * 32, smem>>>(g); }, reps);
+}
+template <int MT, int NT, int WM, int WN, int BK, int ST, int EPI>
+float run_tma(const CUtensorMap &tx, const CUtensorMap &ty, TmaGemmArgs g, int grid, int reps) {
+    const size_t smem = tma_gemm_smem<MT, NT, WM, WN, BK, ST>();
+    auto k = gemm_tma_kernel<MT, NT, WM, WN, BK, ST, EPI>;
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    return timeit([&] { k<<<grid, WM * WN * 32, smem>>>(tx, ty, g); }, reps);
+}
+
+int main(int argc, char **argv) {
+    const bool prof = argc > 1;
+    int sms;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    struct Shape { const char *name; int64_t rows, cols, K; };
+    const int64_t maxe = 32768LL * 32768;
+    double *A, *A2, *W2, *Vt, *V, *W, *Wb, *P, *dmax;
+    CK(cudaMalloc(&A, maxe * 8));
+    CK(cudaMalloc(&A2, 4096LL * 4096 * 8));
+    CK(cudaMalloc(&W2, 128LL * 65536 * 8));
+    CK(cudaMalloc(&Vt, 128LL * 65536 * 8));
+    CK(cudaMalloc(&V, 128LL * 65536 * 8));
+    CK(cudaMalloc(&W, 128LL * 65536 * 8));
+    CK(cudaMalloc(&Wb, 128LL * 65536 * 8));
+    CK(cudaMalloc(&P, 64LL << 20));
+    CK(cudaMalloc(&dmax, 8));
+    fill<<<1024, 256>>>(A, maxe, 1);
+    fill<<<1024, 256>>>(W2, 128LL * 65536, 2);
+    fill<<<1024, 256>>>(Vt, 128LL * 65536, 3);
+    fill<<<1024, 256>>>(V, 128LL * 65536, 4);
+    CK(cudaDeviceSynchronize());
+    if (argc > 2) {  // small-shape TMA probe: M=8, N=30, K=40 with box 32 x 256 (bigger than the tensor)
+        const int64_t M = 8, N = atoi(argv[2]), K = 40;
+        CUtensorMap tx = make_map(V, K, M, K, 32), ty = make_map(A, K, N, K, 256);
+        TmaGemmArgs t{M, N, K, 0, 0, 0, 0, W, M, 64, 1, 0};
+        run_tma<4, 4, 1, 8, 32, 3, EPI_STORE>(tx, ty, t, 1, 0);
+        cudaError_t e = cudaDeviceSynchronize();
+        printf("small N=%ld: %s\n", (long)N, cudaGetErrorString(e));
+        return 0;
+    }
+    if (prof) {  // one launch of each TMA kernel at C4 shape, for ncu
+        const int64_t rows = 32768, cols = 32640, K = 128;
+        CUtensorMap tx = make_map(W2, K, cols, K, 64), ty = make_map(Vt, K, rows, K, 128);
+        TmaGemmArgs t{cols, rows, K, 0, 0, 0, 0, A, rows, 128, 1, 0};
+        run_tma<4, 4, 2, 4, 32, 3, EPI_ACCUM_T_PRE>(tx, ty, t, sms, 0);
+        CUtensorMap vx = make_map(V, rows, K, rows, (int)K), ay = make_map(A, rows, cols, rows, 64);
+        TmaGemmArgs w{K, cols, rows, 0, 0, 0, 0, P, K, (rows / 2 + 31) / 32 * 32, 2, K * cols};
+        run_tma<4, 4, 4, 2, 32, 4, EPI_PARTIAL>(vx, ay, w, sms, 0);
+        CK(cudaDeviceSynchronize());
+        printf("prof done\n");
+        return 0;
+    }
+    // ---- correctness: update on a ragged 4000 x 3001, K = 72 (cp.async vs TMA) ----
+    {
+        const int64_t rows = 4000, cols = 3001, K = 72;
+        fill<<<1024, 256>>>(A2, rows * cols, 9);
+        CK(cudaMemcpy(A, A2, rows * cols * 8, cudaMemcpyDeviceToDevice));
+        GemmArgs g{cols, rows, K, W2, 80, Vt, 80, A, rows, 96, 0};
+        run_cp<4, 4, 2, 4, 32, 2, EPI_ACCUM_T>(g, 1, 0);  // one launch (timeit warmup) -> A += ...
+        CUtensorMap tx = make_map(W2, K, cols, 80, 64), ty = make_map(Vt, K, rows, 80, 128);
+        TmaGemmArgs t{cols, rows, K, 0, 0, 0, 0, A2, rows, 96, 1, 0};
+        run_tma<4, 4, 2, 4, 32, 4, EPI_ACCUM_T_PRE>(tx, ty, t, sms, 0);
+        CK(cudaMemset(dmax, 0, 8));
+        maxdiff<<<256, 256>>>(A, A2, rows * cols, dmax);
+        double h; CK(cudaMemcpy(&h, dmax, 8, cudaMemcpyDeviceToHost));
+        printf("{\"update_check_maxdiff\": %.3e, ", h);
+    }
+    std::vector<Shape> ups = {{"C2p0", 4096, 4032, 64}, {"C4p0", 32768, 32640, 128}, {"C5p0", 65536, 16384, 128}};
+    printf("\"update\": [");
+    for (size_t si = 0; si < ups.size(); ++si) {
+        auto s = ups[si];
+        int64_t rows = s.rows, cols = s.cols;
+        if (rows * cols > maxe) cols = maxe / rows;
+        const double fl = 2.0 * rows * cols * s.K;
+        GemmArgs g{cols, rows, s.K, W2, s.K, Vt, s.K, A, rows, (s.K + 31) / 32 * 32, 0};
+        float t0 = run_cp<4, 4, 2, 4, 32, 2, EPI_ACCUM_T>(g, 1, 5);
+        CUtensorMap tx = make_map(W2, s.K, cols, s.K, 64), ty = make_map(Vt, s.K, rows, s.K, 128);
+        TmaGemmArgs t{cols, rows, s.K, 0, 0, 0, 0, A, rows, (s.K + 31) / 32 * 32, 1, 0};
+        float t1 = run_tma<4, 4, 2, 4, 32, 4, EPI_ACCUM_T_PRE>(tx, ty, t, sms, 5);
+        float t2 = run_tma<4, 4, 2, 4, 32, 3, EPI_ACCUM_T_PRE>(tx, ty, t, sms, 5);
+        CUtensorMap ty2 = make_map(Vt, s.K, rows, s.K, 64);
+        float t3 = run_tma<4, 4, 2, 2, 32, 4, EPI_ACCUM_T_PRE>(tx, ty2, t, 2 * sms, 5);
+        printf("%s{\"shape\": \"%s\", \"tflops\": {\"cp_epi\": %.2f, \"tma_st4\": %.2f, \"tma_st3\": %.2f, \"tma_64x64_x2\": %.2f}}",
+               si ? ", " : "", s.name, fl / t0 / 1e9, fl / t1 / 1e9, fl / t2 / 1e9, fl / t3 / 1e9);
+    }
+    printf("], \"w\": [");
+    std::vector<Shape> ws = {{"C2p0", 4096, 4032, 64}, {"C4p0", 32768, 32640, 128}, {"C5p0", 65536, 16384, 128}};
+    for (size_t si = 0; si < ws.size(); ++si) {
+        auto s = ws[si];
+        int64_t rows = s.rows, cols = s.cols;
+        if (rows * cols > maxe) cols = maxe / rows;
+        const double fl = 2.0 * rows * cols * s.K;
+        // W = V^T A22: X = V (rows x K, ld rows), Y = A (rows x cols)
+        CUtensorMap tx = make_map(V, rows, s.K, rows, (int)s.K), ty = make_map(A, rows, cols, rows, s.K == 64 ? 128 : 64);
+        for (int splits : {1, 2, 4}) {
+            int64_t kps = ((rows + splits - 1) / splits + 31) / 32 * 32;
+            TmaGemmArgs t{s.K, cols, rows, 0, 0, 0, 0, splits > 1 ? P : W, s.K, kps, splits, s.K * cols};
+            float tt;
+            if (s.K == 64) tt = splits > 1 ? run_tma<4, 4, 2, 4, 32, 4, EPI_PARTIAL>(tx, ty, t, sms, 5) : run_tma<4, 4, 2, 4, 32, 4, EPI_STORE>(tx, ty, t, sms, 5);
+            else tt = splits > 1 ? run_tma<4, 4, 4, 2, 32, 4, EPI_PARTIAL>(tx, ty, t, sms, 5) : run_tma<4, 4, 4, 2, 32, 4, EPI_STORE>(tx, ty, t, sms, 5);
+            printf("%s{\"shape\": \"%s\", \"splits\": %d, \"tma_tflops\": %.2f}", (si || splits > 1) ? ", " : "", s.name, splits, fl / tt / 1e9);
+        }
+        // W correctness vs cp.async version (split 1)
+        GemmArgs g{s.K, cols, rows, V, rows, A, rows, Wb, s.K, (rows + 31) / 32 * 32, 0};
+        if (s.K == 64) run_cp<4, 4, 2, 2, 32, 3, EPI_STORE>(g, 1, 0); else run_cp<4, 4, 4, 2, 32, 3, EPI_STORE>(g, 1, 0);
+        TmaGemmArgs t{s.K, cols, rows, 0, 0, 0, 0, W, s.K, (rows + 31) / 32 * 32, 1, 0};
+        if (s.K == 64) run_tma<4, 4, 2, 4, 32, 4, EPI_STORE>(tx, ty, t, sms, 0); else run_tma<4, 4, 4, 2, 32, 4, EPI_STORE>(tx, ty, t, sms, 0);
+        CK(cudaMemset(dmax, 0, 8));
+        maxdiff<<<256, 256>>>(W, Wb, s.K * cols, dmax);
+        double h; CK(cudaMemcpy(&h, dmax, 8, cudaMemcpyDeviceToHost));
+        printf(", {\"shape\": \"%s\", \"w_check_maxdiff\": %.3e}", s.name, h);
+    }
+    printf("]}\n");
+    return 0;
+}
