@@ -60,6 +60,15 @@ RQ_DEV void grid_barrier(unsigned *count, unsigned nblocks, unsigned &epoch) {
     __syncthreads();
 }
 
+RQ_DEV double2 ld_volatile_v2(const double2 *p) {
+    double2 v;
+    asm volatile("ld.volatile.global.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    return v;
+}
+RQ_DEV void st_cg_v2(double2 *p, double2 v) {
+    asm volatile("st.global.cg.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
 // L2 load for data written by other CTAs (after a grid barrier); not
 // volatile, so the compiler may batch several in flight.
 RQ_DEV double ld_cg(const double *p) { return __ldcg(p); }

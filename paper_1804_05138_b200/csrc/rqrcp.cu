@@ -53,11 +53,10 @@ struct rqrcp_ctx {
     double *tauhat = nullptr;
     double *splitk = nullptr;
     int64_t splitk_elems = 0;
-    double *sq_r = nullptr, *sq_r0 = nullptr;
-    int *sq_lpos = nullptr;
-    int *sq_active = nullptr;
-    double *slot_val = nullptr, *slot_data = nullptr;
-    int64_t *slot_pos = nullptr, *slot_col = nullptr;
+    SqHdr *slot_hdr = nullptr;
+    int *slot_col = nullptr;
+    unsigned launch_seq = 0;  // tags of the sample-QRCP candidate headers
+    double *slot_v2 = nullptr, *slot_data = nullptr;
     double *pn_part = nullptr, *pn_rowj = nullptr;
     double *swap_stage = nullptr;
     int64_t *swap_dst = nullptr, *swap_src = nullptr, *swap_jstage = nullptr;
@@ -85,6 +84,7 @@ struct rqrcp_ctx {
     rqrcp_timings last{};
     int64_t launches = 0;
     bool debug_sync = false;  // RQRCP_DEBUG_SYNC=1: synchronise after every launch
+    unsigned long long *trace = nullptr;  // RQRCP_TRACE=1: per-step phase stamps of the sample QRCP
 };
 
 static const char *g_static_err = "no context";
@@ -351,10 +351,10 @@ extern "C" int rqrcp_flops(int64_t m, int64_t n, int64_t k, int b, int p, double
 static int free_all(rqrcp_ctx *ctx) {
     void *ptrs[] = {ctx->omt,     ctx->bs[0],   ctx->bs[1],     ctx->vfull,     ctx->vt,        ctx->w,
                     ctx->w2,      ctx->tneg, ctx->ybuf,   ctx->rhat11,    ctx->omhat,     ctx->vhat,      ctx->tauhat,
-                    ctx->splitk,  ctx->sq_r,    ctx->sq_r0,     ctx->sq_lpos,   ctx->sq_active, ctx->slot_val,
-                    ctx->slot_data, ctx->slot_pos, ctx->slot_col, ctx->pn_part, ctx->pn_rowj,   ctx->swap_stage,
+                    ctx->splitk,  ctx->slot_hdr, ctx->slot_col, ctx->slot_v2,
+                    ctx->slot_data, ctx->pn_part, ctx->pn_rowj,   ctx->swap_stage,
                     ctx->swap_dst, ctx->swap_src, ctx->swap_jstage, ctx->swap_np, ctx->perm,     ctx->piv,       ctx->sumsq_part,
-                    ctx->iscal,   ctx->stop_tol2, ctx->bars,    ctx->a_dev,     ctx->jpvt_dev,  ctx->tau_dev};
+                    ctx->iscal,   ctx->stop_tol2, ctx->bars,  ctx->trace,    ctx->a_dev,     ctx->jpvt_dev,  ctx->tau_dev};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     return 0;
@@ -379,6 +379,8 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
         const char *d = getenv("RQRCP_DEBUG_SYNC");
         ctx->debug_sync = d && d[0] == '1';
     }
+    const char *tr = getenv("RQRCP_TRACE");
+    const bool want_trace = tr && tr[0] == '1';
     auto fail = [&](int code) {
         free_all(ctx);
         int rc = code;
@@ -422,14 +424,11 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(dalloc(&ctx->tauhat, bp));
     ctx->splitk_elems = std::max<int64_t>(4 << 20, 0);
     CKC(dalloc(&ctx->splitk, ctx->splitk_elems));
-    CKC(dalloc(&ctx->sq_r, nn));
-    CKC(dalloc(&ctx->sq_r0, nn));
-    CKC(cudaMalloc((void **)&ctx->sq_lpos, sizeof(int) * nn));
-    CKC(cudaMalloc((void **)&ctx->sq_active, sizeof(int) * nn));
-    CKC(dalloc(&ctx->slot_val, 2 * 2 * G));
+    CKC(cudaMalloc((void **)&ctx->slot_hdr, sizeof(SqHdr) * 2 * G));
+    CKC(cudaMemset(ctx->slot_hdr, 0, sizeof(SqHdr) * 2 * G));
+    CKC(cudaMalloc((void **)&ctx->slot_col, sizeof(int) * 2 * G));
+    CKC(dalloc(&ctx->slot_v2, 2 * G));
     CKC(dalloc(&ctx->slot_data, 2 * G * lp));
-    CKC(cudaMalloc((void **)&ctx->slot_pos, sizeof(int64_t) * 2 * G));
-    CKC(cudaMalloc((void **)&ctx->slot_col, sizeof(int64_t) * 2 * G));
     CKC(dalloc(&ctx->pn_part, 2 * G * bp));
     CKC(dalloc(&ctx->pn_rowj, 2 * bp));
     CKC(dalloc(&ctx->swap_stage, 2 * bp * mm));
@@ -453,6 +452,10 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
     for (auto &e : ctx->ev) CKC(cudaEventCreate(&e));
+    if (want_trace) {
+        CKC(cudaMalloc((void **)&ctx->trace, sizeof(unsigned long long) * 2 * 64 * 8));
+        CKC(cudaMemset(ctx->trace, 0, sizeof(unsigned long long) * 2 * 64 * 8));
+    }
 #undef CKC
     *out = ctx;
     return 0;
@@ -592,13 +595,10 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.nn = np;
             a.bb = bb;
             a.stop_tol2 = ctx->stop_tol2;
-            a.r = ctx->sq_r;
-            a.r0 = ctx->sq_r0;
-            a.lpos = ctx->sq_lpos;
-            a.active = ctx->sq_active;
-            a.slot_val = ctx->slot_val;
-            a.slot_pos = ctx->slot_pos;
+            a.slot_hdr = ctx->slot_hdr;
             a.slot_col = ctx->slot_col;
+            a.tag0 = (++ctx->launch_seq) << 8;
+            a.slot_v2 = ctx->slot_v2;
             a.slot_data = ctx->slot_data;
             a.piv = ctx->piv;
             a.tauhat = ctx->tauhat;
@@ -615,12 +615,15 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.swap_dst = ctx->swap_dst;
             a.swap_src = ctx->swap_src;
             a.swap_np = ctx->swap_np;
+            a.trace = (panels == 1) ? ctx->trace : nullptr;
             const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(G, (np + 7) / 8));
             const int64_t cpb = (np + grid - 1) / grid;
-            const size_t smem = sq_smem_bytes(cpb, lpad);
-            a.use_smem = smem <= (size_t)kDynSmemMax;
+            // as many columns in shared memory as the budget allows, the rest in L2
+            const int64_t room = (int64_t)kDynSmemMax - cpb * (2 * (int64_t)sizeof(double) + 2 * (int64_t)sizeof(int));
+            a.nsm = (int)std::max<int64_t>(0, std::min<int64_t>(cpb, room / ((int64_t)lpad * 8)));
+            const size_t smem = sq_smem_bytes(a.nsm, cpb, lpad);
             void *args[] = {&a};
-            rc = coop_launch(ctx, (const void *)sample_qrcp_kernel, grid, SQ_THREADS, args, a.use_smem ? smem : 0);
+            rc = coop_launch(ctx, (const void *)sample_qrcp_kernel, grid, SQ_THREADS, args, smem);
             if (rc) return rc;
         }
         ph_end(ctx);
@@ -740,6 +743,26 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         t.trailing_ms = acc[PH_TRAIL];
         t.sample_update_ms = acc[PH_SUPD];
         t.comm_ms = acc[PH_COMM];
+    }
+    if (ctx->trace) {
+        unsigned long long h[2 * 64 * 8];
+        cudaMemcpy(h, ctx->trace, sizeof(h), cudaMemcpyDeviceToHost);
+        const char *names[6] = {"scan", "householder", "out+apply", "publish", "barrier", "->next"};
+        for (int c = 0; c < 2; ++c) {
+            double acc[6] = {0};
+            int cnt = 0;
+            for (int jj = 1; jj < 63; ++jj) {
+                const unsigned long long *r = h + ((size_t)c * 64 + jj) * 8;
+                const unsigned long long *nx = h + ((size_t)c * 64 + jj + 1) * 8;
+                if (!r[0] || !r[5] || !nx[0]) continue;
+                for (int q = 0; q < 5; ++q) acc[q] += (double)(r[q + 1] - r[q]);
+                acc[5] += (double)(nx[0] - r[5]);
+                ++cnt;
+            }
+            fprintf(stderr, "[rqrcp trace] sample QRCP CTA %s, %d steps, mean cycles:", c ? "last" : "0", cnt);
+            for (int q = 0; q < 6; ++q) fprintf(stderr, " %s=%.0f", names[q], cnt ? acc[q] / cnt : 0.0);
+            fprintf(stderr, "\n");
+        }
     }
     t.panels = panels;
     t.kernel_launches = ctx->launches;

@@ -2,39 +2,52 @@
 // (Alg. 1) on the l x n' sample B(:, i:n) (Alg. 2 line P:147).
 //
 // One persistent cooperative kernel; CTA g owns a contiguous range of the
-// sample's PHYSICAL columns, caches them (and their norms) in shared memory
-// when they fit, and keeps them in place for the whole panel: a
-// transposition j <-> s* only relabels logical positions.  Warp per column,
-// lanes over the l <= 160 rows, deterministic butterfly sums.  Per step j,
-// exactly one grid barrier:
-//   1. warp 0 of every CTA scans the G candidate slots in parallel and
-//      reduces (value, logical position) -> the global argmax of the squared
-//      norms, lowest logical position on exact ties (reading R-G5);
-//   2. every CTA loads the winner's column (published in its slot by the
-//      owner before the barrier) and computes the same dlarfg (R-G7)
+// sample's PHYSICAL columns and keeps them in place for the whole panel (a
+// transposition j <-> s* only relabels logical positions).  As many of its
+// columns as fit live in shared memory, the rest stay in global memory (L2);
+// per-column state (squared norm, its panel-start value, logical position,
+// active flag) always lives in shared memory.  Each warp processes SQ_CB
+// columns at a time with all their loads in flight, lanes over the l <= 160
+// rows, deterministic butterfly sums.  Per step j, exactly one grid barrier:
+//   1. warp 0 of every CTA loads the G candidate headers (one 16-byte load
+//      each; a step tag makes stale slots detectable) and reduces
+//      (value, logical position) -> the global argmax of
+//      the squared norms, lowest logical position on exact ties (R-G5);
+//   2. warp 0 of every CTA loads the winner's column (published in its slot
+//      by the owner before the barrier) and computes the same dlarfg (R-G7)
 //      redundantly -- identical bits everywhere (same code, same data);
 //   3. each CTA applies H_j to its active columns and downdates the squared
 //      norms, r_s -= B(j,s)^2, recomputing when r_s < 1e-6 r0_s (R-G6); the
-//      column that sat at logical position j takes position s*;
-//   4. each CTA publishes its best (and second best) candidate + column into
-//      the slot buffer of parity (j+1)&1, then the grid barrier.
+//      column that sat at logical position j takes position s*; each warp
+//      tracks its best remaining column on the fly;
+//   4. each CTA publishes its best candidate (header + column) into the slot
+//      buffer of parity (j+1)&1, then the grid barrier.
 // Stops early (bb_eff < bb) when the winning squared norm is <= stop_tol2
 // = (1e3 eps)^2 ||Omega A||_F^2 (reading R-G12).
-// CTA 0 alone maintains pos2phys (logical position -> physical column) in
-// global memory; at the end it emits the (dst, src) column moves that apply
-// the same transpositions, in order, to A and Pi (S3) and pos2phys becomes
-// `perm` for the sample update (S6).
+// CTA 0 tracks the logical -> physical map of the touched positions in
+// shared memory (positions < bb direct-mapped, others in a short list); at the
+// end it writes `perm` (consumed by S6) and the (dst, src) column moves that
+// apply the same transpositions, in order, to A and Pi (S3).
 // Other outputs: piv[j] (s* of step j, relative to column i), tauhat, Vhat
 // (l x bb reflectors), Rhat11 (bb x bb), bb_eff, rank, gaps (diagnostic).
 #pragma once
+#include <climits>
 #include "common.cuh"
 
 namespace rq {
 
 constexpr int SQ_THREADS = 256;
 constexpr int SQ_WARPS = SQ_THREADS / 32;
-constexpr int SQ_MAXL = 160;   // l = b + p <= 160 rows (5 per lane)
-constexpr int SQ_MAXB = 128;   // panel width
+constexpr int SQ_MAXL = 160;  // l = b + p <= 160 rows
+constexpr int SQ_RPL = 5;     // rows per lane
+constexpr int SQ_MAXB = 128;  // panel width
+constexpr int SQ_CB = 4;      // columns per warp iteration (memory-level parallelism)
+
+struct SqHdr {    // one candidate slot header (16 bytes, written as one vector store)
+    double v;       // squared norm of the best active column (-1: none)
+    unsigned tag;   // launch sequence * 256 + step: never repeats within a context
+    int pos;        // logical position (INT_MAX: none)
+};
 
 struct SqArgs {
     double *B;            // sample, physical columns, lpad x nn, ld ldb
@@ -42,21 +55,18 @@ struct SqArgs {
     int l, lpad;
     int64_t nn;           // n' = trailing columns of this panel
     int bb;               // planned panel width
-    int use_smem;         // cache own columns + state in dynamic shared memory
+    int nsm;              // columns per CTA cached in shared memory
     const double *stop_tol2;
-    double *r, *r0;       // per physical column (global mode)
-    int *lpos;            // logical position per physical column (global mode)
-    int *active;          // (global mode)
-    double *slot_val;     // [2][G][2] best, second best
-    int64_t *slot_pos;    // [2][G]
-    int64_t *slot_col;    // [2][G]
+    SqHdr *slot_hdr;      // [2][G]
+    int *slot_col;        // [2][G] physical column of the candidate (written before the header)
+    double *slot_v2;      // [2][G] second best (diagnostic, only with gaps)
     double *slot_data;    // [2][G][lpad]
     int64_t *piv;         // [bb]
     double *tauhat;       // [bb]
     double *vhat;         // lpad x bbpad (ld lpad)
     double *rhat11;       // bbpad x bbpad (ld bbpad)
     int bbpad;
-    int64_t *perm;        // [nn] pos2phys: logical -> physical
+    int64_t *perm;        // [nn] logical -> physical
     int64_t *swap_dst, *swap_src;  // [2 bb] column moves for S3
     int *swap_np;
     int *bb_eff;          // out
@@ -65,55 +75,28 @@ struct SqArgs {
     const int *status;    // non-zero -> no-op
     double *gaps;         // [bb] or nullptr
     unsigned *bar;        // per-launch barrier counter (zeroed by the host)
+    unsigned tag0;        // launch sequence * 256 (distinct per launch)
+    unsigned long long *trace;  // debug: [2 CTAs][64 steps][8 phases] clock64 stamps, or nullptr
 };
 
-RQ_DEV bool sq_better(double v, int64_t pos, double bv, int64_t bpos) {
-    return (v > bv) || (v == bv && pos < bpos);
-}
+RQ_DEV bool sq_better(double v, int pos, double bv, int bpos) { return (v > bv) || (v == bv && pos < bpos); }
 
-// (best value, position, column, slot) + second-best value, reduced over a warp.
-struct SqCand {
-    double v, v2;
-    int64_t pos, col;
-    int slot;
-};
-RQ_DEV SqCand sq_combine(SqCand a, SqCand b) {
-    SqCand r;
-    if (sq_better(b.v, b.pos, a.v, a.pos)) {
-        r = b;
-        r.v2 = fmax(fmax(a.v2, b.v2), a.v);
-    } else {
-        r = a;
-        r.v2 = fmax(fmax(a.v2, b.v2), b.v);
-    }
-    return r;
-}
-RQ_DEV SqCand sq_warp_reduce(SqCand c) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        SqCand d;
-        d.v = __shfl_xor_sync(0xffffffffu, c.v, o);
-        d.v2 = __shfl_xor_sync(0xffffffffu, c.v2, o);
-        d.pos = __shfl_xor_sync(0xffffffffu, c.pos, o);
-        d.col = __shfl_xor_sync(0xffffffffu, c.col, o);
-        d.slot = __shfl_xor_sync(0xffffffffu, c.slot, o);
-        c = sq_combine(c, d);
-    }
-    return c;
-}
-
-// dynamic shared memory bytes needed to cache cpb columns
-__host__ __device__ inline size_t sq_smem_bytes(int64_t cpb, int lpad) {
-    return (size_t)cpb * ((size_t)lpad * sizeof(double) + 2 * sizeof(double) + 2 * sizeof(int));
+// dynamic shared memory: nsm cached columns + state of cpb columns
+__host__ __device__ inline size_t sq_smem_bytes(int64_t nsm, int64_t cpb, int lpad) {
+    return (size_t)nsm * lpad * sizeof(double) + (size_t)cpb * (2 * sizeof(double) + 2 * sizeof(int));
 }
 
 __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
     extern __shared__ __align__(16) double sq_dyn[];
     __shared__ double xs[SQ_MAXL];
-    __shared__ SqCand wc[SQ_WARPS];
-    __shared__ double s_tau, s_beta;
-    __shared__ int64_t s_wpos, s_wcol;
-    __shared__ int s_wslot, s_stop, s_np;
+    __shared__ double wv[SQ_WARPS], wv2[SQ_WARPS];
+    __shared__ int wpos[SQ_WARPS], wcol[SQ_WARPS];
+    __shared__ double s_tau, s_beta, s_hv;
+    __shared__ int s_wpos, s_wcol, s_wslot, s_stop, s_np, s_hpos;
+    __shared__ int64_t low[SQ_MAXB];  // CTA 0: phys column at positions < bb
+    __shared__ int hi_pos[SQ_MAXB];   // CTA 0: touched positions >= bb ...
+    __shared__ int64_t hi_phys[SQ_MAXB];  // ... and their phys columns
+    __shared__ int hi_n;
 
     const int G = gridDim.x;
     const int g = blockIdx.x;
@@ -123,132 +106,197 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
     const int64_t cpb = (nn + G - 1) / G;
     const int64_t c_lo = min(nn, (int64_t)g * cpb), c_hi = min(nn, c_lo + cpb);
     const int ncol = (int)(c_hi - c_lo);
+    const int nsm = min(ncol, a.nsm);
+    const bool want_v2 = a.gaps != nullptr;
 
     if (*a.status != 0 || *a.done) {
         if (g == 0 && tid == 0) { *a.bb_eff = 0; *a.swap_np = 0; }
         return;
     }
     const double stop2 = *a.stop_tol2;
-    unsigned epoch = 0;
 
-    // column storage (local index cl = c - c_lo) and per-column state
-    double *cols;
-    int64_t ldc;
-    double *r, *r0;
-    int *lpos, *act;
-    if (a.use_smem) {
-        cols = sq_dyn;
-        ldc = lpad;
-        r = sq_dyn + (size_t)cpb * lpad;
-        r0 = r + cpb;
-        lpos = reinterpret_cast<int *>(r0 + cpb);
-        act = lpos + cpb;
-        for (int e = tid; e < ncol * l; e += SQ_THREADS) {
-            const int t = e % l, cl = e / l;
-            cols[t + (int64_t)cl * ldc] = a.B[t + (c_lo + cl) * a.ldb];
-        }
-        __syncthreads();
-    } else {
-        cols = a.B + c_lo * a.ldb;
-        ldc = a.ldb;
-        r = a.r + c_lo;
-        r0 = a.r0 + c_lo;
-        lpos = a.lpos + c_lo;
-        act = a.active + c_lo;
+    // shared layout: [nsm cached columns][r][r0][lpos][act]
+    double *cols_s = sq_dyn;
+    double *r = sq_dyn + (size_t)a.nsm * lpad;
+    double *r0 = r + cpb;
+    int *lpos = reinterpret_cast<int *>(r0 + cpb);
+    int *act = lpos + cpb;
+    auto colp = [&](int cl) -> const double * {
+        return (cl < nsm) ? cols_s + (size_t)cl * lpad : a.B + (c_lo + cl) * a.ldb;
+    };
+    for (int e = tid; e < nsm * l; e += SQ_THREADS) {
+        const int t = e % l, cl = e / l;
+        cols_s[t + (size_t)cl * lpad] = a.B[t + (c_lo + cl) * a.ldb];
     }
     for (int64_t x = c_lo + tid; x < c_hi; x += SQ_THREADS) a.perm[x] = x;
-
-    // ---- initial squared norms (K3) ---------------------------------------
-    for (int cl = warp; cl < ncol; cl += SQ_WARPS) {
-        const double *col = cols + (int64_t)cl * ldc;
-        double s = 0.0;
-        for (int t = lane; t < l; t += 32) s += col[t] * col[t];
-        s = warp_sum(s);
-        if (lane == 0) { r[cl] = s; r0[cl] = s; lpos[cl] = (int)(c_lo + cl); act[cl] = 1; }
+    if (g == 0) {
+        for (int x = tid; x < a.bb; x += SQ_THREADS) low[x] = x;
+        if (tid == 0) hi_n = 0;
     }
     __syncthreads();
 
-    // publish this CTA's best candidate into slot buffer `parity`
-    auto publish = [&](int parity) {
-        SqCand c{-1.0, -1.0, INT64_MAX, -1, g};
-        for (int cl = warp; cl < ncol; cl += SQ_WARPS) {
-            if (!act[cl]) continue;
-            SqCand d{r[cl], -1.0, (int64_t)lpos[cl], c_lo + cl, g};
-            c = sq_combine(c, d);
+    // this warp's best active column (and second-best value)
+    double bv = -1.0, bv2 = -1.0;
+    int bpos = INT_MAX, bcol = -1;
+    auto consider = [&](double v, int pos, int col) {
+        if (sq_better(v, pos, bv, bpos)) {
+            bv2 = fmax(bv2, bv);
+            bv = v; bpos = pos; bcol = col;
+        } else {
+            bv2 = fmax(bv2, v);
         }
-        if (lane == 0) wc[warp] = c;
+    };
+    // ---- initial squared norms (K3) ---------------------------------------
+    for (int cl0 = warp * SQ_CB; cl0 < ncol; cl0 += SQ_WARPS * SQ_CB) {
+        double x[SQ_CB][SQ_RPL];
+#pragma unroll
+        for (int u = 0; u < SQ_CB; ++u) {
+            const int cl = cl0 + u;
+            const double *col = (cl < ncol) ? colp(cl) : nullptr;
+#pragma unroll
+            for (int q = 0; q < SQ_RPL; ++q) {
+                const int t = lane + 32 * q;
+                x[u][q] = (col && t < l) ? col[t] : 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < SQ_CB; ++u) {
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < SQ_RPL; ++q) s += x[u][q] * x[u][q];
+            s = warp_sum(s);
+            const int cl = cl0 + u;
+            if (cl < ncol) {
+                if (lane == 0) { r[cl] = s; r0[cl] = s; lpos[cl] = (int)(c_lo + cl); act[cl] = 1; }
+                consider(s, (int)(c_lo + cl), (int)(c_lo + cl));
+            }
+        }
+    }
+
+    // publish this CTA's best candidate for step `step` (slot parity step & 1);
+    // the grid barrier that follows makes it visible.
+    auto publish = [&](int step) {
+        const int parity = step & 1;
+        if (lane == 0) { wv[warp] = bv; wv2[warp] = bv2; wpos[warp] = bpos; wcol[warp] = bcol; }
         __syncthreads();
         if (warp == 0) {
-            SqCand d = (lane < SQ_WARPS) ? wc[lane] : SqCand{-1.0, -1.0, INT64_MAX, -1, g};
-            d = sq_warp_reduce(d);
+            double v = -1.0, v2 = -1.0;
+            int p = INT_MAX, c = -1;
+            if (lane < SQ_WARPS) { v = wv[lane]; v2 = wv2[lane]; p = wpos[lane]; c = wcol[lane]; }
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) {  // 8 warps
+                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                const double ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
+                const int op = __shfl_xor_sync(0xffffffffu, p, o);
+                const int oc = __shfl_xor_sync(0xffffffffu, c, o);
+                if (sq_better(ov, op, v, p)) {
+                    v2 = fmax(fmax(v2, ov2), v);
+                    v = ov; p = op; c = oc;
+                } else {
+                    v2 = fmax(fmax(v2, ov2), ov);
+                }
+            }
             if (lane == 0) {
-                const int si = parity * G + g;
-                a.slot_val[2 * si] = d.v;
-                a.slot_val[2 * si + 1] = d.v2;
-                a.slot_pos[si] = d.pos;
-                a.slot_col[si] = d.col;
-                s_wcol = d.col;
+                s_hv = v; s_hpos = p; s_wcol = c;
+                if (want_v2) a.slot_v2[parity * G + g] = v2;
+                a.slot_col[parity * G + g] = c;
             }
         }
         __syncthreads();
-        const int64_t c0 = s_wcol;
+        const int c0 = s_wcol;
         if (c0 >= 0) {
             double *dst = a.slot_data + (int64_t)(parity * G + g) * lpad;
-            const double *src = cols + (c0 - c_lo) * ldc;
+            const int cl = c0 - (int)c_lo;
+            const double *src = (cl < nsm) ? cols_s + (size_t)cl * lpad : a.B + (int64_t)c0 * a.ldb;
             for (int t = tid; t < l; t += SQ_THREADS) dst[t] = src[t];
+        }
+        __syncthreads();
+        if (tid == 0) {
+            SqHdr h;
+            h.v = s_hv;
+            h.tag = a.tag0 + (unsigned)step;
+            h.pos = s_hpos;
+            st_cg_v2(reinterpret_cast<double2 *>(a.slot_hdr + parity * G + g), *reinterpret_cast<double2 *>(&h));
         }
     };
 
     publish(0);
+    unsigned epoch = 0;
     grid_barrier(a.bar, G, epoch);
 
     int j = 0;
+    const int tsel = (g == 0) ? 0 : (g == (int)gridDim.x - 1 ? 1 : -1);
+    auto stamp = [&](int ph) {
+        if (a.trace && tsel >= 0 && tid == 0 && j < 64) a.trace[((size_t)tsel * 64 + j) * 8 + ph] = clock64();
+    };
     for (; j < a.bb; ++j) {
         const int par = j & 1;
-        // ---- 1. global winner (warp 0, parallel over slots) ---------------
+        stamp(0);
+        // ---- 1. global winner: warp 0 polls the G tagged headers of step j ----
         if (warp == 0) {
-            // all slot loads first (G <= 160: at most 5 per lane), then combine
-            SqCand d[5];
+            double v = -1.0, v2 = -1.0;
+            int p = INT_MAX, c = -1, sl = -1;
 #pragma unroll
-            for (int u = 0; u < 5; ++u) {
+            for (int u = 0; u < 5; ++u) {  // G <= 160
                 const int q = lane + 32 * u;
-                d[u] = SqCand{-1.0, -1.0, INT64_MAX, -1, q};
                 if (q < G) {
-                    const int si = par * G + q;
-                    d[u].col = __ldcg(a.slot_col + si);
-                    d[u].v = __ldcg(a.slot_val + 2 * si);
-                    d[u].v2 = __ldcg(a.slot_val + 2 * si + 1);
-                    d[u].pos = __ldcg(a.slot_pos + si);
+                    const double2 raw = __ldcg(reinterpret_cast<const double2 *>(a.slot_hdr + par * G + q));
+                    const int qp = __double2hiint(raw.y);
+                    if (qp != INT_MAX) {
+                        const double vq2 = want_v2 ? __ldcg(a.slot_v2 + par * G + q) : -1.0;
+                        if (sq_better(raw.x, qp, v, p)) {
+                            v2 = fmax(fmax(v2, vq2), v);
+                            v = raw.x; p = qp; c = 0; sl = q;
+                        } else {
+                            v2 = fmax(fmax(v2, vq2), raw.x);
+                        }
+                    }
                 }
             }
-            SqCand c{-1.0, -1.0, INT64_MAX, -1, -1};
 #pragma unroll
-            for (int u = 0; u < 5; ++u)
-                if (d[u].col >= 0) c = sq_combine(c, d[u]);
-            c = sq_warp_reduce(c);
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                const int op = __shfl_xor_sync(0xffffffffu, p, o);
+                const int oc = __shfl_xor_sync(0xffffffffu, c, o);
+                const int osl = __shfl_xor_sync(0xffffffffu, sl, o);
+                const double ov2 = want_v2 ? __shfl_xor_sync(0xffffffffu, v2, o) : -1.0;
+                if (sq_better(ov, op, v, p)) {
+                    v2 = fmax(fmax(v2, ov2), v);
+                    v = ov; p = op; c = oc; sl = osl;
+                } else {
+                    v2 = fmax(fmax(v2, ov2), ov);
+                }
+            }
             if (lane == 0) {
-                s_wpos = c.pos;
-                s_wcol = c.col;
-                s_wslot = c.slot;
-                s_stop = (c.col < 0) || !(c.v > stop2);
-                if (g == 0 && a.gaps && !s_stop) a.gaps[j] = (c.v2 < 0.0 || c.v == 0.0) ? 1.0 : (c.v - c.v2) / c.v;
+                s_wpos = p;
+                s_wcol = (sl >= 0) ? __ldcg(a.slot_col + par * G + sl) : -1;
+                s_wslot = sl;
+                s_stop = (sl < 0) || !(v > stop2);
+                if (g == 0 && want_v2 && !s_stop) a.gaps[j] = (v2 < 0.0 || v == 0.0) ? 1.0 : (v - v2) / v;
             }
         }
         __syncthreads();
+        stamp(1);
         if (s_stop) break;
-        const int64_t wp = s_wpos, wcl = s_wcol;
-        // ---- 2. winner column -> Householder (identical in every CTA) -----
-        {
-            const double *src = a.slot_data + (int64_t)(par * G + s_wslot) * lpad;
-            for (int t = tid; t < l; t += SQ_THREADS) xs[t] = ld_cg(src + t);
-        }
-        if (wcl >= c_lo && wcl < c_hi && tid == 0) act[wcl - c_lo] = 0;  // retire the pivot
-        __syncthreads();
+        const int wp = s_wpos, wcl = s_wcol;
+        // ---- 2. winner column -> Householder (warp 0, identical everywhere) --
         if (warp == 0) {
-            double s = 0.0;
-            for (int t = j + 1 + lane; t < l; t += 32) s += xs[t] * xs[t];
+            const double *src = a.slot_data + (int64_t)(par * G + s_wslot) * lpad;
+            double xv[SQ_RPL];
+#pragma unroll
+            for (int q = 0; q < SQ_RPL; ++q) {
+                const int t = lane + 32 * q;
+                xv[q] = (t < l) ? __ldcg(src + t) : 0.0;
+            }
+            double s = 0.0, mine = 0.0;
+#pragma unroll
+            for (int q = 0; q < SQ_RPL; ++q) {
+                const int t = lane + 32 * q;
+                if (t > j) s += xv[q] * xv[q];
+                if (q == (j >> 5)) mine = xv[q];
+            }
             s = warp_sum(s);
-            const double alpha = xs[j];
+            const double alpha = __shfl_sync(0xffffffffu, mine, j & 31);
             double tau = 0.0, beta = alpha, scal = 0.0;
             if (s != 0.0) {
                 const double nrm = sqrt(alpha * alpha + s);
@@ -256,86 +304,141 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
                 tau = (beta - alpha) / beta;
                 scal = 1.0 / (alpha - beta);
             }
-            __syncwarp();
-            for (int t = j + 1 + lane; t < l; t += 32) xs[t] *= scal;
+#pragma unroll
+            for (int q = 0; q < SQ_RPL; ++q) {
+                const int t = lane + 32 * q;
+                if (t < l) xs[t] = (t > j) ? xv[q] * scal : (t == j ? 1.0 : xv[q]);
+            }
             if (lane == 0) { s_tau = tau; s_beta = beta; }
+        } else if (warp == 1 && lane == 0 && wcl >= c_lo && wcl < c_hi) {
+            act[wcl - c_lo] = 0;  // retire the pivot
         }
         __syncthreads();
+        stamp(2);
         const double tau = s_tau;
-        // ---- outputs (CTA 0) ------------------------------------------------
+        // ---- outputs + position map (CTA 0) ----------------------------------
         if (g == 0) {
             for (int t = tid; t < lpad; t += SQ_THREADS)
                 a.vhat[t + (int64_t)j * lpad] = (t < j) ? 0.0 : (t == j ? 1.0 : (t < l ? xs[t] : 0.0));
             for (int t = tid; t < a.bbpad; t += SQ_THREADS)
                 a.rhat11[t + (int64_t)j * a.bbpad] = (t < j) ? xs[t] : (t == j ? s_beta : 0.0);
-            if (tid == 0) {
-                a.piv[j] = wp;
-                a.tauhat[j] = tau;
-                // transposition j <-> wp on the logical -> physical map
-                const int64_t q = a.perm[j];
-                a.perm[j] = wcl;
-                if (wp != j) a.perm[wp] = q;
+            if (warp == SQ_WARPS - 1) {
+                // transposition j <-> wp; q = phys column at position j (< bb)
+                const int64_t q = low[j];
+                __syncwarp();
+                if (lane == 0) {
+                    a.piv[j] = wp;
+                    a.tauhat[j] = tau;
+                    low[j] = wcl;
+                }
+                if (wp != j) {
+                    if (wp < a.bb) {
+                        if (lane == 0) low[wp] = q;
+                    } else {
+                        // find wp in the short list (warp-parallel), else append
+                        int found = -1;
+                        for (int e0 = 0; e0 < hi_n; e0 += 32) {
+                            const int e = e0 + lane;
+                            const unsigned m = __ballot_sync(0xffffffffu, e < hi_n && hi_pos[e] == wp);
+                            if (m) { found = e0 + __ffs(m) - 1; break; }
+                        }
+                        if (lane == 0) {
+                            if (found >= 0) hi_phys[found] = q;
+                            else { hi_pos[hi_n] = wp; hi_phys[hi_n] = q; ++hi_n; }
+                        }
+                    }
+                }
+                __syncwarp();
             }
         }
         // ---- 3. apply H_j to own active columns, downdate norms -----------
-        for (int cl = warp; cl < ncol; cl += SQ_WARPS) {
-            if (!act[cl]) continue;
-            double *col = cols + (int64_t)cl * ldc;
-            double wsum = 0.0;
-            for (int t = j + lane; t < l; t += 32) wsum += ((t == j) ? 1.0 : xs[t]) * col[t];
-            wsum = warp_sum(wsum);
-            const double tw = tau * wsum;
-            for (int t = j + lane; t < l; t += 32) col[t] -= tw * ((t == j) ? 1.0 : xs[t]);
-            __syncwarp();
-            const double bj = col[j];
-            double rn = r[cl] - bj * bj;
-            if (rn < 1e-6 * r0[cl]) {
-                double s = 0.0;
-                for (int t = j + 1 + lane; t < l; t += 32) s += col[t] * col[t];
-                rn = warp_sum(s);
+        bv = -1.0; bv2 = -1.0; bpos = INT_MAX; bcol = -1;
+        auto apply_batch = [&](int cl0, int cend, auto colbase, int64_t ldcol) {
+            double x[SQ_CB][SQ_RPL];
+            bool live[SQ_CB];
+#pragma unroll
+            for (int u = 0; u < SQ_CB; ++u) {
+                const int cl = cl0 + u;
+                live[u] = (cl < cend) && act[cl];
+                const double *col = colbase + (int64_t)(live[u] ? cl : 0) * ldcol;
+#pragma unroll
+                for (int q = 0; q < SQ_RPL; ++q) {
+                    const int t = lane + 32 * q;
+                    x[u][q] = (live[u] && t < l) ? col[t] : 0.0;
+                }
             }
-            if (lane == 0) {
-                r[cl] = rn;
-                if (lpos[cl] == j) lpos[cl] = (int)wp;  // the column at position j moves to s*
+            double w[SQ_CB];
+#pragma unroll
+            for (int u = 0; u < SQ_CB; ++u) {
+                double sacc = 0.0;
+#pragma unroll
+                for (int q = 0; q < SQ_RPL; ++q) {
+                    const int t = lane + 32 * q;
+                    if (t >= j && t < l) sacc += xs[t] * x[u][q];
+                }
+                w[u] = sacc;
             }
-        }
-        __syncthreads();
-        // ---- 4. candidates for step j+1 -----------------------------------
-        publish(par ^ 1);
+#pragma unroll
+            for (int u = 0; u < SQ_CB; ++u) w[u] = warp_sum(w[u]);
+#pragma unroll
+            for (int u = 0; u < SQ_CB; ++u) {
+                if (!live[u]) continue;
+                const int cl = cl0 + u;
+                const double tw = tau * w[u];
+                double *col = colbase + (int64_t)cl * ldcol;
+                double bj = 0.0, tail = 0.0;
+#pragma unroll
+                for (int q = 0; q < SQ_RPL; ++q) {
+                    const int t = lane + 32 * q;
+                    if (t >= j && t < l) {
+                        x[u][q] -= tw * xs[t];
+                        col[t] = x[u][q];
+                    }
+                    if (t == j) bj = x[u][q];
+                    if (t > j && t < l) tail += x[u][q] * x[u][q];
+                }
+                bj = __shfl_sync(0xffffffffu, bj, j & 31);
+                double rn = r[cl] - bj * bj;
+                if (rn < 1e-6 * r0[cl]) rn = warp_sum(tail);  // uniform per column
+                int pos = lpos[cl];
+                if (pos == j) pos = wp;  // the column at position j moves to s*
+                __syncwarp();
+                if (lane == 0) { r[cl] = rn; lpos[cl] = pos; }
+                consider(rn, pos, (int)(c_lo + cl));
+            }
+        };
+        // shared-memory columns (LDS/STS), then the L2-resident rest
+        for (int cl0 = warp * SQ_CB; cl0 < nsm; cl0 += SQ_WARPS * SQ_CB) apply_batch(cl0, nsm, cols_s, (int64_t)lpad);
+        for (int cl0 = nsm + warp * SQ_CB; cl0 < ncol; cl0 += SQ_WARPS * SQ_CB)
+            apply_batch(cl0, ncol, a.B + c_lo * a.ldb, a.ldb);
+        stamp(3);
+        // ---- 4. candidates for step j+1, then the step barrier -------------
+        publish(j + 1);
+        stamp(4);
         grid_barrier(a.bar, G, epoch);
+        stamp(5);
     }
 
     // ---- results ------------------------------------------------------------
-    if (a.use_smem) {  // write the transformed columns back (S6 reads R-hat12/22)
-        for (int e = tid; e < ncol * l; e += SQ_THREADS) {
-            const int t = e % l, cl = e / l;
-            a.B[t + (c_lo + cl) * a.ldb] = cols[t + (int64_t)cl * ldc];
-        }
+    // transformed cached columns back to global (S6 reads R-hat12/22)
+    for (int e = tid; e < nsm * l; e += SQ_THREADS) {
+        const int t = e % l, cl = e / l;
+        a.B[t + (c_lo + cl) * a.ldb] = cols_s[t + (size_t)cl * lpad];
     }
     if (g == 0) {
         if (tid == 0) s_np = 0;
         __syncthreads();
-        // column moves (dst <- src) for every touched position whose content changed
-        for (int e = tid; e < 2 * j; e += SQ_THREADS) {
-            int64_t x;
-            bool take;
-            if (e < j) {
-                x = e;
-                take = true;
-            } else {
-                const int jj = e - j;
-                x = a.piv[jj];
-                take = x >= j;  // positions < j are covered above
-                for (int q = jj + 1; q < j && take; ++q)
-                    if (a.piv[q] == x) take = false;  // keep only the last occurrence
-            }
-            if (take) {
-                const int64_t src = a.perm[x];
-                if (src != x) {
-                    const int slot = atomicAdd(&s_np, 1);
-                    a.swap_dst[slot] = x;
-                    a.swap_src[slot] = src;
-                }
+        // perm + column moves for every touched position whose content changed
+        const int nlow = a.bb;
+        for (int e = tid; e < nlow + hi_n; e += SQ_THREADS) {
+            int64_t x, src;
+            if (e < nlow) { x = e; src = low[e]; }
+            else { x = hi_pos[e - nlow]; src = hi_phys[e - nlow]; }
+            a.perm[x] = src;
+            if (src != x) {
+                const int slot = atomicAdd(&s_np, 1);
+                a.swap_dst[slot] = x;
+                a.swap_src[slot] = src;
             }
         }
         __syncthreads();
