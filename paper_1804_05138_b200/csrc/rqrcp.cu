@@ -22,6 +22,7 @@
 #include "philox.cuh"
 #include "sample_qrcp.cuh"
 #include "tri.cuh"
+#include "cluster.cuh"
 
 using namespace rq;
 
@@ -75,6 +76,7 @@ struct rqrcp_ctx {
     double *tau_dev = nullptr;
     // cooperative limits
     int sq_max_grid = 0, pn_max_grid = 0;
+    int cluster_max = 0;  // largest usable cluster for the DSMEM kernels (0: none)
     // timing
     bool timing = true;
     cudaEvent_t ev[2 * 4096 + 8];
@@ -447,6 +449,34 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(cudaMemset(ctx->tneg, 0, sizeof(double) * bp * bp));
     CKC(cudaFuncSetAttribute(sample_qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
     CKC(cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
+    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
+    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
+    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    {
+        // largest cluster (<= 16) that can be resident with a full shared-memory budget
+        ctx->cluster_max = 0;
+        for (int cs = 16; cs >= 2 && !ctx->cluster_max; cs /= 2) {
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3(cs);
+            lc.blockDim = dim3(SQ_THREADS);
+            lc.dynamicSmemBytes = kDynSmemMax;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cs;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, (void *)sample_qrcp_cluster_kernel, &lc) == cudaSuccess &&
+                nclusters >= 1)
+                ctx->cluster_max = cs;
+        }
+        cudaGetLastError();
+        const char *nc = getenv("RQRCP_NO_CLUSTER");
+        if (nc && nc[0] == '1') ctx->cluster_max = 0;
+    }
     CKC(cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (128 * 128 + 64 * 64) * 8));
     CKC(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
@@ -507,6 +537,29 @@ static int coop_launch(rqrcp_ctx *ctx, const void *func, int grid, int threads, 
 __global__ void iota_kernel(int64_t *x, int64_t n) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
         x[e] = e;
+}
+
+static int cluster_launch(rqrcp_ctx *ctx, const void *func, int cs, int threads, void **args, size_t smem) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(cs);
+    lc.blockDim = dim3(threads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelExC(&lc, func, args);
+    if (e == cudaSuccess && ctx->debug_sync) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+        ctx->err = std::string("cluster launch: ") + cudaGetErrorString(e);
+        return RQRCP_E_CUDA;
+    }
+    ctx->launches++;
+    return 0;
 }
 
 static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
@@ -616,7 +669,22 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.swap_src = ctx->swap_src;
             a.swap_np = ctx->swap_np;
             a.trace = (panels == 1) ? ctx->trace : nullptr;
-            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(G, (np + 7) / 8));
+            bool launched = false;
+            if (ctx->cluster_max >= 2) {
+                const int cs = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->cluster_max, np));
+                const int64_t ccpb = (np + cs - 1) / cs;
+                const size_t csm = (size_t)ccpb * ((size_t)lpad * 8 + 24);
+                if (cs >= 2 && csm <= (size_t)kDynSmemMax) {
+                    void *args[] = {&a};
+                    rc = cluster_launch(ctx, (const void *)sample_qrcp_cluster_kernel, cs, SQ_THREADS, args, csm);
+                    if (rc) return rc;
+                    launched = true;
+                }
+            }
+            if (!launched) {
+            int gcap = G;
+            if (const char *e = getenv("RQRCP_SQ_GRID")) gcap = std::max(1, std::min(G, atoi(e)));
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(gcap, (np + 7) / 8));
             const int64_t cpb = (np + grid - 1) / grid;
             // as many columns in shared memory as the budget allows, the rest in L2
             const int64_t room = (int64_t)kDynSmemMax - cpb * (2 * (int64_t)sizeof(double) + 2 * (int64_t)sizeof(int));
@@ -625,6 +693,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             void *args[] = {&a};
             rc = coop_launch(ctx, (const void *)sample_qrcp_kernel, grid, SQ_THREADS, args, smem);
             if (rc) return rc;
+            }
         }
         ph_end(ctx);
         // ---- S3: swaps on A and Pi -----------------------------------------
@@ -658,8 +727,23 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.part = ctx->pn_part;
             a.rowj = ctx->pn_rowj;
             a.bar = ctx->bars + 2 * (panels - 1) + 1;
+            bool launched = false;
+            if (ctx->cluster_max >= 2) {
+                const int cs = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->cluster_max, (mp + 31) / 32));
+                const int64_t crpb = (mp + cs - 1) / cs;
+                const size_t csm = ((size_t)crpb * bb + 4 * (size_t)bbpad) * sizeof(double);
+                if (cs >= 2 && crpb <= PN_MAXROWS && csm <= (size_t)kDynSmemMax) {
+                    void *args[] = {&a};
+                    rc = cluster_launch(ctx, (const void *)panel_qr_cluster_kernel, cs, PN_THREADS, args, csm);
+                    if (rc) return rc;
+                    launched = true;
+                }
+            }
+            if (!launched) {
+            int pcap = G;
+            if (const char *e = getenv("RQRCP_PN_GRID")) pcap = std::max(1, std::min(G, atoi(e)));
             const int grid = (int)std::max<int64_t>((mp + PN_MAXROWS - 1) / PN_MAXROWS,
-                                                    std::min<int64_t>(G, (mp + 31) / 32));
+                                                    std::min<int64_t>(pcap, (mp + 31) / 32));
             const int64_t rpb = (mp + grid - 1) / grid;
             if (rpb > PN_MAXROWS) {
                 ctx->err = "panel too tall for the cooperative grid";
@@ -670,6 +754,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             void *args[] = {&a};
             rc = coop_launch(ctx, (const void *)panel_qr_kernel, grid, PN_THREADS, args, a.use_smem ? smem : 0);
             if (rc) return rc;
+            }
         }
         // T and Omega-hat11 on the side stream, overlapping W = V^T A22
         {

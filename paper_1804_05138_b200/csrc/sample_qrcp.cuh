@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
     __shared__ double wv[SQ_WARPS], wv2[SQ_WARPS];
     __shared__ int wpos[SQ_WARPS], wcol[SQ_WARPS];
     __shared__ double s_tau, s_beta, s_hv;
-    __shared__ int s_wpos, s_wcol, s_wslot, s_stop, s_np, s_hpos;
+    __shared__ int s_wpos, s_wcol, s_stop, s_np, s_hpos;
     __shared__ int64_t low[SQ_MAXB];  // CTA 0: phys column at positions < bb
     __shared__ int hi_pos[SQ_MAXB];   // CTA 0: touched positions >= bb ...
     __shared__ int64_t hi_phys[SQ_MAXB];  // ... and their phys columns
@@ -232,105 +232,115 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
     for (; j < a.bb; ++j) {
         const int par = j & 1;
         stamp(0);
-        // ---- 1. global winner: warp 0 polls the G tagged headers of step j ----
-        if (warp == 0) {
+        // ---- 1+2. global winner and its Householder reflector ----------------
+        // warps 0..ceil(G/32)-1 each reduce 32 headers (one 16-byte load per
+        // lane) and speculatively prefetch their local winner's column; the
+        // warp holding the global winner then forms dlarfg (R-G7) from its
+        // registers -- identical bits in every CTA (same data, same code).
+        const int nsw = (G + 31) >> 5;  // scanning warps (<= 5)
+        double xv[SQ_RPL];
+        if (warp < nsw) {
             double v = -1.0, v2 = -1.0;
-            int p = INT_MAX, c = -1, sl = -1;
-#pragma unroll
-            for (int u = 0; u < 5; ++u) {  // G <= 160
-                const int q = lane + 32 * u;
-                if (q < G) {
-                    const double2 raw = __ldcg(reinterpret_cast<const double2 *>(a.slot_hdr + par * G + q));
-                    const int qp = __double2hiint(raw.y);
-                    if (qp != INT_MAX) {
-                        const double vq2 = want_v2 ? __ldcg(a.slot_v2 + par * G + q) : -1.0;
-                        if (sq_better(raw.x, qp, v, p)) {
-                            v2 = fmax(fmax(v2, vq2), v);
-                            v = raw.x; p = qp; c = 0; sl = q;
-                        } else {
-                            v2 = fmax(fmax(v2, vq2), raw.x);
-                        }
-                    }
-                }
+            int p = INT_MAX, sl = -1;
+            const int q = lane + 32 * warp;
+            if (q < G) {
+                const double2 raw = __ldcg(reinterpret_cast<const double2 *>(a.slot_hdr + par * G + q));
+                const int qp = __double2hiint(raw.y);
+                if (qp != INT_MAX) { v = raw.x; p = qp; sl = q; }
+                if (want_v2) v2 = __ldcg(a.slot_v2 + par * G + q);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 const double ov = __shfl_xor_sync(0xffffffffu, v, o);
                 const int op = __shfl_xor_sync(0xffffffffu, p, o);
-                const int oc = __shfl_xor_sync(0xffffffffu, c, o);
                 const int osl = __shfl_xor_sync(0xffffffffu, sl, o);
                 const double ov2 = want_v2 ? __shfl_xor_sync(0xffffffffu, v2, o) : -1.0;
                 if (sq_better(ov, op, v, p)) {
                     v2 = fmax(fmax(v2, ov2), v);
-                    v = ov; p = op; c = oc; sl = osl;
+                    v = ov; p = op; sl = osl;
                 } else {
                     v2 = fmax(fmax(v2, ov2), ov);
                 }
             }
+            const double *src = a.slot_data + (int64_t)(par * G + (sl >= 0 ? sl : 0)) * lpad;
+#pragma unroll
+            for (int qq = 0; qq < SQ_RPL; ++qq) {
+                const int t = lane + 32 * qq;
+                xv[qq] = (sl >= 0 && t < l) ? __ldcg(src + t) : 0.0;
+            }
+            if (lane == 0) { wv[warp] = v; wv2[warp] = v2; wpos[warp] = p; wcol[warp] = sl; }
+        }
+        __syncthreads();
+        int ww = 0;  // warp holding the global winner (same choice in every thread)
+        {
+            double v = wv[0];
+            int p = wpos[0];
+            for (int w2 = 1; w2 < nsw; ++w2)
+                if (wcol[w2] >= 0 && (wcol[ww] < 0 || sq_better(wv[w2], wpos[w2], v, p))) {
+                    ww = w2; v = wv[w2]; p = wpos[w2];
+                }
+        }
+        if (warp == ww) {
+            const int sl = wcol[ww];
+            const double vbest = wv[ww];
+            double v2 = -1.0;
+            for (int w2 = 0; w2 < nsw; ++w2) v2 = fmax(v2, (w2 == ww) ? wv2[w2] : wv[w2]);
+            const bool stop = (sl < 0) || !(vbest > stop2);
             if (lane == 0) {
-                s_wpos = p;
+                s_stop = stop;
+                s_wpos = wpos[ww];
                 s_wcol = (sl >= 0) ? __ldcg(a.slot_col + par * G + sl) : -1;
-                s_wslot = sl;
-                s_stop = (sl < 0) || !(v > stop2);
-                if (g == 0 && want_v2 && !s_stop) a.gaps[j] = (v2 < 0.0 || v == 0.0) ? 1.0 : (v - v2) / v;
+                if (g == 0 && want_v2 && !stop) a.gaps[j] = (v2 < 0.0 || vbest == 0.0) ? 1.0 : (vbest - v2) / vbest;
+            }
+            if (!stop) {
+                double sx = 0.0, mine = 0.0;
+#pragma unroll
+                for (int qq = 0; qq < SQ_RPL; ++qq) {
+                    const int t = lane + 32 * qq;
+                    if (t > j) sx += xv[qq] * xv[qq];
+                    if (qq == (j >> 5)) mine = xv[qq];
+                }
+                sx = warp_sum(sx);
+                const double alpha = __shfl_sync(0xffffffffu, mine, j & 31);
+                double tau = 0.0, beta = alpha, scal = 0.0;
+                if (sx != 0.0) {
+                    const double nrm = sqrt(alpha * alpha + sx);
+                    beta = (alpha >= 0.0) ? -nrm : nrm;
+                    tau = (beta - alpha) / beta;
+                    scal = 1.0 / (alpha - beta);
+                }
+#pragma unroll
+                for (int qq = 0; qq < SQ_RPL; ++qq) {
+                    const int t = lane + 32 * qq;
+                    if (t < l) xs[t] = (t > j) ? xv[qq] * scal : (t == j ? 1.0 : xv[qq]);
+                }
+                if (lane == 0) { s_tau = tau; s_beta = beta; }
             }
         }
         __syncthreads();
         stamp(1);
         if (s_stop) break;
         const int wp = s_wpos, wcl = s_wcol;
-        // ---- 2. winner column -> Householder (warp 0, identical everywhere) --
-        if (warp == 0) {
-            const double *src = a.slot_data + (int64_t)(par * G + s_wslot) * lpad;
-            double xv[SQ_RPL];
-#pragma unroll
-            for (int q = 0; q < SQ_RPL; ++q) {
-                const int t = lane + 32 * q;
-                xv[q] = (t < l) ? __ldcg(src + t) : 0.0;
-            }
-            double s = 0.0, mine = 0.0;
-#pragma unroll
-            for (int q = 0; q < SQ_RPL; ++q) {
-                const int t = lane + 32 * q;
-                if (t > j) s += xv[q] * xv[q];
-                if (q == (j >> 5)) mine = xv[q];
-            }
-            s = warp_sum(s);
-            const double alpha = __shfl_sync(0xffffffffu, mine, j & 31);
-            double tau = 0.0, beta = alpha, scal = 0.0;
-            if (s != 0.0) {
-                const double nrm = sqrt(alpha * alpha + s);
-                beta = (alpha >= 0.0) ? -nrm : nrm;
-                tau = (beta - alpha) / beta;
-                scal = 1.0 / (alpha - beta);
-            }
-#pragma unroll
-            for (int q = 0; q < SQ_RPL; ++q) {
-                const int t = lane + 32 * q;
-                if (t < l) xs[t] = (t > j) ? xv[q] * scal : (t == j ? 1.0 : xv[q]);
-            }
-            if (lane == 0) { s_tau = tau; s_beta = beta; }
-        } else if (warp == 1 && lane == 0 && wcl >= c_lo && wcl < c_hi) {
-            act[wcl - c_lo] = 0;  // retire the pivot
-        }
+        if (tid == 0 && wcl >= c_lo && wcl < c_hi) act[wcl - c_lo] = 0;  // retire the pivot
         __syncthreads();
         stamp(2);
         const double tau = s_tau;
         // ---- outputs + position map (CTA 0) ----------------------------------
-        if (g == 0) {
+        // step-j outputs written by CTA (j+1) mod G (spreads the extra work:
+        // every CTA waits for the slowest at the barrier)
+        if (g == (j + 1) % G) {
             for (int t = tid; t < lpad; t += SQ_THREADS)
                 a.vhat[t + (int64_t)j * lpad] = (t < j) ? 0.0 : (t == j ? 1.0 : (t < l ? xs[t] : 0.0));
             for (int t = tid; t < a.bbpad; t += SQ_THREADS)
                 a.rhat11[t + (int64_t)j * a.bbpad] = (t < j) ? xs[t] : (t == j ? s_beta : 0.0);
+            if (tid == 0) { a.piv[j] = wp; a.tauhat[j] = tau; }
+        }
+        if (g == 0) {
             if (warp == SQ_WARPS - 1) {
                 // transposition j <-> wp; q = phys column at position j (< bb)
                 const int64_t q = low[j];
                 __syncwarp();
-                if (lane == 0) {
-                    a.piv[j] = wp;
-                    a.tauhat[j] = tau;
-                    low[j] = wcl;
-                }
+                if (lane == 0) low[j] = wcl;
                 if (wp != j) {
                     if (wp < a.bb) {
                         if (lane == 0) low[wp] = q;
@@ -356,11 +366,18 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
         auto apply_batch = [&](int cl0, int cend, auto colbase, int64_t ldcol) {
             double x[SQ_CB][SQ_RPL];
             bool live[SQ_CB];
+            double rr[SQ_CB], rr0[SQ_CB];
+            int lp[SQ_CB];
+            // all loads of the batch first (column rows + per-column state)
 #pragma unroll
             for (int u = 0; u < SQ_CB; ++u) {
                 const int cl = cl0 + u;
-                live[u] = (cl < cend) && act[cl];
-                const double *col = colbase + (int64_t)(live[u] ? cl : 0) * ldcol;
+                const int cs = (cl < cend) ? cl : cl0;
+                live[u] = (cl < cend) && act[cs];
+                rr[u] = r[cs];
+                rr0[u] = r0[cs];
+                lp[u] = lpos[cs];
+                const double *col = colbase + (int64_t)cs * ldcol;
 #pragma unroll
                 for (int q = 0; q < SQ_RPL; ++q) {
                     const int t = lane + 32 * q;
@@ -380,29 +397,36 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
             }
 #pragma unroll
             for (int u = 0; u < SQ_CB; ++u) w[u] = warp_sum(w[u]);
+            double bj[SQ_CB], tail[SQ_CB];
+#pragma unroll
+            for (int u = 0; u < SQ_CB; ++u) {
+                const double tw = tau * w[u];
+                bj[u] = 0.0;
+                tail[u] = 0.0;
+#pragma unroll
+                for (int q = 0; q < SQ_RPL; ++q) {
+                    const int t = lane + 32 * q;
+                    if (t >= j && t < l) x[u][q] -= tw * xs[t];
+                    if (t == j) bj[u] = x[u][q];
+                    if (t > j && t < l) tail[u] += x[u][q] * x[u][q];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < SQ_CB; ++u) bj[u] = __shfl_sync(0xffffffffu, bj[u], j & 31);
+            // stores + norm downdates (recompute on cancellation, R-G6)
 #pragma unroll
             for (int u = 0; u < SQ_CB; ++u) {
                 if (!live[u]) continue;
                 const int cl = cl0 + u;
-                const double tw = tau * w[u];
                 double *col = colbase + (int64_t)cl * ldcol;
-                double bj = 0.0, tail = 0.0;
 #pragma unroll
                 for (int q = 0; q < SQ_RPL; ++q) {
                     const int t = lane + 32 * q;
-                    if (t >= j && t < l) {
-                        x[u][q] -= tw * xs[t];
-                        col[t] = x[u][q];
-                    }
-                    if (t == j) bj = x[u][q];
-                    if (t > j && t < l) tail += x[u][q] * x[u][q];
+                    if (t >= j && t < l) col[t] = x[u][q];
                 }
-                bj = __shfl_sync(0xffffffffu, bj, j & 31);
-                double rn = r[cl] - bj * bj;
-                if (rn < 1e-6 * r0[cl]) rn = warp_sum(tail);  // uniform per column
-                int pos = lpos[cl];
-                if (pos == j) pos = wp;  // the column at position j moves to s*
-                __syncwarp();
+                double rn = rr[u] - bj[u] * bj[u];
+                if (rn < 1e-6 * rr0[u]) rn = warp_sum(tail[u]);  // uniform per column
+                const int pos = (lp[u] == j) ? wp : lp[u];         // position j moves to s*
                 if (lane == 0) { r[cl] = rn; lpos[cl] = pos; }
                 consider(rn, pos, (int)(c_lo + cl));
             }

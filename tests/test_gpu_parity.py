@@ -210,3 +210,38 @@ def test_factor_host_equals_device(ctx):
     assert rank == 96
     assert np.array_equal(Ah.numpy(), g["A"])
     assert np.array_equal(jp.numpy(), g["jpvt"])
+
+
+# ---- the grid-wide (non-cluster) sample-QRCP / panel kernels on the same cases ----
+@pytest.fixture(scope="module")
+def ctx_grid():
+    import os
+
+    import paper_1804_05138_b200 as rq
+    os.environ["RQRCP_NO_CLUSTER"] = "1"
+    try:
+        c = rq.RQRCP(max_m=4200, max_n=4200, max_b=128, max_p=32)
+    finally:
+        del os.environ["RQRCP_NO_CLUSTER"]
+    yield c
+    c.close()
+
+
+GRID_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "odd", "b128", "b1p0")]
+
+
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", GRID_CASES, ids=[c[0] for c in GRID_CASES])
+def test_factor_parity_grid_kernels(ctx_grid, name, kind, m, n, k, b, p, seed):
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    o = oracle.rqrcp(A, k, b, p, seed=seed)
+    g = gpu_factor(ctx_grid, A, k, b, p, seed)
+    compare(A, g, o, k)
+
+
+def test_cluster_and_grid_agree(ctx, ctx_grid):
+    """Both kernel families compute the same bits (same arithmetic order)."""
+    A = inputs.iid(21, 1200, 1000).numpy()
+    g1 = gpu_factor(ctx, A, 192, 64, 10, 4)
+    g2 = gpu_factor(ctx_grid, A, 192, 64, 10, 4)
+    assert np.array_equal(g1["jpvt"], g2["jpvt"])
+    assert np.max(np.abs(g1["A"] - g2["A"])) <= 1e-12 * np.max(np.abs(g1["A"]))

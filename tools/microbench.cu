@@ -86,6 +86,33 @@ __global__ void barrier_kernel(unsigned *bar, int iters, int variant) {
         for (int i = 0; i < iters; ++i) grid_barrier(bar, gridDim.x, epoch);
 }
 
+// exchange pattern of the sample QRCP step: publish 16-byte header, grid
+// barrier, warp 0 reads all G headers + argmax reduce, CTA barrier.
+__global__ void exchange_kernel(double2 *hdr, unsigned *bar, int iters, double *out) {
+    unsigned epoch = 0;
+    const int G = gridDim.x, g = blockIdx.x;
+    double best = 0;
+    for (int it = 0; it < iters; ++it) {
+        const int par = it & 1;
+        if (threadIdx.x == 0) hdr[par * G + g] = make_double2((double)((g * 7 + it) % G), (double)g);
+        grid_barrier(bar, G, epoch);
+        if (threadIdx.x < 32) {
+            double v = -1, p = 1e9;
+            for (int q = threadIdx.x; q < G; q += 32) {
+                const double2 h = __ldcg(hdr + par * G + q);
+                if (h.x > v || (h.x == v && h.y < p)) { v = h.x; p = h.y; }
+            }
+            for (int o = 16; o; o >>= 1) {
+                const double ov = __shfl_xor_sync(~0u, v, o), op = __shfl_xor_sync(~0u, p, o);
+                if (ov > v || (ov == v && op < p)) { v = ov; p = op; }
+            }
+            best += v + p;
+        }
+        __syncthreads();
+    }
+    if (best == 12345.0) out[0] = best;
+}
+
 int main() {
     int dev = 0, sms = 0, clk = 0;
     CK(cudaSetDevice(dev));
@@ -159,6 +186,26 @@ int main() {
             CK(cudaMemset(bar, 0, 64));
             cudaEventRecord(e0);
             CK(cudaLaunchCooperativeKernel((void *)barrier_kernel, dim3(g), dim3(256), args, 0, 0));
+            cudaEventRecord(e1);
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            printf("%s\"%d\": %.3f", first ? "" : ", ", g, ms * 1e3 / iters);
+            first = false;
+        }
+        printf("}");
+    }
+    printf(", \"exchange_us\": {");
+    {
+        double2 *hdr;
+        CK(cudaMalloc(&hdr, 2 * 160 * sizeof(double2)));
+        bool first = true;
+        for (int g : {8, 16, 32, 64, 96, 128, sms}) {
+            int iters = 2000;
+            void *args[] = {&hdr, &bar, (void *)&iters, &out};
+            CK(cudaMemset(bar, 0, 64));
+            cudaEventRecord(e0);
+            CK(cudaLaunchCooperativeKernel((void *)exchange_kernel, dim3(g), dim3(256), args, 0, 0));
             cudaEventRecord(e1);
             CK(cudaEventSynchronize(e1));
             float ms;
