@@ -90,8 +90,10 @@ int rqrcp_create(rqrcp_ctx **ctx, const rqrcp_config *cfg);
 
 /* Factor A in place (Alg. 2).
  *   A      device, column-major m x n (single GPU) or this rank's shard of the
- *          global columns {j : floor(j/b) mod nranks == rank}, m x n_loc
- *          (multi-GPU), leading dimension lda >= max(1, m); overwritten.
+ *          global columns {j : floor(j/b) mod nranks == rank}, m x n_loc with
+ *          n_loc = rqrcp_shard_columns(n, b, nranks, rank) (multi-GPU: every
+ *          rank calls rqrcp_factor with the same m, n, k, b, p, seed; jpvt and
+ *          tau come back identical on every rank), lda >= max(1, m); overwritten.
  *   m, n   global sizes, 1 <= m, n;  k target rank, 1 <= k <= min(m, n)
  *   b      panel width >= 1;  p oversampling >= 0 with b + p <= m
  *   seed   Philox key for Omega (never invalid)
@@ -137,6 +139,22 @@ int rqrcp_philox_words(rqrcp_ctx *ctx, const uint32_t *ctr, const uint32_t *key,
  * Householder QR sum_j 4(m-j)(n-j), out[2] sample QRCP, out[3] sample
  * update.  Host only; needs no context.  Returns 0 or a negative code. */
 int rqrcp_flops(int64_t m, int64_t n, int64_t k, int b, int p, double out[4]);
+
+/* Multi-GPU layout (1D column-block-cyclic, block = b):
+ * global column j lives on rank (j / b) mod nranks at local index
+ * (j / (b nranks)) b + j mod b; a rank's shard keeps global column order.
+ * Host-only, no context needed.
+ *   rqrcp_shard_columns: number of columns of `rank` (its n_loc); negative on
+ *     invalid arguments (-1 n, -2 b, -3 nranks, -4 rank).
+ *   rqrcp_shard_global_index: global column of local column `local_index`
+ *     of `rank` (negative on invalid arguments). */
+int64_t rqrcp_shard_columns(int64_t n, int b, int nranks, int rank);
+int64_t rqrcp_shard_global_index(int64_t local_index, int b, int nranks, int rank);
+
+/* Fresh ncclUniqueId bytes for rqrcp_config.nccl_uid (call on rank 0 and
+ * broadcast with torch.distributed).  Returns 0, or RQRCP_E_UNSUPPORTED when
+ * libnccl.so.2 cannot be loaded, or RQRCP_E_NCCL.  out: host, 128 bytes. */
+int rqrcp_nccl_unique_id(uint8_t *out);
 
 /* Per-phase timings of the last rqrcp_factor on ctx. */
 int rqrcp_get_timings(const rqrcp_ctx *ctx, rqrcp_timings *out);

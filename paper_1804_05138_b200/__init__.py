@@ -74,13 +74,38 @@ def lib():
         L.rqrcp_last_error.argtypes = [vp]
         L.rqrcp_last_error.restype = ctypes.c_char_p
         L.rqrcp_version.restype = ctypes.c_char_p
+        L.rqrcp_shard_columns.argtypes = [i64, ip, ip, ip]
+        L.rqrcp_shard_columns.restype = i64
+        L.rqrcp_shard_global_index.argtypes = [i64, ip, ip, ip]
+        L.rqrcp_shard_global_index.restype = i64
+        L.rqrcp_nccl_unique_id.argtypes = [ctypes.POINTER(ctypes.c_uint8)]
         _lib = L
     return _lib
 
 
 EXPORTED = ["rqrcp_create", "rqrcp_factor", "rqrcp_factor_host", "rqrcp_factor_ex", "rqrcp_fill_gaussian",
             "rqrcp_philox_words", "rqrcp_flops", "rqrcp_get_timings", "rqrcp_set_timing", "rqrcp_destroy",
-            "rqrcp_last_error", "rqrcp_version"]
+            "rqrcp_last_error", "rqrcp_version", "rqrcp_shard_columns", "rqrcp_shard_global_index",
+            "rqrcp_nccl_unique_id"]
+
+
+def shard_columns(n, b, nranks, rank):
+    """Global column indices held by `rank` in the 1D column-block-cyclic
+    layout (block = b), in local order (host-side, from the C library)."""
+    L = lib()
+    nloc = L.rqrcp_shard_columns(n, b, nranks, rank)
+    if nloc < 0:
+        raise ValueError("invalid layout arguments")
+    return [int(L.rqrcp_shard_global_index(q, b, nranks, rank)) for q in range(nloc)]
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (create on rank 0, broadcast to the others)."""
+    buf = (ctypes.c_uint8 * 128)()
+    rc = lib().rqrcp_nccl_unique_id(buf)
+    if rc:
+        raise RqrcpError(rc, "ncclGetUniqueId failed (libnccl.so.2 missing?)")
+    return bytes(buf)
 
 
 def rqrcp_flops(m, n, k, b, p):
@@ -123,6 +148,7 @@ class RQRCP:
             for i, v in enumerate(bytes(nccl_uid)[:128]):
                 cfg.nccl_uid[i] = v
         cfg.max_m, cfg.max_n, cfg.max_b, cfg.max_p = max_m, max_n, max_b, max_p
+        self.nranks, self.rank = nranks, rank
         h = ctypes.c_void_p()
         rc = lib().rqrcp_create(ctypes.byref(h), ctypes.byref(cfg))
         if rc:
@@ -134,10 +160,14 @@ class RQRCP:
         return RqrcpError(rc, msg.decode() if msg else "")
 
     def factor(self, A, k, b, p, seed=0, jpvt=None, tau=None, omega=None, omega_out=None, gaps=None,
-               allow_rank_deficient=True):
-        """Factor A in place (Alg. 2).  Returns (jpvt, tau, rank)."""
+               allow_rank_deficient=True, n=None):
+        """Factor A in place (Alg. 2).  Returns (jpvt, tau, rank).
+
+        Multi-GPU (nranks > 1): A is this rank's shard (shard_columns(n, b,
+        nranks, rank)) and n the global column count."""
         import torch
-        m, n, lda = _check_colmajor(A)
+        m, n_loc, lda = _check_colmajor(A)
+        n = n_loc if n is None else n
         if jpvt is None:
             jpvt = torch.empty(n, dtype=torch.int64, device=A.device)
         if tau is None:

@@ -101,15 +101,19 @@ __global__ void omhat_kernel(const double *rhat11, const double *A /* &A[i + i l
 }
 
 constexpr int SU_COLS = 16;
+// Local output column c = this rank's trailing column lj0 + c (global column
+// j = dist_global(lj0 + c), position j - i in the replicated sample).  P = 1:
+// j = lj0 + c with lj0 = i + bb.
 __global__ void __launch_bounds__(256) sample_update_kernel(const double *Bold, int64_t ldb, const int64_t *perm,
                                                             const double *omhat, int bbpad,
-                                                            const double *R12 /* &A[i + (i+bb) lda] */, int64_t lda,
-                                                            int bb, int l, int lpad, int64_t npp, const int *bb_eff,
-                                                            double *Bnew, int64_t ldn) {
+                                                            const double *R12 /* &A[i + lj0 lda] */, int64_t lda,
+                                                            int bb, int l, int lpad, int64_t npl, const int *bb_eff,
+                                                            double *Bnew, int64_t ldn, int64_t i, int64_t lj0, int b,
+                                                            int P, int rank) {
     if (*bb_eff != bb) return;
     __shared__ double r12[128 * SU_COLS];
     const int64_t c0 = (int64_t)blockIdx.x * SU_COLS;
-    const int ncols = (int)min((int64_t)SU_COLS, npp - c0);
+    const int ncols = (int)min((int64_t)SU_COLS, npl - c0);
     for (int e = threadIdx.x; e < bb * ncols; e += blockDim.x) {
         const int q = e % bb, c = e / bb;
         r12[q + c * 128] = R12[q + (c0 + c) * lda];
@@ -117,7 +121,9 @@ __global__ void __launch_bounds__(256) sample_update_kernel(const double *Bold, 
     __syncthreads();
     for (int e = threadIdx.x; e < lpad * ncols; e += blockDim.x) {
         const int r = e % lpad, c = e / lpad;
-        const int64_t src = perm[bb + c0 + c];
+        const int64_t lj = lj0 + c0 + c;
+        const int64_t j = ((lj / b) * P + rank) * b + lj % b;  // global column (dist_global)
+        const int64_t src = perm[j - i];
         double v = 0.0;
         if (r < bb) {
             double s = 0.0;

@@ -23,6 +23,7 @@
 #include "sample_qrcp.cuh"
 #include "tri.cuh"
 #include "cluster.cuh"
+#include "dist.cuh"
 
 using namespace rq;
 
@@ -77,6 +78,13 @@ struct rqrcp_ctx {
     // cooperative limits
     int sq_max_grid = 0, pn_max_grid = 0;
     int cluster_max = 0;  // largest usable cluster for the DSMEM kernels (0: none)
+    // multi-GPU (nranks > 1): NCCL communicator + exchange buffers
+    ncclComm_t comm = nullptr;
+    double *gsend = nullptr, *gbuf = nullptr, *pack = nullptr, *r11 = nullptr;
+    int64_t gbuf_elems = 0;
+    int64_t *dl_cols = nullptr;  // device lists for the cross-rank column moves
+    int *dl_slots = nullptr;
+    int64_t *h_pairs = nullptr;  // pinned host copy of (dst, src) pairs + count
     // timing
     bool timing = true;
     cudaEvent_t ev[2 * 4096 + 8];
@@ -351,6 +359,12 @@ extern "C" int rqrcp_flops(int64_t m, int64_t n, int64_t k, int b, int p, double
 }
 
 static int free_all(rqrcp_ctx *ctx) {
+    if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
+    ctx->comm = nullptr;
+    for (void *q : {(void *)ctx->gsend, (void *)ctx->gbuf, (void *)ctx->pack, (void *)ctx->r11, (void *)ctx->dl_cols,
+                    (void *)ctx->dl_slots})
+        if (q) cudaFree(q);
+    if (ctx->h_pairs) cudaFreeHost(ctx->h_pairs);
     void *ptrs[] = {ctx->omt,     ctx->bs[0],   ctx->bs[1],     ctx->vfull,     ctx->vt,        ctx->w,
                     ctx->w2,      ctx->tneg, ctx->ybuf,   ctx->rhat11,    ctx->omhat,     ctx->vhat,      ctx->tauhat,
                     ctx->splitk,  ctx->slot_hdr, ctx->slot_col, ctx->slot_v2,
@@ -368,7 +382,7 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     if (!cfg || cfg->max_m < 1 || cfg->max_n < 1 || cfg->max_b < 1 || cfg->max_b > 128 || cfg->max_p < 0 ||
         cfg->max_b + cfg->max_p > SQ_MAXL || cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks)
         return -2;
-    if (cfg->nranks > 1) return RQRCP_E_UNSUPPORTED;
+    if (cfg->nranks > 1 && !nccl().ok) return RQRCP_E_UNSUPPORTED;
     rqrcp_ctx *ctx = new rqrcp_ctx();
     ctx->device = cfg->device;
     ctx->nranks = cfg->nranks;
@@ -474,14 +488,32 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
                 ctx->cluster_max = cs;
         }
         cudaGetLastError();
-        const char *nc = getenv("RQRCP_NO_CLUSTER");
-        if (nc && nc[0] == '1') ctx->cluster_max = 0;
+        // opt-in: measured slower than the grid kernels from C2 (4096^2) up, where
+        // per-SM work outweighs the cheaper DSMEM exchange (profiles/README.md)
+        const char *cl = getenv("RQRCP_CLUSTER");
+        if (!(cl && cl[0] == '1')) ctx->cluster_max = 0;
     }
     CKC(cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (128 * 128 + 64 * 64) * 8));
     CKC(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
     for (auto &e : ctx->ev) CKC(cudaEventCreate(&e));
+    if (ctx->nranks > 1) {
+        const int P = ctx->nranks;
+        CKC(dalloc(&ctx->gsend, lp * (nn + bp)));
+        ctx->gbuf_elems = lp * (nn + (int64_t)P * bp);
+        CKC(dalloc(&ctx->gbuf, ctx->gbuf_elems));
+        CKC(dalloc(&ctx->pack, bp + 2 * bp * bp));
+        CKC(cudaMalloc((void **)&ctx->dl_cols, sizeof(int64_t) * 4 * bp));
+        CKC(cudaMalloc((void **)&ctx->dl_slots, sizeof(int) * 4 * bp));
+        CKC(cudaMallocHost((void **)&ctx->h_pairs, sizeof(int64_t) * (4 * bp + 2 + 8 * bp)));
+        ncclUniqueId uid;
+        memcpy(uid.internal, cfg->nccl_uid, sizeof(uid.internal));
+        if (nccl().CommInitRank(&ctx->comm, P, uid, ctx->rank) != 0) {
+            fprintf(stderr, "rqrcp_create: ncclCommInitRank failed\n");
+            return fail(RQRCP_E_NCCL);
+        }
+    }
     if (want_trace) {
         CKC(cudaMalloc((void **)&ctx->trace, sizeof(unsigned long long) * 2 * 64 * 8));
         CKC(cudaMemset(ctx->trace, 0, sizeof(unsigned long long) * 2 * 64 * 8));
@@ -502,6 +534,31 @@ extern "C" int rqrcp_destroy(rqrcp_ctx *ctx) {
     if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
+    return 0;
+}
+
+extern "C" int64_t rqrcp_shard_columns(int64_t n, int b, int nranks, int rank) {
+    if (n < 0) return -1;
+    if (b < 1) return -2;
+    if (nranks < 1) return -3;
+    if (rank < 0 || rank >= nranks) return -4;
+    return dist_count(n, b, nranks, rank);
+}
+
+extern "C" int64_t rqrcp_shard_global_index(int64_t local_index, int b, int nranks, int rank) {
+    if (local_index < 0) return -1;
+    if (b < 1) return -2;
+    if (nranks < 1) return -3;
+    if (rank < 0 || rank >= nranks) return -4;
+    return dist_global(local_index, b, nranks, rank);
+}
+
+extern "C" int rqrcp_nccl_unique_id(uint8_t *out) {
+    if (!out) return -1;
+    if (!nccl().ok) return RQRCP_E_UNSUPPORTED;
+    ncclUniqueId id;
+    if (nccl().GetUniqueId(&id) != 0) return RQRCP_E_NCCL;
+    memcpy(out, id.internal, sizeof(id.internal));
     return 0;
 }
 
@@ -562,6 +619,127 @@ static int cluster_launch(rqrcp_ctx *ctx, const void *func, int cs, int threads,
     return 0;
 }
 
+// ---------------------------------------------------------------------------
+// multi-GPU helpers; all enqueue on ctx->stream
+// ---------------------------------------------------------------------------
+#define CKN(call)                                                                     \
+    do {                                                                              \
+        ncclResult_t r_ = (call);                                                     \
+        if (r_ != 0) {                                                                \
+            ctx->err = std::string(#call) + ": " + nccl().GetErrorString(r_);         \
+            return RQRCP_E_NCCL;                                                      \
+        }                                                                             \
+    } while (0)
+
+// AllGather each rank's ncols_loc sample columns (global columns >= j0, local
+// order) and reorder into global order: out(:, p) = column j0 + p.
+static int gather_sample(rqrcp_ctx *ctx, int lpad, int64_t ncols_loc, int64_t j0, int64_t ncols, int b, double *out) {
+    const int P = ctx->nranks;
+    int64_t cmax = 0;
+    for (int r = 0; r < P; ++r)
+        cmax = std::max<int64_t>(cmax, dist_count(j0 + ncols, b, P, r) - dist_count(j0, b, P, r));
+    if (cmax * P * lpad > ctx->gbuf_elems) {
+        ctx->err = "gather buffer too small";
+        return RQRCP_E_WORKSPACE;
+    }
+    (void)ncols_loc;
+    ph_begin(ctx, PH_COMM);
+    CKN(nccl().AllGather(ctx->gsend, ctx->gbuf, (size_t)(cmax * lpad), ncclFloat64, ctx->comm, ctx->stream));
+    ph_end(ctx);
+    if (ncols > 0) {
+        dist_reorder_kernel<<<grid_for(ncols * lpad, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
+            ctx->gbuf, cmax, lpad, lpad, j0, ncols, b, P, out, lpad);
+        CKL();
+    }
+    return 0;
+}
+
+// The sample QRCP's (dst <- src) column moves (positions relative to i) on
+// the block-cyclic shards: local copies through the staging buffer, grouped
+// ncclSend/ncclRecv for pairs that cross ranks; jpvt (replicated) on every rank.
+static int dist_swaps(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t i, int b, int64_t *jpvt) {
+    const int P = ctx->nranks, me = ctx->rank;
+    cudaStream_t st = ctx->stream;
+    const int bp = ctx->bpad_max;
+    int64_t *hp = ctx->h_pairs;  // [0] count, [1..2bp] dst, [..] src
+    int hnp = 0;
+    CK(cudaMemcpyAsync(&hp[0], ctx->swap_np, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hp[1], ctx->swap_dst, sizeof(int64_t) * 2 * bp, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hp[1 + 2 * bp], ctx->swap_src, sizeof(int64_t) * 2 * bp, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));  // the pivots decide who talks to whom
+    memcpy(&hnp, &hp[0], sizeof(int));
+    const int64_t *dst = &hp[1], *src = &hp[1 + 2 * bp];
+    int64_t *lc = &hp[1 + 4 * bp];          // host lists: stage cols, place cols
+    int *ls = reinterpret_cast<int *>(&hp[1 + 6 * bp]);
+    int nst = 0, npl = 0;
+    std::vector<int> send_q, send_peer, recv_q, recv_peer;
+    for (int q = 0; q < hnp; ++q) {
+        const int so = dist_owner(i + src[q], b, P), dn = dist_owner(i + dst[q], b, P);
+        if (so == me) { lc[nst] = dist_local(i + src[q], b, P); ls[nst] = q; ++nst; }
+        if (so == me && dn != me) { send_q.push_back(q); send_peer.push_back(dn); }
+        if (dn == me && so != me) { recv_q.push_back(q); recv_peer.push_back(so); }
+    }
+    for (int q = 0; q < hnp; ++q) {
+        const int dn = dist_owner(i + dst[q], b, P);
+        if (dn == me) { lc[2 * bp + npl] = dist_local(i + dst[q], b, P); ls[2 * bp + npl] = q; ++npl; }
+    }
+    CK(cudaMemcpyAsync(ctx->dl_cols, lc, sizeof(int64_t) * 4 * bp, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->dl_slots, ls, sizeof(int) * 4 * bp, cudaMemcpyHostToDevice, st));
+    const int64_t lds = ctx->max_m;
+    if (nst) {
+        dist_columns_kernel<<<grid_for(nst * m, 256, ctx->num_sms), 256, 0, st>>>(A, lda, m, ctx->dl_cols, ctx->dl_slots,
+                                                                                  nst, ctx->swap_stage, lds, 0);
+        CKL();
+    }
+    if (!send_q.empty() || !recv_q.empty()) {
+        ph_begin(ctx, PH_COMM);
+        CKN(nccl().GroupStart());
+        for (size_t e = 0; e < send_q.size(); ++e)
+            CKN(nccl().Send(ctx->swap_stage + (int64_t)send_q[e] * lds, (size_t)m, ncclFloat64, send_peer[e], ctx->comm, st));
+        for (size_t e = 0; e < recv_q.size(); ++e)
+            CKN(nccl().Recv(ctx->swap_stage + (int64_t)recv_q[e] * lds, (size_t)m, ncclFloat64, recv_peer[e], ctx->comm, st));
+        CKN(nccl().GroupEnd());
+        ph_end(ctx);
+    }
+    if (npl) {
+        dist_columns_kernel<<<grid_for(npl * m, 256, ctx->num_sms), 256, 0, st>>>(
+            A, lda, m, ctx->dl_cols + 2 * bp, ctx->dl_slots + 2 * bp, npl, ctx->swap_stage, lds, 1);
+        CKL();
+    }
+    dist_jpvt_kernel<<<1, 256, 0, st>>>(jpvt + i, ctx->swap_dst, ctx->swap_src, ctx->swap_np);
+    CKL();
+    return 0;
+}
+
+// Owner of the panel broadcasts Vfull (ldo x bbpad), and [tau | V^T V | R11];
+// the others unpack and build V^T.
+static int dist_panel_bcast(rqrcp_ctx *ctx, int owner, const double *panel, int64_t lda, int64_t mp, int bb,
+                            int bbpad, double *tau_i) {
+    cudaStream_t st = ctx->stream;
+    const int me = ctx->rank;
+    const int npk = bbpad + 2 * bbpad * bbpad;
+    if (me == owner) {
+        dist_pack_kernel<<<grid_for(npk, 256, ctx->num_sms), 256, 0, st>>>(tau_i, ctx->ybuf, panel, lda, bb, bbpad,
+                                                                           ctx->pack);
+        CKL();
+    }
+    ph_begin(ctx, PH_COMM);
+    CKN(nccl().GroupStart());
+    CKN(nccl().Broadcast(ctx->vfull, ctx->vfull, (size_t)(ctx->ldo * bbpad), ncclFloat64, owner, ctx->comm, st));
+    CKN(nccl().Broadcast(ctx->pack, ctx->pack, (size_t)npk, ncclFloat64, owner, ctx->comm, st));
+    CKN(nccl().GroupEnd());
+    ph_end(ctx);
+    if (me != owner) {
+        dist_unpack_kernel<<<grid_for(bbpad + bbpad * bbpad, 256, ctx->num_sms), 256, 0, st>>>(ctx->pack, bb, bbpad,
+                                                                                              tau_i, ctx->ybuf);
+        CKL();
+        dist_transpose_kernel<<<grid_for(mp * bbpad, 256, ctx->num_sms), 256, 0, st>>>(ctx->vfull, ctx->ldo, mp, bbpad,
+                                                                                      ctx->vt);
+        CKL();
+    }
+    return 0;
+}
+
 static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
                        uint64_t seed, int64_t *jpvt, double *tau, int64_t *rank_out, const double *omega_in,
                        double *omega_out, double *gaps_out) {
@@ -581,6 +759,8 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         return RQRCP_E_WORKSPACE;
     }
     CK(cudaSetDevice(ctx->device));
+    const int P = ctx->nranks, me = ctx->rank;
+    const int64_t n_loc = dist_count(n, b, P, me);  // this rank's columns (n when P = 1)
     ctx->launches = 0;
     ctx->nev = 0;
     ctx->rec_phase.clear();
@@ -614,11 +794,17 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     ph_begin(ctx, PH_SKETCH);
     int cur = 0;
     bool tdone = false;
-    int rc = tma_skinny(ctx, lpad, n, m, ctx->omt, m, lpad, ctx->ldo, 0, 0, A, m, n, lda, 0, 0, ctx->bs[cur], lpad,
+    // this rank's columns: all of them (P = 1) or its block-cyclic shard
+    double *bdst = (P == 1) ? ctx->bs[cur] : ctx->gsend;
+    int rc = tma_skinny(ctx, lpad, n_loc, m, ctx->omt, m, lpad, ctx->ldo, 0, 0, A, m, n_loc, lda, 0, 0, bdst, lpad,
                         &tdone);
     if (rc) return rc;
-    if (!tdone) rc = gemm_skinny(ctx, lpad, n, m, ctx->omt, ctx->ldo, A, lda, ctx->bs[cur], lpad);
+    if (!tdone) rc = gemm_skinny(ctx, lpad, n_loc, m, ctx->omt, ctx->ldo, A, lda, bdst, lpad);
     if (rc) return rc;
+    if (P > 1) {  // replicate the sample in global column order (AllGather)
+        rc = gather_sample(ctx, lpad, n_loc, 0, n, b, ctx->bs[cur]);
+        if (rc) return rc;
+    }
     sumsq_partial_kernel<<<4 * G, 256, 0, st>>>(ctx->bs[cur], lpad, n, lpad, ctx->sumsq_part);
     CKL();
     sumsq_final_kernel<<<1, 32, 0, st>>>(ctx->sumsq_part, 4 * G, ctx->stop_tol2, ctx->iscal + 0);
@@ -698,7 +884,10 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         ph_end(ctx);
         // ---- S3: swaps on A and Pi -----------------------------------------
         ph_begin(ctx, PH_SWAP);
-        {
+        if (P > 1) {
+            rc = dist_swaps(ctx, A, lda, m, i, b, jpvt);
+            if (rc) return rc;
+        } else {
             const int64_t lds = ctx->max_m;
             const int gg = grid_for(2 * (int64_t)bb * m, 256, G);
             swap_gather_kernel<<<gg, 256, 0, st>>>(A + i * lda, lda, m, jpvt + i, ctx->swap_src, ctx->swap_np,
@@ -711,9 +900,11 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         ph_end(ctx);
         // ---- S4: panel QR + T ----------------------------------------------
         ph_begin(ctx, PH_PANEL);
-        {
+        const int owner = dist_owner(i, b, P);
+        const int64_t ljp = dist_local(i, b, P);  // owner's local column of the panel
+        if (me == owner) {
             PanelArgs a{};
-            a.A = A + i + i * lda;
+            a.A = A + i + ljp * lda;
             a.lda = lda;
             a.mp = mp;
             a.bb = bb;
@@ -756,6 +947,14 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             if (rc) return rc;
             }
         }
+        const double *R11p = A + i + ljp * lda;
+        int64_t ldr11 = lda;
+        if (P > 1) {  // owner broadcasts V, tau, V^T V and R11
+            rc = dist_panel_bcast(ctx, owner, A + i + ljp * lda, lda, mp, bb, bbpad, tau + i);
+            if (rc) return rc;
+            R11p = ctx->pack + bbpad + (int64_t)bbpad * bbpad;
+            ldr11 = bbpad;
+        }
         // T and Omega-hat11 on the side stream, overlapping W = V^T A22
         {
             int nb = 8;
@@ -764,28 +963,31 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             CK(cudaEventRecord(ctx->ev_fork, st));
             CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
             const int do_om = (i + bb < k && npp > 0) ? 1 : 0;
-            tri_kernel<<<2, TRI_THREADS, smem, ctx->side>>>(ctx->ybuf, tau + i, ctx->rhat11, A + i + i * lda, lda,
-                                                          bb, bbpad, nb, bb_eff, ctx->tneg, ctx->omhat, do_om);
+            tri_kernel<<<2, TRI_THREADS, smem, ctx->side>>>(ctx->ybuf, tau + i, ctx->rhat11, R11p, ldr11, bb, bbpad,
+                                                          nb, bb_eff, ctx->tneg, ctx->omhat, do_om);
             CKL();
             CK(cudaEventRecord(ctx->ev_join, ctx->side));
         }
         ph_end(ctx);
         // ---- S5: trailing update A22 -= V T^T V^T A22 ------------------------
         ph_begin(ctx, PH_TRAIL);
-        if (npp > 0) {
-            double *A22 = A + i + (i + bb) * lda;
-            // W = V^T A22: V = Vfull(0:m', 0:bbpad); A22 = A(i:m, i+bb:n) by TMA coordinates
-            rc = tma_skinny(ctx, bbpad, npp, mp, ctx->vfull, mp, bbpad, ctx->ldo, 0, 0, A, m, n, lda, i, i + bb,
+        // this rank's trailing columns: local [lj0, n_loc) = global columns >= i + bb
+        const int64_t lj0 = dist_count(i + bb, b, P, me);
+        const int64_t npl = n_loc - lj0;
+        if (npl > 0) {
+            double *A22 = A + i + lj0 * lda;
+            // W = V^T A22: V = Vfull(0:m', 0:bbpad); A22 = A(i:m, lj0:n_loc) by TMA coordinates
+            rc = tma_skinny(ctx, bbpad, npl, mp, ctx->vfull, mp, bbpad, ctx->ldo, 0, 0, A, m, n_loc, lda, i, lj0,
                             ctx->w, bbpad, &tdone);
             if (rc) return rc;
-            if (!tdone) rc = gemm_skinny(ctx, bbpad, npp, mp, ctx->vfull, ctx->ldo, A22, lda, ctx->w, bbpad);
+            if (!tdone) rc = gemm_skinny(ctx, bbpad, npl, mp, ctx->vfull, ctx->ldo, A22, lda, ctx->w, bbpad);
             if (rc) return rc;
             CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
-            rc = gemm_skinny(ctx, bbpad, npp, bbpad, ctx->tneg, bbpad, ctx->w, bbpad, ctx->w2, bbpad);
+            rc = gemm_skinny(ctx, bbpad, npl, bbpad, ctx->tneg, bbpad, ctx->w, bbpad, ctx->w2, bbpad);
             if (rc) return rc;
-            rc = tma_update(ctx, mp, npp, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda, &tdone);
+            rc = tma_update(ctx, mp, npl, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda, &tdone);
             if (rc) return rc;
-            if (!tdone) rc = gemm_update(ctx, mp, npp, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda);
+            if (!tdone) rc = gemm_update(ctx, mp, npl, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda);
             if (rc) return rc;
         } else {
             CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
@@ -794,10 +996,17 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         // ---- S6: sample update (Eq. (4)); skipped after the last panel (R-G9)
         if (i + bb < k && npp > 0) {
             ph_begin(ctx, PH_SUPD);
-            sample_update_kernel<<<(unsigned)((npp + SU_COLS - 1) / SU_COLS), 256, 0, st>>>(
-                ctx->bs[cur], lpad, ctx->perm, ctx->omhat, bbpad, A + i + (i + bb) * lda, lda, bb, l, lpad, npp,
-                bb_eff, ctx->bs[cur ^ 1], lpad);
-            CKL();
+            double *udst = (P == 1) ? ctx->bs[cur ^ 1] : ctx->gsend;
+            if (npl > 0) {
+                sample_update_kernel<<<(unsigned)((npl + SU_COLS - 1) / SU_COLS), 256, 0, st>>>(
+                    ctx->bs[cur], lpad, ctx->perm, ctx->omhat, bbpad, A + i + lj0 * lda, lda, bb, l, lpad, npl,
+                    bb_eff, udst, lpad, i, lj0, b, P, me);
+                CKL();
+            }
+            if (P > 1) {
+                rc = gather_sample(ctx, lpad, npl, i + bb, n - i - bb, b, ctx->bs[cur ^ 1]);
+                if (rc) return rc;
+            }
             ph_end(ctx);
             cur ^= 1;
         }
@@ -891,6 +1100,10 @@ extern "C" int rqrcp_factor_host(rqrcp_ctx *ctx, const double *A_host, int64_t l
     if (m > ctx->max_m || n > ctx->max_n) {
         ctx->err = "problem exceeds the create-time workspace maxima";
         return RQRCP_E_WORKSPACE;
+    }
+    if (ctx->nranks > 1) {
+        ctx->err = "rqrcp_factor_host is single-GPU only";
+        return RQRCP_E_UNSUPPORTED;
     }
     CK(cudaSetDevice(ctx->device));
     const int64_t need = m * n;

@@ -21,6 +21,7 @@ RES_ATOL = 1e-12
 
 @pytest.fixture(scope="module")
 def ctx():
+    """Default context: grid-wide (cooperative) sample-QRCP / panel kernels."""
     import paper_1804_05138_b200 as rq
     c = rq.RQRCP(max_m=4200, max_n=4200, max_b=128, max_p=32)
     yield c
@@ -212,17 +213,18 @@ def test_factor_host_equals_device(ctx):
     assert np.array_equal(jp.numpy(), g["jpvt"])
 
 
-# ---- the grid-wide (non-cluster) sample-QRCP / panel kernels on the same cases ----
+# ---- the thread-block-cluster (DSMEM) sample-QRCP / panel kernels (opt-in) ----
 @pytest.fixture(scope="module")
 def ctx_grid():
+    """Context with the cluster kernels enabled (RQRCP_CLUSTER=1 at create)."""
     import os
 
     import paper_1804_05138_b200 as rq
-    os.environ["RQRCP_NO_CLUSTER"] = "1"
+    os.environ["RQRCP_CLUSTER"] = "1"
     try:
         c = rq.RQRCP(max_m=4200, max_n=4200, max_b=128, max_p=32)
     finally:
-        del os.environ["RQRCP_NO_CLUSTER"]
+        del os.environ["RQRCP_CLUSTER"]
     yield c
     c.close()
 
@@ -231,7 +233,7 @@ GRID_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "odd", "b128", "b1p0"
 
 
 @pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", GRID_CASES, ids=[c[0] for c in GRID_CASES])
-def test_factor_parity_grid_kernels(ctx_grid, name, kind, m, n, k, b, p, seed):
+def test_factor_parity_cluster_kernels(ctx_grid, name, kind, m, n, k, b, p, seed):
     A = inputs.make(kind, m, n, seed, rank=64).numpy()
     o = oracle.rqrcp(A, k, b, p, seed=seed)
     g = gpu_factor(ctx_grid, A, k, b, p, seed)
