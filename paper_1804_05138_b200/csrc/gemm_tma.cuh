@@ -29,6 +29,7 @@ struct TmaGemmArgs {
     int64_t k_per_split;   // multiple of BK
     int splits;
     int64_t split_stride;
+    int vec2;              // EPI_ACCUM_T_PRE: C 16-byte aligned with even ldc -> double2 accesses
 };
 
 RQ_DEV unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -157,16 +158,31 @@ __global__ void __launch_bounds__(WM *WN * 32, 1)
 #pragma unroll
                 for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
             if (EPI == EPI_ACCUM_T_PRE) {
+                const bool interior = g.vec2 && Cn.m0 + BM <= g.M && Cn.n0 + BN <= g.N;
+                if (interior) {  // no predicates, 16-byte loads of (row, row+1) pairs
 #pragma unroll
-                for (int i = 0; i < MT; ++i) {
-                    const int64_t gm = Cn.m0 + wm * 8 * MT + i * 8 + fr;
+                    for (int i = 0; i < MT; ++i) {
+                        const int64_t gm = Cn.m0 + wm * 8 * MT + i * 8 + fr;
 #pragma unroll
-                    for (int j = 0; j < NT; ++j)
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int64_t gn = Cn.n0 + wn * 8 * NT + j * 8 + fk + h;
-                            cpre[i][j][h] = (gm < g.M && gn < g.N) ? g.C[gn + gm * g.ldc] : 0.0;
+                        for (int j = 0; j < NT; ++j) {
+                            const int64_t gn = Cn.n0 + wn * 8 * NT + j * 8 + fk;
+                            const double2 c2 = *reinterpret_cast<const double2 *>(g.C + gn + gm * g.ldc);
+                            cpre[i][j][0] = c2.x;
+                            cpre[i][j][1] = c2.y;
                         }
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < MT; ++i) {
+                        const int64_t gm = Cn.m0 + wm * 8 * MT + i * 8 + fr;
+#pragma unroll
+                        for (int j = 0; j < NT; ++j)
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int64_t gn = Cn.n0 + wn * 8 * NT + j * 8 + fk + h;
+                                cpre[i][j][h] = (gm < g.M && gn < g.N) ? g.C[gn + gm * g.ldc] : 0.0;
+                            }
+                    }
                 }
             }
         }
@@ -194,24 +210,37 @@ __global__ void __launch_bounds__(WM *WN * 32, 1)
         }
         if (Cn.kc == Cn.nk - 1) {
             // epilogue of this tile (stores overlap the next tile's loads)
+            if (EPI == EPI_ACCUM_T_PRE && g.vec2 && Cn.m0 + BM <= g.M && Cn.n0 + BN <= g.N) {
 #pragma unroll
-            for (int i = 0; i < MT; ++i) {
-                const int64_t gm = Cn.m0 + wm * 8 * MT + i * 8 + fr;
-                if (gm >= g.M) continue;
+                for (int i = 0; i < MT; ++i) {
+                    const int64_t gm = Cn.m0 + wm * 8 * MT + i * 8 + fr;
 #pragma unroll
-                for (int j = 0; j < NT; ++j)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int64_t gn = Cn.n0 + wn * 8 * NT + j * 8 + fk + h;
-                        if (gn >= g.N) continue;
-                        if (EPI == EPI_STORE) {
-                            g.C[gm + gn * g.ldc] = acc[i][j][h];
-                        } else if (EPI == EPI_PARTIAL) {
-                            g.C[(int64_t)Cn.split * g.split_stride + gm + gn * g.M] = acc[i][j][h];
-                        } else if (EPI == EPI_ACCUM_T_PRE) {
-                            g.C[gn + gm * g.ldc] = cpre[i][j][h] + acc[i][j][h];
-                        }
+                    for (int j = 0; j < NT; ++j) {
+                        const int64_t gn = Cn.n0 + wn * 8 * NT + j * 8 + fk;
+                        *reinterpret_cast<double2 *>(g.C + gn + gm * g.ldc) =
+                            make_double2(cpre[i][j][0] + acc[i][j][0], cpre[i][j][1] + acc[i][j][1]);
                     }
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < MT; ++i) {
+                    const int64_t gm = Cn.m0 + wm * 8 * MT + i * 8 + fr;
+                    if (gm >= g.M) continue;
+#pragma unroll
+                    for (int j = 0; j < NT; ++j)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int64_t gn = Cn.n0 + wn * 8 * NT + j * 8 + fk + h;
+                            if (gn >= g.N) continue;
+                            if (EPI == EPI_STORE) {
+                                g.C[gm + gn * g.ldc] = acc[i][j][h];
+                            } else if (EPI == EPI_PARTIAL) {
+                                g.C[(int64_t)Cn.split * g.split_stride + gm + gn * g.M] = acc[i][j][h];
+                            } else if (EPI == EPI_ACCUM_T_PRE) {
+                                g.C[gn + gm * g.ldc] = cpre[i][j][h] + acc[i][j][h];
+                            }
+                        }
+                }
             }
         }
         ++sc;

@@ -29,6 +29,7 @@ constexpr int PN_THREADS = 256;
 constexpr int PN_WARPS = PN_THREADS / 32;
 constexpr int PN_MAXB = 128;
 constexpr int PN_MAXROWS = 1024;  // rows per CTA (x staging buffer)
+constexpr int PN_CB = 8;          // columns per warp batch (interleaved reductions)
 
 struct PanelArgs {
     double *A;          // &A[i + i*lda]
@@ -36,21 +37,24 @@ struct PanelArgs {
     int64_t mp;         // m' rows
     int bb;             // planned panel width (columns present)
     int bbpad;
-    int use_smem;       // cache own rows (rows x bb) in dynamic shared memory
+    int use_smem;       // (cluster kernel) unused by the grid kernel
+    int nsm;            // rows per CTA cached in dynamic shared memory (grid kernel)
     const int *bb_eff;
     double *tau;        // tau + i
     double *vfull;      // mp x bbpad, ld ldv
     int64_t ldv;
     double *vt;         // bbpad x mp, ld bbpad
     double *ybuf;       // bbpad x bbpad: y(c, j) = v_c^T v_j for c < j (strict upper of V^T V)
-    double *part;       // [2][bbpad][G] partial Gram rows (column-major over CTAs)
+    double *part;       // [2][G][bbpad] partial Gram rows (one contiguous row per CTA)
     double *rowj;       // [2][bbpad] published row j
     unsigned *bar;      // per-launch barrier counter (zeroed by the host)
+    unsigned long long *trace;  // debug: [2 CTAs][64 steps][8 phases] clock64 stamps, or nullptr
 };
 
 __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
     extern __shared__ __align__(16) double pn_dyn[];
-    __shared__ double w[PN_MAXB];
+    __shared__ double w[PN_MAXB], rjs[PN_MAXB];
+    __shared__ double wred[PN_WARPS][PN_MAXB];
     __shared__ double xs[PN_MAXROWS];
     __shared__ double s_scal, s_tau, s_beta;
     const int G = gridDim.x, g = blockIdx.x;
@@ -64,59 +68,101 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
     const int64_t lda = a.lda;
     unsigned epoch = 0;
 
-    // P(r, c) = A(r_lo + r, c): shared-memory copy or the panel itself
-    double *P;
-    int64_t ldp;
-    if (a.use_smem) {
-        P = pn_dyn;
-        ldp = nrows;
-        for (int c = warp; c < bb; c += PN_WARPS)
-            for (int r = lane; r < nrows; r += 32) P[r + (int64_t)c * ldp] = a.A[r_lo + r + c * lda];
-        __syncthreads();
-    } else {
-        P = a.A + r_lo;
-        ldp = lda;
-    }
-
+    // rows [0, nsm) of this CTA's block live in shared memory (Ps, ld nsm),
+    // rows [nsm, nrows) stay in the panel itself (L2 / HBM)
+    const int nsm = min(nrows, a.nsm);
+    double *Ps = pn_dyn;
+    const int64_t lds = nsm > 0 ? nsm : 1;
+    double *Pg = a.A + r_lo;
+    for (int c = warp; c < bb; c += PN_WARPS)
+        for (int r = lane; r < nsm; r += 32) Ps[r + (int64_t)c * lds] = Pg[r + c * lda];
+    __syncthreads();
+    auto Pv = [&](int r, int c) -> double { return (r < nsm) ? Ps[r + (int64_t)c * lds] : Pg[r + (int64_t)c * lda]; };
+    const int tsel = (g == 0) ? 0 : (g == G - 1 ? 1 : -1);
     for (int j = 0; j < bbe; ++j) {
+        auto stamp = [&](int ph) {
+            if (a.trace && tsel >= 0 && tid == 0 && j < 64) a.trace[((size_t)tsel * 64 + j) * 8 + ph] = clock64();
+        };
+        stamp(0);
         const int par = j & 1;
         const int rj = (int)(j - r_lo);  // local index of row j (may be out of range)
-        // ---- partial Gram row over own rows r > j -----------------------
         const int rs = max(0, rj + 1);
-        for (int c = warp; c < bb; c += PN_WARPS) {
-            double s = 0.0;
-            for (int r = rs + lane; r < nrows; r += 32) s += P[r + (int64_t)c * ldp] * P[r + (int64_t)j * ldp];
-            s = warp_sum(s);
-            if (lane == 0) a.part[((int64_t)par * a.bbpad + c) * G + g] = s;
+        // ---- partial Gram row over own rows r > j (PN_CB columns per warp at
+        //      a time: all loads in flight, interleaved butterfly sums) -------
+        for (int c0 = warp * PN_CB; c0 < bb; c0 += PN_WARPS * PN_CB) {
+            double acc[PN_CB];
+#pragma unroll
+            for (int u = 0; u < PN_CB; ++u) acc[u] = 0.0;
+            for (int r = rs + lane; r < nsm; r += 32) {
+                const double xr = Ps[r + (int64_t)j * lds];
+#pragma unroll
+                for (int u = 0; u < PN_CB; ++u)
+                    if (c0 + u < bb) acc[u] += Ps[r + (int64_t)(c0 + u) * lds] * xr;
+            }
+            for (int r = max(rs, nsm) + lane; r < nrows; r += 32) {
+                const double xr = Pg[r + (int64_t)j * lda];
+#pragma unroll
+                for (int u = 0; u < PN_CB; ++u)
+                    if (c0 + u < bb) acc[u] += Pg[r + (int64_t)(c0 + u) * lda] * xr;
+            }
+#pragma unroll
+            for (int u = 0; u < PN_CB; ++u) acc[u] = warp_sum(acc[u]);
+            if (lane < PN_CB && c0 + lane < bb) {
+                double v = acc[0];
+#pragma unroll
+                for (int u = 1; u < PN_CB; ++u)
+                    if (lane == u) v = acc[u];
+                a.part[((int64_t)par * G + g) * a.bbpad + c0 + lane] = v;
+            }
         }
         if (rj >= 0 && rj < nrows)
-            for (int c = tid; c < bb; c += PN_THREADS) a.rowj[par * a.bbpad + c] = P[rj + (int64_t)c * ldp];
+            for (int c = tid; c < bb; c += PN_THREADS) a.rowj[par * a.bbpad + c] = Pv(rj, c);
+        stamp(1);
         grid_barrier(a.bar, G, epoch);
-        // ---- reduce the G partials (warp per column, fixed order) ----------
-        // (loads of up to 4 columns x 5 partials per lane issued before any add)
-        for (int c0 = warp; c0 < bb; c0 += 4 * PN_WARPS) {
-            double v[4][5];
+        stamp(2);
+        // ---- reduce the G partial rows (each CTA's row contiguous, coalesced
+        //      reads; warp w sums rows g = w, w+8, ... in order, then the 8 warp
+        //      sums are added in warp order: one fixed order in every CTA) ------
+        {
+            const double *pp = a.part + (int64_t)par * G * a.bbpad;
+            double acc[PN_MAXB / 32];
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
-                const int c = c0 + cc * PN_WARPS;
-                const double *pc = a.part + ((int64_t)par * a.bbpad + c) * G;
+            for (int u = 0; u < PN_MAXB / 32; ++u) acc[u] = 0.0;
+            for (int g0 = warp; g0 < G; g0 += 4 * PN_WARPS) {
+                double v[4][PN_MAXB / 32];
 #pragma unroll
-                for (int u = 0; u < 5; ++u) {
-                    const int q = lane + 32 * u;
-                    v[cc][u] = (c < bb && q < G) ? ld_cg(pc + q) : 0.0;
+                for (int h = 0; h < 4; ++h) {
+                    const int gg = g0 + h * PN_WARPS;
+#pragma unroll
+                    for (int u = 0; u < PN_MAXB / 32; ++u) {
+                        const int c = lane + 32 * u;
+                        v[h][u] = (gg < G && c < bb) ? ld_cg(pp + (int64_t)gg * a.bbpad + c) : 0.0;
+                    }
                 }
+#pragma unroll
+                for (int h = 0; h < 4; ++h)
+#pragma unroll
+                    for (int u = 0; u < PN_MAXB / 32; ++u) acc[u] += v[h][u];
             }
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
-                double s = v[cc][0] + v[cc][1] + v[cc][2] + v[cc][3] + v[cc][4];
-                s = warp_sum(s);
-                const int c = c0 + cc * PN_WARPS;
-                if (lane == 0 && c < bb) w[c] = s;
+            for (int u = 0; u < PN_MAXB / 32; ++u) {
+                const int c = lane + 32 * u;
+                if (c < bb) wred[warp][c] = acc[u];
             }
         }
+        if (warp == PN_WARPS - 1)
+            for (int c = lane; c < bb; c += 32) rjs[c] = ld_cg(a.rowj + par * a.bbpad + c);
         __syncthreads();
+        for (int c = tid; c < bb; c += PN_THREADS) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int ww = 0; ww < PN_WARPS; ++ww) sacc += wred[ww][c];
+            w[c] = sacc;
+        }
+        __syncthreads();
+        stamp(3);
         if (tid == 0) {
-            const double alpha = ld_cg(a.rowj + par * a.bbpad + j);
+            const double alpha = rjs[j];
             const double xn2 = w[j];
             double tau = 0.0, beta = alpha, scal = 0.0;
             if (xn2 != 0.0) {
@@ -133,38 +179,54 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
         // CTA 0 records y_c = v_c^T v_j = A(j,c) + scal g_c (c < j): column j of
         // strict_upper(V^T V), from which tri_kernel builds T off the critical path
         if (g == 0)
-            for (int c = tid; c < j; c += PN_THREADS)
-                a.ybuf[c + (int64_t)j * a.bbpad] = ld_cg(a.rowj + par * a.bbpad + c) + scal * w[c];
+            for (int c = tid; c < j; c += PN_THREADS) a.ybuf[c + (int64_t)j * a.bbpad] = rjs[c] + scal * w[c];
         // w_c = tau * (a_jc + scal g_c) for c > j
-        for (int c = j + 1 + tid; c < bb; c += PN_THREADS) w[c] = tau * (ld_cg(a.rowj + par * a.bbpad + c) + scal * w[c]);
-        for (int r = tid; r < nrows; r += PN_THREADS) xs[r] = P[r + (int64_t)j * ldp];
+        for (int c = j + 1 + tid; c < bb; c += PN_THREADS) w[c] = tau * (rjs[c] + scal * w[c]);
+        for (int r = tid; r < nrows; r += PN_THREADS) xs[r] = Pv(r, j);
         __syncthreads();
+        stamp(4);
         // ---- update own rows ---------------------------------------------
         if (tau != 0.0) {
             for (int c = j + 1 + warp; c < bb; c += PN_WARPS) {
                 const double wc = w[c];
-                for (int r = lane; r < nrows; r += 32) {
-                    if (r > rj) P[r + (int64_t)c * ldp] -= wc * (scal * xs[r]);
-                    else if (r == rj) P[r + (int64_t)c * ldp] -= wc;
+                for (int r = lane; r < nsm; r += 32) {
+                    if (r > rj) Ps[r + (int64_t)c * lds] -= wc * (scal * xs[r]);
+                    else if (r == rj) Ps[r + (int64_t)c * lds] -= wc;
+                }
+            }
+            // L2-resident rows: lane per row, PN_CB columns per batch (loads in flight)
+            for (int r = nsm + lane; r < nrows; r += 32) {
+                const double vr = (r > rj) ? scal * xs[r] : 1.0;
+                if (r < rj) continue;
+                for (int c0 = j + 1 + warp * PN_CB; c0 < bb; c0 += PN_WARPS * PN_CB) {
+                    double x[PN_CB];
+#pragma unroll
+                    for (int u = 0; u < PN_CB; ++u) x[u] = (c0 + u < bb) ? Pg[r + (int64_t)(c0 + u) * lda] : 0.0;
+#pragma unroll
+                    for (int u = 0; u < PN_CB; ++u)
+                        if (c0 + u < bb) Pg[r + (int64_t)(c0 + u) * lda] = x[u] - w[c0 + u] * vr;
                 }
             }
             for (int r = tid; r < nrows; r += PN_THREADS) {
-                if (r > rj) P[r + (int64_t)j * ldp] = scal * xs[r];
-                else if (r == rj) P[r + (int64_t)j * ldp] = s_beta;
+                const double v = (r > rj) ? scal * xs[r] : s_beta;
+                if (r >= rj) {
+                    if (r < nsm) Ps[r + (int64_t)j * lds] = v;
+                    else Pg[r + (int64_t)j * lda] = v;
+                }
             }
         }
         __syncthreads();
+        stamp(5);
     }
     // ---- write back, explicit V / V^T, zero tails (rank stop) -----------
-    if (a.use_smem) {
-        for (int c = warp; c < bb; c += PN_WARPS)
-            for (int r = lane; r < nrows; r += 32) a.A[r_lo + r + c * lda] = P[r + (int64_t)c * ldp];
-    }
+    for (int c = warp; c < bb; c += PN_WARPS)
+        for (int r = lane; r < nsm; r += 32) Pg[r + c * lda] = Ps[r + (int64_t)c * lds];
+    __syncthreads();
     for (int r = warp; r < nrows; r += PN_WARPS) {
         const int64_t gr = r_lo + r;
         for (int c = lane; c < a.bbpad; c += 32) {
             double v = 0.0;
-            if (c < bbe) v = (gr > c) ? P[r + (int64_t)c * ldp] : (gr == c ? 1.0 : 0.0);
+            if (c < bbe) v = (gr > c) ? Pg[r + (int64_t)c * lda] : (gr == c ? 1.0 : 0.0);
             a.vt[c + gr * a.bbpad] = v;
         }
     }
@@ -172,7 +234,7 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
         for (int r = lane; r < nrows; r += 32) {
             const int64_t gr = r_lo + r;
             double v = 0.0;
-            if (c < bbe) v = (gr > c) ? P[r + (int64_t)c * ldp] : (gr == c ? 1.0 : 0.0);
+            if (c < bbe) v = (gr > c) ? Pg[r + (int64_t)c * lda] : (gr == c ? 1.0 : 0.0);
             a.vfull[gr + c * a.ldv] = v;
         }
     if (g == 0)

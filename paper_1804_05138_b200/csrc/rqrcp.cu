@@ -95,6 +95,7 @@ struct rqrcp_ctx {
     int64_t launches = 0;
     bool debug_sync = false;  // RQRCP_DEBUG_SYNC=1: synchronise after every launch
     unsigned long long *trace = nullptr;  // RQRCP_TRACE=1: per-step phase stamps of the sample QRCP
+    unsigned long long *ptrace = nullptr; // ... and of the panel kernel
 };
 
 static const char *g_static_err = "no context";
@@ -275,7 +276,7 @@ static int tma_skinny_cfg(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const
     int splits = choose_splits(tiles, K, ctx->num_sms, M * N, ctx->splitk_elems);
     int64_t kps = rup((K + splits - 1) / splits, 32);
     splits = (int)((K + kps - 1) / kps);
-    TmaGemmArgs g{M, N, K, xk0, xm0, yk0, yn0, C, ldc, kps, splits, M * N};
+    TmaGemmArgs g{M, N, K, xk0, xm0, yk0, yn0, C, ldc, kps, splits, M * N, 0};
     if (splits <= 1) return launch_tma_cfg<MT, NT, WM, WN, EPI_STORE>(ctx, X, xdim0, xdim1, ldx, Y, ydim0, ydim1, ldy, g, done);
     g.C = ctx->splitk;
     int rc = launch_tma_cfg<MT, NT, WM, WN, EPI_PARTIAL>(ctx, X, xdim0, xdim1, ldx, Y, ydim0, ydim1, ldy, g, done);
@@ -305,7 +306,8 @@ static int tma_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, con
     *done = false;
     if (rows <= 0 || cols <= 0) { *done = true; return 0; }
     if ((lda & 1) || ((uintptr_t)A22 & 7)) return 0;
-    TmaGemmArgs g{cols, rows, K, 0, 0, 0, 0, A22, lda, rup(K, 32), 1, 0};
+    TmaGemmArgs g{cols, rows, K, 0, 0, 0, 0, A22, lda, rup(K, 32), 1, 0,
+                  (((uintptr_t)A22 & 15) == 0 && (lda & 1) == 0) ? 1 : 0};
     return launch_tma_cfg<4, 4, 2, 4, EPI_ACCUM_T_PRE>(ctx, w2, K, cols, ldw, vt, K, rows, ldvt, g, done);
 }
 
@@ -370,7 +372,7 @@ static int free_all(rqrcp_ctx *ctx) {
                     ctx->splitk,  ctx->slot_hdr, ctx->slot_col, ctx->slot_v2,
                     ctx->slot_data, ctx->pn_part, ctx->pn_rowj,   ctx->swap_stage,
                     ctx->swap_dst, ctx->swap_src, ctx->swap_jstage, ctx->swap_np, ctx->perm,     ctx->piv,       ctx->sumsq_part,
-                    ctx->iscal,   ctx->stop_tol2, ctx->bars,  ctx->trace,    ctx->a_dev,     ctx->jpvt_dev,  ctx->tau_dev};
+                    ctx->iscal,   ctx->stop_tol2, ctx->bars,  ctx->trace, ctx->ptrace,    ctx->a_dev,     ctx->jpvt_dev,  ctx->tau_dev};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     return 0;
@@ -517,6 +519,8 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     if (want_trace) {
         CKC(cudaMalloc((void **)&ctx->trace, sizeof(unsigned long long) * 2 * 64 * 8));
         CKC(cudaMemset(ctx->trace, 0, sizeof(unsigned long long) * 2 * 64 * 8));
+        CKC(cudaMalloc((void **)&ctx->ptrace, sizeof(unsigned long long) * 2 * 64 * 8));
+        CKC(cudaMemset(ctx->ptrace, 0, sizeof(unsigned long long) * 2 * 64 * 8));
     }
 #undef CKC
     *out = ctx;
@@ -918,6 +922,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.part = ctx->pn_part;
             a.rowj = ctx->pn_rowj;
             a.bar = ctx->bars + 2 * (panels - 1) + 1;
+            a.trace = (panels == 1) ? ctx->ptrace : nullptr;
             bool launched = false;
             if (ctx->cluster_max >= 2) {
                 const int cs = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->cluster_max, (mp + 31) / 32));
@@ -940,10 +945,11 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
                 ctx->err = "panel too tall for the cooperative grid";
                 return RQRCP_E_WORKSPACE;
             }
-            const size_t smem = (size_t)rpb * bb * sizeof(double);
-            a.use_smem = smem <= (size_t)kDynSmemMax;
+            // as many of each CTA's rows in shared memory as fit, the rest via L2
+            a.nsm = (int)std::min<int64_t>(rpb, kDynSmemMax / ((int64_t)bb * sizeof(double)));
+            const size_t smem = (size_t)a.nsm * bb * sizeof(double);
             void *args[] = {&a};
-            rc = coop_launch(ctx, (const void *)panel_qr_kernel, grid, PN_THREADS, args, a.use_smem ? smem : 0);
+            rc = coop_launch(ctx, (const void *)panel_qr_kernel, grid, PN_THREADS, args, smem);
             if (rc) return rc;
             }
         }
@@ -1055,6 +1061,21 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             }
             fprintf(stderr, "[rqrcp trace] sample QRCP CTA %s, %d steps, mean cycles:", c ? "last" : "0", cnt);
             for (int q = 0; q < 6; ++q) fprintf(stderr, " %s=%.0f", names[q], cnt ? acc[q] / cnt : 0.0);
+            fprintf(stderr, "\n");
+        }
+        cudaMemcpy(h, ctx->ptrace, sizeof(h), cudaMemcpyDeviceToHost);
+        const char *pn[5] = {"gram", "barrier", "reduce", "tau+w+x", "update"};
+        for (int c = 0; c < 2; ++c) {
+            double acc[5] = {0};
+            int cnt = 0;
+            for (int jj = 1; jj < 63; ++jj) {
+                const unsigned long long *r = h + ((size_t)c * 64 + jj) * 8;
+                if (!r[0] || !r[5]) continue;
+                for (int q = 0; q < 5; ++q) acc[q] += (double)(r[q + 1] - r[q]);
+                ++cnt;
+            }
+            fprintf(stderr, "[rqrcp trace] panel CTA %s, %d steps, mean cycles:", c ? "last" : "0", cnt);
+            for (int q = 0; q < 5; ++q) fprintf(stderr, " %s=%.0f", pn[q], cnt ? acc[q] / cnt : 0.0);
             fprintf(stderr, "\n");
         }
     }

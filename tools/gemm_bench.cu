@@ -104,7 +104,7 @@ int main(int argc, char **argv) {
     if (argc > 2) {  // small-shape TMA probe: M=8, N=30, K=40 with box 32 x 256 (bigger than the tensor)
         const int64_t M = 8, N = atoi(argv[2]), K = 40;
         CUtensorMap tx = make_map(V, K, M, K, 32), ty = make_map(A, K, N, K, 256);
-        TmaGemmArgs t{M, N, K, 0, 0, 0, 0, W, M, 64, 1, 0};
+        TmaGemmArgs t{M, N, K, 0, 0, 0, 0, W, M, 64, 1, 0, 0};
         run_tma<4, 4, 1, 8, 32, 3, EPI_STORE>(tx, ty, t, 1, 0);
         cudaError_t e = cudaDeviceSynchronize();
         printf("small N=%ld: %s\n", (long)N, cudaGetErrorString(e));
@@ -113,10 +113,10 @@ int main(int argc, char **argv) {
     if (prof) {  // one launch of each TMA kernel at C4 shape, for ncu
         const int64_t rows = 32768, cols = 32640, K = 128;
         CUtensorMap tx = make_map(W2, K, cols, K, 64), ty = make_map(Vt, K, rows, K, 128);
-        TmaGemmArgs t{cols, rows, K, 0, 0, 0, 0, A, rows, 128, 1, 0};
+        TmaGemmArgs t{cols, rows, K, 0, 0, 0, 0, A, rows, 128, 1, 0, 1};
         run_tma<4, 4, 2, 4, 32, 3, EPI_ACCUM_T_PRE>(tx, ty, t, sms, 0);
         CUtensorMap vx = make_map(V, rows, K, rows, (int)K), ay = make_map(A, rows, cols, rows, 64);
-        TmaGemmArgs w{K, cols, rows, 0, 0, 0, 0, P, K, (rows / 2 + 31) / 32 * 32, 2, K * cols};
+        TmaGemmArgs w{K, cols, rows, 0, 0, 0, 0, P, K, (rows / 2 + 31) / 32 * 32, 2, K * cols, 0};
         run_tma<4, 4, 4, 2, 32, 4, EPI_PARTIAL>(vx, ay, w, sms, 0);
         CK(cudaDeviceSynchronize());
         printf("prof done\n");
@@ -130,7 +130,7 @@ int main(int argc, char **argv) {
         GemmArgs g{cols, rows, K, W2, 80, Vt, 80, A, rows, 96, 0};
         run_cp<4, 4, 2, 4, 32, 2, EPI_ACCUM_T>(g, 1, 0);  // one launch (timeit warmup) -> A += ...
         CUtensorMap tx = make_map(W2, K, cols, 80, 64), ty = make_map(Vt, K, rows, 80, 128);
-        TmaGemmArgs t{cols, rows, K, 0, 0, 0, 0, A2, rows, 96, 1, 0};
+        TmaGemmArgs t{cols, rows, K, 0, 0, 0, 0, A2, rows, 96, 1, 0, 1};
         run_tma<4, 4, 2, 4, 32, 4, EPI_ACCUM_T_PRE>(tx, ty, t, sms, 0);
         CK(cudaMemset(dmax, 0, 8));
         maxdiff<<<256, 256>>>(A, A2, rows * cols, dmax);
@@ -147,7 +147,7 @@ int main(int argc, char **argv) {
         GemmArgs g{cols, rows, s.K, W2, s.K, Vt, s.K, A, rows, (s.K + 31) / 32 * 32, 0};
         float t0 = run_cp<4, 4, 2, 4, 32, 2, EPI_ACCUM_T>(g, 1, 5);
         CUtensorMap tx = make_map(W2, s.K, cols, s.K, 64), ty = make_map(Vt, s.K, rows, s.K, 128);
-        TmaGemmArgs t{cols, rows, s.K, 0, 0, 0, 0, A, rows, (s.K + 31) / 32 * 32, 1, 0};
+        TmaGemmArgs t{cols, rows, s.K, 0, 0, 0, 0, A, rows, (s.K + 31) / 32 * 32, 1, 0, 1};
         float t1 = run_tma<4, 4, 2, 4, 32, 4, EPI_ACCUM_T_PRE>(tx, ty, t, sms, 5);
         float t2 = run_tma<4, 4, 2, 4, 32, 3, EPI_ACCUM_T_PRE>(tx, ty, t, sms, 5);
         CUtensorMap ty2 = make_map(Vt, s.K, rows, s.K, 64);
@@ -166,7 +166,7 @@ int main(int argc, char **argv) {
         CUtensorMap tx = make_map(V, rows, s.K, rows, (int)s.K), ty = make_map(A, rows, cols, rows, s.K == 64 ? 128 : 64);
         for (int splits : {1, 2, 4}) {
             int64_t kps = ((rows + splits - 1) / splits + 31) / 32 * 32;
-            TmaGemmArgs t{s.K, cols, rows, 0, 0, 0, 0, splits > 1 ? P : W, s.K, kps, splits, s.K * cols};
+            TmaGemmArgs t{s.K, cols, rows, 0, 0, 0, 0, splits > 1 ? P : W, s.K, kps, splits, s.K * cols, 0};
             float tt;
             if (s.K == 64) tt = splits > 1 ? run_tma<4, 4, 2, 4, 32, 4, EPI_PARTIAL>(tx, ty, t, sms, 5) : run_tma<4, 4, 2, 4, 32, 4, EPI_STORE>(tx, ty, t, sms, 5);
             else tt = splits > 1 ? run_tma<4, 4, 4, 2, 32, 4, EPI_PARTIAL>(tx, ty, t, sms, 5) : run_tma<4, 4, 4, 2, 32, 4, EPI_STORE>(tx, ty, t, sms, 5);
@@ -175,7 +175,7 @@ int main(int argc, char **argv) {
         // W correctness vs cp.async version (split 1)
         GemmArgs g{s.K, cols, rows, V, rows, A, rows, Wb, s.K, (rows + 31) / 32 * 32, 0};
         if (s.K == 64) run_cp<4, 4, 2, 2, 32, 3, EPI_STORE>(g, 1, 0); else run_cp<4, 4, 4, 2, 32, 3, EPI_STORE>(g, 1, 0);
-        TmaGemmArgs t{s.K, cols, rows, 0, 0, 0, 0, W, s.K, (rows + 31) / 32 * 32, 1, 0};
+        TmaGemmArgs t{s.K, cols, rows, 0, 0, 0, 0, W, s.K, (rows + 31) / 32 * 32, 1, 0, 0};
         if (s.K == 64) run_tma<4, 4, 2, 4, 32, 4, EPI_STORE>(tx, ty, t, sms, 0); else run_tma<4, 4, 4, 2, 32, 4, EPI_STORE>(tx, ty, t, sms, 0);
         CK(cudaMemset(dmax, 0, 8));
         maxdiff<<<256, 256>>>(W, Wb, s.K * cols, dmax);
