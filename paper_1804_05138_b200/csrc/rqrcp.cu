@@ -22,7 +22,6 @@
 #include "philox.cuh"
 #include "sample_qrcp.cuh"
 #include "tri.cuh"
-#include "cluster.cuh"
 #include "dist.cuh"
 
 using namespace rq;
@@ -59,7 +58,9 @@ struct rqrcp_ctx {
     int *slot_col = nullptr;
     unsigned launch_seq = 0;  // tags of the sample-QRCP candidate headers
     double *slot_v2 = nullptr, *slot_data = nullptr;
-    double *pn_part = nullptr, *pn_rowj = nullptr;
+    double *sq_spill = nullptr;  // transposed sample columns beyond shared memory (lpad_max x max_n)
+    double *pn_part = nullptr, *pn_rowj = nullptr, *pn_spill = nullptr;
+    unsigned *pn_flags = nullptr;
     double *swap_stage = nullptr;
     int64_t *swap_dst = nullptr, *swap_src = nullptr, *swap_jstage = nullptr;
     int *swap_np = nullptr;
@@ -77,7 +78,6 @@ struct rqrcp_ctx {
     double *tau_dev = nullptr;
     // cooperative limits
     int sq_max_grid = 0, pn_max_grid = 0;
-    int cluster_max = 0;  // largest usable cluster for the DSMEM kernels (0: none)
     // multi-GPU (nranks > 1): NCCL communicator + exchange buffers
     ncclComm_t comm = nullptr;
     double *gsend = nullptr, *gbuf = nullptr, *pack = nullptr, *r11 = nullptr;
@@ -370,7 +370,7 @@ static int free_all(rqrcp_ctx *ctx) {
     void *ptrs[] = {ctx->omt,     ctx->bs[0],   ctx->bs[1],     ctx->vfull,     ctx->vt,        ctx->w,
                     ctx->w2,      ctx->tneg, ctx->ybuf,   ctx->rhat11,    ctx->omhat,     ctx->vhat,      ctx->tauhat,
                     ctx->splitk,  ctx->slot_hdr, ctx->slot_col, ctx->slot_v2,
-                    ctx->slot_data, ctx->pn_part, ctx->pn_rowj,   ctx->swap_stage,
+                    ctx->slot_data, ctx->sq_spill, ctx->pn_part, ctx->pn_rowj, ctx->pn_spill, ctx->pn_flags,   ctx->swap_stage,
                     ctx->swap_dst, ctx->swap_src, ctx->swap_jstage, ctx->swap_np, ctx->perm,     ctx->piv,       ctx->sumsq_part,
                     ctx->iscal,   ctx->stop_tol2, ctx->bars,  ctx->trace, ctx->ptrace,    ctx->a_dev,     ctx->jpvt_dev,  ctx->tau_dev};
     for (void *p : ptrs)
@@ -442,13 +442,17 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(dalloc(&ctx->tauhat, bp));
     ctx->splitk_elems = std::max<int64_t>(4 << 20, 0);
     CKC(dalloc(&ctx->splitk, ctx->splitk_elems));
-    CKC(cudaMalloc((void **)&ctx->slot_hdr, sizeof(SqHdr) * 2 * G));
-    CKC(cudaMemset(ctx->slot_hdr, 0, sizeof(SqHdr) * 2 * G));
+    CKC(cudaMalloc((void **)&ctx->slot_hdr, sizeof(SqHdr) * 2 * SQ_MAXG * 8));
+    CKC(cudaMemset(ctx->slot_hdr, 0, sizeof(SqHdr) * 2 * SQ_MAXG * 8));
     CKC(cudaMalloc((void **)&ctx->slot_col, sizeof(int) * 2 * G));
     CKC(dalloc(&ctx->slot_v2, 2 * G));
     CKC(dalloc(&ctx->slot_data, 2 * G * lp));
+    CKC(dalloc(&ctx->sq_spill, lp * nn));
     CKC(dalloc(&ctx->pn_part, 2 * G * bp));
     CKC(dalloc(&ctx->pn_rowj, 2 * bp));
+    CKC(dalloc(&ctx->pn_spill, mm * bp));
+    CKC(cudaMalloc((void **)&ctx->pn_flags, sizeof(unsigned) * 2 * PN_MAXG * 32));
+    CKC(cudaMemset(ctx->pn_flags, 0, sizeof(unsigned) * 2 * PN_MAXG * 32));
     CKC(dalloc(&ctx->swap_stage, 2 * bp * mm));
     CKC(cudaMalloc((void **)&ctx->swap_dst, sizeof(int64_t) * 2 * bp));
     CKC(cudaMalloc((void **)&ctx->swap_src, sizeof(int64_t) * 2 * bp));
@@ -465,36 +469,6 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(cudaMemset(ctx->tneg, 0, sizeof(double) * bp * bp));
     CKC(cudaFuncSetAttribute(sample_qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
     CKC(cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
-    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
-    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
-    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    {
-        // largest cluster (<= 16) that can be resident with a full shared-memory budget
-        ctx->cluster_max = 0;
-        for (int cs = 16; cs >= 2 && !ctx->cluster_max; cs /= 2) {
-            cudaLaunchConfig_t lc = {};
-            lc.gridDim = dim3(cs);
-            lc.blockDim = dim3(SQ_THREADS);
-            lc.dynamicSmemBytes = kDynSmemMax;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = cs;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            lc.attrs = at;
-            lc.numAttrs = 1;
-            int nclusters = 0;
-            if (cudaOccupancyMaxActiveClusters(&nclusters, (void *)sample_qrcp_cluster_kernel, &lc) == cudaSuccess &&
-                nclusters >= 1)
-                ctx->cluster_max = cs;
-        }
-        cudaGetLastError();
-        // opt-in: measured slower than the grid kernels from C2 (4096^2) up, where
-        // per-SM work outweighs the cheaper DSMEM exchange (profiles/README.md)
-        const char *cl = getenv("RQRCP_CLUSTER");
-        if (!(cl && cl[0] == '1')) ctx->cluster_max = 0;
-    }
     CKC(cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (128 * 128 + 64 * 64) * 8));
     CKC(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
@@ -517,10 +491,10 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
         }
     }
     if (want_trace) {
-        CKC(cudaMalloc((void **)&ctx->trace, sizeof(unsigned long long) * 2 * 64 * 8));
-        CKC(cudaMemset(ctx->trace, 0, sizeof(unsigned long long) * 2 * 64 * 8));
-        CKC(cudaMalloc((void **)&ctx->ptrace, sizeof(unsigned long long) * 2 * 64 * 8));
-        CKC(cudaMemset(ctx->ptrace, 0, sizeof(unsigned long long) * 2 * 64 * 8));
+        CKC(cudaMalloc((void **)&ctx->trace, sizeof(unsigned long long) * SQ_MAXG * 64 * 4));
+        CKC(cudaMemset(ctx->trace, 0, sizeof(unsigned long long) * SQ_MAXG * 64 * 4));
+        CKC(cudaMalloc((void **)&ctx->ptrace, sizeof(unsigned long long) * PN_MAXG * 64 * 4));
+        CKC(cudaMemset(ctx->ptrace, 0, sizeof(unsigned long long) * PN_MAXG * 64 * 4));
     }
 #undef CKC
     *out = ctx;
@@ -598,29 +572,6 @@ static int coop_launch(rqrcp_ctx *ctx, const void *func, int grid, int threads, 
 __global__ void iota_kernel(int64_t *x, int64_t n) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
         x[e] = e;
-}
-
-static int cluster_launch(rqrcp_ctx *ctx, const void *func, int cs, int threads, void **args, size_t smem) {
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(cs);
-    lc.blockDim = dim3(threads);
-    lc.dynamicSmemBytes = smem;
-    lc.stream = ctx->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelExC(&lc, func, args);
-    if (e == cudaSuccess && ctx->debug_sync) e = cudaStreamSynchronize(ctx->stream);
-    if (e != cudaSuccess) {
-        ctx->err = std::string("cluster launch: ") + cudaGetErrorString(e);
-        return RQRCP_E_CUDA;
-    }
-    ctx->launches++;
-    return 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -854,36 +805,41 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.rank = rankd;
             a.status = status;
             a.gaps = gaps_out ? gaps_out + i : nullptr;
-            a.bar = ctx->bars + 2 * (panels - 1);
             a.swap_dst = ctx->swap_dst;
             a.swap_src = ctx->swap_src;
             a.swap_np = ctx->swap_np;
             a.trace = (panels == 1) ? ctx->trace : nullptr;
-            bool launched = false;
-            if (ctx->cluster_max >= 2) {
-                const int cs = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->cluster_max, np));
-                const int64_t ccpb = (np + cs - 1) / cs;
-                const size_t csm = (size_t)ccpb * ((size_t)lpad * 8 + 24);
-                if (cs >= 2 && csm <= (size_t)kDynSmemMax) {
-                    void *args[] = {&a};
-                    rc = cluster_launch(ctx, (const void *)sample_qrcp_cluster_kernel, cs, SQ_THREADS, args, csm);
-                    if (rc) return rc;
-                    launched = true;
-                }
-            }
-            if (!launched) {
-            int gcap = G;
-            if (const char *e = getenv("RQRCP_SQ_GRID")) gcap = std::max(1, std::min(G, atoi(e)));
+            a.spill = ctx->sq_spill;
+            a.hstride = 8;
+            a.poll_mode = 1;
+            if (const char *e = getenv("RQRCP_SQ_HSTRIDE")) a.hstride = std::max(1, std::min(8, atoi(e)));
+            if (const char *e = getenv("RQRCP_SQ_POLL")) a.poll_mode = std::max(0, std::min(2, atoi(e)));
+            int gcap = std::min(G, SQ_MAXG);
+            if (const char *e = getenv("RQRCP_SQ_GRID")) gcap = std::max(1, std::min(gcap, atoi(e)));
             const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(gcap, (np + 7) / 8));
             const int64_t cpb = (np + grid - 1) / grid;
-            // as many columns in shared memory as the budget allows, the rest in L2
-            const int64_t room = (int64_t)kDynSmemMax - cpb * (2 * (int64_t)sizeof(double) + 2 * (int64_t)sizeof(int));
-            a.nsm = (int)std::max<int64_t>(0, std::min<int64_t>(cpb, room / ((int64_t)lpad * 8)));
-            const size_t smem = sq_smem_bytes(a.nsm, cpb, lpad);
+            // threads per column: fill the CTA (columns x tpc <= 256)
+            int tpc = 32;
+            while (tpc > 1 && cpb * tpc > SQ_THREADS) tpc >>= 1;
+            a.tpc = tpc;
+            const int cpw = 32 / tpc;
+            // as many columns in shared memory as the budget allows (row stride
+            // ncs = cpw mod 16 keeps the group's accesses conflict-free), the
+            // rest transposed in the L2-resident spill buffer
+            auto pad_ncs = [&](int64_t x) -> int64_t {
+                if (cpw >= 16 || x <= 0) return std::max<int64_t>(x, 1);
+                return x + (((cpw - x) % 16) + 16) % 16;
+            };
+            const int64_t state = cpb * (2 * (int64_t)sizeof(double) + 2 * (int64_t)sizeof(int));
+            int64_t nsm = cpb;
+            if (const char *e = getenv("RQRCP_SQ_NSM")) nsm = std::max<int64_t>(0, std::min<int64_t>(nsm, atoi(e)));
+            while (nsm > 0 && (int64_t)l * pad_ncs(nsm) * 8 + state > kDynSmemMax) --nsm;
+            a.nsm = (int)nsm;
+            a.ncs = (int)pad_ncs(nsm);
+            const size_t smem = sq_smem_bytes(a.ncs, cpb, l);
             void *args[] = {&a};
             rc = coop_launch(ctx, (const void *)sample_qrcp_kernel, grid, SQ_THREADS, args, smem);
             if (rc) return rc;
-            }
         }
         ph_end(ctx);
         // ---- S3: swaps on A and Pi -----------------------------------------
@@ -921,37 +877,33 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.ybuf = ctx->ybuf;
             a.part = ctx->pn_part;
             a.rowj = ctx->pn_rowj;
-            a.bar = ctx->bars + 2 * (panels - 1) + 1;
+            a.flags = ctx->pn_flags;
+            a.tag0 = (++ctx->launch_seq) << 8;
+            a.spill = ctx->pn_spill;
+            a.poll_mode = 1;
+            if (const char *e = getenv("RQRCP_PN_POLL")) a.poll_mode = std::max(0, std::min(1, atoi(e)));
             a.trace = (panels == 1) ? ctx->ptrace : nullptr;
-            bool launched = false;
-            if (ctx->cluster_max >= 2) {
-                const int cs = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->cluster_max, (mp + 31) / 32));
-                const int64_t crpb = (mp + cs - 1) / cs;
-                const size_t csm = ((size_t)crpb * bb + 4 * (size_t)bbpad) * sizeof(double);
-                if (cs >= 2 && crpb <= PN_MAXROWS && csm <= (size_t)kDynSmemMax) {
-                    void *args[] = {&a};
-                    rc = cluster_launch(ctx, (const void *)panel_qr_cluster_kernel, cs, PN_THREADS, args, csm);
-                    if (rc) return rc;
-                    launched = true;
-                }
-            }
-            if (!launched) {
-            int pcap = G;
-            if (const char *e = getenv("RQRCP_PN_GRID")) pcap = std::max(1, std::min(G, atoi(e)));
+            int pcap = std::min(G, PN_MAXG);
+            if (const char *e = getenv("RQRCP_PN_GRID")) pcap = std::max(1, std::min(pcap, atoi(e)));
+            int64_t rows_target = 64;
+            if (const char *e = getenv("RQRCP_PN_ROWS")) rows_target = std::max(1, atoi(e));
             const int grid = (int)std::max<int64_t>((mp + PN_MAXROWS - 1) / PN_MAXROWS,
-                                                    std::min<int64_t>(pcap, (mp + 31) / 32));
+                                                    std::min<int64_t>(pcap, (mp + rows_target - 1) / rows_target));
             const int64_t rpb = (mp + grid - 1) / grid;
-            if (rpb > PN_MAXROWS) {
+            if (rpb > PN_MAXROWS || grid > pcap) {
                 ctx->err = "panel too tall for the cooperative grid";
                 return RQRCP_E_WORKSPACE;
             }
-            // as many of each CTA's rows in shared memory as fit, the rest via L2
-            a.nsm = (int)std::min<int64_t>(rpb, kDynSmemMax / ((int64_t)bb * sizeof(double)));
-            const size_t smem = (size_t)a.nsm * bb * sizeof(double);
+            // row-major tile with an odd row stride (conflict-free column and
+            // row walks); as many rows in shared memory as fit, the rest in the
+            // row-major scratch
+            a.ldt = bb | 1;
+            a.nsm = (int)std::min<int64_t>(rpb, kDynSmemMax / ((int64_t)a.ldt * sizeof(double)));
+            if (const char *e = getenv("RQRCP_PN_NSM")) a.nsm = std::max(0, std::min(a.nsm, atoi(e)));
+            const size_t smem = std::max<size_t>(8, (size_t)a.nsm * a.ldt * sizeof(double));
             void *args[] = {&a};
             rc = coop_launch(ctx, (const void *)panel_qr_kernel, grid, PN_THREADS, args, smem);
             if (rc) return rc;
-            }
         }
         const double *R11p = A + i + ljp * lda;
         int64_t ldr11 = lda;
@@ -1045,37 +997,65 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         t.comm_ms = acc[PH_COMM];
     }
     if (ctx->trace) {
-        unsigned long long h[2 * 64 * 8];
-        cudaMemcpy(h, ctx->trace, sizeof(h), cudaMemcpyDeviceToHost);
-        const char *names[6] = {"scan", "householder", "out+apply", "publish", "barrier", "->next"};
-        for (int c = 0; c < 2; ++c) {
-            double acc[6] = {0};
+        std::vector<unsigned long long> H((size_t)SQ_MAXG * 64 * 4);
+        cudaMemcpy(H.data(), ctx->trace, sizeof(unsigned long long) * H.size(), cudaMemcpyDeviceToHost);
+        const char *names[4] = {"poll+winner+householder", "apply", "publish", "->next"};
+        double all[4] = {0}, worst_apply = 0;
+        int ncta = 0, worst = -1;
+        for (int c = 0; c < SQ_MAXG; ++c) {
+            double acc[4] = {0};
             int cnt = 0;
             for (int jj = 1; jj < 63; ++jj) {
-                const unsigned long long *r = h + ((size_t)c * 64 + jj) * 8;
-                const unsigned long long *nx = h + ((size_t)c * 64 + jj + 1) * 8;
-                if (!r[0] || !r[5] || !nx[0]) continue;
-                for (int q = 0; q < 5; ++q) acc[q] += (double)(r[q + 1] - r[q]);
-                acc[5] += (double)(nx[0] - r[5]);
+                const unsigned long long *r = H.data() + ((size_t)c * 64 + jj) * 4;
+                const unsigned long long *nx = H.data() + ((size_t)c * 64 + jj + 1) * 4;
+                if (!r[0] || !r[3] || !nx[0]) continue;
+                for (int q = 0; q < 3; ++q) acc[q] += (double)(r[q + 1] - r[q]);
+                acc[3] += (double)(nx[0] - r[3]);
                 ++cnt;
             }
-            fprintf(stderr, "[rqrcp trace] sample QRCP CTA %s, %d steps, mean cycles:", c ? "last" : "0", cnt);
-            for (int q = 0; q < 6; ++q) fprintf(stderr, " %s=%.0f", names[q], cnt ? acc[q] / cnt : 0.0);
-            fprintf(stderr, "\n");
+            if (!cnt) continue;
+            for (int q = 0; q < 4; ++q) acc[q] /= cnt;
+            if (c == 0) {
+                fprintf(stderr, "[rqrcp trace] sample QRCP CTA 0, %d steps, mean cycles:", cnt);
+                for (int q = 0; q < 4; ++q) fprintf(stderr, " %s=%.0f", names[q], acc[q]);
+                fprintf(stderr, "\n");
+            }
+            for (int q = 0; q < 4; ++q) all[q] += acc[q];
+            if (acc[1] + acc[2] > worst_apply) { worst_apply = acc[1] + acc[2]; worst = c; }
+            ++ncta;
         }
-        cudaMemcpy(h, ctx->ptrace, sizeof(h), cudaMemcpyDeviceToHost);
-        const char *pn[5] = {"gram", "barrier", "reduce", "tau+w+x", "update"};
-        for (int c = 0; c < 2; ++c) {
-            double acc[5] = {0};
+        if (ncta) {
+            fprintf(stderr, "[rqrcp trace] sample QRCP mean over %d CTAs:", ncta);
+            for (int q = 0; q < 4; ++q) fprintf(stderr, " %s=%.0f", names[q], all[q] / ncta);
+            fprintf(stderr, "; slowest apply+publish: CTA %d (%.0f cycles)\n", worst, worst_apply);
+        }
+        cudaMemcpy(H.data(), ctx->ptrace, sizeof(unsigned long long) * (size_t)PN_MAXG * 64 * 4, cudaMemcpyDeviceToHost);
+        const char *pn[4] = {"poll", "reduce+coeffs", "pass", "publish"};
+        double pall[4] = {0};
+        int pcta = 0;
+        for (int c = 0; c < PN_MAXG; ++c) {
+            double acc[4] = {0};
             int cnt = 0;
             for (int jj = 1; jj < 63; ++jj) {
-                const unsigned long long *r = h + ((size_t)c * 64 + jj) * 8;
-                if (!r[0] || !r[5]) continue;
-                for (int q = 0; q < 5; ++q) acc[q] += (double)(r[q + 1] - r[q]);
+                const unsigned long long *r = H.data() + ((size_t)c * 64 + jj) * 4;
+                const unsigned long long *nx = H.data() + ((size_t)c * 64 + jj + 1) * 4;
+                if (!r[0] || !r[3] || !nx[0]) continue;
+                for (int q = 0; q < 3; ++q) acc[q] += (double)(r[q + 1] - r[q]);
+                acc[3] += (double)(nx[0] - r[3]);
                 ++cnt;
             }
-            fprintf(stderr, "[rqrcp trace] panel CTA %s, %d steps, mean cycles:", c ? "last" : "0", cnt);
-            for (int q = 0; q < 5; ++q) fprintf(stderr, " %s=%.0f", pn[q], cnt ? acc[q] / cnt : 0.0);
+            if (!cnt) continue;
+            for (int q = 0; q < 4; ++q) pall[q] += acc[q] / cnt;
+            if (c == 0) {
+                fprintf(stderr, "[rqrcp trace] panel CTA 0, %d steps, mean cycles:", cnt);
+                for (int q = 0; q < 4; ++q) fprintf(stderr, " %s=%.0f", pn[q], acc[q] / cnt);
+                fprintf(stderr, "\n");
+            }
+            ++pcta;
+        }
+        if (pcta) {
+            fprintf(stderr, "[rqrcp trace] panel mean over %d CTAs:", pcta);
+            for (int q = 0; q < 4; ++q) fprintf(stderr, " %s=%.0f", pn[q], pall[q] / pcta);
             fprintf(stderr, "\n");
         }
     }

@@ -3,33 +3,40 @@
 //
 // One persistent cooperative kernel; CTA g owns a contiguous range of the
 // sample's PHYSICAL columns and keeps them in place for the whole panel (a
-// transposition j <-> s* only relabels logical positions).  As many of its
-// columns as fit live in shared memory, the rest stay in global memory (L2);
-// per-column state (squared norm, its panel-start value, logical position,
-// active flag) always lives in shared memory.  Each warp processes SQ_CB
-// columns at a time with all their loads in flight, lanes over the l <= 160
-// rows, deterministic butterfly sums.  Per step j, exactly one grid barrier:
-//   1. warp 0 of every CTA loads the G candidate headers (one 16-byte load
-//      each; a step tag makes stale slots detectable) and reduces
-//      (value, logical position) -> the global argmax of
-//      the squared norms, lowest logical position on exact ties (R-G5);
-//   2. warp 0 of every CTA loads the winner's column (published in its slot
-//      by the owner before the barrier) and computes the same dlarfg (R-G7)
-//      redundantly -- identical bits everywhere (same code, same data);
-//   3. each CTA applies H_j to its active columns and downdates the squared
-//      norms, r_s -= B(j,s)^2, recomputing when r_s < 1e-6 r0_s (R-G6); the
-//      column that sat at logical position j takes position s*; each warp
-//      tracks its best remaining column on the fly;
-//   4. each CTA publishes its best candidate (header + column) into the slot
-//      buffer of parity (j+1)&1, then the grid barrier.
+// transposition j <-> s* only relabels logical positions).
+//
+// Layout.  A CTA's columns are held TRANSPOSED (row-major, [row][column]) so
+// that a group of TPC threads per column (TPC = 1..32, a power of two chosen
+// by the host so that columns x TPC fills the 256 threads) reads rows
+// t = h, h+TPC, ... of consecutive columns with conflict-free shared-memory
+// accesses (row stride ncs = CPW mod 16, CPW = 32/TPC columns per warp).
+// Columns that do not fit in shared memory live transposed in a global
+// scratch (`spill`, L2-resident, coalesced across the column group).  Per-
+// column state (squared norm, panel-start norm, logical position, active
+// flag) lives in shared memory.
+//
+// Per step j (all sums in a fixed order: identical bits run to run):
+//   1. warp 0 polls the G candidate headers of step j (16 bytes each: value,
+//      logical position, step tag) until every tag is current -- no separate
+//      grid barrier -- reduces them to the global argmax of the squared norms
+//      (lowest logical position on exact ties, R-G5), loads the winner's
+//      published column and forms dlarfg (R-G7) in registers; every CTA does
+//      this redundantly on the same bits and gets the same reflector;
+//   2. every thread group applies H_j to its active columns (dot over its rows
+//      + butterfly over the group, then the AXPY) and downdates the squared
+//      norm r_s -= B(j,s)^2, recomputing it from the updated rows when
+//      r_s < 1e-6 r0_s (R-G6); the column at logical position j takes s*'s
+//      position;
+//   3. the CTA's best remaining column is published: warp 0 copies its l
+//      values to the CTA's slot, then lane 0 stores the header with release
+//      semantics (the readers' acquire loads of the header order the data).
 // Stops early (bb_eff < bb) when the winning squared norm is <= stop_tol2
 // = (1e3 eps)^2 ||Omega A||_F^2 (reading R-G12).
 // CTA 0 tracks the logical -> physical map of the touched positions in
-// shared memory (positions < bb direct-mapped, others in a short list); at the
-// end it writes `perm` (consumed by S6) and the (dst, src) column moves that
-// apply the same transpositions, in order, to A and Pi (S3).
-// Other outputs: piv[j] (s* of step j, relative to column i), tauhat, Vhat
-// (l x bb reflectors), Rhat11 (bb x bb), bb_eff, rank, gaps (diagnostic).
+// shared memory; at the end it writes `perm` (consumed by S6) and the
+// (dst, src) column moves that apply the same transpositions, in order, to A
+// and Pi (S3).  Other outputs: piv[j] (s* of step j, relative to column i),
+// tauhat, Vhat (l x bb reflectors), Rhat11 (bb x bb), bb_eff, rank, gaps.
 #pragma once
 #include <climits>
 #include "common.cuh"
@@ -39,14 +46,14 @@ namespace rq {
 constexpr int SQ_THREADS = 256;
 constexpr int SQ_WARPS = SQ_THREADS / 32;
 constexpr int SQ_MAXL = 160;  // l = b + p <= 160 rows
-constexpr int SQ_RPL = 5;     // rows per lane
+constexpr int SQ_RPL = 5;     // rows per lane of a warp-held column (SQ_MAXL / 32)
 constexpr int SQ_MAXB = 128;  // panel width
-constexpr int SQ_CB = 4;      // columns per warp iteration (memory-level parallelism)
+constexpr int SQ_MAXG = 256;  // CTAs (headers scanned by one warp, 8 per lane)
 
-struct SqHdr {    // one candidate slot header (16 bytes, written as one vector store)
-    double v;       // squared norm of the best active column (-1: none)
-    unsigned tag;   // launch sequence * 256 + step: never repeats within a context
-    int pos;        // logical position (INT_MAX: none)
+struct __align__(16) SqHdr {  // one candidate header (16 bytes, one vector store)
+    double v;                 // squared norm of the best active column (-1: none)
+    int pos;                  // its logical position (INT_MAX: none)
+    unsigned tag;             // launch sequence * 256 + step: never repeats within a context
 };
 
 struct SqArgs {
@@ -55,9 +62,12 @@ struct SqArgs {
     int l, lpad;
     int64_t nn;           // n' = trailing columns of this panel
     int bb;               // planned panel width
-    int nsm;              // columns per CTA cached in shared memory
+    int tpc;              // threads per column (power of two, <= 32)
+    int nsm;              // columns per CTA held in shared memory
+    int ncs;              // row stride of the shared-memory tile (>= nsm)
+    double *spill;        // global scratch for the other columns (transposed, per CTA)
     const double *stop_tol2;
-    SqHdr *slot_hdr;      // [2][G]
+    SqHdr *slot_hdr;      // [2][G] x hstride
     int *slot_col;        // [2][G] physical column of the candidate (written before the header)
     double *slot_v2;      // [2][G] second best (diagnostic, only with gaps)
     double *slot_data;    // [2][G][lpad]
@@ -74,25 +84,46 @@ struct SqArgs {
     int *rank;            // in/out: accumulated rank
     const int *status;    // non-zero -> no-op
     double *gaps;         // [bb] or nullptr
-    unsigned *bar;        // per-launch barrier counter (zeroed by the host)
     unsigned tag0;        // launch sequence * 256 (distinct per launch)
-    unsigned long long *trace;  // debug: [2 CTAs][64 steps][8 phases] clock64 stamps, or nullptr
+    int hstride;          // header stride in headers (8: one header per 128-byte line)
+    int poll_mode;        // 0: acquire polls; 1: relaxed polls + one acquire fence; 2: 1 + nanosleep backoff
+    unsigned long long *trace;  // debug: [G][64 steps][4 phases] clock64 stamps, or nullptr
 };
 
 RQ_DEV bool sq_better(double v, int pos, double bv, int bpos) { return (v > bv) || (v == bv && pos < bpos); }
 
-// dynamic shared memory: nsm cached columns + state of cpb columns
-__host__ __device__ inline size_t sq_smem_bytes(int64_t nsm, int64_t cpb, int lpad) {
-    return (size_t)nsm * lpad * sizeof(double) + (size_t)cpb * (2 * sizeof(double) + 2 * sizeof(int));
+// dynamic shared memory: l x ncs tile + state of cpb columns
+__host__ __device__ inline size_t sq_smem_bytes(int ncs, int64_t cpb, int l) {
+    return (size_t)l * ncs * sizeof(double) + (size_t)cpb * (2 * sizeof(double) + 2 * sizeof(int));
 }
 
-__global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
+RQ_DEV void st_release_hdr(SqHdr *p, double v, int pos, unsigned tag) {
+    const unsigned long long w0 = (unsigned long long)__double_as_longlong(v);
+    const unsigned long long w1 = (unsigned long long)(unsigned)pos | ((unsigned long long)tag << 32);
+    asm volatile("st.release.gpu.global.v2.u64 [%0], {%1, %2};\n" ::"l"(p), "l"(w0), "l"(w1) : "memory");
+}
+RQ_DEV void ld_relaxed_hdr(const SqHdr *p, double &v, int &pos, unsigned &tag) {
+    unsigned long long a, b;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+    v = __longlong_as_double((long long)a);
+    pos = (int)(unsigned)(b & 0xffffffffull);
+    tag = (unsigned)(b >> 32);
+}
+RQ_DEV void ld_acquire_hdr(const SqHdr *p, double &v, int &pos, unsigned &tag) {
+    unsigned long long a, b;
+    asm volatile("ld.acquire.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+    v = __longlong_as_double((long long)a);
+    pos = (int)(unsigned)(b & 0xffffffffull);
+    tag = (unsigned)(b >> 32);
+}
+
+__global__ void __launch_bounds__(SQ_THREADS, 1) sample_qrcp_kernel(SqArgs a) {
     extern __shared__ __align__(16) double sq_dyn[];
     __shared__ double xs[SQ_MAXL];
     __shared__ double wv[SQ_WARPS], wv2[SQ_WARPS];
     __shared__ int wpos[SQ_WARPS], wcol[SQ_WARPS];
-    __shared__ double s_tau, s_beta, s_hv;
-    __shared__ int s_wpos, s_wcol, s_stop, s_np, s_hpos;
+    __shared__ double s_tau, s_beta, s_alpha;
+    __shared__ int s_wpos, s_wcol, s_stop, s_np;
     __shared__ int64_t low[SQ_MAXB];  // CTA 0: phys column at positions < bb
     __shared__ int hi_pos[SQ_MAXB];   // CTA 0: touched positions >= bb ...
     __shared__ int64_t hi_phys[SQ_MAXB];  // ... and their phys columns
@@ -107,7 +138,14 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
     const int64_t c_lo = min(nn, (int64_t)g * cpb), c_hi = min(nn, c_lo + cpb);
     const int ncol = (int)(c_hi - c_lo);
     const int nsm = min(ncol, a.nsm);
+    const int nov = ncol - nsm;  // spilled columns (row stride nov in the scratch)
+    const int ncs = a.ncs;
     const bool want_v2 = a.gaps != nullptr;
+    const int TPC = a.tpc, CPW = 32 / TPC;
+    const int gh = lane / CPW;                   // row phase of this thread in its group
+    const int gslot = warp * CPW + (lane % CPW);  // column slot within a round
+    const int CPR = SQ_WARPS * CPW;              // columns per round
+    const int nrounds = (ncol + CPR - 1) / CPR;
 
     if (*a.status != 0 || *a.done) {
         if (g == 0 && tid == 0) { *a.bb_eff = 0; *a.swap_np = 0; }
@@ -115,18 +153,21 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
     }
     const double stop2 = *a.stop_tol2;
 
-    // shared layout: [nsm cached columns][r][r0][lpos][act]
-    double *cols_s = sq_dyn;
-    double *r = sq_dyn + (size_t)a.nsm * lpad;
+    double *tile = sq_dyn;  // [l][ncs]
+    double *r = sq_dyn + (size_t)l * ncs;
     double *r0 = r + cpb;
     int *lpos = reinterpret_cast<int *>(r0 + cpb);
     int *act = lpos + cpb;
-    auto colp = [&](int cl) -> const double * {
-        return (cl < nsm) ? cols_s + (size_t)cl * lpad : a.B + (c_lo + cl) * a.ldb;
+    double *spill = a.spill + c_lo * (int64_t)lpad;  // [l][nov]
+    // element (t, cl) of this CTA's columns
+    auto elem = [&](int t, int cl) -> double * {
+        return (cl < nsm) ? tile + (size_t)t * ncs + cl : spill + (size_t)t * nov + (cl - nsm);
     };
-    for (int e = tid; e < nsm * l; e += SQ_THREADS) {
+
+    // ---- load (transpose) this CTA's columns --------------------------------
+    for (int e = tid; e < ncol * l; e += SQ_THREADS) {
         const int t = e % l, cl = e / l;
-        cols_s[t + (size_t)cl * lpad] = a.B[t + (c_lo + cl) * a.ldb];
+        *elem(t, cl) = a.B[t + (c_lo + cl) * a.ldb];
     }
     for (int64_t x = c_lo + tid; x < c_hi; x += SQ_THREADS) a.perm[x] = x;
     if (g == 0) {
@@ -135,7 +176,13 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
     }
     __syncthreads();
 
-    // this warp's best active column (and second-best value)
+    // group butterfly (lanes of one column differ in the bits CPW..16)
+    auto gsum = [&](double v) {
+        for (int o = CPW; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    };
+
+    // this thread's best active column (and second-best value)
     double bv = -1.0, bv2 = -1.0;
     int bpos = INT_MAX, bcol = -1;
     auto consider = [&](double v, int pos, int col) {
@@ -146,45 +193,55 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
             bv2 = fmax(bv2, v);
         }
     };
-    // ---- initial squared norms (K3) ---------------------------------------
-    for (int cl0 = warp * SQ_CB; cl0 < ncol; cl0 += SQ_WARPS * SQ_CB) {
-        double x[SQ_CB][SQ_RPL];
-#pragma unroll
-        for (int u = 0; u < SQ_CB; ++u) {
-            const int cl = cl0 + u;
-            const double *col = (cl < ncol) ? colp(cl) : nullptr;
-#pragma unroll
-            for (int q = 0; q < SQ_RPL; ++q) {
-                const int t = lane + 32 * q;
-                x[u][q] = (col && t < l) ? col[t] : 0.0;
+
+    // ---- initial squared norms (K3) -----------------------------------------
+    for (int rd = 0; rd < nrounds; ++rd) {
+        const int cl = rd * CPR + gslot;
+        const bool have = cl < ncol;
+        double s0 = 0.0, s1 = 0.0;
+        if (have) {
+            int t = gh;
+            for (; t + TPC < l; t += 2 * TPC) {
+                const double x0 = *elem(t, cl), x1 = *elem(t + TPC, cl);
+                s0 += x0 * x0;
+                s1 += x1 * x1;
             }
+            if (t < l) { const double x0 = *elem(t, cl); s0 += x0 * x0; }
         }
-#pragma unroll
-        for (int u = 0; u < SQ_CB; ++u) {
-            double s = 0.0;
-#pragma unroll
-            for (int q = 0; q < SQ_RPL; ++q) s += x[u][q] * x[u][q];
-            s = warp_sum(s);
-            const int cl = cl0 + u;
-            if (cl < ncol) {
-                if (lane == 0) { r[cl] = s; r0[cl] = s; lpos[cl] = (int)(c_lo + cl); act[cl] = 1; }
-                consider(s, (int)(c_lo + cl), (int)(c_lo + cl));
-            }
+        const double s = gsum(s0 + s1);
+        if (have) {
+            if (gh == 0) { r[cl] = s; r0[cl] = s; lpos[cl] = (int)(c_lo + cl); act[cl] = 1; }
+            consider(s, (int)(c_lo + cl), (int)(c_lo + cl));
         }
     }
 
-    // publish this CTA's best candidate for step `step` (slot parity step & 1);
-    // the grid barrier that follows makes it visible.
+    // CTA-best of this thread's candidates -> header + column of slot (step & 1).
+    // Warp reduce, then warp 0 reduces the SQ_WARPS candidates, copies the
+    // column and releases the header.
     auto publish = [&](int step) {
         const int parity = step & 1;
-        if (lane == 0) { wv[warp] = bv; wv2[warp] = bv2; wpos[warp] = bpos; wcol[warp] = bcol; }
+        double v = bv, v2 = bv2;
+        int p = bpos, c = bcol;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const double ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
+            const int op = __shfl_xor_sync(0xffffffffu, p, o);
+            const int oc = __shfl_xor_sync(0xffffffffu, c, o);
+            if (sq_better(ov, op, v, p)) {
+                v2 = fmax(fmax(v2, ov2), (oc == c) ? ov2 : v);
+                v = ov; p = op; c = oc;
+            } else {
+                v2 = fmax(fmax(v2, ov2), (oc == c) ? v2 : ov);
+            }
+        }
+        if (lane == 0) { wv[warp] = v; wv2[warp] = v2; wpos[warp] = p; wcol[warp] = c; }
         __syncthreads();
         if (warp == 0) {
-            double v = -1.0, v2 = -1.0;
-            int p = INT_MAX, c = -1;
+            v = -1.0; v2 = -1.0; p = INT_MAX; c = -1;
             if (lane < SQ_WARPS) { v = wv[lane]; v2 = wv2[lane]; p = wpos[lane]; c = wcol[lane]; }
 #pragma unroll
-            for (int o = 4; o > 0; o >>= 1) {  // 8 warps
+            for (int o = SQ_WARPS / 2; o > 0; o >>= 1) {
                 const double ov = __shfl_xor_sync(0xffffffffu, v, o);
                 const double ov2 = __shfl_xor_sync(0xffffffffu, v2, o);
                 const int op = __shfl_xor_sync(0xffffffffu, p, o);
@@ -196,112 +253,112 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
                     v2 = fmax(fmax(v2, ov2), ov);
                 }
             }
-            if (lane == 0) {
-                s_hv = v; s_hpos = p; s_wcol = c;
-                if (want_v2) a.slot_v2[parity * G + g] = v2;
-                a.slot_col[parity * G + g] = c;
+            v = __shfl_sync(0xffffffffu, v, 0);  // lanes 0..7 hold the CTA best
+            v2 = __shfl_sync(0xffffffffu, v2, 0);
+            p = __shfl_sync(0xffffffffu, p, 0);
+            c = __shfl_sync(0xffffffffu, c, 0);
+            if (c >= 0) {
+                double *dst = a.slot_data + (int64_t)(parity * G + g) * lpad;
+                const int cl = c - (int)c_lo;
+                for (int t = lane; t < l; t += 32) __stcg(dst + t, *elem(t, cl));
             }
-        }
-        __syncthreads();
-        const int c0 = s_wcol;
-        if (c0 >= 0) {
-            double *dst = a.slot_data + (int64_t)(parity * G + g) * lpad;
-            const int cl = c0 - (int)c_lo;
-            const double *src = (cl < nsm) ? cols_s + (size_t)cl * lpad : a.B + (int64_t)c0 * a.ldb;
-            for (int t = tid; t < l; t += SQ_THREADS) dst[t] = src[t];
-        }
-        __syncthreads();
-        if (tid == 0) {
-            SqHdr h;
-            h.v = s_hv;
-            h.tag = a.tag0 + (unsigned)step;
-            h.pos = s_hpos;
-            st_cg_v2(reinterpret_cast<double2 *>(a.slot_hdr + parity * G + g), *reinterpret_cast<double2 *>(&h));
+            if (lane == 0) {
+                a.slot_col[parity * G + g] = c;
+                if (want_v2) a.slot_v2[parity * G + g] = v2;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                st_release_hdr(a.slot_hdr + (int64_t)(parity * G + g) * a.hstride, v, p, a.tag0 + (unsigned)step);
+            }
         }
     };
 
     publish(0);
-    unsigned epoch = 0;
-    grid_barrier(a.bar, G, epoch);
 
     int j = 0;
-    const int tsel = (g == 0) ? 0 : (g == (int)gridDim.x - 1 ? 1 : -1);
     auto stamp = [&](int ph) {
-        if (a.trace && tsel >= 0 && tid == 0 && j < 64) a.trace[((size_t)tsel * 64 + j) * 8 + ph] = clock64();
+        if (a.trace && tid == 0 && j < 64) a.trace[((size_t)g * 64 + j) * 4 + ph] = clock64();
     };
     for (; j < a.bb; ++j) {
         const int par = j & 1;
         stamp(0);
-        // ---- 1+2. global winner and its Householder reflector ----------------
-        // warps 0..ceil(G/32)-1 each reduce 32 headers (one 16-byte load per
-        // lane) and speculatively prefetch their local winner's column; the
-        // warp holding the global winner then forms dlarfg (R-G7) from its
-        // registers -- identical bits in every CTA (same data, same code).
-        const int nsw = (G + 31) >> 5;  // scanning warps (<= 5)
-        double xv[SQ_RPL];
-        if (warp < nsw) {
-            double v = -1.0, v2 = -1.0;
+        // ---- 1. global winner and its Householder reflector (warp 0) ----------
+        if (warp == 0) {
+            const unsigned want = a.tag0 + (unsigned)j;
+            constexpr int HPL = SQ_MAXG / 32;  // headers per lane
+            double v = -1.0;
             int p = INT_MAX, sl = -1;
-            const int q = lane + 32 * warp;
-            if (q < G) {
-                const double2 raw = __ldcg(reinterpret_cast<const double2 *>(a.slot_hdr + par * G + q));
-                const int qp = __double2hiint(raw.y);
-                if (qp != INT_MAX) { v = raw.x; p = qp; sl = q; }
-                if (want_v2) v2 = __ldcg(a.slot_v2 + par * G + q);
+            bool ready[HPL];
+            double hv[HPL];
+            int hp[HPL];
+#pragma unroll
+            for (int u = 0; u < HPL; ++u) { ready[u] = (lane + 32 * u >= G); hv[u] = -1.0; hp[u] = INT_MAX; }
+            // poll until every header of step j is visible (acquire loads)
+            const int pm = a.poll_mode;
+            while (true) {
+                bool all = true;
+#pragma unroll
+                for (int u = 0; u < HPL; ++u) {
+                    if (!ready[u]) {
+                        unsigned tg;
+                        const SqHdr *hp_ = a.slot_hdr + (int64_t)(par * G + lane + 32 * u) * a.hstride;
+                        if (pm == 0) ld_acquire_hdr(hp_, hv[u], hp[u], tg);
+                        else ld_relaxed_hdr(hp_, hv[u], hp[u], tg);
+                        ready[u] = (tg == want);
+                    }
+                    all = all && ready[u];
+                }
+                if (__all_sync(0xffffffffu, all)) break;
+                if (pm == 2) __nanosleep(64);
+            }
+            if (pm != 0) asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+#pragma unroll
+            for (int u = 0; u < HPL; ++u) {
+                const int q = lane + 32 * u;
+                if (q < G && hp[u] != INT_MAX && sq_better(hv[u], hp[u], v, p)) {
+                    v = hv[u]; p = hp[u]; sl = q;
+                }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 const double ov = __shfl_xor_sync(0xffffffffu, v, o);
                 const int op = __shfl_xor_sync(0xffffffffu, p, o);
                 const int osl = __shfl_xor_sync(0xffffffffu, sl, o);
-                const double ov2 = want_v2 ? __shfl_xor_sync(0xffffffffu, v2, o) : -1.0;
-                if (sq_better(ov, op, v, p)) {
-                    v2 = fmax(fmax(v2, ov2), v);
-                    v = ov; p = op; sl = osl;
-                } else {
-                    v2 = fmax(fmax(v2, ov2), ov);
-                }
+                if (osl >= 0 && (sl < 0 || sq_better(ov, op, v, p))) { v = ov; p = op; sl = osl; }
             }
+            const bool stop = (sl < 0) || !(v > stop2);
+            double xv[SQ_RPL];
             const double *src = a.slot_data + (int64_t)(par * G + (sl >= 0 ? sl : 0)) * lpad;
 #pragma unroll
             for (int qq = 0; qq < SQ_RPL; ++qq) {
                 const int t = lane + 32 * qq;
-                xv[qq] = (sl >= 0 && t < l) ? __ldcg(src + t) : 0.0;
+                xv[qq] = (!stop && t < l) ? __ldcg(src + t) : 0.0;
             }
-            if (lane == 0) { wv[warp] = v; wv2[warp] = v2; wpos[warp] = p; wcol[warp] = sl; }
-        }
-        __syncthreads();
-        int ww = 0;  // warp holding the global winner (same choice in every thread)
-        {
-            double v = wv[0];
-            int p = wpos[0];
-            for (int w2 = 1; w2 < nsw; ++w2)
-                if (wcol[w2] >= 0 && (wcol[ww] < 0 || sq_better(wv[w2], wpos[w2], v, p))) {
-                    ww = w2; v = wv[w2]; p = wpos[w2];
-                }
-        }
-        if (warp == ww) {
-            const int sl = wcol[ww];
-            const double vbest = wv[ww];
-            double v2 = -1.0;
-            for (int w2 = 0; w2 < nsw; ++w2) v2 = fmax(v2, (w2 == ww) ? wv2[w2] : wv[w2]);
-            const bool stop = (sl < 0) || !(vbest > stop2);
+            const int wc = (sl >= 0) ? __ldcg(a.slot_col + par * G + sl) : -1;
             if (lane == 0) {
                 s_stop = stop;
-                s_wpos = wpos[ww];
-                s_wcol = (sl >= 0) ? __ldcg(a.slot_col + par * G + sl) : -1;
-                if (g == 0 && want_v2 && !stop) a.gaps[j] = (v2 < 0.0 || vbest == 0.0) ? 1.0 : (vbest - v2) / vbest;
+                s_wpos = p;
+                s_wcol = wc;
+                if (g == 0 && want_v2 && !stop) {
+                    double v2 = -1.0;
+                    for (int q = 0; q < G; ++q) {
+                        const double hv = __ldcg(&a.slot_hdr[(int64_t)(par * G + q) * a.hstride].v);
+                        v2 = fmax(v2, (q == sl) ? __ldcg(a.slot_v2 + par * G + q) : hv);
+                    }
+                    a.gaps[j] = (v2 < 0.0 || v == 0.0) ? 1.0 : (v - v2) / v;
+                }
             }
             if (!stop) {
-                double sx = 0.0, mine = 0.0;
+                double sx = 0.0;
 #pragma unroll
                 for (int qq = 0; qq < SQ_RPL; ++qq) {
                     const int t = lane + 32 * qq;
                     if (t > j) sx += xv[qq] * xv[qq];
-                    if (qq == (j >> 5)) mine = xv[qq];
+                    if (t == j) s_alpha = xv[qq];
                 }
                 sx = warp_sum(sx);
-                const double alpha = __shfl_sync(0xffffffffu, mine, j & 31);
+                __syncwarp();
+                const double alpha = s_alpha;
                 double tau = 0.0, beta = alpha, scal = 0.0;
                 if (sx != 0.0) {
                     const double nrm = sqrt(alpha * alpha + sx);
@@ -321,13 +378,9 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
         stamp(1);
         if (s_stop) break;
         const int wp = s_wpos, wcl = s_wcol;
-        if (tid == 0 && wcl >= c_lo && wcl < c_hi) act[wcl - c_lo] = 0;  // retire the pivot
-        __syncthreads();
-        stamp(2);
         const double tau = s_tau;
-        // ---- outputs + position map (CTA 0) ----------------------------------
-        // step-j outputs written by CTA (j+1) mod G (spreads the extra work:
-        // every CTA waits for the slowest at the barrier)
+        // ---- outputs + position map ------------------------------------------
+        // step-j outputs written by CTA (j+1) mod G (spreads the extra work)
         if (g == (j + 1) % G) {
             for (int t = tid; t < lpad; t += SQ_THREADS)
                 a.vhat[t + (int64_t)j * lpad] = (t < j) ? 0.0 : (t == j ? 1.0 : (t < l ? xs[t] : 0.0));
@@ -335,119 +388,91 @@ __global__ void __launch_bounds__(SQ_THREADS) sample_qrcp_kernel(SqArgs a) {
                 a.rhat11[t + (int64_t)j * a.bbpad] = (t < j) ? xs[t] : (t == j ? s_beta : 0.0);
             if (tid == 0) { a.piv[j] = wp; a.tauhat[j] = tau; }
         }
-        if (g == 0) {
-            if (warp == SQ_WARPS - 1) {
-                // transposition j <-> wp; q = phys column at position j (< bb)
-                const int64_t q = low[j];
-                __syncwarp();
-                if (lane == 0) low[j] = wcl;
-                if (wp != j) {
-                    if (wp < a.bb) {
-                        if (lane == 0) low[wp] = q;
-                    } else {
-                        // find wp in the short list (warp-parallel), else append
-                        int found = -1;
-                        for (int e0 = 0; e0 < hi_n; e0 += 32) {
-                            const int e = e0 + lane;
-                            const unsigned m = __ballot_sync(0xffffffffu, e < hi_n && hi_pos[e] == wp);
-                            if (m) { found = e0 + __ffs(m) - 1; break; }
-                        }
-                        if (lane == 0) {
-                            if (found >= 0) hi_phys[found] = q;
-                            else { hi_pos[hi_n] = wp; hi_phys[hi_n] = q; ++hi_n; }
-                        }
+        if (g == 0 && warp == SQ_WARPS - 1) {
+            // transposition j <-> wp; q = phys column at position j (< bb)
+            const int64_t q = low[j];
+            __syncwarp();
+            if (lane == 0) low[j] = wcl;
+            if (wp != j) {
+                if (wp < a.bb) {
+                    if (lane == 0) low[wp] = q;
+                } else {
+                    int found = -1;
+                    for (int e0 = 0; e0 < hi_n; e0 += 32) {
+                        const int e = e0 + lane;
+                        const unsigned m = __ballot_sync(0xffffffffu, e < hi_n && hi_pos[e] == wp);
+                        if (m) { found = e0 + __ffs(m) - 1; break; }
+                    }
+                    if (lane == 0) {
+                        if (found >= 0) hi_phys[found] = q;
+                        else { hi_pos[hi_n] = wp; hi_phys[hi_n] = q; ++hi_n; }
                     }
                 }
-                __syncwarp();
+            }
+            __syncwarp();
+        }
+        // ---- 2. apply H_j to own active columns, downdate norms -------------
+        bv = -1.0; bv2 = -1.0; bpos = INT_MAX; bcol = -1;
+        const int t0 = j + ((gh - j) % TPC + TPC) % TPC;  // first row >= j of this phase
+        for (int rd = 0; rd < nrounds; ++rd) {
+            const int cl = rd * CPR + gslot;
+            const int64_t pc = c_lo + cl;
+            bool live = cl < ncol;
+            if (live && pc == wcl) { live = false; if (gh == 0) act[cl] = 0; }  // retire the pivot
+            live = live && act[cl < ncol ? cl : 0];
+            // dot over this thread's rows (two chains), then the group butterfly
+            double d0 = 0.0, d1 = 0.0;
+            double *base = nullptr;
+            int rs = 0;
+            if (live) {
+                if (cl < nsm) { base = tile + cl; rs = ncs; }
+                else { base = spill + (cl - nsm); rs = nov; }
+                int t = t0;
+                for (; t + TPC < l; t += 2 * TPC) {
+                    d0 += xs[t] * base[(size_t)t * rs];
+                    d1 += xs[t + TPC] * base[(size_t)(t + TPC) * rs];
+                }
+                if (t < l) d0 += xs[t] * base[(size_t)t * rs];
+            }
+            const double w = gsum(d0 + d1);
+            double bj = 0.0, tail = 0.0;
+            if (live) {
+                const double tw = tau * w;
+                for (int t = t0; t < l; t += TPC) {
+                    const double x = base[(size_t)t * rs] - tw * xs[t];
+                    base[(size_t)t * rs] = x;
+                    if (t == j) bj = x;
+                    else tail += x * x;
+                }
+            }
+            bj = gsum(bj);  // exactly one thread of the group holds row j
+            const double rr = live ? r[cl] : 0.0, rr0 = live ? r0[cl] : 0.0;
+            double rn = rr - bj * bj;
+            const bool need = live && (rn < 1e-6 * rr0);
+            if (__any_sync(0xffffffffu, need)) {
+                const double ts = gsum(tail);
+                if (need) rn = ts;
+            }
+            const int lp = live ? lpos[cl] : 0;
+            __syncwarp();  // the group's reads of r/lpos precede the writes below
+            if (live) {
+                const int pos = (lp == j) ? wp : lp;  // position j moves to s*
+                if (gh == 0) { r[cl] = rn; lpos[cl] = pos; }
+                consider(rn, pos, (int)pc);
             }
         }
-        // ---- 3. apply H_j to own active columns, downdate norms -----------
-        bv = -1.0; bv2 = -1.0; bpos = INT_MAX; bcol = -1;
-        auto apply_batch = [&](int cl0, int cend, auto colbase, int64_t ldcol) {
-            double x[SQ_CB][SQ_RPL];
-            bool live[SQ_CB];
-            double rr[SQ_CB], rr0[SQ_CB];
-            int lp[SQ_CB];
-            // all loads of the batch first (column rows + per-column state)
-#pragma unroll
-            for (int u = 0; u < SQ_CB; ++u) {
-                const int cl = cl0 + u;
-                const int cs = (cl < cend) ? cl : cl0;
-                live[u] = (cl < cend) && act[cs];
-                rr[u] = r[cs];
-                rr0[u] = r0[cs];
-                lp[u] = lpos[cs];
-                const double *col = colbase + (int64_t)cs * ldcol;
-#pragma unroll
-                for (int q = 0; q < SQ_RPL; ++q) {
-                    const int t = lane + 32 * q;
-                    x[u][q] = (live[u] && t < l) ? col[t] : 0.0;
-                }
-            }
-            double w[SQ_CB];
-#pragma unroll
-            for (int u = 0; u < SQ_CB; ++u) {
-                double sacc = 0.0;
-#pragma unroll
-                for (int q = 0; q < SQ_RPL; ++q) {
-                    const int t = lane + 32 * q;
-                    if (t >= j && t < l) sacc += xs[t] * x[u][q];
-                }
-                w[u] = sacc;
-            }
-#pragma unroll
-            for (int u = 0; u < SQ_CB; ++u) w[u] = warp_sum(w[u]);
-            double bj[SQ_CB], tail[SQ_CB];
-#pragma unroll
-            for (int u = 0; u < SQ_CB; ++u) {
-                const double tw = tau * w[u];
-                bj[u] = 0.0;
-                tail[u] = 0.0;
-#pragma unroll
-                for (int q = 0; q < SQ_RPL; ++q) {
-                    const int t = lane + 32 * q;
-                    if (t >= j && t < l) x[u][q] -= tw * xs[t];
-                    if (t == j) bj[u] = x[u][q];
-                    if (t > j && t < l) tail[u] += x[u][q] * x[u][q];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < SQ_CB; ++u) bj[u] = __shfl_sync(0xffffffffu, bj[u], j & 31);
-            // stores + norm downdates (recompute on cancellation, R-G6)
-#pragma unroll
-            for (int u = 0; u < SQ_CB; ++u) {
-                if (!live[u]) continue;
-                const int cl = cl0 + u;
-                double *col = colbase + (int64_t)cl * ldcol;
-#pragma unroll
-                for (int q = 0; q < SQ_RPL; ++q) {
-                    const int t = lane + 32 * q;
-                    if (t >= j && t < l) col[t] = x[u][q];
-                }
-                double rn = rr[u] - bj[u] * bj[u];
-                if (rn < 1e-6 * rr0[u]) rn = warp_sum(tail[u]);  // uniform per column
-                const int pos = (lp[u] == j) ? wp : lp[u];         // position j moves to s*
-                if (lane == 0) { r[cl] = rn; lpos[cl] = pos; }
-                consider(rn, pos, (int)(c_lo + cl));
-            }
-        };
-        // shared-memory columns (LDS/STS), then the L2-resident rest
-        for (int cl0 = warp * SQ_CB; cl0 < nsm; cl0 += SQ_WARPS * SQ_CB) apply_batch(cl0, nsm, cols_s, (int64_t)lpad);
-        for (int cl0 = nsm + warp * SQ_CB; cl0 < ncol; cl0 += SQ_WARPS * SQ_CB)
-            apply_batch(cl0, ncol, a.B + c_lo * a.ldb, a.ldb);
+        stamp(2);
+        // ---- 3. candidates for step j+1 -------------------------------------
+        if (j + 1 < a.bb) publish(j + 1);
         stamp(3);
-        // ---- 4. candidates for step j+1, then the step barrier -------------
-        publish(j + 1);
-        stamp(4);
-        grid_barrier(a.bar, G, epoch);
-        stamp(5);
     }
 
-    // ---- results ------------------------------------------------------------
-    // transformed cached columns back to global (S6 reads R-hat12/22)
-    for (int e = tid; e < nsm * l; e += SQ_THREADS) {
+    // ---- results --------------------------------------------------------------
+    __syncthreads();
+    // transformed columns back to global, column-major (S6 reads R-hat12/22)
+    for (int e = tid; e < ncol * l; e += SQ_THREADS) {
         const int t = e % l, cl = e / l;
-        a.B[t + (c_lo + cl) * a.ldb] = cols_s[t + (size_t)cl * lpad];
+        a.B[t + (c_lo + cl) * a.ldb] = *elem(t, cl);
     }
     if (g == 0) {
         if (tid == 0) s_np = 0;

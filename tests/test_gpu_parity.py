@@ -213,37 +213,26 @@ def test_factor_host_equals_device(ctx):
     assert np.array_equal(jp.numpy(), g["jpvt"])
 
 
-# ---- the thread-block-cluster (DSMEM) sample-QRCP / panel kernels (opt-in) ----
-@pytest.fixture(scope="module")
-def ctx_grid():
-    """Context with the cluster kernels enabled (RQRCP_CLUSTER=1 at create)."""
+# ---- launch-shape variants of the sample QRCP (threads per column, spill) ----
+# RQRCP_SQ_GRID caps the cooperative grid (fewer CTAs -> more columns per CTA,
+# fewer threads per column) and RQRCP_SQ_NSM caps the columns a CTA keeps in
+# shared memory (the rest go through the transposed L2 spill buffer).
+SQ_VARIANTS = [("148", None), ("2", "0"), ("7", "5"), ("33", None), ("1", "40")]
+SQ_CASES = [c for c in CASES if c[0] in ("ragged", "odd", "b128", "b1p0", "lowrank")]
+
+
+@pytest.mark.parametrize("grid,nsm", SQ_VARIANTS, ids=[f"g{g}-nsm{n}" for g, n in SQ_VARIANTS])
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", SQ_CASES, ids=[c[0] for c in SQ_CASES])
+def test_sample_qrcp_launch_variants(ctx, grid, nsm, name, kind, m, n, k, b, p, seed):
     import os
-
-    import paper_1804_05138_b200 as rq
-    os.environ["RQRCP_CLUSTER"] = "1"
-    try:
-        c = rq.RQRCP(max_m=4200, max_n=4200, max_b=128, max_p=32)
-    finally:
-        del os.environ["RQRCP_CLUSTER"]
-    yield c
-    c.close()
-
-
-GRID_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "odd", "b128", "b1p0")]
-
-
-@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", GRID_CASES, ids=[c[0] for c in GRID_CASES])
-def test_factor_parity_cluster_kernels(ctx_grid, name, kind, m, n, k, b, p, seed):
     A = inputs.make(kind, m, n, seed, rank=64).numpy()
     o = oracle.rqrcp(A, k, b, p, seed=seed)
-    g = gpu_factor(ctx_grid, A, k, b, p, seed)
+    os.environ["RQRCP_SQ_GRID"] = grid
+    if nsm is not None:
+        os.environ["RQRCP_SQ_NSM"] = nsm
+    try:
+        g = gpu_factor(ctx, A, k, b, p, seed)
+    finally:
+        os.environ.pop("RQRCP_SQ_GRID", None)
+        os.environ.pop("RQRCP_SQ_NSM", None)
     compare(A, g, o, k)
-
-
-def test_cluster_and_grid_agree(ctx, ctx_grid):
-    """Both kernel families compute the same bits (same arithmetic order)."""
-    A = inputs.iid(21, 1200, 1000).numpy()
-    g1 = gpu_factor(ctx, A, 192, 64, 10, 4)
-    g2 = gpu_factor(ctx_grid, A, 192, 64, 10, 4)
-    assert np.array_equal(g1["jpvt"], g2["jpvt"])
-    assert np.max(np.abs(g1["A"] - g2["A"])) <= 1e-12 * np.max(np.abs(g1["A"]))
