@@ -59,8 +59,7 @@ struct rqrcp_ctx {
     unsigned launch_seq = 0;  // tags of the sample-QRCP candidate headers
     double *slot_v2 = nullptr, *slot_data = nullptr;
     double *sq_spill = nullptr;  // transposed sample columns beyond shared memory (lpad_max x max_n)
-    double *pn_part = nullptr, *pn_rowj = nullptr, *pn_spill = nullptr;
-    unsigned *pn_flags = nullptr;
+    double *pn_part = nullptr, *pn_rowj = nullptr;
     double *swap_stage = nullptr;
     int64_t *swap_dst = nullptr, *swap_src = nullptr, *swap_jstage = nullptr;
     int *swap_np = nullptr;
@@ -370,7 +369,7 @@ static int free_all(rqrcp_ctx *ctx) {
     void *ptrs[] = {ctx->omt,     ctx->bs[0],   ctx->bs[1],     ctx->vfull,     ctx->vt,        ctx->w,
                     ctx->w2,      ctx->tneg, ctx->ybuf,   ctx->rhat11,    ctx->omhat,     ctx->vhat,      ctx->tauhat,
                     ctx->splitk,  ctx->slot_hdr, ctx->slot_col, ctx->slot_v2,
-                    ctx->slot_data, ctx->sq_spill, ctx->pn_part, ctx->pn_rowj, ctx->pn_spill, ctx->pn_flags,   ctx->swap_stage,
+                    ctx->slot_data, ctx->sq_spill, ctx->pn_part, ctx->pn_rowj,   ctx->swap_stage,
                     ctx->swap_dst, ctx->swap_src, ctx->swap_jstage, ctx->swap_np, ctx->perm,     ctx->piv,       ctx->sumsq_part,
                     ctx->iscal,   ctx->stop_tol2, ctx->bars,  ctx->trace, ctx->ptrace,    ctx->a_dev,     ctx->jpvt_dev,  ctx->tau_dev};
     for (void *p : ptrs)
@@ -450,9 +449,6 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(dalloc(&ctx->sq_spill, lp * nn));
     CKC(dalloc(&ctx->pn_part, 2 * G * bp));
     CKC(dalloc(&ctx->pn_rowj, 2 * bp));
-    CKC(dalloc(&ctx->pn_spill, mm * bp));
-    CKC(cudaMalloc((void **)&ctx->pn_flags, sizeof(unsigned) * 2 * PN_MAXG * 32));
-    CKC(cudaMemset(ctx->pn_flags, 0, sizeof(unsigned) * 2 * PN_MAXG * 32));
     CKC(dalloc(&ctx->swap_stage, 2 * bp * mm));
     CKC(cudaMalloc((void **)&ctx->swap_dst, sizeof(int64_t) * 2 * bp));
     CKC(cudaMalloc((void **)&ctx->swap_src, sizeof(int64_t) * 2 * bp));
@@ -493,8 +489,8 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     if (want_trace) {
         CKC(cudaMalloc((void **)&ctx->trace, sizeof(unsigned long long) * SQ_MAXG * 64 * 4));
         CKC(cudaMemset(ctx->trace, 0, sizeof(unsigned long long) * SQ_MAXG * 64 * 4));
-        CKC(cudaMalloc((void **)&ctx->ptrace, sizeof(unsigned long long) * PN_MAXG * 64 * 4));
-        CKC(cudaMemset(ctx->ptrace, 0, sizeof(unsigned long long) * PN_MAXG * 64 * 4));
+        CKC(cudaMalloc((void **)&ctx->ptrace, sizeof(unsigned long long) * 2 * 64 * 8));
+        CKC(cudaMemset(ctx->ptrace, 0, sizeof(unsigned long long) * 2 * 64 * 8));
     }
 #undef CKC
     *out = ctx;
@@ -877,30 +873,20 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.ybuf = ctx->ybuf;
             a.part = ctx->pn_part;
             a.rowj = ctx->pn_rowj;
-            a.flags = ctx->pn_flags;
-            a.tag0 = (++ctx->launch_seq) << 8;
-            a.spill = ctx->pn_spill;
-            a.poll_mode = 1;
-            if (const char *e = getenv("RQRCP_PN_POLL")) a.poll_mode = std::max(0, std::min(1, atoi(e)));
+            a.bar = ctx->bars + 2 * (panels - 1) + 1;
             a.trace = (panels == 1) ? ctx->ptrace : nullptr;
-            int pcap = std::min(G, PN_MAXG);
-            if (const char *e = getenv("RQRCP_PN_GRID")) pcap = std::max(1, std::min(pcap, atoi(e)));
-            int64_t rows_target = 64;
-            if (const char *e = getenv("RQRCP_PN_ROWS")) rows_target = std::max(1, atoi(e));
+            int pcap = G;
+            if (const char *e = getenv("RQRCP_PN_GRID")) pcap = std::max(1, std::min(G, atoi(e)));
             const int grid = (int)std::max<int64_t>((mp + PN_MAXROWS - 1) / PN_MAXROWS,
-                                                    std::min<int64_t>(pcap, (mp + rows_target - 1) / rows_target));
+                                                    std::min<int64_t>(pcap, (mp + 31) / 32));
             const int64_t rpb = (mp + grid - 1) / grid;
-            if (rpb > PN_MAXROWS || grid > pcap) {
+            if (rpb > PN_MAXROWS) {
                 ctx->err = "panel too tall for the cooperative grid";
                 return RQRCP_E_WORKSPACE;
             }
-            // row-major tile with an odd row stride (conflict-free column and
-            // row walks); as many rows in shared memory as fit, the rest in the
-            // row-major scratch
-            a.ldt = bb | 1;
-            a.nsm = (int)std::min<int64_t>(rpb, kDynSmemMax / ((int64_t)a.ldt * sizeof(double)));
-            if (const char *e = getenv("RQRCP_PN_NSM")) a.nsm = std::max(0, std::min(a.nsm, atoi(e)));
-            const size_t smem = std::max<size_t>(8, (size_t)a.nsm * a.ldt * sizeof(double));
+            // as many of each CTA's rows in shared memory as fit, the rest via L2
+            a.nsm = (int)std::min<int64_t>(rpb, kDynSmemMax / ((int64_t)bb * sizeof(double)));
+            const size_t smem = (size_t)a.nsm * bb * sizeof(double);
             void *args[] = {&a};
             rc = coop_launch(ctx, (const void *)panel_qr_kernel, grid, PN_THREADS, args, smem);
             if (rc) return rc;
@@ -1029,33 +1015,20 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             for (int q = 0; q < 4; ++q) fprintf(stderr, " %s=%.0f", names[q], all[q] / ncta);
             fprintf(stderr, "; slowest apply+publish: CTA %d (%.0f cycles)\n", worst, worst_apply);
         }
-        cudaMemcpy(H.data(), ctx->ptrace, sizeof(unsigned long long) * (size_t)PN_MAXG * 64 * 4, cudaMemcpyDeviceToHost);
-        const char *pn[4] = {"poll", "reduce+coeffs", "pass", "publish"};
-        double pall[4] = {0};
-        int pcta = 0;
-        for (int c = 0; c < PN_MAXG; ++c) {
-            double acc[4] = {0};
+        unsigned long long h[2 * 64 * 8];
+        cudaMemcpy(h, ctx->ptrace, sizeof(h), cudaMemcpyDeviceToHost);
+        const char *pn[5] = {"gram", "barrier", "reduce", "tau+w+x", "update"};
+        for (int c = 0; c < 2; ++c) {
+            double acc[5] = {0};
             int cnt = 0;
             for (int jj = 1; jj < 63; ++jj) {
-                const unsigned long long *r = H.data() + ((size_t)c * 64 + jj) * 4;
-                const unsigned long long *nx = H.data() + ((size_t)c * 64 + jj + 1) * 4;
-                if (!r[0] || !r[3] || !nx[0]) continue;
-                for (int q = 0; q < 3; ++q) acc[q] += (double)(r[q + 1] - r[q]);
-                acc[3] += (double)(nx[0] - r[3]);
+                const unsigned long long *r = h + ((size_t)c * 64 + jj) * 8;
+                if (!r[0] || !r[5]) continue;
+                for (int q = 0; q < 5; ++q) acc[q] += (double)(r[q + 1] - r[q]);
                 ++cnt;
             }
-            if (!cnt) continue;
-            for (int q = 0; q < 4; ++q) pall[q] += acc[q] / cnt;
-            if (c == 0) {
-                fprintf(stderr, "[rqrcp trace] panel CTA 0, %d steps, mean cycles:", cnt);
-                for (int q = 0; q < 4; ++q) fprintf(stderr, " %s=%.0f", pn[q], acc[q] / cnt);
-                fprintf(stderr, "\n");
-            }
-            ++pcta;
-        }
-        if (pcta) {
-            fprintf(stderr, "[rqrcp trace] panel mean over %d CTAs:", pcta);
-            for (int q = 0; q < 4; ++q) fprintf(stderr, " %s=%.0f", pn[q], pall[q] / pcta);
+            fprintf(stderr, "[rqrcp trace] panel CTA %s, %d steps, mean cycles:", c ? "last" : "0", cnt);
+            for (int q = 0; q < 5; ++q) fprintf(stderr, " %s=%.0f", pn[q], cnt ? acc[q] / cnt : 0.0);
             fprintf(stderr, "\n");
         }
     }
