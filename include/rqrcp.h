@@ -81,6 +81,10 @@ typedef struct rqrcp_timings {
     double comm_ms;         /* NCCL collectives (nranks > 1) */
     int64_t panels;
     int64_t kernel_launches;/* kernels this library launched in the call */
+    int64_t panels_householder; /* panels factored column by column (the
+                                   CholeskyQR2 path declined: ill-conditioned
+                                   or rank-stopped panel, or RQRCP_PANEL=hh);
+                                   on this rank's owned panels */
 } rqrcp_timings;
 
 /* Create a context: allocates every workspace buffer for the maxima in cfg

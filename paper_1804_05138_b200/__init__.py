@@ -42,7 +42,8 @@ class RqrcpTimings(ctypes.Structure):
     _fields_ = [("total_ms", ctypes.c_double), ("omega_ms", ctypes.c_double), ("sketch_ms", ctypes.c_double),
                 ("sample_qrcp_ms", ctypes.c_double), ("swap_ms", ctypes.c_double), ("panel_ms", ctypes.c_double),
                 ("trailing_ms", ctypes.c_double), ("sample_update_ms", ctypes.c_double),
-                ("comm_ms", ctypes.c_double), ("panels", ctypes.c_int64), ("kernel_launches", ctypes.c_int64)]
+                ("comm_ms", ctypes.c_double), ("panels", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
+                ("panels_householder", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

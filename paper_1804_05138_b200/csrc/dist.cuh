@@ -51,23 +51,33 @@ __global__ void dist_reorder_kernel(const double *gath, int64_t cmax, int rows, 
 }
 
 // panel broadcast pack: [tau (bbpad) | ybuf (bbpad^2) | R11 (bbpad^2, ld bbpad)]
+// pack = [tau (bbpad) | Y = strict_upper(V^T V) (bbpad^2) | R11 (bbpad^2) |
+//         -T (bbpad^2, valid when the CholeskyQR2 path ran) | status (1)]
 __global__ void dist_pack_kernel(const double *tau, const double *ybuf, const double *A /* &A[i + lj lda] */,
-                                 int64_t lda, int bb, int bbpad, double *pk) {
+                                 int64_t lda, int bb, int bbpad, const double *tneg, const int *status, double *pk) {
     const int n2 = bbpad * bbpad;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bbpad + 2 * n2; e += gridDim.x * blockDim.x) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bbpad + 3 * n2 + 1; e += gridDim.x * blockDim.x) {
         if (e < bbpad) pk[e] = (e < bb) ? tau[e] : 0.0;
         else if (e < bbpad + n2) pk[e] = ybuf[e - bbpad];
-        else {
+        else if (e < bbpad + 2 * n2) {
             const int q = e - bbpad - n2, r = q % bbpad, c = q / bbpad;
             pk[e] = (r < bb && c < bb) ? A[r + (int64_t)c * lda] : 0.0;
+        } else if (e < bbpad + 3 * n2) {
+            pk[e] = tneg[e - bbpad - 2 * n2];
+        } else {
+            pk[e] = (double)*status;
         }
     }
 }
-__global__ void dist_unpack_kernel(const double *pk, int bb, int bbpad, double *tau, double *ybuf) {
+__global__ void dist_unpack_kernel(const double *pk, int bb, int bbpad, double *tau, double *ybuf, double *tneg,
+                                   int *status) {
     const int n2 = bbpad * bbpad;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bbpad + n2; e += gridDim.x * blockDim.x) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bbpad + 3 * n2 + 1; e += gridDim.x * blockDim.x) {
         if (e < bbpad) { if (e < bb) tau[e] = pk[e]; }
-        else ybuf[e - bbpad] = pk[e];
+        else if (e < bbpad + n2) ybuf[e - bbpad] = pk[e];
+        else if (e < bbpad + 2 * n2) continue;
+        else if (e < bbpad + 3 * n2) tneg[e - bbpad - 2 * n2] = pk[e];
+        else *status = (int)pk[e];
     }
 }
 // Vt (bbpad x mp) from Vfull (mp x bbpad, ld ldv)

@@ -37,7 +37,8 @@ struct PanelArgs {
     int64_t mp;         // m' rows
     int bb;             // planned panel width (columns present)
     int bbpad;
-    int use_smem;       // (cluster kernel) unused by the grid kernel
+    const int *skip;    // non-null and *skip == 0: the CholeskyQR2 path (cqr.cuh) already factored the panel
+    int *count;         // incremented (CTA 0) when this kernel factors the panel
     int nsm;            // rows per CTA cached in dynamic shared memory (grid kernel)
     const int *bb_eff;
     double *tau;        // tau + i
@@ -57,6 +58,7 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
     __shared__ double wred[PN_WARPS][PN_MAXB];
     __shared__ double xs[PN_MAXROWS];
     __shared__ double s_scal, s_tau, s_beta;
+    if (a.skip && *a.skip == 0) return;
     const int G = gridDim.x, g = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int bb = a.bb;
@@ -239,6 +241,7 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
         }
     if (g == 0)
         for (int c = bbe + tid; c < bb; c += PN_THREADS) a.tau[c] = 0.0;
+    if (g == 0 && tid == 0 && a.count) atomicAdd(a.count, 1);
 }
 
 }  // namespace rq

@@ -21,7 +21,9 @@
 #include "panel.cuh"
 #include "philox.cuh"
 #include "sample_qrcp.cuh"
+#include "sample_qrcp_cl.cuh"
 #include "tri.cuh"
+#include "cqr.cuh"
 #include "dist.cuh"
 
 using namespace rq;
@@ -60,6 +62,10 @@ struct rqrcp_ctx {
     double *slot_v2 = nullptr, *slot_data = nullptr;
     double *sq_spill = nullptr;  // transposed sample columns beyond shared memory (lpad_max x max_n)
     double *pn_part = nullptr, *pn_rowj = nullptr;
+    // CholeskyQR2 + reconstruction panel (cqr.cuh): Gram, R factors, inverses
+    double *cq_g = nullptr, *cq_rc = nullptr, *cq_rinv = nullptr, *cq_uinv = nullptr, *cq_lu = nullptr;
+    int *cqr_status = nullptr;  // 0: the CholeskyQR2 path factored the panel; 1: Householder fallback
+    bool cqr_enabled = true;
     double *swap_stage = nullptr;
     int64_t *swap_dst = nullptr, *swap_src = nullptr, *swap_jstage = nullptr;
     int *swap_np = nullptr;
@@ -77,6 +83,7 @@ struct rqrcp_ctx {
     double *tau_dev = nullptr;
     // cooperative limits
     int sq_max_grid = 0, pn_max_grid = 0;
+    int sqc_max = 0;  // largest cluster the register-resident sample QRCP can use (0: none)
     // multi-GPU (nranks > 1): NCCL communicator + exchange buffers
     ncclComm_t comm = nullptr;
     double *gsend = nullptr, *gbuf = nullptr, *pack = nullptr, *r11 = nullptr;
@@ -225,8 +232,9 @@ static bool make_tmap(CUtensorMap *m, const double *base, int64_t dim0, int64_t 
 }
 
 // splits minimising ceil(T*S / grid) / S (persistent-grid wave quantisation)
-static int choose_splits(int64_t tiles, int64_t K, int grid, int64_t max_elems_per_split, int64_t partial_cap) {
-    int64_t smax = std::max<int64_t>(1, K / 512);
+static int choose_splits(int64_t tiles, int64_t K, int grid, int64_t max_elems_per_split, int64_t partial_cap,
+                         int64_t kmin = 512) {
+    int64_t smax = std::max<int64_t>(1, K / kmin);
     if (max_elems_per_split > 0) smax = std::min<int64_t>(smax, std::max<int64_t>(1, partial_cap / max_elems_per_split));
     int best = 1;
     double best_t = 1e30;
@@ -269,10 +277,11 @@ static int launch_tma_cfg(rqrcp_ctx *ctx, const double *X, int64_t xdim0, int64_
 template <int MT, int NT, int WM, int WN>
 static int tma_skinny_cfg(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const double *X, int64_t xdim0,
                           int64_t xdim1, int64_t ldx, int64_t xk0, int64_t xm0, const double *Y, int64_t ydim0,
-                          int64_t ydim1, int64_t ldy, int64_t yk0, int64_t yn0, double *C, int64_t ldc, bool *done) {
+                          int64_t ydim1, int64_t ldy, int64_t yk0, int64_t yn0, double *C, int64_t ldc, bool *done,
+                          int64_t kmin) {
     constexpr int BM = 8 * MT * WM, BN = 8 * NT * WN;
     const int64_t tiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM);
-    int splits = choose_splits(tiles, K, ctx->num_sms, M * N, ctx->splitk_elems);
+    int splits = choose_splits(tiles, K, ctx->num_sms, M * N, ctx->splitk_elems, kmin);
     int64_t kps = rup((K + splits - 1) / splits, 32);
     splits = (int)((K + kps - 1) / kps);
     TmaGemmArgs g{M, N, K, xk0, xm0, yk0, yn0, C, ldc, kps, splits, M * N, 0};
@@ -288,14 +297,14 @@ static int tma_skinny_cfg(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const
 
 static int tma_skinny(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const double *X, int64_t xdim0, int64_t xdim1,
                       int64_t ldx, int64_t xk0, int64_t xm0, const double *Y, int64_t ydim0, int64_t ydim1, int64_t ldy,
-                      int64_t yk0, int64_t yn0, double *C, int64_t ldc, bool *done) {
+                      int64_t yk0, int64_t yn0, double *C, int64_t ldc, bool *done, int64_t kmin = 512) {
     *done = false;
-    if (M <= 32) return tma_skinny_cfg<4, 4, 1, 8>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done);
-    if (M <= 40) return tma_skinny_cfg<5, 4, 1, 8>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done);
-    if (M <= 64) return tma_skinny_cfg<4, 4, 2, 4>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done);
-    if (M <= 80) return tma_skinny_cfg<5, 4, 2, 4>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done);
-    if (M <= 128) return tma_skinny_cfg<4, 4, 4, 2>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done);
-    if (M <= 144) return tma_skinny_cfg<6, 4, 3, 2>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done);
+    if (M <= 32) return tma_skinny_cfg<4, 4, 1, 8>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done, kmin);
+    if (M <= 40) return tma_skinny_cfg<5, 4, 1, 8>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done, kmin);
+    if (M <= 64) return tma_skinny_cfg<4, 4, 2, 4>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done, kmin);
+    if (M <= 80) return tma_skinny_cfg<5, 4, 2, 4>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done, kmin);
+    if (M <= 128) return tma_skinny_cfg<4, 4, 4, 2>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done, kmin);
+    if (M <= 144) return tma_skinny_cfg<6, 4, 3, 2>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done, kmin);
     return 0;
 }
 
@@ -369,7 +378,7 @@ static int free_all(rqrcp_ctx *ctx) {
     void *ptrs[] = {ctx->omt,     ctx->bs[0],   ctx->bs[1],     ctx->vfull,     ctx->vt,        ctx->w,
                     ctx->w2,      ctx->tneg, ctx->ybuf,   ctx->rhat11,    ctx->omhat,     ctx->vhat,      ctx->tauhat,
                     ctx->splitk,  ctx->slot_hdr, ctx->slot_col, ctx->slot_v2,
-                    ctx->slot_data, ctx->sq_spill, ctx->pn_part, ctx->pn_rowj,   ctx->swap_stage,
+                    ctx->slot_data, ctx->sq_spill, ctx->pn_part, ctx->pn_rowj, ctx->cq_g, ctx->cq_rc, ctx->cq_rinv, ctx->cq_uinv, ctx->cq_lu, ctx->cqr_status,   ctx->swap_stage,
                     ctx->swap_dst, ctx->swap_src, ctx->swap_jstage, ctx->swap_np, ctx->perm,     ctx->piv,       ctx->sumsq_part,
                     ctx->iscal,   ctx->stop_tol2, ctx->bars,  ctx->trace, ctx->ptrace,    ctx->a_dev,     ctx->jpvt_dev,  ctx->tau_dev};
     for (void *p : ptrs)
@@ -449,6 +458,16 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(dalloc(&ctx->sq_spill, lp * nn));
     CKC(dalloc(&ctx->pn_part, 2 * G * bp));
     CKC(dalloc(&ctx->pn_rowj, 2 * bp));
+    for (double **q : {&ctx->cq_g, &ctx->cq_rc, &ctx->cq_rinv, &ctx->cq_uinv, &ctx->cq_lu}) CKC(dalloc(q, bp * bp));
+    CKC(cudaMalloc((void **)&ctx->cqr_status, sizeof(int)));
+    CKC(cudaMemset(ctx->cqr_status, 0xff, sizeof(int)));
+    CKC(cudaFuncSetAttribute(cqr_chol_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (128 * 128 + 64 * 64) * 8));
+    CKC(cudaFuncSetAttribute(cqr_chol_kernel<CQR_EPT_U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (128 * 128 + 64 * 64) * 8));
+    CKC(cudaFuncSetAttribute(cqr_recon_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (128 * 128 + 64 * 64) * 8));
+    CKC(cudaFuncSetAttribute(cqr_recon_kernel<CQR_EPT_F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (128 * 128 + 64 * 64) * 8));
+    CKC(cudaFuncSetAttribute(cqr_rowmul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 132 * 8));
     CKC(dalloc(&ctx->swap_stage, 2 * bp * mm));
     CKC(cudaMalloc((void **)&ctx->swap_dst, sizeof(int64_t) * 2 * bp));
     CKC(cudaMalloc((void **)&ctx->swap_src, sizeof(int64_t) * 2 * bp));
@@ -465,6 +484,32 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(cudaMemset(ctx->tneg, 0, sizeof(double) * bp * bp));
     CKC(cudaFuncSetAttribute(sample_qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
     CKC(cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
+    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel<40>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel<40>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 40 * 8));
+    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel<74>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel<74>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 74 * 8));
+    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel<80>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel<80>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 80 * 8));
+    {
+        ctx->sqc_max = 0;
+        for (int cs = SQC_MAXG; cs >= 1 && !ctx->sqc_max; --cs) {
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3(cs);
+            lc.blockDim = dim3(SQC_THREADS);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cs;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            int ncl = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, (void *)sample_qrcp_cluster_kernel<80>, &lc) == cudaSuccess &&
+                ncl >= 1)
+                ctx->sqc_max = cs;
+        }
+        cudaGetLastError();
+    }
     CKC(cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (128 * 128 + 64 * 64) * 8));
     CKC(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
@@ -475,7 +520,7 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
         CKC(dalloc(&ctx->gsend, lp * (nn + bp)));
         ctx->gbuf_elems = lp * (nn + (int64_t)P * bp);
         CKC(dalloc(&ctx->gbuf, ctx->gbuf_elems));
-        CKC(dalloc(&ctx->pack, bp + 2 * bp * bp));
+        CKC(dalloc(&ctx->pack, bp + 3 * bp * bp + 1));
         CKC(cudaMalloc((void **)&ctx->dl_cols, sizeof(int64_t) * 4 * bp));
         CKC(cudaMalloc((void **)&ctx->dl_slots, sizeof(int) * 4 * bp));
         CKC(cudaMallocHost((void **)&ctx->h_pairs, sizeof(int64_t) * (4 * bp + 2 + 8 * bp)));
@@ -668,10 +713,10 @@ static int dist_panel_bcast(rqrcp_ctx *ctx, int owner, const double *panel, int6
                             int bbpad, double *tau_i) {
     cudaStream_t st = ctx->stream;
     const int me = ctx->rank;
-    const int npk = bbpad + 2 * bbpad * bbpad;
+    const int npk = bbpad + 3 * bbpad * bbpad + 1;
     if (me == owner) {
         dist_pack_kernel<<<grid_for(npk, 256, ctx->num_sms), 256, 0, st>>>(tau_i, ctx->ybuf, panel, lda, bb, bbpad,
-                                                                           ctx->pack);
+                                                                           ctx->tneg, ctx->cqr_status, ctx->pack);
         CKL();
     }
     ph_begin(ctx, PH_COMM);
@@ -681,11 +726,75 @@ static int dist_panel_bcast(rqrcp_ctx *ctx, int owner, const double *panel, int6
     CKN(nccl().GroupEnd());
     ph_end(ctx);
     if (me != owner) {
-        dist_unpack_kernel<<<grid_for(bbpad + bbpad * bbpad, 256, ctx->num_sms), 256, 0, st>>>(ctx->pack, bb, bbpad,
-                                                                                              tau_i, ctx->ybuf);
+        dist_unpack_kernel<<<grid_for(npk, 256, ctx->num_sms), 256, 0, st>>>(ctx->pack, bb, bbpad, tau_i, ctx->ybuf,
+                                                                             ctx->tneg, ctx->cqr_status);
         CKL();
         dist_transpose_kernel<<<grid_for(mp * bbpad, 256, ctx->num_sms), 256, 0, st>>>(ctx->vfull, ctx->ldo, mp, bbpad,
                                                                                       ctx->vt);
+        CKL();
+    }
+    return 0;
+}
+
+// S4 via CholeskyQR2 + Householder reconstruction (cqr.cuh).  Enqueues the
+// whole sequence; every kernel is a no-op once *cqr_status = 1.
+static int panel_cqr(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n_loc, int64_t i, int64_t ljp,
+                     int64_t mp, int bb, int bbpad, const int *bb_eff, double *tau_i) {
+    cudaStream_t st = ctx->stream;
+    if (!ctx->cqr_enabled) {
+        CK(cudaMemsetAsync(ctx->cqr_status, 0x01, sizeof(int), st));  // != 0: fallback
+        return 0;
+    }
+    int nb = 8;
+    while (nb < bbpad) nb *= 2;
+    const size_t csm = ((size_t)nb * nb + (size_t)(nb / 2) * (nb / 2)) * sizeof(double);
+    const size_t rsm = (size_t)bbpad * (bbpad + 4) * sizeof(double);
+    double *P = A + i + ljp * lda;
+    const int rows_per_cta = RM_ROWS * (CQR_THREADS / 32);
+    const int rgrid = (int)std::max<int64_t>(1, (mp + rows_per_cta - 1) / rows_per_cta);
+    bool done = false;
+    int rc = 0;
+    // G1 = P^T P (the panel: columns ljp.. of the local A, rows i..m)
+    rc = tma_skinny(ctx, bb, bb, mp, A, m, n_loc, lda, i, ljp, A, m, n_loc, lda, i, ljp, ctx->cq_g, bbpad, &done, 128);
+    if (rc) return rc;
+    if (!done) rc = gemm_skinny(ctx, bb, bb, mp, P, lda, P, lda, ctx->cq_g, bbpad);
+    if (rc) return rc;
+    if (bb <= 64) cqr_chol_kernel<9><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 1, bb_eff, ctx->cqr_status,
+                                                               ctx->cq_rc, ctx->cq_rinv);
+    else cqr_chol_kernel<CQR_EPT_U><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 1, bb_eff, ctx->cqr_status,
+                                                                ctx->cq_rc, ctx->cq_rinv);
+    CKL();
+    // Q1 = P R1^{-1} -> Vfull
+    cqr_rowmul_kernel<<<rgrid, CQR_THREADS, rsm, st>>>(P, lda, 0, mp, bb, bbpad, ctx->cq_rinv, 1.0, ctx->vfull, ctx->ldo,
+                                                       ctx->cqr_status, 0, nullptr, 0, nullptr);
+    CKL();
+    // G2 = Q1^T Q1, R2, Rc = R2 R1; Q = Q1 R2^{-1} (in place)
+    rc = tma_skinny(ctx, bb, bb, mp, ctx->vfull, mp, bbpad, ctx->ldo, 0, 0, ctx->vfull, mp, bbpad, ctx->ldo, 0, 0,
+                    ctx->cq_g, bbpad, &done, 128);
+    if (rc) return rc;
+    if (!done) rc = gemm_skinny(ctx, bb, bb, mp, ctx->vfull, ctx->ldo, ctx->vfull, ctx->ldo, ctx->cq_g, bbpad);
+    if (rc) return rc;
+    if (bb <= 64) cqr_chol_kernel<9><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 2, bb_eff, ctx->cqr_status,
+                                                               ctx->cq_rc, ctx->cq_rinv);
+    else cqr_chol_kernel<CQR_EPT_U><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 2, bb_eff, ctx->cqr_status,
+                                                                ctx->cq_rc, ctx->cq_rinv);
+    CKL();
+    cqr_rowmul_kernel<<<rgrid, CQR_THREADS, rsm, st>>>(ctx->vfull, ctx->ldo, 0, mp, bb, bbpad, ctx->cq_rinv, 1.0,
+                                                       ctx->vfull, ctx->ldo, ctx->cqr_status, 0, nullptr, 0, nullptr);
+    CKL();
+    // reconstruction: top block (L, R, T, tau), then V2 = -Q2 U^{-1} with the outputs
+    if (bb <= 64)
+        cqr_recon_kernel<16><<<1, CQR_THREADS, csm, st>>>(ctx->vfull, ctx->ldo, bb, bbpad, nb, ctx->cq_rc,
+                                                          ctx->cqr_status, P, lda, tau_i, ctx->tneg, ctx->cq_uinv, ctx->vt);
+    else
+        cqr_recon_kernel<CQR_EPT_F><<<1, CQR_THREADS, csm, st>>>(ctx->vfull, ctx->ldo, bb, bbpad, nb, ctx->cq_rc,
+                                                                 ctx->cqr_status, P, lda, tau_i, ctx->tneg,
+                                                                 ctx->cq_uinv, ctx->vt);
+    CKL();
+    if (mp > bb) {
+        const int vgrid = (int)std::max<int64_t>(1, (mp - bb + rows_per_cta - 1) / rows_per_cta);
+        cqr_rowmul_kernel<<<vgrid, CQR_THREADS, rsm, st>>>(ctx->vfull, ctx->ldo, bb, mp, bb, bbpad, ctx->cq_uinv, -1.0,
+                                                           ctx->vfull, ctx->ldo, ctx->cqr_status, 1, P, lda, ctx->vt);
         CKL();
     }
     return 0;
@@ -710,6 +819,10 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         return RQRCP_E_WORKSPACE;
     }
     CK(cudaSetDevice(ctx->device));
+    {
+        const char *e = getenv("RQRCP_PANEL");
+        ctx->cqr_enabled = !(e && (e[0] == 'h' || e[0] == 'H'));  // RQRCP_PANEL=hh: column-by-column Householder only
+    }
     const int P = ctx->nranks, me = ctx->rank;
     const int64_t n_loc = dist_count(n, b, P, me);  // this rank's columns (n when P = 1)
     ctx->launches = 0;
@@ -806,6 +919,36 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.swap_np = ctx->swap_np;
             a.trace = (panels == 1) ? ctx->trace : nullptr;
             a.spill = ctx->sq_spill;
+            bool sq_done = false;
+            {
+                // one column per thread in registers, one cluster (sample_qrcp_cl.cuh)
+                const char *e = getenv("RQRCP_SQ_CLUSTER");
+                const bool allow = !(e && e[0] == '0');
+                const int64_t need = (np + SQC_THREADS - 1) / SQC_THREADS;
+                void (*kfn)(SqArgs) = nullptr;
+                if (l == 40) kfn = sample_qrcp_cluster_kernel<40>;
+                else if (l == 74) kfn = sample_qrcp_cluster_kernel<74>;
+                else if (l == 80) kfn = sample_qrcp_cluster_kernel<80>;
+                if (allow && kfn && need <= ctx->sqc_max && !a.gaps) {
+                    const int cs = (int)std::max<int64_t>(1, need);
+                    cudaLaunchConfig_t lc = {};
+                    lc.gridDim = dim3(cs);
+                    lc.blockDim = dim3(SQC_THREADS);
+                    lc.dynamicSmemBytes = (size_t)bb * l * sizeof(double);
+                    lc.stream = st;
+                    cudaLaunchAttribute at[1];
+                    at[0].id = cudaLaunchAttributeClusterDimension;
+                    at[0].val.clusterDim.x = cs;
+                    at[0].val.clusterDim.y = 1;
+                    at[0].val.clusterDim.z = 1;
+                    lc.attrs = at;
+                    lc.numAttrs = 1;
+                    CK(cudaLaunchKernelEx(&lc, kfn, a));
+                    CKL();
+                    sq_done = true;
+                }
+            }
+            if (!sq_done) {
             a.hstride = 8;
             a.poll_mode = 1;
             if (const char *e = getenv("RQRCP_SQ_HSTRIDE")) a.hstride = std::max(1, std::min(8, atoi(e)));
@@ -836,6 +979,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             void *args[] = {&a};
             rc = coop_launch(ctx, (const void *)sample_qrcp_kernel, grid, SQ_THREADS, args, smem);
             if (rc) return rc;
+            }
         }
         ph_end(ctx);
         // ---- S3: swaps on A and Pi -----------------------------------------
@@ -859,7 +1003,13 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         const int owner = dist_owner(i, b, P);
         const int64_t ljp = dist_local(i, b, P);  // owner's local column of the panel
         if (me == owner) {
+            // CholeskyQR2 + Householder reconstruction (cqr.cuh); on failure
+            // (*cqr_status = 1) the column-by-column kernel below factors it
+            rc = panel_cqr(ctx, A, lda, m, n_loc, i, ljp, mp, bb, bbpad, bb_eff, tau + i);
+            if (rc) return rc;
             PanelArgs a{};
+            a.skip = ctx->cqr_status;
+            a.count = ctx->iscal + 4;
             a.A = A + i + ljp * lda;
             a.lda = lda;
             a.mp = mp;
@@ -908,7 +1058,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
             const int do_om = (i + bb < k && npp > 0) ? 1 : 0;
             tri_kernel<<<2, TRI_THREADS, smem, ctx->side>>>(ctx->ybuf, tau + i, ctx->rhat11, R11p, ldr11, bb, bbpad,
-                                                          nb, bb_eff, ctx->tneg, ctx->omhat, do_om);
+                                                          nb, bb_eff, ctx->tneg, ctx->omhat, do_om, ctx->cqr_status);
             CKL();
             CK(cudaEventRecord(ctx->ev_join, ctx->side));
         }
@@ -956,8 +1106,8 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         }
     }
     // ---- status ----------------------------------------------------------
-    int hs[4];
-    CK(cudaMemcpyAsync(hs, ctx->iscal, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
+    int hs[5];
+    CK(cudaMemcpyAsync(hs, ctx->iscal, sizeof(int) * 5, cudaMemcpyDeviceToHost, st));
     const int ev_t1 = ctx->nev;
     if (ctx->timing) cudaEventRecord(ctx->ev[ctx->nev++], st);
     CK(cudaStreamSynchronize(st));
@@ -985,7 +1135,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     if (ctx->trace) {
         std::vector<unsigned long long> H((size_t)SQ_MAXG * 64 * 4);
         cudaMemcpy(H.data(), ctx->trace, sizeof(unsigned long long) * H.size(), cudaMemcpyDeviceToHost);
-        const char *names[4] = {"poll+winner+householder", "apply", "publish", "->next"};
+        const char *names[4] = {"wait/poll+winner+householder", "apply", "publish", "->next"};
         double all[4] = {0}, worst_apply = 0;
         int ncta = 0, worst = -1;
         for (int c = 0; c < SQ_MAXG; ++c) {
@@ -1033,6 +1183,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         }
     }
     t.panels = panels;
+    t.panels_householder = hs[4];
     t.kernel_launches = ctx->launches;
     ctx->last = t;
     *rank_out = hs[3];

@@ -1,0 +1,320 @@
+// sample_qrcp_cl.cuh -- S2 sample QRCP (Alg. 1, on the l x n'
+// sample, Alg. 2 line P:147) for samples that fit one thread-block cluster
+// with ONE COLUMN PER THREAD held in registers: l <= SQC_L rows and
+// n' <= 16 CTAs x 256 threads.  Same arithmetic and outputs as the grid
+// kernel in sample_qrcp.cuh (dlarfg reading R-G7, squared-norm downdates with
+// the R-G6 recompute, lowest-position ties R-G5, stop rule R-G12); the
+// per-step exchange goes through distributed shared memory and one
+// split-phase cluster barrier instead of L2:
+//   publish(j): each CTA's best remaining column (value, position, physical
+//     column, its l entries) into its own shared-memory slot (parity j & 1),
+//     then barrier.cluster.arrive.release;
+//   step j: barrier.cluster.wait.acquire; warp 0 reads the G candidate
+//     headers and the winner's column with ld.shared::cluster, forms the
+//     reflector redundantly in every CTA (same bits), then every thread
+//     applies it to its register-resident column.
+// Double-buffered slots + the barrier order every reuse (a slot of parity p
+// is rewritten two steps later, after every CTA passed the barrier between).
+#pragma once
+#include <climits>
+#include "common.cuh"
+#include "sample_qrcp.cuh"
+
+namespace rq {
+
+constexpr int SQC_L = 80;         // max rows (l = b + p); kernels are instantiated for exact l
+constexpr int SQC_THREADS = 256;  // columns per CTA
+constexpr int SQC_MAXG = 16;      // CTAs (one cluster)
+
+RQ_DEV unsigned cl_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+RQ_DEV void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
+RQ_DEV void cl_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+RQ_DEV unsigned cl_map(const void *p, unsigned rank) {
+    unsigned a = (unsigned)__cvta_generic_to_shared(p), r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+RQ_DEV double cl_ld_f64(unsigned addr) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+}
+RQ_DEV int cl_ld_s32(unsigned addr) {
+    int v;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];\n" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+
+template <int L>
+__global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqArgs a) {
+    extern __shared__ __align__(16) double comp[];  // CTA 0: [bb][L] winner columns (LAPACK format)
+    __shared__ int s_piv[SQ_MAXB];
+    __shared__ double s_tauh[SQ_MAXB];
+    __shared__ double slot_v[2];
+    __shared__ int slot_pos[2], slot_col[2];
+    __shared__ double slot_x[2][SQC_L];
+    __shared__ __align__(16) double xs[SQC_L];
+    __shared__ double xraw[SQC_L];  // the winner column (rows < j: R-hat entries)
+    __shared__ double wv[SQ_WARPS];
+    __shared__ int wpos[SQ_WARPS], wcol[SQ_WARPS];
+    __shared__ double s_tau, s_beta, s_alpha;
+    __shared__ int s_wpos, s_wcol, s_stop, s_np;
+    __shared__ int64_t low[SQ_MAXB];
+    __shared__ int hi_pos[SQ_MAXB];
+    __shared__ int64_t hi_phys[SQ_MAXB];
+    __shared__ int hi_n;
+
+    const int G = gridDim.x;
+    const int g = (int)cl_rank();
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int l = a.l;
+    const int64_t nn = a.nn;
+    const int64_t cpb = (nn + G - 1) / G;  // <= 256
+    const int64_t c_lo = min(nn, (int64_t)g * cpb), c_hi = min(nn, c_lo + cpb);
+    const bool have = tid < (int)(c_hi - c_lo);
+    const int64_t pc = c_lo + tid;  // this thread's physical column
+    // every CTA takes part in every barrier, so an early exit is uniform
+    const bool noop = (*a.status != 0 || *a.done);
+    if (noop) {
+        if (g == 0 && tid == 0) { *a.bb_eff = 0; *a.swap_np = 0; }
+        return;
+    }
+    const double stop2 = *a.stop_tol2;
+
+    double x[L];
+#pragma unroll
+    for (int t = 0; t < L; ++t) x[t] = have ? a.B[t + pc * a.ldb] : 0.0;
+    double r = 0.0;
+#pragma unroll
+    for (int t = 0; t < L; ++t) r += x[t] * x[t];
+    double r0 = r;
+    int lpos = (int)pc;
+    bool act = have;
+    if (have) a.perm[pc] = pc;
+    if (g == 0) {
+        for (int q = tid; q < a.bb; q += SQC_THREADS) low[q] = q;
+        if (tid == 0) hi_n = 0;
+    }
+
+    // CTA-best candidate -> this CTA's slot of parity (step & 1); then arrive
+    auto publish = [&](int step) {
+        const int par = step & 1;
+        double v = act ? r : -1.0;
+        int p = act ? lpos : INT_MAX, c = act ? (int)pc : -1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int op = __shfl_xor_sync(0xffffffffu, p, o);
+            const int oc = __shfl_xor_sync(0xffffffffu, c, o);
+            if (sq_better(ov, op, v, p)) { v = ov; p = op; c = oc; }
+        }
+        if (lane == 0) { wv[warp] = v; wpos[warp] = p; wcol[warp] = c; }
+        __syncthreads();
+        // every thread reduces the SQ_WARPS candidates (same order: same result)
+        double bv = wv[0];
+        int bp = wpos[0], bc = wcol[0];
+        for (int w = 1; w < SQ_WARPS; ++w)
+            if (sq_better(wv[w], wpos[w], bv, bp)) { bv = wv[w]; bp = wpos[w]; bc = wcol[w]; }
+        if (act && (int)pc == bc) {
+#pragma unroll
+            for (int t = 0; t < L; ++t) slot_x[par][t] = x[t];
+        }
+        if (tid == 0) {
+            slot_v[par] = bv;
+            slot_pos[par] = bp;
+            slot_col[par] = bc;
+        }
+        cl_arrive();
+    };
+
+    publish(0);
+
+    int j = 0;
+    auto stamp = [&](int ph) {
+        if (a.trace && tid == 0 && j < 64) a.trace[((size_t)g * 64 + j) * 4 + ph] = clock64();
+    };
+    for (; j < a.bb; ++j) {
+        const int par = j & 1;
+        stamp(0);
+        cl_wait();
+        // ---- 1. winner and its reflector (warp 0, redundantly per CTA) --------
+        if (warp == 0) {
+            double v = -1.0;
+            int p = INT_MAX, sl = -1;
+            if (lane < G) {
+                v = cl_ld_f64(cl_map(&slot_v[par], lane));
+                p = cl_ld_s32(cl_map(&slot_pos[par], lane));
+                if (p != INT_MAX) sl = lane;
+                else v = -1.0;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                const int op = __shfl_xor_sync(0xffffffffu, p, o);
+                const int osl = __shfl_xor_sync(0xffffffffu, sl, o);
+                if (osl >= 0 && (sl < 0 || sq_better(ov, op, v, p))) { v = ov; p = op; sl = osl; }
+            }
+            const bool stop = (sl < 0) || !(v > stop2);
+            double xv[SQ_RPL];
+#pragma unroll
+            for (int qq = 0; qq < SQ_RPL; ++qq) {
+                const int t = lane + 32 * qq;
+                xv[qq] = (!stop && t < l) ? cl_ld_f64(cl_map(&slot_x[par][t], sl)) : 0.0;
+            }
+            const int wc = (sl >= 0) ? cl_ld_s32(cl_map(&slot_col[par], sl)) : -1;
+            if (lane == 0) {
+                s_stop = stop;
+                s_wpos = p;
+                s_wcol = wc;
+            }
+            if (!stop) {
+                double sx = 0.0;
+#pragma unroll
+                for (int qq = 0; qq < SQ_RPL; ++qq) {
+                    const int t = lane + 32 * qq;
+                    if (t > j) sx += xv[qq] * xv[qq];
+                    if (t == j) s_alpha = xv[qq];
+                }
+                sx = warp_sum(sx);
+                __syncwarp();
+                const double alpha = s_alpha;
+                double tau = 0.0, beta = alpha, scal = 0.0;
+                if (sx != 0.0) {
+                    const double nrm = sqrt(alpha * alpha + sx);
+                    beta = (alpha >= 0.0) ? -nrm : nrm;
+                    tau = (beta - alpha) / beta;
+                    scal = 1.0 / (alpha - beta);
+                }
+                // reflector rows >= j; rows < j zeroed so the apply needs no predicates
+#pragma unroll
+                for (int qq = 0; qq < SQ_RPL; ++qq) {
+                    const int t = lane + 32 * qq;
+                    if (t < L) xs[t] = (t > j) ? xv[qq] * scal : (t == j ? 1.0 : 0.0);
+                    if (t < L) xraw[t] = xv[qq];
+                }
+                if (lane == 0) { s_tau = tau; s_beta = beta; }
+            }
+        }
+        __syncthreads();
+        stamp(1);
+        if (s_stop) break;
+        const int wp = s_wpos, wcl = s_wcol;
+        const double tau = s_tau;
+        // ---- outputs (staged in CTA 0's shared memory, written at the end) -----
+        if (g == 0) {
+            // column j in LAPACK format: R-hat above the diagonal, beta, v below
+            for (int t = tid; t < L; t += SQC_THREADS) comp[j * L + t] = (t < j) ? xraw[t] : (t == j ? s_beta : xs[t]);
+            if (tid == 0) { s_piv[j] = wp; s_tauh[j] = tau; }
+        }
+        if (g == 0 && warp == SQ_WARPS - 1) {
+            const int64_t q = low[j];
+            __syncwarp();
+            if (lane == 0) low[j] = wcl;
+            if (wp != j) {
+                if (wp < a.bb) {
+                    if (lane == 0) low[wp] = q;
+                } else {
+                    int found = -1;
+                    for (int e0 = 0; e0 < hi_n; e0 += 32) {
+                        const int e = e0 + lane;
+                        const unsigned m = __ballot_sync(0xffffffffu, e < hi_n && hi_pos[e] == wp);
+                        if (m) { found = e0 + __ffs(m) - 1; break; }
+                    }
+                    if (lane == 0) {
+                        if (found >= 0) hi_phys[found] = q;
+                        else { hi_pos[hi_n] = wp; hi_phys[hi_n] = q; ++hi_n; }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        // ---- 2. apply H_j to this thread's column, downdate the norm ---------
+        if (act && (int)pc == wcl) act = false;  // retire the pivot
+        if (act) {
+            // w = v^T x over rows >= j (xs is zero above row j)
+            double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+            for (int t = 0; t + 1 < L; t += 2) {
+                const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
+                d0 += v2.x * x[t];
+                d1 += v2.y * x[t + 1];
+            }
+            if (L & 1) d0 += xs[L - 1] * x[L - 1];
+            const double tw = tau * (d0 + d1);
+            double bj = 0.0;
+#pragma unroll
+            for (int t = 0; t + 1 < L; t += 2) {
+                const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
+                x[t] -= tw * v2.x;
+                x[t + 1] -= tw * v2.y;
+                if (t == j) bj = x[t];
+                if (t + 1 == j) bj = x[t + 1];
+            }
+            if (L & 1) {
+                x[L - 1] -= tw * xs[L - 1];
+                if (L - 1 == j) bj = x[L - 1];
+            }
+            double rn = r - bj * bj;
+            if (rn < 1e-6 * r0) {  // recompute from the updated rows (R-G6)
+                double s0 = 0.0;
+#pragma unroll
+                for (int t = 0; t < L; ++t)
+                    if (t > j) s0 += x[t] * x[t];
+                rn = s0;
+            }
+            r = rn;
+            if (lpos == j) lpos = wp;  // position j moves to s*
+        }
+        stamp(2);
+        if (j + 1 < a.bb) publish(j + 1);
+        stamp(3);
+    }
+    // the last reads of every CTA's slots precede this barrier
+    cl_arrive();
+    cl_wait();
+
+    // ---- results --------------------------------------------------------------
+    if (have) {
+#pragma unroll
+        for (int t = 0; t < L; ++t) a.B[t + pc * a.ldb] = x[t];
+    }
+    if (g == 0) {
+        // Vhat (lpad x bbpad: unit diagonal, v below), Rhat11 (bbpad x bbpad), piv, tauhat
+        for (int e = tid; e < j * a.lpad; e += SQC_THREADS) {
+            const int t = e % a.lpad, c = e / a.lpad;
+            a.vhat[e] = (t < c || t >= L) ? 0.0 : (t == c ? 1.0 : comp[c * L + t]);
+        }
+        for (int e = tid; e < j * a.bbpad; e += SQC_THREADS) {
+            const int t = e % a.bbpad, c = e / a.bbpad;
+            a.rhat11[e] = (t <= c) ? comp[c * L + t] : 0.0;
+        }
+        for (int c = tid; c < j; c += SQC_THREADS) { a.piv[c] = s_piv[c]; a.tauhat[c] = s_tauh[c]; }
+        if (tid == 0) s_np = 0;
+        __syncthreads();
+        const int nlow = a.bb;
+        for (int e = tid; e < nlow + hi_n; e += SQC_THREADS) {
+            int64_t xq, src;
+            if (e < nlow) { xq = e; src = low[e]; }
+            else { xq = hi_pos[e - nlow]; src = hi_phys[e - nlow]; }
+            a.perm[xq] = src;
+            if (src != xq) {
+                const int slot = atomicAdd(&s_np, 1);
+                a.swap_dst[slot] = xq;
+                a.swap_src[slot] = src;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            *a.swap_np = s_np;
+            *a.bb_eff = j;
+            *a.rank += j;
+            if (j < a.bb) *a.done = 1;
+        }
+    }
+}
+
+}  // namespace rq

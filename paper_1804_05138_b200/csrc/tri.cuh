@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(TRI_THREADS) tri_kernel(const double *ybuf /* 
                                                           const double *rhat11 /* bbpad x bbpad */,
                                                           const double *R11 /* &A[i+i lda] */, int64_t lda, int bb,
                                                           int bbpad, int nb, const int *bb_eff, double *tneg,
-                                                          double *omhat, int do_omhat) {
+                                                          double *omhat, int do_omhat, const int *t_ready) {
     extern __shared__ __align__(16) double tsm[];
     double *M = tsm;             // nb x nb
     double *tmp = tsm + nb * nb; // (nb/2) x (nb/2)
@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(TRI_THREADS) tri_kernel(const double *ybuf /* 
     const int tid = threadIdx.x;
     if (blockIdx.x == 0) {
         // ---------------- T ----------------
+        if (t_ready && *t_ready == 0) return;  // written by the CholeskyQR2 reconstruction
         for (int e = tid; e < nb * nb; e += blockDim.x) M[e] = 0.0;
         __syncthreads();
         // base: each thread owns one 8x8 diagonal block, column recurrence

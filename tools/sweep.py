@@ -39,7 +39,8 @@ def main():
             if best is None or t["total_ms"] < best["total_ms"]:
                 best = t
         keys = ["total_ms", "sketch_ms", "sample_qrcp_ms", "swap_ms", "panel_ms", "trailing_ms", "sample_update_ms"]
-        print(label, " ".join(f"{kk[:-3]}={best[kk]:.3f}" for kk in keys), flush=True)
+        print(label, " ".join(f"{kk[:-3]}={best[kk]:.3f}" for kk in keys),
+              f"hh_panels={best['panels_householder']}/{best['panels']}", flush=True)
 
     run("default")
     for s in [x for x in args.sq.split(",") if x]:
