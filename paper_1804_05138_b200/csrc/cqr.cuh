@@ -35,6 +35,11 @@
 namespace rq {
 
 constexpr int CQR_THREADS = 256;
+// debug: phase stamps (clock64) of cqr_chol_kernel / cqr_recon_kernel, set by tools only
+__device__ unsigned long long *g_cqr_dbg = nullptr;
+RQ_DEV void cqr_stamp(int ph) {
+    if (g_cqr_dbg && threadIdx.x == 0) g_cqr_dbg[ph] = clock64();
+}
 constexpr double CQR_MAX_DIAG_RATIO = 1e5;
 constexpr double CQR_MAX_ORTH_ERR = 1e-4;
 constexpr int CQR_MAXB = 128;
@@ -46,7 +51,8 @@ constexpr int CQR_EPT_F = (CQR_MAXB * CQR_MAXB + CQR_THREADS - 1) / CQR_THREADS;
 // (nb = 8 * 2^k, ld nb; identity padding beyond the live size) by
 // block-recursive doubling: invert the 8x8 diagonal blocks, then
 // B <- -A^{-1} B D^{-1} for the off-diagonal block of every 2s x 2s block.
-// tmp: (nb/2)^2 doubles.  All threads of the CTA must call it.
+// tmp: nb^2/4 doubles (nb/(2s) blocks of s^2 per level).  All threads of the
+// CTA must call it.
 // ---------------------------------------------------------------------------
 RQ_DEV void tri_inv_upper_smem(double *M, int nb, double *tmp) {
     const int ld = nb, tid = threadIdx.x;
@@ -74,27 +80,88 @@ RQ_DEV void tri_inv_upper_smem(double *M, int nb, double *tmp) {
         }
     }
     __syncthreads();
+    // levels: every thread owns up to TI_E elements (r, c, block k) of the
+    // nblk s x s off-diagonal blocks; q-outer loops keep TI_E independent
+    // accumulators in flight
+    constexpr int TI_E = 8;
     for (int s = 8; s < nb; s *= 2) {
         const int ls = __ffs(s) - 1;
-        for (int k = 0; k < nb; k += 2 * s) {
-            // tmp = A^{-1} B (A^{-1} upper, already inverted)
-            for (int e = tid; e < s * s; e += blockDim.x) {
-                const int r = e & (s - 1), c = e >> ls;
-                double acc = 0.0;
-                for (int q = r; q < s; ++q) acc += M[(k + r) + (k + q) * ld] * M[(k + q) + (k + s + c) * ld];
-                tmp[r + c * h] = acc;
+        const int nblk = nb / (2 * s);
+        const int ne = nblk * s * s;  // <= nb^2 / 4 = 4096 for nb = 128 -> <= 16 per thread
+        for (int e0 = 0; e0 < ne; e0 += TI_E * CQR_THREADS) {
+            // tmp_k = A_k^{-1} B_k  (A^{-1} upper, already inverted)
+            double acc[TI_E];
+            int rr[TI_E], cc[TI_E], kk[TI_E];
+#pragma unroll
+            for (int u = 0; u < TI_E; ++u) {
+                const int e = e0 + u * CQR_THREADS + tid;
+                rr[u] = e & (s - 1);
+                cc[u] = (e >> ls) & (s - 1);
+                kk[u] = (e < ne) ? (e >> (2 * ls)) * 2 * s : -1;
+                acc[u] = 0.0;
             }
-            __syncthreads();
-            // B = -tmp D^{-1} (D^{-1} upper, already inverted)
-            for (int e = tid; e < s * s; e += blockDim.x) {
-                const int r = e & (s - 1), c = e >> ls;
-                double acc = 0.0;
-                for (int q = 0; q <= c; ++q) acc += tmp[r + q * h] * M[(k + s + q) + (k + s + c) * ld];
-                M[(k + r) + (k + s + c) * ld] = -acc;
+            for (int q = 0; q < s; ++q) {
+                double av[TI_E], bv[TI_E];
+#pragma unroll
+                for (int u = 0; u < TI_E; ++u) {
+                    const int k = kk[u] < 0 ? 0 : kk[u];
+                    av[u] = M[(k + rr[u]) + (k + q) * ld];
+                    bv[u] = M[(k + q) + (k + s + cc[u]) * ld];
+                }
+#pragma unroll
+                for (int u = 0; u < TI_E; ++u)
+                    if (q >= rr[u]) acc[u] += av[u] * bv[u];
             }
-            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < TI_E; ++u) {
+                const int e = e0 + u * CQR_THREADS + tid;
+                if (e < ne) tmp[e] = acc[u];
+            }
         }
+        __syncthreads();
+        for (int e0 = 0; e0 < ne; e0 += TI_E * CQR_THREADS) {
+            // B_k = -tmp_k D_k^{-1}  (D^{-1} upper, already inverted)
+            double acc[TI_E];
+            int rr[TI_E], cc[TI_E], kb[TI_E];
+#pragma unroll
+            for (int u = 0; u < TI_E; ++u) {
+                const int e = e0 + u * CQR_THREADS + tid;
+                rr[u] = e & (s - 1);
+                cc[u] = (e >> ls) & (s - 1);
+                kb[u] = (e < ne) ? (e >> (2 * ls)) : -1;
+                acc[u] = 0.0;
+            }
+            for (int q = 0; q < s; ++q) {
+                double tv[TI_E], dv[TI_E];
+#pragma unroll
+                for (int u = 0; u < TI_E; ++u) {
+                    const int b = kb[u] < 0 ? 0 : kb[u], k = b * 2 * s;
+                    tv[u] = tmp[b * s * s + rr[u] + (q << ls)];
+                    dv[u] = M[(k + s + q) + (k + s + cc[u]) * ld];
+                }
+#pragma unroll
+                for (int u = 0; u < TI_E; ++u)
+                    if (q <= cc[u]) acc[u] += tv[u] * dv[u];
+            }
+#pragma unroll
+            for (int u = 0; u < TI_E; ++u) {
+                const int k = kb[u] * 2 * s;
+                if (kb[u] >= 0) M[(k + rr[u]) + (k + s + cc[u]) * ld] = -acc[u];
+            }
+        }
+        __syncthreads();
     }
+}
+
+// 1/d to ~1 ulp: hardware approximation + two Newton steps (no division
+// subroutine on the critical path of the per-column steps)
+RQ_DEV double fast_rcp(double d) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    double e = fma(-d, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-d, y, 1.0);
+    return fma(y, e, y);
 }
 
 // packed upper-triangle index e -> (a, c), a <= c, e = c (c + 1) / 2 + a
@@ -125,6 +192,8 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_chol_kernel(const double *
     double *tmp = cq_sm + nb * nb;  // (nb/2)^2
     __shared__ double rowb[2][CQR_MAXB];
     __shared__ double s_d[CQR_MAXB];
+    __shared__ double s_idl[2];
+    __shared__ int s_fail;
     __shared__ double s_red[CQR_THREADS / 32];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (pass == 1) {
@@ -132,16 +201,18 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_chol_kernel(const double *
         __syncthreads();
     }
     if (*status != 0) return;
+    cqr_stamp(0);
     const int ne = bb * (bb + 1) / 2;
     double v[EPT];
-    int eac[EPT];  // a | c << 16 (a = 0xffff: no element)
+    int ea[EPT], ec[EPT];  // element (a, c), a <= c; a = -1: no element
     double mx = 0.0;
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
         const int e = tid + CQR_THREADS * i;
         int a = 0, c = 0;
         if (e < ne) upper_index(e, a, c);
-        eac[i] = (e < ne ? a : 0xffff) | (c << 16);
+        ea[i] = (e < ne) ? a : -1;
+        ec[i] = c;
         v[i] = (e < ne) ? G[a + (int64_t)c * bbpad] : 0.0;
         if (e < ne) mx = fmax(mx, fabs(v[i] - (a == c ? 1.0 : 0.0)));
         if (e < ne && a == 0) rowb[0][c] = v[i];
@@ -160,27 +231,49 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_chol_kernel(const double *
             return;
         }
     }
+    cqr_stamp(1);
+    // step j: M(a,c) -= M(j,a) M(j,c) / M(j,j) for a > j; the owners of row
+    // j+1 publish it, the owner of (j+1, j+1) also 1/M(j+1,j+1) (or a failure)
+    if (tid == 0) {
+        const double d0 = rowb[0][0];
+        s_d[0] = d0;
+        s_idl[0] = fast_rcp(d0);
+        s_fail = !(d0 > 0.0);
+    }
+    __syncthreads();
+    // (a failed pivot only poisons the remaining entries; checked after the loop)
     for (int j = 0; j < bb; ++j) {
         const double *rj = rowb[j & 1];
         double *rn = rowb[(j + 1) & 1];
-        const double d = rj[j];
-        if (!(d > 0.0)) break;  // uniform (also NaN); caught below
-        if (tid == 0) s_d[j] = d;
-        const double idl = 1.0 / d;
+        const double idl = s_idl[j & 1];
+        // all loads first (the stores below may alias them for the compiler),
+        // then the updates, then the publication of row j+1
+        double ra[EPT], rc[EPT];
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
-            const int a = eac[i] & 0xffff, c = eac[i] >> 16;
-            if (a > j && a != 0xffff) {
-                v[i] -= rj[a] * rj[c] * idl;
-                if (a == j + 1) rn[c] = v[i];
-            }
+            ra[i] = rj[ea[i] > 0 ? ea[i] : 0];
+            rc[i] = rj[ec[i]];
         }
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) v[i] -= (ea[i] > j) ? ra[i] * rc[i] * idl : 0.0;
+#pragma unroll
+        for (int i = 0; i < EPT; ++i)
+            if (ea[i] == j + 1) rn[ec[i]] = v[i];
+#pragma unroll
+        for (int i = 0; i < EPT; ++i)
+            if (ea[i] == j + 1 && ec[i] == j + 1) {  // next pivot (one thread)
+                s_d[j + 1] = v[i];
+                s_idl[(j + 1) & 1] = fast_rcp(v[i]);
+                if (!(v[i] > 0.0)) s_fail = 1;
+            }
         __syncthreads();
     }
-    // the loop broke early iff some pivot was not positive: s_d is then short
+    __syncthreads();
+    cqr_stamp(2);
+    // a failed (non-positive / NaN) pivot leaves s_fail set and s_d short
     {
         double dmax = 0.0, dmin = 1e308;
-        bool ok = true;
+        bool ok = !s_fail;
         for (int j = 0; j < bb; ++j) {
             const double dj = s_d[j];
             ok = ok && (dj > 0.0);
@@ -201,15 +294,15 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_chol_kernel(const double *
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
-        const int a = eac[i] & 0xffff, c = eac[i] >> 16;
-        if (a != 0xffff) M[a + c * nb] = (a == c) ? sqrt(s_d[a]) : v[i] / sqrt(s_d[a]);
+        const int a = ea[i], c = ec[i];
+        if (a >= 0) M[a + c * nb] = (a == c) ? sqrt(s_d[a]) : v[i] / sqrt(s_d[a]);
     }
     __syncthreads();
     // Rc = R (pass 1) or R Rc_old (pass 2; staged in Rinv)
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
-        const int a = eac[i] & 0xffff, c = eac[i] >> 16;
-        if (a == 0xffff) continue;
+        const int a = ea[i], c = ec[i];
+        if (a < 0) continue;
         double acc;
         if (pass == 1) acc = M[a + c * nb];
         else {
@@ -222,8 +315,10 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_chol_kernel(const double *
     for (int c = warp; c < bbpad; c += CQR_THREADS / 32)
         for (int r = lane; r < bbpad; r += 32)
             Rc[r + (int64_t)c * bbpad] = (r < bb && c < bb && r <= c) ? Rinv[r + (int64_t)c * bbpad] : 0.0;
+    cqr_stamp(3);
     tri_inv_upper_smem(M, nb, tmp);
     __syncthreads();
+    cqr_stamp(4);
     for (int c = warp; c < bbpad; c += CQR_THREADS / 32)
         for (int r = lane; r < bbpad; r += 32) Rinv[r + (int64_t)c * bbpad] = (r < bb && c < bb) ? M[r + c * nb] : 0.0;
 }
@@ -261,20 +356,27 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_rowmul_kernel(const double
 #pragma unroll
         for (int nt = 0; nt < 16; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
     const int NT = bbpad / 8;
-    for (int k0 = 0; k0 < bbpad; k0 += 4) {
-        const int k = k0 + fk;
-        double a[2];
+    // all A fragments of this warp's rows first (one round trip), then the MMAs
+    double af[2][CQR_MAXB / 4];
+#pragma unroll
+    for (int kk = 0; kk < CQR_MAXB / 4; ++kk) {
+        const int k = kk * 4 + fk;
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
             const int64_t r = rbase + mt * 8 + fr;
-            a[mt] = (r < rows && k < bb) ? X[r + (int64_t)k * ldx] : 0.0;
+            af[mt][kk] = (kk * 4 < bbpad && r < rows && k < bb) ? X[r + (int64_t)k * ldx] : 0.0;
         }
+    }
+#pragma unroll
+    for (int kk = 0; kk < CQR_MAXB / 4; ++kk) {
+        if (kk * 4 >= bbpad) break;
+        const int k = kk * 4 + fk;
 #pragma unroll
         for (int nt = 0; nt < 16; ++nt) {
             if (nt < NT) {
                 const double b = rm_sm[k + (nt * 8 + fr) * ldr];
 #pragma unroll
-                for (int mt = 0; mt < 2; ++mt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], b);
+                for (int mt = 0; mt < 2; ++mt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt][kk], b);
             }
         }
     }
@@ -322,6 +424,8 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_recon_kernel(double *vfull
     double *tmp = rc_sm + nb * nb; // (nb/2)^2
     __shared__ double rowb[2][CQR_MAXB], colb[2][CQR_MAXB];
     __shared__ double sgn[CQR_MAXB], s_piv[CQR_MAXB];
+    __shared__ double s_ip[2];
+    __shared__ int s_fail;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (*status != 0) return;
     const int ne = bb * bb;
@@ -337,27 +441,55 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_recon_kernel(double *vfull
         if (e < ne && c == 0) colb[0][r] = v[i];
     }
     __syncthreads();
-    bool bad = false;
+    // step j: X(r,c) -= X(r,j) X(j,c) / piv_j for r, c > j; the owners of row
+    // and column j+1 publish them, the owner of (j+1, j+1) the next pivot
+    // (with its sign S_{j+1}) and its reciprocal
+    if (tid == 0) {
+        const double a0 = rowb[0][0];
+        const double sj = (a0 < 0.0) ? -1.0 : 1.0;
+        sgn[0] = sj;
+        s_piv[0] = a0 + sj;
+        s_ip[0] = fast_rcp(a0 + sj);
+        s_fail = !isfinite(a0);
+    }
+    __syncthreads();
     for (int j = 0; j < bb; ++j) {
         const double *rj = rowb[j & 1], *cj = colb[j & 1];
         double *rn = rowb[(j + 1) & 1], *cn = colb[(j + 1) & 1];
-        const double a0 = rj[j];
-        const double sj = (a0 < 0.0) ? -1.0 : 1.0;
-        const double piv = a0 + sj;
-        if (!isfinite(piv)) { bad = true; break; }  // uniform
-        if (tid == 0) { sgn[j] = sj; s_piv[j] = piv; }
-        const double ip = 1.0 / piv;
+        const double ip = s_ip[j & 1];
+        // all loads first, then the updates, then the publication
+        double xr[EPT], xc[EPT];
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+            xr[i] = cj[(erc[i] & 0xffff) & 127];
+            xc[i] = rj[erc[i] >> 16];
+        }
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+            const int r = erc[i] & 0xffff, c = erc[i] >> 16;  // r = 0xffff: no element
+            const bool act = (r > j) && (c > j) && (r != 0xffff);
+            v[i] -= act ? xr[i] * ip * xc[i] : 0.0;
+        }
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
             const int r = erc[i] & 0xffff, c = erc[i] >> 16;
-            if (r > j && c > j && r != 0xffff) {
-                v[i] -= cj[r] * ip * rj[c];
-                if (r == j + 1) rn[c] = v[i];
-                if (c == j + 1) cn[r] = v[i];
-            }
+            const bool act = (r > j) && (c > j) && (r != 0xffff);
+            if (act && r == j + 1) rn[c] = v[i];
+            if (act && c == j + 1) cn[r] = v[i];
         }
+#pragma unroll
+        for (int i = 0; i < EPT; ++i)
+            if ((erc[i] & 0xffff) == j + 1 && (erc[i] >> 16) == j + 1) {  // next pivot (one thread)
+                const double sn = (v[i] < 0.0) ? -1.0 : 1.0;
+                sgn[j + 1] = sn;
+                s_piv[j + 1] = v[i] + sn;
+                s_ip[(j + 1) & 1] = fast_rcp(v[i] + sn);
+                if (!isfinite(v[i])) s_fail = 1;
+            }
         __syncthreads();
     }
+    const bool bad = s_fail;
+    __syncthreads();
     if (bad) {
         if (tid == 0) *status = 1;
         return;

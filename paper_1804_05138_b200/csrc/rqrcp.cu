@@ -127,7 +127,8 @@ static const char *g_static_err = "no context";
         ctx->launches++;                                                              \
     } while (0)
 
-static constexpr int kDynSmemMax = 200 * 1024;  // dynamic shared memory cap for cached kernels
+static constexpr int kDynSmemMax = 200 * 1024;
+static constexpr int64_t kCqrMinRows = 8192;  // auto panel path: CholeskyQR2 from this many rows  // dynamic shared memory cap for cached kernels
 
 static int grid_for(int64_t total, int threads, int num_sms) {
     int64_t g = (total + threads - 1) / threads;
@@ -819,10 +820,11 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         return RQRCP_E_WORKSPACE;
     }
     CK(cudaSetDevice(ctx->device));
-    {
-        const char *e = getenv("RQRCP_PANEL");
-        ctx->cqr_enabled = !(e && (e[0] == 'h' || e[0] == 'H'));  // RQRCP_PANEL=hh: column-by-column Householder only
-    }
+    // panel path: RQRCP_PANEL=hh (column-by-column Householder), =cqr
+    // (CholeskyQR2 + reconstruction wherever it is accurate), default auto:
+    // CholeskyQR2 for panels of >= kCqrMinRows rows (measured faster there)
+    int panel_mode = 2;
+    if (const char *e = getenv("RQRCP_PANEL")) panel_mode = (e[0] == 'h' || e[0] == 'H') ? 0 : 1;
     const int P = ctx->nranks, me = ctx->rank;
     const int64_t n_loc = dist_count(n, b, P, me);  // this rank's columns (n when P = 1)
     ctx->launches = 0;
@@ -1005,6 +1007,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         if (me == owner) {
             // CholeskyQR2 + Householder reconstruction (cqr.cuh); on failure
             // (*cqr_status = 1) the column-by-column kernel below factors it
+            ctx->cqr_enabled = (panel_mode == 1) || (panel_mode == 2 && mp >= kCqrMinRows);
             rc = panel_cqr(ctx, A, lda, m, n_loc, i, ljp, mp, bb, bbpad, bb_eff, tau + i);
             if (rc) return rc;
             PanelArgs a{};

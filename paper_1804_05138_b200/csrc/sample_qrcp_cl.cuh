@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
     __shared__ int slot_pos[2], slot_col[2];
     __shared__ double slot_x[2][SQC_L];
     __shared__ __align__(16) double xs[SQC_L];
+    __shared__ __align__(16) double xe[2 * SQC_L];  // (v_t, [t == j]) pairs
     __shared__ double xraw[SQC_L];  // the winner column (rows < j: R-hat entries)
     __shared__ double wv[SQ_WARPS];
     __shared__ int wpos[SQ_WARPS], wcol[SQ_WARPS];
@@ -193,8 +194,13 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
 #pragma unroll
                 for (int qq = 0; qq < SQ_RPL; ++qq) {
                     const int t = lane + 32 * qq;
-                    if (t < L) xs[t] = (t > j) ? xv[qq] * scal : (t == j ? 1.0 : 0.0);
-                    if (t < L) xraw[t] = xv[qq];
+                    if (t < L) {
+                        const double vt = (t > j) ? xv[qq] * scal : (t == j ? 1.0 : 0.0);
+                        xs[t] = vt;
+                        xe[2 * t] = vt;
+                        xe[2 * t + 1] = (t == j) ? 1.0 : 0.0;
+                        xraw[t] = xv[qq];
+                    }
                 }
                 if (lane == 0) { s_tau = tau; s_beta = beta; }
             }
@@ -235,28 +241,34 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
         // ---- 2. apply H_j to this thread's column, downdate the norm ---------
         if (act && (int)pc == wcl) act = false;  // retire the pivot
         if (act) {
-            // w = v^T x over rows >= j (xs is zero above row j)
+            // w = v^T x over rows >= j (xs is zero above row j); 8-row chunks
+            // entirely above row j are skipped (uniform branches)
             double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-            for (int t = 0; t + 1 < L; t += 2) {
-                const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
-                d0 += v2.x * x[t];
-                d1 += v2.y * x[t + 1];
+            for (int c0 = 0; c0 < L; c0 += 8) {
+                if (j < c0 + 8) {
+#pragma unroll
+                    for (int t = c0; t < c0 + 8 && t + 1 < L; t += 2) {
+                        const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
+                        d0 += v2.x * x[t];
+                        d1 += v2.y * x[t + 1];
+                    }
+                    if ((L & 1) && c0 + 8 >= L) d0 += xs[L - 1] * x[L - 1];
+                }
             }
-            if (L & 1) d0 += xs[L - 1] * x[L - 1];
             const double tw = tau * (d0 + d1);
+            // x -= tw v; bj = x(j) through the one-hot half of xe = (v_t, [t == j])
             double bj = 0.0;
 #pragma unroll
-            for (int t = 0; t + 1 < L; t += 2) {
-                const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
-                x[t] -= tw * v2.x;
-                x[t + 1] -= tw * v2.y;
-                if (t == j) bj = x[t];
-                if (t + 1 == j) bj = x[t + 1];
-            }
-            if (L & 1) {
-                x[L - 1] -= tw * xs[L - 1];
-                if (L - 1 == j) bj = x[L - 1];
+            for (int c0 = 0; c0 < L; c0 += 8) {
+                if (j < c0 + 8) {
+#pragma unroll
+                    for (int t = c0; t < c0 + 8 && t < L; ++t) {
+                        const double2 e2 = *reinterpret_cast<const double2 *>(&xe[2 * t]);
+                        x[t] -= tw * e2.x;
+                        bj += e2.y * x[t];
+                    }
+                }
             }
             double rn = r - bj * bj;
             if (rn < 1e-6 * r0) {  // recompute from the updated rows (R-G6)

@@ -62,30 +62,34 @@ int main() {
     CK(cudaEventSynchronize(e1));
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     printf("empty kernel back-to-back: %.2f us per launch\n", ms);
-    // Cholesky of a 64x64 SPD matrix
-    for (int bb : {64}) {
-        const int bbpad = bb;
+    // Cholesky of a 64x64 SPD matrix, with phase stamps
+    {
+        const int bb = 64, bbpad = 64, nb = 64;
         std::vector<double> G(bbpad * bbpad);
         for (int c = 0; c < bb; ++c)
             for (int r = 0; r < bb; ++r) G[r + c * bbpad] = (r == c ? bb : 0.0) + 1.0 / (1.0 + r + c);
-        double *dG, *dR, *dd, *dRc;
+        double *dG, *dR, *dRc;
         int *st, *be;
-        CK(cudaMalloc(&dG, 8 * bbpad * bbpad)); CK(cudaMalloc(&dR, 8 * bbpad * bbpad));
-        CK(cudaMalloc(&dd, 8 * bbpad)); CK(cudaMalloc(&dRc, 8 * bbpad * bbpad));
-        CK(cudaMalloc(&st, 4)); CK(cudaMalloc(&be, 4));
+        unsigned long long *dbg;
+        CK(cudaMalloc(&dG, 8 * bbpad * bbpad)); CK(cudaMalloc(&dR, 8 * bbpad * bbpad)); CK(cudaMalloc(&dRc, 8 * bbpad * bbpad));
+        CK(cudaMalloc(&st, 4)); CK(cudaMalloc(&be, 4)); CK(cudaMalloc(&dbg, 8 * 16));
         CK(cudaMemcpy(dG, G.data(), 8 * bbpad * bbpad, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(be, &bb, 4, cudaMemcpyHostToDevice));
-        const size_t sm = (size_t)bb * (bb | 1) * 8;
+        CK(cudaMemcpyToSymbol(g_cqr_dbg, &dbg, sizeof(dbg)));
+        const size_t sm = ((size_t)nb * nb + (nb / 2) * (nb / 2)) * 8;
         CK(cudaFuncSetAttribute(cqr_chol_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        for (int i = 0; i < 5; ++i) cqr_chol_kernel<9><<<1, CQR_THREADS, sm>>>(dG, bb, bbpad, 64, 1, be, st, dRc, dR);
-        CK(cudaDeviceSynchronize());
-        cudaEventRecord(e0);
-        for (int i = 0; i < 100; ++i) cqr_chol_kernel<9><<<1, CQR_THREADS, sm>>>(dG, bb, bbpad, 64, 1, be, st, dRc, dR);
-        cudaEventRecord(e1);
-        CK(cudaEventSynchronize(e1));
-        cudaEventElapsedTime(&ms, e0, e1);
-        int hs; CK(cudaMemcpy(&hs, st, 4, cudaMemcpyDeviceToHost));
-        printf("cqr_chol_kernel bb=%d: %.2f us per launch (status %d)\n", bb, ms * 10.0, hs);
+        for (int rep = 0; rep < 3; ++rep) {
+            cudaEventRecord(e0);
+            cqr_chol_kernel<9><<<1, CQR_THREADS, sm>>>(dG, bb, bbpad, nb, 1, be, st, dRc, dR);
+            cudaEventRecord(e1);
+            CK(cudaEventSynchronize(e1));
+            cudaEventElapsedTime(&ms, e0, e1);
+            unsigned long long h[8];
+            CK(cudaMemcpy(h, dbg, 8 * 5, cudaMemcpyDeviceToHost));
+            int hs; CK(cudaMemcpy(&hs, st, 4, cudaMemcpyDeviceToHost));
+            printf("cqr_chol<9> bb=64: %.2f us (status %d); cycles: load %llu, factor %llu, Rc %llu, inverse %llu\n", ms * 1e3, hs,
+                   h[1] - h[0], h[2] - h[1], h[3] - h[2], h[4] - h[3]);
+        }
     }
     return 0;
 }
