@@ -163,6 +163,14 @@ int rqrcp_nccl_unique_id(uint8_t *out);
 /* Per-phase timings of the last rqrcp_factor on ctx. */
 int rqrcp_get_timings(const rqrcp_ctx *ctx, rqrcp_timings *out);
 
+/* Sample updating formula for subsequent rqrcp_factor calls on ctx (Alg. 2
+ * line P:151): 1 = Eq. (4) (default: reuse the sample's triangular
+ * factor, O(nkb) flops), 2 = Eq. (5) (keep Omega-bar = Omega Q
+ * up to date and form B2 - Omega-bar_1 R12, O((b+p)(m+n)k) flops).  Both give
+ * the same pivots in exact arithmetic.  Returns 0, -1 (ctx null) or
+ * -2 (rule not 1 or 2). */
+int rqrcp_set_update_rule(rqrcp_ctx *ctx, int rule);
+
 /* Enable (1) / disable (0) per-phase CUDA-event timing (default 1). */
 int rqrcp_set_timing(rqrcp_ctx *ctx, int enabled);
 

@@ -71,6 +71,7 @@ def lib():
         L.rqrcp_flops.argtypes = [i64, i64, i64, ip, ip, ctypes.POINTER(ctypes.c_double)]
         L.rqrcp_get_timings.argtypes = [vp, ctypes.POINTER(RqrcpTimings)]
         L.rqrcp_set_timing.argtypes = [vp, ip]
+        L.rqrcp_set_update_rule.argtypes = [vp, ip]
         L.rqrcp_destroy.argtypes = [vp]
         L.rqrcp_last_error.argtypes = [vp]
         L.rqrcp_last_error.restype = ctypes.c_char_p
@@ -85,7 +86,7 @@ def lib():
 
 
 EXPORTED = ["rqrcp_create", "rqrcp_factor", "rqrcp_factor_host", "rqrcp_factor_ex", "rqrcp_fill_gaussian",
-            "rqrcp_philox_words", "rqrcp_flops", "rqrcp_get_timings", "rqrcp_set_timing", "rqrcp_destroy",
+            "rqrcp_philox_words", "rqrcp_flops", "rqrcp_get_timings", "rqrcp_set_timing", "rqrcp_set_update_rule", "rqrcp_destroy",
             "rqrcp_last_error", "rqrcp_version", "rqrcp_shard_columns", "rqrcp_shard_global_index",
             "rqrcp_nccl_unique_id"]
 
@@ -232,6 +233,12 @@ class RQRCP:
         t = RqrcpTimings()
         lib().rqrcp_get_timings(self._h, ctypes.byref(t))
         return t.as_dict()
+
+    def set_update_rule(self, rule: int):
+        """1: Eq. (4) (default), 2: Eq. (5) -- see rqrcp_set_update_rule in include/rqrcp.h."""
+        rc = lib().rqrcp_set_update_rule(self._h, int(rule))
+        if rc:
+            raise ValueError(f"update rule must be 1 or 2 (rc {rc})")
 
     def set_timing(self, enabled: bool):
         lib().rqrcp_set_timing(self._h, 1 if enabled else 0)

@@ -136,4 +136,26 @@ __global__ void __launch_bounds__(256) sample_update_kernel(const double *Bold, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// S6 by updating formula 2, Eq. (5): B_next = B2 - Omega-bar_1 R12
+// with B2 the pre-QRCP sample's columns in pivoted order (perm[bb + ...]) and
+// C = Omega-bar_1 R12 (l x n'') computed by a DMMA contraction; this kernel
+// forms B2 - C for this rank's local trailing columns (same mapping as
+// sample_update_kernel).  Rows l..lpad-1 are 0.
+// ---------------------------------------------------------------------------
+__global__ void sample_update5_kernel(const double *Bpre, int64_t ldb, const int64_t *perm, const double *Cm,
+                                      int64_t ldc, int bb, int l, int lpad, int64_t npl, const int *bb_eff,
+                                      double *Bnew, int64_t ldn, int64_t i, int64_t lj0, int b, int P, int rank) {
+    if (*bb_eff != bb) return;
+    const int64_t total = (int64_t)lpad * npl;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(e % lpad);
+        const int64_t c = e / lpad;
+        const int64_t lj = lj0 + c;
+        const int64_t j = ((lj / b) * P + rank) * b + lj % b;  // global column (dist_global)
+        const int64_t src = perm[j - i];
+        Bnew[r + c * ldn] = (r < l) ? Bpre[r + src * ldb] - Cm[r + c * ldc] : 0.0;
+    }
+}
+
 }  // namespace rq

@@ -75,6 +75,9 @@ struct rqrcp_ctx {
     int *iscal = nullptr;
     double *stop_tol2 = nullptr;
     unsigned *bars = nullptr;  // one grid-barrier counter per cooperative launch
+    // updating formula 2 (Eq. (5)): the pre-QRCP sample, Omega-bar_1 R12, W for Q^T Omega^T
+    int update_rule = 1;
+    double *bpre = nullptr, *c5 = nullptr, *wom = nullptr, *w2om = nullptr;
     int64_t nbars = 0;
     // host-path buffer (lazily allocated)
     double *a_dev = nullptr;
@@ -379,7 +382,7 @@ static int free_all(rqrcp_ctx *ctx) {
     void *ptrs[] = {ctx->omt,     ctx->bs[0],   ctx->bs[1],     ctx->vfull,     ctx->vt,        ctx->w,
                     ctx->w2,      ctx->tneg, ctx->ybuf,   ctx->rhat11,    ctx->omhat,     ctx->vhat,      ctx->tauhat,
                     ctx->splitk,  ctx->slot_hdr, ctx->slot_col, ctx->slot_v2,
-                    ctx->slot_data, ctx->sq_spill, ctx->pn_part, ctx->pn_rowj, ctx->cq_g, ctx->cq_rc, ctx->cq_rinv, ctx->cq_uinv, ctx->cq_lu, ctx->cqr_status,   ctx->swap_stage,
+                    ctx->slot_data, ctx->sq_spill, ctx->pn_part, ctx->pn_rowj, ctx->cq_g, ctx->cq_rc, ctx->cq_rinv, ctx->cq_uinv, ctx->cq_lu, ctx->cqr_status, ctx->bpre, ctx->c5, ctx->wom, ctx->w2om,   ctx->swap_stage,
                     ctx->swap_dst, ctx->swap_src, ctx->swap_jstage, ctx->swap_np, ctx->perm,     ctx->piv,       ctx->sumsq_part,
                     ctx->iscal,   ctx->stop_tol2, ctx->bars,  ctx->trace, ctx->ptrace,    ctx->a_dev,     ctx->jpvt_dev,  ctx->tau_dev};
     for (void *p : ptrs)
@@ -457,6 +460,10 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(dalloc(&ctx->slot_v2, 2 * G));
     CKC(dalloc(&ctx->slot_data, 2 * G * lp));
     CKC(dalloc(&ctx->sq_spill, lp * nn));
+    CKC(dalloc(&ctx->bpre, lp * nn));
+    CKC(dalloc(&ctx->c5, lp * nn));
+    CKC(dalloc(&ctx->wom, bp * lp));
+    CKC(dalloc(&ctx->w2om, bp * lp));
     CKC(dalloc(&ctx->pn_part, 2 * G * bp));
     CKC(dalloc(&ctx->pn_rowj, 2 * bp));
     for (double **q : {&ctx->cq_g, &ctx->cq_rc, &ctx->cq_rinv, &ctx->cq_uinv, &ctx->cq_lu}) CKC(dalloc(q, bp * bp));
@@ -579,6 +586,13 @@ extern "C" int rqrcp_nccl_unique_id(uint8_t *out) {
     ncclUniqueId id;
     if (nccl().GetUniqueId(&id) != 0) return RQRCP_E_NCCL;
     memcpy(out, id.internal, sizeof(id.internal));
+    return 0;
+}
+
+extern "C" int rqrcp_set_update_rule(rqrcp_ctx *ctx, int rule) {
+    if (!ctx) return -1;
+    if (rule != 1 && rule != 2) return -2;
+    ctx->update_rule = rule;
     return 0;
 }
 
@@ -889,6 +903,10 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         const int bbpad = (int)rup(bb, 8);
         const int64_t mp = m - i, np = n - i, npp = np - bb;
         ++panels;
+        const bool rule5 = ctx->update_rule == 2 && i + bb < k && npp > 0;
+        if (rule5)  // Eq. (5) needs B2 = the pre-QRCP sample
+            CK(cudaMemcpyAsync(ctx->bpre, ctx->bs[cur], sizeof(double) * (size_t)lpad * (size_t)np,
+                               cudaMemcpyDeviceToDevice, st));
         // ---- S2: sample QRCP ---------------------------------------------
         ph_begin(ctx, PH_SQRCP);
         {
@@ -1059,7 +1077,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             const size_t smem = ((size_t)nb * nb + (size_t)(nb / 2) * (nb / 2)) * sizeof(double);
             CK(cudaEventRecord(ctx->ev_fork, st));
             CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-            const int do_om = (i + bb < k && npp > 0) ? 1 : 0;
+            const int do_om = (i + bb < k && npp > 0 && !rule5) ? 1 : 0;
             tri_kernel<<<2, TRI_THREADS, smem, ctx->side>>>(ctx->ybuf, tau + i, ctx->rhat11, R11p, ldr11, bb, bbpad,
                                                           nb, bb_eff, ctx->tneg, ctx->omhat, do_om, ctx->cqr_status);
             CKL();
@@ -1090,11 +1108,36 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
         }
         ph_end(ctx);
-        // ---- S6: sample update (Eq. (4)); skipped after the last panel (R-G9)
+        // ---- S6: sample update (Eq. (4) or (5)); skipped after the last panel (R-G9)
         if (i + bb < k && npp > 0) {
             ph_begin(ctx, PH_SUPD);
             double *udst = (P == 1) ? ctx->bs[cur ^ 1] : ctx->gsend;
-            if (npl > 0) {
+            if (rule5) {
+                // Omega-bar^T = Q_panel^T Omega_cur^T on rows i..m of Omega^T (same
+                // three contractions as the trailing update), then
+                // C = Omega-bar_1 R12 and B_next = B2 - C
+                bool dn = false;
+                rc = tma_skinny(ctx, bbpad, lpad, mp, ctx->vfull, mp, bbpad, ctx->ldo, 0, 0, ctx->omt, m, lpad,
+                                ctx->ldo, i, 0, ctx->wom, bbpad, &dn);
+                if (rc) return rc;
+                if (!dn) rc = gemm_skinny(ctx, bbpad, lpad, mp, ctx->vfull, ctx->ldo, ctx->omt + i, ctx->ldo, ctx->wom,
+                                          bbpad);
+                if (rc) return rc;
+                rc = gemm_skinny(ctx, bbpad, lpad, bbpad, ctx->tneg, bbpad, ctx->wom, bbpad, ctx->w2om, bbpad);
+                if (rc) return rc;
+                rc = tma_update(ctx, mp, lpad, bbpad, ctx->w2om, bbpad, ctx->vt, bbpad, ctx->omt + i, ctx->ldo, &dn);
+                if (rc) return rc;
+                if (!dn) rc = gemm_update(ctx, mp, lpad, bbpad, ctx->w2om, bbpad, ctx->vt, bbpad, ctx->omt + i, ctx->ldo);
+                if (rc) return rc;
+                if (npl > 0) {
+                    rc = gemm_skinny(ctx, lpad, npl, bb, ctx->omt + i, ctx->ldo, A + i + lj0 * lda, lda, ctx->c5, lpad);
+                    if (rc) return rc;
+                    sample_update5_kernel<<<grid_for((int64_t)lpad * npl, 256, G), 256, 0, st>>>(
+                        ctx->bpre, lpad, ctx->perm, ctx->c5, lpad, bb, l, lpad, npl, bb_eff, udst, lpad, i, lj0, b, P,
+                        me);
+                    CKL();
+                }
+            } else if (npl > 0) {
                 sample_update_kernel<<<(unsigned)((npl + SU_COLS - 1) / SU_COLS), 256, 0, st>>>(
                     ctx->bs[cur], lpad, ctx->perm, ctx->omhat, bbpad, A + i + lj0 * lda, lda, bb, l, lpad, npl,
                     bb_eff, udst, lpad, i, lj0, b, P, me);

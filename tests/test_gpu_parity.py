@@ -236,3 +236,37 @@ def test_sample_qrcp_launch_variants(ctx, grid, nsm, name, kind, m, n, k, b, p, 
         os.environ.pop("RQRCP_SQ_GRID", None)
         os.environ.pop("RQRCP_SQ_NSM", None)
     compare(A, g, o, k)
+
+
+# ---- updating formula 2 (Eq. (5)) on the GPU: SURVEY.md §8(f) N2 ----
+EQ5_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "lowrank", "b128", "odd")]
+
+
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", EQ5_CASES, ids=[c[0] for c in EQ5_CASES])
+def test_eq5_update_parity(ctx, name, kind, m, n, k, b, p, seed):
+    """GPU Eq. (5) vs the oracle's Eq. (5) mode: identical pivots, |diag R| and
+    residuals within the acceptance tolerances."""
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    o = oracle.rqrcp(A, k, b, p, seed=seed, update_rule=2)
+    ctx.set_update_rule(2)
+    try:
+        g = gpu_factor(ctx, A, k, b, p, seed)
+    finally:
+        ctx.set_update_rule(1)
+    compare(A, g, o, k)
+
+
+def test_eq4_eq5_identical_permutations_gpu(ctx):
+    """the two updating formulas give the same permutation (C2 shape
+    scaled down, iid: the pivot-choice stress case)."""
+    A = inputs.iid(31, 1024, 1024).numpy()
+    g4 = gpu_factor(ctx, A, 256, 64, 10, 31)
+    ctx.set_update_rule(2)
+    try:
+        g5 = gpu_factor(ctx, A, 256, 64, 10, 31)
+    finally:
+        ctx.set_update_rule(1)
+    assert np.array_equal(g4["jpvt"], g5["jpvt"])
+    d4 = np.abs(np.diag(g4["A"])[:256])
+    d5 = np.abs(np.diag(g5["A"])[:256])
+    assert np.max(np.abs(d4 - d5) / d4) <= DIAG_RTOL
