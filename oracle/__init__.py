@@ -210,3 +210,68 @@ def min_oversampling(n: int, k: int, eps: float, delta: float) -> int:
     if not (0 < eps < 1 and 0 < delta < 1):
         raise ValueError("eps, delta must lie in (0,1)")
     return int(math.ceil(4.0 / (eps ** 2 - eps ** 3) * math.log(2.0 * n * k / delta))) - 1
+
+
+# ---------------------------------------------------------------------------
+# SRQR verification (Alg. 3, first half)
+# ---------------------------------------------------------------------------
+SRQR_STREAM = 7  # Philox stream of the d x (l+1) Gaussian of the g2 estimate
+
+
+def srqr_verify(A, k: int, b: int, p: int, seed: int = 0, d: int = 8, omega=None, update_rule: int = 1):
+    """Alg. 3's verification on top of Alg. 2 run to rank k (the paper's l):
+
+    * the sample after the LAST panel's update (reading G9: kept here) gives
+      r_i = ||B(:, i)||^2 / (b + p) for the trailing columns (P:635-637);
+    * iota = argmax r_i (lowest position on ties, reading G5); columns k and
+      k + iota of A and Pi are swapped (P:638);
+    * one QR step on A(k:m, k:n): |alpha| = ||A(k:m, k)|| (P:639-640);
+    * g1 = ||R22||_{1,2} / |alpha| (Eq. 8, P:500), R22 = A(k:m, k:n);
+    * R-hat = [[R11, a], [0, alpha]] (P:505-511) and
+      g2 ~= |alpha| / sqrt(d) ||Omega_d R-hat^{-T}||_{1,2} with Omega_d a
+      d x (k+1) N(0,1) matrix (P:642-643), formed by d triangular solves;
+      also the exact g2 = |alpha| ||R-hat^{-T}||_{1,2} (Eq. 8);
+    * the tau caps of Eqs. (10) and (12): g1 g2 sqrt((l+1)(n-l)) and
+      g1 g2 sqrt(l(n-l)), with l = k.
+    Returns a dict (the factorization after the swap under 'res')."""
+    import scipy.linalg as sla
+    state = {}
+
+    def cb(i, bb, l_, mp, np_, Rhat, Bnext, OmCur, OmNew, Af):
+        state["Bnext"] = Bnext
+
+    res = rqrcp(A, k, b, p, seed=seed, omega=omega, update_rule=update_rule, invariant=True, callback=cb)
+    F = res["A"]
+    jpvt = res["jpvt"]
+    m, n = F.shape
+    out = dict(res=res, k=k, d=d)
+    if k >= n or k >= m or state.get("Bnext") is None:
+        out.update(g1=0.0, g2_est=0.0, g2_exact=0.0, alpha=0.0, pivot=-1, tau_bound=0.0, tau_hat_bound=0.0)
+        return out
+    B = state["Bnext"]                   # l x (n - k): the sample of R22
+    r = np.zeros(B.shape[1])
+    for c in range(B.shape[1]):          # ascending sums of squares (P:635)
+        s = 0.0
+        for t in range(B.shape[0]):
+            s += B[t, c] * B[t, c]
+        r[c] = s / (b + p)               # P:637
+    iota = int(np.argmax(r))             # first (lowest) index on exact ties
+    if iota != 0:
+        F[:, [k, k + iota]] = F[:, [k + iota, k]]
+        jpvt[[k, k + iota]] = jpvt[[k + iota, k]]
+    colnorm = np.sqrt(np.sum(F[k:, k:] ** 2, axis=0))
+    alpha = float(colnorm[0])
+    g1 = float(np.max(colnorm) / alpha) if alpha > 0 else float("inf")
+    Rh = np.zeros((k + 1, k + 1))
+    Rh[:k, :k] = np.triu(F[:k, :k])
+    Rh[:k, k] = F[:k, k]
+    Rh[k, k] = alpha
+    Od = normal(seed, SRQR_STREAM, d, k + 1)
+    Y = sla.solve_triangular(Rh, Od.T, lower=False)      # R-hat^{-1} Omega_d^T = (Omega_d R-hat^{-T})^T
+    g2_est = alpha / math.sqrt(d) * float(np.max(np.sqrt(np.sum(Y * Y, axis=1))))
+    Rinv = sla.solve_triangular(Rh, np.eye(k + 1), lower=False)
+    g2_exact = alpha * float(np.max(np.sqrt(np.sum(Rinv * Rinv, axis=1))))  # max column norm of R-hat^{-T}
+    out.update(g1=g1, g2_est=g2_est, g2_exact=g2_exact, alpha=alpha, pivot=iota,
+               tau_bound=g1 * g2_est * math.sqrt((k + 1) * (n - k)),
+               tau_hat_bound=g1 * g2_est * math.sqrt(k * (n - k)))
+    return out

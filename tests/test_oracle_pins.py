@@ -472,3 +472,91 @@ def test_gaussian_omega_matches_explicit():
     a = oracle.rqrcp(A, 20, 8, 4, seed=21)
     c = oracle.rqrcp(A, 20, 8, 4, omega=oracle.omega(21, 12, 70))
     assert np.array_equal(a["A"], c["A"])
+
+
+# ----------------------------------------------------------------------------
+# SRQR verification (Alg. 3 first half)
+# ----------------------------------------------------------------------------
+def _orth_cols(seed, m, n, ratio):
+    rng = np.random.default_rng(seed)
+    U, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    d = ratio ** (-np.arange(n, dtype=np.float64))
+    rng.shuffle(d)
+    return U * d, np.sort(d)[::-1]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_srqr_qrcp_mode_g1_is_one(seed):
+    """for QRCP |alpha| is the largest trailing column norm, so g1 = 1.
+    Omega = I_m makes Alg. 2 a QRCP (SURVEY ST-2); separated norms."""
+    A, _ = graded_matrix(np.random.default_rng(seed), 60, 45, 1.7)
+    m = A.shape[0]
+    o = oracle.srqr_verify(A, 14, 7, m - 7, seed=seed, omega=np.eye(m))
+    assert o["g1"] == 1.0
+
+
+@pytest.mark.parametrize("omega_identity", [True, False])
+def test_srqr_orthogonal_columns_closed_form(omega_identity):
+    """Orthonormal columns scaled by well-separated d: R-hat = diag(d_1..d_{k+1})
+    up to signs, |alpha| = d_{k+1}, so g1 = 1 and g2 = |alpha| max 1/d_i = 1."""
+    A, ds = _orth_cols(3, 70, 50, 10.0 ** 0.5)
+    m, k, b = 70, 15, 5
+    p = m - b if omega_identity else 6
+    o = oracle.srqr_verify(A, k, b, p, seed=2, omega=np.eye(m) if omega_identity else None)
+    assert o["g1"] == pytest.approx(1.0, abs=1e-12)
+    assert o["g2_exact"] == pytest.approx(1.0, rel=1e-10)
+    assert o["alpha"] == pytest.approx(ds[k], rel=1e-12)
+
+
+def test_srqr_kahan_pathology():
+    """g2 'can be exceptionally large for contrived pathological
+    matrices' -- the Kahan matrix under QRCP (identity pivots, Table I) -- and
+    stays below the QRCP bound g2 <= 2^l; RQRCP's random pivots give a
+    modest g2 on the same matrix (Table I 'SRQR' residuals)."""
+    n = 96
+    K = inputs.kahan(n).numpy()
+    oq = oracle.srqr_verify(K, n - 1, 64, n - 64, seed=1, omega=np.eye(n))
+    assert oq["g2_exact"] > 1e6
+    assert oq["g2_exact"] <= 2.0 ** n
+    for seed in range(3):
+        orr = oracle.srqr_verify(K, n - 1, 64, 10, seed=seed)
+        assert orr["g2_exact"] < 10.0
+
+
+def test_srqr_estimator_statistics():
+    """The d-row Gaussian estimate of g2 against the exact value:
+    within a factor 3 in >= 95% of 60 seeds (d = 8)."""
+    A = inputs.make("svd_exp", 120, 90, 4).numpy()
+    ok = 0
+    for seed in range(60):
+        o = oracle.srqr_verify(A, 20, 10, 6, seed=seed, d=8)
+        r = o["g2_est"] / o["g2_exact"]
+        ok += (1.0 / 3.0 <= r <= 3.0)
+    assert ok >= 57
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_srqr_tau_caps(seed):
+    """Eqs. (9)-(12) with exact quantities: tau = g1 g2 (||R22||_2/||R22||_{1,2})
+    (||R-hat^{-T}||_{1,2}^{-1}/sigma_{l+1}(A)) <= g1 g2 sqrt((l+1)(n-l)) and
+    tau-hat <= g1 g2 sqrt(l (n-l)), l = k."""
+    A = inputs.make("svd_exp", 100, 80, 10 + seed).numpy()
+    k = 16
+    o = oracle.srqr_verify(A, k, 8, 6, seed=seed)
+    F = o["res"]["A"]
+    m, n = F.shape
+    R22 = F[k:, k:]
+    c12 = np.max(np.linalg.norm(R22, axis=0))
+    s22 = np.linalg.norm(R22, 2)
+    sA = np.linalg.svd(A, compute_uv=False)
+    g1, g2 = o["g1"], o["g2_exact"]
+    rinv_12 = g2 / o["alpha"]   # ||R-hat^{-T}||_{1,2}
+    tau = g1 * g2 * (s22 / c12) * (1.0 / rinv_12) / sA[k]
+    assert s22 == pytest.approx(tau * sA[k], rel=1e-12)          # Eq. (9) as an identity
+    assert tau <= g1 * g2 * np.sqrt((k + 1) * (n - k)) * (1 + 1e-12)  # Eq. (10)
+    R11 = np.triu(F[:k, :k])
+    r11inv_12 = np.max(np.linalg.norm(np.linalg.inv(R11), axis=1))  # ||R11^{-T}||_{1,2}
+    Rt = np.triu(F[:k, :])
+    s_l = np.linalg.svd(Rt, compute_uv=False)[k - 1]
+    tau_hat = g1 * g2 * (s22 / c12) * (1.0 / r11inv_12) / s_l
+    assert tau_hat <= g1 * g2 * np.sqrt(k * (n - k)) * (1 + 1e-12)  # Eq. (12)
