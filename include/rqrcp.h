@@ -163,6 +163,24 @@ int rqrcp_nccl_unique_id(uint8_t *out);
 /* Per-phase timings of the last rqrcp_factor on ctx. */
 int rqrcp_get_timings(const rqrcp_ctx *ctx, rqrcp_timings *out);
 
+/* SRQR verification (Alg. 3 first half): RQRCP to rank k exactly
+ * as rqrcp_factor (same arguments and outputs), keeping the sample after the
+ * last panel (reading G9), then
+ *   r_i = ||B(:, i)||^2 / (b+p) for the trailing columns, iota = argmax
+ *   (P:635-637); columns k and k + iota of A and jpvt are swapped;
+ *   |alpha| = ||A(k:m, k)|| (one QR step; its reflector is not
+ *   applied); g1 = ||A(k:m, k:n)||_{1,2} / |alpha| (Eq. 8);
+ *   g2 ~= |alpha|/sqrt(d) ||Omega_d R-hat^{-T}||_{1,2}, Omega_d the d x (k+1)
+ *   N(0,1) matrix of (seed, Philox stream 7), R-hat = [[R11, a], [0, |alpha|]]
+ *   (P:505-511).
+ * Requires k < min(m, n) and 1 <= d <= 64; single GPU (nranks = 1).
+ * diag (host, 6 doubles): {g1, g2 estimate, |alpha|, the tau cap
+ * g1 g2 sqrt((k+1)(n-k)) of Eq. (10), the tau-hat cap g1 g2 sqrt(k(n-k)) of
+ * Eq. (12), iota}.  Returns as rqrcp_factor, -13 for an invalid d, or
+ * RQRCP_E_UNSUPPORTED (nranks > 1 or k = min(m, n)). */
+int rqrcp_srqr_verify(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
+                      uint64_t seed, int d, int64_t *jpvt, double *tau, int64_t *rank_out, double *diag);
+
 /* Sample updating formula for subsequent rqrcp_factor calls on ctx (Alg. 2
  * line P:151): 1 = Eq. (4) (default: reuse the sample's triangular
  * factor, O(nkb) flops), 2 = Eq. (5) (keep Omega-bar = Omega Q

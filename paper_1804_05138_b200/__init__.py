@@ -72,6 +72,8 @@ def lib():
         L.rqrcp_get_timings.argtypes = [vp, ctypes.POINTER(RqrcpTimings)]
         L.rqrcp_set_timing.argtypes = [vp, ip]
         L.rqrcp_set_update_rule.argtypes = [vp, ip]
+        L.rqrcp_srqr_verify.argtypes = [vp, vp, i64, i64, i64, i64, ip, ip, ctypes.c_uint64, ip, vp, vp,
+                                        ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double)]
         L.rqrcp_destroy.argtypes = [vp]
         L.rqrcp_last_error.argtypes = [vp]
         L.rqrcp_last_error.restype = ctypes.c_char_p
@@ -86,7 +88,7 @@ def lib():
 
 
 EXPORTED = ["rqrcp_create", "rqrcp_factor", "rqrcp_factor_host", "rqrcp_factor_ex", "rqrcp_fill_gaussian",
-            "rqrcp_philox_words", "rqrcp_flops", "rqrcp_get_timings", "rqrcp_set_timing", "rqrcp_set_update_rule", "rqrcp_destroy",
+            "rqrcp_philox_words", "rqrcp_flops", "rqrcp_get_timings", "rqrcp_set_timing", "rqrcp_set_update_rule", "rqrcp_srqr_verify", "rqrcp_destroy",
             "rqrcp_last_error", "rqrcp_version", "rqrcp_shard_columns", "rqrcp_shard_global_index",
             "rqrcp_nccl_unique_id"]
 
@@ -233,6 +235,28 @@ class RQRCP:
         t = RqrcpTimings()
         lib().rqrcp_get_timings(self._h, ctypes.byref(t))
         return t.as_dict()
+
+    def srqr_verify(self, A, k, b, p, seed=0, d=8, jpvt=None, tau=None):
+        """RQRCP to rank k + the SRQR verification of Alg. 3, see
+        rqrcp_srqr_verify in include/rqrcp.h.  A is factored in place (with the
+        (k+1)-th pivot swapped to position k).  Returns (jpvt, tau, rank, diag)
+        with diag = dict(g1, g2_est, alpha, tau_bound, tau_hat_bound, pivot)."""
+        import torch
+        m, n, lda = _check_colmajor(A)
+        if jpvt is None:
+            jpvt = torch.empty(n, dtype=torch.int64, device=A.device)
+        if tau is None:
+            tau = torch.empty(max(k, 1), dtype=torch.float64, device=A.device)
+        rank = ctypes.c_int64(0)
+        out = (ctypes.c_double * 6)()
+        rc = lib().rqrcp_srqr_verify(self._h, A.data_ptr(), lda, m, n, k, b, p, seed, d, jpvt.data_ptr(),
+                                     tau.data_ptr(), ctypes.byref(rank), out)
+        if rc:
+            raise self._err(rc)
+        names = ("g1", "g2_est", "alpha", "tau_bound", "tau_hat_bound", "pivot")
+        diag = {nm: float(v) for nm, v in zip(names, out)}
+        diag["pivot"] = int(diag["pivot"])
+        return jpvt, tau[:k], int(rank.value), diag
 
     def set_update_rule(self, rule: int):
         """1: Eq. (4) (default), 2: Eq. (5) -- see rqrcp_set_update_rule in include/rqrcp.h."""

@@ -25,6 +25,7 @@
 #include "tri.cuh"
 #include "cqr.cuh"
 #include "dist.cuh"
+#include "srqr.cuh"
 
 using namespace rq;
 
@@ -817,7 +818,7 @@ static int panel_cqr(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t 
 
 static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
                        uint64_t seed, int64_t *jpvt, double *tau, int64_t *rank_out, const double *omega_in,
-                       double *omega_out, double *gaps_out) {
+                       double *omega_out, double *gaps_out, bool keep_last = false, int *final_sample = nullptr) {
     if (!ctx) return -1;
     if (!A) return -2;
     if (lda < std::max<int64_t>(1, m)) return -3;
@@ -903,7 +904,8 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         const int bbpad = (int)rup(bb, 8);
         const int64_t mp = m - i, np = n - i, npp = np - bb;
         ++panels;
-        const bool rule5 = ctx->update_rule == 2 && i + bb < k && npp > 0;
+        const bool more = (i + bb < k) || keep_last;  // a sample update follows this panel
+        const bool rule5 = ctx->update_rule == 2 && more && npp > 0;
         if (rule5)  // Eq. (5) needs B2 = the pre-QRCP sample
             CK(cudaMemcpyAsync(ctx->bpre, ctx->bs[cur], sizeof(double) * (size_t)lpad * (size_t)np,
                                cudaMemcpyDeviceToDevice, st));
@@ -1077,7 +1079,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             const size_t smem = ((size_t)nb * nb + (size_t)(nb / 2) * (nb / 2)) * sizeof(double);
             CK(cudaEventRecord(ctx->ev_fork, st));
             CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-            const int do_om = (i + bb < k && npp > 0 && !rule5) ? 1 : 0;
+            const int do_om = (more && npp > 0 && !rule5) ? 1 : 0;
             tri_kernel<<<2, TRI_THREADS, smem, ctx->side>>>(ctx->ybuf, tau + i, ctx->rhat11, R11p, ldr11, bb, bbpad,
                                                           nb, bb_eff, ctx->tneg, ctx->omhat, do_om, ctx->cqr_status);
             CKL();
@@ -1109,7 +1111,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         }
         ph_end(ctx);
         // ---- S6: sample update (Eq. (4) or (5)); skipped after the last panel (R-G9)
-        if (i + bb < k && npp > 0) {
+        if (more && npp > 0) {
             ph_begin(ctx, PH_SUPD);
             double *udst = (P == 1) ? ctx->bs[cur ^ 1] : ctx->gsend;
             if (rule5) {
@@ -1151,6 +1153,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             cur ^= 1;
         }
     }
+    if (final_sample) *final_sample = cur;
     // ---- status ----------------------------------------------------------
     int hs[5];
     CK(cudaMemcpyAsync(hs, ctx->iscal, sizeof(int) * 5, cudaMemcpyDeviceToHost, st));
@@ -1253,6 +1256,67 @@ extern "C" int rqrcp_factor_ex(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m
                                uint64_t seed, int64_t *jpvt, double *tau, int64_t *rank_out, const double *omega_in,
                                double *omega_out, double *gaps_out) {
     return factor_impl(ctx, A, lda, m, n, k, b, p, seed, jpvt, tau, rank_out, omega_in, omega_out, gaps_out);
+}
+
+extern "C" int rqrcp_srqr_verify(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b,
+                                 int p, uint64_t seed, int d, int64_t *jpvt, double *tau, int64_t *rank_out,
+                                 double *diag) {
+    if (ctx && (d < 1 || d > 64)) return -13;
+    if (ctx && ctx->nranks > 1) {
+        ctx->err = "rqrcp_srqr_verify is single-GPU only";
+        return RQRCP_E_UNSUPPORTED;
+    }
+    if (ctx && m >= 1 && n >= 1 && k >= std::min(m, n)) {
+        ctx->err = "SRQR verification needs k < min(m, n)";
+        return RQRCP_E_UNSUPPORTED;
+    }
+    int fin = 0;
+    int rc = factor_impl(ctx, A, lda, m, n, k, b, p, seed, jpvt, tau, rank_out, nullptr, nullptr, nullptr, true, &fin);
+    if (rc != 0) return rc;  // including the rank-deficient early stop: nothing to verify
+    if (!diag) return -14;
+    cudaStream_t st = ctx->stream;
+    const int l = b + p;
+    const int lpad = (int)rup(l, 8);
+    const int64_t nt = n - k;
+    int *iota = ctx->iscal + 5;
+    srqr_pick_kernel<<<1, SRQR_THREADS, 0, st>>>(ctx->bs[fin], lpad, l, nt, iota);
+    CKL();
+    srqr_swaplist_kernel<<<1, 1, 0, st>>>(iota, ctx->swap_dst, ctx->swap_src, ctx->swap_np);
+    CKL();
+    const int64_t lds = ctx->max_m;
+    swap_gather_kernel<<<grid_for(2 * m, 256, ctx->num_sms), 256, 0, st>>>(A + k * lda, lda, m, jpvt + k, ctx->swap_src,
+                                                                            ctx->swap_np, ctx->swap_stage, lds,
+                                                                            ctx->swap_jstage);
+    CKL();
+    swap_scatter_kernel<<<grid_for(2 * m, 256, ctx->num_sms), 256, 0, st>>>(A + k * lda, lda, m, jpvt + k,
+                                                                             ctx->swap_dst, ctx->swap_np,
+                                                                             ctx->swap_stage, lds, ctx->swap_jstage);
+    CKL();
+    unsigned long long *maxbits = reinterpret_cast<unsigned long long *>(ctx->sumsq_part);
+    double *alpha = ctx->sumsq_part + 1;
+    CK(cudaMemsetAsync(ctx->sumsq_part, 0, 2 * sizeof(double), st));
+    srqr_norms_kernel<<<grid_for(nt * 32, 256, ctx->num_sms), 256, 0, st>>>(A + k + k * lda, lda, m - k, nt, maxbits,
+                                                                            alpha);
+    CKL();
+    const size_t ssm = sizeof(double) * (size_t)(k + 1);
+    if (ssm > 200 * 1024) {
+        ctx->err = "SRQR verification: k too large for the shared-memory solve";
+        return RQRCP_E_WORKSPACE;
+    }
+    CK(cudaFuncSetAttribute(srqr_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+    double *Y = ctx->splitk;  // (k+1) x d <= 4 M doubles
+    if ((k + 1) * (int64_t)d > ctx->splitk_elems) {
+        ctx->err = "SRQR verification: workspace";
+        return RQRCP_E_WORKSPACE;
+    }
+    srqr_solve_kernel<<<d, SRQR_THREADS, ssm, st>>>(A, lda, k, alpha, seed, Y);
+    CKL();
+    double *dout = ctx->sumsq_part + 2;
+    srqr_g2_kernel<<<1, SRQR_THREADS, 0, st>>>(Y, k, d, maxbits, alpha, iota, n, dout);
+    CKL();
+    CK(cudaMemcpyAsync(diag, dout, 6 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return 0;
 }
 
 extern "C" int rqrcp_factor_host(rqrcp_ctx *ctx, const double *A_host, int64_t lda, int64_t m, int64_t n, int64_t k,

@@ -270,3 +270,40 @@ def test_eq4_eq5_identical_permutations_gpu(ctx):
     d4 = np.abs(np.diag(g4["A"])[:256])
     d5 = np.abs(np.diag(g5["A"])[:256])
     assert np.max(np.abs(d4 - d5) / d4) <= DIAG_RTOL
+
+
+# ---- SRQR verification (Alg. 3 first half): SURVEY.md §8(f) N1 ----
+SRQR_CASES = [
+    ("C1", "svd_exp", 512, 512, 64, 32, 8, 1001),
+    ("ragged", "iid", 700, 523, 100, 32, 8, 11),
+    ("lowrank", "lowrank", 1024, 1024, 160, 64, 10, 14),
+    ("b128", "graded", 900, 1100, 256, 128, 16, 17),
+]
+
+
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", SRQR_CASES, ids=[c[0] for c in SRQR_CASES])
+def test_srqr_verify_parity(ctx, name, kind, m, n, k, b, p, seed):
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    o = oracle.srqr_verify(A, k, b, p, seed=seed, d=8)
+    Ad = to_dev(A)
+    jpvt, tau, rank, diag = ctx.srqr_verify(Ad, k, b, p, seed=seed, d=8)
+    torch.cuda.synchronize()
+    assert rank == k
+    assert diag["pivot"] == o["pivot"]
+    assert np.array_equal(jpvt.cpu().numpy(), o["res"]["jpvt"])
+    assert diag["alpha"] == pytest.approx(o["alpha"], rel=1e-10)
+    assert diag["g1"] == pytest.approx(o["g1"], rel=1e-10)
+    assert diag["g2_est"] == pytest.approx(o["g2_est"], rel=1e-9)
+    assert diag["tau_bound"] == pytest.approx(o["tau_bound"], rel=1e-9)
+    F = Ad.cpu().numpy()
+    dg, do = np.abs(np.diag(F)[:k]), np.abs(np.diag(o["res"]["A"])[:k])
+    assert np.max(np.abs(dg - do) / do) <= DIAG_RTOL
+
+
+def test_srqr_verify_errors(ctx):
+    import paper_1804_05138_b200 as rq
+    A = to_dev(inputs.iid(3, 64, 48).numpy())
+    with pytest.raises(rq.RqrcpError):
+        ctx.srqr_verify(A, 48, 16, 4, d=8)     # k = min(m, n): nothing to verify
+    with pytest.raises(rq.RqrcpError):
+        ctx.srqr_verify(A, 16, 8, 4, d=0)      # d out of range
