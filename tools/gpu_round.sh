@@ -1,8 +1,12 @@
+# Round-end evidence run: GPU test suite, bench lines for every config, C2 launch list.
 set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
-tail -5 gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke.log
-timeout 600 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo "bench rc=$?"; cat gpurun_out/bench_c2.json
-timeout 600 python bench.py --config C3 --steps 5 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; echo "bench c3 rc=$?"; cat gpurun_out/bench_c3.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python tools/profile_step.py --config C2 > gpurun_out/ncu_launch.log 2>&1; echo "ncu rc=$?"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log
+timeout 600 python bench.py > gpurun_out/bench_C2.json 2> gpurun_out/bench_C2.err; echo "bench C2 rc=$?"
+timeout 600 python bench.py --config C3 --steps 5 --no-cpu-baseline > gpurun_out/bench_C3.json 2> gpurun_out/bench_C3.err; echo "bench C3 rc=$?"
+timeout 900 python bench.py --config C4 --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.err; echo "bench C4 rc=$?"
+timeout 900 python bench.py --config C5 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err; echo "bench C5 rc=$?"
+for c in C2 C3 C4 C5; do cat gpurun_out/bench_$c.json; tail -2 gpurun_out/bench_$c.err; done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_C2.csv python tools/profile_step.py --config C2 > gpurun_out/ncu_launch.log 2>&1; echo "ncu rc=$?"
