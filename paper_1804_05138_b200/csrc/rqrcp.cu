@@ -835,11 +835,11 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         return RQRCP_E_WORKSPACE;
     }
     CK(cudaSetDevice(ctx->device));
-    // panel path: RQRCP_PANEL=hh (column-by-column Householder), =cqr
-    // (CholeskyQR2 + reconstruction wherever it is accurate), default auto:
-    // CholeskyQR2 for panels of >= kCqrMinRows rows (measured faster there)
-    int panel_mode = 2;
-    if (const char *e = getenv("RQRCP_PANEL")) panel_mode = (e[0] == 'h' || e[0] == 'H') ? 0 : 1;
+    // panel path: RQRCP_PANEL=hh (column-by-column Householder, default),
+    // =cqr (CholeskyQR2 + reconstruction wherever it is accurate), =auto
+    // (CholeskyQR2 for panels of >= kCqrMinRows rows)
+    int panel_mode = 0;  // measured (C2-C5): the column-by-column kernel is as fast or faster
+    if (const char *e = getenv("RQRCP_PANEL")) panel_mode = (e[0] == 'h' || e[0] == 'H') ? 0 : (e[0] == 'a' ? 2 : 1);
     const int P = ctx->nranks, me = ctx->rank;
     const int64_t n_loc = dist_count(n, b, P, me);  // this rank's columns (n when P = 1)
     ctx->launches = 0;
