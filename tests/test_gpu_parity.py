@@ -307,3 +307,49 @@ def test_srqr_verify_errors(ctx):
         ctx.srqr_verify(A, 48, 16, 4, d=8)     # k = min(m, n): nothing to verify
     with pytest.raises(rq.RqrcpError):
         ctx.srqr_verify(A, 16, 8, 4, d=0)      # d out of range
+
+
+# ---- the CholeskyQR2 + Householder-reconstruction panel (cqr.cuh; the "TSQR
+#      for the panel" future work of P:775) ----
+CQR_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "wide", "lowrank", "b128", "odd")]
+
+
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", CQR_CASES, ids=[c[0] for c in CQR_CASES])
+def test_cqr_panel_parity(ctx, name, kind, m, n, k, b, p, seed):
+    """RQRCP_PANEL=cqr: every well-conditioned panel goes through CholeskyQR2 +
+    reconstruction (checked through the panels_householder counter) and the
+    result meets the same acceptance as the column-by-column panel."""
+    import os
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    o = oracle.rqrcp(A, k, b, p, seed=seed)
+    os.environ["RQRCP_PANEL"] = "cqr"
+    try:
+        g = gpu_factor(ctx, A, k, b, p, seed)
+        t = ctx.timings()
+    finally:
+        os.environ.pop("RQRCP_PANEL", None)
+    compare(A, g, o, k)
+    assert t["panels_householder"] < t["panels"]  # the CholeskyQR2 path factored panels
+
+
+def test_cqr_guard_falls_back(ctx):
+    """A rank-stopped panel (rank 40 < k = 64, b = 32: the second panel stops
+    at bb_eff = 8, reading R-G12) fails the CholeskyQR2 guard and is factored
+    by the column-by-column kernel; the result matches the oracle's."""
+    import os
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((300, 40)) @ rng.standard_normal((40, 260))
+    o = oracle.rqrcp(A, 64, 32, 8, seed=3, check=False)
+    os.environ["RQRCP_PANEL"] = "cqr"
+    try:
+        Ad = to_dev(A)
+        jpvt, tau, rank = ctx.factor(Ad, 64, 32, 8, seed=3)
+        torch.cuda.synchronize()
+        t = ctx.timings()
+    finally:
+        os.environ.pop("RQRCP_PANEL", None)
+    assert rank == o["rank"] == 40
+    assert t["panels_householder"] >= 1
+    assert np.array_equal(jpvt.cpu().numpy()[:40], o["jpvt"][:40])
+    dg, do = np.abs(np.diag(Ad.cpu().numpy())[:40]), np.abs(np.diag(o["A"])[:40])
+    assert np.max(np.abs(dg - do) / do) <= DIAG_RTOL
