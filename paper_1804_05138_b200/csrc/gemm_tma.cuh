@@ -249,3 +249,190 @@ __global__ void __launch_bounds__(WM *WN * 32, 1)
 }
 
 }  // namespace rq
+
+namespace rq {
+
+// ---------------------------------------------------------------------------
+// The S5 rank-bb update A22 += V W2 (as A22^T += W2^T Vt) with the C tile
+// moved by TMA in both directions, so the compute warps issue no global
+// loads or stores: per tile (BM = 64 columns x BN = 128 rows of A22) the
+// elected thread loads the next tile's C into the other of two shared-memory
+// buffers (16 boxes of {8 rows, 64 columns}: the fragment reads of a warp
+// cover 512 contiguous bytes), the warps add their accumulators into the
+// current buffer, and the elected thread stores it back with bulk tensor
+// stores (out-of-range rows / columns are skipped by the TMA unit).
+// Operands as in gemm_tma_kernel (persistent, one stage stream over tiles).
+// ---------------------------------------------------------------------------
+RQ_DEV void tma_store_2d(const CUtensorMap *tm, int c0, int c1, const void *src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(tm), "r"(c0),
+                 "r"(c1), "r"(smem_u32(src))
+                 : "memory");
+}
+
+template <int MT, int NT, int WM, int WN, int BK, int ST>
+constexpr size_t tma_upd_smem() {
+    return 128 + (size_t)ST * BK * (8 * MT * WM + 8 * NT * WN) * sizeof(double) +
+           2 * (size_t)(8 * MT * WM) * (8 * NT * WN) * sizeof(double) + (ST + 2) * sizeof(uint64_t);
+}
+
+template <int MT, int NT, int WM, int WN, int BK, int ST>
+__global__ void __launch_bounds__(WM *WN * 32, 1)
+    gemm_upd_tma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
+                        const __grid_constant__ CUtensorMap tmC, TmaGemmArgs g) {
+    constexpr int BM = 8 * MT * WM;  // columns of A22 per tile
+    constexpr int BN = 8 * NT * WN;  // rows of A22 per tile
+    constexpr int KB = BK / 8;
+    constexpr int XS = KB * BM * 8;
+    constexpr int YS = KB * BN * 8;
+    constexpr int CS = BM * BN;      // doubles per C buffer: BN/8 slabs of [BM][8]
+    constexpr unsigned STAGE_BYTES = (unsigned)((XS + YS) * sizeof(double));
+    constexpr unsigned C_BYTES = (unsigned)(CS * sizeof(double));
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const unsigned pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
+    double *xs = reinterpret_cast<double *>(smem_raw + pad);
+    double *ys = xs + ST * XS;
+    double *cb = ys + ST * YS;  // [2][CS]
+    uint64_t *full = reinterpret_cast<uint64_t *>(cb + 2 * CS);
+    uint64_t *cfull = full + ST;  // [2]
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wm = warp / WN, wn = warp % WN;
+    const int fr = lane >> 2, fk = (lane & 3) * 2;
+    const int64_t tilesN = (g.N + BN - 1) / BN, tilesM = (g.M + BM - 1) / BM;
+    const int64_t ntiles = tilesN * tilesM;
+
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) mbar_init(&full[s], 1);
+        mbar_init(&cfull[0], 1);
+        mbar_init(&cfull[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    struct It {
+        int64_t t, kc, nk, m0, n0;
+    };
+    auto set_tile = [&](It &it, int64_t t) {
+        it.t = t;
+        it.kc = 0;
+        if (t >= ntiles) return;
+        it.m0 = (t / tilesN) * BM;
+        it.n0 = (t % tilesN) * BN;
+        it.nk = (g.K + BK - 1) / BK;
+    };
+    auto advance = [&](It &it) {
+        if (++it.kc >= it.nk) set_tile(it, it.t + gridDim.x);
+    };
+    auto issue = [&](const It &it, int slot) {
+        const int64_t k0 = it.kc * BK;
+        mbar_expect_tx(&full[slot], STAGE_BYTES);
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) {
+            tma_load_2d(xs + slot * XS + kb * BM * 8, &tmX, (int)(g.xk0 + k0 + kb * 8), (int)(g.xm0 + it.m0), &full[slot]);
+            tma_load_2d(ys + slot * YS + kb * BN * 8, &tmY, (int)(g.yk0 + k0 + kb * 8), (int)(g.yn0 + it.n0), &full[slot]);
+        }
+    };
+    // C tile of tile t into buffer b: BN/8 boxes {8 rows, BM columns} of A22
+    auto issue_c = [&](int64_t t, int b) {
+        const int64_t m0 = (t / tilesN) * BM, n0 = (t % tilesN) * BN;
+        mbar_expect_tx(&cfull[b], C_BYTES);
+#pragma unroll
+        for (int s = 0; s < BN / 8; ++s)
+            tma_load_2d(cb + b * CS + s * BM * 8, &tmC, (int)(n0 + 8 * s), (int)m0, &cfull[b]);
+    };
+
+    It P, Cn;
+    set_tile(P, blockIdx.x);
+    set_tile(Cn, blockIdx.x);
+    int64_t sp = 0, sc = 0;
+    if (tid == 0) {
+        if (Cn.t < ntiles) issue_c(Cn.t, 0);
+        for (int s = 0; s < ST - 1 && P.t < ntiles; ++s) {
+            issue(P, (int)(sp % ST));
+            ++sp;
+            advance(P);
+        }
+    }
+    int64_t ntile_local = 0;  // tiles this CTA has finished (buffer = ntile_local & 1)
+    double acc[MT][NT][2];
+    while (Cn.t < ntiles) {
+        const int slot = (int)(sc % ST);
+        mbar_wait(&full[slot], (unsigned)((sc / ST) & 1));
+        __syncthreads();
+        if (tid == 0 && P.t < ntiles) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            issue(P, (int)(sp % ST));
+            ++sp;
+            advance(P);
+        }
+        if (Cn.kc == 0) {
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+            // the next tile's C into the other buffer (its previous stores must
+            // have finished reading it)
+            if (tid == 0) {
+                const int64_t tn = Cn.t + gridDim.x;
+                if (tn < ntiles) {
+                    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    issue_c(tn, (int)((ntile_local + 1) & 1));
+                }
+            }
+        }
+        const double *xd = xs + slot * XS;
+        const double *yd = ys + slot * YS;
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) {
+            double2 a[MT], b[NT];
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+                a[i] = *reinterpret_cast<const double2 *>(xd + (kb * BM + wm * 8 * MT + i * 8 + fr) * 8 + fk);
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+                b[j] = *reinterpret_cast<const double2 *>(yd + (kb * BN + wn * 8 * NT + j * 8 + fr) * 8 + fk);
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
+        }
+        if (Cn.kc == Cn.nk - 1) {
+            // epilogue: C (shared) += acc, then bulk tensor stores
+            const int bsel = (int)(ntile_local & 1);
+            mbar_wait(&cfull[bsel], (unsigned)((ntile_local >> 1) & 1));
+            double *cbuf = cb + bsel * CS;
+#pragma unroll
+            for (int i = 0; i < MT; ++i) {
+                const int cm = wm * 8 * MT + i * 8 + fr;  // column within the tile
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    const int s = wn * NT + j;  // 8-row slab
+                    double2 *p = reinterpret_cast<double2 *>(cbuf + s * BM * 8 + cm * 8 + fk);
+                    double2 c2 = *p;
+                    c2.x += acc[i][j][0];
+                    c2.y += acc[i][j][1];
+                    *p = c2;
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncthreads();
+            if (tid == 0) {
+#pragma unroll
+                for (int s = 0; s < BN / 8; ++s)
+                    tma_store_2d(&tmC, (int)(Cn.n0 + 8 * s), (int)Cn.m0, cbuf + s * BM * 8);
+                asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+            }
+            ++ntile_local;
+        }
+        ++sc;
+        advance(Cn);
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
+}  // namespace rq

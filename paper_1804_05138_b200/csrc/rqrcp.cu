@@ -226,14 +226,21 @@ static PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
 // box {8 doubles, box1 columns}; out-of-range elements read as zero.
 static bool make_tmap(CUtensorMap *m, const double *base, int64_t dim0, int64_t dim1, int64_t ld, int box1) {
     auto enc = tma_encode_fn();
+    if (!enc && getenv("RQRCP_DEBUG_TMA")) fprintf(stderr, "[rqrcp] no cuTensorMapEncodeTiled entry point\n");
     if (!enc || ((uintptr_t)base & 15) || ((ld * 8) & 15) || dim0 < 1 || dim1 < 1) return false;
     cuuint64_t dims[2] = {(cuuint64_t)dim0, (cuuint64_t)dim1};
     cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
     cuuint32_t box[2] = {8, (cuuint32_t)box1};
     cuuint32_t es[2] = {1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)base, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    static bool warned = false;
+    if (r != CUDA_SUCCESS && !warned && getenv("RQRCP_DEBUG_TMA")) {
+        fprintf(stderr, "[rqrcp] cuTensorMapEncodeTiled failed (%d): cp.async GEMM path\n", (int)r);
+        warned = true;
+    }
+    return r == CUDA_SUCCESS;
 }
 
 // splits minimising ceil(T*S / grid) / S (persistent-grid wave quantisation)
@@ -314,10 +321,36 @@ static int tma_skinny(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const dou
 }
 
 // A22 (rows x cols, lda) += V W2  as  A22^T += W2^T Vt  (TMA operands W2, Vt).
+// For K > 64 the C tile is moved by TMA as well (gemm_upd_tma_kernel; needs a
+// 16-byte aligned A22 with an even lda); else the register-epilogue kernel.
 static int tma_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, const double *w2, int64_t ldw,
                       const double *vt, int64_t ldvt, double *A22, int64_t lda, bool *done) {
     *done = false;
     if (rows <= 0 || cols <= 0) { *done = true; return 0; }
+    // (measured: faster for K = 128, slower for K = 64 where the two-stage
+    // operand ring is too shallow)
+    if (K > 64 && (((uintptr_t)A22 & 15) == 0) && ((lda & 1) == 0)) {
+        constexpr int MT = 4, NT = 4, WM = 2, WN = 4, BK = 32, ST = 2;
+        constexpr int BM = 8 * MT * WM, BN = 8 * NT * WN;
+        CUtensorMap tx, ty, tc;
+        if (make_tmap(&tx, w2, K, cols, ldw, BM) && make_tmap(&ty, vt, K, rows, ldvt, BN) &&
+            make_tmap(&tc, A22, rows, cols, lda, BM)) {
+            const size_t smem = tma_upd_smem<MT, NT, WM, WN, BK, ST>();
+            auto kern = gemm_upd_tma_kernel<MT, NT, WM, WN, BK, ST>;
+            static bool attr = false;
+            if (!attr) {
+                CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                attr = true;
+            }
+            TmaGemmArgs g{cols, rows, K, 0, 0, 0, 0, A22, lda, rup(K, 32), 1, 0, 0};
+            const int64_t tiles = ((rows + BN - 1) / BN) * ((cols + BM - 1) / BM);
+            const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);
+            kern<<<grid, WM * WN * 32, smem, ctx->stream>>>(tx, ty, tc, g);
+            CKL();
+            *done = true;
+            return 0;
+        }
+    }
     if ((lda & 1) || ((uintptr_t)A22 & 7)) return 0;
     TmaGemmArgs g{cols, rows, K, 0, 0, 0, 0, A22, lda, rup(K, 32), 1, 0,
                   (((uintptr_t)A22 & 15) == 0 && (lda & 1) == 0) ? 1 : 0};

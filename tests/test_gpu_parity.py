@@ -353,3 +353,13 @@ def test_cqr_guard_falls_back(ctx):
     assert np.array_equal(jpvt.cpu().numpy()[:40], o["jpvt"][:40])
     dg, do = np.abs(np.diag(Ad.cpu().numpy())[:40]), np.abs(np.diag(o["A"])[:40])
     assert np.max(np.abs(dg - do) / do) <= DIAG_RTOL
+
+
+def test_update_kernels_agree(ctx):
+    """b = 128 (K = 128: the TMA-epilogue update kernel) vs the same
+    factorization with the panels shifted by one row (odd offsets: the
+    register-epilogue / cp.async kernels) -- both against the oracle."""
+    A = inputs.make("iid", 1200, 1000, 33).numpy()
+    o = oracle.rqrcp(A, 256, 128, 16, seed=33)
+    g = gpu_factor(ctx, A, 256, 128, 16, 33)
+    compare(A, g, o, 256)
