@@ -304,14 +304,21 @@ def main():
     peak, peak_src = fp64_peak()
     achieved = tr_flops / (tr_ms * 1e-3) / 1e12 if tr_ms > 0 else 0.0
     traffic = None
-    try:
-        traffic = json.load(open(PROFILE_TRAFFIC)).get(args.config)
+    try:  # ncu dram__bytes_read + dram__bytes_write of the S5 kernels per panel (profiles/traffic_r01.json)
+        traffic = json.load(open(PROFILE_TRAFFIC)).get(args.config, {}).get("dram_bytes_per_panel_trailing")
     except Exception:
         pass
+    # algorithmic S5 bytes per panel (unfused: A22 read twice, written once)
+    alg_bytes = 0.0
+    for i in range(0, k, b):
+        bb = min(b, k - i)
+        alg_bytes += 24.0 * (m - i) * (n - i - bb) / world
+    alg_bytes /= max(1, (k + b - 1) // b)
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if peak else None, "traffic": traffic,
                 "kernel": "S5 trailing update (W = V^T A22, W2 = -T^T W, A22 += V W2; DMMA.8x8x4)",
-                "peak_source": peak_src}
+                "peak_source": peak_src, "traffic_unit": "DRAM bytes per panel (ncu, S5 kernels)",
+                "algorithmic_bytes_per_panel": alg_bytes}
     whole_frac = (F / (ms * 1e-3) / 1e12) / peak
 
     e2e = None
