@@ -181,6 +181,28 @@ int rqrcp_get_timings(const rqrcp_ctx *ctx, rqrcp_timings *out);
 int rqrcp_srqr_verify(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
                       uint64_t seed, int d, int64_t *jpvt, double *tau, int64_t *rank_out, double *diag);
 
+/* Low-rank outputs of a factorization (SURVEY.md
+ * §8(f) N4), from the outputs of rqrcp_factor (single GPU):
+ *
+ * rqrcp_form_q1: Q1 (device, m x k, ld ldq >= m, caller-owned, overwritten) =
+ *   the first k columns of Q = H_1 ... H_k, from the reflectors below the
+ *   diagonal of the factored A (device, ld lda) and tau (device, k); b is
+ *   the panel width the factorization used (T is rebuilt per panel).
+ *   A Pi ~= Q1 [R11 R12].  Returns 0, -1 ctx null, -2 A null, -3 lda,
+ *   -4 m, -5 n, -6 k, -7 b, -8 tau null, -9 Q1 null, -10 ldq, or RQRCP_E_*.
+ *
+ * rqrcp_cx: X (device, k x n, ld ldx >= k, caller-owned) = C^+ A with
+ *   C = A Pi(:, 0:k) the first k pivot columns (the CX decomposition of
+ *   P:813-815; exact for full-rank R11: X Pi = [I, R11^{-1} R12]), from the
+ *   factored A and jpvt (device, n).  Allocates and frees k*k + (k+64)(n-k)
+ *   doubles of temporary device memory.  ||A - C X||_F = ||R22||_F.
+ *   Returns 0, -1 ctx null, -2 A null, -3 lda, -4 m, -5 n, -6 k, -7 jpvt
+ *   null, -8 X null, -9 ldx, or RQRCP_E_*. */
+int rqrcp_form_q1(rqrcp_ctx *ctx, const double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b,
+                  const double *tau, double *Q1, int64_t ldq);
+int rqrcp_cx(rqrcp_ctx *ctx, const double *A, int64_t lda, int64_t m, int64_t n, int64_t k, const int64_t *jpvt,
+             double *X, int64_t ldx);
+
 /* Sample updating formula for subsequent rqrcp_factor calls on ctx (Alg. 2
  * line P:151): 1 = Eq. (4) (default: reuse the sample's triangular
  * factor, O(nkb) flops), 2 = Eq. (5) (keep Omega-bar = Omega Q

@@ -72,6 +72,8 @@ def lib():
         L.rqrcp_get_timings.argtypes = [vp, ctypes.POINTER(RqrcpTimings)]
         L.rqrcp_set_timing.argtypes = [vp, ip]
         L.rqrcp_set_update_rule.argtypes = [vp, ip]
+        L.rqrcp_form_q1.argtypes = [vp, vp, i64, i64, i64, i64, ip, vp, vp, i64]
+        L.rqrcp_cx.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp, i64]
         L.rqrcp_srqr_verify.argtypes = [vp, vp, i64, i64, i64, i64, ip, ip, ctypes.c_uint64, ip, vp, vp,
                                         ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double)]
         L.rqrcp_destroy.argtypes = [vp]
@@ -88,7 +90,8 @@ def lib():
 
 
 EXPORTED = ["rqrcp_create", "rqrcp_factor", "rqrcp_factor_host", "rqrcp_factor_ex", "rqrcp_fill_gaussian",
-            "rqrcp_philox_words", "rqrcp_flops", "rqrcp_get_timings", "rqrcp_set_timing", "rqrcp_set_update_rule", "rqrcp_srqr_verify", "rqrcp_destroy",
+            "rqrcp_philox_words", "rqrcp_flops", "rqrcp_get_timings", "rqrcp_set_timing", "rqrcp_set_update_rule", "rqrcp_srqr_verify",
+            "rqrcp_form_q1", "rqrcp_cx", "rqrcp_destroy",
             "rqrcp_last_error", "rqrcp_version", "rqrcp_shard_columns", "rqrcp_shard_global_index",
             "rqrcp_nccl_unique_id"]
 
@@ -257,6 +260,30 @@ class RQRCP:
         diag = {nm: float(v) for nm, v in zip(names, out)}
         diag["pivot"] = int(diag["pivot"])
         return jpvt, tau[:k], int(rank.value), diag
+
+    def form_q1(self, A, k, b, tau, Q1=None):
+        """Q1 = first k columns of Q = H_1...H_k from a factored A."""
+        import torch
+        m, n, lda = _check_colmajor(A)
+        if Q1 is None:
+            Q1 = torch.empty(k, m, dtype=torch.float64, device=A.device).t()
+        _, _, ldq = _check_colmajor(Q1)
+        rc = lib().rqrcp_form_q1(self._h, A.data_ptr(), lda, m, n, k, b, tau.data_ptr(), Q1.data_ptr(), ldq)
+        if rc:
+            raise self._err(rc)
+        return Q1
+
+    def cx(self, A, k, jpvt, X=None):
+        """CX coefficients X = C^+ A, C = A Pi(:, :k), from a factored A."""
+        import torch
+        m, n, lda = _check_colmajor(A)
+        if X is None:
+            X = torch.empty(n, k, dtype=torch.float64, device=A.device).t()
+        _, _, ldx = _check_colmajor(X)
+        rc = lib().rqrcp_cx(self._h, A.data_ptr(), lda, m, n, k, jpvt.data_ptr(), X.data_ptr(), ldx)
+        if rc:
+            raise self._err(rc)
+        return X
 
     def set_update_rule(self, rule: int):
         """1: Eq. (4) (default), 2: Eq. (5) -- see rqrcp_set_update_rule in include/rqrcp.h."""

@@ -26,6 +26,7 @@
 #include "cqr.cuh"
 #include "dist.cuh"
 #include "srqr.cuh"
+#include "lowrank.cuh"
 
 using namespace rq;
 
@@ -1349,6 +1350,116 @@ extern "C" int rqrcp_srqr_verify(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t
     CKL();
     CK(cudaMemcpyAsync(diag, dout, 6 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+extern "C" int rqrcp_form_q1(rqrcp_ctx *ctx, const double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b,
+                             const double *tau, double *Q1, int64_t ldq) {
+    if (!ctx) return -1;
+    if (!A) return -2;
+    if (lda < std::max<int64_t>(1, m)) return -3;
+    if (m < 1) return -4;
+    if (n < 1) return -5;
+    if (k < 1 || k > std::min(m, n)) return -6;
+    if (b < 1) return -7;
+    if (!tau) return -8;
+    if (!Q1) return -9;
+    if (ldq < m) return -10;
+    if (m > ctx->max_m || b > ctx->max_b || k > ctx->max_n) {
+        ctx->err = "problem exceeds the create-time workspace maxima";
+        return RQRCP_E_WORKSPACE;
+    }
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const int G = ctx->num_sms;
+    int rc = 0;
+    lr_eye_kernel<<<grid_for(m * k, 256, G), 256, 0, st>>>(Q1, ldq, m, k);
+    CKL();
+    int *bbd = ctx->iscal + 6;
+    const int64_t npanels = (k + b - 1) / b;
+    for (int64_t t = npanels - 1; t >= 0; --t) {
+        const int64_t i = t * b;
+        const int bb = (int)std::min<int64_t>(b, k - i);
+        const int bbpad = (int)rup(bb, 8);
+        const int64_t mp = m - i, ncols = k - i;
+        lr_extract_v_kernel<<<grid_for(mp * bbpad, 256, G), 256, 0, st>>>(A + i + i * lda, lda, mp, bb, bbpad,
+                                                                          ctx->vfull, ctx->ldo, ctx->vt);
+        CKL();
+        rc = gemm_skinny(ctx, bbpad, bbpad, mp, ctx->vfull, ctx->ldo, ctx->vfull, ctx->ldo, ctx->ybuf, bbpad);
+        if (rc) return rc;
+        lr_set_int_kernel<<<1, 1, 0, st>>>(bbd, bb);
+        CKL();
+        int nb = 8;
+        while (nb < bbpad) nb *= 2;
+        const size_t tsm = ((size_t)nb * nb + (size_t)(nb / 2) * (nb / 2)) * sizeof(double);
+        tri_kernel<<<1, TRI_THREADS, tsm, st>>>(ctx->ybuf, tau + i, nullptr, nullptr, 0, bb, bbpad, nb, bbd, ctx->tneg,
+                                                ctx->omhat, 0, nullptr);
+        CKL();
+        lr_transpose_kernel<<<grid_for((int64_t)bbpad * bbpad, 256, G), 256, 0, st>>>(ctx->tneg, bbpad, ctx->omhat);
+        CKL();
+        double *X = Q1 + i + i * ldq;
+        // X <- (I - V T V^T) X:  W = V^T X,  W2 = -T W,  X += V W2
+        rc = gemm_skinny(ctx, bbpad, ncols, mp, ctx->vfull, ctx->ldo, X, ldq, ctx->w, bbpad);
+        if (rc) return rc;
+        rc = gemm_skinny(ctx, bbpad, ncols, bbpad, ctx->omhat, bbpad, ctx->w, bbpad, ctx->w2, bbpad);
+        if (rc) return rc;
+        rc = gemm_update(ctx, mp, ncols, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, X, ldq);
+        if (rc) return rc;
+    }
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+extern "C" int rqrcp_cx(rqrcp_ctx *ctx, const double *A, int64_t lda, int64_t m, int64_t n, int64_t k,
+                        const int64_t *jpvt, double *X, int64_t ldx) {
+    if (!ctx) return -1;
+    if (!A) return -2;
+    if (lda < std::max<int64_t>(1, m)) return -3;
+    if (m < 1) return -4;
+    if (n < 1) return -5;
+    if (k < 1 || k > std::min(m, n)) return -6;
+    if (!jpvt) return -7;
+    if (!X) return -8;
+    if (ldx < k) return -9;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const int G = ctx->num_sms;
+    const int64_t n2 = n - k;
+    double *RT = nullptr, *Z = nullptr, *C = nullptr;
+    auto cleanup = [&]() {
+        cudaStreamSynchronize(st);
+        if (RT) cudaFree(RT);
+        if (Z) cudaFree(Z);
+        if (C) cudaFree(C);
+    };
+    if (n2 > 0) {
+        if (cudaMalloc((void **)&RT, sizeof(double) * (size_t)(k * k)) != cudaSuccess ||
+            cudaMalloc((void **)&Z, sizeof(double) * (size_t)(k * n2)) != cudaSuccess ||
+            cudaMalloc((void **)&C, sizeof(double) * (size_t)(64 * n2)) != cudaSuccess) {
+            cleanup();
+            ctx->err = "rqrcp_cx: temporary allocation failed";
+            return RQRCP_E_WORKSPACE;
+        }
+        lr_r11t_kernel<<<grid_for(k * k, 256, G), 256, 0, st>>>(A, lda, k, RT);
+        CKL();
+        // Z = R11^{-1} R12, 64-row blocks from the bottom
+        const int64_t nblk = (k + 63) / 64;
+        for (int64_t bi = nblk - 1; bi >= 0; --bi) {
+            const int64_t r0 = bi * 64, r1 = std::min<int64_t>(k, r0 + 64);
+            const int bs = (int)(r1 - r0);
+            const double *Cp = nullptr;
+            if (r1 < k) {  // C = R11(r0:r1, r1:k) Z(r1:k, :) = RT(r1:k, r0:r1)^T Z(r1:k, :)
+                int rc = gemm_skinny(ctx, bs, n2, k - r1, RT + r1 + r0 * k, k, Z + r1, k, C, 64);
+                if (rc) { cleanup(); return rc; }
+                Cp = C;
+            }
+            lr_block_solve_kernel<<<(unsigned)((n2 + 127) / 128), 128, 0, st>>>(A, lda, k, n2, r0, bs, Cp, 64, Z, k);
+            CKL();
+        }
+    }
+    lr_cx_scatter_kernel<<<grid_for(k * n, 256, G), 256, 0, st>>>(Z, k, jpvt, k, n, X, ldx);
+    CKL();
+    cleanup();
     return 0;
 }
 

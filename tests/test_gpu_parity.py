@@ -363,3 +363,39 @@ def test_update_kernels_agree(ctx):
     o = oracle.rqrcp(A, 256, 128, 16, seed=33)
     g = gpu_factor(ctx, A, 256, 128, 16, 33)
     compare(A, g, o, 256)
+
+
+# ---- low-rank outputs: SURVEY.md §8(f) N4 ----
+LR_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "wide", "b128", "odd")]
+
+
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", LR_CASES, ids=[c[0] for c in LR_CASES])
+def test_lowrank_outputs(ctx, name, kind, m, n, k, b, p, seed):
+    """Q1 against the oracle's reflectors applied to [I; 0] (P:120 'Q = H1 H2
+    ... Hk'), Q1^T Q1 = I, Q1 [R11 R12] = A Pi truncated; CX
+    coefficients against the definition X = C^+ A (least squares) and
+    ||A - C X||_F = ||R22||_F."""
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    o = oracle.rqrcp(A, k, b, p, seed=seed)
+    Ad = to_dev(A)
+    jpvt, tau, rank = ctx.factor(Ad, k, b, p, seed=seed)
+    torch.cuda.synchronize()
+    assert np.array_equal(jpvt.cpu().numpy(), o["jpvt"])
+    Q1 = ctx.form_q1(Ad, k, b, tau)
+    X = ctx.cx(Ad, k, jpvt)
+    torch.cuda.synchronize()
+    Q1h, Xh = Q1.cpu().numpy(), X.cpu().numpy()
+    E = np.zeros((m, k))
+    E[:k, :k] = np.eye(k)
+    Q1o = oracle.apply_q(o["A"], o["tau"], E)
+    assert np.max(np.abs(Q1h - Q1o)) <= 1e-10
+    assert np.linalg.norm(Q1h.T @ Q1h - np.eye(k)) <= 1e-12 * k
+    F = Ad.cpu().numpy()
+    Rt = np.triu(F[:k, :])
+    jp = jpvt.cpu().numpy()
+    assert np.linalg.norm(A[:, jp][:, :k] - Q1h @ Rt[:, :k]) <= 1e-12 * np.linalg.norm(A)
+    C = A[:, jp[:k]]
+    Xref = np.linalg.lstsq(C, A, rcond=None)[0]
+    assert np.linalg.norm(Xh - Xref) <= 1e-8 * np.linalg.norm(Xref)
+    r22 = np.linalg.norm(F[k:, k:])
+    assert abs(np.linalg.norm(A - C @ Xh) - r22) <= 1e-10 * np.linalg.norm(A)
