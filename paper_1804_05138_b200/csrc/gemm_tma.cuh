@@ -269,13 +269,16 @@ RQ_DEV void tma_store_2d(const CUtensorMap *tm, int c0, int c1, const void *src)
                  : "memory");
 }
 
-template <int MT, int NT, int WM, int WN, int BK, int ST>
+template <int MT, int NT, int WM, int WN, int BK, int ST, int CB = 2>
 constexpr size_t tma_upd_smem() {
     return 128 + (size_t)ST * BK * (8 * MT * WM + 8 * NT * WN) * sizeof(double) +
-           2 * (size_t)(8 * MT * WM) * (8 * NT * WN) * sizeof(double) + (ST + 2) * sizeof(uint64_t);
+           CB * (size_t)(8 * MT * WM) * (8 * NT * WN) * sizeof(double) + (ST + 2) * sizeof(uint64_t);
 }
 
-template <int MT, int NT, int WM, int WN, int BK, int ST>
+// CB = 2: the next tile's C loads into the other buffer during this tile;
+// CB = 1: one buffer, the next tile's load is issued once this tile's stores
+// have read it (frees shared memory for a deeper operand ring)
+template <int MT, int NT, int WM, int WN, int BK, int ST, int CB = 2>
 __global__ void __launch_bounds__(WM *WN * 32, 1)
     gemm_upd_tma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
                         const __grid_constant__ CUtensorMap tmC, TmaGemmArgs g) {
@@ -291,8 +294,8 @@ __global__ void __launch_bounds__(WM *WN * 32, 1)
     const unsigned pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
     double *xs = reinterpret_cast<double *>(smem_raw + pad);
     double *ys = xs + ST * XS;
-    double *cb = ys + ST * YS;  // [2][CS]
-    uint64_t *full = reinterpret_cast<uint64_t *>(cb + 2 * CS);
+    double *cb = ys + ST * YS;  // [CB][CS]
+    uint64_t *full = reinterpret_cast<uint64_t *>(cb + CB * CS);
     uint64_t *cfull = full + ST;  // [2]
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -370,9 +373,9 @@ __global__ void __launch_bounds__(WM *WN * 32, 1)
             for (int i = 0; i < MT; ++i)
 #pragma unroll
                 for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-            // the next tile's C into the other buffer (its previous stores must
-            // have finished reading it)
-            if (tid == 0) {
+            // CB = 2: the next tile's C into the other buffer (its previous
+            // stores must have finished reading it)
+            if (CB == 2 && tid == 0) {
                 const int64_t tn = Cn.t + gridDim.x;
                 if (tn < ntiles) {
                     asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
@@ -403,8 +406,8 @@ __global__ void __launch_bounds__(WM *WN * 32, 1)
         }
         if (Cn.kc == Cn.nk - 1) {
             // epilogue: C (shared) += acc, then bulk tensor stores
-            const int bsel = (int)(ntile_local & 1);
-            mbar_wait(&cfull[bsel], (unsigned)((ntile_local >> 1) & 1));
+            const int bsel = (CB == 2) ? (int)(ntile_local & 1) : 0;
+            mbar_wait(&cfull[bsel], (unsigned)(((CB == 2) ? (ntile_local >> 1) : ntile_local) & 1));
             double *cbuf = cb + bsel * CS;
 #pragma unroll
             for (int i = 0; i < MT; ++i) {
@@ -426,6 +429,14 @@ __global__ void __launch_bounds__(WM *WN * 32, 1)
                 for (int s = 0; s < BN / 8; ++s)
                     tma_store_2d(&tmC, (int)(Cn.n0 + 8 * s), (int)Cn.m0, cbuf + s * BM * 8);
                 asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                if (CB == 1) {  // the next tile's C into the same buffer once the stores have read it
+                    const int64_t tn = Cn.t + gridDim.x;
+                    if (tn < ntiles) {
+                        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                        issue_c(tn, 0);
+                    }
+                }
             }
             ++ntile_local;
         }

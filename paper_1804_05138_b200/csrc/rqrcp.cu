@@ -1084,8 +1084,13 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.trace = (panels == 1) ? ctx->ptrace : nullptr;
             int pcap = G;
             if (const char *e = getenv("RQRCP_PN_GRID")) pcap = std::max(1, std::min(G, atoi(e)));
+            // ~64 rows per CTA: fewer CTAs shrink the per-column all-to-all of
+            // partial Gram rows (G x bb doubles read by every CTA), more rows
+            // per CTA lengthen the local pass (measured best at C2)
+            int64_t prows = 64;
+            if (const char *e = getenv("RQRCP_PN_ROWS")) prows = std::max(1, atoi(e));
             const int grid = (int)std::max<int64_t>((mp + PN_MAXROWS - 1) / PN_MAXROWS,
-                                                    std::min<int64_t>(pcap, (mp + 31) / 32));
+                                                    std::min<int64_t>(pcap, (mp + prows - 1) / prows));
             const int64_t rpb = (mp + grid - 1) / grid;
             if (rpb > PN_MAXROWS) {
                 ctx->err = "panel too tall for the cooperative grid";
