@@ -22,6 +22,7 @@
 #include "philox.cuh"
 #include "sample_qrcp.cuh"
 #include "sample_qrcp_cl.cuh"
+#include "sample_qrcp_reg.cuh"
 #include "tri.cuh"
 #include "cqr.cuh"
 #include "dist.cuh"
@@ -527,6 +528,9 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(cudaMemset(ctx->tneg, 0, sizeof(double) * bp * bp));
     CKC(cudaFuncSetAttribute(sample_qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
     CKC(cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
+    CKC(cudaFuncSetAttribute(sample_qrcp_reg_kernel<40, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 40 * 8));
+    CKC(cudaFuncSetAttribute(sample_qrcp_reg_kernel<74, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 74 * 8));
+    CKC(cudaFuncSetAttribute(sample_qrcp_reg_kernel<72, 72>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 144 * 8));
     CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel<40>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel<40>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 40 * 8));
     CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel<74>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -1001,6 +1005,26 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
                     lc.numAttrs = 1;
                     CK(cudaLaunchKernelEx(&lc, kfn, a));
                     CKL();
+                    sq_done = true;
+                }
+            }
+            if (!sq_done) {
+                // one column per thread in registers (+ shared memory), a grid of
+                // 1 + ceil(n'/256) CTAs (sample_qrcp_reg.cuh)
+                const char *e = getenv("RQRCP_SQ_REG");
+                const bool allow = !(e && e[0] == '0');
+                const int grid = 1 + (int)((np + SQR_THREADS - 1) / SQR_THREADS);
+                void (*kfn)(SqArgs) = nullptr;
+                if (l == 40) kfn = sample_qrcp_reg_kernel<40, 0>;
+                else if (l == 74) kfn = sample_qrcp_reg_kernel<74, 0>;
+                else if (l == 144) kfn = sample_qrcp_reg_kernel<72, 72>;
+                if (allow && kfn && !a.gaps && grid <= std::min(G, SQ_MAXG)) {
+                    const int ls = (l == 144) ? 72 : 0;
+                    const size_t smem = (size_t)std::max(ls * SQR_THREADS, bb * l) * sizeof(double);
+                    a.hstride = 8;
+                    void *args[] = {&a};
+                    rc = coop_launch(ctx, (const void *)kfn, grid, SQR_THREADS, args, smem);
+                    if (rc) return rc;
                     sq_done = true;
                 }
             }

@@ -228,13 +228,39 @@ def test_sample_qrcp_launch_variants(ctx, grid, nsm, name, kind, m, n, k, b, p, 
     A = inputs.make(kind, m, n, seed, rank=64).numpy()
     o = oracle.rqrcp(A, k, b, p, seed=seed)
     os.environ["RQRCP_SQ_GRID"] = grid
+    os.environ["RQRCP_SQ_CLUSTER"] = "0"
+    os.environ["RQRCP_SQ_REG"] = "0"
     if nsm is not None:
         os.environ["RQRCP_SQ_NSM"] = nsm
     try:
         g = gpu_factor(ctx, A, k, b, p, seed)
     finally:
-        os.environ.pop("RQRCP_SQ_GRID", None)
-        os.environ.pop("RQRCP_SQ_NSM", None)
+        for v in ("RQRCP_SQ_GRID", "RQRCP_SQ_NSM", "RQRCP_SQ_CLUSTER", "RQRCP_SQ_REG"):
+            os.environ.pop(v, None)
+    compare(A, g, o, k)
+
+
+# ---- the register-resident grid sample QRCP (sample_qrcp_reg.cuh) ----------
+# RQRCP_SQ_CLUSTER=0 takes the one-cluster kernel out, so every sample with
+# l in {40, 74, 144} runs on the grid of 1 + ceil(n'/256) CTAs; the wide cases
+# span several column CTAs with a ragged last one.
+REG_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "lowrank", "kfull", "b128")] + [
+    ("reg_wide74", "iid", 800, 1900, 192, 64, 10, 21),
+    ("reg_wide144", "graded", 900, 2100, 256, 128, 16, 22),
+    ("reg_lowrank144", "lowrank", 700, 1300, 300, 128, 16, 23),
+]
+
+
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", REG_CASES, ids=[c[0] for c in REG_CASES])
+def test_sample_qrcp_register_grid(ctx, name, kind, m, n, k, b, p, seed):
+    import os
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    o = oracle.rqrcp(A, k, b, p, seed=seed)
+    os.environ["RQRCP_SQ_CLUSTER"] = "0"
+    try:
+        g = gpu_factor(ctx, A, k, b, p, seed)
+    finally:
+        os.environ.pop("RQRCP_SQ_CLUSTER", None)
     compare(A, g, o, k)
 
 

@@ -80,10 +80,10 @@ float run_tma(const CUtensorMap &tx, const CUtensorMap &ty, TmaGemmArgs g, int g
     return timeit([&] { k<<<grid, WM * WN * 32, smem>>>(tx, ty, g); }, reps);
 }
 
-template <int MT, int NT, int WM, int WN, int BK, int ST>
+template <int MT, int NT, int WM, int WN, int BK, int ST, int CB = 2>
 float run_upd(const CUtensorMap &tx, const CUtensorMap &ty, const CUtensorMap &tc, TmaGemmArgs g, int grid, int reps) {
-    const size_t smem = tma_upd_smem<MT, NT, WM, WN, BK, ST>();
-    auto k = gemm_upd_tma_kernel<MT, NT, WM, WN, BK, ST>;
+    const size_t smem = tma_upd_smem<MT, NT, WM, WN, BK, ST, CB>();
+    auto k = gemm_upd_tma_kernel<MT, NT, WM, WN, BK, ST, CB>;
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     return timeit([&] { k<<<grid, WM * WN * 32, smem>>>(tx, ty, tc, g); }, reps);
 }
@@ -152,6 +152,12 @@ int main(int argc, char **argv) {
         maxdiff<<<256, 256>>>(A, A2, rows * cols, dmax);
         CK(cudaMemcpy(&h, dmax, 8, cudaMemcpyDeviceToHost));
         printf("\"upd_tma_check_maxdiff\": %.3e, ", h);
+        fill<<<1024, 256>>>(A2, rows * cols, 9);
+        run_upd<4, 4, 2, 4, 32, 3, 1>(tx, ty, tc, t, sms, 0);
+        CK(cudaMemset(dmax, 0, 8));
+        maxdiff<<<256, 256>>>(A, A2, rows * cols, dmax);
+        CK(cudaMemcpy(&h, dmax, 8, cudaMemcpyDeviceToHost));
+        printf("\"upd_tma_cb1_check_maxdiff\": %.3e, ", h);
     }
     std::vector<Shape> ups = {{"C2p0", 4096, 4032, 64}, {"C4p0", 32768, 32640, 128}, {"C5p0", 65536, 16384, 128}};
     printf("\"update\": [");
@@ -170,9 +176,10 @@ int main(int argc, char **argv) {
         float t3 = run_tma<4, 4, 2, 2, 32, 4, EPI_ACCUM_T_PRE>(tx, ty2, t, 2 * sms, 5);
         CUtensorMap tc = make_map(A, rows, cols, rows, 64);
         float t4 = run_upd<4, 4, 2, 4, 32, 2>(tx, ty, tc, t, sms, 5);
-        float t5 = run_upd<4, 4, 2, 4, 16, 4>(tx, ty, tc, t, sms, 5);
-        printf("%s{\"shape\": \"%s\", \"tflops\": {\"cp_epi\": %.2f, \"tma_st4\": %.2f, \"tma_st3\": %.2f, \"tma_64x64_x2\": %.2f, \"upd_bk32_st2\": %.2f, \"upd_bk16_st4\": %.2f}}",
-               si ? ", " : "", s.name, fl / t0 / 1e9, fl / t1 / 1e9, fl / t2 / 1e9, fl / t3 / 1e9, fl / t4 / 1e9, fl / t5 / 1e9);
+        float t5 = run_upd<4, 4, 2, 4, 32, 3, 1>(tx, ty, tc, t, sms, 5);
+        float t6 = run_upd<4, 4, 2, 4, 32, 2, 1>(tx, ty, tc, t, sms, 5);
+        printf("%s{\"shape\": \"%s\", \"tflops\": {\"cp_epi\": %.2f, \"tma_st4\": %.2f, \"tma_st3\": %.2f, \"tma_64x64_x2\": %.2f, \"upd_st2_cb2\": %.2f, \"upd_st3_cb1\": %.2f, \"upd_st2_cb1\": %.2f}}",
+               si ? ", " : "", s.name, fl / t0 / 1e9, fl / t1 / 1e9, fl / t2 / 1e9, fl / t3 / 1e9, fl / t4 / 1e9, fl / t5 / 1e9, fl / t6 / 1e9);
     }
     printf("], \"w\": [");
     std::vector<Shape> ws = {{"C2p0", 4096, 4032, 64}, {"C4p0", 32768, 32640, 128}, {"C5p0", 65536, 16384, 128}};
