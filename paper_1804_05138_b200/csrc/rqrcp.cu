@@ -63,6 +63,7 @@ struct rqrcp_ctx {
     int *slot_col = nullptr;
     unsigned launch_seq = 0;  // tags of the sample-QRCP candidate headers
     double *slot_v2 = nullptr, *slot_data = nullptr;
+    uint4 *sq_ll = nullptr;  // tagged exchange slots of the register grid sample QRCP
     double *sq_spill = nullptr;  // transposed sample columns beyond shared memory (lpad_max x max_n)
     double *pn_part = nullptr, *pn_rowj = nullptr;
     // CholeskyQR2 + reconstruction panel (cqr.cuh): Gram, R factors, inverses
@@ -418,7 +419,7 @@ static int free_all(rqrcp_ctx *ctx) {
     void *ptrs[] = {ctx->omt,     ctx->bs[0],   ctx->bs[1],     ctx->vfull,     ctx->vt,        ctx->w,
                     ctx->w2,      ctx->tneg, ctx->ybuf,   ctx->rhat11,    ctx->omhat,     ctx->vhat,      ctx->tauhat,
                     ctx->splitk,  ctx->slot_hdr, ctx->slot_col, ctx->slot_v2,
-                    ctx->slot_data, ctx->sq_spill, ctx->pn_part, ctx->pn_rowj, ctx->cq_g, ctx->cq_rc, ctx->cq_rinv, ctx->cq_uinv, ctx->cq_lu, ctx->cqr_status, ctx->bpre, ctx->c5, ctx->wom, ctx->w2om,   ctx->swap_stage,
+                    ctx->slot_data, ctx->sq_ll, ctx->sq_spill, ctx->pn_part, ctx->pn_rowj, ctx->cq_g, ctx->cq_rc, ctx->cq_rinv, ctx->cq_uinv, ctx->cq_lu, ctx->cqr_status, ctx->bpre, ctx->c5, ctx->wom, ctx->w2om,   ctx->swap_stage,
                     ctx->swap_dst, ctx->swap_src, ctx->swap_jstage, ctx->swap_np, ctx->perm,     ctx->piv,       ctx->sumsq_part,
                     ctx->iscal,   ctx->stop_tol2, ctx->bars,  ctx->trace, ctx->ptrace,    ctx->a_dev,     ctx->jpvt_dev,  ctx->tau_dev};
     for (void *p : ptrs)
@@ -495,6 +496,8 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(cudaMalloc((void **)&ctx->slot_col, sizeof(int) * 2 * G));
     CKC(dalloc(&ctx->slot_v2, 2 * G));
     CKC(dalloc(&ctx->slot_data, 2 * G * lp));
+    CKC(cudaMalloc((void **)&ctx->sq_ll, sizeof(uint4) * 2 * SQ_MAXG * (SQ_MAXL + 2)));
+    CKC(cudaMemset(ctx->sq_ll, 0, sizeof(uint4) * 2 * SQ_MAXG * (SQ_MAXL + 2)));
     CKC(dalloc(&ctx->sq_spill, lp * nn));
     CKC(dalloc(&ctx->bpre, lp * nn));
     CKC(dalloc(&ctx->c5, lp * nn));
@@ -646,6 +649,15 @@ extern "C" int rqrcp_get_timings(const rqrcp_ctx *ctx, rqrcp_timings *out) {
     if (!out) return -2;
     *out = ctx->last;
     return 0;
+}
+
+// RQRCP_TRACE_PANEL=n: the panel (1-based) whose steps the trace records
+static int trace_panel() {
+    static const int tp = [] {
+        const char *e = getenv("RQRCP_TRACE_PANEL");
+        return e ? std::max(1, atoi(e)) : 1;
+    }();
+    return tp;
 }
 
 static int coop_launch(rqrcp_ctx *ctx, const void *func, int grid, int threads, void **args, size_t smem) {
@@ -963,6 +975,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.tag0 = (++ctx->launch_seq) << 8;
             a.slot_v2 = ctx->slot_v2;
             a.slot_data = ctx->slot_data;
+            a.ll = ctx->sq_ll;
             a.piv = ctx->piv;
             a.tauhat = ctx->tauhat;
             a.vhat = ctx->vhat;
@@ -977,7 +990,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.swap_dst = ctx->swap_dst;
             a.swap_src = ctx->swap_src;
             a.swap_np = ctx->swap_np;
-            a.trace = (panels == 1) ? ctx->trace : nullptr;
+            a.trace = (panels == trace_panel()) ? ctx->trace : nullptr;
             a.spill = ctx->sq_spill;
             bool sq_done = false;
             {
@@ -1105,7 +1118,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.part = ctx->pn_part;
             a.rowj = ctx->pn_rowj;
             a.bar = ctx->bars + 2 * (panels - 1) + 1;
-            a.trace = (panels == 1) ? ctx->ptrace : nullptr;
+            a.trace = (panels == trace_panel()) ? ctx->ptrace : nullptr;
             int pcap = G;
             if (const char *e = getenv("RQRCP_PN_GRID")) pcap = std::max(1, std::min(G, atoi(e)));
             // ~64 rows per CTA: fewer CTAs shrink the per-column all-to-all of
@@ -1247,6 +1260,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     if (ctx->trace) {
         std::vector<unsigned long long> H((size_t)SQ_MAXG * 64 * 4);
         cudaMemcpy(H.data(), ctx->trace, sizeof(unsigned long long) * H.size(), cudaMemcpyDeviceToHost);
+        cudaMemset(ctx->trace, 0, sizeof(unsigned long long) * H.size());
         const char *names[4] = {"wait/poll+winner+householder", "apply", "publish", "->next"};
         double all[4] = {0}, worst_apply = 0;
         int ncta = 0, worst = -1;

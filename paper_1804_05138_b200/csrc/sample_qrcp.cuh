@@ -66,6 +66,7 @@ struct SqArgs {
     int nsm;              // columns per CTA held in shared memory
     int ncs;              // row stride of the shared-memory tile (>= nsm)
     double *spill;        // global scratch for the other columns (transposed, per CTA)
+    uint4 *ll;            // [2][G][SQ_MAXL + 2] tagged 16-byte units (sample_qrcp_reg.cuh)
     const double *stop_tol2;
     SqHdr *slot_hdr;      // [2][G] x hstride
     int *slot_col;        // [2][G] physical column of the candidate (written before the header)

@@ -5,10 +5,14 @@
 // arithmetic and outputs as sample_qrcp.cuh / sample_qrcp_cl.cuh (dlarfg
 // reading R-G7, squared-norm downdates with the R-G6 recompute, lowest
 // position on ties R-G5, stop rule R-G12); the per-step exchange is the grid
-// kernel's: every CTA publishes its best candidate (column in a global slot,
-// then a 16-byte header with a release store) and warp 0 of every CTA polls
-// the G headers with acquire loads, picks the winner, loads its column and
-// forms the reflector redundantly.  CTA 0 holds no columns: it stages the
+// kernel's, without fences: every CTA publishes its best candidate (header
+// and column) in a global slot in which each 32-bit half of every word
+// travels with the step's tag in one 64-bit store (two per 16-byte unit, the
+// "low-latency" flag protocol), and warp 0 of every CTA polls the G headers
+// with relaxed loads until the tags match, picks the winner, polls its
+// column the same way and forms the reflector redundantly.  A 64-bit aligned
+// store is single-copy atomic, so a matching tag proves its half is current;
+// no release/acquire fence (each costs an L2 round trip per step) is needed.  CTA 0 holds no columns: it stages the
 // reflectors and R-hat rows in shared memory and writes the outputs at the
 // end (so its shared memory is free for them).  Used for samples larger than one
 // cluster can hold in registers (C3: 16384 columns; C4: 32768 columns of
@@ -20,14 +24,31 @@
 
 namespace rq {
 
+#ifndef SQR_TRACE_DETAIL
+#define SQR_TRACE_DETAIL 0
+#endif
 constexpr int SQR_THREADS = 256;
+constexpr int SQR_UNITS = SQ_MAXL + 2;  // 16-byte units per slot: header (2) + column
+
+// unit = {lo32 | tag << 32, hi32 | tag << 32}
+RQ_DEV void ll_store(uint4 *p, unsigned long long w, unsigned tag) {
+    const unsigned long long t = (unsigned long long)tag << 32;
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};\n" ::"l"(p), "l"((w & 0xffffffffull) | t),
+                 "l"((w >> 32) | t)
+                 : "memory");
+}
+RQ_DEV bool ll_load(const uint4 *p, unsigned tag, unsigned long long &w) {
+    unsigned long long a, b;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+    w = (a & 0xffffffffull) | (b << 32);
+    return (unsigned)(a >> 32) == tag && (unsigned)(b >> 32) == tag;
+}
 
 template <int LR, int LS>
 __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs a) {
     constexpr int L = LR + LS;
     extern __shared__ __align__(16) double sq_dyn[];  // max(LS x 256, bb x L) doubles
     __shared__ __align__(16) double xs[L + 1];
-    __shared__ __align__(16) double xe[2 * L];  // (v_t, [t == j]) pairs
     __shared__ double xraw[L];
     __shared__ double wv[SQ_WARPS];
     __shared__ int wpos[SQ_WARPS], wcol[SQ_WARPS];
@@ -39,6 +60,7 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
     __shared__ int hi_n;
     __shared__ int s_piv[SQ_MAXB];
     __shared__ double s_tauh[SQ_MAXB];
+    __shared__ unsigned long long s_trace[64 * 4];  // RQRCP_TRACE phase stamps
 
     const int G = gridDim.x, g = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -100,68 +122,102 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
         }
         __syncthreads();
         if (warp == 0) {
+            uint4 *dst = a.ll + (int64_t)(par * G + g) * SQR_UNITS;
+            const unsigned tg = a.tag0 + (unsigned)step;
             if (bc >= 0) {
-                double *dst = a.slot_data + (int64_t)(par * G + g) * a.lpad;
                 const int oc = bc - (int)c_lo;
-                for (int t = lane; t < l; t += 32)
-                    __stcg(dst + t, (t < LR) ? xraw[t] : xsm[(t - LR) * SQR_THREADS + oc]);
+                for (int t = lane; t < l; t += 32) {
+                    const double xv = (t < LR) ? xraw[t] : xsm[(t - LR) * SQR_THREADS + oc];
+                    ll_store(dst + 2 + t, (unsigned long long)__double_as_longlong(xv), tg);
+                }
             }
-            if (lane == 0) a.slot_col[par * G + g] = bc;
-            __syncwarp();
-            if (lane == 0) st_release_hdr(a.slot_hdr + (int64_t)(par * G + g) * a.hstride, bv, bp, a.tag0 + (unsigned)step);
+            if (lane == 0) ll_store(dst, (unsigned long long)__double_as_longlong(bv), tg);
+            if (lane == 1) ll_store(dst + 1, (unsigned long long)(unsigned)bp | ((unsigned long long)(unsigned)bc << 32), tg);
         }
     };
 
+    if (a.trace)
+        for (int e = tid; e < 64 * 4; e += SQR_THREADS) s_trace[e] = 0ull;
     publish(0);
 
     int j = 0;
+    // phase stamps (RQRCP_TRACE): kept in shared memory, written at the end so
+    // the trace adds no global traffic to the steps it measures
+    auto stamp = [&](int ph) {
+        if (a.trace && tid == 0 && j < 64) s_trace[j * 4 + ph] = clock64();
+    };
     for (; j < a.bb; ++j) {
         const int par = j & 1;
+        stamp(0);
         // ---- 1. winner and its reflector (warp 0, redundantly per CTA) --------
         if (warp == 0) {
             const unsigned want = a.tag0 + (unsigned)j;
             constexpr int HPL = SQ_MAXG / 32;
+            const uint4 *slots = a.ll + (int64_t)(par * G) * SQR_UNITS;
             double v = -1.0;
-            int p = INT_MAX, sl = -1;
+            int p = INT_MAX, sl = -1, wc = -1;
             bool ready[HPL];
-            double hv[HPL];
-            int hp[HPL];
+            unsigned long long h0[HPL], h1[HPL];
 #pragma unroll
-            for (int u = 0; u < HPL; ++u) { ready[u] = (lane + 32 * u >= G); hv[u] = -1.0; hp[u] = INT_MAX; }
+            for (int u = 0; u < HPL; ++u) { ready[u] = (lane + 32 * u >= G); h0[u] = 0; h1[u] = 0; }
             while (true) {
                 bool all = true;
 #pragma unroll
                 for (int u = 0; u < HPL; ++u) {
                     if (!ready[u]) {
-                        unsigned tg;
-                        ld_acquire_hdr(a.slot_hdr + (int64_t)(par * G + lane + 32 * u) * a.hstride, hv[u], hp[u], tg);
-                        ready[u] = (tg == want);
+                        const uint4 *hq = slots + (int64_t)(lane + 32 * u) * SQR_UNITS;
+                        const bool r0_ = ll_load(hq, want, h0[u]);
+                        const bool r1_ = ll_load(hq + 1, want, h1[u]);
+                        ready[u] = r0_ && r1_;
                     }
                     all = all && ready[u];
                 }
                 if (__all_sync(0xffffffffu, all)) break;
             }
+#if SQR_TRACE_DETAIL
+            stamp(1);
+#endif
 #pragma unroll
             for (int u = 0; u < HPL; ++u) {
                 const int q = lane + 32 * u;
-                if (q < G && hp[u] != INT_MAX && sq_better(hv[u], hp[u], v, p)) { v = hv[u]; p = hp[u]; sl = q; }
+                const double hv = __longlong_as_double((long long)h0[u]);
+                const int hp = (int)(unsigned)(h1[u] & 0xffffffffull);
+                if (q < G && hp != INT_MAX && sq_better(hv, hp, v, p)) {
+                    v = hv; p = hp; sl = q; wc = (int)(unsigned)(h1[u] >> 32);
+                }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 const double ov = __shfl_xor_sync(0xffffffffu, v, o);
                 const int op = __shfl_xor_sync(0xffffffffu, p, o);
                 const int osl = __shfl_xor_sync(0xffffffffu, sl, o);
-                if (osl >= 0 && (sl < 0 || sq_better(ov, op, v, p))) { v = ov; p = op; sl = osl; }
+                const int owc = __shfl_xor_sync(0xffffffffu, wc, o);
+                if (osl >= 0 && (sl < 0 || sq_better(ov, op, v, p))) { v = ov; p = op; sl = osl; wc = owc; }
             }
             const bool stop = (sl < 0) || !(v > stop2);
             double xv[SQ_RPL];
-            const double *src = a.slot_data + (int64_t)(par * G + (sl >= 0 ? sl : 0)) * a.lpad;
+            {
+                const uint4 *src = slots + (int64_t)(sl >= 0 ? sl : 0) * SQR_UNITS + 2;
+                bool ok[SQ_RPL];
 #pragma unroll
-            for (int qq = 0; qq < SQ_RPL; ++qq) {
-                const int t = lane + 32 * qq;
-                xv[qq] = (!stop && t < l) ? __ldcg(src + t) : 0.0;
+                for (int qq = 0; qq < SQ_RPL; ++qq) { ok[qq] = stop || lane + 32 * qq >= l; xv[qq] = 0.0; }
+                while (true) {
+                    bool all = true;
+#pragma unroll
+                    for (int qq = 0; qq < SQ_RPL; ++qq) {
+                        if (!ok[qq]) {
+                            unsigned long long w;
+                            ok[qq] = ll_load(src + lane + 32 * qq, want, w);
+                            xv[qq] = __longlong_as_double((long long)w);
+                        }
+                        all = all && ok[qq];
+                    }
+                    if (__all_sync(0xffffffffu, all)) break;
+                }
+#if SQR_TRACE_DETAIL
+                stamp(2);
+#endif
             }
-            const int wc = (sl >= 0) ? __ldcg(a.slot_col + par * G + sl) : -1;
             if (lane == 0) { s_stop = stop; s_wpos = p; s_wcol = wc; }
             if (!stop) {
                 double sx = 0.0;
@@ -187,8 +243,6 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
                     if (t < L) {
                         const double vt = (t > j) ? xv[qq] * scal : (t == j ? 1.0 : 0.0);
                         xs[t] = vt;
-                        xe[2 * t] = vt;
-                        xe[2 * t + 1] = (t == j) ? 1.0 : 0.0;
                         xraw[t] = xv[qq];
                     }
                 }
@@ -196,6 +250,11 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
             }
         }
         __syncthreads();
+#if SQR_TRACE_DETAIL
+        stamp(3);
+#else
+        stamp(1);
+#endif
         if (s_stop) break;
         const int wp = s_wpos, wcl = s_wcol;
         const double tau = s_tau;
@@ -228,33 +287,52 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
         // ---- 2. apply H_j to this thread's column, downdate the norm ---------
         if (act && (int)pc == wcl) act = false;
         if (act) {
-            double d0 = 0.0, d1 = 0.0;
+            // w = v^T x over rows >= j (xs is zero above row j); 8-row chunks
+            // entirely above row j are skipped (uniform branches); four
+            // independent accumulators
+            double d[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
             for (int c0 = 0; c0 < LR; c0 += 8) {
                 if (j < c0 + 8) {
 #pragma unroll
                     for (int t = c0; t < c0 + 8 && t + 1 < LR; t += 2) {
                         const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
-                        d0 += v2.x * x[t];
-                        d1 += v2.y * x[t + 1];
+                        d[(t >> 1) & 3] += v2.x * x[t] + v2.y * x[t + 1];
                     }
-                    if ((LR & 1) && c0 + 8 >= LR) d0 += xs[LR - 1] * x[LR - 1];
+                    if ((LR & 1) && c0 + 8 >= LR) d[0] += xs[LR - 1] * x[LR - 1];
                 }
             }
-            for (int t = (j > LR ? j : LR); t < L; ++t) d0 += xs[t] * xsm[(t - LR) * SQR_THREADS + tid];
-            const double tw = tau * (d0 + d1);
+            if (LS > 0) {
+                int t = (j > LR ? j : LR);
+                const double *xc = xsm + tid - LR * SQR_THREADS;
+                for (; t + 3 < L; t += 4) {
+                    d[0] += xs[t] * xc[t * SQR_THREADS];
+                    d[1] += xs[t + 1] * xc[(t + 1) * SQR_THREADS];
+                    d[2] += xs[t + 2] * xc[(t + 2) * SQR_THREADS];
+                    d[3] += xs[t + 3] * xc[(t + 3) * SQR_THREADS];
+                }
+                for (; t < L; ++t) d[0] += xs[t] * xc[t * SQR_THREADS];
+            }
+            const double tw = tau * ((d[0] + d[1]) + (d[2] + d[3]));
+            // x -= tw v; bj = x(j) picked in the chunk that holds row j
             double bj = 0.0;
 #pragma unroll
             for (int c0 = 0; c0 < LR; c0 += 8) {
                 if (j < c0 + 8) {
 #pragma unroll
-                    for (int t = c0; t < c0 + 8 && t < LR; ++t) {
-                        const double2 e2 = *reinterpret_cast<const double2 *>(&xe[2 * t]);
-                        x[t] -= tw * e2.x;
-                        bj += e2.y * x[t];
+                    for (int t = c0; t < c0 + 8 && t + 1 < LR; t += 2) {
+                        const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
+                        x[t] -= tw * v2.x;
+                        x[t + 1] -= tw * v2.y;
+                    }
+                    if ((LR & 1) && c0 + 8 >= LR) x[LR - 1] -= tw * xs[LR - 1];
+                    if (j >= c0) {
+#pragma unroll
+                        for (int t = c0; t < c0 + 8 && t < LR; ++t) bj = (t == j) ? x[t] : bj;
                     }
                 }
             }
+#pragma unroll 4
             for (int t = (j > LR ? j : LR); t < L; ++t) {
                 double *p = &xsm[(t - LR) * SQR_THREADS + tid];
                 const double nv = *p - tw * xs[t];
@@ -274,11 +352,20 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
             r = rn;
             if (lpos == j) lpos = wp;
         }
+#if !SQR_TRACE_DETAIL
+        stamp(2);
+#endif
         if (j + 1 < a.bb) publish(j + 1);
+#if !SQR_TRACE_DETAIL
+        stamp(3);
+#endif
     }
     __syncthreads();
 
     // ---- results --------------------------------------------------------------
+    if (a.trace)
+        for (int e = tid; e < 64 * 4; e += SQR_THREADS)
+            a.trace[(size_t)g * 256 + e] = (e / 4 < min(j + 1, 64)) ? s_trace[e] : 0ull;
     if (have) {
 #pragma unroll
         for (int t = 0; t < LR; ++t) a.B[t + pc * a.ldb] = x[t];
