@@ -19,6 +19,7 @@
 #include "gemm_tma.cuh"
 #include "misc.cuh"
 #include "panel.cuh"
+#include "panel_cl.cuh"
 #include "philox.cuh"
 #include "sample_qrcp.cuh"
 #include "sample_qrcp_cl.cuh"
@@ -91,6 +92,7 @@ struct rqrcp_ctx {
     // cooperative limits
     int sq_max_grid = 0, pn_max_grid = 0;
     int sqc_max = 0;  // largest cluster the register-resident sample QRCP can use (0: none)
+    int pnc_max = 0;  // ... and the register-resident cluster panel kernel
     // multi-GPU (nranks > 1): NCCL communicator + exchange buffers
     ncclComm_t comm = nullptr;
     double *gsend = nullptr, *gbuf = nullptr, *pack = nullptr, *r11 = nullptr;
@@ -109,6 +111,7 @@ struct rqrcp_ctx {
     bool debug_sync = false;  // RQRCP_DEBUG_SYNC=1: synchronise after every launch
     unsigned long long *trace = nullptr;  // RQRCP_TRACE=1: per-step phase stamps of the sample QRCP
     unsigned long long *ptrace = nullptr; // ... and of the panel kernel
+    int ptrace_kind = 0;                  // 0: grid panel kernel, 1: cluster panel kernel
 };
 
 static const char *g_static_err = "no context";
@@ -557,6 +560,31 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
             if (cudaOccupancyMaxActiveClusters(&ncl, (void *)sample_qrcp_cluster_kernel<80>, &lc) == cudaSuccess &&
                 ncl >= 1)
                 ctx->sqc_max = cs;
+        }
+        cudaGetLastError();
+    }
+    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<32, 64>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<64, 64>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 65 * 8));
+    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 65 * 8));
+    {
+        ctx->pnc_max = 0;
+        for (int cs = PNC_MAXG; cs >= 1 && !ctx->pnc_max; --cs) {
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3(cs);
+            lc.blockDim = dim3(PNC_THREADS);
+            lc.dynamicSmemBytes = 64 * 65 * 8;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cs;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            int ncl = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, (void *)panel_qr_cluster_kernel<64, 64>, &lc) == cudaSuccess &&
+                ncl >= 1)
+                ctx->pnc_max = cs;
         }
         cudaGetLastError();
     }
@@ -1119,6 +1147,37 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.rowj = ctx->pn_rowj;
             a.bar = ctx->bars + 2 * (panels - 1) + 1;
             a.trace = (panels == trace_panel()) ? ctx->ptrace : nullptr;
+            // register-resident cluster kernel (panel_cl.cuh) when the panel fits
+            // one cluster: bb <= 64 and m' <= clusters x rows per CTA
+            bool pn_done = false;
+            {
+                const char *e = getenv("RQRCP_PN_CLUSTER");
+                const bool allow = !(e && e[0] == '0');
+                void (*kfn)(PanelArgs) = nullptr;
+                int64_t rc_rows = 0;
+                int bbk = 0;
+                if (bb <= 32) { kfn = panel_qr_cluster_kernel<32, 64>; rc_rows = 8 * 64; bbk = 32; }
+                else if (bb <= 64) { kfn = panel_qr_cluster_kernel<64, 64>; rc_rows = 4 * 64; bbk = 64; }
+                const int64_t cs = kfn ? (mp + rc_rows - 1) / rc_rows : 0;
+                if (allow && kfn && cs <= ctx->pnc_max) {
+                    cudaLaunchConfig_t lc = {};
+                    lc.gridDim = dim3((unsigned)cs);
+                    lc.blockDim = dim3(PNC_THREADS);
+                    lc.dynamicSmemBytes = (size_t)bbk * 65 * sizeof(double);
+                    lc.stream = st;
+                    cudaLaunchAttribute at[1];
+                    at[0].id = cudaLaunchAttributeClusterDimension;
+                    at[0].val.clusterDim.x = (unsigned)cs;
+                    at[0].val.clusterDim.y = 1;
+                    at[0].val.clusterDim.z = 1;
+                    lc.attrs = at;
+                    lc.numAttrs = 1;
+                    CK(cudaLaunchKernelEx(&lc, kfn, a));
+                    CKL();
+                    pn_done = true;
+                    if (a.trace) ctx->ptrace_kind = 1;
+                }
+            }
             int pcap = G;
             if (const char *e = getenv("RQRCP_PN_GRID")) pcap = std::max(1, std::min(G, atoi(e)));
             // ~64 rows per CTA: fewer CTAs shrink the per-column all-to-all of
@@ -1137,7 +1196,10 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             a.nsm = (int)std::min<int64_t>(rpb, kDynSmemMax / ((int64_t)bb * sizeof(double)));
             const size_t smem = (size_t)a.nsm * bb * sizeof(double);
             void *args[] = {&a};
-            rc = coop_launch(ctx, (const void *)panel_qr_kernel, grid, PN_THREADS, args, smem);
+            if (!pn_done) {
+                rc = coop_launch(ctx, (const void *)panel_qr_kernel, grid, PN_THREADS, args, smem);
+                if (a.trace) ctx->ptrace_kind = 0;
+            }
             if (rc) return rc;
         }
         const double *R11p = A + i + ljp * lda;
@@ -1293,7 +1355,9 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         }
         unsigned long long h[2 * 64 * 8];
         cudaMemcpy(h, ctx->ptrace, sizeof(h), cudaMemcpyDeviceToHost);
-        const char *pn[5] = {"gram", "barrier", "reduce", "tau+w+x", "update"};
+        const char *pn0[5] = {"gram", "barrier", "reduce", "tau+w+x", "update"};
+        const char *pn1[5] = {"gram", "push", "mbar-wait", "sum", "update+publish"};
+        const char **pn = ctx->ptrace_kind ? pn1 : pn0;
         for (int c = 0; c < 2; ++c) {
             double acc[5] = {0};
             int cnt = 0;

@@ -51,19 +51,18 @@ RQ_DEV int cl_ld_s32(unsigned addr) {
 
 template <int L>
 __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqArgs a) {
+    constexpr int RECW = (L + 2 + 1) / 2 * 2;  // pushed record: v, (pos, col) bits, the column, padded to pairs
+    constexpr int NPAIR = RECW / 2;
     extern __shared__ __align__(16) double comp[];  // CTA 0: [bb][L] winner columns (LAPACK format)
     __shared__ int s_piv[SQ_MAXB];
     __shared__ double s_tauh[SQ_MAXB];
-    __shared__ double slot_v[2];
-    __shared__ int slot_pos[2], slot_col[2];
-    __shared__ double slot_x[2][SQC_L];
-    __shared__ __align__(16) double xs[SQC_L];
-    __shared__ __align__(16) double xe[2 * SQC_L];  // (v_t, [t == j]) pairs
-    __shared__ double xraw[SQC_L];  // the winner column (rows < j: R-hat entries)
+    __shared__ __align__(16) double rec[RECW];                   // this CTA's candidate record
+    __shared__ __align__(16) double recv[2][SQC_MAXG][RECW];     // pushed records (slot = source CTA)
+    __shared__ __align__(16) double vw[SQ_WARPS][SQC_L];         // per-warp copy of the reflector
+    __shared__ __align__(8) unsigned long long mbar[2];
     __shared__ double wv[SQ_WARPS];
     __shared__ int wpos[SQ_WARPS], wcol[SQ_WARPS];
-    __shared__ double s_tau, s_beta, s_alpha;
-    __shared__ int s_wpos, s_wcol, s_stop, s_np;
+    __shared__ int s_np;
     __shared__ int64_t low[SQ_MAXB];
     __shared__ int hi_pos[SQ_MAXB];
     __shared__ int64_t hi_phys[SQ_MAXB];
@@ -78,13 +77,20 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
     const int64_t c_lo = min(nn, (int64_t)g * cpb), c_hi = min(nn, c_lo + cpb);
     const bool have = tid < (int)(c_hi - c_lo);
     const int64_t pc = c_lo + tid;  // this thread's physical column
-    // every CTA takes part in every barrier, so an early exit is uniform
+    // every CTA takes part in every exchange, so an early exit is uniform
     const bool noop = (*a.status != 0 || *a.done);
     if (noop) {
         if (g == 0 && tid == 0) { *a.bb_eff = 0; *a.swap_np = 0; }
         return;
     }
     const double stop2 = *a.stop_tol2;
+    const unsigned mb0 = (unsigned)__cvta_generic_to_shared(&mbar[0]);
+    const unsigned step_bytes = (unsigned)(G * RECW * sizeof(double));
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb0) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb0 + 8) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
 
     double x[L];
 #pragma unroll
@@ -100,8 +106,16 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
         for (int q = tid; q < a.bb; q += SQC_THREADS) low[q] = q;
         if (tid == 0) hi_n = 0;
     }
+    // every CTA's mbarriers are initialised before anyone pushes
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    cl_wait();
+    if (tid == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb0), "r"(step_bytes) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb0 + 8), "r"(step_bytes) : "memory");
+    }
 
-    // CTA-best candidate -> this CTA's slot of parity (step & 1); then arrive
+    // CTA-best candidate (value, position, physical column, its l entries),
+    // pushed into slot g of every CTA's receive buffer of parity (step & 1)
     auto publish = [&](int step) {
         const int par = step & 1;
         double v = act ? r : -1.0;
@@ -121,15 +135,28 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
         for (int w = 1; w < SQ_WARPS; ++w)
             if (sq_better(wv[w], wpos[w], bv, bp)) { bv = wv[w]; bp = wpos[w]; bc = wcol[w]; }
         if (act && (int)pc == bc) {
+            double2 *r2 = reinterpret_cast<double2 *>(&rec[2]);
 #pragma unroll
-            for (int t = 0; t < L; ++t) slot_x[par][t] = x[t];
+            for (int t = 0; t + 1 < L; t += 2) r2[t / 2] = make_double2(x[t], x[t + 1]);
+            if (L & 1) rec[2 + L - 1] = x[L - 1];
         }
         if (tid == 0) {
-            slot_v[par] = bv;
-            slot_pos[par] = bp;
-            slot_col[par] = bc;
+            rec[0] = bv;
+            rec[1] = __longlong_as_double(((long long)bp << 32) | (unsigned)bc);
         }
-        cl_arrive();
+        __syncthreads();
+        const unsigned lm = mb0 + 8 * par;
+        for (int e = tid; e < G * NPAIR; e += SQC_THREADS) {
+            const int d = e / NPAIR, w = 2 * (e % NPAIR);
+            const double2 val = *reinterpret_cast<const double2 *>(&rec[w]);
+            const unsigned la = (unsigned)__cvta_generic_to_shared(&recv[par][g][w]);
+            unsigned ra, rm;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(la), "r"(d));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rm) : "r"(lm), "r"(d));
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(ra),
+                         "d"(val.x), "d"(val.y), "r"(rm)
+                         : "memory");
+        }
     };
 
     publish(0);
@@ -141,80 +168,82 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
     for (; j < a.bb; ++j) {
         const int par = j & 1;
         stamp(0);
-        cl_wait();
-        // ---- 1. winner and its reflector (warp 0, redundantly per CTA) --------
-        if (warp == 0) {
-            double v = -1.0;
-            int p = INT_MAX, sl = -1;
-            if (lane < G) {
-                v = cl_ld_f64(cl_map(&slot_v[par], lane));
-                p = cl_ld_s32(cl_map(&slot_pos[par], lane));
-                if (p != INT_MAX) sl = lane;
-                else v = -1.0;
-            }
+        {
+            unsigned ok = 0;
+            const unsigned ph = (unsigned)((j >> 1) & 1);
+            while (!ok)
+                asm volatile(
+                    "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+                    " selp.u32 %0, 1, 0, p;\n}\n"
+                    : "=r"(ok)
+                    : "r"(mb0 + 8 * par), "r"(ph)
+                    : "memory");
+        }
+        // step j+2 re-arms this mbarrier: its bytes can only come after every
+        // CTA received this CTA's step j+1 record (sent after all reads below)
+        if (tid == 0 && j + 2 < a.bb)
+            asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb0 + 8 * par),
+                         "r"(step_bytes)
+                         : "memory");
+        // ---- 1. winner and its reflector, redundantly in EVERY warp (local
+        //      shared memory only: same bits everywhere, no CTA barrier) ------
+        double v = -1.0;
+        int p = INT_MAX, sl = -1, wc = -1;
+        if (lane < G) {
+            v = recv[par][lane][0];
+            const long long pcb = __double_as_longlong(recv[par][lane][1]);
+            p = (int)(pcb >> 32);
+            wc = (int)(unsigned)(pcb & 0xffffffffll);
+            if (p != INT_MAX) sl = lane;
+            else v = -1.0;
+        }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-                const int op = __shfl_xor_sync(0xffffffffu, p, o);
-                const int osl = __shfl_xor_sync(0xffffffffu, sl, o);
-                if (osl >= 0 && (sl < 0 || sq_better(ov, op, v, p))) { v = ov; p = op; sl = osl; }
-            }
-            const bool stop = (sl < 0) || !(v > stop2);
-            double xv[SQ_RPL];
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int op = __shfl_xor_sync(0xffffffffu, p, o);
+            const int osl = __shfl_xor_sync(0xffffffffu, sl, o);
+            const int owc = __shfl_xor_sync(0xffffffffu, wc, o);
+            if (osl >= 0 && (sl < 0 || sq_better(ov, op, v, p))) { v = ov; p = op; sl = osl; wc = owc; }
+        }
+        const bool stop = (sl < 0) || !(v > stop2);
+        stamp(1);
+        if (stop) break;  // uniform: every warp of every CTA sees the same records
+        const int wp = p, wcl = wc;
+        const double *wx = &recv[par][sl][2];  // the winner column (rows < j: R-hat entries)
+        double xv[SQ_RPL];
+        double sx = 0.0, alpha = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < SQ_RPL; ++qq) {
+            const int t = lane + 32 * qq;
+            xv[qq] = (t < L) ? wx[t] : 0.0;
+            if (t > j && t < L) sx += xv[qq] * xv[qq];
+        }
+        alpha = wx[j];
+        sx = warp_sum(sx);
+        double tau = 0.0, beta = alpha, scal = 0.0;
+        if (sx != 0.0) {
+            const double nrm = sqrt(alpha * alpha + sx);
+            beta = (alpha >= 0.0) ? -nrm : nrm;
+            tau = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        // this warp's copy of the reflector (rows < j zero: the apply needs no predicates)
+        double *xs = vw[warp];
+#pragma unroll
+        for (int qq = 0; qq < SQ_RPL; ++qq) {
+            const int t = lane + 32 * qq;
+            if (t < L) xs[t] = (t > j) ? xv[qq] * scal : (t == j ? 1.0 : 0.0);
+        }
+        __syncwarp();
+        // ---- outputs (staged in CTA 0's shared memory, written at the end) -----
+        if (g == 0 && warp == 0) {
+            // column j in LAPACK format: R-hat above the diagonal, beta, v below
 #pragma unroll
             for (int qq = 0; qq < SQ_RPL; ++qq) {
                 const int t = lane + 32 * qq;
-                xv[qq] = (!stop && t < l) ? cl_ld_f64(cl_map(&slot_x[par][t], sl)) : 0.0;
+                if (t < L) comp[j * L + t] = (t < j) ? xv[qq] : (t == j ? beta : xs[t]);
             }
-            const int wc = (sl >= 0) ? cl_ld_s32(cl_map(&slot_col[par], sl)) : -1;
-            if (lane == 0) {
-                s_stop = stop;
-                s_wpos = p;
-                s_wcol = wc;
-            }
-            if (!stop) {
-                double sx = 0.0;
-#pragma unroll
-                for (int qq = 0; qq < SQ_RPL; ++qq) {
-                    const int t = lane + 32 * qq;
-                    if (t > j) sx += xv[qq] * xv[qq];
-                    if (t == j) s_alpha = xv[qq];
-                }
-                sx = warp_sum(sx);
-                __syncwarp();
-                const double alpha = s_alpha;
-                double tau = 0.0, beta = alpha, scal = 0.0;
-                if (sx != 0.0) {
-                    const double nrm = sqrt(alpha * alpha + sx);
-                    beta = (alpha >= 0.0) ? -nrm : nrm;
-                    tau = (beta - alpha) / beta;
-                    scal = 1.0 / (alpha - beta);
-                }
-                // reflector rows >= j; rows < j zeroed so the apply needs no predicates
-#pragma unroll
-                for (int qq = 0; qq < SQ_RPL; ++qq) {
-                    const int t = lane + 32 * qq;
-                    if (t < L) {
-                        const double vt = (t > j) ? xv[qq] * scal : (t == j ? 1.0 : 0.0);
-                        xs[t] = vt;
-                        xe[2 * t] = vt;
-                        xe[2 * t + 1] = (t == j) ? 1.0 : 0.0;
-                        xraw[t] = xv[qq];
-                    }
-                }
-                if (lane == 0) { s_tau = tau; s_beta = beta; }
-            }
-        }
-        __syncthreads();
-        stamp(1);
-        if (s_stop) break;
-        const int wp = s_wpos, wcl = s_wcol;
-        const double tau = s_tau;
-        // ---- outputs (staged in CTA 0's shared memory, written at the end) -----
-        if (g == 0) {
-            // column j in LAPACK format: R-hat above the diagonal, beta, v below
-            for (int t = tid; t < L; t += SQC_THREADS) comp[j * L + t] = (t < j) ? xraw[t] : (t == j ? s_beta : xs[t]);
-            if (tid == 0) { s_piv[j] = wp; s_tauh[j] = tau; }
+            if (lane == 0) { s_piv[j] = wp; s_tauh[j] = tau; }
         }
         if (g == 0 && warp == SQ_WARPS - 1) {
             const int64_t q = low[j];
@@ -243,30 +272,38 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
         if (act) {
             // w = v^T x over rows >= j (xs is zero above row j); 8-row chunks
             // entirely above row j are skipped (uniform branches)
-            double d0 = 0.0, d1 = 0.0;
+            // four independent accumulators (row t goes to accumulator t mod 4)
+            double d[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
             for (int c0 = 0; c0 < L; c0 += 8) {
                 if (j < c0 + 8) {
 #pragma unroll
                     for (int t = c0; t < c0 + 8 && t + 1 < L; t += 2) {
                         const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
-                        d0 += v2.x * x[t];
-                        d1 += v2.y * x[t + 1];
+                        d[t & 3] += v2.x * x[t];
+                        d[(t + 1) & 3] += v2.y * x[t + 1];
                     }
-                    if ((L & 1) && c0 + 8 >= L) d0 += xs[L - 1] * x[L - 1];
+                    if ((L & 1) && c0 + 8 >= L) d[(L - 1) & 3] += xs[L - 1] * x[L - 1];
                 }
             }
-            const double tw = tau * (d0 + d1);
-            // x -= tw v; bj = x(j) through the one-hot half of xe = (v_t, [t == j])
+            const double tw = tau * ((d[0] + d[1]) + (d[2] + d[3]));
+            // x -= tw v (v is zero above row j); bj = the updated x(j), selected
+            // inside the one 8-row chunk that holds row j (uniform branch)
             double bj = 0.0;
 #pragma unroll
             for (int c0 = 0; c0 < L; c0 += 8) {
                 if (j < c0 + 8) {
 #pragma unroll
-                    for (int t = c0; t < c0 + 8 && t < L; ++t) {
-                        const double2 e2 = *reinterpret_cast<const double2 *>(&xe[2 * t]);
-                        x[t] -= tw * e2.x;
-                        bj += e2.y * x[t];
+                    for (int t = c0; t < c0 + 8 && t + 1 < L; t += 2) {
+                        const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
+                        x[t] -= tw * v2.x;
+                        x[t + 1] -= tw * v2.y;
+                    }
+                    if ((L & 1) && c0 + 8 >= L) x[L - 1] -= tw * xs[L - 1];
+                    if (j >= c0) {
+#pragma unroll
+                        for (int t = c0; t < c0 + 8 && t < L; ++t)
+                            if (t == j) bj = x[t];
                     }
                 }
             }
@@ -285,8 +322,8 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
         if (j + 1 < a.bb) publish(j + 1);
         stamp(3);
     }
-    // the last reads of every CTA's slots precede this barrier
-    cl_arrive();
+    // no CTA leaves while pushes into it may be in flight
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     cl_wait();
 
     // ---- results --------------------------------------------------------------

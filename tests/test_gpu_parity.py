@@ -23,7 +23,7 @@ RES_ATOL = 1e-12
 def ctx():
     """Default context: grid-wide (cooperative) sample-QRCP / panel kernels."""
     import paper_1804_05138_b200 as rq
-    c = rq.RQRCP(max_m=4200, max_n=4200, max_b=128, max_p=32)
+    c = rq.RQRCP(max_m=5000, max_n=4200, max_b=128, max_p=32)
     yield c
     c.close()
 
@@ -199,7 +199,7 @@ def test_argument_errors(ctx):
     assert call(h, A.data_ptr(), 10, 10, 8, 4, 2, 2, 0, None, ta.data_ptr(), ctypes.byref(r)) == -10
     assert call(h, A.data_ptr(), 10, 10, 8, 4, 2, 2, 0, jp.data_ptr(), None, ctypes.byref(r)) == -11
     assert call(h, A.data_ptr(), 10, 10, 8, 4, 2, 2, 0, jp.data_ptr(), ta.data_ptr(), None) == -12
-    big = L.rqrcp_factor(h, A.data_ptr(), 5000, 5000, 8, 4, 2, 2, 0, jp.data_ptr(), ta.data_ptr(), ctypes.byref(r))
+    big = L.rqrcp_factor(h, A.data_ptr(), 6000, 6000, 8, 4, 2, 2, 0, jp.data_ptr(), ta.data_ptr(), ctypes.byref(r))
     assert big == rq.RQRCP_E_WORKSPACE
 
 
@@ -261,6 +261,30 @@ def test_sample_qrcp_register_grid(ctx, name, kind, m, n, k, b, p, seed):
         g = gpu_factor(ctx, A, k, b, p, seed)
     finally:
         os.environ.pop("RQRCP_SQ_CLUSTER", None)
+    compare(A, g, o, k)
+
+
+# ---- panel kernels: the register-resident cluster kernel (panel_cl.cuh) is the
+# default when bb <= 64 and m' fits one cluster (256 rows per CTA at bb <= 64,
+# 512 at bb <= 32, <= 16 CTAs); RQRCP_PN_CLUSTER=0 forces the cooperative grid
+# kernel (panel.cuh) everywhere.  Both are checked against the oracle.
+PN_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "wide", "odd", "kfull", "b1p0")] + [
+    ("pncl_tall32", "iid", 5000, 300, 96, 32, 8, 24),   # 10 CTAs of 512 rows, ragged last
+    ("pncl_4096", "lowrank", 4096, 700, 192, 64, 10, 25),  # 16 CTAs of 256 rows
+]
+
+
+@pytest.mark.parametrize("cluster", ["1", "0"], ids=["cluster", "grid"])
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", PN_CASES, ids=[c[0] for c in PN_CASES])
+def test_panel_kernels(ctx, cluster, name, kind, m, n, k, b, p, seed):
+    import os
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    o = oracle.rqrcp(A, k, b, p, seed=seed)
+    os.environ["RQRCP_PN_CLUSTER"] = cluster
+    try:
+        g = gpu_factor(ctx, A, k, b, p, seed)
+    finally:
+        os.environ.pop("RQRCP_PN_CLUSTER", None)
     compare(A, g, o, k)
 
 
