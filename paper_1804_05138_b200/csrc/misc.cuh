@@ -70,69 +70,32 @@ __global__ void swap_scatter_kernel(double *A, int64_t lda, int64_t m, int64_t *
 
 // ---------------------------------------------------------------------------
 // S6 sample update, Eq. (4) (readings R-G1..G3, R-G20):
-//   Omega-hat11 = R-hat11 R11^{-1}   (b x b upper triangular)
+//   Omega-hat11 = R-hat11 R11^{-1}   (b x b upper triangular; tri.cuh)
 //   B_next(0:bb, c) = R-hat12(:, c) - Omega-hat11 R12(:, c)
 //   B_next(bb:l, c) = R-hat22(:, c);  rows l..lpad-1 = 0
-// R-hat12/22 are read from the physical sample columns perm[bb + c].
-// Skipped (no-op) when the panel ended early (bb_eff < bb).
+// R-hat12/22 are read from the physical sample columns through the position
+// map perm written by the sample QRCP.  C = Omega-hat11 R12 (bbpad x n'') comes
+// from a DMMA contraction; this kernel forms
+// B_next(r, c) = R-hat12(r, src) - C(r, c) for r < bb, copies the R-hat22 rows
+// and zeroes rows l..lpad-1.  Local output column c = this rank's trailing
+// column lj0 + c (global column j = dist_global(lj0 + c), position j - i in the
+// replicated sample); P = 1: j = lj0 + c with lj0 = i + bb.
 // ---------------------------------------------------------------------------
-// Omega-hat11 = R-hat11 R11^{-1}: x^T R11 = rhat11(r, :) for every row r, one
-// thread per row, the solution kept in shared memory (upper triangular).
-__global__ void omhat_kernel(const double *rhat11, const double *A /* &A[i + i lda] */, int64_t lda, int bb,
-                             int bbpad, const int *bb_eff, double *omhat) {
-    extern __shared__ double oh[];  // bbpad x bbpad, oh[r + c*bbpad]
+__global__ void sample_update4_kernel(const double *Bold, int64_t ldb, const int64_t *perm, const double *Cm,
+                                      int64_t ldc, int bb, int l, int lpad, int64_t npl, const int *bb_eff,
+                                      double *Bnew, int64_t ldn, int64_t i, int64_t lj0, int b, int P, int rank) {
     if (*bb_eff != bb) return;
-    __shared__ double dinv[128];
-    for (int c = threadIdx.x; c < bb; c += blockDim.x) dinv[c] = 1.0 / A[c + (int64_t)c * lda];
-    __syncthreads();
-    for (int c = 0; c < bb; ++c) {
-        // column c of A's R11 is read by every thread: broadcast via L1
-        for (int r = threadIdx.x; r <= c; r += blockDim.x) {
-            double s = rhat11[r + (int64_t)c * bbpad];
-            for (int q = r; q < c; ++q) s -= oh[r + q * bbpad] * __ldg(A + q + (int64_t)c * lda);
-            oh[r + c * bbpad] = s * dinv[c];
-        }
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < bbpad * bbpad; e += blockDim.x) {
-        const int r = e % bbpad, c = e / bbpad;
-        omhat[e] = (r <= c && c < bb) ? oh[e] : 0.0;
-    }
-}
-
-constexpr int SU_COLS = 16;
-// Local output column c = this rank's trailing column lj0 + c (global column
-// j = dist_global(lj0 + c), position j - i in the replicated sample).  P = 1:
-// j = lj0 + c with lj0 = i + bb.
-__global__ void __launch_bounds__(256) sample_update_kernel(const double *Bold, int64_t ldb, const int64_t *perm,
-                                                            const double *omhat, int bbpad,
-                                                            const double *R12 /* &A[i + lj0 lda] */, int64_t lda,
-                                                            int bb, int l, int lpad, int64_t npl, const int *bb_eff,
-                                                            double *Bnew, int64_t ldn, int64_t i, int64_t lj0, int b,
-                                                            int P, int rank) {
-    if (*bb_eff != bb) return;
-    __shared__ double r12[128 * SU_COLS];
-    const int64_t c0 = (int64_t)blockIdx.x * SU_COLS;
-    const int ncols = (int)min((int64_t)SU_COLS, npl - c0);
-    for (int e = threadIdx.x; e < bb * ncols; e += blockDim.x) {
-        const int q = e % bb, c = e / bb;
-        r12[q + c * 128] = R12[q + (c0 + c) * lda];
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < lpad * ncols; e += blockDim.x) {
-        const int r = e % lpad, c = e / lpad;
-        const int64_t lj = lj0 + c0 + c;
+    const int64_t total = (int64_t)lpad * npl;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(e % lpad);
+        const int64_t c = e / lpad;
+        const int64_t lj = lj0 + c;
         const int64_t j = ((lj / b) * P + rank) * b + lj % b;  // global column (dist_global)
         const int64_t src = perm[j - i];
         double v = 0.0;
-        if (r < bb) {
-            double s = 0.0;
-            for (int q = r; q < bb; ++q) s += omhat[r + (int64_t)q * bbpad] * r12[q + c * 128];
-            v = Bold[r + src * ldb] - s;
-        } else if (r < l) {
-            v = Bold[r + src * ldb];
-        }
-        Bnew[r + (c0 + c) * ldn] = v;
+        if (r < bb) v = Bold[r + src * ldb] - Cm[r + c * ldc];
+        else if (r < l) v = Bold[r + src * ldb];
+        Bnew[r + c * ldn] = v;
     }
 }
 
@@ -141,7 +104,7 @@ __global__ void __launch_bounds__(256) sample_update_kernel(const double *Bold, 
 // with B2 the pre-QRCP sample's columns in pivoted order (perm[bb + ...]) and
 // C = Omega-bar_1 R12 (l x n'') computed by a DMMA contraction; this kernel
 // forms B2 - C for this rank's local trailing columns (same mapping as
-// sample_update_kernel).  Rows l..lpad-1 are 0.
+// sample_update4_kernel).  Rows l..lpad-1 are 0.
 // ---------------------------------------------------------------------------
 __global__ void sample_update5_kernel(const double *Bpre, int64_t ldb, const int64_t *perm, const double *Cm,
                                       int64_t ldc, int bb, int l, int lpad, int64_t npl, const int *bb_eff,

@@ -549,6 +549,7 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
             cudaLaunchConfig_t lc = {};
             lc.gridDim = dim3(cs);
             lc.blockDim = dim3(SQC_THREADS);
+            lc.dynamicSmemBytes = 64 * 80 * 8;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeClusterDimension;
             at[0].val.clusterDim.x = cs;
@@ -1278,9 +1279,13 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
                     CKL();
                 }
             } else if (npl > 0) {
-                sample_update_kernel<<<(unsigned)((npl + SU_COLS - 1) / SU_COLS), 256, 0, st>>>(
-                    ctx->bs[cur], lpad, ctx->perm, ctx->omhat, bbpad, A + i + lj0 * lda, lda, bb, l, lpad, npl,
-                    bb_eff, udst, lpad, i, lj0, b, P, me);
+                // C = Omega-hat11 R12 (DMMA; omhat holds Omega-hat11^T), then the
+                // gather B_next = [R-hat12 - C; R-hat22] (Eq. (4))
+                rc = gemm_skinny(ctx, bbpad, npl, bb, ctx->omhat, bbpad, A + i + lj0 * lda, lda, ctx->c5, lpad);
+                if (rc) return rc;
+                sample_update4_kernel<<<grid_for((int64_t)lpad * npl, 256, G), 256, 0, st>>>(
+                    ctx->bs[cur], lpad, ctx->perm, ctx->c5, lpad, bb, l, lpad, npl, bb_eff, udst, lpad, i, lj0, b, P,
+                    me);
                 CKL();
             }
             if (P > 1) {

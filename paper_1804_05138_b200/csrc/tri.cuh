@@ -7,7 +7,9 @@
 //     Written negated (Tneg = -T) for the W2 = -T^T W contraction.
 //  block 1: Omega-hat11 = R-hat11 R11^{-1} (Eq. (4), reading
 //     R-G20): R11^{-1} by the same doubling (inverse 8x8 blocks, then
-//     B <- -A^{-1} B D^{-1}), then the upper-triangular product.
+//     B <- -A^{-1} B D^{-1}), then the upper-triangular product, written
+//     TRANSPOSED (omhat[c + r bbpad] = Omega-hat11(r, c)) for the DMMA product
+//     Omega-hat11 R12 of the sample update.
 //
 // One CTA each, run on a side stream concurrently with W = V^T A22 (neither
 // result is needed before W2 = -T^T W / the sample update).  Entries beyond
@@ -153,7 +155,7 @@ __global__ void __launch_bounds__(TRI_THREADS) tri_kernel(const double *ybuf /* 
             double acc = 0.0;
             if (r <= c && c < bb)
                 for (int q = r; q <= c; ++q) acc += rhat11[r + (int64_t)q * bbpad] * M[q + c * ld];
-            omhat[e] = acc;
+            omhat[c + r * bbpad] = acc;  // stored transposed: the K-contiguous X of C = X^T R12
         }
     }
 }
