@@ -21,9 +21,8 @@
 //      slot of every CTA's receive buffer with st.async (DSMEM), completing
 //      bytes on the receiver's mbarrier; CTA 0 pushes row j the same way;
 //   3. each CTA waits on its own mbarrier (no cluster barrier, no fence, no
-//      remote loads), sums the G partials in CTA order (identical bits in
-//      every CTA) and evaluates dlarfg redundantly: beta, tau,
-//      scal = 1/(alpha - beta);
+//      remote loads), sums the G partials by a fixed tree (identical bits in
+//      every CTA); thread j evaluates dlarfg: beta, tau, scal = 1/(alpha - beta);
 //   4. column c > j: w_c = tau (a_jc + scal g_c); a_rc -= (w_c scal) x_r (x is
 //      zero at rows <= j).  The row-j result a_jc - w_c is final, so CTA 0
 //      keeps it in shared memory (Rrow) instead of patching the register;
@@ -75,6 +74,17 @@ RQ_DEV void st_async_f64(unsigned raddr, double v, unsigned rmbar) {
                  : "memory");
 }
 
+// pairwise tree sum of N (power of two) values in a fixed order
+template <int N>
+RQ_DEV double tree_sum(double (&v)[N]) {
+    static_assert((N & (N - 1)) == 0, "power of two");
+#pragma unroll
+    for (int w = N / 2; w >= 1; w >>= 1)
+#pragma unroll
+        for (int i = 0; i < w; ++i) v[i] = v[2 * i] + v[2 * i + 1];
+    return v[0];
+}
+
 // av[j] for a runtime j < 2^LOG (binary select tree on the bits of j)
 template <int N>
 RQ_DEV double select_rt(const double (&av)[N], int j) {
@@ -90,33 +100,37 @@ RQ_DEV double select_rt(const double (&av)[N], int j) {
     return s[0];
 }
 
-template <int BB, int RPT>
+template <int BB, int RPT, int CPT = 1>
 __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelArgs a) {
-    constexpr int RG = PNC_THREADS / BB;  // row groups
+    constexpr int CG = BB / CPT;          // column groups (CPT adjacent columns per thread)
+    constexpr int RG = PNC_THREADS / CG;  // row groups
     constexpr int RC = RG * RPT;          // rows per CTA
-    constexpr int LDS = RPT + 1;          // staging stride (conflict-free column reads)
-    static_assert(BB % 32 == 0 && RG >= 1 && RPT >= BB, "a warp is 32 columns of one row group; R rows in rg 0");
-    extern __shared__ __align__(16) double stage[];  // [BB][LDS] staging, then Rrow [BB][BB] (CTA 0)
+    constexpr int LDS = RPT + 1;          // staging stride
+    constexpr int PG = PNC_THREADS / BB;  // push groups (thread -> (push group, column))
+    static_assert(CG % 32 == 0 && RG >= 1, "a warp is 32 column groups of one row group");
+    static_assert(RC >= BB, "the R rows (0..bb-1) live in CTA 0");
+    // dynamic: max(BB * LDS, BB * BB) doubles: [BB][LDS] staging, then Rrow [BB][BB] (CTA 0)
+    extern __shared__ __align__(16) double stage[];
     __shared__ __align__(16) double xs[2][RC];       // masked column j (rows > j), double buffered
-    __shared__ double part[RG][BB];
+    __shared__ __align__(16) double part[RG][BB];
     __shared__ double rj_s[BB];
     __shared__ __align__(16) double recv[2][PNC_MAXG][BB];  // pushed CTA partials (slot = source CTA)
     __shared__ __align__(16) double recv_rj[2][BB];          // pushed row j (from CTA 0)
     __shared__ __align__(8) unsigned long long mbar[2];
     __shared__ double gsum[BB], rjv[BB];
     __shared__ double scal_s[BB], beta_s[BB];
+    __shared__ double s_hh[2];  // this step's tau, scal
 
     if (a.skip && *a.skip == 0) return;  // uniform: the CholeskyQR2 path already factored the panel
     const int G = gridDim.x;
     const int g = (int)cl_rank();
     const int tid = threadIdx.x;
-    const int c = tid % BB, rg = tid / BB;
+    const int cg = tid % CG, rg = tid / CG;
     const int bb = a.bb;
     const int bbe = *a.bb_eff;
     const int64_t mp = a.mp, lda = a.lda;
     const int64_t cta_r0 = (int64_t)g * RC;
-    const int rowbase = (int)(cta_r0 + rg * RPT);  // panel row of av[0]
-    const bool top = (rowbase == 0);               // CTA 0, row group 0: rows 0..RPT-1 (warp-uniform)
+    const int rowbase = (int)(cta_r0 + rg * RPT);  // panel row of av[.][0]
     double *Rrow = stage;                          // CTA 0: Rrow[j * BB + c] = R(j, c), c > j
 
     const unsigned mb0 = (unsigned)__cvta_generic_to_shared(&mbar[0]);
@@ -126,7 +140,7 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
         mbar_init(mb0 + 8, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    double av[RPT];
+    double av[CPT][RPT];
     // ---- load: coalesced column reads into the staging buffer, one row group at a time
     for (int q = 0; q < RG; ++q) {
         const int64_t r0 = cta_r0 + (int64_t)q * RPT;
@@ -137,7 +151,9 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
         __syncthreads();
         if (rg == q) {
 #pragma unroll
-            for (int t = 0; t < RPT; ++t) av[t] = stage[c * LDS + t];
+            for (int k = 0; k < CPT; ++k)
+#pragma unroll
+                for (int t = 0; t < RPT; ++t) av[k][t] = stage[(cg * CPT + k) * LDS + t];
         }
         __syncthreads();
     }
@@ -148,58 +164,84 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
         mbar_expect_tx(mb0, step_bytes);      // step 0
         mbar_expect_tx(mb0 + 8, step_bytes);  // step 1
     }
-    auto publish_x = [&](int col, int buf) {  // owners of column `col`: x masked to rows > col
-        if (c == col) {
-            double2 *x2 = reinterpret_cast<double2 *>(&xs[buf][rg * RPT]);
-            if (rowbase > col) {
+    // owners of column `col`: x masked to rows > col.  Each of the CPT columns
+    // is stored under its own predicate (no register-array selection).
+    auto publish_x = [&](int col, int buf) {
+        if (col / CPT != cg) return;
+        const int kk = col % CPT;
+        double2 *x2 = reinterpret_cast<double2 *>(&xs[buf][rg * RPT]);
+        if (rowbase > col) {
 #pragma unroll
-                for (int t = 0; t < RPT; t += 2) x2[t / 2] = make_double2(av[t], av[t + 1]);
-            } else {
+            for (int k = 0; k < CPT; ++k)
+                if (k == kk) {
 #pragma unroll
-                for (int t = 0; t < RPT; t += 2)
-                    x2[t / 2] = make_double2((rowbase + t > col) ? av[t] : 0.0, (rowbase + t + 1 > col) ? av[t + 1] : 0.0);
-            }
+                    for (int t = 0; t < RPT; t += 2) x2[t / 2] = make_double2(av[k][t], av[k][t + 1]);
+                }
+        } else {
+#pragma unroll
+            for (int k = 0; k < CPT; ++k)
+                if (k == kk) {
+#pragma unroll
+                    for (int t = 0; t < RPT; t += 2)
+                        x2[t / 2] = make_double2((rowbase + t > col) ? av[k][t] : 0.0,
+                                                 (rowbase + t + 1 > col) ? av[k][t + 1] : 0.0);
+                }
         }
     };
     if (bbe > 0) publish_x(0, 0);
 
     const int tsel = (g == 0) ? 0 : (g == G - 1 ? 1 : -1);
+    const int pq = tid / BB, pc = tid % BB;  // push mapping
     for (int j = 0; j < bbe; ++j) {
         auto stamp = [&](int ph) {
             if (a.trace && tsel >= 0 && tid == 0 && j < 64) a.trace[((size_t)tsel * 64 + j) * 8 + ph] = clock64();
         };
         stamp(0);
         const int par = j & 1;
+        const bool rowj_here = (j >= rowbase && j < rowbase + RPT);  // warp-uniform
         __syncthreads();  // xs[par] published
-        // ---- 1. partial Gram entry over this thread's rows -----------------
+        // ---- 1. partial Gram entries over this thread's rows ----------------
         {
             const double2 *x2 = reinterpret_cast<const double2 *>(&xs[par][rg * RPT]);
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            double s[CPT][2];
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) s[k][0] = s[k][1] = 0.0;
+            double s2[CPT][2];
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) s2[k][0] = s2[k][1] = 0.0;
 #pragma unroll
             for (int t = 0; t < RPT; t += 4) {
                 const double2 u = x2[t / 2], v = x2[t / 2 + 1];
-                s0 = fma(av[t], u.x, s0);
-                s1 = fma(av[t + 1], u.y, s1);
-                s2 = fma(av[t + 2], v.x, s2);
-                s3 = fma(av[t + 3], v.y, s3);
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) {
+                    s[k][0] = fma(av[k][t], u.x, s[k][0]);
+                    s[k][1] = fma(av[k][t + 1], u.y, s[k][1]);
+                    s2[k][0] = fma(av[k][t + 2], v.x, s2[k][0]);
+                    s2[k][1] = fma(av[k][t + 3], v.y, s2[k][1]);
+                }
             }
-            part[rg][c] = (s0 + s1) + (s2 + s3);
-            if (top) rj_s[c] = select_rt(av, j);  // row j = av[j] in CTA 0's row group 0
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) part[rg][cg * CPT + k] = (s[k][0] + s[k][1]) + (s2[k][0] + s2[k][1]);
+            if (rowj_here) {
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) rj_s[cg * CPT + k] = select_rt(av[k], j - rowbase);
+            }
         }
         stamp(1);
         __syncthreads();
         // ---- 2. CTA partial (and row j) pushed into every CTA's slot --------
         {
-            double s = part[0][c];
+            double pv[RG];
 #pragma unroll
-            for (int q = 1; q < RG; ++q) s += part[q][c];
-            const unsigned la = (unsigned)__cvta_generic_to_shared(&recv[par][g][c]);
-            const unsigned lr = (unsigned)__cvta_generic_to_shared(&recv_rj[par][c]);
+            for (int q = 0; q < RG; ++q) pv[q] = part[q][pc];
+            const double sum = tree_sum(pv);
+            const unsigned la = (unsigned)__cvta_generic_to_shared(&recv[par][g][pc]);
+            const unsigned lr = (unsigned)__cvta_generic_to_shared(&recv_rj[par][pc]);
             const unsigned lm = mb0 + 8 * par;
-            const double r = rj_s[c];
-            for (int d = rg; d < G; d += RG) {
+            const double r = rj_s[pc];
+            for (int d = pq; d < G; d += PG) {
                 const unsigned rm = cl_map_u32(lm, d);
-                st_async_f64(cl_map_u32(la, d), s, rm);
+                st_async_f64(cl_map_u32(la, d), sum, rm);
                 if (g == 0) st_async_f64(cl_map_u32(lr, d), r, rm);
             }
         }
@@ -208,47 +250,66 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
         stamp(3);
         // ---- 3. cluster sum in CTA order ------------------------------------
         if (tid < BB) {
+            // fixed pairwise tree over 16 slots (absent CTAs contribute +0.0):
+            // the same order, hence the same bits, in every CTA
             double v[PNC_MAXG];
 #pragma unroll
-            for (int q = 0; q < PNC_MAXG; ++q)
-                if (q < G) v[q] = recv[par][q][tid];
-            double s = v[0];
-#pragma unroll
-            for (int q = 1; q < PNC_MAXG; ++q)
-                if (q < G) s += v[q];
-            gsum[tid] = s;
-            rjv[tid] = recv_rj[par][tid];
+            for (int q = 0; q < PNC_MAXG; ++q) v[q] = (q < G) ? recv[par][q][tid] : 0.0;
+            const double gs = tree_sum(v), rj = recv_rj[par][tid];
+            gsum[tid] = gs;
+            rjv[tid] = rj;
+            if (tid == j) {  // dlarfg (reading R-G7) once per CTA, from the same bits everywhere
+                const double alpha = rj, xn2 = gs;
+                double tau = 0.0, beta = alpha, scal = 0.0;
+                if (xn2 != 0.0) {
+                    const double nrm = sqrt(alpha * alpha + xn2);
+                    beta = (alpha >= 0.0) ? -nrm : nrm;
+                    tau = (beta - alpha) / beta;
+                    scal = 1.0 / (alpha - beta);
+                }
+                s_hh[0] = tau;
+                s_hh[1] = scal;
+                scal_s[j] = scal;
+                beta_s[j] = beta;
+            }
         }
         __syncthreads();
         // step j+2 reuses this mbarrier (every read of recv[par] is above)
         if (tid == 0 && j + 2 < bbe) mbar_expect_tx(mb0 + 8 * par, step_bytes);
         stamp(4);
-        // ---- 4. dlarfg (redundant, identical bits) and the update ----------
-        const double alpha = rjv[j], xn2 = gsum[j];
-        double tau = 0.0, beta = alpha, scal = 0.0;
-        if (xn2 != 0.0) {
-            const double nrm = sqrt(alpha * alpha + xn2);
-            beta = (alpha >= 0.0) ? -nrm : nrm;
-            tau = (beta - alpha) / beta;
-            scal = 1.0 / (alpha - beta);
+        // ---- 4. the update with this step's reflector ------------------------
+        const double tau = s_hh[0], scal = s_hh[1];
+        double ws[CPT];
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            const int c = cg * CPT + k;
+            ws[k] = 0.0;
+            if (g == 0 && rg == 0) {
+                if (c == 0) a.tau[j] = tau;
+                if (c < j) a.ybuf[c + (int64_t)j * a.bbpad] = scal_s[c] * (rjv[c] + scal * gsum[c]);
+            }
+            if (c > j && c < bb) {
+                const double w = tau * (rjv[c] + scal * gsum[c]);
+                ws[k] = w * scal;
+                any = true;
+                if (g == 0 && rg == 0) Rrow[j * BB + c] = rjv[c] - w;  // R(j, c): final
+            }
         }
-        if (tid == 0) { scal_s[j] = scal; beta_s[j] = beta; }
-        if (g == 0 && rg == 0) {
-            if (c == 0) a.tau[j] = tau;
-            if (c < j) a.ybuf[c + (int64_t)j * a.bbpad] = scal_s[c] * (rjv[c] + scal * gsum[c]);
-        }
-        if (c > j && c < bb) {
-            const double w = tau * (rjv[c] + scal * gsum[c]);
-            const double ws = w * scal;
+        stamp(6);
+        if (any) {  // columns <= j (or >= bb) have ws = 0: a - 0 x = a exactly
             const double2 *x2 = reinterpret_cast<const double2 *>(&xs[par][rg * RPT]);
 #pragma unroll
             for (int t = 0; t < RPT; t += 2) {
                 const double2 u = x2[t / 2];
-                av[t] = fma(-ws, u.x, av[t]);
-                av[t + 1] = fma(-ws, u.y, av[t + 1]);
+#pragma unroll
+                for (int k = 0; k < CPT; ++k) {
+                    av[k][t] = fma(-ws[k], u.x, av[k][t]);
+                    av[k][t + 1] = fma(-ws[k], u.y, av[k][t + 1]);
+                }
             }
-            if (g == 0 && rg == 0) Rrow[j * BB + c] = rjv[c] - w;  // R(j, c): final
         }
+        stamp(7);
         if (j + 1 < bbe) publish_x(j + 1, par ^ 1);
         stamp(5);
     }
@@ -259,20 +320,26 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
     // ---- store: A in place (columns < bb), explicit V (m' x bbpad) and V^T.
     //      Element (r, c): r < bbe, c > r: R(r, c) (Rrow); r == c < bbe: beta;
     //      c < bbe, r > c: v = scal_c x; otherwise the updated value.
+    // CTA 0: the final R rows live in Rrow (= the staging buffer); take them first
+    if (g == 0 && rowbase < bbe) {
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            const int c = cg * CPT + k;
+#pragma unroll
+            for (int t = 0; t < RPT; ++t) {
+                const int row = rowbase + t;
+                if (row < bbe && c > row && c < bb) av[k][t] = Rrow[row * BB + c];
+            }
+        }
+    }
     for (int q = 0; q < RG; ++q) {
         const int64_t r0 = cta_r0 + (int64_t)q * RPT;
         __syncthreads();
-        // CTA 0, q = 0: the R rows live in Rrow (= stage); move them first
-        if (g == 0 && q == 0 && rg == 0) {
-#pragma unroll
-            for (int t = 0; t < RPT; ++t) {
-                if (t < bbe && c > t && c < bb) av[t] = Rrow[t * BB + c];
-            }
-        }
-        __syncthreads();
         if (rg == q) {
 #pragma unroll
-            for (int t = 0; t < RPT; ++t) stage[c * LDS + t] = av[t];
+            for (int k = 0; k < CPT; ++k)
+#pragma unroll
+                for (int t = 0; t < RPT; ++t) stage[(cg * CPT + k) * LDS + t] = av[k][t];
         }
         __syncthreads();
         for (int e = tid; e < BB * RPT; e += PNC_THREADS) {

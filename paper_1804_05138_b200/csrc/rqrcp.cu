@@ -566,8 +566,10 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     }
     CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<32, 64>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<64, 64>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<64, 32, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 65 * 8));
     CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 65 * 8));
+    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<64, 32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 64 * 8));
     {
         ctx->pnc_max = 0;
         for (int cs = PNC_MAXG; cs >= 1 && !ctx->pnc_max; --cs) {
@@ -1156,15 +1158,19 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
                 const bool allow = !(e && e[0] == '0');
                 void (*kfn)(PanelArgs) = nullptr;
                 int64_t rc_rows = 0;
-                int bbk = 0;
-                if (bb <= 32) { kfn = panel_qr_cluster_kernel<32, 64>; rc_rows = 8 * 64; bbk = 32; }
-                else if (bb <= 64) { kfn = panel_qr_cluster_kernel<64, 64>; rc_rows = 4 * 64; bbk = 64; }
+                size_t psm = 0;
+                const char *ec = getenv("RQRCP_PN_CPT");
+                const bool cpt2 = !(ec && ec[0] == '1');
+                if (bb <= 32) { kfn = panel_qr_cluster_kernel<32, 64>; rc_rows = 8 * 64; psm = 32 * 65 * 8; }
+                else if (bb <= 64 && cpt2) {  // two columns x 32 rows per thread
+                    kfn = panel_qr_cluster_kernel<64, 32, 2>; rc_rows = 8 * 32; psm = 64 * 64 * 8;
+                } else if (bb <= 64) { kfn = panel_qr_cluster_kernel<64, 64>; rc_rows = 4 * 64; psm = 64 * 65 * 8; }
                 const int64_t cs = kfn ? (mp + rc_rows - 1) / rc_rows : 0;
                 if (allow && kfn && cs <= ctx->pnc_max) {
                     cudaLaunchConfig_t lc = {};
                     lc.gridDim = dim3((unsigned)cs);
                     lc.blockDim = dim3(PNC_THREADS);
-                    lc.dynamicSmemBytes = (size_t)bbk * 65 * sizeof(double);
+                    lc.dynamicSmemBytes = psm;
                     lc.stream = st;
                     cudaLaunchAttribute at[1];
                     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1374,6 +1380,17 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             }
             fprintf(stderr, "[rqrcp trace] panel CTA %s, %d steps, mean cycles:", c ? "last" : "0", cnt);
             for (int q = 0; q < 5; ++q) fprintf(stderr, " %s=%.0f", pn[q], cnt ? acc[q] / cnt : 0.0);
+            if (ctx->ptrace_kind == 1) {  // update+publish split: dlarfg+w | update loop | publish
+                double d6 = 0, d7 = 0, d5 = 0;
+                for (int jj = 1; jj < 63; ++jj) {
+                    const unsigned long long *r = h + ((size_t)c * 64 + jj) * 8;
+                    if (!r[0] || !r[5]) continue;
+                    d6 += (double)(r[6] - r[4]);
+                    d7 += (double)(r[7] - r[6]);
+                    d5 += (double)(r[5] - r[7]);
+                }
+                if (cnt) fprintf(stderr, " [dlarfg+w=%.0f loop=%.0f publish=%.0f]", d6 / cnt, d7 / cnt, d5 / cnt);
+            }
             fprintf(stderr, "\n");
         }
     }

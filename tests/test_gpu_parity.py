@@ -274,17 +274,21 @@ PN_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "wide", "odd", 
 ]
 
 
-@pytest.mark.parametrize("cluster", ["1", "0"], ids=["cluster", "grid"])
+@pytest.mark.parametrize("variant", ["cluster2", "cluster1", "grid"])
 @pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", PN_CASES, ids=[c[0] for c in PN_CASES])
-def test_panel_kernels(ctx, cluster, name, kind, m, n, k, b, p, seed):
+def test_panel_kernels(ctx, variant, name, kind, m, n, k, b, p, seed):
+    """cluster2: two columns x 32 rows per thread (bb in (32, 64]); cluster1: one
+    column x 64 rows per thread; grid: the cooperative grid kernel."""
     import os
     A = inputs.make(kind, m, n, seed, rank=64).numpy()
     o = oracle.rqrcp(A, k, b, p, seed=seed)
-    os.environ["RQRCP_PN_CLUSTER"] = cluster
+    os.environ["RQRCP_PN_CLUSTER"] = "0" if variant == "grid" else "1"
+    os.environ["RQRCP_PN_CPT"] = "1" if variant == "cluster1" else "2"
     try:
         g = gpu_factor(ctx, A, k, b, p, seed)
     finally:
         os.environ.pop("RQRCP_PN_CLUSTER", None)
+        os.environ.pop("RQRCP_PN_CPT", None)
     compare(A, g, o, k)
 
 
