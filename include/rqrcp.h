@@ -68,7 +68,12 @@ typedef struct rqrcp_config {
     int max_p;
 } rqrcp_config;
 
-/* Per-phase device times of the last rqrcp_factor (CUDA events, ms). */
+/* Per-phase device times of the last rqrcp_factor (CUDA events, ms).
+ * total_ms is the wall time of the call on the device.  The phases are
+ * timed on the stream that runs them; when the bulk rows of a panel's
+ * trailing update run concurrently with the next panel's sample QRCP
+ * (single GPU, Eq. (4), sample QRCP on one cluster), trailing_ms includes
+ * that concurrent update, so the phases may sum to more than total_ms. */
 typedef struct rqrcp_timings {
     double total_ms;
     double omega_ms;        /* S0: Philox Omega */

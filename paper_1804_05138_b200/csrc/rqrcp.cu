@@ -41,6 +41,12 @@ struct rqrcp_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // concurrent small kernels (tri_kernel)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // overlap of the bulk trailing update (rows i+bb..m) with the next panel's
+    // sample QRCP: the update runs on `upd` (lowest priority), the main stream
+    // (highest priority when ctx-owned) joins it before the next swap
+    cudaStream_t upd = nullptr;
+    cudaEvent_t ev_r12 = nullptr, ev_upd = nullptr;
+    int grid_cap = 0;  // > 0: persistent GEMM grids use at most this many CTAs
     bool own_stream = false;
     int nranks = 1, rank = 0;
     int64_t max_m = 0, max_n = 0;
@@ -283,7 +289,7 @@ static int launch_tma_cfg(rqrcp_ctx *ctx, const double *X, int64_t xdim0, int64_
         attr = true;
     }
     const int64_t tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM) * g.splits;
-    const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);
+    const int grid = (int)std::min<int64_t>(tiles, ctx->grid_cap > 0 ? ctx->grid_cap : ctx->num_sms);
     kern<<<grid, WM * WN * 32, smem, ctx->stream>>>(tx, ty, g);
     CKL();
     *done = true;
@@ -470,7 +476,9 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     if (cfg->stream) {
         ctx->stream = (cudaStream_t)cfg->stream;
     } else {
-        CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        int prio_lo = 0, prio_hi = 0;
+        CKC(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        CKC(cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, prio_hi));
         ctx->own_stream = true;
     }
     ctx->lpad_max = (int)rup(cfg->max_b + cfg->max_p, 8);
@@ -593,6 +601,13 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     }
     CKC(cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (128 * 128 + 64 * 64) * 8));
     CKC(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    {
+        int prio_lo = 0, prio_hi = 0;
+        CKC(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        CKC(cudaStreamCreateWithPriority(&ctx->upd, cudaStreamNonBlocking, prio_lo));
+    }
+    CKC(cudaEventCreateWithFlags(&ctx->ev_r12, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_upd, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
     for (auto &e : ctx->ev) CKC(cudaEventCreate(&e));
@@ -632,6 +647,9 @@ extern "C" int rqrcp_destroy(rqrcp_ctx *ctx) {
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->upd) cudaStreamDestroy(ctx->upd);
+    if (ctx->ev_r12) cudaEventDestroy(ctx->ev_r12);
+    if (ctx->ev_upd) cudaEventDestroy(ctx->ev_upd);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return 0;
@@ -980,6 +998,10 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     CK(cudaMemsetAsync(tau, 0, sizeof(double) * k, st));
 
     int panels = 0;
+    bool upd_pending = false;
+    double *bulk_A22 = nullptr;  // deferred bulk trailing update of this panel (overlap)
+    int64_t bulk_cols = 0;
+    int bulk_cs = 0;
     for (int64_t i = 0; i < k; i += b) {
         const int bb = (int)std::min<int64_t>(b, k - i);
         const int bbpad = (int)rup(bb, 8);
@@ -1108,6 +1130,10 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
         ph_end(ctx);
         // ---- S3: swaps on A and Pi -----------------------------------------
         ph_begin(ctx, PH_SWAP);
+        if (upd_pending) {  // the previous panel's bulk trailing update (overlapped with S2)
+            CK(cudaStreamWaitEvent(st, ctx->ev_upd, 0));
+            upd_pending = false;
+        }
         if (P > 1) {
             rc = dist_swaps(ctx, A, lda, m, i, b, jpvt);
             if (rc) return rc;
@@ -1247,10 +1273,33 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
             rc = gemm_skinny(ctx, bbpad, npl, bbpad, ctx->tneg, bbpad, ctx->w, bbpad, ctx->w2, bbpad);
             if (rc) return rc;
-            rc = tma_update(ctx, mp, npl, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda, &tdone);
-            if (rc) return rc;
-            if (!tdone) rc = gemm_update(ctx, mp, npl, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda);
-            if (rc) return rc;
+            // Overlap: when the next panel's sample QRCP runs on one cluster, only
+            // the R12 rows (all Eq. (4) needs) are updated here; the bulk A22 rows
+            // i+bb..m go to the low-priority `upd` stream on G - (cluster) CTAs and
+            // run concurrently with S6 and the next sample QRCP (the next swap
+            // waits for them).  P = 1, Eq. (4) only.
+            bool ovl = false;
+            int next_cs = 0;
+            if (P == 1 && !rule5 && more && npp > 0 && mp > bb && (bb % 2) == 0 && !gaps_out &&
+                (l == 40 || l == 74 || l == 80)) {
+                const char *e1 = getenv("RQRCP_OVERLAP"), *e2 = getenv("RQRCP_SQ_CLUSTER");
+                next_cs = (int)std::max<int64_t>(1, (npp + SQC_THREADS - 1) / SQC_THREADS);
+                ovl = !(e1 && e1[0] == '0') && !(e2 && e2[0] == '0') && next_cs <= ctx->sqc_max;
+            }
+            if (ovl) {
+                rc = tma_update(ctx, bb, npl, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda, &tdone);
+                if (rc) return rc;
+                if (!tdone) rc = gemm_update(ctx, bb, npl, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda);
+                if (rc) return rc;
+                bulk_A22 = A22;
+                bulk_cols = npl;
+                bulk_cs = next_cs;
+            } else {
+                rc = tma_update(ctx, mp, npl, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda, &tdone);
+                if (rc) return rc;
+                if (!tdone) rc = gemm_update(ctx, mp, npl, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda);
+                if (rc) return rc;
+            }
         } else {
             CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
         }
@@ -1301,7 +1350,34 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             ph_end(ctx);
             cur ^= 1;
         }
+        if (bulk_A22) {
+            // the bulk rows i+bb..m of the trailing update, launched once S6 is
+            // queued: it becomes ready together with the next sample QRCP, which
+            // the high-priority main stream places first on one cluster
+            CK(cudaEventRecord(ctx->ev_r12, st));
+            CK(cudaStreamWaitEvent(ctx->upd, ctx->ev_r12, 0));
+            cudaStream_t keep = ctx->stream;
+            ctx->stream = ctx->upd;
+            ctx->grid_cap = G - bulk_cs;
+            // timed on its own stream: trailing_ms adds the bulk update's duration
+            // (concurrent with S2, so the phases sum to more than total_ms)
+            ph_begin(ctx, PH_TRAIL);
+            bool dn = false;
+            rc = tma_update(ctx, mp - bb, bulk_cols, bbpad, ctx->w2, bbpad, ctx->vt + (int64_t)bb * bbpad, bbpad,
+                            bulk_A22 + bb, lda, &dn);
+            if (!rc && !dn)
+                rc = gemm_update(ctx, mp - bb, bulk_cols, bbpad, ctx->w2, bbpad, ctx->vt + (int64_t)bb * bbpad, bbpad,
+                                 bulk_A22 + bb, lda);
+            ph_end(ctx);
+            ctx->stream = keep;
+            ctx->grid_cap = 0;
+            if (rc) return rc;
+            CK(cudaEventRecord(ctx->ev_upd, ctx->upd));
+            upd_pending = true;
+            bulk_A22 = nullptr;
+        }
     }
+    if (upd_pending) CK(cudaStreamWaitEvent(st, ctx->ev_upd, 0));
     if (final_sample) *final_sample = cur;
     // ---- status ----------------------------------------------------------
     int hs[5];

@@ -292,6 +292,42 @@ def test_panel_kernels(ctx, variant, name, kind, m, n, k, b, p, seed):
     compare(A, g, o, k)
 
 
+# ---- the bulk trailing update overlapped with the next sample QRCP (default
+# when that runs on one cluster, P = 1, Eq. (4)) vs the serial schedule.
+OVL_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "lowrank", "kfull")]
+
+
+@pytest.mark.parametrize("overlap", ["1", "0"])
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", OVL_CASES, ids=[c[0] for c in OVL_CASES])
+def test_overlap_schedule(ctx, overlap, name, kind, m, n, k, b, p, seed):
+    import os
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    o = oracle.rqrcp(A, k, b, p, seed=seed)
+    os.environ["RQRCP_OVERLAP"] = overlap
+    try:
+        g = gpu_factor(ctx, A, k, b, p, seed)
+    finally:
+        os.environ.pop("RQRCP_OVERLAP", None)
+    compare(A, g, o, k)
+
+
+def test_overlap_bitwise_equal_serial(ctx):
+    """Overlapping changes the schedule, not the arithmetic: bitwise equal outputs."""
+    import os
+    c = inputs.CONFIGS["C2"]
+    A = inputs.config_matrix("C2").numpy()
+    outs = []
+    for ov in ("1", "0"):
+        os.environ["RQRCP_OVERLAP"] = ov
+        try:
+            outs.append(gpu_factor(ctx, A, c["k"], c["b"], c["p"], c["seed"]))
+        finally:
+            os.environ.pop("RQRCP_OVERLAP", None)
+    assert np.array_equal(outs[0]["jpvt"], outs[1]["jpvt"])
+    assert np.array_equal(outs[0]["tau"], outs[1]["tau"])
+    assert np.array_equal(outs[0]["A"], outs[1]["A"])
+
+
 # ---- updating formula 2 (Eq. (5), P:224-246) on the GPU: SURVEY.md §8(f) N2 ----
 EQ5_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "lowrank", "b128", "odd")]
 
