@@ -140,6 +140,49 @@ __global__ void pull_kernel(long long *out, double *sink, int n, int words) {
     sink[tid] = acc;
 }
 
+// shared-memory load throughput with 256 threads (8 warps): LDS.128 broadcast
+// (every lane the same address) vs distinct conflict-free addresses, and the
+// DFMA issue rate, in SM cycles per warp-instruction (whole SM).
+__global__ void lds_tput_kernel(long long *out, unsigned *sink, int n, int mode) {
+    __shared__ __align__(16) uint4 buf[1024];
+    for (int e = threadIdx.x; e < 1024; e += blockDim.x) buf[e] = make_uint4(e, e + 1, e + 2, e + 3);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    double d[16];
+    for (int k = 0; k < 16; ++k) d[k] = threadIdx.x + k;
+    __syncthreads();
+    long long t0 = clock64();
+    if (mode == 0) {
+        for (int i = 0; i < n; ++i) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint4 v = buf[(i * 8 + k) & 1023];  // broadcast
+                acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
+            }
+        }
+    } else if (mode == 1) {
+        for (int i = 0; i < n; ++i) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint4 v = buf[((i * 8 + k) * 32 + lane) & 1023];  // 32 distinct 16-byte words
+                acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
+            }
+        }
+    } else {
+        for (int i = 0; i < n; ++i) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) d[k] = fma(d[k], 0.999999, 1e-9);
+        }
+    }
+    __syncthreads();
+    long long t1 = clock64();
+    if (threadIdx.x == 0) out[0] = t1 - t0;
+    double s = 0;
+    for (int k = 0; k < 16; ++k) s += d[k];
+    sink[threadIdx.x] = acc.x ^ acc.y ^ acc.z ^ acc.w ^ (unsigned)s;
+}
+
 int main() {
     long long *d_out, h[8];
     double *sink;
@@ -209,6 +252,20 @@ int main() {
             CK(cudaMemcpy(h, d_out, 8, cudaMemcpyDeviceToHost));
             printf("%s\"%d\": %.1f", first ? "" : ", ", cs, h[0] / (double)n);
             first = 0;
+        }
+        printf("}");
+    }
+    {
+        unsigned *usink;
+        CK(cudaMalloc(&usink, 4096));
+        const char *names[3] = {"lds128_broadcast", "lds128_distinct", "dfma"};
+        const double per[3] = {8.0 * 8, 8.0 * 8, 16.0 * 8};  // warp-instructions per iteration (8 warps)
+        printf(", \"sm_cycles_per_warp_instr_256thr\": {");
+        for (int mode = 0; mode < 3; ++mode) {
+            lds_tput_kernel<<<1, 256>>>(d_out, usink, n, mode);
+            CK(cudaDeviceSynchronize());
+            CK(cudaMemcpy(h, d_out, 8, cudaMemcpyDeviceToHost));
+            printf("%s\"%s\": %.2f", mode ? ", " : "", names[mode], h[0] / (n * per[mode]));
         }
         printf("}");
     }
