@@ -29,9 +29,11 @@ __global__ void sumsq_partial_kernel(const double *B, int64_t rows, int64_t cols
 }
 
 __global__ void sumsq_final_kernel(const double *part, int nparts, double *stop_tol2, int *status) {
-    if (threadIdx.x != 0) return;
+    // one warp: lane-strided partial sums, then the fixed butterfly (deterministic)
     double s = 0.0;
-    for (int q = 0; q < nparts; ++q) s += part[q];
+    for (int q = threadIdx.x; q < nparts; q += 32) s += part[q];
+    s = warp_sum(s);
+    if (threadIdx.x != 0) return;
     const double eps = 0x1p-52;
     *stop_tol2 = (1e3 * eps) * (1e3 * eps) * s;
     if (!isfinite(s)) *status = 4;
