@@ -366,6 +366,9 @@ static int tma_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, con
     if ((lda & 1) || ((uintptr_t)A22 & 7)) return 0;
     TmaGemmArgs g{cols, rows, K, 0, 0, 0, 0, A22, lda, rup(K, 32), 1, 0,
                   (((uintptr_t)A22 & 15) == 0 && (lda & 1) == 0) ? 1 : 0};
+    // a short update (the R12 rows of the overlapped schedule): 32 x 64 tiles,
+    // twice as many CTAs; same per-element DMMA sequence (same bits)
+    if (rows <= 64) return launch_tma_cfg<2, 4, 2, 2, EPI_ACCUM_T_PRE>(ctx, w2, K, cols, ldw, vt, K, rows, ldvt, g, done);
     return launch_tma_cfg<4, 4, 2, 4, EPI_ACCUM_T_PRE>(ctx, w2, K, cols, ldw, vt, K, rows, ldvt, g, done);
 }
 
