@@ -49,6 +49,7 @@ constexpr int SQ_MAXL = 160;  // l = b + p <= 160 rows
 constexpr int SQ_RPL = 5;     // rows per lane of a warp-held column (SQ_MAXL / 32)
 constexpr int SQ_MAXB = 128;  // panel width
 constexpr int SQ_MAXG = 256;  // CTAs (headers scanned by one warp, 8 per lane)
+constexpr int SQ_SPB = 16;    // loads in flight per thread for L2-resident (spilled) columns
 
 struct __align__(16) SqHdr {  // one candidate header (16 bytes, one vector store)
     double v;                 // squared norm of the best active column (-1: none)
@@ -429,6 +430,20 @@ __global__ void __launch_bounds__(SQ_THREADS, 1) sample_qrcp_kernel(SqArgs a) {
                 if (cl < nsm) { base = tile + cl; rs = ncs; }
                 else { base = spill + (cl - nsm); rs = nov; }
                 int t = t0;
+                if (cl >= nsm) {
+                    // L2-resident column: SQ_SPB loads in flight per thread (the
+                    // loop below would expose one L2 latency per pair of rows)
+                    for (; t + (SQ_SPB - 1) * TPC < l; t += SQ_SPB * TPC) {
+                        double xv[SQ_SPB];
+#pragma unroll
+                        for (int u = 0; u < SQ_SPB; ++u) xv[u] = base[(size_t)(t + u * TPC) * rs];
+#pragma unroll
+                        for (int u = 0; u < SQ_SPB; u += 2) {
+                            d0 += xs[t + u * TPC] * xv[u];
+                            d1 += xs[t + (u + 1) * TPC] * xv[u + 1];
+                        }
+                    }
+                }
                 for (; t + TPC < l; t += 2 * TPC) {
                     d0 += xs[t] * base[(size_t)t * rs];
                     d1 += xs[t + TPC] * base[(size_t)(t + TPC) * rs];
@@ -439,7 +454,23 @@ __global__ void __launch_bounds__(SQ_THREADS, 1) sample_qrcp_kernel(SqArgs a) {
             double bj = 0.0, tail = 0.0;
             if (live) {
                 const double tw = tau * w;
-                for (int t = t0; t < l; t += TPC) {
+                int t = t0;
+                if (cl >= nsm) {  // L2-resident column: batches of SQ_SPB loads
+                    for (; t + (SQ_SPB - 1) * TPC < l; t += SQ_SPB * TPC) {
+                        double xv[SQ_SPB];
+#pragma unroll
+                        for (int u = 0; u < SQ_SPB; ++u) xv[u] = base[(size_t)(t + u * TPC) * rs];
+#pragma unroll
+                        for (int u = 0; u < SQ_SPB; ++u) {
+                            const int tt = t + u * TPC;
+                            const double x = xv[u] - tw * xs[tt];
+                            base[(size_t)tt * rs] = x;
+                            if (tt == j) bj = x;
+                            else tail += x * x;
+                        }
+                    }
+                }
+                for (; t < l; t += TPC) {
                     const double x = base[(size_t)t * rs] - tw * xs[t];
                     base[(size_t)t * rs] = x;
                     if (t == j) bj = x;
