@@ -141,8 +141,30 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     double av[CPT][RPT];
-    // ---- load: coalesced column reads into the staging buffer, one row group at a time
-    for (int q = 0; q < RG; ++q) {
+    // ---- load.  CPT = 2: straight into registers (each thread's 32 rows of a
+    // column are 256 contiguous bytes; 16-byte loads, all in flight at once).
+    // CPT = 1: coalesced column reads through the staging buffer, one row group
+    // at a time.
+    const bool vec_ok = ((lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(a.A) & 15) == 0);
+    if (CPT == 2) {
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            const int c = cg * CPT + k;
+            const double *src = a.A + rowbase + (int64_t)c * lda;
+            if (c < bb && vec_ok && rowbase + RPT <= mp) {
+#pragma unroll
+                for (int t = 0; t < RPT; t += 2) {
+                    const double2 v = reinterpret_cast<const double2 *>(src)[t / 2];
+                    av[k][t] = v.x;
+                    av[k][t + 1] = v.y;
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < RPT; ++t) av[k][t] = (c < bb && rowbase + t < mp) ? src[t] : 0.0;
+            }
+        }
+    }
+    for (int q = 0; q < (CPT == 2 ? 0 : RG); ++q) {
         const int64_t r0 = cta_r0 + (int64_t)q * RPT;
         for (int e = tid; e < BB * RPT; e += PNC_THREADS) {
             const int r = e % RPT, cc = e / RPT;
@@ -316,6 +338,7 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
     // no CTA leaves while pushes into it may be in flight
     cl_arrive_relaxed();
     cl_wait();
+    __syncthreads();  // the last step's Rrow / scal / beta writes are visible
 
     // ---- store: A in place (columns < bb), explicit V (m' x bbpad) and V^T.
     //      Element (r, c): r < bbe, c > r: R(r, c) (Rrow); r == c < bbe: beta;
@@ -332,7 +355,64 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
             }
         }
     }
-    for (int q = 0; q < RG; ++q) {
+    if (CPT == 2) {
+        // straight from registers.  Element (gr, cc): A = scal_c x below the
+        // diagonal, beta_c on it, x (or the R row) above; V = scal_c x below, 1
+        // on, 0 above (and 0 for unfactored columns).  V^T: the two columns of
+        // a row are adjacent (one 16-byte store; a warp writes 512 contiguous
+        // bytes); A and V: 16-byte stores along this thread's rows.
+        const bool vo = vec_ok && ((a.ldv & 1) == 0) && ((reinterpret_cast<uintptr_t>(a.vfull) & 15) == 0) &&
+                        rowbase + RPT <= mp;
+        const int c0 = cg * CPT;
+        double sc[CPT], be[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            sc[k] = (c0 + k < bbe) ? scal_s[c0 + k] : 0.0;
+            be[k] = (c0 + k < bbe) ? beta_s[c0 + k] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < RPT; t += 2) {  // rows gr, gr + 1
+            const int64_t gr = rowbase + t;
+            double o[CPT][2], v[CPT][2];
+#pragma unroll
+            for (int k = 0; k < CPT; ++k)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int cc = c0 + k;
+                    double x = av[k][t + h], w = 0.0;
+                    if (cc < bbe) {
+                        if (gr + h > cc) { w = sc[k] * x; x = w; }
+                        else if (gr + h == cc) { w = 1.0; x = be[k]; }
+                    }
+                    o[k][h] = x;
+                    v[k][h] = w;
+                }
+            if (c0 < a.bbpad) {  // bbpad is a multiple of 8: both columns present
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    if (gr + h < mp)
+                        *reinterpret_cast<double2 *>(a.vt + c0 + (gr + h) * a.bbpad) = make_double2(v[0][h], v[CPT - 1][h]);
+            }
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) {
+                const int cc = c0 + k;
+                double *dst = a.A + gr + (int64_t)cc * lda;
+                double *vd = a.vfull + gr + (int64_t)cc * a.ldv;
+                if (vo) {
+                    if (cc < bb) *reinterpret_cast<double2 *>(dst) = make_double2(o[k][0], o[k][1]);
+                    if (cc < a.bbpad) *reinterpret_cast<double2 *>(vd) = make_double2(v[k][0], v[k][1]);
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        if (gr + h < mp) {
+                            if (cc < bb) dst[h] = o[k][h];
+                            if (cc < a.bbpad) vd[h] = v[k][h];
+                        }
+                }
+            }
+        }
+    }
+    for (int q = 0; q < (CPT == 2 ? 0 : RG); ++q) {
         const int64_t r0 = cta_r0 + (int64_t)q * RPT;
         __syncthreads();
         if (rg == q) {
