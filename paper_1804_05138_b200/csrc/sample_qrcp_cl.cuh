@@ -94,7 +94,22 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
 
     double x[L];
 #pragma unroll
-    for (int t = 0; t < L; ++t) x[t] = have ? a.B[t + pc * a.ldb] : 0.0;
+    for (int t = 0; t < L; ++t) x[t] = 0.0;
+    if (have) {  // the column's l entries are contiguous: 16-byte loads when aligned
+        const double *src = a.B + pc * a.ldb;
+        if (((a.ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(a.B) & 15) == 0)) {
+#pragma unroll
+            for (int t = 0; t + 1 < L; t += 2) {
+                const double2 v = reinterpret_cast<const double2 *>(src)[t / 2];
+                x[t] = v.x;
+                x[t + 1] = v.y;
+            }
+            if (L & 1) x[L - 1] = src[L - 1];
+        } else {
+#pragma unroll
+            for (int t = 0; t < L; ++t) x[t] = src[t];
+        }
+    }
     double r = 0.0;
 #pragma unroll
     for (int t = 0; t < L; ++t) r += x[t] * x[t];
@@ -328,8 +343,15 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
 
     // ---- results --------------------------------------------------------------
     if (have) {
+        double *dst = a.B + pc * a.ldb;
+        if (((a.ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(a.B) & 15) == 0)) {
 #pragma unroll
-        for (int t = 0; t < L; ++t) a.B[t + pc * a.ldb] = x[t];
+            for (int t = 0; t + 1 < L; t += 2) reinterpret_cast<double2 *>(dst)[t / 2] = make_double2(x[t], x[t + 1]);
+            if (L & 1) dst[L - 1] = x[L - 1];
+        } else {
+#pragma unroll
+            for (int t = 0; t < L; ++t) dst[t] = x[t];
+        }
     }
     if (g == 0) {
         // Vhat (lpad x bbpad: unit diagonal, v below), Rhat11 (bbpad x bbpad), piv, tauhat
