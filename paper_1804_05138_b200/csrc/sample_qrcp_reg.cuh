@@ -81,10 +81,28 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
     const double stop2 = *a.stop_tol2;
 
     double x[LR];
+    // the column's entries are contiguous: 16-byte loads when aligned
+    const bool vec = ((a.ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(a.B) & 15) == 0) && !(LR & 1) && !(LS & 1);
+    if (have && vec) {
+        const double2 *src = reinterpret_cast<const double2 *>(a.B + pc * a.ldb);
 #pragma unroll
-    for (int t = 0; t < LR; ++t) x[t] = have ? a.B[t + pc * a.ldb] : 0.0;
+        for (int t = 0; t < LR; t += 2) {
+            const double2 v = src[t / 2];
+            x[t] = v.x;
+            x[t + 1] = v.y;
+        }
 #pragma unroll 4
-    for (int t = 0; t < LS; ++t) xsm[t * SQR_THREADS + tid] = have ? a.B[(LR + t) + pc * a.ldb] : 0.0;
+        for (int t = 0; t < LS; t += 2) {
+            const double2 v = src[(LR + t) / 2];
+            xsm[t * SQR_THREADS + tid] = v.x;
+            xsm[(t + 1) * SQR_THREADS + tid] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < LR; ++t) x[t] = have ? a.B[t + pc * a.ldb] : 0.0;
+#pragma unroll 4
+        for (int t = 0; t < LS; ++t) xsm[t * SQR_THREADS + tid] = have ? a.B[(LR + t) + pc * a.ldb] : 0.0;
+    }
     double r = 0.0;
 #pragma unroll
     for (int t = 0; t < LR; ++t) r += x[t] * x[t];
@@ -366,7 +384,13 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
     if (a.trace)
         for (int e = tid; e < 64 * 4; e += SQR_THREADS)
             a.trace[(size_t)g * 256 + e] = (e / 4 < min(j + 1, 64)) ? s_trace[e] : 0ull;
-    if (have) {
+    if (have && vec) {
+        double2 *dst = reinterpret_cast<double2 *>(a.B + pc * a.ldb);
+#pragma unroll
+        for (int t = 0; t < LR; t += 2) dst[t / 2] = make_double2(x[t], x[t + 1]);
+        for (int t = 0; t < LS; t += 2)
+            dst[(LR + t) / 2] = make_double2(xsm[t * SQR_THREADS + tid], xsm[(t + 1) * SQR_THREADS + tid]);
+    } else if (have) {
 #pragma unroll
         for (int t = 0; t < LR; ++t) a.B[t + pc * a.ldb] = x[t];
         for (int t = 0; t < LS; ++t) a.B[(LR + t) + pc * a.ldb] = xsm[t * SQR_THREADS + tid];
