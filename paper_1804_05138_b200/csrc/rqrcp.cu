@@ -1216,10 +1216,11 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             }
             int pcap = G;
             if (const char *e = getenv("RQRCP_PN_GRID")) pcap = std::max(1, std::min(G, atoi(e)));
-            // ~64 rows per CTA: fewer CTAs shrink the per-column all-to-all of
+            // ~128 rows per CTA: fewer CTAs shrink the per-column all-to-all of
             // partial Gram rows (G x bb doubles read by every CTA), more rows
-            // per CTA lengthen the local pass (measured best at C2)
-            int64_t prows = 64;
+            // per CTA lengthen the local pass (measured best at C3: 64 / 96 /
+            // 128 / 192 / 256 rows -> 8.17 / 8.16 / 7.76 / 8.32 / 9.18 ms)
+            int64_t prows = 128;
             if (const char *e = getenv("RQRCP_PN_ROWS")) prows = std::max(1, atoi(e));
             const int grid = (int)std::max<int64_t>((mp + PN_MAXROWS - 1) / PN_MAXROWS,
                                                     std::min<int64_t>(pcap, (mp + prows - 1) / prows));
