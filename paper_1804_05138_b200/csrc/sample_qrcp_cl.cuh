@@ -70,6 +70,9 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
 
     const int G = gridDim.x;
     const int g = (int)cl_rank();
+    // the recorder CTA (stages the outputs, receives whole records): the last
+    // one, which holds the ragged remainder of the columns (least apply work)
+    const int rg0 = G - 1;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int l = a.l;
     const int64_t nn = a.nn;
@@ -85,7 +88,12 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
     }
     const double stop2 = *a.stop_tol2;
     const unsigned mb0 = (unsigned)__cvta_generic_to_shared(&mbar[0]);
-    const unsigned step_bytes = (unsigned)(G * RECW * sizeof(double));
+    // bytes a CTA receives for step st: the recorder rg0 gets every record whole
+    // (it stages the R-hat rows); the others the header and rows >= (st & ~1) only
+    auto step_bytes = [&](int st) -> unsigned {
+        const int np = (g == rg0) ? NPAIR : NPAIR - (st & ~1) / 2;
+        return (unsigned)(G * np * 16);
+    };
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb0) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb0 + 8) : "memory");
@@ -117,7 +125,7 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
     int lpos = (int)pc;
     bool act = have;
     if (have) a.perm[pc] = pc;
-    if (g == 0) {
+    if (g == rg0) {
         for (int q = tid; q < a.bb; q += SQC_THREADS) low[q] = q;
         if (tid == 0) hi_n = 0;
     }
@@ -125,8 +133,8 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
     asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     cl_wait();
     if (tid == 0) {
-        asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb0), "r"(step_bytes) : "memory");
-        asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb0 + 8), "r"(step_bytes) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb0), "r"(step_bytes(0)) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb0 + 8), "r"(step_bytes(1)) : "memory");
     }
 
     // CTA-best candidate (value, position, physical column, its l entries),
@@ -161,8 +169,19 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
         }
         __syncthreads();
         const unsigned lm = mb0 + 8 * par;
-        for (int e = tid; e < G * NPAIR; e += SQC_THREADS) {
-            const int d = e / NPAIR, w = 2 * (e % NPAIR);
+        // pair 0 (header) and the column pairs: all of them to the recorder CTA
+        // rg0, from the pair holding row (step & ~1) on to the others
+        const int p0 = 1 + (step & ~1) / 2;      // first column pair sent to CTAs != 0
+        const int np_o = NPAIR - p0 + 1;          // pairs per record for CTAs != 0
+        const int ntot = NPAIR + (G - 1) * np_o;
+        for (int e = tid; e < ntot; e += SQC_THREADS) {
+            int d, w;
+            if (e < NPAIR) { d = rg0; w = 2 * e; }
+            else {
+                const int f = e - NPAIR, q = f % np_o;
+                d = f / np_o;  // 0 .. G-2: the CTAs other than rg0
+                w = 2 * ((q == 0) ? 0 : p0 + q - 1);
+            }
             const double2 val = *reinterpret_cast<const double2 *>(&rec[w]);
             const unsigned la = (unsigned)__cvta_generic_to_shared(&recv[par][g][w]);
             unsigned ra, rm;
@@ -198,7 +217,7 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
         // CTA received this CTA's step j+1 record (sent after all reads below)
         if (tid == 0 && j + 2 < a.bb)
             asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb0 + 8 * par),
-                         "r"(step_bytes)
+                         "r"(step_bytes(j + 2))
                          : "memory");
         // ---- 1. winner and its reflector, redundantly in EVERY warp (local
         //      shared memory only: same bits everywhere, no CTA barrier) ------
@@ -251,7 +270,7 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
         }
         __syncwarp();
         // ---- outputs (staged in CTA 0's shared memory, written at the end) -----
-        if (g == 0 && warp == 0) {
+        if (g == rg0 && warp == 0) {
             // column j in LAPACK format: R-hat above the diagonal, beta, v below
 #pragma unroll
             for (int qq = 0; qq < SQ_RPL; ++qq) {
@@ -260,7 +279,7 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
             }
             if (lane == 0) { s_piv[j] = wp; s_tauh[j] = tau; }
         }
-        if (g == 0 && warp == SQ_WARPS - 1) {
+        if (g == rg0 && warp == SQ_WARPS - 1) {
             const int64_t q = low[j];
             __syncwarp();
             if (lane == 0) low[j] = wcl;
@@ -353,7 +372,7 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
             for (int t = 0; t < L; ++t) dst[t] = x[t];
         }
     }
-    if (g == 0) {
+    if (g == rg0) {
         // Vhat (lpad x bbpad: unit diagonal, v below), Rhat11 (bbpad x bbpad), piv, tauhat
         for (int e = tid; e < j * a.lpad; e += SQC_THREADS) {
             const int t = e % a.lpad, c = e / a.lpad;
