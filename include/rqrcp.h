@@ -216,7 +216,9 @@ int rqrcp_cx(rqrcp_ctx *ctx, const double *A, int64_t lda, int64_t m, int64_t n,
  * -2 (rule not 1 or 2). */
 int rqrcp_set_update_rule(rqrcp_ctx *ctx, int rule);
 
-/* Enable (1) / disable (0) per-phase CUDA-event timing (default 1). */
+/* Enable (1) / disable (0) reading the per-phase CUDA-event times in
+ * rqrcp_get_timings (default 1).  The events themselves are always recorded
+ * (they are cheap, and the overlapped schedule measured faster with them). */
 int rqrcp_set_timing(rqrcp_ctx *ctx, int enabled);
 
 /* Destroy: frees workspace and the communicator.  NULL is a no-op. */

@@ -113,6 +113,8 @@ struct rqrcp_ctx {
     int open_phase = -1, open_ev = -1;
     std::vector<int> rec_phase, rec_s, rec_e;
     rqrcp_timings last{};
+    int lt_t0 = -1, lt_t1 = -1;  // total-time events of the last factorization (read lazily)
+    int *hstatus = nullptr;      // pinned host copy of the device status words
     int64_t launches = 0;
     bool debug_sync = false;  // RQRCP_DEBUG_SYNC=1: synchronise after every launch
     unsigned long long *trace = nullptr;  // RQRCP_TRACE=1: per-step phase stamps of the sample QRCP
@@ -378,7 +380,10 @@ static int tma_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, con
 static constexpr int kMaxEv = 2 * 4096 + 8;
 static void ph_begin(rqrcp_ctx *ctx, int phase) {
     ctx->open_phase = -1;
-    if (!ctx->timing || ctx->nev + 3 > kMaxEv) return;
+    // phase events are always recorded (measured: the schedule runs faster with
+    // them than without, 4.31 vs 4.58 ms at C2); rqrcp_set_timing(ctx, 0) only
+    // turns their reading off
+    if (ctx->nev + 3 > kMaxEv) return;
     ctx->open_phase = phase;
     ctx->open_ev = ctx->nev;
     cudaEventRecord(ctx->ev[ctx->nev++], ctx->stream);
@@ -428,6 +433,8 @@ static int free_all(rqrcp_ctx *ctx) {
                     (void *)ctx->dl_slots})
         if (q) cudaFree(q);
     if (ctx->h_pairs) cudaFreeHost(ctx->h_pairs);
+    if (ctx->hstatus) cudaFreeHost(ctx->hstatus);
+    ctx->hstatus = nullptr;
     void *ptrs[] = {ctx->omt,     ctx->bs[0],   ctx->bs[1],     ctx->vfull,     ctx->vt,        ctx->w,
                     ctx->w2,      ctx->tneg, ctx->ybuf,   ctx->rhat11,    ctx->omhat,     ctx->vhat,      ctx->tauhat,
                     ctx->splitk,  ctx->slot_hdr, ctx->slot_col, ctx->slot_v2,
@@ -604,6 +611,7 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     }
     CKC(cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (128 * 128 + 64 * 64) * 8));
     CKC(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    CKC(cudaMallocHost((void **)&ctx->hstatus, sizeof(int) * 8));
     {
         int prio_lo = 0, prio_hi = 0;
         CKC(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
@@ -699,7 +707,27 @@ extern "C" int rqrcp_set_timing(rqrcp_ctx *ctx, int enabled) {
 extern "C" int rqrcp_get_timings(const rqrcp_ctx *ctx, rqrcp_timings *out) {
     if (!ctx) return -1;
     if (!out) return -2;
-    *out = ctx->last;
+    rqrcp_timings t = ctx->last;
+    if (ctx->lt_t0 >= 0 && ctx->lt_t1 >= 0) {  // the last factorization's events (complete: it synchronized)
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ctx->ev[ctx->lt_t0], ctx->ev[ctx->lt_t1]);
+        t.total_ms = ms;
+        double acc[PH_N] = {0};
+        for (size_t q = 0; q < ctx->rec_phase.size(); ++q) {
+            float x = 0;
+            cudaEventElapsedTime(&x, ctx->ev[ctx->rec_s[q]], ctx->ev[ctx->rec_e[q]]);
+            acc[ctx->rec_phase[q]] += x;
+        }
+        t.omega_ms = acc[PH_OMEGA];
+        t.sketch_ms = acc[PH_SKETCH];
+        t.sample_qrcp_ms = acc[PH_SQRCP];
+        t.swap_ms = acc[PH_SWAP];
+        t.panel_ms = acc[PH_PANEL];
+        t.trailing_ms = acc[PH_TRAIL];
+        t.sample_update_ms = acc[PH_SUPD];
+        t.comm_ms = acc[PH_COMM];
+    }
+    *out = t;
     return 0;
 }
 
@@ -946,6 +974,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     const int64_t n_loc = dist_count(n, b, P, me);  // this rank's columns (n when P = 1)
     ctx->launches = 0;
     ctx->nev = 0;
+    ctx->lt_t0 = ctx->lt_t1 = -1;
     ctx->rec_phase.clear();
     ctx->rec_s.clear();
     ctx->rec_e.clear();
@@ -955,7 +984,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     const int G = ctx->num_sms;
     cudaStream_t st = ctx->stream;
     const int ev_t0 = ctx->nev;
-    if (ctx->timing) cudaEventRecord(ctx->ev[ctx->nev++], st);
+    cudaEventRecord(ctx->ev[ctx->nev++], st);
     ph_begin(ctx, PH_OMEGA);
     CK(cudaMemsetAsync(ctx->iscal, 0, sizeof(int) * 8, st));
     const int64_t npanels = (k + b - 1) / b;
@@ -1005,6 +1034,35 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     double *bulk_A22 = nullptr;  // deferred bulk trailing update of this panel (overlap)
     int64_t bulk_cols = 0;
     int bulk_cs = 0;
+    // the deferred update waiting for launch (after the next sample QRCP is queued)
+    bool bulk_ready = false;
+    double *bulk_A22_saved = nullptr;
+    int64_t bulk_rows = 0;
+    int bulk_bb = 0, bulk_bbpad = 0;
+    auto launch_bulk = [&]() -> int {
+        bulk_ready = false;
+        CK(cudaStreamWaitEvent(ctx->upd, ctx->ev_r12, 0));
+        cudaStream_t keep = ctx->stream;
+        ctx->stream = ctx->upd;
+        ctx->grid_cap = G - bulk_cs;
+        // timed on its own stream: trailing_ms adds the bulk update's duration
+        // (concurrent with S2, so the phases sum to more than total_ms)
+        ph_begin(ctx, PH_TRAIL);
+        bool dn = false;
+        const double *vt_b = ctx->vt + (int64_t)bulk_bb * bulk_bbpad;
+        int r = tma_update(ctx, bulk_rows, bulk_cols, bulk_bbpad, ctx->w2, bulk_bbpad, vt_b, bulk_bbpad,
+                           bulk_A22_saved + bulk_bb, lda, &dn);
+        if (!r && !dn)
+            r = gemm_update(ctx, bulk_rows, bulk_cols, bulk_bbpad, ctx->w2, bulk_bbpad, vt_b, bulk_bbpad,
+                            bulk_A22_saved + bulk_bb, lda);
+        ph_end(ctx);
+        ctx->stream = keep;
+        ctx->grid_cap = 0;
+        if (r) return r;
+        CK(cudaEventRecord(ctx->ev_upd, ctx->upd));
+        upd_pending = true;
+        return 0;
+    };
     for (int64_t i = 0; i < k; i += b) {
         const int bb = (int)std::min<int64_t>(b, k - i);
         const int bbpad = (int)rup(bb, 8);
@@ -1131,6 +1189,10 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             }
         }
         ph_end(ctx);
+        if (bulk_ready) {  // the previous panel's bulk update, now that S2 is queued
+            rc = launch_bulk();
+            if (rc) return rc;
+        }
         // ---- S3: swaps on A and Pi -----------------------------------------
         ph_begin(ctx, PH_SWAP);
         if (upd_pending) {  // the previous panel's bulk trailing update (overlapped with S2)
@@ -1355,61 +1417,35 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             cur ^= 1;
         }
         if (bulk_A22) {
-            // the bulk rows i+bb..m of the trailing update, launched once S6 is
-            // queued: it becomes ready together with the next sample QRCP, which
-            // the high-priority main stream places first on one cluster
+            // the bulk rows i+bb..m of this panel's trailing update may start once
+            // S6 is done; they are launched after the next sample QRCP has been
+            // queued (below), so that kernel is dispatched onto its cluster first
             CK(cudaEventRecord(ctx->ev_r12, st));
-            CK(cudaStreamWaitEvent(ctx->upd, ctx->ev_r12, 0));
-            cudaStream_t keep = ctx->stream;
-            ctx->stream = ctx->upd;
-            ctx->grid_cap = G - bulk_cs;
-            // timed on its own stream: trailing_ms adds the bulk update's duration
-            // (concurrent with S2, so the phases sum to more than total_ms)
-            ph_begin(ctx, PH_TRAIL);
-            bool dn = false;
-            rc = tma_update(ctx, mp - bb, bulk_cols, bbpad, ctx->w2, bbpad, ctx->vt + (int64_t)bb * bbpad, bbpad,
-                            bulk_A22 + bb, lda, &dn);
-            if (!rc && !dn)
-                rc = gemm_update(ctx, mp - bb, bulk_cols, bbpad, ctx->w2, bbpad, ctx->vt + (int64_t)bb * bbpad, bbpad,
-                                 bulk_A22 + bb, lda);
-            ph_end(ctx);
-            ctx->stream = keep;
-            ctx->grid_cap = 0;
-            if (rc) return rc;
-            CK(cudaEventRecord(ctx->ev_upd, ctx->upd));
-            upd_pending = true;
+            bulk_rows = mp - bb;
+            bulk_bb = bb;
+            bulk_bbpad = bbpad;
+            bulk_ready = true;
+            bulk_A22_saved = bulk_A22;
             bulk_A22 = nullptr;
         }
     }
+    if (bulk_ready) {
+        rc = launch_bulk();
+        if (rc) return rc;
+    }
     if (upd_pending) CK(cudaStreamWaitEvent(st, ctx->ev_upd, 0));
     if (final_sample) *final_sample = cur;
-    // ---- status ----------------------------------------------------------
-    int hs[5];
+    // ---- status (pinned host words) ----------------------------------------
+    int *hs = ctx->hstatus;
     CK(cudaMemcpyAsync(hs, ctx->iscal, sizeof(int) * 5, cudaMemcpyDeviceToHost, st));
     const int ev_t1 = ctx->nev;
-    if (ctx->timing) cudaEventRecord(ctx->ev[ctx->nev++], st);
+    cudaEventRecord(ctx->ev[ctx->nev++], st);
     CK(cudaStreamSynchronize(st));
-    // timings
+    // timings: the events are read lazily by rqrcp_get_timings (the elapsed-time
+    // queries stay off the caller's critical path between factorizations)
     rqrcp_timings t{};
-    if (ctx->timing) {
-        float ms = 0;
-        cudaEventElapsedTime(&ms, ctx->ev[ev_t0], ctx->ev[ev_t1]);
-        t.total_ms = ms;
-        double acc[PH_N] = {0};
-        for (size_t q = 0; q < ctx->rec_phase.size(); ++q) {
-            float x = 0;
-            cudaEventElapsedTime(&x, ctx->ev[ctx->rec_s[q]], ctx->ev[ctx->rec_e[q]]);
-            acc[ctx->rec_phase[q]] += x;
-        }
-        t.omega_ms = acc[PH_OMEGA];
-        t.sketch_ms = acc[PH_SKETCH];
-        t.sample_qrcp_ms = acc[PH_SQRCP];
-        t.swap_ms = acc[PH_SWAP];
-        t.panel_ms = acc[PH_PANEL];
-        t.trailing_ms = acc[PH_TRAIL];
-        t.sample_update_ms = acc[PH_SUPD];
-        t.comm_ms = acc[PH_COMM];
-    }
+    ctx->lt_t0 = ctx->timing ? ev_t0 : -1;
+    ctx->lt_t1 = ctx->timing ? ev_t1 : -1;
     if (ctx->trace) {
         std::vector<unsigned long long> H((size_t)SQ_MAXG * 64 * 4);
         cudaMemcpy(H.data(), ctx->trace, sizeof(unsigned long long) * H.size(), cudaMemcpyDeviceToHost);
