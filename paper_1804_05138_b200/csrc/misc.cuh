@@ -59,6 +59,36 @@ __global__ void swap_gather_kernel(const double *A /* + i*lda */, int64_t lda, i
     }
 }
 
+// One-kernel form: CTA b moves rows [b R, b R + R) of every (src -> dst) pair
+// through shared memory -- all reads of its rows, then all writes -- so no
+// staging buffer and no second launch (rows are independent); CTA 0 also moves
+// jpvt.  np <= SW_MAXP pairs.
+constexpr int SW_ROWS = 16, SW_MAXP = 256;
+__global__ void __launch_bounds__(256) swap_fused_kernel(double *A /* + i*lda */, int64_t lda, int64_t m,
+                                                         int64_t *jpvt, const int64_t *src, const int64_t *dst,
+                                                         const int *npairs) {
+    __shared__ double st[SW_MAXP][SW_ROWS + 1];
+    __shared__ int64_t js[SW_MAXP];
+    __shared__ int64_t ss[SW_MAXP], ds[SW_MAXP];
+    const int np = *npairs;
+    const int64_t r0 = (int64_t)blockIdx.x * SW_ROWS;
+    for (int q = threadIdx.x; q < np; q += blockDim.x) { ss[q] = src[q]; ds[q] = dst[q]; }
+    __syncthreads();
+    for (int e = threadIdx.x; e < np * SW_ROWS; e += blockDim.x) {
+        const int r = e % SW_ROWS, q = e / SW_ROWS;
+        if (r0 + r < m) st[q][r] = A[r0 + r + ss[q] * lda];
+    }
+    if (blockIdx.x == 0)
+        for (int q = threadIdx.x; q < np; q += blockDim.x) js[q] = jpvt[ss[q]];
+    __syncthreads();
+    for (int e = threadIdx.x; e < np * SW_ROWS; e += blockDim.x) {
+        const int r = e % SW_ROWS, q = e / SW_ROWS;
+        if (r0 + r < m) A[r0 + r + ds[q] * lda] = st[q][r];
+    }
+    if (blockIdx.x == 0)
+        for (int q = threadIdx.x; q < np; q += blockDim.x) jpvt[ds[q]] = js[q];
+}
+
 __global__ void swap_scatter_kernel(double *A, int64_t lda, int64_t m, int64_t *jpvt, const int64_t *dst,
                                     const int *npairs, const double *stage, int64_t lds, const int64_t *jstage) {
     const int np = *npairs;

@@ -1203,14 +1203,20 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
             rc = dist_swaps(ctx, A, lda, m, i, b, jpvt);
             if (rc) return rc;
         } else {
-            const int64_t lds = ctx->max_m;
-            const int gg = grid_for(2 * (int64_t)bb * m, 256, G);
-            swap_gather_kernel<<<gg, 256, 0, st>>>(A + i * lda, lda, m, jpvt + i, ctx->swap_src, ctx->swap_np,
-                                                    ctx->swap_stage, lds, ctx->swap_jstage);
-            CKL();
-            swap_scatter_kernel<<<gg, 256, 0, st>>>(A + i * lda, lda, m, jpvt + i, ctx->swap_dst, ctx->swap_np,
-                                                     ctx->swap_stage, lds, ctx->swap_jstage);
-            CKL();
+            if (2 * bb <= SW_MAXP) {  // one launch: rows are independent
+                swap_fused_kernel<<<(unsigned)((m + SW_ROWS - 1) / SW_ROWS), 256, 0, st>>>(
+                    A + i * lda, lda, m, jpvt + i, ctx->swap_src, ctx->swap_dst, ctx->swap_np);
+                CKL();
+            } else {
+                const int64_t lds = ctx->max_m;
+                const int gg = grid_for(2 * (int64_t)bb * m, 256, G);
+                swap_gather_kernel<<<gg, 256, 0, st>>>(A + i * lda, lda, m, jpvt + i, ctx->swap_src, ctx->swap_np,
+                                                        ctx->swap_stage, lds, ctx->swap_jstage);
+                CKL();
+                swap_scatter_kernel<<<gg, 256, 0, st>>>(A + i * lda, lda, m, jpvt + i, ctx->swap_dst, ctx->swap_np,
+                                                         ctx->swap_stage, lds, ctx->swap_jstage);
+                CKL();
+            }
         }
         ph_end(ctx);
         // ---- S4: panel QR + T ----------------------------------------------
