@@ -1,4 +1,4 @@
-# Round-end evidence run (v9): GPU tests, smoke, bench lines for C2-C5, the ncu
+# Round-end evidence run (v10): GPU tests, smoke, bench lines for C2-C5, the ncu
 # launch list of the bench command, one ncu --set full capture of the
 # latency-bound cluster kernels.
 set -x
@@ -7,6 +7,7 @@ python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log
 timeout 600 python bench.py > gpurun_out/bench_C2.json 2> gpurun_out/bench_C2.err; echo "bench C2 rc=$?"
+timeout 300 python bench.py --config C1 --steps 20 --no-cpu-baseline > gpurun_out/bench_C1.json 2> gpurun_out/bench_C1.err; echo "bench C1 rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_C2.json 2> gpurun_out/bench_ref_C2.err; echo "bench ref rc=$?"
 timeout 600 python bench.py --config C3 --steps 5 --no-cpu-baseline > gpurun_out/bench_C3.json 2> gpurun_out/bench_C3.err; echo "bench C3 rc=$?"
 timeout 900 python bench.py --config C4 --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.err; echo "bench C4 rc=$?"
