@@ -25,6 +25,10 @@ namespace rq {
 constexpr int SQC_L = 80;         // max rows (l = b + p); kernels are instantiated for exact l
 constexpr int SQC_THREADS = 256;  // columns per CTA
 constexpr int SQC_MAXG = 16;      // CTAs (one cluster)
+#ifndef SQC_CH
+#define SQC_CH 16                 // rows per skipped chunk in the apply (uniform branches;
+                                  // measured at C2: 8 / 16 / 24 / 32 rows -> S2 1.70 / 1.59 / 1.60 / 1.61 ms)
+#endif
 
 RQ_DEV unsigned cl_rank() {
     unsigned r;
@@ -304,20 +308,20 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
         // ---- 2. apply H_j to this thread's column, downdate the norm ---------
         if (act && (int)pc == wcl) act = false;  // retire the pivot
         if (act) {
-            // w = v^T x over rows >= j (xs is zero above row j); 8-row chunks
+            // w = v^T x over rows >= j (xs is zero above row j); SQC_CH-row chunks
             // entirely above row j are skipped (uniform branches)
             // four independent accumulators (row t goes to accumulator t mod 4)
             double d[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int c0 = 0; c0 < L; c0 += 8) {
-                if (j < c0 + 8) {
+            for (int c0 = 0; c0 < L; c0 += SQC_CH) {
+                if (j < c0 + SQC_CH) {
 #pragma unroll
-                    for (int t = c0; t < c0 + 8 && t + 1 < L; t += 2) {
+                    for (int t = c0; t < c0 + SQC_CH && t + 1 < L; t += 2) {
                         const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
                         d[t & 3] += v2.x * x[t];
                         d[(t + 1) & 3] += v2.y * x[t + 1];
                     }
-                    if ((L & 1) && c0 + 8 >= L) d[(L - 1) & 3] += xs[L - 1] * x[L - 1];
+                    if ((L & 1) && c0 + SQC_CH >= L) d[(L - 1) & 3] += xs[L - 1] * x[L - 1];
                 }
             }
             const double tw = tau * ((d[0] + d[1]) + (d[2] + d[3]));
@@ -325,18 +329,18 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
             // inside the one 8-row chunk that holds row j (uniform branch)
             double bj = 0.0;
 #pragma unroll
-            for (int c0 = 0; c0 < L; c0 += 8) {
-                if (j < c0 + 8) {
+            for (int c0 = 0; c0 < L; c0 += SQC_CH) {
+                if (j < c0 + SQC_CH) {
 #pragma unroll
-                    for (int t = c0; t < c0 + 8 && t + 1 < L; t += 2) {
+                    for (int t = c0; t < c0 + SQC_CH && t + 1 < L; t += 2) {
                         const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
                         x[t] -= tw * v2.x;
                         x[t + 1] -= tw * v2.y;
                     }
-                    if ((L & 1) && c0 + 8 >= L) x[L - 1] -= tw * xs[L - 1];
+                    if ((L & 1) && c0 + SQC_CH >= L) x[L - 1] -= tw * xs[L - 1];
                     if (j >= c0) {
 #pragma unroll
-                        for (int t = c0; t < c0 + 8 && t < L; ++t)
+                        for (int t = c0; t < c0 + SQC_CH && t < L; ++t)
                             if (t == j) bj = x[t];
                     }
                 }
