@@ -28,6 +28,7 @@ namespace rq {
 #define SQR_TRACE_DETAIL 0
 #endif
 constexpr int SQR_THREADS = 256;
+constexpr int SQR_CH = 16;  // rows per skipped chunk of the register rows (as SQC_CH)
 constexpr int SQR_UNITS = SQ_MAXL + 2;  // 16-byte units per slot: header (2) + column
 
 // unit = {lo32 | tag << 32, hi32 | tag << 32}
@@ -305,19 +306,19 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
         // ---- 2. apply H_j to this thread's column, downdate the norm ---------
         if (act && (int)pc == wcl) act = false;
         if (act) {
-            // w = v^T x over rows >= j (xs is zero above row j); 8-row chunks
+            // w = v^T x over rows >= j (xs is zero above row j); SQR_CH-row chunks
             // entirely above row j are skipped (uniform branches); four
             // independent accumulators
             double d[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int c0 = 0; c0 < LR; c0 += 8) {
-                if (j < c0 + 8) {
+            for (int c0 = 0; c0 < LR; c0 += SQR_CH) {
+                if (j < c0 + SQR_CH) {
 #pragma unroll
-                    for (int t = c0; t < c0 + 8 && t + 1 < LR; t += 2) {
+                    for (int t = c0; t < c0 + SQR_CH && t + 1 < LR; t += 2) {
                         const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
                         d[(t >> 1) & 3] += v2.x * x[t] + v2.y * x[t + 1];
                     }
-                    if ((LR & 1) && c0 + 8 >= LR) d[0] += xs[LR - 1] * x[LR - 1];
+                    if ((LR & 1) && c0 + SQR_CH >= LR) d[0] += xs[LR - 1] * x[LR - 1];
                 }
             }
             if (LS > 0) {
@@ -335,18 +336,18 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
             // x -= tw v; bj = x(j) picked in the chunk that holds row j
             double bj = 0.0;
 #pragma unroll
-            for (int c0 = 0; c0 < LR; c0 += 8) {
-                if (j < c0 + 8) {
+            for (int c0 = 0; c0 < LR; c0 += SQR_CH) {
+                if (j < c0 + SQR_CH) {
 #pragma unroll
-                    for (int t = c0; t < c0 + 8 && t + 1 < LR; t += 2) {
+                    for (int t = c0; t < c0 + SQR_CH && t + 1 < LR; t += 2) {
                         const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
                         x[t] -= tw * v2.x;
                         x[t + 1] -= tw * v2.y;
                     }
-                    if ((LR & 1) && c0 + 8 >= LR) x[LR - 1] -= tw * xs[LR - 1];
+                    if ((LR & 1) && c0 + SQR_CH >= LR) x[LR - 1] -= tw * xs[LR - 1];
                     if (j >= c0) {
 #pragma unroll
-                        for (int t = c0; t < c0 + 8 && t < LR; ++t) bj = (t == j) ? x[t] : bj;
+                        for (int t = c0; t < c0 + SQR_CH && t < LR; ++t) bj = (t == j) ? x[t] : bj;
                     }
                 }
             }
