@@ -358,7 +358,7 @@ static int tma_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, con
             }
             TmaGemmArgs g{cols, rows, K, 0, 0, 0, 0, A22, lda, rup(K, 32), 1, 0, 0};
             const int64_t tiles = ((rows + BN - 1) / BN) * ((cols + BM - 1) / BM);
-            const int grid = (int)std::min<int64_t>(tiles, ctx->num_sms);
+            const int grid = (int)std::min<int64_t>(tiles, ctx->grid_cap > 0 ? ctx->grid_cap : ctx->num_sms);
             kern<<<grid, WM * WN * 32, smem, ctx->stream>>>(tx, ty, tc, g);
             CKL();
             *done = true;
