@@ -56,7 +56,6 @@ constexpr int CQR_EPT_F = (CQR_MAXB * CQR_MAXB + CQR_THREADS - 1) / CQR_THREADS;
 // ---------------------------------------------------------------------------
 RQ_DEV void tri_inv_upper_smem(double *M, int nb, double *tmp) {
     const int ld = nb, tid = threadIdx.x;
-    const int h = nb / 2;
     // base: 8x8 diagonal blocks, one warp each (lane = column of the block,
     // back substitution down the rows; 8 lanes active)
     {

@@ -78,8 +78,7 @@ __global__ void __launch_bounds__(SQC_THREADS, 1) sample_qrcp_cluster_kernel(SqA
     // one, which holds the ragged remainder of the columns (least apply work)
     const int rg0 = G - 1;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int l = a.l;
-    const int64_t nn = a.nn;
+    const int64_t nn = a.nn;  // (a.l == L: the kernel is instantiated per sample height)
     const int64_t cpb = (nn + G - 1) / G;  // <= 256
     const int64_t c_lo = min(nn, (int64_t)g * cpb), c_hi = min(nn, c_lo + cpb);
     const bool have = tid < (int)(c_hi - c_lo);
