@@ -30,6 +30,7 @@ struct TmaGemmArgs {
     int splits;
     int64_t split_stride;
     int vec2;              // EPI_ACCUM_T_PRE: C 16-byte aligned with even ldc -> double2 accesses
+    int *tile_ctr;         // DYN kernels: tiles are claimed from this zeroed counter (atomicAdd)
 };
 
 RQ_DEV unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -65,7 +66,12 @@ constexpr size_t tma_gemm_smem() {
     return 128 + (size_t)ST * BK * (8 * MT * WM + 8 * NT * WN) * sizeof(double) + ST * sizeof(uint64_t);
 }
 
-template <int MT, int NT, int WM, int WN, int BK, int ST, int EPI>
+// DYN: tiles are claimed dynamically (atomicAdd on g.tile_ctr) instead of the
+// static stride-gridDim walk, so CTAs that become resident late (the GPU is
+// shared with a concurrent kernel) simply take fewer tiles.  The producer
+// thread records each stage's tile in shared memory and ends the stream with
+// a data-less stage (tile -1).  Same per-tile arithmetic: same bits.
+template <int MT, int NT, int WM, int WN, int BK, int ST, int EPI, bool DYN = false>
 __global__ void __launch_bounds__(WM *WN * 32, 1)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY, TmaGemmArgs g) {
     constexpr int BM = 8 * MT * WM;
@@ -114,11 +120,17 @@ __global__ void __launch_bounds__(WM *WN * 32, 1)
         const int64_t kend = min(g.K, it.kbeg + g.k_per_split);
         it.nk = (kend > it.kbeg) ? (kend - it.kbeg + BK - 1) / BK : 0;
     };
+    __shared__ int64_t stage_t[ST];  // DYN: the tile of each stage slot (-1: end of stream)
+    auto next_tile = [&](int64_t cur) -> int64_t {
+        if (DYN) return (int64_t)atomicAdd(g.tile_ctr, 1);
+        return cur + gridDim.x;
+    };
     auto advance = [&](It &it) {
-        if (++it.kc >= it.nk) set_tile(it, it.t + gridDim.x);
+        if (++it.kc >= it.nk) set_tile(it, next_tile(it.t));
     };
     auto issue = [&](const It &it, int slot) {
         const int64_t k0 = it.kbeg + it.kc * BK;
+        if (DYN) stage_t[slot] = it.t;
         mbar_expect_tx(&full[slot], STAGE_BYTES);
 #pragma unroll
         for (int kb = 0; kb < KB; ++kb) {
@@ -128,29 +140,50 @@ __global__ void __launch_bounds__(WM *WN * 32, 1)
     };
 
     It P, Cn;
-    set_tile(P, blockIdx.x);
+    if (tid == 0) set_tile(P, DYN ? next_tile(0) : (int64_t)blockIdx.x);
     set_tile(Cn, blockIdx.x);
     // skip tiles with no K work (cannot happen for K >= 1, kept for safety)
     int64_t sp = 0, sc = 0;
+    bool pend_end = DYN;  // DYN: the end-of-stream stage is still to be issued
+    auto issue_end = [&](int slot) {  // DYN: a data-less stage carrying tile -1
+        stage_t[slot] = -1;
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&full[slot])) : "memory");
+        pend_end = false;
+    };
     if (tid == 0) {
-        for (int s = 0; s < ST - 1 && P.t < ntiles; ++s) {
-            issue(P, (int)(sp % ST));
-            ++sp;
-            advance(P);
+        for (int s = 0; s < ST - 1; ++s) {
+            if (P.t < ntiles) {
+                issue(P, (int)(sp % ST));
+                ++sp;
+                advance(P);
+            } else {
+                if (DYN && pend_end) { issue_end((int)(sp % ST)); ++sp; }
+                break;
+            }
         }
     }
 
     double acc[MT][NT][2];
     double cpre[EPI == EPI_ACCUM_T_PRE ? MT : 1][EPI == EPI_ACCUM_T_PRE ? NT : 1][2];
-    while (Cn.t < ntiles) {
+    while (DYN || Cn.t < ntiles) {
         const int slot = (int)(sc % ST);
         mbar_wait(&full[slot], (unsigned)((sc / ST) & 1));
         __syncthreads();  // everyone is past stage sc-1: its slot may be refilled
-        if (tid == 0 && P.t < ntiles) {
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            issue(P, (int)(sp % ST));
-            ++sp;
-            advance(P);
+        if (DYN) {
+            const int64_t tt = stage_t[slot];
+            if (tt < 0) break;  // uniform: every thread read the same slot
+            if (Cn.kc == 0) set_tile(Cn, tt);
+        }
+        if (tid == 0) {
+            if (P.t < ntiles) {
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                issue(P, (int)(sp % ST));
+                ++sp;
+                advance(P);
+            } else if (DYN && pend_end) {
+                issue_end((int)(sp % ST));
+                ++sp;
+            }
         }
         if (Cn.kc == 0) {
 #pragma unroll
@@ -244,7 +277,11 @@ __global__ void __launch_bounds__(WM *WN * 32, 1)
             }
         }
         ++sc;
-        advance(Cn);
+        if (DYN) {  // the next stage's tile comes from stage_t
+            if (++Cn.kc >= Cn.nk) Cn.kc = 0;
+        } else {
+            advance(Cn);
+        }
     }
 }
 

@@ -47,6 +47,7 @@ struct rqrcp_ctx {
     cudaStream_t upd = nullptr;
     cudaEvent_t ev_r12 = nullptr, ev_upd = nullptr;
     int grid_cap = 0;  // > 0: persistent GEMM grids use at most this many CTAs
+    int *tctr = nullptr;  // per-panel tile counters of the dynamically scheduled bulk update
     bool own_stream = false;
     int nranks = 1, rank = 0;
     int64_t max_m = 0, max_n = 0;
@@ -271,7 +272,7 @@ static int choose_splits(int64_t tiles, int64_t K, int grid, int64_t max_elems_p
     return best;
 }
 
-template <int MT, int NT, int WM, int WN, int EPI>
+template <int MT, int NT, int WM, int WN, int EPI, bool DYN = false>
 static int launch_tma_cfg(rqrcp_ctx *ctx, const double *X, int64_t xdim0, int64_t xdim1, int64_t ldx, const double *Y,
                           int64_t ydim0, int64_t ydim1, int64_t ldy, TmaGemmArgs g, bool *done) {
     constexpr int BK = 32;
@@ -284,7 +285,7 @@ static int launch_tma_cfg(rqrcp_ctx *ctx, const double *X, int64_t xdim0, int64_
     CUtensorMap tx, ty;
     if (!make_tmap(&tx, X, xdim0, xdim1, ldx, BM) || !make_tmap(&ty, Y, ydim0, ydim1, ldy, BN)) return 0;
     const size_t smem = tma_gemm_smem<MT, NT, WM, WN, BK, ST>();
-    auto kern = gemm_tma_kernel<MT, NT, WM, WN, BK, ST, EPI>;
+    auto kern = gemm_tma_kernel<MT, NT, WM, WN, BK, ST, EPI, DYN>;
     static bool attr = false;
     if (!attr) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -338,12 +339,12 @@ static int tma_skinny(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const dou
 // For K > 64 the C tile is moved by TMA as well (gemm_upd_tma_kernel; needs a
 // 16-byte aligned A22 with an even lda); else the register-epilogue kernel.
 static int tma_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, const double *w2, int64_t ldw,
-                      const double *vt, int64_t ldvt, double *A22, int64_t lda, bool *done) {
+                      const double *vt, int64_t ldvt, double *A22, int64_t lda, bool *done, int *tile_ctr = nullptr) {
     *done = false;
     if (rows <= 0 || cols <= 0) { *done = true; return 0; }
     // (measured: faster for K = 128, slower for K = 64 where the two-stage
     // operand ring is too shallow)
-    if (K > 64 && (((uintptr_t)A22 & 15) == 0) && ((lda & 1) == 0)) {
+    if (K > 64 && !tile_ctr && (((uintptr_t)A22 & 15) == 0) && ((lda & 1) == 0)) {
         constexpr int MT = 4, NT = 4, WM = 2, WN = 4, BK = 32, ST = 2;
         constexpr int BM = 8 * MT * WM, BN = 8 * NT * WN;
         CUtensorMap tx, ty, tc;
@@ -371,6 +372,10 @@ static int tma_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, con
     // a short update (the R12 rows of the overlapped schedule): 32 x 64 tiles,
     // twice as many CTAs; same per-element DMMA sequence (same bits)
     if (rows <= 64) return launch_tma_cfg<2, 4, 2, 2, EPI_ACCUM_T_PRE>(ctx, w2, K, cols, ldw, vt, K, rows, ldvt, g, done);
+    if (tile_ctr) {  // dynamic tile claiming (the GPU is shared with a concurrent kernel)
+        g.tile_ctr = tile_ctr;
+        return launch_tma_cfg<4, 4, 2, 4, EPI_ACCUM_T_PRE, true>(ctx, w2, K, cols, ldw, vt, K, rows, ldvt, g, done);
+    }
     return launch_tma_cfg<4, 4, 2, 4, EPI_ACCUM_T_PRE>(ctx, w2, K, cols, ldw, vt, K, rows, ldvt, g, done);
 }
 
@@ -435,6 +440,8 @@ static int free_all(rqrcp_ctx *ctx) {
     if (ctx->h_pairs) cudaFreeHost(ctx->h_pairs);
     if (ctx->hstatus) cudaFreeHost(ctx->hstatus);
     ctx->hstatus = nullptr;
+    if (ctx->tctr) cudaFree(ctx->tctr);
+    ctx->tctr = nullptr;
     void *ptrs[] = {ctx->omt,     ctx->bs[0],   ctx->bs[1],     ctx->vfull,     ctx->vt,        ctx->w,
                     ctx->w2,      ctx->tneg, ctx->ybuf,   ctx->rhat11,    ctx->omhat,     ctx->vhat,      ctx->tauhat,
                     ctx->splitk,  ctx->slot_hdr, ctx->slot_col, ctx->slot_v2,
@@ -612,6 +619,7 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (128 * 128 + 64 * 64) * 8));
     CKC(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     CKC(cudaMallocHost((void **)&ctx->hstatus, sizeof(int) * 8));
+    CKC(cudaMalloc((void **)&ctx->tctr, sizeof(int) * 8192));
     {
         int prio_lo = 0, prio_hi = 0;
         CKC(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
@@ -989,6 +997,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     CK(cudaMemsetAsync(ctx->iscal, 0, sizeof(int) * 8, st));
     const int64_t npanels = (k + b - 1) / b;
     CK(cudaMemsetAsync(ctx->bars, 0, sizeof(unsigned) * 2 * npanels, st));
+    CK(cudaMemsetAsync(ctx->tctr, 0, sizeof(int) * std::min<int64_t>(npanels, 8192), st));
     // ---- S0: Omega^T -----------------------------------------------------
     if (omega_in) {
         omega_t_from_kernel<<<grid_for((int64_t)lpad * m, 256, G), 256, 0, st>>>(omega_in, l, lpad, m, ctx->omt,
@@ -1039,19 +1048,20 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     double *bulk_A22_saved = nullptr;
     int64_t bulk_rows = 0;
     int bulk_bb = 0, bulk_bbpad = 0;
+    int *bulk_dyn = nullptr;  // non-null: dynamically scheduled bulk update (its tile counter)
     auto launch_bulk = [&]() -> int {
         bulk_ready = false;
         CK(cudaStreamWaitEvent(ctx->upd, ctx->ev_r12, 0));
         cudaStream_t keep = ctx->stream;
         ctx->stream = ctx->upd;
-        ctx->grid_cap = G - bulk_cs;
+        ctx->grid_cap = bulk_dyn ? 0 : G - bulk_cs;
         // timed on its own stream: trailing_ms adds the bulk update's duration
         // (concurrent with S2, so the phases sum to more than total_ms)
         ph_begin(ctx, PH_TRAIL);
         bool dn = false;
         const double *vt_b = ctx->vt + (int64_t)bulk_bb * bulk_bbpad;
         int r = tma_update(ctx, bulk_rows, bulk_cols, bulk_bbpad, ctx->w2, bulk_bbpad, vt_b, bulk_bbpad,
-                           bulk_A22_saved + bulk_bb, lda, &dn);
+                           bulk_A22_saved + bulk_bb, lda, &dn, bulk_dyn);
         if (!r && !dn)
             r = gemm_update(ctx, bulk_rows, bulk_cols, bulk_bbpad, ctx->w2, bulk_bbpad, vt_b, bulk_bbpad,
                             bulk_A22_saved + bulk_bb, lda);
@@ -1358,6 +1368,21 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
                 next_cs = (int)std::max<int64_t>(1, (npp + SQC_THREADS - 1) / SQC_THREADS);
                 ovl = !(e1 && e1[0] == '0') && !(e2 && e2[0] == '0') && next_cs <= ctx->sqc_max;
             }
+            // the next sample QRCP on the register grid (C3-sized samples): the bulk
+            // update runs on the whole GPU with dynamically claimed tiles, so the
+            // CTAs that find their SM taken by the sample QRCP start late and take
+            // fewer tiles (bb <= 64: the K <= 64 update kernel)
+            bool dyn = false;
+            if (!ovl && P == 1 && !rule5 && more && npp > 0 && mp > bb && (bb % 2) == 0 && bbpad <= 64 &&
+                !gaps_out && (l == 40 || l == 74)) {
+                const char *e1 = getenv("RQRCP_OVERLAP"), *e2 = getenv("RQRCP_SQ_REG"),
+                           *e3 = getenv("RQRCP_OVERLAP_GRID");
+                const int64_t ngrid = 1 + (npp + SQR_THREADS - 1) / SQR_THREADS;
+                dyn = !(e1 && e1[0] == '0') && !(e2 && e2[0] == '0') && !(e3 && e3[0] == '0') &&
+                      ngrid <= std::min(G, SQ_MAXG) && panels <= 8192;
+                ovl = dyn;
+                next_cs = 0;
+            }
             if (ovl) {
                 rc = tma_update(ctx, bb, npl, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda, &tdone);
                 if (rc) return rc;
@@ -1366,6 +1391,7 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
                 bulk_A22 = A22;
                 bulk_cols = npl;
                 bulk_cs = next_cs;
+                bulk_dyn = dyn ? ctx->tctr + (panels - 1) : nullptr;
             } else {
                 rc = tma_update(ctx, mp, npl, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda, &tdone);
                 if (rc) return rc;

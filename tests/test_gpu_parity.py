@@ -23,7 +23,7 @@ RES_ATOL = 1e-12
 def ctx():
     """Default context: grid-wide (cooperative) sample-QRCP / panel kernels."""
     import paper_1804_05138_b200 as rq
-    c = rq.RQRCP(max_m=5000, max_n=4200, max_b=128, max_p=32)
+    c = rq.RQRCP(max_m=5000, max_n=5000, max_b=128, max_p=32)
     yield c
     c.close()
 
@@ -294,7 +294,11 @@ def test_panel_kernels(ctx, variant, name, kind, m, n, k, b, p, seed):
 
 # ---- the bulk trailing update overlapped with the next sample QRCP (default
 # when that runs on one cluster, P = 1, Eq. (4)) vs the serial schedule.
-OVL_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "lowrank", "kfull")]
+OVL_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "lowrank", "kfull")] + [
+    # n' > 4096: the next sample QRCP runs on the register grid, the bulk update
+    # with dynamically claimed tiles beside it
+    ("ovl_grid74", "iid", 700, 4700, 192, 64, 10, 28),
+]
 
 
 @pytest.mark.parametrize("overlap", ["1", "0"])
@@ -309,6 +313,21 @@ def test_overlap_schedule(ctx, overlap, name, kind, m, n, k, b, p, seed):
     finally:
         os.environ.pop("RQRCP_OVERLAP", None)
     compare(A, g, o, k)
+
+
+def test_overlap_grid_bitwise_equal_serial(ctx):
+    """The dynamically scheduled bulk update (grid sample QRCP) gives the same bits."""
+    import os
+    A = inputs.make("graded", 800, 4800, 29).numpy()
+    outs = []
+    for ov in ("1", "0"):
+        os.environ["RQRCP_OVERLAP"] = ov
+        try:
+            outs.append(gpu_factor(ctx, A, 256, 64, 10, 29))
+        finally:
+            os.environ.pop("RQRCP_OVERLAP", None)
+    assert np.array_equal(outs[0]["jpvt"], outs[1]["jpvt"])
+    assert np.array_equal(outs[0]["A"], outs[1]["A"])
 
 
 def test_overlap_bitwise_equal_serial(ctx):
