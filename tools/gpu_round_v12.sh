@@ -1,4 +1,4 @@
-# Round-end evidence run (v11): GPU tests, smoke, bench lines for C2-C5, the ncu
+# Round-end evidence run (v12): GPU tests, smoke, bench lines for C2-C5, the ncu
 # launch list of the bench command, one ncu --set full capture of the
 # latency-bound cluster kernels.
 set -x
