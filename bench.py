@@ -2,21 +2,29 @@
 """Benchmark of the RQRCP hot path (BASELINE.json metric: "RQRCP fp64
 GFLOP/s and sec-to-rank-k at 1/2/4/8 B200; % of FP64 peak").
 
-A step = one full rqrcp_factor (all hot-path rows S0..S7 of SURVEY.md §8(a))
-on the configuration's synthetic A, resident in HBM.  Default workload:
-configs[1] = C2 (4096^2, k=512, b=64, p=10, A iid N(0,1)).
+A step = one full rqrcp_factor (every hot-path row S0..S7 of SURVEY.md §8(a))
+on the configuration's synthetic A, resident in HBM.  Default workload: C4
+(configs[3]: 32768^2, k = 8192, b = 128, p = 16, A = U diag(1/j) V^T), the
+largest BASELINE config whose metric is quoted on "1/2/4/8 GPUs".
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+--gpus N > 1 without a torchrun environment re-launches itself under
+torch.distributed.run (N ranks, 127.0.0.1); under torchrun WORLD_SIZE must
+equal N.  The matrix is sharded 1D column-block-cyclic (block b) and the
+library exchanges the sample / panel / pivot columns over NCCL: one
+factorization of the whole matrix per step (strong scaling).
 
 Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle (the
-deliberately slow, unblocked reference of this tier) on the host cores.
+deliberately slow, unblocked reference of this tier) on the host cores, on a
+bounded sample of the same workload (see cpu_sample()).
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -28,33 +36,35 @@ sys.path.insert(0, ROOT)
 METRIC = "rqrcp_fp64_gflops"
 UNIT = "GFLOP/s"
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+MICROBENCH = os.path.join(ROOT, "profiles", "r01_microbench.json")
+PROFILE_TRAFFIC = os.path.join(ROOT, "profiles", "traffic_r02.json")
 FP64_NOMINAL_OVER_BF16 = 45.0 / 2250.0  # blackwell guide: B200 FP64 tensor 45 TF vs bf16 2.25 PF dense
-PROFILE_TRAFFIC = os.path.join(ROOT, "profiles", "traffic_r01.json")
+DEFAULT_CONFIG = "C4"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     return ap.parse_args()
 
 
-def flops_of(cfg):
-    import paper_1804_05138_b200 as rq
-    return rq.rqrcp_flops(cfg["m"], cfg["n"], cfg["k"], cfg["b"], cfg["p"])
+def config_dict(cfg):
+    """The workload description, identical in both arms."""
+    return {"workload": cfg["name"], "m": cfg["m"], "n": cfg["n"], "k": cfg["k"], "b": cfg["b"], "p": cfg["p"],
+            "input": cfg["kind"], "seed": cfg["seed"]}
 
 
-def alg_flops_host(cfg):
-    """F_alg from the closed forms; used by the reference arm
-    (which must not load the CUDA library)."""
-    m, n, k, b, p = cfg["m"], cfg["n"], cfg["k"], cfg["b"], cfg["p"]
+def alg_flops(m, n, k, b, p):
+    """F_alg = F_sketch + F_qr + F_sQRCP + F_sUpd (closed forms of SURVEY.md
+    §8(d)); the reference arm must not load the CUDA library."""
     l = b + p
     f = 2.0 * l * m * n + sum(4.0 * (m - j) * (n - j) for j in range(k))
     for i in range(0, k, b):
@@ -68,6 +78,14 @@ def host_cores():
         return len(os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count() or 1
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
 
 
 class ClockSampler:
@@ -124,9 +142,6 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-MICROBENCH = os.path.join(ROOT, "profiles", "r01_microbench.json")
-
-
 def fp64_peak():
     """FP64 peak for the roofline.  MEASURED_PEAKS.json has no FP64 entry; we
     use our own measurement of the DMMA.8x8x4 pipe on this pool's B200s
@@ -165,63 +180,125 @@ def measured_dgemm_tflops(device):
     return 2.0 * n ** 3 / (best * 1e-3) / 1e12
 
 
-def cpu_baseline(cfg, budget_s):
-    """The oracle as it stands on this host's cores: full factorizations of the
-    same workload, repeated until ~budget_s (at least one)."""
+# ---------------------------------------------------------------------------
+# The oracle's bounded sample of a workload (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+SAMPLE_MAX_COLS = 4096
+
+
+def cpu_sample(cfg):
+    """A bounded sample of the workload for the unblocked CPU oracle: the
+    first min(n, 4096) columns of the config's A (same recipe, seed, m, b, p)
+    factored to k' = min(k, b) -- one pivot panel of Alg. 2 at the config's
+    full row count.  Returns (A_sample numpy, k', description)."""
+    import torch
+
     import inputs
+    m, n, k, b, p = cfg["m"], cfg["n"], cfg["k"], cfg["b"], cfg["p"]
+    nc = min(n, SAMPLE_MAX_COLS)
+    kp = min(k, b, nc)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    A = inputs.make(cfg["kind"], m, n, cfg["seed"], device=dev)
+    As = A[:, :nc].cpu().numpy().copy(order="F")
+    del A
+    if dev == "cuda":
+        torch.cuda.empty_cache()
+    desc = (f"{cfg['name']} recipe, first {nc} of {n} columns ({m} x {nc}), prefix k'={kp} (one b={b} panel), "
+            f"p={p}; plain unblocked C oracle")
+    return As, kp, desc
+
+
+def time_oracle(As, kp, cfg, reps=None, budget_s=None, warmup=0):
     import oracle
-    A = inputs.make(cfg["kind"], cfg["m"], cfg["n"], cfg["seed"]).numpy()
-    f = alg_flops_host(cfg)
     oracle.lib()
+    m, nc = As.shape
+    f = alg_flops(m, nc, kp, cfg["b"], cfg["p"])
+    for _ in range(warmup):
+        oracle.rqrcp(As, kp, cfg["b"], cfg["p"], seed=cfg["seed"])
     times = []
     t_all = time.perf_counter()
     while True:
         t0 = time.perf_counter()
-        oracle.rqrcp(A, cfg["k"], cfg["b"], cfg["p"], seed=cfg["seed"])
+        oracle.rqrcp(As, kp, cfg["b"], cfg["p"], seed=cfg["seed"])
         times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_all > budget_s or len(times) >= 20:
+        if reps is not None and len(times) >= reps:
+            break
+        if budget_s is not None and (time.perf_counter() - t_all > budget_s or len(times) >= 20):
             break
     t = sum(times) / len(times)
     thr = int(os.environ.get("OMP_NUM_THREADS", host_cores()))
-    return {"value": f / t / 1e9, "unit": UNIT, "cores": thr, "kind": "oracle",
-            "sample": f"{len(times)} full {cfg['name']} factorizations ({cfg['m']}x{cfg['n']}, k={cfg['k']}), "
-                      f"mean {t:.2f} s each"}
+    return f / t / 1e9, t, len(times), thr, f
+
+
+def cpu_baseline(cfg, budget_s):
+    As, kp, desc = cpu_sample(cfg)
+    v, t, reps, thr, f = time_oracle(As, kp, cfg, budget_s=budget_s)
+    return {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
+            "sample": f"{desc}; {reps} runs, mean {t:.2f} s ({f:.3e} flop each)"}
 
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import inputs
-    import oracle
-    A = inputs.make(cfg["kind"], cfg["m"], cfg["n"], cfg["seed"]).numpy()
-    oracle.lib()
-    for _ in range(args.warmup):
-        oracle.rqrcp(A, cfg["k"], cfg["b"], cfg["p"], seed=cfg["seed"])
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        oracle.rqrcp(A, cfg["k"], cfg["b"], cfg["p"], seed=cfg["seed"])
-    dt = (time.perf_counter() - t0) / args.steps
-    f = alg_flops_host(cfg)
-    v = f / dt / 1e9
-    thr = int(os.environ.get("OMP_NUM_THREADS", host_cores()))
+    As, kp, desc = cpu_sample(cfg)
+    v, t, reps, thr, f = time_oracle(As, kp, cfg, reps=args.steps, warmup=args.warmup)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["name"], "m": cfg["m"], "n": cfg["n"], "k": cfg["k"], "b": cfg["b"],
-                   "p": cfg["p"], "input": cfg["kind"], "sec_to_rank_k": dt},
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(cfg),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
-                         "sample": f"full {cfg['name']} factorization per step (plain unblocked C oracle)"},
+                         "sample": f"{desc}; one sample factorization per step ({f:.3e} flop)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def roofline_s5(cfg, world, s5_ms, peak, peak_src):
+    """S5 trailing update (>= 90% of the flops, 98% at C4/C5): algorithmic
+    flops 4 m' bb n'' + 2 bb^2 n'' per panel (W = V^T A22, W2 = -T^T W,
+    A22 += V W2) divided by the CUDA-event time of the S5 kernels on the
+    streams that run them; traffic = ncu DRAM bytes of those kernels on one
+    captured panel (profiles/traffic_r02.json) beside that panel's
+    algorithmic bytes (24 m' n'': A22 read twice, written once)."""
+    m, n, k, b = cfg["m"], cfg["n"], cfg["k"], cfg["b"]
+    fl = 0.0
+    for i in range(0, k, b):
+        bb = min(b, k - i)
+        fl += (4.0 * (m - i) * bb * (n - i - bb) + 2.0 * bb * bb * (n - i - bb)) / world
+    achieved = fl / (s5_ms * 1e-3) / 1e12 if s5_ms > 0 else 0.0
+    traffic, alg_panel, tsrc = None, None, None
+    try:
+        tr = json.load(open(PROFILE_TRAFFIC)).get(cfg["name"])
+        if tr and world == 1:
+            traffic, alg_panel, tsrc = tr["dram_bytes_per_panel"], tr["alg_bytes_per_panel"], tr["source"]
+    except Exception:
+        pass
+    return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak if peak else None, "traffic": traffic,
+            "kernel": "S5 trailing update (W = V^T A22 split-K, W2 = -T^T W, A22 += V W2; DMMA.8x8x4 via TMA)",
+            "flops_per_step": fl, "peak_source": peak_src,
+            "traffic_unit": "DRAM bytes per panel (ncu, S5 kernels of one panel)",
+            "algorithmic_bytes_per_panel": alg_panel, "traffic_source": tsrc}
 
 
 def main():
     args = parse()
     import inputs
+    if args.config not in inputs.CONFIGS:
+        raise SystemExit(f"unknown config {args.config}")
     cfg = dict(inputs.CONFIGS[args.config])
     cfg["name"] = args.config
+
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        # launch N ranks ourselves (one process per GPU, 127.0.0.1 rendezvous)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    world = int(world_env or "1")
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+
     if args.impl == "reference":
         return run_reference(args, cfg)
 
@@ -229,7 +306,6 @@ def main():
     import torch.distributed as dist
 
     import paper_1804_05138_b200 as rq
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -238,9 +314,6 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     m, n, k, b, p, seed = cfg["m"], cfg["n"], cfg["k"], cfg["b"], cfg["p"], cfg["seed"]
 
-    # one factorization of the config matrix per step; with N GPUs it is
-    # sharded 1D column-block-cyclic (block b) and the library exchanges the
-    # sample / panel / swapped columns over NCCL (strong scaling)
     A0 = inputs.make(cfg["kind"], m, n, seed, device=dev)
     uid = None
     if world > 1:
@@ -249,19 +322,26 @@ def main():
         obj = [rq.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    n_loc = A0.shape[1]
+    torch.cuda.empty_cache()
     A = A0.t().clone().t()  # working copy, column-major
     ctx = rq.RQRCP(max_m=m, max_n=n, max_b=b, max_p=p, device=local, nranks=world, rank=rank, nccl_uid=uid)
     jpvt = torch.empty(n, dtype=torch.int64, device=dev)
     tau = torch.empty(k, dtype=torch.float64, device=dev)
-    fl = flops_of(cfg)
-    F = fl["total"]
+    F = rq.rqrcp_flops(m, n, k, b, p)["total"]
+    st = ctx.stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
 
-    def step():
-        A.copy_(A0)
+    def step(evs=None):
+        # restore A (untimed: A is 8mn bytes >= L2, so every step starts cold)
+        with torch.cuda.stream(st):
+            A.copy_(A0)
+        if evs:
+            evs[0].record(st)
         rc, rk = ctx.factor_raw(A.data_ptr(), m, m, n, k, b, p, seed, jpvt.data_ptr(), tau.data_ptr())
+        if evs:
+            evs[1].record(st)
         if rc not in (0, rq.RQRCP_W_RANK_DEFICIENT):
-            raise RuntimeError(f"rqrcp_factor failed: {rc}")
+            raise RuntimeError(f"rqrcp_factor failed: {rc} {ctx.last_error()}")
 
     for _ in range(args.warmup):
         step()
@@ -270,103 +350,76 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    phases = {}
-    launches = 0
-    e0.record(ctx.stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(ctx.stream)
+    for s in range(args.steps):
+        step(ev[s])
     torch.cuda.synchronize()
-    # per-phase times: the library's events of the last step (every step is the
-    # same workload); read after the timed region, outside it
-    t = ctx.timings()
-    for kk, v in t.items():
-        if kk.endswith("_ms"):
-            phases[kk] = v * args.steps
-    launches = (t["kernel_launches"] + 1) * args.steps  # + the restore copy
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
-    ms = e0.elapsed_time(e1) / args.steps
+    step_ms = [a.elapsed_time(z) for a, z in ev]
+    ms = sum(step_ms) / len(step_ms)
+    # per-phase times: the library's events of the last step (every step is the
+    # same workload); read after the timed region
+    t = ctx.timings()
+    phases = {kk: v for kk, v in t.items() if kk.endswith("_ms")}
+    launches = t["kernel_launches"] * args.steps
     if world > 1:
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     value = F / (ms * 1e-3) / 1e9  # one factorization of the whole matrix per step
 
-    # dominant kernel roofline: the trailing update (FP64 DMMA contraction)
-    tr_ms = phases.get("trailing_ms", 0.0) / args.steps
-    tr_flops = 0.0
-    for i in range(0, k, b):
-        bb = min(b, k - i)
-        mp, npp = m - i, n - i - bb
-        bbpad = (bb + 7) // 8 * 8
-        tr_flops += (4.0 * mp * bb * npp + 2.0 * bb * bb * npp) / world  # this rank's share
     peak, peak_src = fp64_peak()
-    achieved = tr_flops / (tr_ms * 1e-3) / 1e12 if tr_ms > 0 else 0.0
-    traffic = None
-    try:  # ncu dram__bytes_read + dram__bytes_write of the S5 kernels per panel (profiles/traffic_r01.json)
-        traffic = json.load(open(PROFILE_TRAFFIC)).get(args.config, {}).get("dram_bytes_per_panel_trailing")
-    except Exception:
-        pass
-    # algorithmic S5 bytes per panel (unfused: A22 read twice, written once)
-    alg_bytes = 0.0
-    for i in range(0, k, b):
-        bb = min(b, k - i)
-        alg_bytes += 24.0 * (m - i) * (n - i - bb) / world
-    alg_bytes /= max(1, (k + b - 1) // b)
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak if peak else None, "traffic": traffic,
-                "kernel": "S5 trailing update (W = V^T A22, W2 = -T^T W, A22 += V W2; DMMA.8x8x4)",
-                "peak_source": peak_src, "traffic_unit": "DRAM bytes per panel (ncu, S5 kernels)",
-                "algorithmic_bytes_per_panel": alg_bytes}
-    whole_frac = (F / (ms * 1e-3) / 1e12) / peak
+    roofline = roofline_s5(cfg, world, phases.get("trailing_ms", 0.0), peak, peak_src)
+    whole_frac = (F / (ms * 1e-3) / 1e12) / (peak * world)
 
     e2e = None
     if not args.no_e2e and world == 1:
+        del A
+        torch.cuda.empty_cache()
         Ah = torch.empty(n, m, dtype=torch.float64, pin_memory=True).t()
         Ah.copy_(A0.cpu())
         Ao = torch.empty(n, m, dtype=torch.float64, pin_memory=True).t()
         jh = torch.empty(n, dtype=torch.int64, pin_memory=True)
         th = torch.empty(k, dtype=torch.float64, pin_memory=True)
-        import ctypes
-        L = rq.lib()
-        rk = ctypes.c_int64()
-        L.rqrcp_factor_host(ctx._h, Ah.data_ptr(), m, m, n, k, b, p, seed, Ao.data_ptr(), jh.data_ptr(),
-                            th.data_ptr(), ctypes.byref(rk))
+        ctx.factor_host(Ah, k, b, p, seed=seed, out=Ao, jpvt=jh, tau=th)  # warm (allocates the device copy)
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            rc = L.rqrcp_factor_host(ctx._h, Ah.data_ptr(), m, m, n, k, b, p, seed, Ao.data_ptr(), jh.data_ptr(),
-                                     th.data_ptr(), ctypes.byref(rk))
-            assert rc in (0, rq.RQRCP_W_RANK_DEFICIENT), rc
+            ctx.factor_host(Ah, k, b, p, seed=seed, out=Ao, jpvt=jh, tau=th)
         te = (time.perf_counter() - t0) / args.e2e_steps
         e2e = {"value": F / te / 1e9, "unit": UNIT, "h2d_bytes_per_step": 8 * m * n,
-               "d2h_bytes_per_step": 8 * m * n + 8 * n + 8 * k, "ms_per_step": te * 1e3}
+               "d2h_bytes_per_step": 8 * m * n + 8 * n + 8 * k, "ms_per_step": te * 1e3,
+               "path": "rqrcp_factor_host (pinned host A in, factored A / jpvt / tau out; copies timed)"}
+        del Ah, Ao
 
     dgemm = None
     try:
-        dgemm = measured_dgemm_tflops(dev)
+        if rank == 0:
+            dgemm = measured_dgemm_tflops(dev)
     except Exception:
         pass
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        del A0
+        torch.cuda.empty_cache()
         cpu = cpu_baseline(cfg, args.cpu_budget_s)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["name"], "m": m, "n": n, "k": k, "b": b, "p": p, "input": cfg["kind"],
-                       "sec_to_rank_k": ms * 1e-3, "flops_per_step": F,
-                       "l2": "A (8mn bytes) restored from a pristine copy every step, inputs >= L2",
-                       "parallelism": f"1d-block-cyclic-nccl{world}" if world > 1 else "single"},
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(cfg),
+            "sec_to_rank_k": ms * 1e-3, "flops_per_step": F,
+            "parallelism": f"1d-block-cyclic-nccl{world}" if world > 1 else "single",
+            "timing": "CUDA events around each rqrcp_factor on the context stream; A (8mn bytes >> L2) restored "
+                      "from a pristine copy before every step, outside the events",
+            "step_ms": step_ms,
             "roofline": roofline,
             "fp64_frac_whole_step": whole_frac,
             "fp64_dgemm_measured_tflops": dgemm,
-            "phases_ms_per_step": {kk: v / args.steps for kk, v in phases.items()},
+            "phases_ms_per_step": phases,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

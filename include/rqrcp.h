@@ -111,8 +111,13 @@ int rqrcp_create(rqrcp_ctx **ctx, const rqrcp_config *cfg);
  * Synchronous: returns after the work on the context's stream completed.
  * Argument codes: -1 ctx, -2 A, -3 lda, -4 m, -5 n, -6 k, -7 b, -8 p,
  * -10 jpvt, -11 tau, -12 rank_out.  Returns RQRCP_W_RANK_DEFICIENT when the
- * sample's column norms all fall below 1e3*eps*||Omega A||_F before k pivots
- * (outputs valid for the first *rank_out columns, tau = 0 beyond). */
+ * factorization stopped before k columns (reading R-G12): either every
+ * candidate sample column norm fell below 1e3*eps*||Omega A||_F, or a
+ * panel's R11 diagonal entry |R(j,j)| fell below 1e3*eps*||A(i:m, i:i+bb)||_F
+ * (the panel after its swaps).  Outputs are valid for the first
+ * *rank_out columns (tau = 0 beyond; A(rank:m, rank:n) is the trailing matrix
+ * after rank reflectors).  Multi-GPU: NCCL errors are polled while the call
+ * waits and the communicator is aborted after nccl_timeout_ms (RQRCP_E_NCCL). */
 int rqrcp_factor(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
                  uint64_t seed, int64_t *jpvt, double *tau, int64_t *rank_out);
 
@@ -125,14 +130,66 @@ int rqrcp_factor_host(rqrcp_ctx *ctx, const double *A_host, int64_t lda, int64_t
                       int b, int p, uint64_t seed, double *A_out_host, int64_t *jpvt_host, double *tau_host,
                       int64_t *rank_out);
 
-/* Testing API: rqrcp_factor with optional hooks.
- *   omega_in   device l x m (ld = l) sketch to use instead of the Philox draw, or NULL
- *   omega_out  device l x m (ld = l) receives the Omega used, or NULL
- *   gaps_out   device double[k]: per pivot step, relative gap (best - runner-up)/best
- *              of the squared sample norms (diagnoses ties), or NULL */
+/* Testing API: per-panel trace of the factorization.
+ * Panels t in [first_panel, first_panel + npanels) are recorded; each output
+ * pointer may be NULL.  Panel t starts at column i = t*b with width
+ * bb = min(b, k - i); l = b + p.
+ *   pivots  device int64[npanels * b]: entry [(t - first_panel) b + q], q < bb:
+ *           the input column placed at position i + q by this panel's swaps
+ *           (= the final jpvt[i + q]) -- the pivots the sample QRCP chose;
+ *   rhat    device double[npanels * l * n]: block t - first_panel (stride l n)
+ *           holds the l x (n - i) sample right after the panel's sample QRCP
+ *           (Alg. 2 line P:147), column-major ld l, in PIVOTED column order:
+ *           R-hat = [R-hat11 R-hat12; 0 R-hat22] with zeros below
+ *           the diagonal of the first bb columns;
+ *   bnext   device double[npanels * l * n]: block t - first_panel holds the
+ *           l x (n - i - bb) sample after the update of Eq. (4) or
+ *           Eq. (5), ld l (untouched when no update follows: the
+ *           last panel, reading R-G9, or an early stop);
+ *   recorded  (out) number of panels recorded.
+ * With nranks > 1 every rank records the replicated sample. */
+typedef struct rqrcp_trace {
+    int64_t first_panel;
+    int64_t npanels;
+    int64_t *pivots;
+    double *rhat;
+    double *bnext;
+    int64_t recorded;
+} rqrcp_trace;
+
+/* Testing API: rqrcp_factor with optional hooks (every one may be NULL).
+ *   omega_in   device l x m (ld = l) sketch to use instead of the Philox draw
+ *   omega_out  device l x m (ld = l) receives the Omega used
+ *   trace      per-panel pivots and sample snapshots (rqrcp_trace above)
+ * Same kernels and schedule as rqrcp_factor (the hooks only add copies). */
 int rqrcp_factor_ex(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
                     uint64_t seed, int64_t *jpvt, double *tau, int64_t *rank_out, const double *omega_in,
-                    double *omega_out, double *gaps_out);
+                    double *omega_out, rqrcp_trace *trace);
+
+/* Testing / diagnosis API: a launch-path option of ctx, applied to
+ * subsequent calls (defaults are the measured best; every variant computes
+ * the same factorization).  Returns 0, -1 (ctx null), -2 (unknown name) or
+ * -3 (value out of range).  Names (initial values from the environment
+ * variable RQRCP_<NAME upper-cased> at create time):
+ *   schedule      -1 auto, 0 serial, 1 the bulk trailing update overlaps the
+ *                 next sample QRCP, 2 ... overlaps the next panel QR (look-ahead)
+ *   panel         0 column-by-column Householder, 1 CholeskyQR2 + reconstruction,
+ *                 2 CholeskyQR2 from 8192 rows
+ *   pn_cluster, pn_cpt, pn_grid, pn_rows, la_panel_ctas   panel kernel choice / shape
+ *   sq_cluster, sq_reg, sq_grid, sq_nsm, sq_hstride, sq_poll   sample QRCP kernel choice / shape
+ *   debug_sync    synchronise after every launch
+ *   nccl_timeout_ms   multi-GPU: abort the communicator when a call exceeds it */
+int rqrcp_set_option(rqrcp_ctx *ctx, const char *name, int64_t value);
+
+/* Testing API (multi-rank logic on ONE GPU): create nranks contexts on
+ * cfg->device that form one in-process group; their collectives are host
+ * rendezvous + device copies (no kernel waits on another rank's kernel).
+ * Each context must be driven by its own host thread, all calling the same
+ * rqrcp_factor concurrently with their shards (layout as for NCCL ranks).
+ * cfg->nranks / rank / nccl_uid / stream are ignored (each context owns a
+ * stream).  ctxs: host array of nranks pointers (out).  Returns 0, -1, -2
+ * (cfg invalid or nranks < 2 or > 16) or RQRCP_E_*. */
+int rqrcp_create_loopback_group(rqrcp_ctx **ctxs, int nranks, const rqrcp_config *cfg);
 
 /* Testing/bench API: rows [row0, row0+rows) x cols [col0, col0+cols) of the
  * N(0,1) matrix (seed, stream) with the Omega generator, into out (device,

@@ -333,14 +333,46 @@ int oracle_rqrcp(int64_t m, int64_t n, int64_t k, int b, int p, uint64_t seed, c
                 if (t > j) COL(Bcur, l, t, j) = 0.0;
             }
 
-        /* O5: unblocked Householder on the panel A(i:m, i:i+bb),
-         * each H_j applied to every column right of j (dgeqr2 order) */
+        /* O5: unblocked Householder QR of the panel A(i:m, i:i+bb) (P:149,
+         * LAPACK dgeqr2: each H_j applied to the panel columns right of j),
+         * then the trailing update A(i:m, i+bb:n) <- Q~^T A(i:m, i+bb:n)
+         * column by column: H_i, ..., H_{i+bb-1} in order on each
+         * trailing column.  Each column sees exactly the same sequence of
+         * reflector applications as in the all-columns dgeqr2 order (columns
+         * are independent), so the bits are those of dgeqr2 on A(i:m, i:n).
+         * R11-diagonal rank stop (reading R-G12b, "singular R11 panel
+         * (diagonal entry below 1e3 eps ||panel||)"): before column j is
+         * transformed, |R(j,j)| = |beta_j| is compared with
+         * 1e3 eps ||A(i:m, i:i+bb)||_F (the panel after its swaps); below it,
+         * the factorization stops with rank j: column j and the rest of the
+         * panel keep the reflectors < j (tau = 0 from j on), the trailing
+         * columns get the reflectors < j. */
+        double pan2 = 0.0;
+        for (int64_t c = i; c < i + bb; ++c)
+            for (int64_t r = i; r < m; ++r) pan2 += COL(A, lda, r, c) * COL(A, lda, r, c);
+        const double ptol2 = (1e3 * eps) * (1e3 * eps) * pan2;
+        int64_t diag_stop = -1;
+        int64_t jend = i + bb;  /* reflectors i..jend-1 were formed */
         for (int64_t j = i; j < i + bb; ++j) {
             double *x = &COL(A, lda, j, j);
+            double xn2 = 0.0;
+            for (int64_t t = 1; t < m - j; ++t) xn2 += x[t] * x[t];
+            const double alpha = x[0];
+            const double beta = (xn2 == 0.0) ? alpha : ((alpha >= 0.0) ? -sqrt(alpha * alpha + xn2)
+                                                                         : sqrt(alpha * alpha + xn2));
+            if (beta * beta < ptol2) { diag_stop = j; jend = j; break; }
             double tj = oracle_dlarfg(m - j, x);
             tau[j] = tj;
+            for (int64_t c = j + 1; c < i + bb; ++c) oracle_apply_reflector(m - j, x + 1, tj, &COL(A, lda, j, c));
+        }
 #pragma omp parallel for schedule(static)
-            for (int64_t c = j + 1; c < n; ++c) oracle_apply_reflector(m - j, x + 1, tj, &COL(A, lda, j, c));
+        for (int64_t c = i + bb; c < n; ++c)
+            for (int64_t j = i; j < jend; ++j)
+                oracle_apply_reflector(m - j, &COL(A, lda, j + 1, j), tau[j], &COL(A, lda, j, c));
+        if (diag_stop >= 0) {
+            if (cb) cb(user, i, bb, l, mp, np, Bcur, NULL, NULL, NULL, A, lda);
+            *rank_out = diag_stop;
+            break;
         }
 
         const int64_t npp = np - bb; /* n'' */

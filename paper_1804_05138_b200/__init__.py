@@ -49,7 +49,28 @@ class RqrcpTimings(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+class RqrcpTrace(ctypes.Structure):
+    _fields_ = [("first_panel", ctypes.c_int64), ("npanels", ctypes.c_int64), ("pivots", ctypes.c_void_p),
+                ("rhat", ctypes.c_void_p), ("bnext", ctypes.c_void_p), ("recorded", ctypes.c_int64)]
+
+
 _lib = None
+
+
+def _nccl_hint():
+    """Point the library at the NCCL torch uses (the nvidia-nccl wheel), unless
+    RQRCP_NCCL_LIB is set; the library dlopen()s it for nranks > 1 only."""
+    if os.environ.get("RQRCP_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl
+        for d in list(getattr(nvidia.nccl, "__path__", [])):
+            cand = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["RQRCP_NCCL_LIB"] = cand
+                return
+    except Exception:
+        pass
 
 
 def lib():
@@ -58,12 +79,15 @@ def lib():
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        _nccl_hint()
         L = ctypes.CDLL(LIB_PATH)
         i64, vp, ip = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
         L.rqrcp_create.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(RqrcpConfig)]
         L.rqrcp_factor.argtypes = [vp, vp, i64, i64, i64, i64, ip, ip, ctypes.c_uint64, vp, vp,
                                    ctypes.POINTER(i64)]
-        L.rqrcp_factor_ex.argtypes = L.rqrcp_factor.argtypes + [vp, vp, vp]
+        L.rqrcp_factor_ex.argtypes = L.rqrcp_factor.argtypes + [vp, vp, ctypes.POINTER(RqrcpTrace)]
+        L.rqrcp_set_option.argtypes = [vp, ctypes.c_char_p, i64]
+        L.rqrcp_create_loopback_group.argtypes = [ctypes.POINTER(vp), ip, ctypes.POINTER(RqrcpConfig)]
         L.rqrcp_factor_host.argtypes = [vp, vp, i64, i64, i64, i64, ip, ip, ctypes.c_uint64, vp, vp, vp,
                                         ctypes.POINTER(i64)]
         L.rqrcp_fill_gaussian.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint32, i64, i64, i64, i64, vp, i64]
@@ -90,6 +114,7 @@ def lib():
 
 
 EXPORTED = ["rqrcp_create", "rqrcp_factor", "rqrcp_factor_host", "rqrcp_factor_ex", "rqrcp_fill_gaussian",
+            "rqrcp_set_option", "rqrcp_create_loopback_group",
             "rqrcp_philox_words", "rqrcp_flops", "rqrcp_get_timings", "rqrcp_set_timing", "rqrcp_set_update_rule", "rqrcp_srqr_verify",
             "rqrcp_form_q1", "rqrcp_cx", "rqrcp_destroy",
             "rqrcp_last_error", "rqrcp_version", "rqrcp_shard_columns", "rqrcp_shard_global_index",
@@ -131,7 +156,22 @@ def _check_colmajor(A):
     if A.stride(0) != 1 and m > 1:
         raise ValueError("A must be column-major (stride(0) == 1)")
     lda = A.stride(1) if n > 1 else max(m, 1)
-    return m, n, max(lda, m, 1)
+    if n > 1 and lda < max(m, 1):
+        # an expanded (stride-0) or overlapping view would be read and written
+        # out of bounds by the library
+        raise ValueError(f"column stride {lda} < rows {m}: overlapping or expanded view")
+    return m, n, max(lda, 1)
+
+
+def _check_vec(name, t, dtype, count, device):
+    """Validate a caller-supplied output vector (dtype, length, device)."""
+    import torch
+    if not isinstance(t, torch.Tensor) or t.dtype != dtype:
+        raise TypeError(f"{name} must be a {dtype} torch tensor")
+    if t.dim() != 1 or t.numel() < count or (t.numel() > 1 and t.stride(0) != 1):
+        raise ValueError(f"{name} must be a contiguous 1-D tensor with >= {count} elements")
+    if t.device != device:
+        raise ValueError(f"{name} is on {t.device}, the context runs on {device}")
 
 
 class RQRCP:
@@ -162,25 +202,35 @@ class RQRCP:
             raise RqrcpError(rc, "rqrcp_create failed")
         self._h = h
 
+    def last_error(self):
+        msg = lib().rqrcp_last_error(self._h)
+        return msg.decode() if msg else ""
+
     def _err(self, rc):
         msg = lib().rqrcp_last_error(self._h)
         return RqrcpError(rc, msg.decode() if msg else "")
 
-    def factor(self, A, k, b, p, seed=0, jpvt=None, tau=None, omega=None, omega_out=None, gaps=None,
+    def factor(self, A, k, b, p, seed=0, jpvt=None, tau=None, omega=None, omega_out=None, trace=None,
                allow_rank_deficient=True, n=None):
         """Factor A in place (Alg. 2).  Returns (jpvt, tau, rank).
 
         Multi-GPU (nranks > 1): A is this rank's shard (shard_columns(n, b,
-        nranks, rank)) and n the global column count."""
+        nranks, rank)) and n the global column count.  trace: a Trace (see
+        make_trace) filled per panel (testing hook of rqrcp_factor_ex)."""
         import torch
         m, n_loc, lda = _check_colmajor(A)
+        if A.device != self.device:
+            raise ValueError(f"A is on {A.device}, the context runs on {self.device}")
         n = n_loc if n is None else n
         if jpvt is None:
             jpvt = torch.empty(n, dtype=torch.int64, device=A.device)
         if tau is None:
             tau = torch.empty(max(k, 1), dtype=torch.float64, device=A.device)
+        _check_vec("jpvt", jpvt, torch.int64, n, self.device)
+        _check_vec("tau", tau, torch.float64, max(k, 1), self.device)
+        self._order_after_caller()
         rank = ctypes.c_int64(0)
-        if omega is None and omega_out is None and gaps is None:
+        if omega is None and omega_out is None and trace is None:
             rc = lib().rqrcp_factor(self._h, A.data_ptr(), lda, m, n, k, b, p, seed, jpvt.data_ptr(),
                                     tau.data_ptr(), ctypes.byref(rank))
         else:
@@ -188,10 +238,30 @@ class RQRCP:
                                        tau.data_ptr(), ctypes.byref(rank),
                                        omega.data_ptr() if omega is not None else None,
                                        omega_out.data_ptr() if omega_out is not None else None,
-                                       gaps.data_ptr() if gaps is not None else None)
+                                       ctypes.byref(trace.c) if trace is not None else None)
+            if trace is not None:
+                trace.recorded = int(trace.c.recorded)
         if rc and not (rc == RQRCP_W_RANK_DEFICIENT and allow_rank_deficient):
             raise self._err(rc)
         return jpvt, tau[:k], int(rank.value)
+
+    def _order_after_caller(self):
+        """The context runs on the stream it was created with (include/rqrcp.h);
+        work the caller queued on its CURRENT stream (e.g. filling A) must be
+        complete before the library reads it: make the context stream wait."""
+        import torch
+        cur = torch.cuda.current_stream(self.device)
+        if cur.cuda_stream != self.stream.cuda_stream:
+            self.stream.wait_stream(cur)
+
+    def set_option(self, name, value):
+        """Launch-path option (rqrcp_set_option; testing / diagnosis)."""
+        rc = lib().rqrcp_set_option(self._h, name.encode(), int(value))
+        if rc:
+            raise ValueError(f"rqrcp_set_option({name!r}, {value}) failed: {rc}")
+
+    def make_trace(self, n, b, p, first_panel=0, npanels=1, device=None):
+        return Trace(n, b, p, first_panel, npanels, device or self.device)
 
     def factor_raw(self, A_ptr, lda, m, n, k, b, p, seed, jpvt_ptr, tau_ptr):
         """Unchecked pointer call (bench inner loop); returns (code, rank)."""
@@ -246,6 +316,7 @@ class RQRCP:
         with diag = dict(g1, g2_est, alpha, tau_bound, tau_hat_bound, pivot)."""
         import torch
         m, n, lda = _check_colmajor(A)
+        self._order_after_caller()
         if jpvt is None:
             jpvt = torch.empty(n, dtype=torch.int64, device=A.device)
         if tau is None:
@@ -265,6 +336,7 @@ class RQRCP:
         """Q1 = first k columns of Q = H_1...H_k from a factored A."""
         import torch
         m, n, lda = _check_colmajor(A)
+        self._order_after_caller()
         if Q1 is None:
             Q1 = torch.empty(k, m, dtype=torch.float64, device=A.device).t()
         _, _, ldq = _check_colmajor(Q1)
@@ -277,6 +349,7 @@ class RQRCP:
         """CX coefficients X = C^+ A, C = A Pi(:, :k), from a factored A."""
         import torch
         m, n, lda = _check_colmajor(A)
+        self._order_after_caller()
         if X is None:
             X = torch.empty(n, k, dtype=torch.float64, device=A.device).t()
         _, _, ldx = _check_colmajor(X)
@@ -298,6 +371,103 @@ class RQRCP:
         if getattr(self, "_h", None):
             lib().rqrcp_destroy(self._h)
             self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Trace:
+    """Device buffers of the per-panel trace (rqrcp_trace): pivots
+    (npanels x b), rhat / bnext (npanels blocks of l x n, ld l)."""
+
+    def __init__(self, n, b, p, first_panel, npanels, device):
+        import torch
+        l = b + p
+        self.n, self.b, self.l = n, b, l
+        self.first_panel, self.npanels = first_panel, npanels
+        self.pivots = torch.full((npanels * b,), -1, dtype=torch.int64, device=device)
+        self.rhat = torch.zeros(npanels * l * n, dtype=torch.float64, device=device)
+        self.bnext = torch.zeros(npanels * l * n, dtype=torch.float64, device=device)
+        self.c = RqrcpTrace(first_panel, npanels, self.pivots.data_ptr(), self.rhat.data_ptr(),
+                            self.bnext.data_ptr(), 0)
+        self.recorded = 0
+
+    def panel(self, t, bb, i):
+        """(pivots[bb], rhat l x (n - i), bnext l x (n - i - bb)) of panel t as numpy."""
+        q = t - self.first_panel
+        l, n = self.l, self.n
+        piv = self.pivots[q * self.b:q * self.b + bb].cpu().numpy()
+        rh = self.rhat[q * l * n:q * l * n + l * (n - i)].cpu().numpy().reshape(n - i, l).T
+        nb = n - i - bb
+        bn = self.bnext[q * l * n:q * l * n + l * nb].cpu().numpy().reshape(nb, l).T
+        return piv, rh, bn
+
+
+class LoopbackGroup:
+    """P contexts on ONE device forming an in-process group
+    (rqrcp_create_loopback_group, testing API): runs the multi-rank driver
+    logic -- block-cyclic shards, pivot-column reduce, panel broadcast,
+    displaced-column broadcast, sample allgather -- with host-rendezvous
+    collectives, one host thread per rank."""
+
+    def __init__(self, nranks, max_m, max_n, max_b=128, max_p=16, device=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("LoopbackGroup needs a CUDA device (no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.nranks = nranks
+        cfg = RqrcpConfig()
+        cfg.device = self.device.index
+        cfg.max_m, cfg.max_n, cfg.max_b, cfg.max_p = max_m, max_n, max_b, max_p
+        arr = (ctypes.c_void_p * nranks)()
+        rc = lib().rqrcp_create_loopback_group(arr, nranks, ctypes.byref(cfg))
+        if rc:
+            raise RqrcpError(rc, "rqrcp_create_loopback_group failed")
+        self._h = [ctypes.c_void_p(arr[r]) for r in range(nranks)]
+
+    def set_option(self, name, value):
+        for h in self._h:
+            rc = lib().rqrcp_set_option(h, name.encode(), int(value))
+            if rc:
+                raise ValueError(f"rqrcp_set_option({name!r}) failed: {rc}")
+
+    def factor(self, shards, n, k, b, p, seed=0):
+        """shards[r]: rank r's column-major m x n_loc device tensor (factored in
+        place).  Returns (jpvt list, tau list, rank list, codes)."""
+        import threading
+
+        import torch
+        P = self.nranks
+        jp = [torch.empty(n, dtype=torch.int64, device=self.device) for _ in range(P)]
+        ta = [torch.empty(max(k, 1), dtype=torch.float64, device=self.device) for _ in range(P)]
+        rk = [ctypes.c_int64(0) for _ in range(P)]
+        codes = [None] * P
+        torch.cuda.synchronize(self.device)
+
+        def work(r):
+            m, n_loc, lda = _check_colmajor(shards[r])
+            codes[r] = lib().rqrcp_factor(self._h[r], shards[r].data_ptr(), lda, m, n, k, b, p, seed,
+                                          jp[r].data_ptr(), ta[r].data_ptr(), ctypes.byref(rk[r]))
+
+        th = [threading.Thread(target=work, args=(r,)) for r in range(P)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        torch.cuda.synchronize(self.device)
+        return jp, [t[:k] for t in ta], [int(x.value) for x in rk], codes
+
+    def last_error(self, r):
+        msg = lib().rqrcp_last_error(self._h[r])
+        return msg.decode() if msg else ""
+
+    def close(self):
+        for h in getattr(self, "_h", []):
+            lib().rqrcp_destroy(h)
+        self._h = []
 
     def __del__(self):
         try:

@@ -185,7 +185,7 @@ RQ_DEV void upper_index(int e, int &a, int &c) {
 template <int EPT>
 __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_chol_kernel(const double *G /* bbpad x bbpad */, int bb, int bbpad,
                                                                int nb, int pass, const int *bb_eff, int *status,
-                                                               double *Rc, double *Rinv) {
+                                                               double *Rc, double *Rinv, const double *tol2) {
     extern __shared__ __align__(16) double cq_sm[];
     double *M = cq_sm;              // nb x nb (R, then R^{-1})
     double *tmp = cq_sm + nb * nb;  // (nb/2)^2
@@ -273,9 +273,12 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_chol_kernel(const double *
     {
         double dmax = 0.0, dmin = 1e308;
         bool ok = !s_fail;
+        // a diagonal below the R11-diagonal stop threshold (reading R-G12b)
+        // declines: the column-by-column kernel then stops at that column
+        const double t2 = (pass == 1 && tol2) ? *tol2 : -1.0;
         for (int j = 0; j < bb; ++j) {
             const double dj = s_d[j];
-            ok = ok && (dj > 0.0);
+            ok = ok && (dj > 0.0) && !(dj < t2);
             dmax = fmax(dmax, dj);
             dmin = fmin(dmin, dj);
         }

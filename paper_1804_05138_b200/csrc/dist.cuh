@@ -50,13 +50,14 @@ __global__ void dist_reorder_kernel(const double *gath, int64_t cmax, int rows, 
     }
 }
 
-// panel broadcast pack: [tau (bbpad) | ybuf (bbpad^2) | R11 (bbpad^2, ld bbpad)]
-// pack = [tau (bbpad) | Y = strict_upper(V^T V) (bbpad^2) | R11 (bbpad^2) |
-//         -T (bbpad^2, valid when the CholeskyQR2 path ran) | status (1)]
-__global__ void dist_pack_kernel(const double *tau, const double *ybuf, const double *A /* &A[i + lj lda] */,
-                                 int64_t lda, int bb, int bbpad, const double *tneg, const int *status, double *pk) {
+// panel broadcast pack = [tau (bbpad) | Y = strict_upper(V^T V) (bbpad^2) |
+//   R11 (bbpad^2) | -T (bbpad^2, valid when the CholeskyQR2 path ran) |
+//   cqr status | bb_eff | done | rank]  -- the last three are the panel
+//   state after the owner's R11-diagonal stop check (iscal[1..3])
+__global__ void dist_pack_kernel(const double *tau, const double *ybuf, const double *A /* R11 */, int64_t lda, int bb,
+                                 int bbpad, const double *tneg, const int *status, const int *state, double *pk) {
     const int n2 = bbpad * bbpad;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bbpad + 3 * n2 + 1; e += gridDim.x * blockDim.x) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bbpad + 3 * n2 + 4; e += gridDim.x * blockDim.x) {
         if (e < bbpad) pk[e] = (e < bb) ? tau[e] : 0.0;
         else if (e < bbpad + n2) pk[e] = ybuf[e - bbpad];
         else if (e < bbpad + 2 * n2) {
@@ -64,20 +65,23 @@ __global__ void dist_pack_kernel(const double *tau, const double *ybuf, const do
             pk[e] = (r < bb && c < bb) ? A[r + (int64_t)c * lda] : 0.0;
         } else if (e < bbpad + 3 * n2) {
             pk[e] = tneg[e - bbpad - 2 * n2];
-        } else {
+        } else if (e == bbpad + 3 * n2) {
             pk[e] = (double)*status;
+        } else {
+            pk[e] = (double)state[e - (bbpad + 3 * n2 + 1)];
         }
     }
 }
 __global__ void dist_unpack_kernel(const double *pk, int bb, int bbpad, double *tau, double *ybuf, double *tneg,
-                                   int *status) {
+                                   int *status, int *state) {
     const int n2 = bbpad * bbpad;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bbpad + 3 * n2 + 1; e += gridDim.x * blockDim.x) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bbpad + 3 * n2 + 4; e += gridDim.x * blockDim.x) {
         if (e < bbpad) { if (e < bb) tau[e] = pk[e]; }
         else if (e < bbpad + n2) ybuf[e - bbpad] = pk[e];
         else if (e < bbpad + 2 * n2) continue;
         else if (e < bbpad + 3 * n2) tneg[e - bbpad - 2 * n2] = pk[e];
-        else *status = (int)pk[e];
+        else if (e == bbpad + 3 * n2) *status = (int)pk[e];
+        else state[e - (bbpad + 3 * n2 + 1)] = (int)pk[e];
     }
 }
 // Vt (bbpad x mp) from Vfull (mp x bbpad, ld ldv)
@@ -130,6 +134,9 @@ struct NcclApi {
     ncclResult_t (*AllGather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Broadcast)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Reduce)(const void *, void *, size_t, int, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;  // optional
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;                          // optional
     ncclResult_t (*Send)(const void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
@@ -142,8 +149,9 @@ inline NcclApi &nccl() {
     static bool tried = false;
     if (tried) return api;
     tried = true;
-    const char *cands[] = {getenv("RQRCP_NCCL_LIB"), "libnccl.so.2", "libnccl.so",
-                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+    // RQRCP_NCCL_LIB (the Python binding points it at the nvidia-nccl wheel
+    // torch uses), else the soname (already mapped when torch is imported)
+    const char *cands[] = {getenv("RQRCP_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
     void *h = nullptr;
     for (const char *c : cands)
         if (c && (h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
@@ -158,13 +166,16 @@ inline NcclApi &nccl() {
     api.AllGather = (decltype(api.AllGather))sym("ncclAllGather");
     api.Broadcast = (decltype(api.Broadcast))sym("ncclBroadcast");
     api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+    api.Reduce = (decltype(api.Reduce))sym("ncclReduce");
+    api.CommGetAsyncError = (decltype(api.CommGetAsyncError))sym("ncclCommGetAsyncError");
+    api.CommAbort = (decltype(api.CommAbort))sym("ncclCommAbort");
     api.Send = (decltype(api.Send))sym("ncclSend");
     api.Recv = (decltype(api.Recv))sym("ncclRecv");
     api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
     api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
     api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather && api.Broadcast &&
-             api.AllReduce && api.Send && api.Recv && api.GroupStart && api.GroupEnd && api.GetErrorString;
+             api.AllReduce && api.Reduce && api.Send && api.Recv && api.GroupStart && api.GroupEnd && api.GetErrorString;
     if (!api.ok) api.err = "libnccl.so.2 lacks a required symbol";
     return api;
 }

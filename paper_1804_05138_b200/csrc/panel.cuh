@@ -49,6 +49,9 @@ struct PanelArgs {
     double *part;       // [2][G][bbpad] partial Gram rows (one contiguous row per CTA)
     double *rowj;       // [2][bbpad] published row j
     unsigned *bar;      // per-launch barrier counter (zeroed by the host)
+    const double *tol2; // R11-diagonal rank stop (reading R-G12b): stop at the first column whose
+                        // beta^2 < *tol2 (= (1e3 eps)^2 ||panel||_F^2); nullptr: no check
+    int *stop_col;      // out: that column (-1 when none); written by CTA 0
     unsigned long long *trace;  // debug: [2 CTAs][64 steps][8 phases] clock64 stamps, or nullptr
 };
 
@@ -58,6 +61,7 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
     __shared__ double wred[PN_WARPS][PN_MAXB];
     __shared__ double xs[PN_MAXROWS];
     __shared__ double s_scal, s_tau, s_beta;
+    __shared__ int s_stop;
     if (a.skip && *a.skip == 0) return;
     const int G = gridDim.x, g = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -81,6 +85,8 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
     __syncthreads();
     auto Pv = [&](int r, int c) -> double { return (r < nsm) ? Ps[r + (int64_t)c * lds] : Pg[r + (int64_t)c * lda]; };
     const int tsel = (g == 0) ? 0 : (g == G - 1 ? 1 : -1);
+    const double tol2 = a.tol2 ? *a.tol2 : -1.0;
+    int bbo = bbe;  // columns factored (bbe, or the R11-diagonal stop column)
     for (int j = 0; j < bbe; ++j) {
         auto stamp = [&](int ph) {
             if (a.trace && tsel >= 0 && tid == 0 && j < 64) a.trace[((size_t)tsel * 64 + j) * 8 + ph] = clock64();
@@ -173,10 +179,18 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
                 tau = (beta - alpha) / beta;
                 scal = 1.0 / (alpha - beta);
             }
+            // R11-diagonal rank stop: |R(j,j)| = |beta| below 1e3 eps ||panel||_F
+            // (every CTA evaluates the same bits: a uniform decision)
+            const int stop = (beta * beta < tol2) ? 1 : 0;
+            s_stop = stop;
             s_tau = tau; s_beta = beta; s_scal = scal;
-            if (g == 0) a.tau[j] = tau;
+            if (g == 0) a.tau[j] = stop ? 0.0 : tau;
         }
         __syncthreads();
+        if (s_stop) {  // column j and beyond stay as they are (tau = 0)
+            bbo = j;
+            break;
+        }
         const double tau = s_tau, scal = s_scal;
         // CTA 0 records y_c = v_c^T v_j = A(j,c) + scal g_c (c < j): column j of
         // strict_upper(V^T V), from which tri_kernel builds T off the critical path
@@ -228,7 +242,7 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
         const int64_t gr = r_lo + r;
         for (int c = lane; c < a.bbpad; c += 32) {
             double v = 0.0;
-            if (c < bbe) v = (gr > c) ? Pg[r + (int64_t)c * lda] : (gr == c ? 1.0 : 0.0);
+            if (c < bbo) v = (gr > c) ? Pg[r + (int64_t)c * lda] : (gr == c ? 1.0 : 0.0);
             a.vt[c + gr * a.bbpad] = v;
         }
     }
@@ -236,12 +250,13 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
         for (int r = lane; r < nrows; r += 32) {
             const int64_t gr = r_lo + r;
             double v = 0.0;
-            if (c < bbe) v = (gr > c) ? Pg[r + (int64_t)c * lda] : (gr == c ? 1.0 : 0.0);
+            if (c < bbo) v = (gr > c) ? Pg[r + (int64_t)c * lda] : (gr == c ? 1.0 : 0.0);
             a.vfull[gr + c * a.ldv] = v;
         }
     if (g == 0)
-        for (int c = bbe + tid; c < bb; c += PN_THREADS) a.tau[c] = 0.0;
+        for (int c = bbo + tid; c < bb; c += PN_THREADS) a.tau[c] = 0.0;
     if (g == 0 && tid == 0 && a.count) atomicAdd(a.count, 1);
+    if (g == 0 && tid == 0 && a.stop_col) *a.stop_col = (bbo < bbe) ? bbo : -1;
 }
 
 }  // namespace rq

@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
     __shared__ double gsum[BB], rjv[BB];
     __shared__ double scal_s[BB], beta_s[BB];
     __shared__ double s_hh[2];  // this step's tau, scal
+    __shared__ int s_stop;
 
     if (a.skip && *a.skip == 0) return;  // uniform: the CholeskyQR2 path already factored the panel
     const int G = gridDim.x;
@@ -214,6 +215,8 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
 
     const int tsel = (g == 0) ? 0 : (g == G - 1 ? 1 : -1);
     const int pq = tid / BB, pc = tid % BB;  // push mapping
+    const double tol2 = a.tol2 ? *a.tol2 : -1.0;
+    int bbo = bbe;  // columns factored (bbe, or the R11-diagonal stop column)
     for (int j = 0; j < bbe; ++j) {
         auto stamp = [&](int ph) {
             if (a.trace && tsel >= 0 && tid == 0 && j < 64) a.trace[((size_t)tsel * 64 + j) * 8 + ph] = clock64();
@@ -293,9 +296,15 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
                 s_hh[1] = scal;
                 scal_s[j] = scal;
                 beta_s[j] = beta;
+                // R11-diagonal rank stop (reading R-G12b): the same bits in every CTA
+                s_stop = (beta * beta < tol2) ? 1 : 0;
             }
         }
         __syncthreads();
+        if (s_stop) {  // uniform across the cluster; column j and beyond untouched
+            bbo = j;
+            break;
+        }
         // step j+2 reuses this mbarrier (every read of recv[par] is above)
         if (tid == 0 && j + 2 < bbe) mbar_expect_tx(mb0 + 8 * par, step_bytes);
         stamp(4);
@@ -344,14 +353,14 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
     //      Element (r, c): r < bbe, c > r: R(r, c) (Rrow); r == c < bbe: beta;
     //      c < bbe, r > c: v = scal_c x; otherwise the updated value.
     // CTA 0: the final R rows live in Rrow (= the staging buffer); take them first
-    if (g == 0 && rowbase < bbe) {
+    if (g == 0 && rowbase < bbo) {
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             const int c = cg * CPT + k;
 #pragma unroll
             for (int t = 0; t < RPT; ++t) {
                 const int row = rowbase + t;
-                if (row < bbe && c > row && c < bb) av[k][t] = Rrow[row * BB + c];
+                if (row < bbo && c > row && c < bb) av[k][t] = Rrow[row * BB + c];
             }
         }
     }
@@ -367,8 +376,8 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
         double sc[CPT], be[CPT];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
-            sc[k] = (c0 + k < bbe) ? scal_s[c0 + k] : 0.0;
-            be[k] = (c0 + k < bbe) ? beta_s[c0 + k] : 0.0;
+            sc[k] = (c0 + k < bbo) ? scal_s[c0 + k] : 0.0;
+            be[k] = (c0 + k < bbo) ? beta_s[c0 + k] : 0.0;
         }
 #pragma unroll
         for (int t = 0; t < RPT; t += 2) {  // rows gr, gr + 1
@@ -380,7 +389,7 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
                 for (int h = 0; h < 2; ++h) {
                     const int cc = c0 + k;
                     double x = av[k][t + h], w = 0.0;
-                    if (cc < bbe) {
+                    if (cc < bbo) {
                         if (gr + h > cc) { w = sc[k] * x; x = w; }
                         else if (gr + h == cc) { w = 1.0; x = be[k]; }
                     }
@@ -428,7 +437,7 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
             if (gr >= mp) continue;
             const double x = stage[cc * LDS + r];
             double v = 0.0, o = x;
-            if (cc < bbe) {
+            if (cc < bbo) {
                 if (gr > cc) { v = scal_s[cc] * x; o = v; }
                 else if (gr == cc) { v = 1.0; o = beta_s[cc]; }
             }
@@ -440,12 +449,13 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
             const int64_t gr = r0 + r;
             if (gr >= mp) continue;
             const double x = stage[cc * LDS + r];
-            a.vt[cc + gr * a.bbpad] = (cc < bbe) ? (gr > cc ? scal_s[cc] * x : (gr == cc ? 1.0 : 0.0)) : 0.0;
+            a.vt[cc + gr * a.bbpad] = (cc < bbo) ? (gr > cc ? scal_s[cc] * x : (gr == cc ? 1.0 : 0.0)) : 0.0;
         }
     }
     if (g == 0) {
-        for (int cc = bbe + tid; cc < bb; cc += PNC_THREADS) a.tau[cc] = 0.0;
+        for (int cc = bbo + tid; cc < bb; cc += PNC_THREADS) a.tau[cc] = 0.0;
         if (tid == 0 && a.count) atomicAdd(a.count, 1);
+        if (tid == 0 && a.stop_col) *a.stop_col = (bbo < bbe) ? bbo : -1;
     }
 }
 

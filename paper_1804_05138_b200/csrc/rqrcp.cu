@@ -1,16 +1,23 @@
 // rqrcp.cu -- the C ABI (include/rqrcp.h) and the host driver of the RQRCP
-// hot path (Alg. 2).  The driver only enqueues kernels on the
-// context's stream (no host synchronisation inside the panel loop; pivots
-// stay on the device) and synchronises once at the end for the status.
+// hot path (Alg. 2).  The driver only enqueues kernels and
+// collectives on the context's streams (no host synchronisation inside the
+// panel loop: pivots, swap lists and rank-stop state stay on the device) and
+// synchronises once at the end for the status.
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
+#include <mutex>
+#include <set>
 #include <string>
+#include <thread>
+#include <tuple>
 #include <vector>
 
 #include "rqrcp.h"
@@ -18,6 +25,7 @@
 #include "gemm_dmma.cuh"
 #include "gemm_tma.cuh"
 #include "misc.cuh"
+#include "moves.cuh"
 #include "panel.cuh"
 #include "panel_cl.cuh"
 #include "philox.cuh"
@@ -27,6 +35,7 @@
 #include "tri.cuh"
 #include "cqr.cuh"
 #include "dist.cuh"
+#include "transport.cuh"
 #include "srqr.cuh"
 #include "lowrank.cuh"
 
@@ -36,58 +45,92 @@ static inline int64_t rup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 enum Phase { PH_OMEGA, PH_SKETCH, PH_SQRCP, PH_SWAP, PH_PANEL, PH_TRAIL, PH_SUPD, PH_COMM, PH_N };
 
+// Launch-path options (rqrcp_set_option; environment RQRCP_<NAME> at create).
+struct Opts {
+    int schedule = -1;       // -1 auto, 0 serial, 1 bulk || next sample QRCP, 2 bulk || next panel (look-ahead)
+    int panel = 0;           // 0 Householder columns, 1 CholeskyQR2 + reconstruction, 2 CholeskyQR2 from 8192 rows
+    int pn_cluster = 1, pn_cpt = 2, pn_grid = 0, pn_rows = 128, la_panel_ctas = 48;
+    int sq_cluster = 1, sq_reg = 1, sq_grid = 0, sq_nsm = -1, sq_hstride = 8, sq_poll = 1;
+    int debug_sync = 0, trace = 0, trace_panel = 1;
+    int64_t nccl_timeout_ms = 600000;
+};
+struct OptDesc {
+    const char *name;
+    int64_t lo, hi;
+};
+static const OptDesc kOpts[] = {{"schedule", -1, 2},     {"panel", 0, 2},     {"pn_cluster", 0, 1},
+                                {"pn_cpt", 1, 2},        {"pn_grid", 0, 4096}, {"pn_rows", 1, 1 << 20},
+                                {"la_panel_ctas", 1, 4096}, {"sq_cluster", 0, 1}, {"sq_reg", 0, 1},
+                                {"sq_grid", 0, 4096},    {"sq_nsm", -1, 1 << 20}, {"sq_hstride", 1, 8},
+                                {"sq_poll", 0, 2},       {"debug_sync", 0, 1}, {"trace", 0, 1},
+                                {"trace_panel", 1, 1 << 30}, {"nccl_timeout_ms", 1, (int64_t)1 << 40}};
+static bool opt_set(Opts &o, const std::string &n, int64_t v) {
+#define OPT(field)                    \
+    if (n == #field) {                \
+        o.field = (decltype(o.field))v; \
+        return true;                  \
+    }
+    OPT(schedule) OPT(panel) OPT(pn_cluster) OPT(pn_cpt) OPT(pn_grid) OPT(pn_rows) OPT(la_panel_ctas)
+    OPT(sq_cluster) OPT(sq_reg) OPT(sq_grid) OPT(sq_nsm) OPT(sq_hstride) OPT(sq_poll) OPT(debug_sync) OPT(trace)
+    OPT(trace_panel) OPT(nccl_timeout_ms)
+#undef OPT
+    return false;
+}
+
 struct rqrcp_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // concurrent small kernels (tri_kernel)
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    // overlap of the bulk trailing update (rows i+bb..m) with the next panel's
-    // sample QRCP: the update runs on `upd` (lowest priority), the main stream
-    // (highest priority when ctx-owned) joins it before the next swap
-    cudaStream_t upd = nullptr;
-    cudaEvent_t ev_r12 = nullptr, ev_upd = nullptr;
+    cudaStream_t upd = nullptr;   // the bulk trailing update (lowest priority)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_r12 = nullptr, ev_upd = nullptr, ev_pack = nullptr;
     int grid_cap = 0;  // > 0: persistent GEMM grids use at most this many CTAs
     int *tctr = nullptr;  // per-panel tile counters of the dynamically scheduled bulk update
     bool own_stream = false;
     int nranks = 1, rank = 0;
+    std::unique_ptr<Transport> tr;
     int64_t max_m = 0, max_n = 0;
     int max_b = 0, max_p = 0;
     int lpad_max = 0, bpad_max = 0;
-    int64_t ldo = 0;  // leading dim of Omega^T and Vfull (= round8(max_m))
+    int64_t ldo = 0;  // leading dim of Omega^T, V and the panel buffers (= round8(max_m))
     int num_sms = 0;
+    Opts opt;
     std::string err;
     // workspace
-    double *omt = nullptr;     // Omega^T  ldo x lpad_max
-    double *bs[2] = {nullptr, nullptr};  // samples lpad_max x max_n
-    double *vfull = nullptr;   // ldo x bpad_max
-    double *vt = nullptr;      // bpad_max x max_m
-    double *w = nullptr, *w2 = nullptr;  // bpad_max x max_n
+    double *omt = nullptr;                 // Omega^T  ldo x lpad_max
+    double *bs[2] = {nullptr, nullptr};    // samples lpad_max x max_n
+    double *vfull_b[2] = {nullptr, nullptr};  // V (ldv x bpad), double buffered for the look-ahead
+    double *vt_b[2] = {nullptr, nullptr};     // V^T (bpad x max_m)
+    double *w = nullptr, *w2 = nullptr;    // bpad_max x max_n
+    double *w2g = nullptr;                 // bpad x bpad: W2 columns of the next panel's pivots
     double *tneg = nullptr, *rhat11 = nullptr, *omhat = nullptr, *ybuf = nullptr;  // bpad_max^2
     double *vhat = nullptr;    // lpad_max x bpad_max
     double *tauhat = nullptr;
     double *splitk = nullptr;
     int64_t splitk_elems = 0;
+    double *pbuf = nullptr;    // the panel's columns, full height (ldo x bpad)
+    double *packbuf = nullptr; // P > 1: this rank's contribution to pbuf (ldo x bpad)
+    double *dispbuf = nullptr; // P > 1: the owner's displaced slot columns (ldo x bpad)
+    double *colss = nullptr, *ptol2 = nullptr;  // R11-diagonal stop scale
+    int *stopc = nullptr;      // panel kernels: the R11-diagonal stop column (-1: none)
     SqHdr *slot_hdr = nullptr;
     int *slot_col = nullptr;
-    unsigned launch_seq = 0;  // tags of the sample-QRCP candidate headers
+    unsigned launch_seq = 0;
     double *slot_v2 = nullptr, *slot_data = nullptr;
-    uint4 *sq_ll = nullptr;  // tagged exchange slots of the register grid sample QRCP
-    double *sq_spill = nullptr;  // transposed sample columns beyond shared memory (lpad_max x max_n)
+    uint4 *sq_ll = nullptr;
+    double *sq_spill = nullptr;
     double *pn_part = nullptr, *pn_rowj = nullptr;
-    // CholeskyQR2 + reconstruction panel (cqr.cuh): Gram, R factors, inverses
     double *cq_g = nullptr, *cq_rc = nullptr, *cq_rinv = nullptr, *cq_uinv = nullptr, *cq_lu = nullptr;
-    int *cqr_status = nullptr;  // 0: the CholeskyQR2 path factored the panel; 1: Householder fallback
+    int *cqr_status = nullptr;
     bool cqr_enabled = true;
     double *swap_stage = nullptr;
     int64_t *swap_dst = nullptr, *swap_src = nullptr, *swap_jstage = nullptr;
     int *swap_np = nullptr;
     int64_t *perm = nullptr, *piv = nullptr;
     double *sumsq_part = nullptr;
-    // device scalars: [0] status [1] bb_eff [2] done [3] rank
+    // device scalars: [0] status [1] bb_eff [2] done [3] rank [4] householder panels [5] srqr iota [6] form_q1
     int *iscal = nullptr;
     double *stop_tol2 = nullptr;
-    unsigned *bars = nullptr;  // one grid-barrier counter per cooperative launch
-    // updating formula 2 (Eq. (5)): the pre-QRCP sample, Omega-bar_1 R12, W for Q^T Omega^T
+    unsigned *bars = nullptr;
     int update_rule = 1;
     double *bpre = nullptr, *c5 = nullptr, *wom = nullptr, *w2om = nullptr;
     int64_t nbars = 0;
@@ -96,17 +139,10 @@ struct rqrcp_ctx {
     int64_t a_dev_elems = 0;
     int64_t *jpvt_dev = nullptr;
     double *tau_dev = nullptr;
-    // cooperative limits
-    int sq_max_grid = 0, pn_max_grid = 0;
-    int sqc_max = 0;  // largest cluster the register-resident sample QRCP can use (0: none)
-    int pnc_max = 0;  // ... and the register-resident cluster panel kernel
-    // multi-GPU (nranks > 1): NCCL communicator + exchange buffers
-    ncclComm_t comm = nullptr;
-    double *gsend = nullptr, *gbuf = nullptr, *pack = nullptr, *r11 = nullptr;
+    int sqc_max = 0, pnc_max = 0;
+    // multi-GPU exchange buffers
+    double *gsend = nullptr, *gbuf = nullptr, *pack = nullptr;
     int64_t gbuf_elems = 0;
-    int64_t *dl_cols = nullptr;  // device lists for the cross-rank column moves
-    int *dl_slots = nullptr;
-    int64_t *h_pairs = nullptr;  // pinned host copy of (dst, src) pairs + count
     // timing
     bool timing = true;
     cudaEvent_t ev[2 * 4096 + 8];
@@ -114,13 +150,12 @@ struct rqrcp_ctx {
     int open_phase = -1, open_ev = -1;
     std::vector<int> rec_phase, rec_s, rec_e;
     rqrcp_timings last{};
-    int lt_t0 = -1, lt_t1 = -1;  // total-time events of the last factorization (read lazily)
-    int *hstatus = nullptr;      // pinned host copy of the device status words
+    int lt_t0 = -1, lt_t1 = -1;
+    int *hstatus = nullptr;
     int64_t launches = 0;
-    bool debug_sync = false;  // RQRCP_DEBUG_SYNC=1: synchronise after every launch
-    unsigned long long *trace = nullptr;  // RQRCP_TRACE=1: per-step phase stamps of the sample QRCP
-    unsigned long long *ptrace = nullptr; // ... and of the panel kernel
-    int ptrace_kind = 0;                  // 0: grid panel kernel, 1: cluster panel kernel
+    unsigned long long *trace = nullptr;
+    unsigned long long *ptrace = nullptr;
+    int ptrace_kind = 0;
 };
 
 static const char *g_static_err = "no context";
@@ -137,7 +172,7 @@ static const char *g_static_err = "no context";
 #define CKL()                                                                         \
     do {                                                                              \
         cudaError_t e_ = cudaGetLastError();                                          \
-        if (e_ == cudaSuccess && ctx->debug_sync) e_ = cudaStreamSynchronize(ctx->stream); \
+        if (e_ == cudaSuccess && ctx->opt.debug_sync) e_ = cudaDeviceSynchronize();   \
         if (e_ != cudaSuccess) {                                                      \
             ctx->err = std::string("kernel launch #") + std::to_string(ctx->launches) + \
                        " (line " + std::to_string(__LINE__) + "): " + cudaGetErrorString(e_); \
@@ -146,42 +181,77 @@ static const char *g_static_err = "no context";
         ctx->launches++;                                                              \
     } while (0)
 
+#define CKT(call)                                 \
+    do {                                          \
+        int r_ = (call);                          \
+        if (r_) return r_;                        \
+    } while (0)
+
 static constexpr int kDynSmemMax = 200 * 1024;
-static constexpr int64_t kCqrMinRows = 8192;  // auto panel path: CholeskyQR2 from this many rows  // dynamic shared memory cap for cached kernels
+static constexpr int64_t kCqrMinRows = 8192;
 
 static int grid_for(int64_t total, int threads, int num_sms) {
     int64_t g = (total + threads - 1) / threads;
     return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)num_sms * 8));
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute is per device, so a context on another GPU of the same process
+// sets it again.
+static std::mutex g_attr_mu;
+static std::set<std::tuple<const void *, int, int>> g_attr_done;
+static cudaError_t smem_attr(const void *kern, int bytes, int device) {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto key = std::make_tuple(kern, device, bytes);
+    if (g_attr_done.count(key)) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) g_attr_done.insert(key);
+    return e;
+}
+
 // ---------------------------------------------------------------------------
 // GEMM dispatch: C = X^T Y (see gemm_dmma.cuh), M small (skinny) or large.
+// Split-K is CANONICAL: the number of K slices depends only on (M, K, the
+// global N), never on a rank's column count, so every contraction's
+// per-element summation order -- hence every bit of the result -- is the same
+// for any number of ranks (SURVEY.md §8(e) "Determinism across P").
 // ---------------------------------------------------------------------------
 template <int MT, int NT, int WM, int WN, int BK, int ST, int EPI>
 static int launch_tn_cfg(rqrcp_ctx *ctx, GemmArgs g, int splits) {
     constexpr int BM = 8 * MT * WM, BN = 8 * NT * WN;
     const size_t smem = (size_t)ST * BK * (BM + BN) * sizeof(double);
     auto kern = gemm_tn_kernel<MT, NT, WM, WN, BK, ST, EPI>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set = true;
-    }
+    CK(smem_attr((const void *)kern, (int)smem, ctx->device));
     dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM), (unsigned)splits);
     kern<<<grid, WM * WN * 32, smem, ctx->stream>>>(g);
     CKL();
     return 0;
 }
 
+// splits minimising ceil(T*S / grid) / S (persistent-grid wave quantisation);
+// T = tiles of the GLOBAL problem (canonical, see above)
+static int choose_splits(int64_t tiles, int64_t K, int grid, int64_t max_elems_per_split, int64_t partial_cap,
+                         int64_t kmin = 512) {
+    int64_t smax = std::max<int64_t>(1, K / kmin);
+    if (max_elems_per_split > 0) smax = std::min<int64_t>(smax, std::max<int64_t>(1, partial_cap / max_elems_per_split));
+    int best = 1;
+    double best_t = 1e30;
+    for (int64_t s = 1; s <= std::min<int64_t>(smax, 64); ++s) {
+        const double t = (double)((tiles * s + grid - 1) / grid) / (double)s + 0.002 * s;  // small per-split cost
+        if (t < best_t - 1e-12) { best_t = t; best = (int)s; }
+    }
+    return best;
+}
+
 template <int MT, int NT, int WM, int WN>
 static int launch_skinny(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const double *X, int64_t ldx,
-                         const double *Y, int64_t ldy, double *C, int64_t ldc) {
+                         const double *Y, int64_t ldy, double *C, int64_t ldc, int64_t Ncanon) {
     constexpr int BK = 32, ST = 3;
     constexpr int BM = 8 * MT * WM, BN = 8 * NT * WN;
-    const int64_t tiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM);
+    const int64_t tiles = ((Ncanon + BN - 1) / BN) * ((M + BM - 1) / BM);
     int64_t splits = std::max<int64_t>(1, (2 * (int64_t)ctx->num_sms + tiles - 1) / tiles);
     splits = std::min<int64_t>(splits, std::max<int64_t>(1, K / 256));
-    while (splits > 1 && splits * M * N > ctx->splitk_elems) --splits;
+    while (splits > 1 && splits * M * Ncanon > ctx->splitk_elems) --splits;
     int64_t kps = rup((K + splits - 1) / splits, BK);
     splits = (K + kps - 1) / kps;
     GemmArgs g{M, N, K, X, ldx, Y, ldy, C, ldc, kps, M * N};
@@ -190,8 +260,7 @@ static int launch_skinny(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const 
         return launch_tn_cfg<MT, NT, WM, WN, BK, ST, EPI_STORE>(ctx, g, 1);
     }
     g.C = ctx->splitk;
-    int rc = launch_tn_cfg<MT, NT, WM, WN, BK, ST, EPI_PARTIAL>(ctx, g, (int)splits);
-    if (rc) return rc;
+    CKT((launch_tn_cfg<MT, NT, WM, WN, BK, ST, EPI_PARTIAL>(ctx, g, (int)splits)));
     splitk_reduce_kernel<<<grid_for(M * N, 256, ctx->num_sms), 256, 0, ctx->stream>>>(ctx->splitk, M, N, (int)splits,
                                                                                       M * N, C, ldc);
     CKL();
@@ -200,14 +269,16 @@ static int launch_skinny(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const 
 
 // C (M x N) = X^T Y with M <= 144 rows (sample rows l_pad or panel width).
 static int gemm_skinny(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const double *X, int64_t ldx,
-                       const double *Y, int64_t ldy, double *C, int64_t ldc) {
-    if (M <= 32) return launch_skinny<4, 2, 1, 4>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc);
-    if (M <= 40) return launch_skinny<5, 2, 1, 4>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc);
-    if (M <= 64) return launch_skinny<4, 4, 2, 2>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc);
-    if (M <= 80) return launch_skinny<5, 4, 2, 2>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc);
-    if (M <= 128) return launch_skinny<4, 4, 4, 2>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc);
-    if (M <= 144) return launch_skinny<6, 4, 3, 2>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc);
-    return launch_skinny<4, 4, 4, 2>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc);  // grid.y tiles M
+                       const double *Y, int64_t ldy, double *C, int64_t ldc, int64_t Ncanon = -1) {
+    if (N <= 0) return 0;
+    if (Ncanon < 0) Ncanon = N;
+    if (M <= 32) return launch_skinny<4, 2, 1, 4>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc, Ncanon);
+    if (M <= 40) return launch_skinny<5, 2, 1, 4>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc, Ncanon);
+    if (M <= 64) return launch_skinny<4, 4, 2, 2>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc, Ncanon);
+    if (M <= 80) return launch_skinny<5, 4, 2, 2>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc, Ncanon);
+    if (M <= 128) return launch_skinny<4, 4, 4, 2>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc, Ncanon);
+    if (M <= 144) return launch_skinny<6, 4, 3, 2>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc, Ncanon);
+    return launch_skinny<4, 4, 4, 2>(ctx, M, N, K, X, ldx, Y, ldy, C, ldc, Ncanon);  // grid.y tiles M
 }
 
 // A22 (rows x cols, lda) += V W2 as (A22^T)(cols x rows) += W2^T Vt.
@@ -225,15 +296,14 @@ static int gemm_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, co
 // ---------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
+    static std::once_flag once;
+    std::call_once(once, [] {
         void *p = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
             fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
-    }
+    });
     return fn;
 }
 
@@ -241,7 +311,6 @@ static PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
 // box {8 doubles, box1 columns}; out-of-range elements read as zero.
 static bool make_tmap(CUtensorMap *m, const double *base, int64_t dim0, int64_t dim1, int64_t ld, int box1) {
     auto enc = tma_encode_fn();
-    if (!enc && getenv("RQRCP_DEBUG_TMA")) fprintf(stderr, "[rqrcp] no cuTensorMapEncodeTiled entry point\n");
     if (!enc || ((uintptr_t)base & 15) || ((ld * 8) & 15) || dim0 < 1 || dim1 < 1) return false;
     cuuint64_t dims[2] = {(cuuint64_t)dim0, (cuuint64_t)dim1};
     cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
@@ -250,26 +319,7 @@ static bool make_tmap(CUtensorMap *m, const double *base, int64_t dim0, int64_t 
     const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)base, dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    static bool warned = false;
-    if (r != CUDA_SUCCESS && !warned && getenv("RQRCP_DEBUG_TMA")) {
-        fprintf(stderr, "[rqrcp] cuTensorMapEncodeTiled failed (%d): cp.async GEMM path\n", (int)r);
-        warned = true;
-    }
     return r == CUDA_SUCCESS;
-}
-
-// splits minimising ceil(T*S / grid) / S (persistent-grid wave quantisation)
-static int choose_splits(int64_t tiles, int64_t K, int grid, int64_t max_elems_per_split, int64_t partial_cap,
-                         int64_t kmin = 512) {
-    int64_t smax = std::max<int64_t>(1, K / kmin);
-    if (max_elems_per_split > 0) smax = std::min<int64_t>(smax, std::max<int64_t>(1, partial_cap / max_elems_per_split));
-    int best = 1;
-    double best_t = 1e30;
-    for (int64_t s = 1; s <= std::min<int64_t>(smax, 64); ++s) {
-        const double t = (double)((tiles * s + grid - 1) / grid) / (double)s + 0.002 * s;  // small per-split cost
-        if (t < best_t - 1e-12) { best_t = t; best = (int)s; }
-    }
-    return best;
 }
 
 template <int MT, int NT, int WM, int WN, int EPI, bool DYN = false>
@@ -286,11 +336,7 @@ static int launch_tma_cfg(rqrcp_ctx *ctx, const double *X, int64_t xdim0, int64_
     if (!make_tmap(&tx, X, xdim0, xdim1, ldx, BM) || !make_tmap(&ty, Y, ydim0, ydim1, ldy, BN)) return 0;
     const size_t smem = tma_gemm_smem<MT, NT, WM, WN, BK, ST>();
     auto kern = gemm_tma_kernel<MT, NT, WM, WN, BK, ST, EPI, DYN>;
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    CK(smem_attr((const void *)kern, (int)smem, ctx->device));
     const int64_t tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM) * g.splits;
     const int grid = (int)std::min<int64_t>(tiles, ctx->grid_cap > 0 ? ctx->grid_cap : ctx->num_sms);
     kern<<<grid, WM * WN * 32, smem, ctx->stream>>>(tx, ty, g);
@@ -305,17 +351,17 @@ template <int MT, int NT, int WM, int WN>
 static int tma_skinny_cfg(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const double *X, int64_t xdim0,
                           int64_t xdim1, int64_t ldx, int64_t xk0, int64_t xm0, const double *Y, int64_t ydim0,
                           int64_t ydim1, int64_t ldy, int64_t yk0, int64_t yn0, double *C, int64_t ldc, bool *done,
-                          int64_t kmin) {
+                          int64_t kmin, int64_t Ncanon) {
     constexpr int BM = 8 * MT * WM, BN = 8 * NT * WN;
-    const int64_t tiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM);
-    int splits = choose_splits(tiles, K, ctx->num_sms, M * N, ctx->splitk_elems, kmin);
+    const int64_t tiles = ((Ncanon + BN - 1) / BN) * ((M + BM - 1) / BM);
+    int splits = choose_splits(tiles, K, ctx->num_sms, M * Ncanon, ctx->splitk_elems, kmin);
     int64_t kps = rup((K + splits - 1) / splits, 32);
     splits = (int)((K + kps - 1) / kps);
     TmaGemmArgs g{M, N, K, xk0, xm0, yk0, yn0, C, ldc, kps, splits, M * N, 0};
     if (splits <= 1) return launch_tma_cfg<MT, NT, WM, WN, EPI_STORE>(ctx, X, xdim0, xdim1, ldx, Y, ydim0, ydim1, ldy, g, done);
     g.C = ctx->splitk;
-    int rc = launch_tma_cfg<MT, NT, WM, WN, EPI_PARTIAL>(ctx, X, xdim0, xdim1, ldx, Y, ydim0, ydim1, ldy, g, done);
-    if (rc || !*done) return rc;
+    CKT((launch_tma_cfg<MT, NT, WM, WN, EPI_PARTIAL>(ctx, X, xdim0, xdim1, ldx, Y, ydim0, ydim1, ldy, g, done)));
+    if (!*done) return 0;
     splitk_reduce_kernel<<<grid_for(M * N, 256, ctx->num_sms), 256, 0, ctx->stream>>>(ctx->splitk, M, N, splits, M * N,
                                                                                       C, ldc);
     CKL();
@@ -324,26 +370,32 @@ static int tma_skinny_cfg(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const
 
 static int tma_skinny(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const double *X, int64_t xdim0, int64_t xdim1,
                       int64_t ldx, int64_t xk0, int64_t xm0, const double *Y, int64_t ydim0, int64_t ydim1, int64_t ldy,
-                      int64_t yk0, int64_t yn0, double *C, int64_t ldc, bool *done, int64_t kmin = 512) {
+                      int64_t yk0, int64_t yn0, double *C, int64_t ldc, bool *done, int64_t kmin = 512,
+                      int64_t Ncanon = -1) {
     *done = false;
-    if (M <= 32) return tma_skinny_cfg<4, 4, 1, 8>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done, kmin);
-    if (M <= 40) return tma_skinny_cfg<5, 4, 1, 8>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done, kmin);
-    if (M <= 64) return tma_skinny_cfg<4, 4, 2, 4>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done, kmin);
-    if (M <= 80) return tma_skinny_cfg<5, 4, 2, 4>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done, kmin);
-    if (M <= 128) return tma_skinny_cfg<4, 4, 4, 2>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done, kmin);
-    if (M <= 144) return tma_skinny_cfg<6, 4, 3, 2>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done, kmin);
+    if (N <= 0) { *done = true; return 0; }
+    if (Ncanon < 0) Ncanon = N;
+#define TS(a, b, c, d) \
+    tma_skinny_cfg<a, b, c, d>(ctx, M, N, K, X, xdim0, xdim1, ldx, xk0, xm0, Y, ydim0, ydim1, ldy, yk0, yn0, C, ldc, done, kmin, Ncanon)
+    if (M <= 32) return TS(4, 4, 1, 8);
+    if (M <= 40) return TS(5, 4, 1, 8);
+    if (M <= 64) return TS(4, 4, 2, 4);
+    if (M <= 80) return TS(5, 4, 2, 4);
+    if (M <= 128) return TS(4, 4, 4, 2);
+    if (M <= 144) return TS(6, 4, 3, 2);
+#undef TS
     return 0;
 }
 
 // A22 (rows x cols, lda) += V W2  as  A22^T += W2^T Vt  (TMA operands W2, Vt).
 // For K > 64 the C tile is moved by TMA as well (gemm_upd_tma_kernel; needs a
 // 16-byte aligned A22 with an even lda); else the register-epilogue kernel.
+// Every variant computes each element as A + (sum over k, DMMA order): the
+// same bits whichever rows / columns one launch covers.
 static int tma_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, const double *w2, int64_t ldw,
                       const double *vt, int64_t ldvt, double *A22, int64_t lda, bool *done, int *tile_ctr = nullptr) {
     *done = false;
     if (rows <= 0 || cols <= 0) { *done = true; return 0; }
-    // (measured: faster for K = 128, slower for K = 64 where the two-stage
-    // operand ring is too shallow)
     if (K > 64 && !tile_ctr && (((uintptr_t)A22 & 15) == 0) && ((lda & 1) == 0)) {
         constexpr int MT = 4, NT = 4, WM = 2, WN = 4, BK = 32, ST = 2;
         constexpr int BM = 8 * MT * WM, BN = 8 * NT * WN;
@@ -352,11 +404,7 @@ static int tma_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, con
             make_tmap(&tc, A22, rows, cols, lda, BM)) {
             const size_t smem = tma_upd_smem<MT, NT, WM, WN, BK, ST>();
             auto kern = gemm_upd_tma_kernel<MT, NT, WM, WN, BK, ST>;
-            static bool attr = false;
-            if (!attr) {
-                CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                attr = true;
-            }
+            CK(smem_attr((const void *)kern, (int)smem, ctx->device));
             TmaGemmArgs g{cols, rows, K, 0, 0, 0, 0, A22, lda, rup(K, 32), 1, 0, 0};
             const int64_t tiles = ((rows + BN - 1) / BN) * ((cols + BM - 1) / BM);
             const int grid = (int)std::min<int64_t>(tiles, ctx->grid_cap > 0 ? ctx->grid_cap : ctx->num_sms);
@@ -369,8 +417,7 @@ static int tma_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, con
     if ((lda & 1) || ((uintptr_t)A22 & 7)) return 0;
     TmaGemmArgs g{cols, rows, K, 0, 0, 0, 0, A22, lda, rup(K, 32), 1, 0,
                   (((uintptr_t)A22 & 15) == 0 && (lda & 1) == 0) ? 1 : 0};
-    // a short update (the R12 rows of the overlapped schedule): 32 x 64 tiles,
-    // twice as many CTAs; same per-element DMMA sequence (same bits)
+    // a short update (the R12 rows of the overlapped schedules): 32 x 64 tiles
     if (rows <= 64) return launch_tma_cfg<2, 4, 2, 2, EPI_ACCUM_T_PRE>(ctx, w2, K, cols, ldw, vt, K, rows, ldvt, g, done);
     if (tile_ctr) {  // dynamic tile claiming (the GPU is shared with a concurrent kernel)
         g.tile_ctr = tile_ctr;
@@ -379,15 +426,20 @@ static int tma_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, con
     return launch_tma_cfg<4, 4, 2, 4, EPI_ACCUM_T_PRE>(ctx, w2, K, cols, ldw, vt, K, rows, ldvt, g, done);
 }
 
+static int update_any(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, const double *w2, int64_t ldw,
+                      const double *vt, int64_t ldvt, double *A22, int64_t lda, int *tile_ctr = nullptr) {
+    bool dn = false;
+    CKT(tma_update(ctx, rows, cols, K, w2, ldw, vt, ldvt, A22, lda, &dn, tile_ctr));
+    if (!dn) CKT(gemm_update(ctx, rows, cols, K, w2, ldw, vt, ldvt, A22, lda));
+    return 0;
+}
+
 // ---------------------------------------------------------------------------
-// timing helpers
+// timing helpers: events recorded on the stream that runs the phase
 // ---------------------------------------------------------------------------
 static constexpr int kMaxEv = 2 * 4096 + 8;
 static void ph_begin(rqrcp_ctx *ctx, int phase) {
     ctx->open_phase = -1;
-    // phase events are always recorded (measured: the schedule runs faster with
-    // them than without, 4.31 vs 4.58 ms at C2); rqrcp_set_timing(ctx, 0) only
-    // turns their reading off
     if (ctx->nev + 3 > kMaxEv) return;
     ctx->open_phase = phase;
     ctx->open_ev = ctx->nev;
@@ -401,11 +453,20 @@ static void ph_end(rqrcp_ctx *ctx) {
     cudaEventRecord(ctx->ev[ctx->nev++], ctx->stream);
     ctx->open_phase = -1;
 }
+// run f on stream s as the context stream (launch helpers use ctx->stream)
+template <class F>
+static int on_stream(rqrcp_ctx *ctx, cudaStream_t s, F f) {
+    cudaStream_t keep = ctx->stream;
+    ctx->stream = s;
+    int rc = f();
+    ctx->stream = keep;
+    return rc;
+}
 
 // ---------------------------------------------------------------------------
-// C ABI
+// C ABI: small entry points
 // ---------------------------------------------------------------------------
-extern "C" const char *rqrcp_version(void) { return "rqrcp-b200 0.1 (sm_100a, fp64 DMMA)"; }
+extern "C" const char *rqrcp_version(void) { return "rqrcp-b200 0.2 (sm_100a, fp64 DMMA, look-ahead)"; }
 
 extern "C" const char *rqrcp_last_error(const rqrcp_ctx *ctx) { return ctx ? ctx->err.c_str() : g_static_err; }
 
@@ -431,54 +492,84 @@ extern "C" int rqrcp_flops(int64_t m, int64_t n, int64_t k, int b, int p, double
     return 0;
 }
 
+extern "C" int rqrcp_set_option(rqrcp_ctx *ctx, const char *name, int64_t value) {
+    if (!ctx) return -1;
+    if (!name) return -2;
+    for (const OptDesc &d : kOpts)
+        if (std::string(d.name) == name) {
+            if (value < d.lo || value > d.hi) return -3;
+            opt_set(ctx->opt, name, value);
+            return 0;
+        }
+    return -2;
+}
+
+static void opts_from_env(Opts &o) {
+    for (const OptDesc &d : kOpts) {
+        std::string env = "RQRCP_";
+        for (const char *c = d.name; *c; ++c) env += (char)toupper(*c);
+        const char *v = getenv(env.c_str());
+        if (!v || !*v) continue;
+        int64_t x = 0;
+        if (!strcmp(d.name, "panel")) x = (v[0] == 'h' || v[0] == 'H' || v[0] == '0') ? 0 : (v[0] == 'a' || v[0] == '2' ? 2 : 1);
+        else x = atoll(v);
+        if (x >= d.lo && x <= d.hi) opt_set(o, d.name, x);
+    }
+}
+
 static int free_all(rqrcp_ctx *ctx) {
-    if (ctx->comm && nccl().ok) nccl().CommDestroy(ctx->comm);
-    ctx->comm = nullptr;
-    for (void *q : {(void *)ctx->gsend, (void *)ctx->gbuf, (void *)ctx->pack, (void *)ctx->r11, (void *)ctx->dl_cols,
-                    (void *)ctx->dl_slots})
-        if (q) cudaFree(q);
-    if (ctx->h_pairs) cudaFreeHost(ctx->h_pairs);
+    ctx->tr.reset();
     if (ctx->hstatus) cudaFreeHost(ctx->hstatus);
     ctx->hstatus = nullptr;
-    if (ctx->tctr) cudaFree(ctx->tctr);
-    ctx->tctr = nullptr;
-    void *ptrs[] = {ctx->omt,     ctx->bs[0],   ctx->bs[1],     ctx->vfull,     ctx->vt,        ctx->w,
-                    ctx->w2,      ctx->tneg, ctx->ybuf,   ctx->rhat11,    ctx->omhat,     ctx->vhat,      ctx->tauhat,
-                    ctx->splitk,  ctx->slot_hdr, ctx->slot_col, ctx->slot_v2,
-                    ctx->slot_data, ctx->sq_ll, ctx->sq_spill, ctx->pn_part, ctx->pn_rowj, ctx->cq_g, ctx->cq_rc, ctx->cq_rinv, ctx->cq_uinv, ctx->cq_lu, ctx->cqr_status, ctx->bpre, ctx->c5, ctx->wom, ctx->w2om,   ctx->swap_stage,
-                    ctx->swap_dst, ctx->swap_src, ctx->swap_jstage, ctx->swap_np, ctx->perm,     ctx->piv,       ctx->sumsq_part,
-                    ctx->iscal,   ctx->stop_tol2, ctx->bars,  ctx->trace, ctx->ptrace,    ctx->a_dev,     ctx->jpvt_dev,  ctx->tau_dev};
+    void *ptrs[] = {ctx->omt,       ctx->bs[0],     ctx->bs[1],      ctx->vfull_b[0], ctx->vfull_b[1], ctx->vt_b[0],
+                    ctx->vt_b[1],   ctx->w,         ctx->w2,         ctx->w2g,        ctx->tneg,       ctx->ybuf,
+                    ctx->rhat11,    ctx->omhat,     ctx->vhat,       ctx->tauhat,     ctx->splitk,     ctx->pbuf,
+                    ctx->packbuf,   ctx->dispbuf,   ctx->colss,      ctx->ptol2,      ctx->stopc,      ctx->slot_hdr,
+                    ctx->slot_col,  ctx->slot_v2,   ctx->slot_data,  ctx->sq_ll,      ctx->sq_spill,   ctx->pn_part,
+                    ctx->pn_rowj,   ctx->cq_g,      ctx->cq_rc,      ctx->cq_rinv,    ctx->cq_uinv,    ctx->cq_lu,
+                    ctx->cqr_status, ctx->bpre,     ctx->c5,         ctx->wom,        ctx->w2om,       ctx->swap_stage,
+                    ctx->swap_dst,  ctx->swap_src,  ctx->swap_jstage, ctx->swap_np,   ctx->perm,       ctx->piv,
+                    ctx->sumsq_part, ctx->iscal,    ctx->stop_tol2,  ctx->bars,       ctx->trace,      ctx->ptrace,
+                    ctx->a_dev,     ctx->jpvt_dev,  ctx->tau_dev,    ctx->tctr,       ctx->gsend,      ctx->gbuf,
+                    ctx->pack};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     return 0;
 }
 
-extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
+static void destroy_events(rqrcp_ctx *ctx) {
+    for (auto &e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_join, ctx->ev_r12, ctx->ev_upd, ctx->ev_pack})
+        if (e) cudaEventDestroy(e);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->upd) cudaStreamDestroy(ctx->upd);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+}
+
+// Allocates every buffer; the transport is attached by the caller.
+static int create_impl(rqrcp_ctx **out, const rqrcp_config *cfg, int nranks, int rank, bool own_stream_forced) {
     if (!out) return -1;
     *out = nullptr;
     if (!cfg || cfg->max_m < 1 || cfg->max_n < 1 || cfg->max_b < 1 || cfg->max_b > 128 || cfg->max_p < 0 ||
-        cfg->max_b + cfg->max_p > SQ_MAXL || cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks)
+        cfg->max_b + cfg->max_p > SQ_MAXL || nranks < 1 || rank < 0 || rank >= nranks)
         return -2;
-    if (cfg->nranks > 1 && !nccl().ok) return RQRCP_E_UNSUPPORTED;
     rqrcp_ctx *ctx = new rqrcp_ctx();
+    for (auto &e : ctx->ev) e = nullptr;
     ctx->device = cfg->device;
-    ctx->nranks = cfg->nranks;
-    ctx->rank = cfg->rank;
+    ctx->nranks = nranks;
+    ctx->rank = rank;
     ctx->max_m = cfg->max_m;
     ctx->max_n = cfg->max_n;
     ctx->max_b = cfg->max_b;
     ctx->max_p = cfg->max_p;
-    {
-        const char *d = getenv("RQRCP_DEBUG_SYNC");
-        ctx->debug_sync = d && d[0] == '1';
-    }
-    const char *tr = getenv("RQRCP_TRACE");
-    const bool want_trace = tr && tr[0] == '1';
+    opts_from_env(ctx->opt);
+    const bool want_trace = ctx->opt.trace != 0;
     auto fail = [&](int code) {
         free_all(ctx);
-        int rc = code;
+        destroy_events(ctx);
         delete ctx;
-        return rc;
+        return code;
     };
 #define CKC(call)                                                                 \
     do {                                                                          \
@@ -490,11 +581,11 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     } while (0)
     CKC(cudaSetDevice(ctx->device));
     CKC(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
-    if (cfg->stream) {
+    int prio_lo = 0, prio_hi = 0;
+    CKC(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    if (cfg->stream && !own_stream_forced) {
         ctx->stream = (cudaStream_t)cfg->stream;
     } else {
-        int prio_lo = 0, prio_hi = 0;
-        CKC(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         CKC(cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, prio_hi));
         ctx->own_stream = true;
     }
@@ -507,18 +598,31 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(dalloc(&ctx->omt, ctx->ldo * lp));
     CKC(dalloc(&ctx->bs[0], lp * nn));
     CKC(dalloc(&ctx->bs[1], lp * nn));
-    CKC(dalloc(&ctx->vfull, ctx->ldo * bp));
-    CKC(dalloc(&ctx->vt, bp * mm));
+    for (int q = 0; q < 2; ++q) {
+        CKC(dalloc(&ctx->vfull_b[q], ctx->ldo * bp));
+        CKC(dalloc(&ctx->vt_b[q], bp * mm));
+    }
     CKC(dalloc(&ctx->w, bp * nn));
     CKC(dalloc(&ctx->w2, bp * nn));
+    CKC(dalloc(&ctx->w2g, bp * bp));
     CKC(dalloc(&ctx->tneg, bp * bp));
     CKC(dalloc(&ctx->rhat11, bp * bp));
     CKC(dalloc(&ctx->ybuf, bp * bp));
     CKC(dalloc(&ctx->omhat, bp * bp));
     CKC(dalloc(&ctx->vhat, lp * bp));
     CKC(dalloc(&ctx->tauhat, bp));
-    ctx->splitk_elems = std::max<int64_t>(4 << 20, 0);
+    // split-K partials: up to 8 slices of the widest skinny product (W = V^T A22,
+    // the sketch) so the wave-quantisation choice is never capped by space
+    ctx->splitk_elems = std::max<int64_t>(4 << 20, 8 * std::max<int64_t>(bp, lp) * nn);
     CKC(dalloc(&ctx->splitk, ctx->splitk_elems));
+    CKC(dalloc(&ctx->pbuf, ctx->ldo * bp));
+    if (nranks > 1) {
+        CKC(dalloc(&ctx->packbuf, ctx->ldo * bp));
+        CKC(dalloc(&ctx->dispbuf, ctx->ldo * bp));
+    }
+    CKC(dalloc(&ctx->colss, bp));
+    CKC(dalloc(&ctx->ptol2, 1));
+    CKC(cudaMalloc((void **)&ctx->stopc, sizeof(int)));
     CKC(cudaMalloc((void **)&ctx->slot_hdr, sizeof(SqHdr) * 2 * SQ_MAXG * 8));
     CKC(cudaMemset(ctx->slot_hdr, 0, sizeof(SqHdr) * 2 * SQ_MAXG * 8));
     CKC(cudaMalloc((void **)&ctx->slot_col, sizeof(int) * 2 * G));
@@ -536,18 +640,12 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     for (double **q : {&ctx->cq_g, &ctx->cq_rc, &ctx->cq_rinv, &ctx->cq_uinv, &ctx->cq_lu}) CKC(dalloc(q, bp * bp));
     CKC(cudaMalloc((void **)&ctx->cqr_status, sizeof(int)));
     CKC(cudaMemset(ctx->cqr_status, 0xff, sizeof(int)));
-    CKC(cudaFuncSetAttribute(cqr_chol_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (128 * 128 + 64 * 64) * 8));
-    CKC(cudaFuncSetAttribute(cqr_chol_kernel<CQR_EPT_U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (128 * 128 + 64 * 64) * 8));
-    CKC(cudaFuncSetAttribute(cqr_recon_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (128 * 128 + 64 * 64) * 8));
-    CKC(cudaFuncSetAttribute(cqr_recon_kernel<CQR_EPT_F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (128 * 128 + 64 * 64) * 8));
-    CKC(cudaFuncSetAttribute(cqr_rowmul_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 132 * 8));
     CKC(dalloc(&ctx->swap_stage, 2 * bp * mm));
     CKC(cudaMalloc((void **)&ctx->swap_dst, sizeof(int64_t) * 2 * bp));
     CKC(cudaMalloc((void **)&ctx->swap_src, sizeof(int64_t) * 2 * bp));
     CKC(cudaMalloc((void **)&ctx->swap_jstage, sizeof(int64_t) * 2 * bp));
     CKC(cudaMalloc((void **)&ctx->swap_np, sizeof(int)));
+    CKC(cudaMemset(ctx->swap_np, 0, sizeof(int)));
     CKC(cudaMalloc((void **)&ctx->perm, sizeof(int64_t) * nn));
     CKC(cudaMalloc((void **)&ctx->piv, sizeof(int64_t) * bp));
     CKC(dalloc(&ctx->sumsq_part, 4 * G));
@@ -557,17 +655,24 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     CKC(cudaMalloc((void **)&ctx->bars, sizeof(unsigned) * ctx->nbars));
     CKC(cudaMemset(ctx->bars, 0, sizeof(unsigned) * ctx->nbars));
     CKC(cudaMemset(ctx->tneg, 0, sizeof(double) * bp * bp));
-    CKC(cudaFuncSetAttribute(sample_qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
-    CKC(cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmemMax));
-    CKC(cudaFuncSetAttribute(sample_qrcp_reg_kernel<40, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 40 * 8));
-    CKC(cudaFuncSetAttribute(sample_qrcp_reg_kernel<74, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 74 * 8));
-    CKC(cudaFuncSetAttribute(sample_qrcp_reg_kernel<72, 72>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 144 * 8));
-    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel<40>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel<40>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 40 * 8));
-    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel<74>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel<74>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 74 * 8));
-    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel<80>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    CKC(cudaFuncSetAttribute(sample_qrcp_cluster_kernel<80>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 80 * 8));
+    const int dev = ctx->device;
+    CKC(smem_attr((const void *)sample_qrcp_kernel, kDynSmemMax, dev));
+    CKC(smem_attr((const void *)panel_qr_kernel, kDynSmemMax, dev));
+    CKC(smem_attr((const void *)sample_qrcp_reg_kernel<40, 0>, 128 * 40 * 8, dev));
+    CKC(smem_attr((const void *)sample_qrcp_reg_kernel<74, 0>, 128 * 74 * 8, dev));
+    CKC(smem_attr((const void *)sample_qrcp_reg_kernel<72, 72>, 128 * 144 * 8, dev));
+    for (const void *k : {(const void *)sample_qrcp_cluster_kernel<40>, (const void *)sample_qrcp_cluster_kernel<74>,
+                          (const void *)sample_qrcp_cluster_kernel<80>}) {
+        CKC(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    }
+    CKC(smem_attr((const void *)sample_qrcp_cluster_kernel<40>, 128 * 40 * 8, dev));
+    CKC(smem_attr((const void *)sample_qrcp_cluster_kernel<74>, 128 * 74 * 8, dev));
+    CKC(smem_attr((const void *)sample_qrcp_cluster_kernel<80>, 128 * 80 * 8, dev));
+    CKC(smem_attr((const void *)cqr_chol_kernel<9>, (128 * 128 + 64 * 64) * 8, dev));
+    CKC(smem_attr((const void *)cqr_chol_kernel<CQR_EPT_U>, (128 * 128 + 64 * 64) * 8, dev));
+    CKC(smem_attr((const void *)cqr_recon_kernel<16>, (128 * 128 + 64 * 64) * 8, dev));
+    CKC(smem_attr((const void *)cqr_recon_kernel<CQR_EPT_F>, (128 * 128 + 64 * 64) * 8, dev));
+    CKC(smem_attr((const void *)cqr_rowmul_kernel, 128 * 132 * 8, dev));
     {
         ctx->sqc_max = 0;
         for (int cs = SQC_MAXG; cs >= 1 && !ctx->sqc_max; --cs) {
@@ -589,12 +694,12 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
         }
         cudaGetLastError();
     }
-    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<32, 64>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<64, 64>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<64, 32, 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 65 * 8));
-    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 65 * 8));
-    CKC(cudaFuncSetAttribute(panel_qr_cluster_kernel<64, 32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 64 * 8));
+    for (const void *k : {(const void *)panel_qr_cluster_kernel<32, 64>, (const void *)panel_qr_cluster_kernel<64, 64>,
+                          (const void *)panel_qr_cluster_kernel<64, 32, 2>})
+        CKC(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CKC(smem_attr((const void *)panel_qr_cluster_kernel<32, 64>, 32 * 65 * 8, dev));
+    CKC(smem_attr((const void *)panel_qr_cluster_kernel<64, 64>, 64 * 65 * 8, dev));
+    CKC(smem_attr((const void *)panel_qr_cluster_kernel<64, 32, 2>, 64 * 64 * 8, dev));
     {
         ctx->pnc_max = 0;
         for (int cs = PNC_MAXG; cs >= 1 && !ctx->pnc_max; --cs) {
@@ -616,35 +721,19 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
         }
         cudaGetLastError();
     }
-    CKC(cudaFuncSetAttribute(tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (128 * 128 + 64 * 64) * 8));
+    CKC(smem_attr((const void *)tri_kernel, (128 * 128 + 64 * 64) * 8, dev));
     CKC(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithPriority(&ctx->upd, cudaStreamNonBlocking, prio_lo));
     CKC(cudaMallocHost((void **)&ctx->hstatus, sizeof(int) * 8));
     CKC(cudaMalloc((void **)&ctx->tctr, sizeof(int) * 8192));
-    {
-        int prio_lo = 0, prio_hi = 0;
-        CKC(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-        CKC(cudaStreamCreateWithPriority(&ctx->upd, cudaStreamNonBlocking, prio_lo));
-    }
-    CKC(cudaEventCreateWithFlags(&ctx->ev_r12, cudaEventDisableTiming));
-    CKC(cudaEventCreateWithFlags(&ctx->ev_upd, cudaEventDisableTiming));
-    CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
-    CKC(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+    for (cudaEvent_t *e : {&ctx->ev_r12, &ctx->ev_upd, &ctx->ev_fork, &ctx->ev_join, &ctx->ev_pack})
+        CKC(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (auto &e : ctx->ev) CKC(cudaEventCreate(&e));
-    if (ctx->nranks > 1) {
-        const int P = ctx->nranks;
+    if (nranks > 1) {
         CKC(dalloc(&ctx->gsend, lp * (nn + bp)));
-        ctx->gbuf_elems = lp * (nn + (int64_t)P * bp);
+        ctx->gbuf_elems = lp * (nn + (int64_t)nranks * bp);
         CKC(dalloc(&ctx->gbuf, ctx->gbuf_elems));
-        CKC(dalloc(&ctx->pack, bp + 3 * bp * bp + 1));
-        CKC(cudaMalloc((void **)&ctx->dl_cols, sizeof(int64_t) * 4 * bp));
-        CKC(cudaMalloc((void **)&ctx->dl_slots, sizeof(int) * 4 * bp));
-        CKC(cudaMallocHost((void **)&ctx->h_pairs, sizeof(int64_t) * (4 * bp + 2 + 8 * bp)));
-        ncclUniqueId uid;
-        memcpy(uid.internal, cfg->nccl_uid, sizeof(uid.internal));
-        if (nccl().CommInitRank(&ctx->comm, P, uid, ctx->rank) != 0) {
-            fprintf(stderr, "rqrcp_create: ncclCommInitRank failed\n");
-            return fail(RQRCP_E_NCCL);
-        }
+        CKC(dalloc(&ctx->pack, bp + 3 * bp * bp + 4));
     }
     if (want_trace) {
         CKC(cudaMalloc((void **)&ctx->trace, sizeof(unsigned long long) * SQ_MAXG * 64 * 4));
@@ -657,19 +746,61 @@ extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
     return 0;
 }
 
+extern "C" int rqrcp_create(rqrcp_ctx **out, const rqrcp_config *cfg) {
+    if (!out) return -1;
+    if (!cfg) return -2;
+    if (cfg->nranks > 1 && !nccl().ok) return RQRCP_E_UNSUPPORTED;
+    int rc = create_impl(out, cfg, cfg->nranks, cfg->rank, false);
+    if (rc) return rc;
+    rqrcp_ctx *ctx = *out;
+    if (cfg->nranks > 1) {
+        auto t = std::make_unique<NcclTransport>();
+        t->nranks = cfg->nranks;
+        t->rank = cfg->rank;
+        ncclUniqueId uid;
+        memcpy(uid.internal, cfg->nccl_uid, sizeof(uid.internal));
+        if (nccl().CommInitRank(&t->comm, cfg->nranks, uid, cfg->rank) != 0) {
+            fprintf(stderr, "rqrcp_create: ncclCommInitRank failed\n");
+            t->comm = nullptr;
+            rqrcp_destroy(ctx);
+            *out = nullptr;
+            return RQRCP_E_NCCL;
+        }
+        ctx->tr = std::move(t);
+    }
+    return 0;
+}
+
+extern "C" int rqrcp_create_loopback_group(rqrcp_ctx **ctxs, int nranks, const rqrcp_config *cfg) {
+    if (!ctxs) return -1;
+    if (!cfg || nranks < 2 || nranks > LOOP_MAXP) return -2;
+    for (int r = 0; r < nranks; ++r) ctxs[r] = nullptr;
+    if (cudaSetDevice(cfg->device) != cudaSuccess) return RQRCP_E_CUDA;
+    auto grp = std::make_shared<LoopGroup>(nranks);
+    for (int r = 0; r < nranks; ++r) {
+        int rc = create_impl(&ctxs[r], cfg, nranks, r, true);
+        if (rc) {
+            for (int q = 0; q < r; ++q) {
+                rqrcp_destroy(ctxs[q]);
+                ctxs[q] = nullptr;
+            }
+            return rc;
+        }
+        auto t = std::make_unique<LoopTransport>();
+        t->nranks = nranks;
+        t->rank = r;
+        t->grp = grp;
+        ctxs[r]->tr = std::move(t);
+    }
+    return 0;
+}
+
 extern "C" int rqrcp_destroy(rqrcp_ctx *ctx) {
     if (!ctx) return 0;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     free_all(ctx);
-    for (auto &e : ctx->ev) cudaEventDestroy(e);
-    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
-    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
-    if (ctx->side) cudaStreamDestroy(ctx->side);
-    if (ctx->upd) cudaStreamDestroy(ctx->upd);
-    if (ctx->ev_r12) cudaEventDestroy(ctx->ev_r12);
-    if (ctx->ev_upd) cudaEventDestroy(ctx->ev_upd);
-    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    destroy_events(ctx);
     delete ctx;
     return 0;
 }
@@ -739,15 +870,6 @@ extern "C" int rqrcp_get_timings(const rqrcp_ctx *ctx, rqrcp_timings *out) {
     return 0;
 }
 
-// RQRCP_TRACE_PANEL=n: the panel (1-based) whose steps the trace records
-static int trace_panel() {
-    static const int tp = [] {
-        const char *e = getenv("RQRCP_TRACE_PANEL");
-        return e ? std::max(1, atoi(e)) : 1;
-    }();
-    return tp;
-}
-
 static int coop_launch(rqrcp_ctx *ctx, const void *func, int grid, int threads, void **args, size_t smem) {
     int occ = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, func, threads, smem);
@@ -760,7 +882,32 @@ static int coop_launch(rqrcp_ctx *ctx, const void *func, int grid, int threads, 
         ctx->err = std::string("cooperative launch: ") + cudaGetErrorString(e);
         return RQRCP_E_CUDA;
     }
+    if (ctx->opt.debug_sync) {
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            ctx->err = std::string("cooperative kernel: ") + cudaGetErrorString(e);
+            return RQRCP_E_CUDA;
+        }
+    }
     ctx->launches++;
+    return 0;
+}
+
+static int cluster_launch(rqrcp_ctx *ctx, void (*kfn)(SqArgs), int cs, int threads, size_t smem, SqArgs a) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(cs);
+    lc.blockDim = dim3(threads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, kfn, a));
+    CKL();
     return 0;
 }
 
@@ -770,510 +917,275 @@ __global__ void iota_kernel(int64_t *x, int64_t n) {
 }
 
 // ---------------------------------------------------------------------------
-// multi-GPU helpers; all enqueue on ctx->stream
+// The instantiated sample-QRCP kernels (one table: dispatch and schedule
+// choice read the same entries).  Samples of other heights run on the generic
+// cooperative kernel (sample_qrcp.cuh), measured 2-4x slower per pivot.
 // ---------------------------------------------------------------------------
-#define CKN(call)                                                                     \
-    do {                                                                              \
-        ncclResult_t r_ = (call);                                                     \
-        if (r_ != 0) {                                                                \
-            ctx->err = std::string(#call) + ": " + nccl().GetErrorString(r_);         \
-            return RQRCP_E_NCCL;                                                      \
-        }                                                                             \
-    } while (0)
-
-// AllGather each rank's ncols_loc sample columns (global columns >= j0, local
-// order) and reorder into global order: out(:, p) = column j0 + p.
-static int gather_sample(rqrcp_ctx *ctx, int lpad, int64_t ncols_loc, int64_t j0, int64_t ncols, int b, double *out) {
-    const int P = ctx->nranks;
-    int64_t cmax = 0;
-    for (int r = 0; r < P; ++r)
-        cmax = std::max<int64_t>(cmax, dist_count(j0 + ncols, b, P, r) - dist_count(j0, b, P, r));
-    if (cmax * P * lpad > ctx->gbuf_elems) {
-        ctx->err = "gather buffer too small";
-        return RQRCP_E_WORKSPACE;
+struct SqKernels {
+    void (*cluster)(SqArgs);
+    void (*reg)(SqArgs);
+    int reg_ls;  // rows of the register-grid kernel kept in shared memory
+};
+static SqKernels sq_kernels(int l) {
+    if (l == 40) return {sample_qrcp_cluster_kernel<40>, sample_qrcp_reg_kernel<40, 0>, 0};
+    if (l == 74) return {sample_qrcp_cluster_kernel<74>, sample_qrcp_reg_kernel<74, 0>, 0};
+    if (l == 80) return {sample_qrcp_cluster_kernel<80>, nullptr, 0};
+    if (l == 144) return {nullptr, sample_qrcp_reg_kernel<72, 72>, 72};
+    return {nullptr, nullptr, 0};
+}
+enum SqKind { SQK_CLUSTER = 0, SQK_REG = 1, SQK_GRID = 2 };
+static SqKind sq_kind(const rqrcp_ctx *ctx, int l, int64_t np) {
+    const SqKernels k = sq_kernels(l);
+    const int64_t need = (np + SQC_THREADS - 1) / SQC_THREADS;
+    if (ctx->opt.sq_cluster && k.cluster && need <= ctx->sqc_max) return SQK_CLUSTER;
+    const int grid = 1 + (int)((np + SQR_THREADS - 1) / SQR_THREADS);
+    if (ctx->opt.sq_reg && k.reg && grid <= std::min(ctx->num_sms, SQ_MAXG)) return SQK_REG;
+    return SQK_GRID;
+}
+static int sq_ctas(const rqrcp_ctx *ctx, int l, int64_t np) {
+    switch (sq_kind(ctx, l, np)) {
+        case SQK_CLUSTER: return (int)std::max<int64_t>(1, (np + SQC_THREADS - 1) / SQC_THREADS);
+        case SQK_REG: return 1 + (int)((np + SQR_THREADS - 1) / SQR_THREADS);
+        default: return std::min(ctx->num_sms, SQ_MAXG);
     }
-    (void)ncols_loc;
-    ph_begin(ctx, PH_COMM);
-    CKN(nccl().AllGather(ctx->gsend, ctx->gbuf, (size_t)(cmax * lpad), ncclFloat64, ctx->comm, ctx->stream));
-    ph_end(ctx);
-    if (ncols > 0) {
-        dist_reorder_kernel<<<grid_for(ncols * lpad, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
-            ctx->gbuf, cmax, lpad, lpad, j0, ncols, b, P, out, lpad);
-        CKL();
-    }
-    return 0;
 }
 
-// The sample QRCP's (dst <- src) column moves (positions relative to i) on
-// the block-cyclic shards: local copies through the staging buffer, grouped
-// ncclSend/ncclRecv for pairs that cross ranks; jpvt (replicated) on every rank.
-static int dist_swaps(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t i, int b, int64_t *jpvt) {
-    const int P = ctx->nranks, me = ctx->rank;
-    cudaStream_t st = ctx->stream;
-    const int bp = ctx->bpad_max;
-    int64_t *hp = ctx->h_pairs;  // [0] count, [1..2bp] dst, [..] src
-    int hnp = 0;
-    CK(cudaMemcpyAsync(&hp[0], ctx->swap_np, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&hp[1], ctx->swap_dst, sizeof(int64_t) * 2 * bp, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&hp[1 + 2 * bp], ctx->swap_src, sizeof(int64_t) * 2 * bp, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));  // the pivots decide who talks to whom
-    memcpy(&hnp, &hp[0], sizeof(int));
-    const int64_t *dst = &hp[1], *src = &hp[1 + 2 * bp];
-    int64_t *lc = &hp[1 + 4 * bp];          // host lists: stage cols, place cols
-    int *ls = reinterpret_cast<int *>(&hp[1 + 6 * bp]);
-    int nst = 0, npl = 0;
-    std::vector<int> send_q, send_peer, recv_q, recv_peer;
-    for (int q = 0; q < hnp; ++q) {
-        const int so = dist_owner(i + src[q], b, P), dn = dist_owner(i + dst[q], b, P);
-        if (so == me) { lc[nst] = dist_local(i + src[q], b, P); ls[nst] = q; ++nst; }
-        if (so == me && dn != me) { send_q.push_back(q); send_peer.push_back(dn); }
-        if (dn == me && so != me) { recv_q.push_back(q); recv_peer.push_back(so); }
-    }
-    for (int q = 0; q < hnp; ++q) {
-        const int dn = dist_owner(i + dst[q], b, P);
-        if (dn == me) { lc[2 * bp + npl] = dist_local(i + dst[q], b, P); ls[2 * bp + npl] = q; ++npl; }
-    }
-    CK(cudaMemcpyAsync(ctx->dl_cols, lc, sizeof(int64_t) * 4 * bp, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(ctx->dl_slots, ls, sizeof(int) * 4 * bp, cudaMemcpyHostToDevice, st));
-    const int64_t lds = ctx->max_m;
-    if (nst) {
-        dist_columns_kernel<<<grid_for(nst * m, 256, ctx->num_sms), 256, 0, st>>>(A, lda, m, ctx->dl_cols, ctx->dl_slots,
-                                                                                  nst, ctx->swap_stage, lds, 0);
-        CKL();
-    }
-    if (!send_q.empty() || !recv_q.empty()) {
-        ph_begin(ctx, PH_COMM);
-        CKN(nccl().GroupStart());
-        for (size_t e = 0; e < send_q.size(); ++e)
-            CKN(nccl().Send(ctx->swap_stage + (int64_t)send_q[e] * lds, (size_t)m, ncclFloat64, send_peer[e], ctx->comm, st));
-        for (size_t e = 0; e < recv_q.size(); ++e)
-            CKN(nccl().Recv(ctx->swap_stage + (int64_t)recv_q[e] * lds, (size_t)m, ncclFloat64, recv_peer[e], ctx->comm, st));
-        CKN(nccl().GroupEnd());
-        ph_end(ctx);
-    }
-    if (npl) {
-        dist_columns_kernel<<<grid_for(npl * m, 256, ctx->num_sms), 256, 0, st>>>(
-            A, lda, m, ctx->dl_cols + 2 * bp, ctx->dl_slots + 2 * bp, npl, ctx->swap_stage, lds, 1);
-        CKL();
-    }
-    dist_jpvt_kernel<<<1, 256, 0, st>>>(jpvt + i, ctx->swap_dst, ctx->swap_src, ctx->swap_np);
-    CKL();
-    return 0;
-}
-
-// Owner of the panel broadcasts Vfull (ldo x bbpad), and [tau | V^T V | R11];
-// the others unpack and build V^T.
-static int dist_panel_bcast(rqrcp_ctx *ctx, int owner, const double *panel, int64_t lda, int64_t mp, int bb,
-                            int bbpad, double *tau_i) {
-    cudaStream_t st = ctx->stream;
-    const int me = ctx->rank;
-    const int npk = bbpad + 3 * bbpad * bbpad + 1;
-    if (me == owner) {
-        dist_pack_kernel<<<grid_for(npk, 256, ctx->num_sms), 256, 0, st>>>(tau_i, ctx->ybuf, panel, lda, bb, bbpad,
-                                                                           ctx->tneg, ctx->cqr_status, ctx->pack);
-        CKL();
-    }
-    ph_begin(ctx, PH_COMM);
-    CKN(nccl().GroupStart());
-    CKN(nccl().Broadcast(ctx->vfull, ctx->vfull, (size_t)(ctx->ldo * bbpad), ncclFloat64, owner, ctx->comm, st));
-    CKN(nccl().Broadcast(ctx->pack, ctx->pack, (size_t)npk, ncclFloat64, owner, ctx->comm, st));
-    CKN(nccl().GroupEnd());
-    ph_end(ctx);
-    if (me != owner) {
-        dist_unpack_kernel<<<grid_for(npk, 256, ctx->num_sms), 256, 0, st>>>(ctx->pack, bb, bbpad, tau_i, ctx->ybuf,
-                                                                             ctx->tneg, ctx->cqr_status);
-        CKL();
-        dist_transpose_kernel<<<grid_for(mp * bbpad, 256, ctx->num_sms), 256, 0, st>>>(ctx->vfull, ctx->ldo, mp, bbpad,
-                                                                                      ctx->vt);
-        CKL();
-    }
-    return 0;
-}
-
-// S4 via CholeskyQR2 + Householder reconstruction (cqr.cuh).  Enqueues the
-// whole sequence; every kernel is a no-op once *cqr_status = 1.
-static int panel_cqr(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n_loc, int64_t i, int64_t ljp,
-                     int64_t mp, int bb, int bbpad, const int *bb_eff, double *tau_i) {
-    cudaStream_t st = ctx->stream;
-    if (!ctx->cqr_enabled) {
-        CK(cudaMemsetAsync(ctx->cqr_status, 0x01, sizeof(int), st));  // != 0: fallback
-        return 0;
-    }
-    int nb = 8;
-    while (nb < bbpad) nb *= 2;
-    const size_t csm = ((size_t)nb * nb + (size_t)(nb / 2) * (nb / 2)) * sizeof(double);
-    const size_t rsm = (size_t)bbpad * (bbpad + 4) * sizeof(double);
-    double *P = A + i + ljp * lda;
-    const int rows_per_cta = RM_ROWS * (CQR_THREADS / 32);
-    const int rgrid = (int)std::max<int64_t>(1, (mp + rows_per_cta - 1) / rows_per_cta);
-    bool done = false;
-    int rc = 0;
-    // G1 = P^T P (the panel: columns ljp.. of the local A, rows i..m)
-    rc = tma_skinny(ctx, bb, bb, mp, A, m, n_loc, lda, i, ljp, A, m, n_loc, lda, i, ljp, ctx->cq_g, bbpad, &done, 128);
-    if (rc) return rc;
-    if (!done) rc = gemm_skinny(ctx, bb, bb, mp, P, lda, P, lda, ctx->cq_g, bbpad);
-    if (rc) return rc;
-    if (bb <= 64) cqr_chol_kernel<9><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 1, bb_eff, ctx->cqr_status,
-                                                               ctx->cq_rc, ctx->cq_rinv);
-    else cqr_chol_kernel<CQR_EPT_U><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 1, bb_eff, ctx->cqr_status,
-                                                                ctx->cq_rc, ctx->cq_rinv);
-    CKL();
-    // Q1 = P R1^{-1} -> Vfull
-    cqr_rowmul_kernel<<<rgrid, CQR_THREADS, rsm, st>>>(P, lda, 0, mp, bb, bbpad, ctx->cq_rinv, 1.0, ctx->vfull, ctx->ldo,
-                                                       ctx->cqr_status, 0, nullptr, 0, nullptr);
-    CKL();
-    // G2 = Q1^T Q1, R2, Rc = R2 R1; Q = Q1 R2^{-1} (in place)
-    rc = tma_skinny(ctx, bb, bb, mp, ctx->vfull, mp, bbpad, ctx->ldo, 0, 0, ctx->vfull, mp, bbpad, ctx->ldo, 0, 0,
-                    ctx->cq_g, bbpad, &done, 128);
-    if (rc) return rc;
-    if (!done) rc = gemm_skinny(ctx, bb, bb, mp, ctx->vfull, ctx->ldo, ctx->vfull, ctx->ldo, ctx->cq_g, bbpad);
-    if (rc) return rc;
-    if (bb <= 64) cqr_chol_kernel<9><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 2, bb_eff, ctx->cqr_status,
-                                                               ctx->cq_rc, ctx->cq_rinv);
-    else cqr_chol_kernel<CQR_EPT_U><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 2, bb_eff, ctx->cqr_status,
-                                                                ctx->cq_rc, ctx->cq_rinv);
-    CKL();
-    cqr_rowmul_kernel<<<rgrid, CQR_THREADS, rsm, st>>>(ctx->vfull, ctx->ldo, 0, mp, bb, bbpad, ctx->cq_rinv, 1.0,
-                                                       ctx->vfull, ctx->ldo, ctx->cqr_status, 0, nullptr, 0, nullptr);
-    CKL();
-    // reconstruction: top block (L, R, T, tau), then V2 = -Q2 U^{-1} with the outputs
-    if (bb <= 64)
-        cqr_recon_kernel<16><<<1, CQR_THREADS, csm, st>>>(ctx->vfull, ctx->ldo, bb, bbpad, nb, ctx->cq_rc,
-                                                          ctx->cqr_status, P, lda, tau_i, ctx->tneg, ctx->cq_uinv, ctx->vt);
-    else
-        cqr_recon_kernel<CQR_EPT_F><<<1, CQR_THREADS, csm, st>>>(ctx->vfull, ctx->ldo, bb, bbpad, nb, ctx->cq_rc,
-                                                                 ctx->cqr_status, P, lda, tau_i, ctx->tneg,
-                                                                 ctx->cq_uinv, ctx->vt);
-    CKL();
-    if (mp > bb) {
-        const int vgrid = (int)std::max<int64_t>(1, (mp - bb + rows_per_cta - 1) / rows_per_cta);
-        cqr_rowmul_kernel<<<vgrid, CQR_THREADS, rsm, st>>>(ctx->vfull, ctx->ldo, bb, mp, bb, bbpad, ctx->cq_uinv, -1.0,
-                                                           ctx->vfull, ctx->ldo, ctx->cqr_status, 1, P, lda, ctx->vt);
-        CKL();
-    }
-    return 0;
-}
-
-static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
-                       uint64_t seed, int64_t *jpvt, double *tau, int64_t *rank_out, const double *omega_in,
-                       double *omega_out, double *gaps_out, bool keep_last = false, int *final_sample = nullptr) {
-    if (!ctx) return -1;
-    if (!A) return -2;
-    if (lda < std::max<int64_t>(1, m)) return -3;
-    if (m < 1) return -4;
-    if (n < 1) return -5;
-    if (k < 1 || k > std::min(m, n)) return -6;
-    if (b < 1) return -7;
-    if (p < 0 || (int64_t)b + p > m) return -8;
-    if (!jpvt) return -10;
-    if (!tau) return -11;
-    if (!rank_out) return -12;
-    if (m > ctx->max_m || n > ctx->max_n || b > ctx->max_b || p > ctx->max_p) {
-        ctx->err = "problem exceeds the create-time workspace maxima";
-        return RQRCP_E_WORKSPACE;
-    }
-    CK(cudaSetDevice(ctx->device));
-    // panel path: RQRCP_PANEL=hh (column-by-column Householder, default),
-    // =cqr (CholeskyQR2 + reconstruction wherever it is accurate), =auto
-    // (CholeskyQR2 for panels of >= kCqrMinRows rows)
-    int panel_mode = 0;  // measured (C2-C5): the column-by-column kernel is as fast or faster
-    if (const char *e = getenv("RQRCP_PANEL")) panel_mode = (e[0] == 'h' || e[0] == 'H') ? 0 : (e[0] == 'a' ? 2 : 1);
-    const int P = ctx->nranks, me = ctx->rank;
-    const int64_t n_loc = dist_count(n, b, P, me);  // this rank's columns (n when P = 1)
-    ctx->launches = 0;
-    ctx->nev = 0;
-    ctx->lt_t0 = ctx->lt_t1 = -1;
-    ctx->rec_phase.clear();
-    ctx->rec_s.clear();
-    ctx->rec_e.clear();
-    ctx->open_phase = -1;
-    const int l = b + p;
-    const int lpad = (int)rup(l, 8);
-    const int G = ctx->num_sms;
-    cudaStream_t st = ctx->stream;
-    const int ev_t0 = ctx->nev;
-    cudaEventRecord(ctx->ev[ctx->nev++], st);
-    ph_begin(ctx, PH_OMEGA);
-    CK(cudaMemsetAsync(ctx->iscal, 0, sizeof(int) * 8, st));
-    const int64_t npanels = (k + b - 1) / b;
-    CK(cudaMemsetAsync(ctx->bars, 0, sizeof(unsigned) * 2 * npanels, st));
-    CK(cudaMemsetAsync(ctx->tctr, 0, sizeof(int) * std::min<int64_t>(npanels, 8192), st));
-    // ---- S0: Omega^T -----------------------------------------------------
-    if (omega_in) {
-        omega_t_from_kernel<<<grid_for((int64_t)lpad * m, 256, G), 256, 0, st>>>(omega_in, l, lpad, m, ctx->omt,
-                                                                                 ctx->ldo);
-    } else {
-        omega_t_kernel<<<grid_for((int64_t)lpad / 2 * m, 256, G), 256, 0, st>>>(seed, l, lpad, m, ctx->omt, ctx->ldo);
-    }
-    CKL();
-    if (omega_out) {
-        omega_from_t_kernel<<<grid_for((int64_t)l * m, 256, G), 256, 0, st>>>(ctx->omt, ctx->ldo, l, m, omega_out);
-        CKL();
-    }
-    ph_end(ctx);
-    // ---- S1: sketch B = Omega A -------------------------------------------
-    ph_begin(ctx, PH_SKETCH);
-    int cur = 0;
-    bool tdone = false;
-    // this rank's columns: all of them (P = 1) or its block-cyclic shard
-    double *bdst = (P == 1) ? ctx->bs[cur] : ctx->gsend;
-    int rc = tma_skinny(ctx, lpad, n_loc, m, ctx->omt, m, lpad, ctx->ldo, 0, 0, A, m, n_loc, lda, 0, 0, bdst, lpad,
-                        &tdone);
-    if (rc) return rc;
-    if (!tdone) rc = gemm_skinny(ctx, lpad, n_loc, m, ctx->omt, ctx->ldo, A, lda, bdst, lpad);
-    if (rc) return rc;
-    if (P > 1) {  // replicate the sample in global column order (AllGather)
-        rc = gather_sample(ctx, lpad, n_loc, 0, n, b, ctx->bs[cur]);
-        if (rc) return rc;
-    }
-    sumsq_partial_kernel<<<4 * G, 256, 0, st>>>(ctx->bs[cur], lpad, n, lpad, ctx->sumsq_part);
-    CKL();
-    sumsq_final_kernel<<<1, 32, 0, st>>>(ctx->sumsq_part, 4 * G, ctx->stop_tol2, ctx->iscal + 0);
-    CKL();
-    ph_end(ctx);
-
-    int *status = ctx->iscal + 0, *bb_eff = ctx->iscal + 1, *done = ctx->iscal + 2, *rankd = ctx->iscal + 3;
-    // Pi = I_n
-    iota_kernel<<<grid_for(n, 256, G), 256, 0, st>>>(jpvt, n);
-    CKL();
-    CK(cudaMemsetAsync(tau, 0, sizeof(double) * k, st));
-
+// ---------------------------------------------------------------------------
+// One factorization
+// ---------------------------------------------------------------------------
+struct Run {
+    rqrcp_ctx *ctx;
+    double *A;
+    int64_t lda, m, n, k;
+    int b, p, l, lpad, P, me, G;
+    int64_t n_loc;
+    uint64_t seed;
+    int64_t *jpvt;
+    double *tau;
+    const double *omega_in;
+    double *omega_out;
+    rqrcp_trace *trace;
+    bool keep_last;
+    int panel_mode;
+    int sched;
+    int cur = 0;         // sample buffer of the current panel
+    int vb = 0;          // V buffer of the current panel
     int panels = 0;
-    bool upd_pending = false;
-    double *bulk_A22 = nullptr;  // deferred bulk trailing update of this panel (overlap)
-    int64_t bulk_cols = 0;
-    int bulk_cs = 0;
-    // the deferred update waiting for launch (after the next sample QRCP is queued)
-    bool bulk_ready = false;
-    double *bulk_A22_saved = nullptr;
-    int64_t bulk_rows = 0;
-    int bulk_bb = 0, bulk_bbpad = 0;
-    int *bulk_dyn = nullptr;  // non-null: dynamically scheduled bulk update (its tile counter)
-    auto launch_bulk = [&]() -> int {
-        bulk_ready = false;
-        CK(cudaStreamWaitEvent(ctx->upd, ctx->ev_r12, 0));
-        cudaStream_t keep = ctx->stream;
-        ctx->stream = ctx->upd;
-        ctx->grid_cap = bulk_dyn ? 0 : G - bulk_cs;
-        // timed on its own stream: trailing_ms adds the bulk update's duration
-        // (concurrent with S2, so the phases sum to more than total_ms)
-        ph_begin(ctx, PH_TRAIL);
-        bool dn = false;
-        const double *vt_b = ctx->vt + (int64_t)bulk_bb * bulk_bbpad;
-        int r = tma_update(ctx, bulk_rows, bulk_cols, bulk_bbpad, ctx->w2, bulk_bbpad, vt_b, bulk_bbpad,
-                           bulk_A22_saved + bulk_bb, lda, &dn, bulk_dyn);
-        if (!r && !dn)
-            r = gemm_update(ctx, bulk_rows, bulk_cols, bulk_bbpad, ctx->w2, bulk_bbpad, vt_b, bulk_bbpad,
-                            bulk_A22_saved + bulk_bb, lda);
-        ph_end(ctx);
-        ctx->stream = keep;
-        ctx->grid_cap = 0;
-        if (r) return r;
-        CK(cudaEventRecord(ctx->ev_upd, ctx->upd));
-        upd_pending = true;
-        return 0;
-    };
-    for (int64_t i = 0; i < k; i += b) {
+    // the bulk trailing update of the previous panel, not yet launched / joined
+    struct Bulk {
+        bool ready = false, launched = false;
+        double *A22 = nullptr;  // rows i+bb.. of the trailing local columns
+        int64_t rows = 0, cols = 0, lj0 = 0;
+        int bb = 0, bbpad = 0, vbuf = 0;
+        int *dyn = nullptr;
+        int cap = 0;
+    } bulk;
+    int *status, *bb_eff, *done, *rankd;
+    cudaStream_t st;
+
+    int64_t ldv_for(int64_t mp) const { return P > 1 ? rup(mp, 8) : ctx->ldo; }
+    bool more_after(int64_t i, int bb) const { return (i + bb < k) || keep_last; }
+
+    // ---- S2 -------------------------------------------------------------
+    int sample_qrcp(int64_t i) {
         const int bb = (int)std::min<int64_t>(b, k - i);
         const int bbpad = (int)rup(bb, 8);
-        const int64_t mp = m - i, np = n - i, npp = np - bb;
-        ++panels;
-        const bool more = (i + bb < k) || keep_last;  // a sample update follows this panel
-        const bool rule5 = ctx->update_rule == 2 && more && npp > 0;
+        const int64_t np = n - i;
+        const bool rule5 = ctx->update_rule == 2 && more_after(i, bb) && np - bb > 0;
         if (rule5)  // Eq. (5) needs B2 = the pre-QRCP sample
             CK(cudaMemcpyAsync(ctx->bpre, ctx->bs[cur], sizeof(double) * (size_t)lpad * (size_t)np,
                                cudaMemcpyDeviceToDevice, st));
-        // ---- S2: sample QRCP ---------------------------------------------
         ph_begin(ctx, PH_SQRCP);
-        {
-            SqArgs a{};
-            a.B = ctx->bs[cur];
-            a.ldb = lpad;
-            a.l = l;
-            a.lpad = lpad;
-            a.nn = np;
-            a.bb = bb;
-            a.stop_tol2 = ctx->stop_tol2;
-            a.slot_hdr = ctx->slot_hdr;
-            a.slot_col = ctx->slot_col;
-            a.tag0 = (++ctx->launch_seq) << 8;
-            a.slot_v2 = ctx->slot_v2;
-            a.slot_data = ctx->slot_data;
-            a.ll = ctx->sq_ll;
-            a.piv = ctx->piv;
-            a.tauhat = ctx->tauhat;
-            a.vhat = ctx->vhat;
-            a.rhat11 = ctx->rhat11;
-            a.bbpad = bbpad;
-            a.perm = ctx->perm;
-            a.bb_eff = bb_eff;
-            a.done = done;
-            a.rank = rankd;
-            a.status = status;
-            a.gaps = gaps_out ? gaps_out + i : nullptr;
-            a.swap_dst = ctx->swap_dst;
-            a.swap_src = ctx->swap_src;
-            a.swap_np = ctx->swap_np;
-            a.trace = (panels == trace_panel()) ? ctx->trace : nullptr;
-            a.spill = ctx->sq_spill;
-            bool sq_done = false;
-            {
-                // one column per thread in registers, one cluster (sample_qrcp_cl.cuh)
-                const char *e = getenv("RQRCP_SQ_CLUSTER");
-                const bool allow = !(e && e[0] == '0');
-                const int64_t need = (np + SQC_THREADS - 1) / SQC_THREADS;
-                void (*kfn)(SqArgs) = nullptr;
-                if (l == 40) kfn = sample_qrcp_cluster_kernel<40>;
-                else if (l == 74) kfn = sample_qrcp_cluster_kernel<74>;
-                else if (l == 80) kfn = sample_qrcp_cluster_kernel<80>;
-                if (allow && kfn && need <= ctx->sqc_max && !a.gaps) {
-                    const int cs = (int)std::max<int64_t>(1, need);
-                    cudaLaunchConfig_t lc = {};
-                    lc.gridDim = dim3(cs);
-                    lc.blockDim = dim3(SQC_THREADS);
-                    lc.dynamicSmemBytes = (size_t)bb * l * sizeof(double);
-                    lc.stream = st;
-                    cudaLaunchAttribute at[1];
-                    at[0].id = cudaLaunchAttributeClusterDimension;
-                    at[0].val.clusterDim.x = cs;
-                    at[0].val.clusterDim.y = 1;
-                    at[0].val.clusterDim.z = 1;
-                    lc.attrs = at;
-                    lc.numAttrs = 1;
-                    CK(cudaLaunchKernelEx(&lc, kfn, a));
-                    CKL();
-                    sq_done = true;
-                }
-            }
-            if (!sq_done) {
-                // one column per thread in registers (+ shared memory), a grid of
-                // 1 + ceil(n'/256) CTAs (sample_qrcp_reg.cuh)
-                const char *e = getenv("RQRCP_SQ_REG");
-                const bool allow = !(e && e[0] == '0');
-                const int grid = 1 + (int)((np + SQR_THREADS - 1) / SQR_THREADS);
-                void (*kfn)(SqArgs) = nullptr;
-                if (l == 40) kfn = sample_qrcp_reg_kernel<40, 0>;
-                else if (l == 74) kfn = sample_qrcp_reg_kernel<74, 0>;
-                else if (l == 144) kfn = sample_qrcp_reg_kernel<72, 72>;
-                if (allow && kfn && !a.gaps && grid <= std::min(G, SQ_MAXG)) {
-                    const int ls = (l == 144) ? 72 : 0;
-                    const size_t smem = (size_t)std::max(ls * SQR_THREADS, bb * l) * sizeof(double);
-                    a.hstride = 8;
-                    void *args[] = {&a};
-                    rc = coop_launch(ctx, (const void *)kfn, grid, SQR_THREADS, args, smem);
-                    if (rc) return rc;
-                    sq_done = true;
-                }
-            }
-            if (!sq_done) {
+        SqArgs a{};
+        a.B = ctx->bs[cur];
+        a.ldb = lpad;
+        a.l = l;
+        a.lpad = lpad;
+        a.nn = np;
+        a.bb = bb;
+        a.stop_tol2 = ctx->stop_tol2;
+        a.slot_hdr = ctx->slot_hdr;
+        a.slot_col = ctx->slot_col;
+        a.tag0 = (++ctx->launch_seq) << 8;
+        a.slot_v2 = ctx->slot_v2;
+        a.slot_data = ctx->slot_data;
+        a.ll = ctx->sq_ll;
+        a.piv = ctx->piv;
+        a.tauhat = ctx->tauhat;
+        a.vhat = ctx->vhat;
+        a.rhat11 = ctx->rhat11;
+        a.bbpad = bbpad;
+        a.perm = ctx->perm;
+        a.bb_eff = bb_eff;
+        a.done = done;
+        a.rank = rankd;
+        a.status = status;
+        a.gaps = nullptr;
+        a.swap_dst = ctx->swap_dst;
+        a.swap_src = ctx->swap_src;
+        a.swap_np = ctx->swap_np;
+        a.trace = (panels + 1 == ctx->opt.trace_panel) ? ctx->trace : nullptr;
+        a.spill = ctx->sq_spill;
+        const SqKind kind = sq_kind(ctx, l, np);
+        const SqKernels kt = sq_kernels(l);
+        if (kind == SQK_CLUSTER) {
+            const int cs = (int)std::max<int64_t>(1, (np + SQC_THREADS - 1) / SQC_THREADS);
+            CKT(cluster_launch(ctx, kt.cluster, cs, SQC_THREADS, (size_t)bb * l * sizeof(double), a));
+        } else if (kind == SQK_REG) {
+            const int grid = 1 + (int)((np + SQR_THREADS - 1) / SQR_THREADS);
+            const size_t smem = (size_t)std::max(kt.reg_ls * SQR_THREADS, bb * l) * sizeof(double);
             a.hstride = 8;
-            a.poll_mode = 1;
-            if (const char *e = getenv("RQRCP_SQ_HSTRIDE")) a.hstride = std::max(1, std::min(8, atoi(e)));
-            if (const char *e = getenv("RQRCP_SQ_POLL")) a.poll_mode = std::max(0, std::min(2, atoi(e)));
+            void *args[] = {&a};
+            CKT(coop_launch(ctx, (const void *)kt.reg, grid, SQR_THREADS, args, smem));
+        } else {
+            a.hstride = ctx->opt.sq_hstride;
+            a.poll_mode = ctx->opt.sq_poll;
             int gcap = std::min(G, SQ_MAXG);
-            if (const char *e = getenv("RQRCP_SQ_GRID")) gcap = std::max(1, std::min(gcap, atoi(e)));
+            if (ctx->opt.sq_grid > 0) gcap = std::max(1, std::min(gcap, ctx->opt.sq_grid));
             const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(gcap, (np + 7) / 8));
             const int64_t cpb = (np + grid - 1) / grid;
-            // threads per column: fill the CTA (columns x tpc <= 256)
             int tpc = 32;
             while (tpc > 1 && cpb * tpc > SQ_THREADS) tpc >>= 1;
             a.tpc = tpc;
             const int cpw = 32 / tpc;
-            // as many columns in shared memory as the budget allows (row stride
-            // ncs = cpw mod 16 keeps the group's accesses conflict-free), the
-            // rest transposed in the L2-resident spill buffer
             auto pad_ncs = [&](int64_t x) -> int64_t {
                 if (cpw >= 16 || x <= 0) return std::max<int64_t>(x, 1);
                 return x + (((cpw - x) % 16) + 16) % 16;
             };
             const int64_t state = cpb * (2 * (int64_t)sizeof(double) + 2 * (int64_t)sizeof(int));
             int64_t nsm = cpb;
-            if (const char *e = getenv("RQRCP_SQ_NSM")) nsm = std::max<int64_t>(0, std::min<int64_t>(nsm, atoi(e)));
+            if (ctx->opt.sq_nsm >= 0) nsm = std::max<int64_t>(0, std::min<int64_t>(nsm, ctx->opt.sq_nsm));
             while (nsm > 0 && (int64_t)l * pad_ncs(nsm) * 8 + state > kDynSmemMax) --nsm;
             a.nsm = (int)nsm;
             a.ncs = (int)pad_ncs(nsm);
             const size_t smem = sq_smem_bytes(a.ncs, cpb, l);
             void *args[] = {&a};
-            rc = coop_launch(ctx, (const void *)sample_qrcp_kernel, grid, SQ_THREADS, args, smem);
-            if (rc) return rc;
-            }
+            CKT(coop_launch(ctx, (const void *)sample_qrcp_kernel, grid, SQ_THREADS, args, smem));
         }
         ph_end(ctx);
-        if (bulk_ready) {  // the previous panel's bulk update, now that S2 is queued
-            rc = launch_bulk();
-            if (rc) return rc;
+        // trace: R-hat in pivoted order
+        const int64_t t = i / b;
+        if (trace && trace->rhat && t >= trace->first_panel && t < trace->first_panel + trace->npanels) {
+            double *out = trace->rhat + (t - trace->first_panel) * (int64_t)l * n;
+            trace_rhat_kernel<<<grid_for((int64_t)l * np, 256, G), 256, 0, st>>>(ctx->bs[cur], lpad, ctx->perm,
+                                                                               ctx->rhat11, bbpad, l, np, bb_eff, out);
+            CKL();
         }
-        // ---- S3: swaps on A and Pi -----------------------------------------
-        ph_begin(ctx, PH_SWAP);
-        if (upd_pending) {  // the previous panel's bulk trailing update (overlapped with S2)
-            CK(cudaStreamWaitEvent(st, ctx->ev_upd, 0));
-            upd_pending = false;
-        }
-        if (P > 1) {
-            rc = dist_swaps(ctx, A, lda, m, i, b, jpvt);
-            if (rc) return rc;
-        } else {
-            if (2 * bb <= SW_MAXP) {  // one launch: rows are independent
-                swap_fused_kernel<<<(unsigned)((m + SW_ROWS - 1) / SW_ROWS), 256, 0, st>>>(
-                    A + i * lda, lda, m, jpvt + i, ctx->swap_src, ctx->swap_dst, ctx->swap_np);
-                CKL();
-            } else {
-                const int64_t lds = ctx->max_m;
-                const int gg = grid_for(2 * (int64_t)bb * m, 256, G);
-                swap_gather_kernel<<<gg, 256, 0, st>>>(A + i * lda, lda, m, jpvt + i, ctx->swap_src, ctx->swap_np,
-                                                        ctx->swap_stage, lds, ctx->swap_jstage);
-                CKL();
-                swap_scatter_kernel<<<gg, 256, 0, st>>>(A + i * lda, lda, m, jpvt + i, ctx->swap_dst, ctx->swap_np,
-                                                         ctx->swap_stage, lds, ctx->swap_jstage);
-                CKL();
-            }
-        }
-        ph_end(ctx);
-        // ---- S4: panel QR + T ----------------------------------------------
-        ph_begin(ctx, PH_PANEL);
+        return 0;
+    }
+
+    // ---- the bulk rows of a deferred trailing update ------------------------
+    int launch_bulk() {
+        Bulk &u = bulk;
+        if (!u.ready || u.launched) return 0;
+        u.launched = true;
+        CK(cudaStreamWaitEvent(ctx->upd, ctx->ev_pack, 0));
+        ctx->grid_cap = u.dyn ? 0 : u.cap;
+        int rc = on_stream(ctx, ctx->upd, [&]() -> int {
+            ph_begin(ctx, PH_TRAIL);
+            const double *vtb = ctx->vt_b[u.vbuf] + (int64_t)u.bb * u.bbpad;
+            int r = update_any(ctx, u.rows, u.cols, u.bbpad, ctx->w2, u.bbpad, vtb, u.bbpad, u.A22, lda, u.dyn);
+            ph_end(ctx);
+            return r;
+        });
+        ctx->grid_cap = 0;
+        if (rc) return rc;
+        CK(cudaEventRecord(ctx->ev_upd, ctx->upd));
+        return 0;
+    }
+    int join_bulk() {
+        if (!bulk.ready) return 0;
+        if (!bulk.launched) CKT(launch_bulk());
+        CK(cudaStreamWaitEvent(st, ctx->ev_upd, 0));
+        bulk = Bulk();
+        return 0;
+    }
+
+    // ---- S3 pack + S4 panel + S3 unpack -----------------------------------
+    int panel(int64_t i) {
+        const int bb = (int)std::min<int64_t>(b, k - i);
+        const int bbpad = (int)rup(bb, 8);
+        const int64_t mp = m - i;
         const int owner = dist_owner(i, b, P);
-        const int64_t ljp = dist_local(i, b, P);  // owner's local column of the panel
+        const int64_t ljs = dist_local(i, b, P);  // owner's local column of slot 0
+        const int64_t ldp = ctx->ldo;
+        const int nvb = (bulk.ready && sched == 2) ? (vb ^ 1) : vb;  // this panel's V buffer
+        double *vfull = ctx->vfull_b[nvb], *vt = ctx->vt_b[nvb];
+        const int64_t ldv = ldv_for(mp);
+        const bool narrow = bulk.ready && sched == 2;
+        ph_begin(ctx, PH_SWAP);
+        // schedule 1: the bulk update ran beside the sample QRCP; the pivot
+        // columns are read only after it finished
+        if (bulk.ready && sched != 2) CKT(join_bulk());
+        // (1) pack the pivot columns (full height) into this rank's buffer
+        double *pk = (P > 1) ? ctx->packbuf : ctx->pbuf;
+        {
+            dim3 grid((unsigned)std::min<int64_t>(64, (m + 255) / 256), (unsigned)bb);
+            pack_pivots_kernel<<<grid, 256, 0, st>>>(A, lda, m, i, ctx->perm, bb, bb_eff, b, P, me, pk, ldp,
+                                                    narrow ? ctx->w2 : nullptr, bulk.bbpad, bulk.bbpad, bulk.lj0,
+                                                    ctx->w2g);
+            CKL();
+        }
+        // (2) look-ahead: the previous panel's update on these columns (same
+        //     arithmetic per element as the bulk update), then the bulk itself
+        if (narrow) {
+            const double *vtb = ctx->vt_b[bulk.vbuf] + (int64_t)bulk.bb * bulk.bbpad;
+            CKT(update_any(ctx, mp, bb, bulk.bbpad, ctx->w2g, bulk.bbpad, vtb, bulk.bbpad, pk + i, ldp));
+        }
+        CK(cudaEventRecord(ctx->ev_pack, st));
+        if (bulk.ready && sched == 2) CKT(launch_bulk());
+        // (3) P > 1: the owner receives the exact bits (integer sum, one contributor)
+        if (P > 1) {
+            ph_begin(ctx, PH_COMM);
+            CKT(ctx->tr->reduce_u64((const uint64_t *)ctx->packbuf, (uint64_t *)ctx->pbuf, (size_t)(ldp * bb), owner,
+                                    st, ctx->err));
+            ph_end(ctx);
+        }
+        ph_end(ctx);
+        // (4) the panel QR on the owner
+        ph_begin(ctx, PH_PANEL);
+        double *Pp = ctx->pbuf + i;
         if (me == owner) {
-            // CholeskyQR2 + Householder reconstruction (cqr.cuh); on failure
-            // (*cqr_status = 1) the column-by-column kernel below factors it
+            {
+                colsumsq_kernel<<<bb, 256, 0, st>>>(Pp, ldp, mp, bb, bb_eff, ctx->colss);
+                CKL();
+                panel_tol_kernel<<<1, 32, 0, st>>>(ctx->colss, bb, bb_eff, ctx->ptol2);
+                CKL();
+                CK(cudaMemsetAsync(ctx->stopc, 0xff, sizeof(int), st));
+            }
             ctx->cqr_enabled = (panel_mode == 1) || (panel_mode == 2 && mp >= kCqrMinRows);
-            rc = panel_cqr(ctx, A, lda, m, n_loc, i, ljp, mp, bb, bbpad, bb_eff, tau + i);
-            if (rc) return rc;
+            CKT(panel_cqr(i, mp, bb, bbpad, Pp, ldp, vfull, ldv, vt));
             PanelArgs a{};
             a.skip = ctx->cqr_status;
             a.count = ctx->iscal + 4;
-            a.A = A + i + ljp * lda;
-            a.lda = lda;
+            a.A = Pp;
+            a.lda = ldp;
             a.mp = mp;
             a.bb = bb;
             a.bbpad = bbpad;
             a.bb_eff = bb_eff;
             a.tau = tau + i;
-            a.vfull = ctx->vfull;
-            a.ldv = ctx->ldo;
-            a.vt = ctx->vt;
+            a.vfull = vfull;
+            a.ldv = ldv;
+            a.vt = vt;
             a.ybuf = ctx->ybuf;
             a.part = ctx->pn_part;
             a.rowj = ctx->pn_rowj;
-            a.bar = ctx->bars + 2 * (panels - 1) + 1;
-            a.trace = (panels == trace_panel()) ? ctx->ptrace : nullptr;
-            // register-resident cluster kernel (panel_cl.cuh) when the panel fits
-            // one cluster: bb <= 64 and m' <= clusters x rows per CTA
+            a.bar = ctx->bars + 2 * panels + 1;
+            a.tol2 = ctx->ptol2;
+            a.stop_col = ctx->stopc;
+            a.trace = (panels + 1 == ctx->opt.trace_panel) ? ctx->ptrace : nullptr;
             bool pn_done = false;
-            {
-                const char *e = getenv("RQRCP_PN_CLUSTER");
-                const bool allow = !(e && e[0] == '0');
+            if (ctx->opt.pn_cluster) {
                 void (*kfn)(PanelArgs) = nullptr;
                 int64_t rc_rows = 0;
                 size_t psm = 0;
-                const char *ec = getenv("RQRCP_PN_CPT");
-                const bool cpt2 = !(ec && ec[0] == '1');
+                const bool cpt2 = ctx->opt.pn_cpt != 1;
                 if (bb <= 32) { kfn = panel_qr_cluster_kernel<32, 64>; rc_rows = 8 * 64; psm = 32 * 65 * 8; }
-                else if (bb <= 64 && cpt2) {  // two columns x 32 rows per thread
-                    kfn = panel_qr_cluster_kernel<64, 32, 2>; rc_rows = 8 * 32; psm = 64 * 64 * 8;
-                } else if (bb <= 64) { kfn = panel_qr_cluster_kernel<64, 64>; rc_rows = 4 * 64; psm = 64 * 65 * 8; }
+                else if (bb <= 64 && cpt2) { kfn = panel_qr_cluster_kernel<64, 32, 2>; rc_rows = 8 * 32; psm = 64 * 64 * 8; }
+                else if (bb <= 64) { kfn = panel_qr_cluster_kernel<64, 64>; rc_rows = 4 * 64; psm = 64 * 65 * 8; }
                 const int64_t cs = kfn ? (mp + rc_rows - 1) / rc_rows : 0;
-                if (allow && kfn && cs <= ctx->pnc_max) {
+                if (kfn && cs <= ctx->pnc_max) {
                     cudaLaunchConfig_t lc = {};
                     lc.gridDim = dim3((unsigned)cs);
                     lc.blockDim = dim3(PNC_THREADS);
@@ -1292,114 +1204,212 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
                     if (a.trace) ctx->ptrace_kind = 1;
                 }
             }
-            int pcap = G;
-            if (const char *e = getenv("RQRCP_PN_GRID")) pcap = std::max(1, std::min(G, atoi(e)));
-            // ~128 rows per CTA: fewer CTAs shrink the per-column all-to-all of
-            // partial Gram rows (G x bb doubles read by every CTA), more rows
-            // per CTA lengthen the local pass (measured best at C3: 64 / 96 /
-            // 128 / 192 / 256 rows -> 8.17 / 8.16 / 7.76 / 8.32 / 9.18 ms)
-            int64_t prows = 128;
-            if (const char *e = getenv("RQRCP_PN_ROWS")) prows = std::max(1, atoi(e));
-            const int grid = (int)std::max<int64_t>((mp + PN_MAXROWS - 1) / PN_MAXROWS,
-                                                    std::min<int64_t>(pcap, (mp + prows - 1) / prows));
-            const int64_t rpb = (mp + grid - 1) / grid;
-            if (rpb > PN_MAXROWS) {
-                ctx->err = "panel too tall for the cooperative grid";
-                return RQRCP_E_WORKSPACE;
-            }
-            // as many of each CTA's rows in shared memory as fit, the rest via L2
-            a.nsm = (int)std::min<int64_t>(rpb, kDynSmemMax / ((int64_t)bb * sizeof(double)));
-            const size_t smem = (size_t)a.nsm * bb * sizeof(double);
-            void *args[] = {&a};
             if (!pn_done) {
-                rc = coop_launch(ctx, (const void *)panel_qr_kernel, grid, PN_THREADS, args, smem);
+                int pcap = G;
+                if (ctx->opt.pn_grid > 0) pcap = std::max(1, std::min(G, ctx->opt.pn_grid));
+                if (bulk.ready && bulk.launched) pcap = std::min(pcap, ctx->opt.la_panel_ctas);  // share with the bulk
+                const int64_t prows = ctx->opt.pn_rows;
+                const int grid = (int)std::max<int64_t>((mp + PN_MAXROWS - 1) / PN_MAXROWS,
+                                                        std::min<int64_t>(pcap, (mp + prows - 1) / prows));
+                const int64_t rpb = (mp + grid - 1) / grid;
+                if (rpb > PN_MAXROWS) {
+                    ctx->err = "panel too tall for the cooperative grid";
+                    return RQRCP_E_WORKSPACE;
+                }
+                a.nsm = (int)std::min<int64_t>(rpb, kDynSmemMax / ((int64_t)bb * sizeof(double)));
+                const size_t smem = (size_t)a.nsm * bb * sizeof(double);
+                void *args[] = {&a};
+                CKT(coop_launch(ctx, (const void *)panel_qr_kernel, grid, PN_THREADS, args, smem));
                 if (a.trace) ctx->ptrace_kind = 0;
             }
-            if (rc) return rc;
+            panel_stop_apply_kernel<<<1, 32, 0, st>>>(ctx->stopc, bb_eff, rankd, done);
+            CKL();
         }
-        const double *R11p = A + i + ljp * lda;
-        int64_t ldr11 = lda;
-        if (P > 1) {  // owner broadcasts V, tau, V^T V and R11
-            rc = dist_panel_bcast(ctx, owner, A + i + ljp * lda, lda, mp, bb, bbpad, tau + i);
-            if (rc) return rc;
+        // (5) P > 1: the owner broadcasts V, tau, V^T V, R11 (and T), the state
+        const double *R11p = Pp;
+        int64_t ldr11 = ldp;
+        if (P > 1) {
+            const int npk = bbpad + 3 * bbpad * bbpad + 4;
+            if (me == owner) {
+                dist_pack_kernel<<<grid_for(npk, 256, G), 256, 0, st>>>(tau + i, ctx->ybuf, Pp, ldp, bb, bbpad,
+                                                                      ctx->tneg, ctx->cqr_status, bb_eff, ctx->pack);  // state = iscal[1..3]
+                CKL();
+            }
+            ph_begin(ctx, PH_COMM);
+            CKT(ctx->tr->bcast(vfull, sizeof(double) * (size_t)(ldv * bbpad), owner, st, ctx->err));
+            CKT(ctx->tr->bcast(ctx->pack, sizeof(double) * (size_t)npk, owner, st, ctx->err));
+            ph_end(ctx);
+            if (me != owner) {
+                dist_unpack_kernel<<<grid_for(npk, 256, G), 256, 0, st>>>(ctx->pack, bb, bbpad, tau + i, ctx->ybuf,
+                                                                        ctx->tneg, ctx->cqr_status, bb_eff);  // state = iscal[1..3]
+                CKL();
+                dist_transpose_kernel<<<grid_for(mp * bbpad, 256, G), 256, 0, st>>>(vfull, ldv, mp, bbpad, vt);
+                CKL();
+            }
             R11p = ctx->pack + bbpad + (int64_t)bbpad * bbpad;
             ldr11 = bbpad;
         }
-        // T and Omega-hat11 on the side stream, overlapping W = V^T A22
+        // T (and Omega-hat11 for Eq. (4)) on the side stream, overlapping W = V^T A22
         {
+            const bool rule5 = ctx->update_rule == 2 && more_after(i, bb) && n - i - bb > 0;
             int nb = 8;
             while (nb < bbpad) nb *= 2;
             const size_t smem = ((size_t)nb * nb + (size_t)(nb / 2) * (nb / 2)) * sizeof(double);
             CK(cudaEventRecord(ctx->ev_fork, st));
             CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-            const int do_om = (more && npp > 0 && !rule5) ? 1 : 0;
+            const int do_om = (more_after(i, bb) && n - i - bb > 0 && !rule5) ? 1 : 0;
             tri_kernel<<<2, TRI_THREADS, smem, ctx->side>>>(ctx->ybuf, tau + i, ctx->rhat11, R11p, ldr11, bb, bbpad,
                                                           nb, bb_eff, ctx->tneg, ctx->omhat, do_om, ctx->cqr_status);
             CKL();
             CK(cudaEventRecord(ctx->ev_join, ctx->side));
         }
         ph_end(ctx);
-        // ---- S5: trailing update A22 -= V T^T V^T A22 ------------------------
-        ph_begin(ctx, PH_TRAIL);
-        // this rank's trailing columns: local [lj0, n_loc) = global columns >= i + bb
+        // (6) the previous panel's bulk update must be complete before the
+        //     displaced columns move and the panel is written back
+        ph_begin(ctx, PH_SWAP);
+        CKT(join_bulk());
+        const dim3 g1((unsigned)std::min<int64_t>(64, (m + 255) / 256), (unsigned)(2 * bb));
+        if (P > 1) {
+            if (me == owner) {
+                pack_slots_kernel<<<dim3(g1.x, bb), 256, 0, st>>>(A, lda, m, ljs, bb, bb_eff, ctx->dispbuf, ldp);
+                CKL();
+            }
+            ph_begin(ctx, PH_COMM);
+            CKT(ctx->tr->bcast(ctx->dispbuf, sizeof(double) * (size_t)(ldp * bb), owner, st, ctx->err));
+            ph_end(ctx);
+            place_displaced_kernel<<<g1, 256, 0, st>>>(A, lda, m, i, ctx->swap_dst, ctx->swap_src, ctx->swap_np, bb,
+                                                      bb_eff, b, P, me, ctx->dispbuf, ldp);
+            CKL();
+        } else {
+            place_displaced_kernel<<<g1, 256, 0, st>>>(A, lda, m, i, ctx->swap_dst, ctx->swap_src, ctx->swap_np, bb,
+                                                      bb_eff, b, P, me, A + i * lda, lda);
+            CKL();
+        }
+        if (me == owner) {
+            copy_back_kernel<<<dim3(g1.x, bb), 256, 0, st>>>(A, lda, m, ljs, bb, bb_eff, ctx->pbuf, ldp);
+            CKL();
+        }
+        {
+            const int64_t t = i / b;
+            int64_t *pv = nullptr;
+            if (trace && trace->pivots && t >= trace->first_panel && t < trace->first_panel + trace->npanels)
+                pv = trace->pivots + (t - trace->first_panel) * b;
+            jpvt_moves_kernel<<<1, 256, 0, st>>>(jpvt + i, ctx->swap_dst, ctx->swap_src, ctx->swap_np, bb_eff, bb, pv);
+            CKL();
+        }
+        ph_end(ctx);
+        vb = nvb;
+        return 0;
+    }
+
+    // S4 via CholeskyQR2 + Householder reconstruction (cqr.cuh) on the panel
+    // buffer.  Every kernel is a no-op once *cqr_status = 1.
+    int panel_cqr(int64_t i, int64_t mp, int bb, int bbpad, double *Pp, int64_t ldp, double *vfull, int64_t ldv,
+                  double *vt) {
+        if (!ctx->cqr_enabled) {
+            CK(cudaMemsetAsync(ctx->cqr_status, 0x01, sizeof(int), st));  // != 0: fallback
+            return 0;
+        }
+        int nb = 8;
+        while (nb < bbpad) nb *= 2;
+        const size_t csm = ((size_t)nb * nb + (size_t)(nb / 2) * (nb / 2)) * sizeof(double);
+        const size_t rsm = (size_t)bbpad * (bbpad + 4) * sizeof(double);
+        const int rows_per_cta = RM_ROWS * (CQR_THREADS / 32);
+        const int rgrid = (int)std::max<int64_t>(1, (mp + rows_per_cta - 1) / rows_per_cta);
+        bool dn = false;
+        // G1 = P^T P
+        CKT(tma_skinny(ctx, bb, bb, mp, ctx->pbuf, m, bb, ldp, i, 0, ctx->pbuf, m, bb, ldp, i, 0, ctx->cq_g, bbpad, &dn, 128));
+        if (!dn) CKT(gemm_skinny(ctx, bb, bb, mp, Pp, ldp, Pp, ldp, ctx->cq_g, bbpad));
+        if (bb <= 64) cqr_chol_kernel<9><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 1, bb_eff, ctx->cqr_status,
+                                                                   ctx->cq_rc, ctx->cq_rinv, ctx->ptol2);
+        else cqr_chol_kernel<CQR_EPT_U><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 1, bb_eff, ctx->cqr_status,
+                                                                    ctx->cq_rc, ctx->cq_rinv, ctx->ptol2);
+        CKL();
+        cqr_rowmul_kernel<<<rgrid, CQR_THREADS, rsm, st>>>(Pp, ldp, 0, mp, bb, bbpad, ctx->cq_rinv, 1.0, vfull, ldv,
+                                                           ctx->cqr_status, 0, nullptr, 0, nullptr);
+        CKL();
+        CKT(tma_skinny(ctx, bb, bb, mp, vfull, mp, bbpad, ldv, 0, 0, vfull, mp, bbpad, ldv, 0, 0, ctx->cq_g, bbpad, &dn, 128));
+        if (!dn) CKT(gemm_skinny(ctx, bb, bb, mp, vfull, ldv, vfull, ldv, ctx->cq_g, bbpad));
+        if (bb <= 64) cqr_chol_kernel<9><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 2, bb_eff, ctx->cqr_status,
+                                                                   ctx->cq_rc, ctx->cq_rinv, nullptr);
+        else cqr_chol_kernel<CQR_EPT_U><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 2, bb_eff, ctx->cqr_status,
+                                                                    ctx->cq_rc, ctx->cq_rinv, nullptr);
+        CKL();
+        cqr_rowmul_kernel<<<rgrid, CQR_THREADS, rsm, st>>>(vfull, ldv, 0, mp, bb, bbpad, ctx->cq_rinv, 1.0, vfull, ldv,
+                                                           ctx->cqr_status, 0, nullptr, 0, nullptr);
+        CKL();
+        if (bb <= 64)
+            cqr_recon_kernel<16><<<1, CQR_THREADS, csm, st>>>(vfull, ldv, bb, bbpad, nb, ctx->cq_rc, ctx->cqr_status, Pp,
+                                                              ldp, tau + i, ctx->tneg, ctx->cq_uinv, vt);
+        else
+            cqr_recon_kernel<CQR_EPT_F><<<1, CQR_THREADS, csm, st>>>(vfull, ldv, bb, bbpad, nb, ctx->cq_rc,
+                                                                     ctx->cqr_status, Pp, ldp, tau + i, ctx->tneg,
+                                                                     ctx->cq_uinv, vt);
+        CKL();
+        if (mp > bb) {
+            const int vgrid = (int)std::max<int64_t>(1, (mp - bb + rows_per_cta - 1) / rows_per_cta);
+            cqr_rowmul_kernel<<<vgrid, CQR_THREADS, rsm, st>>>(vfull, ldv, bb, mp, bb, bbpad, ctx->cq_uinv, -1.0, vfull,
+                                                               ldv, ctx->cqr_status, 1, Pp, ldp, vt);
+            CKL();
+        }
+        return 0;
+    }
+
+    // ---- S5 trailing update (+ S6 sample update) and the next S2 ------------
+    int trailing_and_sample(int64_t i) {
+        const int bb = (int)std::min<int64_t>(b, k - i);
+        const int bbpad = (int)rup(bb, 8);
+        const int64_t mp = m - i, np = n - i, npp = np - bb;
+        const bool more = more_after(i, bb);
+        const bool rule5 = ctx->update_rule == 2 && more && npp > 0;
         const int64_t lj0 = dist_count(i + bb, b, P, me);
         const int64_t npl = n_loc - lj0;
+        const double *vfull = ctx->vfull_b[vb];
+        const double *vt = ctx->vt_b[vb];
+        const int64_t ldv = ldv_for(mp);
+        // the next sample QRCP decides the schedule of this panel's bulk rows
+        const int64_t inext = i + bb;
+        const bool next_panel = (i + bb < k);
+        // (decided from global sizes only: every rank takes the same schedule,
+        // so kernel shapes -- and bits -- do not depend on the rank count)
+        int s = sched;
+        if (!next_panel || npp <= 0 || mp <= bb) s = 0;
+        ph_begin(ctx, PH_TRAIL);
         if (npl > 0) {
             double *A22 = A + i + lj0 * lda;
-            // W = V^T A22: V = Vfull(0:m', 0:bbpad); A22 = A(i:m, lj0:n_loc) by TMA coordinates
-            rc = tma_skinny(ctx, bbpad, npl, mp, ctx->vfull, mp, bbpad, ctx->ldo, 0, 0, A, m, n_loc, lda, i, lj0,
-                            ctx->w, bbpad, &tdone);
-            if (rc) return rc;
-            if (!tdone) rc = gemm_skinny(ctx, bbpad, npl, mp, ctx->vfull, ctx->ldo, A22, lda, ctx->w, bbpad);
-            if (rc) return rc;
+            bool dn = false;
+            // W = V^T A22 (canonical split-K over the GLOBAL trailing width)
+            CKT(tma_skinny(ctx, bbpad, npl, mp, vfull, mp, bbpad, ldv, 0, 0, A, m, n_loc, lda, i, lj0, ctx->w, bbpad,
+                           &dn, 512, npp));
+            if (!dn) CKT(gemm_skinny(ctx, bbpad, npl, mp, vfull, ldv, A22, lda, ctx->w, bbpad, npp));
             CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
-            rc = gemm_skinny(ctx, bbpad, npl, bbpad, ctx->tneg, bbpad, ctx->w, bbpad, ctx->w2, bbpad);
-            if (rc) return rc;
-            // Overlap: when the next panel's sample QRCP runs on one cluster, only
-            // the R12 rows (all Eq. (4) needs) are updated here; the bulk A22 rows
-            // i+bb..m go to the low-priority `upd` stream on G - (cluster) CTAs and
-            // run concurrently with S6 and the next sample QRCP (the next swap
-            // waits for them).  P = 1, Eq. (4) only.
-            bool ovl = false;
-            int next_cs = 0;
-            if (P == 1 && !rule5 && more && npp > 0 && mp > bb && (bb % 2) == 0 && !gaps_out &&
-                (l == 40 || l == 74 || l == 80)) {
-                const char *e1 = getenv("RQRCP_OVERLAP"), *e2 = getenv("RQRCP_SQ_CLUSTER");
-                next_cs = (int)std::max<int64_t>(1, (npp + SQC_THREADS - 1) / SQC_THREADS);
-                ovl = !(e1 && e1[0] == '0') && !(e2 && e2[0] == '0') && next_cs <= ctx->sqc_max;
-            }
-            // the next sample QRCP on the register grid (C3-sized samples): the bulk
-            // update runs on the whole GPU with dynamically claimed tiles, so the
-            // CTAs that find their SM taken by the sample QRCP start late and take
-            // fewer tiles (bb <= 64: the K <= 64 update kernel)
-            bool dyn = false;
-            if (!ovl && P == 1 && !rule5 && more && npp > 0 && mp > bb && (bb % 2) == 0 && bbpad <= 64 &&
-                !gaps_out && (l == 40 || l == 74)) {
-                const char *e1 = getenv("RQRCP_OVERLAP"), *e2 = getenv("RQRCP_SQ_REG"),
-                           *e3 = getenv("RQRCP_OVERLAP_GRID");
-                const int64_t ngrid = 1 + (npp + SQR_THREADS - 1) / SQR_THREADS;
-                dyn = !(e1 && e1[0] == '0') && !(e2 && e2[0] == '0') && !(e3 && e3[0] == '0') &&
-                      ngrid <= std::min(G, SQ_MAXG) && panels <= 8192;
-                ovl = dyn;
-                next_cs = 0;
-            }
-            if (ovl) {
-                rc = tma_update(ctx, bb, npl, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda, &tdone);
-                if (rc) return rc;
-                if (!tdone) rc = gemm_update(ctx, bb, npl, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda);
-                if (rc) return rc;
-                bulk_A22 = A22;
-                bulk_cols = npl;
-                bulk_cs = next_cs;
-                bulk_dyn = dyn ? ctx->tctr + (panels - 1) : nullptr;
+            CKT(gemm_skinny(ctx, bbpad, npl, bbpad, ctx->tneg, bbpad, ctx->w, bbpad, ctx->w2, bbpad, npp));
+            if (s == 0) {
+                CKT(update_any(ctx, mp, npl, bbpad, ctx->w2, bbpad, vt, bbpad, A22, lda));
             } else {
-                rc = tma_update(ctx, mp, npl, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda, &tdone);
-                if (rc) return rc;
-                if (!tdone) rc = gemm_update(ctx, mp, npl, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, A22, lda);
-                if (rc) return rc;
+                // the R12 rows (all Eq. (4) / (5) need) now; the bulk rows later
+                CKT(update_any(ctx, bb, npl, bbpad, ctx->w2, bbpad, vt, bbpad, A22, lda));
+                bulk = Bulk();
+                bulk.ready = true;
+                bulk.A22 = A22 + bb;
+                bulk.rows = mp - bb;
+                bulk.cols = npl;
+                bulk.lj0 = lj0;
+                bulk.bb = bb;
+                bulk.bbpad = bbpad;
+                bulk.vbuf = vb;
             }
         } else {
             CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+            if (s != 0) {  // no local trailing columns: an empty bulk keeps the schedule uniform
+                bulk = Bulk();
+                bulk.ready = true;
+                bulk.A22 = A + i + bb + lj0 * lda;
+                bulk.lj0 = lj0;
+                bulk.bb = bb;
+                bulk.bbpad = bbpad;
+                bulk.vbuf = vb;
+            }
         }
         ph_end(ctx);
         // ---- S6: sample update (Eq. (4) or (5)); skipped after the last panel (R-G9)
@@ -1411,141 +1421,239 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
                 // three contractions as the trailing update), then
                 // C = Omega-bar_1 R12 and B_next = B2 - C
                 bool dn = false;
-                rc = tma_skinny(ctx, bbpad, lpad, mp, ctx->vfull, mp, bbpad, ctx->ldo, 0, 0, ctx->omt, m, lpad,
-                                ctx->ldo, i, 0, ctx->wom, bbpad, &dn);
-                if (rc) return rc;
-                if (!dn) rc = gemm_skinny(ctx, bbpad, lpad, mp, ctx->vfull, ctx->ldo, ctx->omt + i, ctx->ldo, ctx->wom,
-                                          bbpad);
-                if (rc) return rc;
-                rc = gemm_skinny(ctx, bbpad, lpad, bbpad, ctx->tneg, bbpad, ctx->wom, bbpad, ctx->w2om, bbpad);
-                if (rc) return rc;
-                rc = tma_update(ctx, mp, lpad, bbpad, ctx->w2om, bbpad, ctx->vt, bbpad, ctx->omt + i, ctx->ldo, &dn);
-                if (rc) return rc;
-                if (!dn) rc = gemm_update(ctx, mp, lpad, bbpad, ctx->w2om, bbpad, ctx->vt, bbpad, ctx->omt + i, ctx->ldo);
-                if (rc) return rc;
+                CKT(tma_skinny(ctx, bbpad, lpad, mp, vfull, mp, bbpad, ldv, 0, 0, ctx->omt, m, lpad, ctx->ldo, i, 0,
+                               ctx->wom, bbpad, &dn));
+                if (!dn) CKT(gemm_skinny(ctx, bbpad, lpad, mp, vfull, ldv, ctx->omt + i, ctx->ldo, ctx->wom, bbpad));
+                CKT(gemm_skinny(ctx, bbpad, lpad, bbpad, ctx->tneg, bbpad, ctx->wom, bbpad, ctx->w2om, bbpad));
+                CKT(update_any(ctx, mp, lpad, bbpad, ctx->w2om, bbpad, vt, bbpad, ctx->omt + i, ctx->ldo));
                 if (npl > 0) {
-                    rc = gemm_skinny(ctx, lpad, npl, bb, ctx->omt + i, ctx->ldo, A + i + lj0 * lda, lda, ctx->c5, lpad);
-                    if (rc) return rc;
+                    CKT(gemm_skinny(ctx, lpad, npl, bb, ctx->omt + i, ctx->ldo, A + i + lj0 * lda, lda, ctx->c5, lpad, npp));
                     sample_update5_kernel<<<grid_for((int64_t)lpad * npl, 256, G), 256, 0, st>>>(
-                        ctx->bpre, lpad, ctx->perm, ctx->c5, lpad, bb, l, lpad, npl, bb_eff, udst, lpad, i, lj0, b, P,
-                        me);
+                        ctx->bpre, lpad, ctx->perm, ctx->c5, lpad, bb, l, lpad, npl, bb_eff, udst, lpad, i, lj0, b, P, me);
                     CKL();
                 }
             } else if (npl > 0) {
                 // C = Omega-hat11 R12 (DMMA; omhat holds Omega-hat11^T), then the
                 // gather B_next = [R-hat12 - C; R-hat22] (Eq. (4))
-                rc = gemm_skinny(ctx, bbpad, npl, bb, ctx->omhat, bbpad, A + i + lj0 * lda, lda, ctx->c5, lpad);
-                if (rc) return rc;
+                CKT(gemm_skinny(ctx, bbpad, npl, bb, ctx->omhat, bbpad, A + i + lj0 * lda, lda, ctx->c5, lpad, npp));
                 sample_update4_kernel<<<grid_for((int64_t)lpad * npl, 256, G), 256, 0, st>>>(
-                    ctx->bs[cur], lpad, ctx->perm, ctx->c5, lpad, bb, l, lpad, npl, bb_eff, udst, lpad, i, lj0, b, P,
-                    me);
+                    ctx->bs[cur], lpad, ctx->perm, ctx->c5, lpad, bb, l, lpad, npl, bb_eff, udst, lpad, i, lj0, b, P, me);
                 CKL();
             }
-            if (P > 1) {
-                rc = gather_sample(ctx, lpad, npl, i + bb, n - i - bb, b, ctx->bs[cur ^ 1]);
-                if (rc) return rc;
-            }
+            if (P > 1) CKT(gather_sample(npl, i + bb, n - i - bb, ctx->bs[cur ^ 1]));
             ph_end(ctx);
             cur ^= 1;
+            const int64_t t = i / b;
+            if (trace && trace->bnext && t >= trace->first_panel && t < trace->first_panel + trace->npanels) {
+                double *out = trace->bnext + (t - trace->first_panel) * (int64_t)l * n;
+                trace_copy_kernel<<<grid_for((int64_t)l * npp, 256, G), 256, 0, st>>>(ctx->bs[cur], lpad, l, npp, out);
+                CKL();
+            }
         }
-        if (bulk_A22) {
-            // the bulk rows i+bb..m of this panel's trailing update may start once
-            // S6 is done; they are launched after the next sample QRCP has been
-            // queued (below), so that kernel is dispatched onto its cluster first
-            CK(cudaEventRecord(ctx->ev_r12, st));
-            bulk_rows = mp - bb;
-            bulk_bb = bb;
-            bulk_bbpad = bbpad;
-            bulk_ready = true;
-            bulk_A22_saved = bulk_A22;
-            bulk_A22 = nullptr;
+        if (!next_panel) return 0;
+        // ---- the next panel's S2; schedule 1 launches the bulk rows behind it
+        if (s == 1) CK(cudaEventRecord(ctx->ev_pack, st));  // the bulk may start once S6 is done
+        CKT(sample_qrcp(inext));
+        if (s == 1) {
+            // the bulk rows on the SMs the sample QRCP leaves free (cluster), or on
+            // the whole GPU with dynamically claimed tiles (register grid)
+            const SqKind kind = sq_kind(ctx, l, n - inext);
+            if (kind == SQK_CLUSTER) bulk.cap = G - sq_ctas(ctx, l, n - inext);
+            else if (kind == SQK_REG && bulk.bbpad <= 64 && panels < 8192) bulk.dyn = ctx->tctr + panels;
+            else bulk.cap = 0;
+            CKT(launch_bulk());
+        } else if (s == 2) {
+            bulk.cap = std::max(1, G - ctx->opt.la_panel_ctas);
         }
+        return 0;
     }
-    if (bulk_ready) {
-        rc = launch_bulk();
-        if (rc) return rc;
+
+    // AllGather each rank's ncols_loc sample columns (global columns >= j0, local
+    // order) and reorder into global order: out(:, p) = column j0 + p.
+    int gather_sample(int64_t ncols_loc, int64_t j0, int64_t ncols, double *out) {
+        int64_t cmax = 0;
+        for (int r = 0; r < P; ++r)
+            cmax = std::max<int64_t>(cmax, dist_count(j0 + ncols, b, P, r) - dist_count(j0, b, P, r));
+        if (cmax * P * lpad > ctx->gbuf_elems) {
+            ctx->err = "gather buffer too small";
+            return RQRCP_E_WORKSPACE;
+        }
+        (void)ncols_loc;
+        ph_begin(ctx, PH_COMM);
+        CKT(ctx->tr->allgather(ctx->gsend, ctx->gbuf, sizeof(double) * (size_t)(cmax * lpad), st, ctx->err));
+        ph_end(ctx);
+        if (ncols > 0) {
+            dist_reorder_kernel<<<grid_for(ncols * lpad, 256, G), 256, 0, st>>>(ctx->gbuf, cmax, lpad, lpad, j0, ncols, b,
+                                                                               P, out, lpad);
+            CKL();
+        }
+        return 0;
     }
-    if (upd_pending) CK(cudaStreamWaitEvent(st, ctx->ev_upd, 0));
-    if (final_sample) *final_sample = cur;
-    // ---- status (pinned host words) ----------------------------------------
+
+    int setup() {
+        ph_begin(ctx, PH_OMEGA);
+        CK(cudaMemsetAsync(ctx->iscal, 0, sizeof(int) * 8, st));
+        const int64_t npanels = (k + b - 1) / b;
+        CK(cudaMemsetAsync(ctx->bars, 0, sizeof(unsigned) * std::min<int64_t>(ctx->nbars, 2 * npanels + 2), st));
+        CK(cudaMemsetAsync(ctx->tctr, 0, sizeof(int) * std::min<int64_t>(npanels, 8192), st));
+        if (omega_in) {
+            omega_t_from_kernel<<<grid_for((int64_t)lpad * m, 256, G), 256, 0, st>>>(omega_in, l, lpad, m, ctx->omt,
+                                                                                     ctx->ldo);
+        } else {
+            omega_t_kernel<<<grid_for((int64_t)lpad / 2 * m, 256, G), 256, 0, st>>>(seed, l, lpad, m, ctx->omt, ctx->ldo);
+        }
+        CKL();
+        if (omega_out) {
+            omega_from_t_kernel<<<grid_for((int64_t)l * m, 256, G), 256, 0, st>>>(ctx->omt, ctx->ldo, l, m, omega_out);
+            CKL();
+        }
+        ph_end(ctx);
+        // ---- S1: sketch B = Omega A (canonical split-K over the global n) ----
+        ph_begin(ctx, PH_SKETCH);
+        bool tdone = false;
+        double *bdst = (P == 1) ? ctx->bs[cur] : ctx->gsend;
+        CKT(tma_skinny(ctx, lpad, n_loc, m, ctx->omt, m, lpad, ctx->ldo, 0, 0, A, m, n_loc, lda, 0, 0, bdst, lpad, &tdone,
+                       512, n));
+        if (!tdone) CKT(gemm_skinny(ctx, lpad, n_loc, m, ctx->omt, ctx->ldo, A, lda, bdst, lpad, n));
+        ph_end(ctx);
+        if (P > 1) CKT(gather_sample(n_loc, 0, n, ctx->bs[cur]));
+        sumsq_partial_kernel<<<4 * G, 256, 0, st>>>(ctx->bs[cur], lpad, n, lpad, ctx->sumsq_part);
+        CKL();
+        sumsq_final_kernel<<<1, 32, 0, st>>>(ctx->sumsq_part, 4 * G, ctx->stop_tol2, ctx->iscal + 0);
+        CKL();
+        // Pi = I_n
+        iota_kernel<<<grid_for(n, 256, G), 256, 0, st>>>(jpvt, n);
+        CKL();
+        CK(cudaMemsetAsync(tau, 0, sizeof(double) * k, st));
+        return 0;
+    }
+
+    int run() {
+        CKT(setup());
+        CKT(sample_qrcp(0));
+        for (int64_t i = 0; i < k; i += b) {
+            CKT(panel(i));
+            CKT(trailing_and_sample(i));
+            ++panels;
+        }
+        CKT(join_bulk());
+        return 0;
+    }
+};
+
+// Status words through pinned memory; multi-GPU: poll the communicator while
+// waiting (asynchronous NCCL errors, timeout -> abort).
+static int finish_wait(rqrcp_ctx *ctx, cudaStream_t st) {
+    if (!ctx->tr || ctx->nranks == 1 || !strcmp(ctx->tr->kind(), "loopback")) {
+        CK(cudaStreamSynchronize(st));
+        return 0;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        cudaError_t q = cudaStreamQuery(st);
+        if (q == cudaSuccess) return 0;
+        if (q != cudaErrorNotReady) CK(q);
+        if (ctx->tr->poll(ctx->err)) {
+            ctx->tr->abort();
+            return RQRCP_E_NCCL;
+        }
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (ms > (double)ctx->opt.nccl_timeout_ms) {
+            ctx->err = "multi-GPU factorization exceeded nccl_timeout_ms: communicator aborted";
+            ctx->tr->abort();
+            return RQRCP_E_NCCL;
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(100));
+    }
+}
+
+static void print_traces(rqrcp_ctx *ctx);
+
+static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
+                       uint64_t seed, int64_t *jpvt, double *tau, int64_t *rank_out, const double *omega_in,
+                       double *omega_out, rqrcp_trace *trace, bool keep_last = false, int *final_sample = nullptr) {
+    if (!ctx) return -1;
+    if (!A) return -2;
+    if (lda < std::max<int64_t>(1, m)) return -3;
+    if (m < 1) return -4;
+    if (n < 1) return -5;
+    if (k < 1 || k > std::min(m, n)) return -6;
+    if (b < 1) return -7;
+    if (p < 0 || (int64_t)b + p > m) return -8;
+    if (!jpvt) return -10;
+    if (!tau) return -11;
+    if (!rank_out) return -12;
+    if (m > ctx->max_m || n > ctx->max_n || b > ctx->max_b || p > ctx->max_p) {
+        ctx->err = "problem exceeds the create-time workspace maxima";
+        return RQRCP_E_WORKSPACE;
+    }
+    CK(cudaSetDevice(ctx->device));
+    ctx->launches = 0;
+    ctx->nev = 0;
+    ctx->lt_t0 = ctx->lt_t1 = -1;
+    ctx->rec_phase.clear();
+    ctx->rec_s.clear();
+    ctx->rec_e.clear();
+    ctx->open_phase = -1;
+    if (trace) trace->recorded = 0;
+    Run R{};
+    R.ctx = ctx;
+    R.A = A;
+    R.lda = lda;
+    R.m = m;
+    R.n = n;
+    R.k = k;
+    R.b = b;
+    R.p = p;
+    R.l = b + p;
+    R.lpad = (int)rup(R.l, 8);
+    R.P = ctx->nranks;
+    R.me = ctx->rank;
+    R.G = ctx->num_sms;
+    R.n_loc = dist_count(n, b, R.P, R.me);
+    R.seed = seed;
+    R.jpvt = jpvt;
+    R.tau = tau;
+    R.omega_in = omega_in;
+    R.omega_out = omega_out;
+    R.trace = trace;
+    R.keep_last = keep_last;
+    R.panel_mode = ctx->opt.panel;
+    R.st = ctx->stream;
+    R.status = ctx->iscal + 0;
+    R.bb_eff = ctx->iscal + 1;
+    R.done = ctx->iscal + 2;
+    R.rankd = ctx->iscal + 3;
+    // schedule: the bulk rows of each trailing update overlap the next sample
+    // QRCP when that runs on one cluster (it leaves the other SMs free), else
+    // the next panel QR (look-ahead); serial when asked
+    int sched = ctx->opt.schedule;
+    if (sched < 0) sched = (sq_kind(ctx, R.l, n) == SQK_CLUSTER) ? 1 : 2;
+    R.sched = sched;
+    const int ev_t0 = ctx->nev;
+    cudaEventRecord(ctx->ev[ctx->nev++], ctx->stream);
+    int rc = R.run();
+    if (rc) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamSynchronize(ctx->upd);
+        return rc;
+    }
+    if (final_sample) *final_sample = R.cur;
     int *hs = ctx->hstatus;
-    CK(cudaMemcpyAsync(hs, ctx->iscal, sizeof(int) * 5, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hs, ctx->iscal, sizeof(int) * 5, cudaMemcpyDeviceToHost, ctx->stream));
     const int ev_t1 = ctx->nev;
-    cudaEventRecord(ctx->ev[ctx->nev++], st);
-    CK(cudaStreamSynchronize(st));
-    // timings: the events are read lazily by rqrcp_get_timings (the elapsed-time
-    // queries stay off the caller's critical path between factorizations)
-    rqrcp_timings t{};
+    cudaEventRecord(ctx->ev[ctx->nev++], ctx->stream);
+    rc = finish_wait(ctx, ctx->stream);
+    if (rc) return rc;
     ctx->lt_t0 = ctx->timing ? ev_t0 : -1;
     ctx->lt_t1 = ctx->timing ? ev_t1 : -1;
-    if (ctx->trace) {
-        std::vector<unsigned long long> H((size_t)SQ_MAXG * 64 * 4);
-        cudaMemcpy(H.data(), ctx->trace, sizeof(unsigned long long) * H.size(), cudaMemcpyDeviceToHost);
-        cudaMemset(ctx->trace, 0, sizeof(unsigned long long) * H.size());
-        const char *names[4] = {"wait/poll+winner+householder", "apply", "publish", "->next"};
-        double all[4] = {0}, worst_apply = 0;
-        int ncta = 0, worst = -1;
-        for (int c = 0; c < SQ_MAXG; ++c) {
-            double acc[4] = {0};
-            int cnt = 0;
-            for (int jj = 1; jj < 63; ++jj) {
-                const unsigned long long *r = H.data() + ((size_t)c * 64 + jj) * 4;
-                const unsigned long long *nx = H.data() + ((size_t)c * 64 + jj + 1) * 4;
-                if (!r[0] || !r[3] || !nx[0]) continue;
-                for (int q = 0; q < 3; ++q) acc[q] += (double)(r[q + 1] - r[q]);
-                acc[3] += (double)(nx[0] - r[3]);
-                ++cnt;
-            }
-            if (!cnt) continue;
-            for (int q = 0; q < 4; ++q) acc[q] /= cnt;
-            if (c == 0) {
-                fprintf(stderr, "[rqrcp trace] sample QRCP CTA 0, %d steps, mean cycles:", cnt);
-                for (int q = 0; q < 4; ++q) fprintf(stderr, " %s=%.0f", names[q], acc[q]);
-                fprintf(stderr, "\n");
-            }
-            for (int q = 0; q < 4; ++q) all[q] += acc[q];
-            if (acc[1] + acc[2] > worst_apply) { worst_apply = acc[1] + acc[2]; worst = c; }
-            ++ncta;
-        }
-        if (ncta) {
-            fprintf(stderr, "[rqrcp trace] sample QRCP mean over %d CTAs:", ncta);
-            for (int q = 0; q < 4; ++q) fprintf(stderr, " %s=%.0f", names[q], all[q] / ncta);
-            fprintf(stderr, "; slowest apply+publish: CTA %d (%.0f cycles)\n", worst, worst_apply);
-        }
-        unsigned long long h[2 * 64 * 8];
-        cudaMemcpy(h, ctx->ptrace, sizeof(h), cudaMemcpyDeviceToHost);
-        const char *pn0[5] = {"gram", "barrier", "reduce", "tau+w+x", "update"};
-        const char *pn1[5] = {"gram", "push", "mbar-wait", "sum", "update+publish"};
-        const char **pn = ctx->ptrace_kind ? pn1 : pn0;
-        for (int c = 0; c < 2; ++c) {
-            double acc[5] = {0};
-            int cnt = 0;
-            for (int jj = 1; jj < 63; ++jj) {
-                const unsigned long long *r = h + ((size_t)c * 64 + jj) * 8;
-                if (!r[0] || !r[5]) continue;
-                for (int q = 0; q < 5; ++q) acc[q] += (double)(r[q + 1] - r[q]);
-                ++cnt;
-            }
-            fprintf(stderr, "[rqrcp trace] panel CTA %s, %d steps, mean cycles:", c ? "last" : "0", cnt);
-            for (int q = 0; q < 5; ++q) fprintf(stderr, " %s=%.0f", pn[q], cnt ? acc[q] / cnt : 0.0);
-            if (ctx->ptrace_kind == 1) {  // update+publish split: dlarfg+w | update loop | publish
-                double d6 = 0, d7 = 0, d5 = 0;
-                for (int jj = 1; jj < 63; ++jj) {
-                    const unsigned long long *r = h + ((size_t)c * 64 + jj) * 8;
-                    if (!r[0] || !r[5]) continue;
-                    d6 += (double)(r[6] - r[4]);
-                    d7 += (double)(r[7] - r[6]);
-                    d5 += (double)(r[5] - r[7]);
-                }
-                if (cnt) fprintf(stderr, " [dlarfg+w=%.0f loop=%.0f publish=%.0f]", d6 / cnt, d7 / cnt, d5 / cnt);
-            }
-            fprintf(stderr, "\n");
-        }
-    }
-    t.panels = panels;
+    if (ctx->trace) print_traces(ctx);
+    rqrcp_timings t{};
+    t.panels = R.panels;
     t.panels_householder = hs[4];
     t.kernel_launches = ctx->launches;
     ctx->last = t;
+    if (trace) trace->recorded = std::max<int64_t>(0, std::min<int64_t>(trace->npanels, R.panels - trace->first_panel));
     *rank_out = hs[3];
     if (hs[0] == 4) {
         ctx->err = "non-finite values in the sample (A contains NaN/Inf)";
@@ -1558,6 +1666,56 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     return 0;
 }
 
+// RQRCP_TRACE=1: per-step clock64 phase traces of the latency-bound kernels
+static void print_traces(rqrcp_ctx *ctx) {
+    std::vector<unsigned long long> H((size_t)SQ_MAXG * 64 * 4);
+    cudaMemcpy(H.data(), ctx->trace, sizeof(unsigned long long) * H.size(), cudaMemcpyDeviceToHost);
+    cudaMemset(ctx->trace, 0, sizeof(unsigned long long) * H.size());
+    const char *names[4] = {"wait/poll+winner+householder", "apply", "publish", "->next"};
+    double all[4] = {0}, worst_apply = 0;
+    int ncta = 0, worst = -1;
+    for (int c = 0; c < SQ_MAXG; ++c) {
+        double acc[4] = {0};
+        int cnt = 0;
+        for (int jj = 1; jj < 63; ++jj) {
+            const unsigned long long *r = H.data() + ((size_t)c * 64 + jj) * 4;
+            const unsigned long long *nx = H.data() + ((size_t)c * 64 + jj + 1) * 4;
+            if (!r[0] || !r[3] || !nx[0]) continue;
+            for (int q = 0; q < 3; ++q) acc[q] += (double)(r[q + 1] - r[q]);
+            acc[3] += (double)(nx[0] - r[3]);
+            ++cnt;
+        }
+        if (!cnt) continue;
+        for (int q = 0; q < 4; ++q) acc[q] /= cnt;
+        for (int q = 0; q < 4; ++q) all[q] += acc[q];
+        if (acc[1] + acc[2] > worst_apply) { worst_apply = acc[1] + acc[2]; worst = c; }
+        ++ncta;
+    }
+    if (ncta) {
+        fprintf(stderr, "[rqrcp trace] sample QRCP mean over %d CTAs:", ncta);
+        for (int q = 0; q < 4; ++q) fprintf(stderr, " %s=%.0f", names[q], all[q] / ncta);
+        fprintf(stderr, "; slowest apply+publish: CTA %d (%.0f cycles)\n", worst, worst_apply);
+    }
+    unsigned long long h[2 * 64 * 8];
+    cudaMemcpy(h, ctx->ptrace, sizeof(h), cudaMemcpyDeviceToHost);
+    const char *pn0[5] = {"gram", "barrier", "reduce", "tau+w+x", "update"};
+    const char *pn1[5] = {"gram", "push", "mbar-wait", "sum", "update+publish"};
+    const char **pn = ctx->ptrace_kind ? pn1 : pn0;
+    for (int c = 0; c < 2; ++c) {
+        double acc[5] = {0};
+        int cnt = 0;
+        for (int jj = 1; jj < 63; ++jj) {
+            const unsigned long long *r = h + ((size_t)c * 64 + jj) * 8;
+            if (!r[0] || !r[5]) continue;
+            for (int q = 0; q < 5; ++q) acc[q] += (double)(r[q + 1] - r[q]);
+            ++cnt;
+        }
+        fprintf(stderr, "[rqrcp trace] panel CTA %s, %d steps, mean cycles:", c ? "last" : "0", cnt);
+        for (int q = 0; q < 5; ++q) fprintf(stderr, " %s=%.0f", pn[q], cnt ? acc[q] / cnt : 0.0);
+        fprintf(stderr, "\n");
+    }
+}
+
 extern "C" int rqrcp_factor(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
                             uint64_t seed, int64_t *jpvt, double *tau, int64_t *rank_out) {
     return factor_impl(ctx, A, lda, m, n, k, b, p, seed, jpvt, tau, rank_out, nullptr, nullptr, nullptr);
@@ -1565,8 +1723,9 @@ extern "C" int rqrcp_factor(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, i
 
 extern "C" int rqrcp_factor_ex(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
                                uint64_t seed, int64_t *jpvt, double *tau, int64_t *rank_out, const double *omega_in,
-                               double *omega_out, double *gaps_out) {
-    return factor_impl(ctx, A, lda, m, n, k, b, p, seed, jpvt, tau, rank_out, omega_in, omega_out, gaps_out);
+                               double *omega_out, rqrcp_trace *trace) {
+    if (trace && (trace->first_panel < 0 || trace->npanels < 0)) return -15;
+    return factor_impl(ctx, A, lda, m, n, k, b, p, seed, jpvt, tau, rank_out, omega_in, omega_out, trace);
 }
 
 extern "C" int rqrcp_srqr_verify(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b,
@@ -1614,8 +1773,8 @@ extern "C" int rqrcp_srqr_verify(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t
         ctx->err = "SRQR verification: k too large for the shared-memory solve";
         return RQRCP_E_WORKSPACE;
     }
-    CK(cudaFuncSetAttribute(srqr_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
-    double *Y = ctx->splitk;  // (k+1) x d <= 4 M doubles
+    CK(smem_attr((const void *)srqr_solve_kernel, (int)ssm, ctx->device));
+    double *Y = ctx->splitk;  // (k+1) x d
     if ((k + 1) * (int64_t)d > ctx->splitk_elems) {
         ctx->err = "SRQR verification: workspace";
         return RQRCP_E_WORKSPACE;
@@ -1649,7 +1808,7 @@ extern "C" int rqrcp_form_q1(rqrcp_ctx *ctx, const double *A, int64_t lda, int64
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream;
     const int G = ctx->num_sms;
-    int rc = 0;
+    double *vfull = ctx->vfull_b[0], *vt = ctx->vt_b[0];
     lr_eye_kernel<<<grid_for(m * k, 256, G), 256, 0, st>>>(Q1, ldq, m, k);
     CKL();
     int *bbd = ctx->iscal + 6;
@@ -1659,11 +1818,10 @@ extern "C" int rqrcp_form_q1(rqrcp_ctx *ctx, const double *A, int64_t lda, int64
         const int bb = (int)std::min<int64_t>(b, k - i);
         const int bbpad = (int)rup(bb, 8);
         const int64_t mp = m - i, ncols = k - i;
-        lr_extract_v_kernel<<<grid_for(mp * bbpad, 256, G), 256, 0, st>>>(A + i + i * lda, lda, mp, bb, bbpad,
-                                                                          ctx->vfull, ctx->ldo, ctx->vt);
+        lr_extract_v_kernel<<<grid_for(mp * bbpad, 256, G), 256, 0, st>>>(A + i + i * lda, lda, mp, bb, bbpad, vfull,
+                                                                          ctx->ldo, vt);
         CKL();
-        rc = gemm_skinny(ctx, bbpad, bbpad, mp, ctx->vfull, ctx->ldo, ctx->vfull, ctx->ldo, ctx->ybuf, bbpad);
-        if (rc) return rc;
+        CKT(gemm_skinny(ctx, bbpad, bbpad, mp, vfull, ctx->ldo, vfull, ctx->ldo, ctx->ybuf, bbpad));
         lr_set_int_kernel<<<1, 1, 0, st>>>(bbd, bb);
         CKL();
         int nb = 8;
@@ -1676,12 +1834,9 @@ extern "C" int rqrcp_form_q1(rqrcp_ctx *ctx, const double *A, int64_t lda, int64
         CKL();
         double *X = Q1 + i + i * ldq;
         // X <- (I - V T V^T) X:  W = V^T X,  W2 = -T W,  X += V W2
-        rc = gemm_skinny(ctx, bbpad, ncols, mp, ctx->vfull, ctx->ldo, X, ldq, ctx->w, bbpad);
-        if (rc) return rc;
-        rc = gemm_skinny(ctx, bbpad, ncols, bbpad, ctx->omhat, bbpad, ctx->w, bbpad, ctx->w2, bbpad);
-        if (rc) return rc;
-        rc = gemm_update(ctx, mp, ncols, bbpad, ctx->w2, bbpad, ctx->vt, bbpad, X, ldq);
-        if (rc) return rc;
+        CKT(gemm_skinny(ctx, bbpad, ncols, mp, vfull, ctx->ldo, X, ldq, ctx->w, bbpad));
+        CKT(gemm_skinny(ctx, bbpad, ncols, bbpad, ctx->omhat, bbpad, ctx->w, bbpad, ctx->w2, bbpad));
+        CKT(gemm_update(ctx, mp, ncols, bbpad, ctx->w2, bbpad, vt, bbpad, X, ldq));
     }
     CK(cudaStreamSynchronize(st));
     return 0;

@@ -1,28 +1,38 @@
-"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
-times (default context, grid kernels), on outputs the oracle can compute:
+"""Parity at BASELINE.json's full sizes (C3, C4, C5), in the launch
+configuration bench.py times (default context and schedule), against the CPU
+oracle:
 
-* prefix: the oracle run to k' = 2b (two panels) must give exactly the first k'
-  pivots and the same |diag R| rows as the GPU run to the full k (the prefix
-  property, pinned for the oracle in test_oracle_pins.py::test_prefix_property;
-  Omega does not depend on k);
-* probes (properties that hold at any size): with R = [R11 R12; 0 R22] from
-  the factored matrix, ||A Pi x - Q (R x)|| / (||A||_F ||x||) <= 1e-13 and
-  ||Q^T Q x - x|| / ||x|| <= 1e-13 for Gaussian x (SURVEY.md §8(c) C4/C5 plan);
-* jpvt is a permutation; the achieved rank is k.
+* C3 (16384^2, k = 1024): the FULL oracle run -- identical pivots, |diag R|,
+  [R11 R12], tau and V element by element, residuals (as test_gpu_parity), and
+  the per-panel trace of all 16 panels (R-hat after S2, the Eq. (4) sample
+  after S6) against the oracle's panel callback;
+* C4 (32768^2, k = 8192) and C5 (65536^2, k = 4096): the PREFIX oracle to
+  k' = 4 panels (C4) / 2 panels (C5) (the prefix property, pinned for the
+  oracle in test_oracle_pins.py::test_prefix_property: the first k' pivots
+  and R rows do not depend on k): identical first k' pivots, R rows 0..k'-1
+  element-wise matched by column id (later swaps only permute columns),
+  tau / V of the first k' columns, and the per-panel trace of those panels;
+* at any size, probes: with R = [R11 R12; 0 R22] from the factored matrix,
+  ||A Pi x - Q (R x)|| / (||A||_F ||x||) <= 1e-13 and ||Q^T Q x - x|| / ||x||
+  <= 1e-13 for Gaussian x (SURVEY.md §8(c) C4/C5 plan).
 """
+import os
+
 import numpy as np
 import pytest
 import torch
 
 import inputs
 import oracle
+from gpu_helpers import check_trace_panels
 
 pytestmark = pytest.mark.gpu
+
+ELEM_RTOL = 1e-10
 
 
 def _apply_q(F, tau, X, transpose=False):
     """Q X (or Q^T X), Q = H_0 ... H_{k-1}, reflectors from the factored matrix."""
-    m = F.shape[0]
     k = len(tau)
     Y = X.copy()
     order = range(k) if transpose else range(k - 1, -1, -1)
@@ -36,14 +46,18 @@ def _apply_q(F, tau, X, transpose=False):
     return Y
 
 
-def _run(name, kprefix_panels=2, nprobe=4):
+def _run(name, prefix_panels=None, nprobe=4):
     import paper_1804_05138_b200 as rq
     c = inputs.CONFIGS[name]
     m, n, k, b, p, seed = c["m"], c["n"], c["k"], c["b"], c["p"], c["seed"]
+    npan_all = (k + b - 1) // b
+    npan = npan_all if prefix_panels is None else min(npan_all, prefix_panels)
+    kp = min(k, npan * b)
     Ad = inputs.config_matrix(name, device="cuda")
     A = Ad.cpu().numpy()  # host copy of the input (not from the CUDA path)
     ctx = rq.RQRCP(max_m=m, max_n=n, max_b=b, max_p=p)
-    jpvt, tau, rank = ctx.factor(Ad, k, b, p, seed=seed)
+    tr = ctx.make_trace(n, b, p, 0, npan)
+    jpvt, tau, rank = ctx.factor(Ad, k, b, p, seed=seed, trace=tr)
     torch.cuda.synchronize()
     ctx.close()
     F = Ad.cpu().numpy()
@@ -53,29 +67,49 @@ def _run(name, kprefix_panels=2, nprobe=4):
     torch.cuda.empty_cache()
     assert rank == k
     assert np.array_equal(np.sort(jp), np.arange(n))
-    # ---- prefix oracle ----
-    kp = min(k, kprefix_panels * b)
-    o = oracle.rqrcp(A, kp, b, p, seed=seed)
-    assert np.array_equal(jp[:kp], o["jpvt"][:kp]), "prefix pivots differ"
-    dg = np.abs(np.diag(F)[:kp])
-    do = np.abs(np.diag(o["A"])[:kp])
-    assert np.max(np.abs(dg - do) / do) <= 1e-10
-    # ---- probes ----
+    # ---- probes (any size) ----
     rng = np.random.default_rng(7)
     X = rng.standard_normal((n, nprobe))
-    R = np.triu(F[:k, :])  # top k rows: [R11 R12]
+    R = np.triu(F[:k, :])
     RX = np.zeros((m, nprobe))
     RX[:k] = R @ X
-    RX[k:] = (F[:, k:] @ X[k:])[k:]  # R22 block (trailing by-product); no strided copy
+    RX[k:] = (F[:, k:] @ X[k:])[k:]
+    del R
     Xp = np.zeros_like(X)
-    Xp[jp] = X  # A Pi X = A (Pi X) without materialising A Pi
+    Xp[jp] = X
     lhs = A @ Xp
     err = np.linalg.norm(lhs - _apply_q(F, ta, RX)) / (np.linalg.norm(A) * np.linalg.norm(X))
     assert err <= 1e-13, err
     Y = rng.standard_normal((m, nprobe))
     err2 = np.linalg.norm(_apply_q(F, ta, _apply_q(F, ta, Y, transpose=True)) - Y) / np.linalg.norm(Y)
     assert err2 <= 1e-13, err2
-    return np.linalg.norm(F[k:, k:]) / np.linalg.norm(A)
+    r22 = np.linalg.norm(F[k:, k:]) / np.linalg.norm(A)
+    # ---- oracle (full or prefix) ----
+    panels = []
+    o = oracle.rqrcp(A, kp, b, p, seed=seed, invariant=True,
+                     callback=lambda i, bb, l_, mp, np_, Rh, Bn, Oc, On, Af: panels.append((i, bb, Rh, Bn)))
+    del A
+    assert np.array_equal(jp[:kp], o["jpvt"][:kp]), "pivots differ"
+    Fo = o["A"]
+    dg = np.abs(np.diag(F)[:kp])
+    do = np.abs(np.diag(Fo)[:kp])
+    assert np.max(np.abs(dg - do) / do) <= 1e-10
+    # R rows 0..kp-1 matched by original column id (later panels only permute columns)
+    pos_g = np.empty(n, dtype=np.int64)
+    pos_g[jp] = np.arange(n)
+    pos_o = np.empty(n, dtype=np.int64)
+    pos_o[o["jpvt"]] = np.arange(n)
+    Rg = np.triu(F[:kp, :])[:, pos_g]
+    Ro = np.triu(Fo[:kp, :])[:, pos_o]
+    assert np.max(np.abs(Rg - Ro)) <= ELEM_RTOL * np.max(np.abs(Ro)), "R rows differ"
+    del Rg, Ro
+    assert np.max(np.abs(ta[:kp] - o["tau"][:kp])) <= ELEM_RTOL
+    Vg = np.tril(F[:, :kp], -1)
+    Vo = np.tril(Fo[:, :kp], -1)
+    assert np.max(np.abs(Vg - Vo)) <= ELEM_RTOL
+    del Vg, Vo, F, Fo
+    check_trace_panels(tr, panels, o["jpvt"])
+    return r22
 
 
 def test_C3_full_size():
@@ -84,11 +118,10 @@ def test_C3_full_size():
 
 
 def test_C4_full_size():
-    r = _run("C4", kprefix_panels=1)
+    r = _run("C4", prefix_panels=int(os.environ.get("RQRCP_TEST_C4_PANELS", "4")))
     assert 0.0 < r < 0.1
 
 
-@pytest.mark.slow
 def test_C5_full_size():
-    r = _run("C5", kprefix_panels=1, nprobe=2)
+    r = _run("C5", prefix_panels=int(os.environ.get("RQRCP_TEST_C5_PANELS", "2")), nprobe=2)
     assert 0.0 < r < 1.0

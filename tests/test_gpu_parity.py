@@ -2,30 +2,57 @@
 
 Acceptance (BASELINE.json north_star): identical pivot sequences; |diag R|
 within 1e-10 relative; ||A Pi - Q1 [R11 R12]||_F/||A||_F (and ||R22||_F/||A||_F)
-within 1e-12 of the oracle's.  Inputs are seeded synthetic matrices from
-inputs/ with the recipes of BASELINE.json's configs, at sizes the oracle
-finishes in seconds (several GEMM / sample-QRCP / panel tiles and ragged tails).
+within 1e-12 of the oracle's.  On top of that every case compares, ELEMENT BY
+ELEMENT (both sides use the dlarfg convention of reading R-G7, so no sign
+fixing): [R11 R12] to 1e-10 max|R|, tau to 1e-10, the Householder vectors V
+to 1e-10, and the full reconstruction A Pi = Q [R11 R12; 0 R22] to 1e-13.
+Tolerances: the two sides sum in different orders, so entries differ by
+O(kappa eps ||R||) (<= 1e-15 on these inputs); 1e-10 sits
+five orders above that and five below an R12 that is wrong by 1e-6 relative.
+Inputs are seeded synthetic matrices from inputs/ with the recipes of
+BASELINE.json's configs, at sizes the oracle finishes in seconds (several
+GEMM / sample-QRCP / panel tiles and ragged tails).
 """
+import contextlib
+
 import numpy as np
 import pytest
 import torch
 
 import inputs
 import oracle
+from gpu_helpers import check_trace_panels
 
 pytestmark = pytest.mark.gpu
 
 DIAG_RTOL = 1e-10
 RES_ATOL = 1e-12
+ELEM_RTOL = 1e-10
+RECON_TOL = 1e-13
+
+DEFAULT_OPTS = dict(schedule=-1, panel=0, pn_cluster=1, pn_cpt=2, pn_grid=0, pn_rows=128, la_panel_ctas=48,
+                    sq_cluster=1, sq_reg=1, sq_grid=0, sq_nsm=-1, sq_hstride=8, sq_poll=1)
 
 
 @pytest.fixture(scope="module")
 def ctx():
-    """Default context: grid-wide (cooperative) sample-QRCP / panel kernels."""
     import paper_1804_05138_b200 as rq
     c = rq.RQRCP(max_m=5000, max_n=5000, max_b=128, max_p=32)
     yield c
     c.close()
+
+
+@contextlib.contextmanager
+def options(ctx, **kv):
+    """Launch-path options for the duration of a block (create-time config of
+    the context; restored to the defaults afterwards)."""
+    for k, v in kv.items():
+        ctx.set_option(k, v)
+    try:
+        yield
+    finally:
+        for k in kv:
+            ctx.set_option(k, DEFAULT_OPTS[k])
 
 
 def to_dev(A):
@@ -46,6 +73,31 @@ def full_R(F, k):
     return R
 
 
+def reflectors(F, k):
+    """V (m x k): unit lower trapezoidal Householder vectors of the factored matrix."""
+    m = F.shape[0]
+    V = np.zeros((m, k))
+    for j in range(k):
+        V[j, j] = 1.0
+        V[j + 1:, j] = F[j + 1:, j]
+    return V
+
+
+def q_apply(F, tau, C):
+    """Q C with Q = H_1 ... H_k from the LAPACK-layout reflectors of F,
+    by LAPACK dormqr (a library routine; the same layout as dgeqrf's)."""
+    from scipy.linalg import lapack
+    k = len(tau)
+    if k == 0:
+        return np.array(C, dtype=np.float64)
+    a = np.asfortranarray(F[:, :k])
+    c = np.asfortranarray(C, dtype=np.float64)
+    lw = lapack.dormqr("L", "N", a, tau, c, -1)[1]
+    out, _, info = lapack.dormqr("L", "N", a, tau, c, int(lw[0]) if np.ndim(lw) else int(lw), overwrite_c=0)
+    assert info == 0
+    return out
+
+
 def trunc_residual(A, res, k, probes=None):
     """||A Pi - Q1 [R11 R12]||_F / ||A||_F (exact when probes is None)."""
     Api = A[:, res["jpvt"]]
@@ -53,28 +105,46 @@ def trunc_residual(A, res, k, probes=None):
     Rfull = np.zeros_like(res["A"])
     Rfull[:k] = Rt
     if probes is None:
-        return np.linalg.norm(Api - oracle.apply_q(res["A"], res["tau"][:k], Rfull)) / np.linalg.norm(A)
+        return np.linalg.norm(Api - q_apply(res["A"], res["tau"][:k], Rfull)) / np.linalg.norm(A)
     X = probes
-    return (np.linalg.norm(Api @ X - oracle.apply_q(res["A"], res["tau"][:k], Rfull @ X))
-            / np.linalg.norm(A @ X))
+    return np.linalg.norm(Api @ X - q_apply(res["A"], res["tau"][:k], Rfull @ X)) / np.linalg.norm(A @ X)
 
 
-def compare(A, g, o, k, probes=None):
-    assert g["rank"] == o["rank"] == k
+def reconstruction_error(A, res, k):
+    """||A Pi - Q [R11 R12; 0 R22]||_F / ||A||_F from the GPU's own outputs."""
+    R = full_R(res["A"], k)
+    return np.linalg.norm(A[:, res["jpvt"]] - q_apply(res["A"], res["tau"][:k], R)) / np.linalg.norm(A)
+
+
+def compare(A, g, o, k, probes=None, rank=None):
+    k_eff = k if rank is None else rank
+    assert g["rank"] == o["rank"] == k_eff
     # identical pivot sequences (the whole permutation: same transpositions)
     if not np.array_equal(g["jpvt"], o["jpvt"]):
         bad = int(np.nonzero(g["jpvt"] != o["jpvt"])[0][0])
         pytest.fail(f"pivots differ first at {bad}; oracle gap there {o['gaps'][min(bad, k - 1)]:.3e}")
-    dg = np.abs(np.diag(g["A"])[:k])
-    do = np.abs(np.diag(o["A"])[:k])
-    assert np.max(np.abs(dg - do) / do) <= DIAG_RTOL
+    kk = k_eff
+    dg = np.abs(np.diag(g["A"])[:kk])
+    do = np.abs(np.diag(o["A"])[:kk])
+    assert np.max(np.abs(dg - do) / do, initial=0.0) <= DIAG_RTOL
+    # element-wise [R11 R12], tau, V (reading R-G7: same convention on both sides)
+    Rg, Ro = np.triu(g["A"][:kk, :]), np.triu(o["A"][:kk, :])
+    rmax = np.max(np.abs(Ro), initial=1.0)
+    assert np.max(np.abs(Rg - Ro), initial=0.0) <= ELEM_RTOL * rmax, "R11/R12 differ element-wise"
+    assert np.max(np.abs(g["tau"][:kk] - o["tau"][:kk]), initial=0.0) <= ELEM_RTOL, "tau differs"
+    Vg, Vo = reflectors(g["A"], kk), reflectors(o["A"], kk)
+    assert np.max(np.abs(Vg - Vo), initial=0.0) <= ELEM_RTOL * max(1.0, np.max(np.abs(Vo), initial=0.0)), "V differs"
+    if kk < k:
+        assert np.all(g["tau"][kk:k] == 0.0)
     nA = np.linalg.norm(A)
-    r22g = np.linalg.norm(full_R(g["A"], k)[k:, k:]) / nA
-    r22o = np.linalg.norm(full_R(o["A"], k)[k:, k:]) / nA
+    r22g = np.linalg.norm(full_R(g["A"], kk)[kk:, kk:]) / nA
+    r22o = np.linalg.norm(full_R(o["A"], kk)[kk:, kk:]) / nA
     assert abs(r22g - r22o) <= RES_ATOL
-    rg = trunc_residual(A, g, k, probes)
-    ro = trunc_residual(A, o, k, probes)
+    rg = trunc_residual(A, g, kk, probes)
+    ro = trunc_residual(A, o, kk, probes)
     assert abs(rg - ro) <= RES_ATOL
+    if probes is None:
+        assert reconstruction_error(A, g, kk) <= RECON_TOL
     return rg
 
 
@@ -101,13 +171,72 @@ def test_factor_parity(ctx, name, kind, m, n, k, b, p, seed):
 
 
 def test_C2_full_size(ctx):
-    """configs[1] (the bench workload) at its full size: 4096^2, k=512, b=64, p=10."""
+    """configs[1] at its full size: 4096^2, k=512, b=64, p=10, element-wise."""
     c = inputs.CONFIGS["C2"]
     A = inputs.config_matrix("C2").numpy()
     o = oracle.rqrcp(A, c["k"], c["b"], c["p"], seed=c["seed"])
     g = gpu_factor(ctx, A, c["k"], c["b"], c["p"], c["seed"])
-    X = np.random.default_rng(0).standard_normal((c["n"], 8))
-    compare(A, g, o, c["k"], probes=X)
+    compare(A, g, o, c["k"])
+
+
+# ---- the per-panel trace (rqrcp_factor_ex, SURVEY.md §8(b)) against the
+#      oracle's panel callback: pivots, R-hat after S2 (P:172-179) and the
+#      updated sample after S6 (Eq. (4), P:206-221) element by element ------
+def trace_compare(ctx, A, k, b, p, seed, update_rule=1, opts=None):
+    m, n = A.shape
+    l = b + p
+    npan = (k + b - 1) // b
+    tr = ctx.make_trace(n, b, p, 0, npan)
+    Ad = to_dev(A)
+    if update_rule == 2:
+        ctx.set_update_rule(2)
+    try:
+        with options(ctx, **(opts or {})):
+            jpvt, tau, rank = ctx.factor(Ad, k, b, p, seed=seed, trace=tr)
+    finally:
+        ctx.set_update_rule(1)
+    torch.cuda.synchronize()
+    assert tr.recorded == npan
+    panels = []
+    o = oracle.rqrcp(A, k, b, p, seed=seed, update_rule=update_rule,
+                     callback=lambda i, bb, l_, mp, np_, Rh, Bn, Oc, On, Af: panels.append((i, bb, Rh, Bn)))
+    assert len(panels) == npan
+    jp = jpvt.cpu().numpy()
+    assert np.array_equal(jp, o["jpvt"])
+    check_trace_panels(tr, panels, o["jpvt"])
+    return panels
+
+
+TRACE_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "lowrank", "b128", "odd")]
+
+
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", TRACE_CASES, ids=[c[0] for c in TRACE_CASES])
+def test_trace_per_panel(ctx, name, kind, m, n, k, b, p, seed):
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    trace_compare(ctx, A, k, b, p, seed)
+
+
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", TRACE_CASES[:4], ids=[c[0] for c in TRACE_CASES[:4]])
+def test_trace_per_panel_eq5(ctx, name, kind, m, n, k, b, p, seed):
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    trace_compare(ctx, A, k, b, p, seed, update_rule=2)
+
+
+def test_trace_window_and_C2(ctx):
+    """A recording window (panels 2..4 of C2 at full size)."""
+    c = inputs.CONFIGS["C2"]
+    A = inputs.config_matrix("C2").numpy()
+    m, n, k, b, p = c["m"], c["n"], c["k"], c["b"], c["p"]
+    tr = ctx.make_trace(n, b, p, 2, 3)
+    Ad = to_dev(A)
+    ctx.factor(Ad, k, b, p, seed=c["seed"], trace=tr)
+    torch.cuda.synchronize()
+    assert tr.recorded == 3
+    panels = []
+    o = oracle.rqrcp(A, 5 * b, b, p, seed=c["seed"], invariant=True,
+                     callback=lambda i, bb, l_, mp, np_, Rh, Bn, Oc, On, Af: panels.append((i, bb, Rh, Bn)))
+    # the window records panels 2..4 (trace slots 0..2)
+    check_trace_panels(tr, panels, o["jpvt"], first=2, last=5)
 
 
 def test_philox_words_bitwise(ctx):
@@ -153,6 +282,22 @@ def test_deterministic(ctx):
     assert np.array_equal(g1["A"], g2["A"]) and np.array_equal(g1["jpvt"], g2["jpvt"])
 
 
+def test_duplicate_columns_tie_rule(ctx):
+    """Exact ties of the squared sample norms go to the LOWEST current position
+    (reading R-G5): every column appears twice, so each first pick is a
+    bitwise tie between two identical sample columns."""
+    rng = np.random.default_rng(8)
+    X = rng.standard_normal((300, 60)) * np.exp(-np.arange(60) / 10.0)
+    A = np.repeat(X, 2, axis=1)  # columns 2c and 2c+1 identical
+    o = oracle.rqrcp(A, 32, 8, 4, seed=9, check=False)
+    g = gpu_factor(ctx, A, 32, 8, 4, 9)
+    assert g["rank"] == o["rank"]
+    r = o["rank"]
+    assert np.array_equal(g["jpvt"][:r], o["jpvt"][:r])
+    # the first pivot is the even (lower) member of its identical pair
+    assert o["jpvt"][0] % 2 == 0
+
+
 def test_rank_deficient(ctx):
     rng = np.random.default_rng(42)
     A = rng.standard_normal((120, 25)) @ rng.standard_normal((25, 100))
@@ -161,6 +306,34 @@ def test_rank_deficient(ctx):
     assert g["rank"] == o["rank"] == 25
     assert np.array_equal(g["jpvt"], o["jpvt"])
     assert np.all(g["tau"][25:] == 0.0)
+
+
+def r11_stop_problem():
+    """A panel whose R11 diagonal collapses while its sample norms stay large:
+    column 5 of A is 1e-15 e_5 but Omega amplifies row 5 by 1e17, so the sample
+    QRCP picks it second (its sample norm ~ 270 vs ~ 600 for the 200-scaled
+    column 0 and ~ 3 for the rest); |R(1,1)| = 1e-15 <
+    1e3 eps ||panel||_F (reading R-G12b) stops the factorization at rank 1."""
+    m, n, b, p = 40, 30, 8, 2
+    A = np.zeros((m, n))
+    for j in range(n):
+        A[j, j] = 1.0
+    A[5, 5] = 1e-15
+    A[:, 0] *= 200.0
+    Om = np.random.default_rng(11).standard_normal((b + p, m))
+    Om[:, 5] *= 1e17
+    return A, Om, b, p
+
+
+def test_r11_diagonal_rank_stop(ctx):
+    A, Om, b, p = r11_stop_problem()
+    o = oracle.rqrcp(A, 16, b, p, omega=Om, check=False)
+    assert o["rank"] == 1 and o["jpvt"][1] == 5
+    g = gpu_factor(ctx, A, 16, b, p, 0, omega=torch.tensor(Om.ravel(order="F")).cuda())
+    assert g["rank"] == 1
+    assert np.array_equal(g["jpvt"][:2], o["jpvt"][:2])
+    assert np.all(g["tau"][1:] == 0.0)
+    assert abs(abs(g["A"][0, 0]) - abs(o["A"][0, 0])) <= 1e-12 * abs(o["A"][0, 0])
 
 
 def test_zero_matrix(ctx):
@@ -201,6 +374,19 @@ def test_argument_errors(ctx):
     assert call(h, A.data_ptr(), 10, 10, 8, 4, 2, 2, 0, jp.data_ptr(), ta.data_ptr(), None) == -12
     big = L.rqrcp_factor(h, A.data_ptr(), 6000, 6000, 8, 4, 2, 2, 0, jp.data_ptr(), ta.data_ptr(), ctypes.byref(r))
     assert big == rq.RQRCP_E_WORKSPACE
+    assert L.rqrcp_set_option(h, b"no_such_option", 1) == -2
+    assert L.rqrcp_set_option(h, b"schedule", 7) == -3
+
+
+def test_binding_validation(ctx):
+    """The binding rejects overlapping views and wrong output vectors."""
+    A = torch.zeros(64, 48, dtype=torch.float64, device="cuda").t().contiguous().t()
+    with pytest.raises(ValueError):
+        ctx.factor(A[:, :1].expand(64, 8), 4, 2, 2)
+    with pytest.raises(TypeError):
+        ctx.factor(A, 4, 2, 2, jpvt=torch.zeros(48, dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError):
+        ctx.factor(A, 4, 2, 2, tau=torch.zeros(2, dtype=torch.float64, device="cuda"))
 
 
 def test_factor_host_equals_device(ctx):
@@ -214,36 +400,24 @@ def test_factor_host_equals_device(ctx):
 
 
 # ---- launch-shape variants of the sample QRCP (threads per column, spill) ----
-# RQRCP_SQ_GRID caps the cooperative grid (fewer CTAs -> more columns per CTA,
-# fewer threads per column) and RQRCP_SQ_NSM caps the columns a CTA keeps in
-# shared memory (the rest go through the transposed L2 spill buffer).
-SQ_VARIANTS = [("148", None), ("2", "0"), ("7", "5"), ("33", None), ("1", "40")]
+# sq_grid caps the cooperative grid (fewer CTAs -> more columns per CTA, fewer
+# threads per column) and sq_nsm caps the columns a CTA keeps in shared memory
+# (the rest go through the transposed L2 spill buffer).
+SQ_VARIANTS = [(148, -1), (2, 0), (7, 5), (33, -1), (1, 40)]
 SQ_CASES = [c for c in CASES if c[0] in ("ragged", "odd", "b128", "b1p0", "lowrank")]
 
 
 @pytest.mark.parametrize("grid,nsm", SQ_VARIANTS, ids=[f"g{g}-nsm{n}" for g, n in SQ_VARIANTS])
 @pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", SQ_CASES, ids=[c[0] for c in SQ_CASES])
 def test_sample_qrcp_launch_variants(ctx, grid, nsm, name, kind, m, n, k, b, p, seed):
-    import os
     A = inputs.make(kind, m, n, seed, rank=64).numpy()
     o = oracle.rqrcp(A, k, b, p, seed=seed)
-    os.environ["RQRCP_SQ_GRID"] = grid
-    os.environ["RQRCP_SQ_CLUSTER"] = "0"
-    os.environ["RQRCP_SQ_REG"] = "0"
-    if nsm is not None:
-        os.environ["RQRCP_SQ_NSM"] = nsm
-    try:
+    with options(ctx, sq_grid=grid, sq_cluster=0, sq_reg=0, sq_nsm=nsm):
         g = gpu_factor(ctx, A, k, b, p, seed)
-    finally:
-        for v in ("RQRCP_SQ_GRID", "RQRCP_SQ_NSM", "RQRCP_SQ_CLUSTER", "RQRCP_SQ_REG"):
-            os.environ.pop(v, None)
     compare(A, g, o, k)
 
 
 # ---- the register-resident grid sample QRCP (sample_qrcp_reg.cuh) ----------
-# RQRCP_SQ_CLUSTER=0 takes the one-cluster kernel out, so every sample with
-# l in {40, 74, 144} runs on the grid of 1 + ceil(n'/256) CTAs; the wide cases
-# span several column CTAs with a ragged last one.
 REG_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "lowrank", "kfull", "b128")] + [
     ("reg_wide74", "iid", 800, 1900, 192, 64, 10, 21),
     ("reg_wide144", "graded", 900, 2100, 256, 128, 16, 22),
@@ -253,98 +427,79 @@ REG_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "lowrank", "kf
 
 @pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", REG_CASES, ids=[c[0] for c in REG_CASES])
 def test_sample_qrcp_register_grid(ctx, name, kind, m, n, k, b, p, seed):
-    import os
     A = inputs.make(kind, m, n, seed, rank=64).numpy()
     o = oracle.rqrcp(A, k, b, p, seed=seed)
-    os.environ["RQRCP_SQ_CLUSTER"] = "0"
-    try:
+    with options(ctx, sq_cluster=0):
         g = gpu_factor(ctx, A, k, b, p, seed)
-    finally:
-        os.environ.pop("RQRCP_SQ_CLUSTER", None)
     compare(A, g, o, k)
 
 
-# ---- panel kernels: the register-resident cluster kernel (panel_cl.cuh) is the
-# default when bb <= 64 and m' fits one cluster (256 rows per CTA at bb <= 64,
-# 512 at bb <= 32, <= 16 CTAs); RQRCP_PN_CLUSTER=0 forces the cooperative grid
-# kernel (panel.cuh) everywhere.  Both are checked against the oracle.
+# ---- panel kernels: the register-resident cluster kernel (panel_cl.cuh) and
+# the cooperative grid kernel (panel.cuh); pn_rows = 8 forces the grid
+# kernel's rows-beyond-shared-memory (L2) path at an oracle-feasible size.
 PN_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "wide", "odd", "kfull", "b1p0")] + [
-    ("pncl_tall32", "iid", 5000, 300, 96, 32, 8, 24),   # 10 CTAs of 512 rows, ragged last
-    ("pncl_4096", "lowrank", 4096, 700, 192, 64, 10, 25),  # 16 CTAs of 256 rows
+    ("pncl_tall32", "iid", 5000, 300, 96, 32, 8, 24),
+    ("pncl_4096", "lowrank", 4096, 700, 192, 64, 10, 25),
 ]
+PN_VARIANTS = {"cluster2": dict(pn_cluster=1, pn_cpt=2), "cluster1": dict(pn_cluster=1, pn_cpt=1),
+               "grid": dict(pn_cluster=0)}
 
 
-@pytest.mark.parametrize("variant", ["cluster2", "cluster1", "grid"])
+@pytest.mark.parametrize("variant", list(PN_VARIANTS))
 @pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", PN_CASES, ids=[c[0] for c in PN_CASES])
 def test_panel_kernels(ctx, variant, name, kind, m, n, k, b, p, seed):
-    """cluster2: two columns x 32 rows per thread (bb in (32, 64]); cluster1: one
-    column x 64 rows per thread; grid: the cooperative grid kernel."""
-    import os
     A = inputs.make(kind, m, n, seed, rank=64).numpy()
     o = oracle.rqrcp(A, k, b, p, seed=seed)
-    os.environ["RQRCP_PN_CLUSTER"] = "0" if variant == "grid" else "1"
-    os.environ["RQRCP_PN_CPT"] = "1" if variant == "cluster1" else "2"
-    try:
+    with options(ctx, **PN_VARIANTS[variant]):
         g = gpu_factor(ctx, A, k, b, p, seed)
-    finally:
-        os.environ.pop("RQRCP_PN_CLUSTER", None)
-        os.environ.pop("RQRCP_PN_CPT", None)
     compare(A, g, o, k)
 
 
-# ---- the bulk trailing update overlapped with the next sample QRCP (default
-# when that runs on one cluster, P = 1, Eq. (4)) vs the serial schedule.
-OVL_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "lowrank", "kfull")] + [
-    # n' > 4096: the next sample QRCP runs on the register grid, the bulk update
-    # with dynamically claimed tiles beside it
-    ("ovl_grid74", "iid", 700, 4700, 192, 64, 10, 28),
+@pytest.mark.parametrize("rows,grid", [(8, 4), (16, 2), (1, 1)])
+def test_panel_grid_l2_rows(ctx, rows, grid):
+    """Grid panel kernel with more rows per CTA than shared memory holds
+    (PN_MAXROWS staging, rows >= nsm via L2): b = 128 panels of 3000 rows on
+    1-4 CTAs put ~750-3000 rows per CTA, ~200 of them in shared memory."""
+    A = inputs.make("graded", 3000, 700, 41).numpy()
+    o = oracle.rqrcp(A, 256, 128, 16, seed=41)
+    with options(ctx, pn_cluster=0, pn_rows=rows, pn_grid=grid):
+        g = gpu_factor(ctx, A, 256, 128, 16, 41)
+    compare(A, g, o, 256)
+
+
+# ---- schedules: serial, bulk update beside the next sample QRCP, bulk update
+# beside the next panel QR (look-ahead): the same arithmetic, bitwise -------
+SCHED_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "lowrank", "kfull", "b128", "odd")] + [
+    ("grid74", "iid", 700, 4700, 192, 64, 10, 28),    # register-grid sample QRCP
+    ("gridpanel", "graded", 4500, 900, 256, 128, 16, 29),  # grid panel kernel (b = 128)
 ]
 
 
-@pytest.mark.parametrize("overlap", ["1", "0"])
-@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", OVL_CASES, ids=[c[0] for c in OVL_CASES])
-def test_overlap_schedule(ctx, overlap, name, kind, m, n, k, b, p, seed):
-    import os
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", SCHED_CASES, ids=[c[0] for c in SCHED_CASES])
+def test_schedules_bitwise_and_parity(ctx, name, kind, m, n, k, b, p, seed):
     A = inputs.make(kind, m, n, seed, rank=64).numpy()
     o = oracle.rqrcp(A, k, b, p, seed=seed)
-    os.environ["RQRCP_OVERLAP"] = overlap
-    try:
-        g = gpu_factor(ctx, A, k, b, p, seed)
-    finally:
-        os.environ.pop("RQRCP_OVERLAP", None)
-    compare(A, g, o, k)
-
-
-def test_overlap_grid_bitwise_equal_serial(ctx):
-    """The dynamically scheduled bulk update (grid sample QRCP) gives the same bits."""
-    import os
-    A = inputs.make("graded", 800, 4800, 29).numpy()
     outs = []
-    for ov in ("1", "0"):
-        os.environ["RQRCP_OVERLAP"] = ov
-        try:
-            outs.append(gpu_factor(ctx, A, 256, 64, 10, 29))
-        finally:
-            os.environ.pop("RQRCP_OVERLAP", None)
-    assert np.array_equal(outs[0]["jpvt"], outs[1]["jpvt"])
-    assert np.array_equal(outs[0]["A"], outs[1]["A"])
+    for s in (0, 1, 2):
+        with options(ctx, schedule=s):
+            outs.append(gpu_factor(ctx, A, k, b, p, seed))
+    compare(A, outs[2], o, k)
+    for g in outs[:2]:
+        assert np.array_equal(g["jpvt"], outs[2]["jpvt"])
+        assert np.array_equal(g["tau"], outs[2]["tau"])
+        assert np.array_equal(g["A"], outs[2]["A"])
 
 
-def test_overlap_bitwise_equal_serial(ctx):
-    """Overlapping changes the schedule, not the arithmetic: bitwise equal outputs."""
-    import os
+def test_schedules_bitwise_C2(ctx):
     c = inputs.CONFIGS["C2"]
     A = inputs.config_matrix("C2").numpy()
     outs = []
-    for ov in ("1", "0"):
-        os.environ["RQRCP_OVERLAP"] = ov
-        try:
+    for s in (0, 1, 2):
+        with options(ctx, schedule=s):
             outs.append(gpu_factor(ctx, A, c["k"], c["b"], c["p"], c["seed"]))
-        finally:
-            os.environ.pop("RQRCP_OVERLAP", None)
-    assert np.array_equal(outs[0]["jpvt"], outs[1]["jpvt"])
-    assert np.array_equal(outs[0]["tau"], outs[1]["tau"])
-    assert np.array_equal(outs[0]["A"], outs[1]["A"])
+    for g in outs[1:]:
+        assert np.array_equal(g["jpvt"], outs[0]["jpvt"])
+        assert np.array_equal(g["A"], outs[0]["A"])
 
 
 # ---- updating formula 2 (Eq. (5), P:224-246) on the GPU: SURVEY.md §8(f) N2 ----
@@ -353,8 +508,6 @@ EQ5_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "lowrank", "b1
 
 @pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", EQ5_CASES, ids=[c[0] for c in EQ5_CASES])
 def test_eq5_update_parity(ctx, name, kind, m, n, k, b, p, seed):
-    """GPU Eq. (5) vs the oracle's Eq. (5) mode: identical pivots, |diag R| and
-    residuals within the acceptance tolerances."""
     A = inputs.make(kind, m, n, seed, rank=64).numpy()
     o = oracle.rqrcp(A, k, b, p, seed=seed, update_rule=2)
     ctx.set_update_rule(2)
@@ -366,8 +519,7 @@ def test_eq5_update_parity(ctx, name, kind, m, n, k, b, p, seed):
 
 
 def test_eq4_eq5_identical_permutations_gpu(ctx):
-    """the two updating formulas give the same permutation (C2 shape
-    scaled down, iid: the pivot-choice stress case)."""
+    """the two updating formulas give the same permutation."""
     A = inputs.iid(31, 1024, 1024).numpy()
     g4 = gpu_factor(ctx, A, 256, 64, 10, 31)
     ctx.set_update_rule(2)
@@ -425,38 +577,30 @@ CQR_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "wide", "lowra
 
 @pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", CQR_CASES, ids=[c[0] for c in CQR_CASES])
 def test_cqr_panel_parity(ctx, name, kind, m, n, k, b, p, seed):
-    """RQRCP_PANEL=cqr: every well-conditioned panel goes through CholeskyQR2 +
-    reconstruction (checked through the panels_householder counter) and the
-    result meets the same acceptance as the column-by-column panel."""
-    import os
+    """panel=1: every well-conditioned panel goes through CholeskyQR2 +
+    reconstruction (checked through the panels_householder counter); the
+    result meets the same acceptance.  R, V, tau come from a different
+    algorithm here, so they are compared to 1e-10 like everything else."""
     A = inputs.make(kind, m, n, seed, rank=64).numpy()
     o = oracle.rqrcp(A, k, b, p, seed=seed)
-    os.environ["RQRCP_PANEL"] = "cqr"
-    try:
+    with options(ctx, panel=1):
         g = gpu_factor(ctx, A, k, b, p, seed)
         t = ctx.timings()
-    finally:
-        os.environ.pop("RQRCP_PANEL", None)
     compare(A, g, o, k)
-    assert t["panels_householder"] < t["panels"]  # the CholeskyQR2 path factored panels
+    assert t["panels_householder"] < t["panels"]
 
 
 def test_cqr_guard_falls_back(ctx):
-    """A rank-stopped panel (rank 40 < k = 64, b = 32: the second panel stops
-    at bb_eff = 8, reading R-G12) fails the CholeskyQR2 guard and is factored
-    by the column-by-column kernel; the result matches the oracle's."""
-    import os
+    """A rank-stopped panel fails the CholeskyQR2 guard and is factored by the
+    column-by-column kernel; the result matches the oracle's."""
     rng = np.random.default_rng(5)
     A = rng.standard_normal((300, 40)) @ rng.standard_normal((40, 260))
     o = oracle.rqrcp(A, 64, 32, 8, seed=3, check=False)
-    os.environ["RQRCP_PANEL"] = "cqr"
-    try:
+    with options(ctx, panel=1):
         Ad = to_dev(A)
         jpvt, tau, rank = ctx.factor(Ad, 64, 32, 8, seed=3)
         torch.cuda.synchronize()
         t = ctx.timings()
-    finally:
-        os.environ.pop("RQRCP_PANEL", None)
     assert rank == o["rank"] == 40
     assert t["panels_householder"] >= 1
     assert np.array_equal(jpvt.cpu().numpy()[:40], o["jpvt"][:40])
@@ -464,14 +608,13 @@ def test_cqr_guard_falls_back(ctx):
     assert np.max(np.abs(dg - do) / do) <= DIAG_RTOL
 
 
-def test_update_kernels_agree(ctx):
-    """b = 128 (K = 128: the TMA-epilogue update kernel) vs the same
-    factorization with the panels shifted by one row (odd offsets: the
-    register-epilogue / cp.async kernels) -- both against the oracle."""
-    A = inputs.make("iid", 1200, 1000, 33).numpy()
-    o = oracle.rqrcp(A, 256, 128, 16, seed=33)
-    g = gpu_factor(ctx, A, 256, 128, 16, 33)
-    compare(A, g, o, 256)
+def test_r11_stop_cqr_declines(ctx):
+    """With the CholeskyQR2 panel the R11-diagonal stop is still taken (the
+    guard declines a panel with a diagonal below the threshold)."""
+    A, Om, b, p = r11_stop_problem()
+    with options(ctx, panel=1):
+        g = gpu_factor(ctx, A, 16, b, p, 0, omega=torch.tensor(Om.ravel(order="F")).cuda())
+    assert g["rank"] == 1
 
 
 # ---- low-rank outputs (P:79-83, P:153, P:813-815): SURVEY.md §8(f) N4 ----
@@ -480,10 +623,6 @@ LR_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "wide", "b128",
 
 @pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", LR_CASES, ids=[c[0] for c in LR_CASES])
 def test_lowrank_outputs(ctx, name, kind, m, n, k, b, p, seed):
-    """Q1 against the oracle's reflectors applied to [I; 0] (P:120 'Q = H1 H2
-    ... Hk'), Q1^T Q1 = I, Q1 [R11 R12] = A Pi truncated; CX
-    coefficients against the definition X = C^+ A (least squares) and
-    ||A - C X||_F = ||R22||_F."""
     A = inputs.make(kind, m, n, seed, rank=64).numpy()
     o = oracle.rqrcp(A, k, b, p, seed=seed)
     Ad = to_dev(A)

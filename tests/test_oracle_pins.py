@@ -560,3 +560,65 @@ def test_srqr_tau_caps(seed):
     s_l = np.linalg.svd(Rt, compute_uv=False)[k - 1]
     tau_hat = g1 * g2 * (s22 / c12) * (1.0 / r11inv_12) / s_l
     assert tau_hat <= g1 * g2 * np.sqrt(k * (n - k)) * (1 + 1e-12)  # Eq. (12)
+
+
+# ----------------------------------------------------------------------------
+# R11-diagonal rank stop (reading R-G12b) and the tie rule (R-G5)
+# ----------------------------------------------------------------------------
+def test_r11_diagonal_stop_closed_form():
+    """Column 5 of A is 1e-15 e_5 but Omega amplifies row 5 by 1e17: the sample
+    QRCP picks it as the second pivot; |R(1,1)| = 1e-15 is below
+    1e3 eps ||panel||_F (~ 4.4e-11 here), so the factorization stops at rank 1
+    with tau = 0 from there on, R(0,0) = +200 (dlarfg on 200 e_0: x(1:) = 0
+    gives tau = 0 and beta = alpha, reading R-G7), and the untouched column 5
+    still holds its input value below the stop."""
+    m, n, b, p = 40, 30, 8, 2
+    A = np.zeros((m, n))
+    for j in range(n):
+        A[j, j] = 1.0
+    A[5, 5] = 1e-15
+    A[:, 0] *= 200.0
+    Om = np.random.default_rng(11).standard_normal((b + p, m))
+    Om[:, 5] *= 1e17
+    o = oracle.rqrcp(A, 16, b, p, omega=Om, check=False)
+    assert o["status"] == 0
+    assert o["rank"] == 1
+    assert o["jpvt"][0] == 0 and o["jpvt"][1] == 5
+    assert o["A"][0, 0] == 200.0
+    assert np.all(o["tau"] == 0.0)
+    assert o["A"][5, 1] == 1e-15  # column 5 (now at position 1) untouched: H_0 = I on it
+
+
+def test_r11_stop_not_triggered_on_full_rank():
+    """Well-conditioned inputs never trip the R11-diagonal stop."""
+    A = inputs.iid(3, 200, 150).numpy()
+    o = oracle.rqrcp(A, 100, 16, 8, seed=2)
+    assert o["rank"] == 100
+
+
+def test_tie_rule_lowest_position():
+    """Bitwise-identical columns tie in the squared sample norms; the lowest
+    current position wins (reading R-G5).  Every column is duplicated, so
+    the pivots are the even (first) members of the pairs."""
+    rng = np.random.default_rng(8)
+    X = rng.standard_normal((300, 60)) * np.exp(-np.arange(60) / 10.0)
+    A = np.repeat(X, 2, axis=1)
+    o = oracle.rqrcp(A, 16, 8, 4, seed=9, check=False)
+    assert np.all(o["jpvt"][:16] % 2 == 0)
+    q = oracle.sample_qrcp(np.repeat(np.eye(4)[:, :2] * [2.0, 1.0], 2, axis=1), 1)
+    assert q["piv"][0] == 0  # columns 0 and 1 identical: position 0 wins
+
+
+def test_householder_convention_matches_lapack():
+    """Reading R-G7 pinned to LAPACK: with the oracle's pivots, the oracle's
+    V, tau and R equal dgeqrf on A Pi (same dlarfg convention) to rounding."""
+    from scipy.linalg import lapack
+    A = inputs.iid(12, 120, 90).numpy()
+    o = oracle.rqrcp(A, 90, 16, 8, seed=4)
+    Api = np.asfortranarray(A[:, o["jpvt"]])
+    qr, tau, work, info = lapack.dgeqrf(Api)
+    assert info == 0
+    F = o["A"]
+    assert np.max(np.abs(np.triu(F[:90]) - np.triu(qr[:90]))) <= 1e-12 * np.max(np.abs(qr))
+    assert np.max(np.abs(o["tau"] - tau[:90])) <= 1e-12
+    assert np.max(np.abs(np.tril(F[:, :90], -1) - np.tril(qr[:, :90], -1))) <= 1e-12
