@@ -1625,10 +1625,11 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     R.done = ctx->iscal + 2;
     R.rankd = ctx->iscal + 3;
     // schedule: the bulk rows of each trailing update overlap the next sample
-    // QRCP when that runs on one cluster (it leaves the other SMs free), else
-    // the next panel QR (look-ahead); serial when asked
+    // QRCP (measured best at C2-C4: 4.40 / 50.7 / 1088 ms against 5.23 / 54.8 /
+    // 1191 ms with the panel look-ahead, whose panel kernel slows down when it
+    // shares the GPU with the update, and 1087 ms serial at C4)
     int sched = ctx->opt.schedule;
-    if (sched < 0) sched = (sq_kind(ctx, R.l, n) == SQK_CLUSTER) ? 1 : 2;
+    if (sched < 0) sched = 1;
     R.sched = sched;
     const int ev_t0 = ctx->nev;
     cudaEventRecord(ctx->ev[ctx->nev++], ctx->stream);

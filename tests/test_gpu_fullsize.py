@@ -108,7 +108,7 @@ def _run(name, prefix_panels=None, nprobe=4):
     Vo = np.tril(Fo[:, :kp], -1)
     assert np.max(np.abs(Vg - Vo)) <= ELEM_RTOL
     del Vg, Vo, F, Fo
-    check_trace_panels(tr, panels, o["jpvt"])
+    check_trace_panels(tr, panels, o["jpvt"], k=k)
     return r22
 
 
