@@ -2,11 +2,15 @@
 (torch.distributed gloo, 127.0.0.1): the 1D column-block-cyclic layout comes
 from the C library's host functions (rqrcp_shard_columns /
 rqrcp_shard_global_index); each rank holds its shard and runs the same
-per-rank schedule as the CUDA driver (rqrcp.cu: gather_sample, dist_swaps,
-dist_panel_bcast, local trailing + sample updates) with numpy arithmetic.
-The result must equal the single-process oracle: identical pivots, R and tau
-to rounding.  This checks the partitioning, the cross-rank swap plan, the
-owner broadcast and the gather/reorder logic without NCCL or a GPU.
+per-rank exchange as the CUDA driver (rqrcp.cu Run::panel / moves.cuh):
+pivot columns packed full height and delivered to the panel owner by an
+INTEGER-SUM reduce of their bit patterns (one contributor per element: exact),
+the owner's panel QR and broadcast of V / tau / R11, the broadcast of the
+owner's displaced slot columns to the move destinations, local trailing and
+sample updates, the sample allgather -- with numpy arithmetic.  The result
+must equal the single-process oracle: identical pivots, R and tau to rounding.
+(The same driver runs on one B200 through the loopback transport in
+tests/test_gpu_multirank.py, bitwise against P = 1.)
 """
 import os
 import socket
@@ -43,9 +47,10 @@ def _householder(x):
     return v, tau, beta
 
 
-def _pairs_from_piv(piv, nb):
-    """(dst, src) moves of the touched positions after the transpositions
-    j <-> piv[j], applied in order (reading R-G5) -- the rule of the kernel."""
+def _perm_and_moves(piv, nb):
+    """The transpositions j <-> piv[j] applied in order (reading R-G5) as the
+    kernels leave them: perm[q] = original position of the column that ends at
+    q (q < nb), and the (dst <- src) moves of every touched position."""
     where = {}
     for j in range(nb):
         s = int(piv[j])
@@ -53,10 +58,12 @@ def _pairs_from_piv(piv, nb):
             continue
         a, b = where.get(j, j), where.get(s, s)
         where[j], where[s] = b, a
-    return [(d, s) for d, s in where.items() if d != s]
+    perm = [where.get(q, q) for q in range(nb)]
+    moves = [(d, s) for d, s in where.items() if d != s]
+    return perm, moves
 
 
-def _worker(rank, world, port, A, k, b, p, seed, out):
+def _worker(rank, world, port, A, k, b, p, seed, out, P_layout=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -94,50 +101,52 @@ def _worker(rank, world, port, A, k, b, p, seed, out):
         bb = min(b, k - i)
         q = oracle.sample_qrcp(B[:, i:], bb)           # replicated on every rank
         Rh = q["R"]                                     # transformed sample, pivoted order
-        # ---- swaps: local moves + send/recv of cross-rank pairs ----
-        pairs = _pairs_from_piv(q["piv"], bb)
-        stage = {}
-        for d, s in pairs:
-            if owner(i + s) == rank:
-                stage[(d, s)] = Al[:, local(i + s)].copy()
-        reqs = []
-        recv = {}
-        for d, s in pairs:
-            so, dn = owner(i + s), owner(i + d)
-            if so == rank and dn != rank:
-                reqs.append(dist.isend(torch.from_numpy(stage[(d, s)]), dn))
-            if dn == rank and so != rank:
-                t = torch.zeros(m, dtype=torch.float64)
-                recv[(d, s)] = t
-                reqs.append(dist.irecv(t, so))
-        for r_ in reqs:
-            r_.wait()
-        for d, s in pairs:
-            if owner(i + d) == rank:
-                Al[:, local(i + d)] = stage[(d, s)] if (d, s) in stage else recv[(d, s)].numpy()
-        jv = jpvt.copy()
-        for d, s in pairs:
-            jpvt[i + d] = jv[i + s]
-        # ---- panel: owner factors (unblocked Householder), broadcasts V, tau, R11 ----
+        perm, moves = _perm_and_moves(q["piv"], bb)
         own = owner(i)
-        pk = torch.zeros(m - i + 1, bb, dtype=torch.float64)  # V (m-i rows) + tau row
+        # ---- (1) pack: the pivot columns this rank owns, full height, zeros
+        #      elsewhere; (3) integer-sum reduce to the owner: exact bits ----
+        pk = np.zeros((m, bb))
+        for qq in range(bb):
+            jg = i + perm[qq]
+            if owner(jg) == rank:
+                pk[:, qq] = Al[:, local(jg)]
+        bits = torch.from_numpy(pk.view(np.int64).copy())
+        dist.reduce(bits, own, op=dist.ReduceOp.SUM)
+        Pbuf = bits.numpy().view(np.float64).copy() if rank == own else None
+        # ---- (4) panel QR on the owner (unblocked Householder), broadcast ----
+        pkv = torch.zeros(m - i + 1, bb, dtype=torch.float64)  # V (m-i rows) + tau row
         r11 = torch.zeros(bb, bb, dtype=torch.float64)
         if rank == own:
-            lj = local(i)
             for j in range(bb):
-                v, t, beta = _householder(Al[i + j:, lj + j].copy())
-                Al[i + j, lj + j] = beta
-                Al[i + j + 1:, lj + j] = v[1:]
-                for c in range(lj + j + 1, lj + bb):
-                    Al[i + j:, c] -= t * v * (v @ Al[i + j:, c])
-                pk[j:m - i, j] = torch.from_numpy(v)
-                pk[m - i, j] = t
-            r11[:] = torch.from_numpy(np.triu(Al[i:i + bb, lj:lj + bb]))
-        dist.broadcast(pk, own)
+                v, t, beta = _householder(Pbuf[i + j:, j].copy())
+                Pbuf[i + j, j] = beta
+                Pbuf[i + j + 1:, j] = v[1:]
+                for c in range(j + 1, bb):
+                    Pbuf[i + j:, c] -= t * v * (v @ Pbuf[i + j:, c])
+                pkv[j:m - i, j] = torch.from_numpy(v)
+                pkv[m - i, j] = t
+            r11[:] = torch.from_numpy(np.triu(Pbuf[i:i + bb, :bb]))
+        dist.broadcast(pkv, own)
         dist.broadcast(r11, own)
-        V = pk[:m - i].numpy()
-        tau[i:i + bb] = pk[m - i].numpy()
+        V = pkv[:m - i].numpy()
+        tau[i:i + bb] = pkv[m - i].numpy()
         R11 = r11.numpy()
+        # ---- (6) displaced: the owner's original slot columns go to the move
+        #      destinations >= bb (fact (b): their sources are slots) ----
+        disp = torch.zeros(m, bb, dtype=torch.float64)
+        if rank == own:
+            disp[:] = torch.from_numpy(Al[:, local(i):local(i) + bb].copy())
+        dist.broadcast(disp, own)
+        for d, s_ in moves:
+            if d >= bb:
+                assert s_ < bb
+                if owner(i + d) == rank:
+                    Al[:, local(i + d)] = disp.numpy()[:, s_]
+        if rank == own:
+            Al[:, local(i):local(i) + bb] = Pbuf
+        jv = jpvt.copy()
+        for d, s_ in moves:
+            jpvt[i + d] = jv[i + s_]
         # ---- local trailing update (each reflector in order, like the oracle) ----
         tr = [q_ for q_, g in enumerate(mine) if g >= i + bb]
         for c in tr:
@@ -197,3 +206,26 @@ def test_layout_functions():
         for r, s in enumerate(shards):
             assert s == sorted(s)
             assert all((c // b) % P == r for c in s)
+
+
+def test_transposition_facts():
+    """The two facts the pack / displaced exchange relies on (moves.cuh),
+    brute force over random transposition sequences j <-> s_j, s_j >= j
+    (reading R-G5): (a) slot q ends up holding the column from perm[q];
+    (b) every touched position >= bb receives an original slot column."""
+    rng = np.random.default_rng(0)
+    for _ in range(2000):
+        nn = int(rng.integers(1, 40))
+        bb = int(rng.integers(1, nn + 1))
+        piv = [int(rng.integers(j, nn)) for j in range(bb)]
+        arr = list(range(nn))
+        for j, s in enumerate(piv):
+            arr[j], arr[s] = arr[s], arr[j]
+        perm, moves = _perm_and_moves(piv, bb)
+        assert perm == arr[:bb]
+        for d, s in moves:
+            assert arr[d] == s
+            if d >= bb:
+                assert s < bb
+        touched = {d for d, _ in moves}
+        assert all(arr[q] == q for q in range(nn) if q not in touched)
