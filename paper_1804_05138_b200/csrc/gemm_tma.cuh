@@ -484,3 +484,167 @@ __global__ void __launch_bounds__(WM *WN * 32, 1)
 }
 
 }  // namespace rq
+
+namespace rq {
+
+// ---------------------------------------------------------------------------
+// The S5 rank-bb update A22 += V W2 (as A22^T += W2^T Vt), warp-specialised:
+//  * one producer warp streams the operand stages by TMA into a ring guarded
+//    by full (transaction bytes) and empty (one arrive per consumer warp)
+//    mbarriers -- no CTA-wide barrier anywhere in the main loop;
+//  * each of the WM x WN consumer warps owns a 32 x 32 sub-tile of the C tile
+//    and moves it ITSELF by TMA: its next tile's C is prefetched into the
+//    other of two private shared-memory buffers while it computes, and its
+//    finished sub-tile is added in shared memory and stored by bulk tensor
+//    stores -- so one warp's epilogue overlaps the other warps' DMMAs (the
+//    CTA-wide epilogue + per-stage __syncthreads of gemm_upd_tma_kernel cost
+//    ~20% of the tensor pipe at C4, ncu).
+// Same per-element arithmetic as every other update kernel: acc = sum over k
+// (ascending, DMMA k4 steps) from zero, then C + acc.
+// ---------------------------------------------------------------------------
+template <int WM, int WN, int BK, int ST>
+constexpr size_t upd_ws_smem() {
+    return 128 + (size_t)ST * BK * (32 * WM + 32 * WN) * sizeof(double) + (size_t)WM * WN * 2 * 32 * 32 * sizeof(double) +
+           (2 * ST + 2 * WM * WN) * sizeof(uint64_t);
+}
+
+RQ_DEV void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int WM, int WN, int BK, int ST>
+__global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
+    gemm_upd_ws_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
+                       const __grid_constant__ CUtensorMap tmC /* box {8, 32} */, TmaGemmArgs g) {
+    constexpr int MT = 4, NT = 4;
+    constexpr int BM = 8 * MT * WM;  // columns of A22 per tile
+    constexpr int BN = 8 * NT * WN;  // rows of A22 per tile
+    constexpr int KB = BK / 8;
+    constexpr int XS = KB * BM * 8;
+    constexpr int YS = KB * BN * 8;
+    constexpr int CW = 32 * 32;      // doubles per warp C buffer: 4 slabs of [32 cols][8 rows]
+    constexpr int NCW = WM * WN;     // consumer warps
+    constexpr unsigned STAGE_BYTES = (unsigned)((XS + YS) * sizeof(double));
+    constexpr unsigned CW_BYTES = (unsigned)(CW * sizeof(double));
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const unsigned pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
+    double *xs = reinterpret_cast<double *>(smem_raw + pad);
+    double *ys = xs + ST * XS;
+    double *cb = ys + ST * YS;  // [NCW][2][CW]
+    uint64_t *full = reinterpret_cast<uint64_t *>(cb + NCW * 2 * CW);
+    uint64_t *empty = full + ST;
+    uint64_t *cfull = empty + ST;  // [NCW][2]
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t tilesN = (g.N + BN - 1) / BN, tilesM = (g.M + BM - 1) / BM;
+    const int64_t ntiles = tilesN * tilesM;
+    const int nk = (int)((g.K + BK - 1) / BK);
+
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        for (int w = 0; w < 2 * NCW; ++w) mbar_init(&cfull[w], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == NCW) {  // ---------------- producer ----------------
+        if (lane != 0) return;
+        int64_t sp = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int64_t m0 = (t / tilesN) * BM, n0 = (t % tilesN) * BN;
+            for (int kc = 0; kc < nk; ++kc, ++sp) {
+                const int slot = (int)(sp % ST);
+                if (sp >= ST) mbar_wait(&empty[slot], (unsigned)(((sp / ST) - 1) & 1));
+                mbar_expect_tx(&full[slot], STAGE_BYTES);
+                const int k0 = kc * BK;
+#pragma unroll
+                for (int kb = 0; kb < KB; ++kb) {
+                    tma_load_2d(xs + slot * XS + kb * BM * 8, &tmX, (int)(g.xk0 + k0 + kb * 8), (int)(g.xm0 + m0), &full[slot]);
+                    tma_load_2d(ys + slot * YS + kb * BN * 8, &tmY, (int)(g.yk0 + k0 + kb * 8), (int)(g.yn0 + n0), &full[slot]);
+                }
+            }
+        }
+        return;
+    }
+    // ---------------- consumers ----------------
+    const int wm = warp / WN, wn = warp % WN;
+    const int fr = lane >> 2, fk = (lane & 3) * 2;
+    double *mycb = cb + (int64_t)warp * 2 * CW;
+    uint64_t *mycf = cfull + 2 * warp;
+    auto issue_c = [&](int64_t t, int buf) {  // lane 0: this warp's sub-tile of tile t
+        const int64_t m0 = (t / tilesN) * BM + wm * 32, n0 = (t % tilesN) * BN + wn * 32;
+        mbar_expect_tx(&mycf[buf], CW_BYTES);
+#pragma unroll
+        for (int s = 0; s < 4; ++s) tma_load_2d(mycb + buf * CW + s * 256, &tmC, (int)(n0 + 8 * s), (int)m0, &mycf[buf]);
+    };
+    if (lane == 0 && (int64_t)blockIdx.x < ntiles) issue_c(blockIdx.x, 0);
+    int64_t sc = 0, nt = 0;
+    double acc[MT][NT][2];
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
+        const int buf = (int)(nt & 1);
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int kc = 0; kc < nk; ++kc, ++sc) {
+            const int slot = (int)(sc % ST);
+            mbar_wait(&full[slot], (unsigned)((sc / ST) & 1));
+            const double *xd = xs + slot * XS;
+            const double *yd = ys + slot * YS;
+#pragma unroll
+            for (int kb = 0; kb < KB; ++kb) {
+                double2 a[MT], b[NT];
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+                    a[i] = *reinterpret_cast<const double2 *>(xd + (kb * BM + wm * 8 * MT + i * 8 + fr) * 8 + fk);
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+                    b[j] = *reinterpret_cast<const double2 *>(yd + (kb * BN + wn * 8 * NT + j * 8 + fr) * 8 + fk);
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            // after the first stage, prefetch this warp's next C sub-tile into the
+            // other buffer (its previous stores have had a stage to drain)
+            if (kc == 0 && lane == 0 && t + gridDim.x < ntiles) {
+                asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                issue_c(t + gridDim.x, buf ^ 1);
+            }
+        }
+        // epilogue of this warp's sub-tile
+        mbar_wait(&mycf[buf], (unsigned)((nt >> 1) & 1));
+        double *cbuf = mycb + buf * CW;
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                double2 *p = reinterpret_cast<double2 *>(cbuf + j * 256 + (i * 8 + fr) * 8 + fk);
+                double2 c2 = *p;
+                c2.x += acc[i][j][0];
+                c2.y += acc[i][j][1];
+                *p = c2;
+            }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+            const int64_t m0 = (t / tilesN) * BM + wm * 32, n0 = (t % tilesN) * BN + wn * 32;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) tma_store_2d(&tmC, (int)(n0 + 8 * s), (int)m0, cbuf + s * 256);
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
+}  // namespace rq

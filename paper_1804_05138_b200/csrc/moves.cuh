@@ -147,13 +147,27 @@ __global__ void panel_tol_kernel(const double *colss, int bb, const int *bb_eff,
 // The R11-diagonal stop found in the panel at column jstop (< bb_eff): the
 // panel kernel wrote *stop_col; fold it into the panel state (one thread,
 // after the panel kernel): bb_eff = jstop, rank -= (old bb_eff - jstop), done.
-__global__ void panel_stop_apply_kernel(const int *stop_col, int *bb_eff, int *rank, int *done) {
+__global__ void panel_stop_apply_kernel(const int *stop_col, int off, int *bb_eff, int *rank, int *done) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const int js = *stop_col;
-    if (js < 0 || js >= *bb_eff) return;
+    if (*stop_col < 0) return;
+    const int js = *stop_col + off;  // the column within the panel (blocked panels: + sub-panel offset)
+    if (js >= *bb_eff) return;
     *rank -= (*bb_eff - js);
     *bb_eff = js;
     *done = 1;
+}
+
+// Blocked panel helpers: the columns a sub-panel factors, and zeros above the
+// diagonal blocks of the explicit V / V^T (each sub-panel writes its rows only)
+__global__ void sub_eff_kernel(const int *bb_eff, int c0, int w, int *out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *out = min(w, max(0, *bb_eff - c0));
+}
+__global__ void zero_top_kernel(double *vfull, int64_t ldv, double *vt, int64_t ldvt, int bbpad) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bbpad * bbpad; e += gridDim.x * blockDim.x) {
+        const int r = e % bbpad, c = e / bbpad;
+        vfull[r + (int64_t)c * ldv] = 0.0;
+        vt[c + (int64_t)r * ldvt] = 0.0;
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -29,7 +29,8 @@ constexpr int PN_THREADS = 256;
 constexpr int PN_WARPS = PN_THREADS / 32;
 constexpr int PN_MAXB = 128;
 constexpr int PN_MAXROWS = 1024;  // rows per CTA (x staging buffer)
-constexpr int PN_CB = 8;          // columns per warp batch (interleaved reductions)
+constexpr int PN_MAXG = 152;      // CTAs of the cooperative grid (<= one per SM)
+constexpr int PN_RMAX = (PN_MAXG + PN_WARPS - 1) / PN_WARPS;  // partial rows summed per warp
 
 struct PanelArgs {
     double *A;          // &A[i + i*lda]
@@ -49,13 +50,20 @@ struct PanelArgs {
     double *part;       // [2][G][bbpad] partial Gram rows (one contiguous row per CTA)
     double *rowj;       // [2][bbpad] published row j
     unsigned *bar;      // per-launch barrier counter (zeroed by the host)
+    int col0;           // blocked panel: this launch factors panel columns col0.. (bb_eff is the panel's)
+    int64_t ldvt;       // leading dimension of vt (0: bbpad)
+    int64_t ldy;        // leading dimension of ybuf (0: bbpad)
     const double *tol2; // R11-diagonal rank stop (reading R-G12b): stop at the first column whose
                         // beta^2 < *tol2 (= (1e3 eps)^2 ||panel||_F^2); nullptr: no check
     int *stop_col;      // out: that column (-1 when none); written by CTA 0
     unsigned long long *trace;  // debug: [2 CTAs][64 steps][8 phases] clock64 stamps, or nullptr
 };
 
+// CB: panel columns per warp batch of the partial Gram row (8; 4 for the
+// 32-column sub-panels of the blocked panel, so all 8 warps have columns)
+template <int CB>
 __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
+    constexpr int PN_CB = CB;
     extern __shared__ __align__(16) double pn_dyn[];
     __shared__ double w[PN_MAXB], rjs[PN_MAXB];
     __shared__ double wred[PN_WARPS][PN_MAXB];
@@ -66,7 +74,8 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
     const int G = gridDim.x, g = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int bb = a.bb;
-    const int bbe = *a.bb_eff;
+    const int bbe = min(bb, max(0, *a.bb_eff - a.col0));
+    const int64_t ldvt = a.ldvt ? a.ldvt : a.bbpad, ldy = a.ldy ? a.ldy : a.bbpad;
     const int64_t mp = a.mp;
     const int64_t rpb = (mp + G - 1) / G;
     const int64_t r_lo = min(mp, (int64_t)g * rpb), r_hi = min(mp, r_lo + rpb);
@@ -132,26 +141,27 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
         //      reads; warp w sums rows g = w, w+8, ... in order, then the 8 warp
         //      sums are added in warp order: one fixed order in every CTA) ------
         {
+            // every load of this warp's rows (g = warp + 8 h) in flight at once:
+            // one L2 round trip instead of one per batch of four rows
             const double *pp = a.part + (int64_t)par * G * a.bbpad;
+            const int nu = (bb + 31) >> 5;
             double acc[PN_MAXB / 32];
 #pragma unroll
             for (int u = 0; u < PN_MAXB / 32; ++u) acc[u] = 0.0;
-            for (int g0 = warp; g0 < G; g0 += 4 * PN_WARPS) {
-                double v[4][PN_MAXB / 32];
+            double v[PN_RMAX][PN_MAXB / 32];
 #pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    const int gg = g0 + h * PN_WARPS;
+            for (int h = 0; h < PN_RMAX; ++h) {
+                const int gg = warp + h * PN_WARPS;
 #pragma unroll
-                    for (int u = 0; u < PN_MAXB / 32; ++u) {
-                        const int c = lane + 32 * u;
-                        v[h][u] = (gg < G && c < bb) ? ld_cg(pp + (int64_t)gg * a.bbpad + c) : 0.0;
-                    }
+                for (int u = 0; u < PN_MAXB / 32; ++u) {
+                    const int c = lane + 32 * u;
+                    v[h][u] = (u < nu && gg < G && c < bb) ? ld_cg(pp + (int64_t)gg * a.bbpad + c) : 0.0;
                 }
-#pragma unroll
-                for (int h = 0; h < 4; ++h)
-#pragma unroll
-                    for (int u = 0; u < PN_MAXB / 32; ++u) acc[u] += v[h][u];
             }
+#pragma unroll
+            for (int h = 0; h < PN_RMAX; ++h)
+#pragma unroll
+                for (int u = 0; u < PN_MAXB / 32; ++u) acc[u] += v[h][u];
 #pragma unroll
             for (int u = 0; u < PN_MAXB / 32; ++u) {
                 const int c = lane + 32 * u;
@@ -195,7 +205,7 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
         // CTA 0 records y_c = v_c^T v_j = A(j,c) + scal g_c (c < j): column j of
         // strict_upper(V^T V), from which tri_kernel builds T off the critical path
         if (g == 0)
-            for (int c = tid; c < j; c += PN_THREADS) a.ybuf[c + (int64_t)j * a.bbpad] = rjs[c] + scal * w[c];
+            for (int c = tid; c < j; c += PN_THREADS) a.ybuf[c + (int64_t)j * ldy] = rjs[c] + scal * w[c];
         // w_c = tau * (a_jc + scal g_c) for c > j
         for (int c = j + 1 + tid; c < bb; c += PN_THREADS) w[c] = tau * (rjs[c] + scal * w[c]);
         for (int r = tid; r < nrows; r += PN_THREADS) xs[r] = Pv(r, j);
@@ -243,7 +253,7 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
         for (int c = lane; c < a.bbpad; c += 32) {
             double v = 0.0;
             if (c < bbo) v = (gr > c) ? Pg[r + (int64_t)c * lda] : (gr == c ? 1.0 : 0.0);
-            a.vt[c + gr * a.bbpad] = v;
+            a.vt[c + gr * ldvt] = v;
         }
     }
     for (int c = warp; c < a.bbpad; c += PN_WARPS)

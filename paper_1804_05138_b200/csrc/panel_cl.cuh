@@ -128,7 +128,8 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
     const int tid = threadIdx.x;
     const int cg = tid % CG, rg = tid / CG;
     const int bb = a.bb;
-    const int bbe = *a.bb_eff;
+    const int bbe = min(bb, max(0, *a.bb_eff - a.col0));
+    const int64_t ldvt = a.ldvt ? a.ldvt : a.bbpad, ldy = a.ldy ? a.ldy : a.bbpad;
     const int64_t mp = a.mp, lda = a.lda;
     const int64_t cta_r0 = (int64_t)g * RC;
     const int rowbase = (int)(cta_r0 + rg * RPT);  // panel row of av[.][0]
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
             ws[k] = 0.0;
             if (g == 0 && rg == 0) {
                 if (c == 0) a.tau[j] = tau;
-                if (c < j) a.ybuf[c + (int64_t)j * a.bbpad] = scal_s[c] * (rjv[c] + scal * gsum[c]);
+                if (c < j) a.ybuf[c + (int64_t)j * ldy] = scal_s[c] * (rjv[c] + scal * gsum[c]);
             }
             if (c > j && c < bb) {
                 const double w = tau * (rjv[c] + scal * gsum[c]);
@@ -400,7 +401,7 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
                     if (gr + h < mp)
-                        *reinterpret_cast<double2 *>(a.vt + c0 + (gr + h) * a.bbpad) = make_double2(v[0][h], v[CPT - 1][h]);
+                        *reinterpret_cast<double2 *>(a.vt + c0 + (gr + h) * ldvt) = make_double2(v[0][h], v[CPT - 1][h]);
             }
 #pragma unroll
             for (int k = 0; k < CPT; ++k) {
@@ -449,7 +450,7 @@ __global__ void __launch_bounds__(PNC_THREADS, 1) panel_qr_cluster_kernel(PanelA
             const int64_t gr = r0 + r;
             if (gr >= mp) continue;
             const double x = stage[cc * LDS + r];
-            a.vt[cc + gr * a.bbpad] = (cc < bbo) ? (gr > cc ? scal_s[cc] * x : (gr == cc ? 1.0 : 0.0)) : 0.0;
+            a.vt[cc + gr * ldvt] = (cc < bbo) ? (gr > cc ? scal_s[cc] * x : (gr == cc ? 1.0 : 0.0)) : 0.0;
         }
     }
     if (g == 0) {

@@ -50,6 +50,9 @@ struct Opts {
     int schedule = -1;       // -1 auto, 0 serial, 1 bulk || next sample QRCP, 2 bulk || next panel (look-ahead)
     int panel = 0;           // 0 Householder columns, 1 CholeskyQR2 + reconstruction, 2 CholeskyQR2 from 8192 rows
     int pn_cluster = 1, pn_cpt = 2, pn_grid = 0, pn_rows = 128, la_panel_ctas = 48;
+    int pn_blocked = 1;      // grid panel on 32-column sub-panels + in-panel DMMA updates: 0 never, 1 when
+                             // a CTA's rows do not fit shared memory, 2 always
+    int upd_kernel = 2;      // update GEMM: 0 CTA-wide TMA epilogue, 1 / 2 warp-specialised (BK 32 x 2 / 16 x 4 stages)
     int sq_cluster = 1, sq_reg = 1, sq_grid = 0, sq_nsm = -1, sq_hstride = 8, sq_poll = 1;
     int debug_sync = 0, trace = 0, trace_panel = 1;
     int64_t nccl_timeout_ms = 600000;
@@ -63,7 +66,8 @@ static const OptDesc kOpts[] = {{"schedule", -1, 2},     {"panel", 0, 2},     {"
                                 {"la_panel_ctas", 1, 4096}, {"sq_cluster", 0, 1}, {"sq_reg", 0, 1},
                                 {"sq_grid", 0, 4096},    {"sq_nsm", -1, 1 << 20}, {"sq_hstride", 1, 8},
                                 {"sq_poll", 0, 2},       {"debug_sync", 0, 1}, {"trace", 0, 1},
-                                {"trace_panel", 1, 1 << 30}, {"nccl_timeout_ms", 1, (int64_t)1 << 40}};
+                                {"trace_panel", 1, 1 << 30}, {"nccl_timeout_ms", 1, (int64_t)1 << 40},
+                                {"upd_kernel", 0, 2}, {"pn_blocked", 0, 2}};
 static bool opt_set(Opts &o, const std::string &n, int64_t v) {
 #define OPT(field)                    \
     if (n == #field) {                \
@@ -72,7 +76,7 @@ static bool opt_set(Opts &o, const std::string &n, int64_t v) {
     }
     OPT(schedule) OPT(panel) OPT(pn_cluster) OPT(pn_cpt) OPT(pn_grid) OPT(pn_rows) OPT(la_panel_ctas)
     OPT(sq_cluster) OPT(sq_reg) OPT(sq_grid) OPT(sq_nsm) OPT(sq_hstride) OPT(sq_poll) OPT(debug_sync) OPT(trace)
-    OPT(trace_panel) OPT(nccl_timeout_ms)
+    OPT(trace_panel) OPT(nccl_timeout_ms) OPT(upd_kernel) OPT(pn_blocked)
 #undef OPT
     return false;
 }
@@ -111,6 +115,8 @@ struct rqrcp_ctx {
     double *packbuf = nullptr; // P > 1: this rank's contribution to pbuf (ldo x bpad)
     double *dispbuf = nullptr; // P > 1: the owner's displaced slot columns (ldo x bpad)
     double *colss = nullptr, *ptol2 = nullptr;  // R11-diagonal stop scale
+    double *ybs = nullptr, *tns = nullptr, *wsub = nullptr, *w2sub = nullptr;  // blocked panel scratch
+    int *subeff = nullptr;
     int *stopc = nullptr;      // panel kernels: the R11-diagonal stop column (-1: none)
     SqHdr *slot_hdr = nullptr;
     int *slot_col = nullptr;
@@ -188,6 +194,7 @@ static const char *g_static_err = "no context";
     } while (0)
 
 static constexpr int kDynSmemMax = 200 * 1024;
+static constexpr int kPanelSub = 32;  // blocked grid panel: sub-panel width (columns factored per kernel)
 static constexpr int64_t kCqrMinRows = 8192;
 
 static int grid_for(int64_t total, int threads, int num_sms) {
@@ -355,6 +362,13 @@ static int tma_skinny_cfg(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const
     constexpr int BM = 8 * MT * WM, BN = 8 * NT * WN;
     const int64_t tiles = ((Ncanon + BN - 1) / BN) * ((M + BM - 1) / BM);
     int splits = choose_splits(tiles, K, ctx->num_sms, M * Ncanon, ctx->splitk_elems, kmin);
+    // a product with a few output tiles (the blocked panel's W_s and V^T V):
+    // spread K over the whole GPU (the partials are small; the K-loop of a few
+    // CTAs was latency-bound: 114 us for 32 x 96 x 32768 on 22 CTAs)
+    if (tiles * 4 < ctx->num_sms) {
+        const int64_t s2 = std::min<int64_t>(std::max<int64_t>(1, K / 128), ctx->num_sms / tiles);
+        if (s2 > splits && s2 * M * Ncanon <= ctx->splitk_elems) splits = (int)s2;
+    }
     int64_t kps = rup((K + splits - 1) / splits, 32);
     splits = (int)((K + kps - 1) / kps);
     TmaGemmArgs g{M, N, K, xk0, xm0, yk0, yn0, C, ldc, kps, splits, M * N, 0};
@@ -396,6 +410,31 @@ static int tma_update(rqrcp_ctx *ctx, int64_t rows, int64_t cols, int64_t K, con
                       const double *vt, int64_t ldvt, double *A22, int64_t lda, bool *done, int *tile_ctr = nullptr) {
     *done = false;
     if (rows <= 0 || cols <= 0) { *done = true; return 0; }
+    // warp-specialised kernel (per-warp TMA epilogue, mbarrier ring): rows > 64
+    const int uk = ctx->opt.upd_kernel;
+    if (uk > 0 && rows > 64 && !tile_ctr && (((uintptr_t)A22 & 15) == 0) && ((lda & 1) == 0)) {
+        CUtensorMap tx, ty, tc;
+        if (make_tmap(&tx, w2, K, cols, ldw, 64) && make_tmap(&ty, vt, K, rows, ldvt, 128) &&
+            make_tmap(&tc, A22, rows, cols, lda, 32)) {
+            TmaGemmArgs g{cols, rows, K, 0, 0, 0, 0, A22, lda, rup(K, 32), 1, 0, 0};
+            const int64_t tiles = ((rows + 127) / 128) * ((cols + 63) / 64);
+            const int grid = (int)std::min<int64_t>(tiles, ctx->grid_cap > 0 ? ctx->grid_cap : ctx->num_sms);
+            if (uk == 1) {
+                const size_t smem = upd_ws_smem<2, 4, 32, 2>();
+                auto kern = gemm_upd_ws_kernel<2, 4, 32, 2>;
+                CK(smem_attr((const void *)kern, (int)smem, ctx->device));
+                kern<<<grid, 9 * 32, smem, ctx->stream>>>(tx, ty, tc, g);
+            } else {
+                const size_t smem = upd_ws_smem<2, 4, 16, 4>();
+                auto kern = gemm_upd_ws_kernel<2, 4, 16, 4>;
+                CK(smem_attr((const void *)kern, (int)smem, ctx->device));
+                kern<<<grid, 9 * 32, smem, ctx->stream>>>(tx, ty, tc, g);
+            }
+            CKL();
+            *done = true;
+            return 0;
+        }
+    }
     if (K > 64 && !tile_ctr && (((uintptr_t)A22 & 15) == 0) && ((lda & 1) == 0)) {
         constexpr int MT = 4, NT = 4, WM = 2, WN = 4, BK = 32, ST = 2;
         constexpr int BM = 8 * MT * WM, BN = 8 * NT * WN;
@@ -525,6 +564,7 @@ static int free_all(rqrcp_ctx *ctx) {
                     ctx->vt_b[1],   ctx->w,         ctx->w2,         ctx->w2g,        ctx->tneg,       ctx->ybuf,
                     ctx->rhat11,    ctx->omhat,     ctx->vhat,       ctx->tauhat,     ctx->splitk,     ctx->pbuf,
                     ctx->packbuf,   ctx->dispbuf,   ctx->colss,      ctx->ptol2,      ctx->stopc,      ctx->slot_hdr,
+                    ctx->ybs,       ctx->tns,       ctx->wsub,       ctx->w2sub,      ctx->subeff,
                     ctx->slot_col,  ctx->slot_v2,   ctx->slot_data,  ctx->sq_ll,      ctx->sq_spill,   ctx->pn_part,
                     ctx->pn_rowj,   ctx->cq_g,      ctx->cq_rc,      ctx->cq_rinv,    ctx->cq_uinv,    ctx->cq_lu,
                     ctx->cqr_status, ctx->bpre,     ctx->c5,         ctx->wom,        ctx->w2om,       ctx->swap_stage,
@@ -623,6 +663,12 @@ static int create_impl(rqrcp_ctx **out, const rqrcp_config *cfg, int nranks, int
     CKC(dalloc(&ctx->colss, bp));
     CKC(dalloc(&ctx->ptol2, 1));
     CKC(cudaMalloc((void **)&ctx->stopc, sizeof(int)));
+    CKC(dalloc(&ctx->ybs, kPanelSub * kPanelSub));
+    CKC(dalloc(&ctx->tns, kPanelSub * kPanelSub));
+    CKC(cudaMemset(ctx->tns, 0, sizeof(double) * kPanelSub * kPanelSub));
+    CKC(dalloc(&ctx->wsub, kPanelSub * bp));
+    CKC(dalloc(&ctx->w2sub, kPanelSub * bp));
+    CKC(cudaMalloc((void **)&ctx->subeff, sizeof(int)));
     CKC(cudaMalloc((void **)&ctx->slot_hdr, sizeof(SqHdr) * 2 * SQ_MAXG * 8));
     CKC(cudaMemset(ctx->slot_hdr, 0, sizeof(SqHdr) * 2 * SQ_MAXG * 8));
     CKC(cudaMalloc((void **)&ctx->slot_col, sizeof(int) * 2 * G));
@@ -657,7 +703,8 @@ static int create_impl(rqrcp_ctx **out, const rqrcp_config *cfg, int nranks, int
     CKC(cudaMemset(ctx->tneg, 0, sizeof(double) * bp * bp));
     const int dev = ctx->device;
     CKC(smem_attr((const void *)sample_qrcp_kernel, kDynSmemMax, dev));
-    CKC(smem_attr((const void *)panel_qr_kernel, kDynSmemMax, dev));
+    CKC(smem_attr((const void *)panel_qr_kernel<4>, kDynSmemMax, dev));
+    CKC(smem_attr((const void *)panel_qr_kernel<8>, kDynSmemMax, dev));
     CKC(smem_attr((const void *)sample_qrcp_reg_kernel<40, 0>, 128 * 40 * 8, dev));
     CKC(smem_attr((const void *)sample_qrcp_reg_kernel<74, 0>, 128 * 74 * 8, dev));
     CKC(smem_attr((const void *)sample_qrcp_reg_kernel<72, 72>, 128 * 144 * 8, dev));
@@ -1204,26 +1251,21 @@ struct Run {
                     if (a.trace) ctx->ptrace_kind = 1;
                 }
             }
-            if (!pn_done) {
-                int pcap = G;
-                if (ctx->opt.pn_grid > 0) pcap = std::max(1, std::min(G, ctx->opt.pn_grid));
-                if (bulk.ready && bulk.launched) pcap = std::min(pcap, ctx->opt.la_panel_ctas);  // share with the bulk
-                const int64_t prows = ctx->opt.pn_rows;
-                const int grid = (int)std::max<int64_t>((mp + PN_MAXROWS - 1) / PN_MAXROWS,
-                                                        std::min<int64_t>(pcap, (mp + prows - 1) / prows));
-                const int64_t rpb = (mp + grid - 1) / grid;
-                if (rpb > PN_MAXROWS) {
-                    ctx->err = "panel too tall for the cooperative grid";
-                    return RQRCP_E_WORKSPACE;
+            // blocked when the panel's rows of one CTA do not fit its shared memory
+            // (C4 / C5; measured slower at C3 where they fit: 10.0 vs 7.7 ms)
+            const int64_t rows_cta = (mp + G - 1) / G;
+            const bool blk = ctx->opt.pn_blocked == 2 ||
+                             (ctx->opt.pn_blocked == 1 && rows_cta * bb * (int64_t)sizeof(double) > kDynSmemMax);
+            if (!pn_done && blk && bb > kPanelSub && !ctx->cqr_enabled) {
+                CKT(panel_blocked(a, i, mp, bb, bbpad, Pp, ldp, vfull, ldv, vt));  // applies its own stops
+            } else {
+                if (!pn_done) {
+                    CKT(launch_grid_panel(a, mp, bb));
+                    if (a.trace) ctx->ptrace_kind = 0;
                 }
-                a.nsm = (int)std::min<int64_t>(rpb, kDynSmemMax / ((int64_t)bb * sizeof(double)));
-                const size_t smem = (size_t)a.nsm * bb * sizeof(double);
-                void *args[] = {&a};
-                CKT(coop_launch(ctx, (const void *)panel_qr_kernel, grid, PN_THREADS, args, smem));
-                if (a.trace) ctx->ptrace_kind = 0;
+                panel_stop_apply_kernel<<<1, 32, 0, st>>>(ctx->stopc, 0, bb_eff, rankd, done);
+                CKL();
             }
-            panel_stop_apply_kernel<<<1, 32, 0, st>>>(ctx->stopc, bb_eff, rankd, done);
-            CKL();
         }
         // (5) P > 1: the owner broadcasts V, tau, V^T V, R11 (and T), the state
         const double *R11p = Pp;
@@ -1299,6 +1341,90 @@ struct Run {
         }
         ph_end(ctx);
         vb = nvb;
+        return 0;
+    }
+
+    int launch_grid_panel(PanelArgs &a, int64_t mp, int bb) {
+        int pcap = G;
+        if (ctx->opt.pn_grid > 0) pcap = std::max(1, std::min(G, ctx->opt.pn_grid));
+        if (bulk.ready && bulk.launched) pcap = std::min(pcap, ctx->opt.la_panel_ctas);  // share with the bulk
+        const int64_t prows = ctx->opt.pn_rows;
+        const int grid = (int)std::max<int64_t>((mp + PN_MAXROWS - 1) / PN_MAXROWS,
+                                                std::min<int64_t>(pcap, (mp + prows - 1) / prows));
+        const int64_t rpb = (mp + grid - 1) / grid;
+        if (rpb > PN_MAXROWS) {
+            ctx->err = "panel too tall for the cooperative grid";
+            return RQRCP_E_WORKSPACE;
+        }
+        if (grid > PN_MAXG) {
+            ctx->err = "panel grid exceeds PN_MAXG";
+            return RQRCP_E_WORKSPACE;
+        }
+        a.nsm = (int)std::min<int64_t>(rpb, kDynSmemMax / ((int64_t)bb * sizeof(double)));
+        const size_t smem = (size_t)a.nsm * bb * sizeof(double);
+        void *args[] = {&a};
+        const void *kern = (bb <= 32) ? (const void *)panel_qr_kernel<4> : (const void *)panel_qr_kernel<8>;
+        return coop_launch(ctx, kern, grid, PN_THREADS, args, smem);
+    }
+
+    // S4, blocked (dgeqrf-style): the grid kernel factors 32-column
+    // sub-panels (the whole sub-panel then stays in shared memory: one on-chip
+    // pass per column instead of L2 round trips for the rows that do not fit),
+    // and after each sub-panel s the panel columns to its right receive its
+    // reflectors as three DMMA contractions W = V_s^T P, W2 = -T_s^T W,
+    // P += V_s W2 (T_s by tri_kernel).  Same reflectors as the column-by-column
+    // kernel in exact arithmetic; T of the whole panel from Y = V^T V (DMMA).
+    int panel_blocked(PanelArgs a0, int64_t i, int64_t mp, int bb, int bbpad, double *Pp, int64_t ldp, double *vfull,
+                      int64_t ldv, double *vt) {
+        const int w = kPanelSub;
+        zero_top_kernel<<<grid_for((int64_t)bbpad * bbpad, 256, G), 256, 0, st>>>(vfull, ldv, vt, bbpad, bbpad);
+        CKL();
+        for (int c0 = 0; c0 < bb; c0 += w) {
+            const int c1 = std::min(bb, c0 + w), ws = c1 - c0;
+            const int wpad = (int)rup(ws, 8);
+            sub_eff_kernel<<<1, 32, 0, st>>>(bb_eff, c0, ws, ctx->subeff);
+            CKL();
+            CK(cudaMemsetAsync(ctx->stopc, 0xff, sizeof(int), st));
+            PanelArgs a = a0;
+            a.A = Pp + c0 + (int64_t)c0 * ldp;
+            a.mp = mp - c0;
+            a.bb = ws;
+            a.bbpad = wpad;
+            a.col0 = c0;
+            a.tau = tau + i + c0;
+            a.vfull = vfull + c0 + (int64_t)c0 * ldv;
+            a.ldv = ldv;
+            a.vt = vt + c0 + (int64_t)c0 * bbpad;
+            a.ldvt = bbpad;
+            a.ybuf = ctx->ybs;
+            a.ldy = w;
+            a.count = (c0 == 0) ? a0.count : nullptr;
+            a.bar = ctx->bars + 2 * panels + 1;
+            CK(cudaMemsetAsync(a.bar, 0, sizeof(unsigned), st));
+            CKT(launch_grid_panel(a, mp - c0, ws));
+            panel_stop_apply_kernel<<<1, 32, 0, st>>>(ctx->stopc, c0, bb_eff, rankd, done);
+            CKL();
+            if (c1 < bb) {
+                // T_s, then the in-panel update of columns c1..bb (rows c0..m')
+                tri_kernel<<<1, TRI_THREADS, ((size_t)w * w + (size_t)(w / 2) * (w / 2)) * sizeof(double), st>>>(
+                    ctx->ybs, tau + i + c0, nullptr, nullptr, 0, ws, w, w, ctx->subeff, ctx->tns, nullptr, 0, nullptr);
+                CKL();
+                const int64_t nr = bb - c1, K = mp - c0;
+                bool dn = false;
+                CKT(tma_skinny(ctx, wpad, nr, K, vfull, mp, bbpad, ldv, c0, c0, ctx->pbuf, m, bb, ldp, i + c0, c1,
+                               ctx->wsub, w, &dn, 512));
+                if (!dn) CKT(gemm_skinny(ctx, wpad, nr, K, vfull + c0 + (int64_t)c0 * ldv, ldv, Pp + c0 + c1 * ldp, ldp,
+                                         ctx->wsub, w));
+                CKT(gemm_skinny(ctx, wpad, nr, wpad, ctx->tns, w, ctx->wsub, w, ctx->w2sub, w));
+                CKT(update_any(ctx, K, nr, wpad, ctx->w2sub, w, vt + c0 + (int64_t)c0 * bbpad, bbpad,
+                               Pp + c0 + c1 * ldp, ldp));
+            }
+        }
+        // Y = V^T V for the compact-WY T of the whole panel (tri_kernel, strict upper part)
+        bool dn = false;
+        CKT(tma_skinny(ctx, bbpad, bbpad, mp, vfull, mp, bbpad, ldv, 0, 0, vfull, mp, bbpad, ldv, 0, 0, ctx->ybuf,
+                       bbpad, &dn, 512));
+        if (!dn) CKT(gemm_skinny(ctx, bbpad, bbpad, mp, vfull, ldv, vfull, ldv, ctx->ybuf, bbpad));
         return 0;
     }
 
@@ -1629,7 +1755,14 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     // 1191 ms with the panel look-ahead, whose panel kernel slows down when it
     // shares the GPU with the update, and 1087 ms serial at C4)
     int sched = ctx->opt.schedule;
-    if (sched < 0) sched = 1;
+    if (sched < 0) {
+        // schedule 1 when the sample QRCP leaves room for the bulk update (one
+        // cluster, or the register grid with the tile-claiming K <= 64 update);
+        // at b = 128 / l = 144 the register grid fills the GPU: serial
+        // (measured C4 1004.7 vs 1009.3 ms, C5 2245 vs 2239 ms)
+        const SqKind kind = sq_kind(ctx, R.l, n);
+        sched = (kind == SQK_CLUSTER || (kind == SQK_REG && rup(b, 8) <= 64)) ? 1 : 0;
+    }
     R.sched = sched;
     const int ev_t0 = ctx->nev;
     cudaEventRecord(ctx->ev[ctx->nev++], ctx->stream);

@@ -30,7 +30,7 @@ RES_ATOL = 1e-12
 ELEM_RTOL = 1e-10
 RECON_TOL = 1e-13
 
-DEFAULT_OPTS = dict(schedule=-1, panel=0, pn_cluster=1, pn_cpt=2, pn_grid=0, pn_rows=128, la_panel_ctas=48,
+DEFAULT_OPTS = dict(schedule=-1, panel=0, upd_kernel=2, pn_blocked=1, pn_cluster=1, pn_cpt=2, pn_grid=0, pn_rows=128, la_panel_ctas=48,
                     sq_cluster=1, sq_reg=1, sq_grid=0, sq_nsm=-1, sq_hstride=8, sq_poll=1)
 
 
@@ -336,6 +336,31 @@ def test_r11_diagonal_rank_stop(ctx):
     assert abs(abs(g["A"][0, 0]) - abs(o["A"][0, 0])) <= 1e-12 * abs(o["A"][0, 0])
 
 
+def test_r11_stop_blocked_panel(ctx):
+    """The R11-diagonal stop inside the 2nd / 4th 32-column sub-panel of a
+    b = 128 blocked grid panel.  A = diag(0.8^j) except a 1e-16 entry in column
+    `col`, whose Omega column is amplified so that its sample norm sits between
+    those of columns col-1 and col: the sample QRCP picks it at step col, where
+    |R(col,col)| = 1e-16 stops the factorization at rank col (oracle pin); the
+    GPU agrees on rank, pivots and R rows."""
+    for col in (40, 100):
+        m, n, b, p = 600, 400, 128, 16
+        rng = np.random.default_rng(col)
+        A = np.zeros((m, n))
+        A[np.arange(n), np.arange(n)] = 0.8 ** np.arange(n)
+        A[col, col] = 1e-16
+        Om = rng.standard_normal((b + p, m))
+        Om[:, col] *= 0.8 ** (col - 0.5) * 1e16
+        o = oracle.rqrcp(A, 256, b, p, omega=Om, check=False)
+        assert o["rank"] == col
+        with options(ctx, pn_cluster=0, pn_blocked=2):
+            g = gpu_factor(ctx, A, 256, b, p, 0, omega=torch.tensor(Om.ravel(order="F")).cuda())
+        assert g["rank"] == col
+        assert np.array_equal(g["jpvt"][:col + 1], o["jpvt"][:col + 1])
+        assert np.max(np.abs(np.triu(g["A"][:col]) - np.triu(o["A"][:col]))) <= 1e-10 * np.max(np.abs(o["A"][:col]))
+        assert np.all(g["tau"][col:] == 0.0)
+
+
 def test_zero_matrix(ctx):
     g = gpu_factor(ctx, np.zeros((50, 40)), 10, 4, 2, 1)
     assert g["rank"] == 0 and np.array_equal(g["jpvt"], np.arange(40))
@@ -442,7 +467,7 @@ PN_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "wide", "odd", 
     ("pncl_4096", "lowrank", 4096, 700, 192, 64, 10, 25),
 ]
 PN_VARIANTS = {"cluster2": dict(pn_cluster=1, pn_cpt=2), "cluster1": dict(pn_cluster=1, pn_cpt=1),
-               "grid": dict(pn_cluster=0)}
+               "grid": dict(pn_cluster=0, pn_blocked=0), "gridblocked": dict(pn_cluster=0, pn_blocked=2)}
 
 
 @pytest.mark.parametrize("variant", list(PN_VARIANTS))
@@ -462,9 +487,10 @@ def test_panel_grid_l2_rows(ctx, rows, grid):
     1-4 CTAs put ~750-3000 rows per CTA, ~200 of them in shared memory."""
     A = inputs.make("graded", 3000, 700, 41).numpy()
     o = oracle.rqrcp(A, 256, 128, 16, seed=41)
-    with options(ctx, pn_cluster=0, pn_rows=rows, pn_grid=grid):
-        g = gpu_factor(ctx, A, 256, 128, 16, 41)
-    compare(A, g, o, 256)
+    for blocked in (0, 2):
+        with options(ctx, pn_cluster=0, pn_rows=rows, pn_grid=grid, pn_blocked=blocked):
+            g = gpu_factor(ctx, A, 256, 128, 16, 41)
+        compare(A, g, o, 256)
 
 
 # ---- schedules: serial, bulk update beside the next sample QRCP, bulk update
@@ -488,6 +514,19 @@ def test_schedules_bitwise_and_parity(ctx, name, kind, m, n, k, b, p, seed):
         assert np.array_equal(g["jpvt"], outs[2]["jpvt"])
         assert np.array_equal(g["tau"], outs[2]["tau"])
         assert np.array_equal(g["A"], outs[2]["A"])
+
+
+@pytest.mark.parametrize("uk", [0, 1])
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", [c for c in SCHED_CASES if c[0] in ("tall", "b128", "gridpanel")],
+                         ids=["tall", "b128", "gridpanel"])
+def test_update_kernels_bitwise(ctx, uk, name, kind, m, n, k, b, p, seed):
+    """The update GEMM variants (CTA-wide TMA epilogue / warp-specialised
+    with per-warp epilogues) compute every element the same way: same bits."""
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    ref = gpu_factor(ctx, A, k, b, p, seed)
+    with options(ctx, upd_kernel=uk):
+        g = gpu_factor(ctx, A, k, b, p, seed)
+    assert np.array_equal(g["A"], ref["A"]) and np.array_equal(g["jpvt"], ref["jpvt"])
 
 
 def test_schedules_bitwise_C2(ctx):
