@@ -63,6 +63,10 @@ def lib():
                                        ctypes.c_int, ctypes.c_int, dp, i64, ctypes.POINTER(i64), dp,
                                        ctypes.POINTER(i64), vp, PANEL_CB, vp]
             L.oracle_rqrcp.restype = ctypes.c_int
+            L.oracle_rqrcp_tp.argtypes = [i64, i64, i64, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, vp,
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, i64, ctypes.POINTER(i64), dp,
+                                          ctypes.POINTER(i64), vp, PANEL_CB, vp]
+            L.oracle_rqrcp_tp.restype = ctypes.c_int
             L.oracle_set_threads.argtypes = [ctypes.c_int]
             L.oracle_set_threads.restype = ctypes.c_int
             _lib = L
@@ -142,12 +146,14 @@ class OracleError(RuntimeError):
 
 
 def rqrcp(A, k: int, b: int, p: int, seed: int = 0, omega=None, update_rule: int = 1,
-          invariant: bool = False, callback=None, check: bool = True):
+          invariant: bool = False, callback=None, check: bool = True, tournament: int = 0):
     """Alg. 2 on a copy of A.  Returns dict(A=factored (LAPACK layout),
     jpvt, tau, rank, gaps, status).
 
     callback(i, bb, l, mp, np_, Rhat, Bnext, OmegaCur, OmegaNew, A) receives
-    numpy copies per panel (tests only; see rqrcp_oracle.c)."""
+    numpy copies per panel (tests only; see rqrcp_oracle.c).
+    tournament = G > 1: the pivots of each panel from tournament pivoting on
+    the sample over G block-cyclic column groups (rqrcp_oracle.c)."""
     Af = _f64f(A)
     m, n = Af.shape
     l = b + p
@@ -173,9 +179,9 @@ def rqrcp(A, k: int, b: int, p: int, seed: int = 0, omega=None, update_rule: int
 
     cbp = PANEL_CB(_cb) if callback is not None else PANEL_CB()
     flags = ORACLE_INVARIANT if invariant else 0
-    st = lib().oracle_rqrcp(m, n, k, b, p, seed, om.ctypes.data if om is not None else None, update_rule, flags,
-                            _dp(Af), max(m, 1), jpvt.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _dp(tau),
-                            ctypes.byref(rank), gaps.ctypes.data, cbp, None)
+    st = lib().oracle_rqrcp_tp(m, n, k, b, p, seed, om.ctypes.data if om is not None else None, update_rule, flags,
+                               int(tournament), _dp(Af), max(m, 1), jpvt.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                               _dp(tau), ctypes.byref(rank), gaps.ctypes.data, cbp, None)
     if check and st != 0:
         raise OracleError(f"oracle_rqrcp returned {st}")
     return dict(A=Af, jpvt=jpvt, tau=tau[:k], rank=int(rank.value), gaps=gaps[:k], status=st)

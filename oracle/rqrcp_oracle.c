@@ -223,6 +223,109 @@ done:
     return steps;
 }
 
+/* ------------------------------------------------------------------------
+ * Tournament pivoting on the sample (the paper's future work: "the
+ * partial QRCP on B ... tournament pivoting"; reading R-TP of DESIGN.md).
+ * The np trailing positions of the panel are split into `groups` groups by
+ * the 1D block-cyclic layout (position c belongs to group ((i + c) / b) mod
+ * groups: the columns a rank of that layout owns).  Each group selects up to
+ * bb candidates by Alg. 1 (the function above: same norm rules, tie rule and
+ * stop rule) on ITS columns of the sample; the candidate lists are then merged
+ * pairwise up a binary tree (group g with g + span, span = 1, 2, 4, ...): the
+ * union (left list, then right list) of original sample columns is reduced
+ * to bb candidates by Alg. 1 again.  The root's pivot order is the panel's
+ * pivot order.  F (out): the chosen positions; returns their number (or -1
+ * on a non-finite norm).  With groups = 1 this is exactly Alg. 1's pivots.
+ * ---------------------------------------------------------------------- */
+static int64_t oracle_tournament(int64_t l, int64_t np, int64_t bb, const double *B, int64_t ldb, int64_t i, int b,
+                                 int groups, double stop_tol2, int64_t *F)
+{
+    int64_t **cand = (int64_t **)calloc((size_t)groups, sizeof(int64_t *));
+    int64_t *nc = (int64_t *)calloc((size_t)groups, sizeof(int64_t));
+    int64_t *idx = (int64_t *)malloc(sizeof(int64_t) * (size_t)(np > 2 * bb ? np : 2 * bb));
+    double *W = (double *)malloc(sizeof(double) * (size_t)(l * (np > 2 * bb ? np : 2 * bb)));
+    int64_t *pv = (int64_t *)malloc(sizeof(int64_t) * (size_t)(bb > 0 ? bb : 1));
+    double *th = (double *)malloc(sizeof(double) * (size_t)(bb > 0 ? bb : 1));
+    int64_t ret = 0;
+    /* local selections */
+    for (int g = 0; g < groups; ++g) {
+        int64_t n_g = 0;
+        for (int64_t c = 0; c < np; ++c)
+            if (((i + c) / b) % groups == g) {
+                idx[n_g] = c;
+                memcpy(&W[n_g * l], &B[c * ldb], sizeof(double) * (size_t)l);
+                ++n_g;
+            }
+        cand[g] = (int64_t *)malloc(sizeof(int64_t) * (size_t)(bb > 0 ? bb : 1));
+        const int64_t want = bb < n_g ? bb : n_g;
+        const int64_t got = want > 0 ? oracle_sample_qrcp(l, n_g, want, W, l, pv, th, stop_tol2, NULL) : 0;
+        if (got < 0) { ret = -1; goto out; }
+        for (int64_t j = 0; j < got; ++j) {  /* the transpositions, in order, on the index list */
+            const int64_t s_ = pv[j], t = idx[j];
+            idx[j] = idx[s_];
+            idx[s_] = t;
+        }
+        for (int64_t j = 0; j < got; ++j) cand[g][j] = idx[j];
+        nc[g] = got;
+    }
+    /* the merge tree */
+    for (int span = 1; span < groups; span *= 2)
+        for (int g = 0; g + span < groups; g += 2 * span) {
+            const int h = g + span;
+            int64_t nu = 0;
+            for (int64_t q = 0; q < nc[g]; ++q) idx[nu++] = cand[g][q];
+            for (int64_t q = 0; q < nc[h]; ++q) idx[nu++] = cand[h][q];
+            for (int64_t q = 0; q < nu; ++q) memcpy(&W[q * l], &B[idx[q] * ldb], sizeof(double) * (size_t)l);
+            const int64_t want = bb < nu ? bb : nu;
+            const int64_t got = want > 0 ? oracle_sample_qrcp(l, nu, want, W, l, pv, th, stop_tol2, NULL) : 0;
+            if (got < 0) { ret = -1; goto out; }
+            for (int64_t j = 0; j < got; ++j) {
+                const int64_t s_ = pv[j], t = idx[j];
+                idx[j] = idx[s_];
+                idx[s_] = t;
+            }
+            for (int64_t j = 0; j < got; ++j) cand[g][j] = idx[j];
+            nc[g] = got;
+        }
+    for (int64_t j = 0; j < nc[0]; ++j) F[j] = cand[0][j];
+    ret = nc[0];
+out:
+    for (int g = 0; g < groups; ++g) free(cand[g]);
+    free(cand); free(nc); free(idx); free(W); free(pv); free(th);
+    return ret;
+}
+
+/* The sample with given pivots (positions F[0..nsel), in order): the
+ * transpositions j <-> current position of F[j] applied to Bw (piv[j] records
+ * them, as Alg. 1 does), then the Householder QR of the first nsel columns,
+ * each H_j applied to every column right of j: R-hat = Q-hat^T B Pi. */
+static void oracle_sample_qr_given(int64_t l, int64_t nn, int64_t nsel, double *Bw, int64_t ldb, const int64_t *F,
+                                   int64_t *piv, double *tauhat)
+{
+    int64_t *where = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nn > 0 ? nn : 1));
+    int64_t *arr = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nn > 0 ? nn : 1));
+    for (int64_t c = 0; c < nn; ++c) { where[c] = c; arr[c] = c; }
+    for (int64_t j = 0; j < nsel; ++j) {
+        const int64_t s_ = where[F[j]];
+        piv[j] = s_;
+        if (s_ != j) {
+            swap_cols(l, Bw, ldb, j, s_);
+            const int64_t a_ = arr[j], b_ = arr[s_];
+            arr[j] = b_; arr[s_] = a_;
+            where[b_] = j; where[a_] = s_;
+        }
+    }
+    for (int64_t j = 0; j < nsel; ++j) {
+        double *x = &COL(Bw, ldb, j, j);
+        const double t = oracle_dlarfg(l - j, x);
+        tauhat[j] = t;
+#pragma omp parallel for schedule(static)
+        for (int64_t s_ = j + 1; s_ < nn; ++s_) oracle_apply_reflector(l - j, x + 1, t, &COL(Bw, ldb, j, s_));
+    }
+    free(where);
+    free(arr);
+}
+
 /* Optional per-panel snapshot callback (tests only).  Pointers are valid only
  * during the call.  Rhat: l x n' (ld l), the sample after the bb-step QRCP in
  * pivoted column order, zero below the diagonal of its first bb columns.
@@ -247,9 +350,23 @@ typedef void (*oracle_panel_cb)(void *user, int64_t i, int64_t bb, int64_t l, in
  *   jpvt[n]: A Pi(:, j) = A(:, jpvt[j]), 0-based.  tau[k].  *rank_out.
  *   gaps[k] (optional): per-step relative pivot gap.
  * ---------------------------------------------------------------------- */
+int oracle_rqrcp_tp(int64_t m, int64_t n, int64_t k, int b, int p, uint64_t seed, const double *Omega_in,
+                    int update_rule, int flags, int tp_groups, double *A, int64_t lda, int64_t *jpvt, double *tau,
+                    int64_t *rank_out, double *gaps, oracle_panel_cb cb, void *user);
+
 int oracle_rqrcp(int64_t m, int64_t n, int64_t k, int b, int p, uint64_t seed, const double *Omega_in,
                  int update_rule, int flags, double *A, int64_t lda, int64_t *jpvt, double *tau,
                  int64_t *rank_out, double *gaps, oracle_panel_cb cb, void *user)
+{
+    return oracle_rqrcp_tp(m, n, k, b, p, seed, Omega_in, update_rule, flags, 0, A, lda, jpvt, tau, rank_out, gaps,
+                           cb, user);
+}
+
+/* tp_groups > 1: the panel pivots come from tournament pivoting on the sample
+ * (oracle_tournament above) instead of Alg. 1; everything else is Alg. 2. */
+int oracle_rqrcp_tp(int64_t m, int64_t n, int64_t k, int b, int p, uint64_t seed, const double *Omega_in,
+                    int update_rule, int flags, int tp_groups, double *A, int64_t lda, int64_t *jpvt, double *tau,
+                    int64_t *rank_out, double *gaps, oracle_panel_cb cb, void *user)
 {
     if (!A) return -2;
     if (lda < (m > 1 ? m : 1)) return -3;
@@ -311,8 +428,16 @@ int oracle_rqrcp(int64_t m, int64_t n, int64_t k, int b, int p, uint64_t seed, c
         double *Bcur = B; /* l x np sample of the trailing columns, ld l */
         if (update_rule == 2) memcpy(Bpre, Bcur, sizeof(double) * (size_t)(l * np));
 
-        /* O3: partial QRCP on B(:, i:n) */
-        int64_t got = oracle_sample_qrcp(l, np, bb, Bcur, l, piv, tauhat, stop_tol2, gaps ? gaps + i : NULL);
+        /* O3: partial QRCP on B(:, i:n), or tournament pivoting */
+        int64_t got;
+        if (tp_groups > 1) {
+            int64_t *F = (int64_t *)malloc(sizeof(int64_t) * (size_t)(bb > 0 ? bb : 1));
+            got = oracle_tournament(l, np, bb, Bcur, l, i, b, tp_groups, stop_tol2, F);
+            if (got > 0) oracle_sample_qr_given(l, np, got, Bcur, l, F, piv, tauhat);
+            free(F);
+        } else {
+            got = oracle_sample_qrcp(l, np, bb, Bcur, l, piv, tauhat, stop_tol2, gaps ? gaps + i : NULL);
+        }
         if (got < 0) { status = 4; break; }
         if (got == 0) break; /* rank exhausted before this panel */
         bb = got;

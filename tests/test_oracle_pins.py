@@ -622,3 +622,106 @@ def test_householder_convention_matches_lapack():
     assert np.max(np.abs(np.triu(F[:90]) - np.triu(qr[:90]))) <= 1e-12 * np.max(np.abs(qr))
     assert np.max(np.abs(o["tau"] - tau[:90])) <= 1e-12
     assert np.max(np.abs(np.tril(F[:, :90], -1) - np.tril(qr[:, :90], -1))) <= 1e-12
+
+
+# ----------------------------------------------------------------------------
+# Tournament pivoting on the sample (reading R-TP): the oracle variant
+# ----------------------------------------------------------------------------
+def brute_force_tournament(B, i, b, groups, bb):
+    """The tournament of reading R-TP from its definition, with the
+    brute-force greedy selector (norms recomputed from scratch by a library
+    QR each step, brute_force_qrcp_pivots): groups by the block-cyclic layout,
+    local selections, pairwise merges up the tree (left list, then right list)."""
+    n = B.shape[1]
+    cand = []
+    for g in range(groups):
+        idx = [c for c in range(n) if ((i + c) // b) % groups == g]
+        sel = brute_force_qrcp_pivots(B[:, idx], min(bb, len(idx))) if idx else []
+        cand.append([idx[s] for s in sel])
+    span = 1
+    while span < groups:
+        for g in range(0, groups - span, 2 * span):
+            u = cand[g] + cand[g + span]
+            sel = brute_force_qrcp_pivots(B[:, u], min(bb, len(u))) if u else []
+            cand[g] = [u[s] for s in sel]
+        span *= 2
+    return cand[0]
+
+
+def test_tournament_one_group_is_alg1():
+    """One group: the tournament is Alg. 1 itself -- bitwise the same factorization."""
+    A = inputs.make("iid", 300, 280, 3).numpy()
+    o0 = oracle.rqrcp(A, 96, 32, 8, seed=4)
+    o1 = oracle.rqrcp(A, 96, 32, 8, seed=4, tournament=1)
+    assert np.array_equal(o0["A"], o1["A"]) and np.array_equal(o0["jpvt"], o1["jpvt"])
+
+
+@pytest.mark.parametrize("groups", [2, 3, 4, 7])
+def test_tournament_matches_brute_force(groups):
+    """The oracle's tournament (per panel, on the sample it sees) equals the
+    brute-force tournament of the definition on the same sample, for tiny
+    generic inputs (distinct residual norms); two panels."""
+    for seed in range(6):
+        rng = np.random.default_rng(700 + 10 * groups + seed)
+        m, n, b, p = 48, 40, 6, 4
+        A = rng.standard_normal((m, n)) * np.exp(-rng.permutation(n) / 8.0)
+        samples = []
+        res = oracle.rqrcp(A, 2 * b, b, p, seed=seed, tournament=groups, invariant=True,
+                           callback=lambda i, bb, l_, mp, np_, Rh, Bn, Oc, On, Af: samples.append((i, bb, Bn)))
+        # panel 0 works on the initial sample Omega A
+        B0 = oracle.sketch(oracle.omega(seed, b + p, m), A)
+        assert list(res["jpvt"][:b]) == brute_force_tournament(B0, 0, b, groups, b)
+        # panel 1 works on panel 0's updated sample, positions relative to column b
+        # of A Pi after panel 0 (whose order the one-panel run gives)
+        one = oracle.rqrcp(A, b, b, p, seed=seed, tournament=groups)
+        sel1 = brute_force_tournament(samples[0][2], b, b, groups, b)
+        assert list(res["jpvt"][b:2 * b]) == [int(one["jpvt"][b + c]) for c in sel1]
+
+
+@pytest.mark.parametrize("groups", [2, 3, 4, 8])
+def test_tournament_separated_equals_qrcp(groups):
+    """Orthogonal columns with norms in ratio 10 (ST-9): every local and merged
+    selection keeps the largest columns, so the tournament gives the QRCP
+    (dgeqp3) pivots and |R11| = diag(d sorted descending)."""
+    m, n, k, b, p = 60, 48, 16, 4, 4
+    for seed in range(10):
+        rng = np.random.default_rng(300 + seed)
+        d = 10.0 ** (-rng.permutation(n).astype(np.float64) / 2.0)
+        U, _ = np.linalg.qr(rng.standard_normal((m, n)))
+        A = U * d
+        res = oracle.rqrcp(A, k, b, p, seed=seed, tournament=groups)
+        _, _, P = sl.qr(A, pivoting=True)
+        assert np.array_equal(res["jpvt"][:k], P[:k])
+        assert np.allclose(np.abs(np.diag(res["A"])[:k]), np.sort(d)[::-1][:k], rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("groups", [2, 4])
+def test_tournament_invariants(groups):
+    """Whatever the pivots, Alg. 2's algebra holds: A Pi = Q R to 100 eps,
+    Q orthogonal, R-hat = the QR of the sample in the chosen order (up to row
+    signs), and the fresh-sketch invariant of Eq. (4)."""
+    rng = np.random.default_rng(77)
+    m, n, k, b, p = 140, 120, 48, 16, 8
+    A = rng.standard_normal((m, n)) * np.exp(-np.arange(n) / 25.0)
+    snaps = []
+    res = oracle.rqrcp(A, k, b, p, seed=6, tournament=groups, invariant=True,
+                       callback=lambda i, bb, l_, mp, np_, Rh, Bn, Oc, On, Af:
+                       snaps.append(dict(i=i, bb=bb, Rhat=Rh, Bnext=Bn, OmCur=Oc, OmNew=On, A=Af)))
+    Api = A[:, res["jpvt"]]
+    R = full_R(res, k)
+    assert np.linalg.norm(Api - oracle.apply_q(res["A"], res["tau"], R)) <= 100 * EPS * np.linalg.norm(A)
+    Q = oracle.apply_q(res["A"], res["tau"], np.eye(m))
+    assert np.linalg.norm(Q.T @ Q - np.eye(m)) <= 10 * m * EPS
+    # panel 0: R-hat11 = the R factor of the initial sample's chosen columns
+    B0 = oracle.sketch(oracle.omega(6, b + p, m), A)
+    Rl = np.linalg.qr(B0[:, res["jpvt"][:b]])[1]
+    assert np.max(np.abs(np.abs(snaps[0]["Rhat"][:b, :b]) - np.abs(Rl))) <= 1e-12 * np.abs(Rl).max()
+    for s in snaps:
+        i, bb = s["i"], s["bb"]
+        R22 = s["A"][i + bb:, i + bb:]
+        R12 = s["A"][i:i + bb, i + bb:]
+        pred = s["OmNew"][:, bb:] @ R22
+        scale = (np.linalg.norm(s["Rhat"][:bb, bb:]) + np.linalg.norm(s["Rhat"][bb:, bb:])
+                 + np.linalg.norm(s["OmNew"][:bb, :bb] @ R12))
+        if s["Bnext"] is not None:
+            assert np.linalg.norm(s["Bnext"] - pred) <= 1e-12 * scale
