@@ -176,6 +176,9 @@ int rqrcp_factor_ex(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n
  *   panel         0 column-by-column Householder, 1 CholeskyQR2 + reconstruction,
  *                 2 CholeskyQR2 from 8192 rows
  *   pn_cluster, pn_cpt, pn_grid, pn_rows, la_panel_ctas   panel kernel choice / shape
+ *   tournament    > 1: the panel pivots come from tournament pivoting on the sample over this
+ *                 many block-cyclic column groups (the paper's future work; DESIGN.md
+ *                 reading R-TP) instead of Alg. 1 on the whole sample; 0 / 1: Alg. 1
  *   upd_kernel    trailing-update GEMM: 0 CTA-wide TMA epilogue, 1 / 2 warp-specialised
  *                 (per-warp TMA epilogue; 32 x 2 / 16 x 4 k-stages)
  *   sq_cluster, sq_reg, sq_grid, sq_nsm, sq_hstride, sq_poll   sample QRCP kernel choice / shape

@@ -36,6 +36,7 @@
 #include "cqr.cuh"
 #include "dist.cuh"
 #include "transport.cuh"
+#include "tournament.cuh"
 #include "srqr.cuh"
 #include "lowrank.cuh"
 
@@ -50,6 +51,7 @@ struct Opts {
     int schedule = -1;       // -1 auto, 0 serial, 1 bulk || next sample QRCP, 2 bulk || next panel (look-ahead)
     int panel = 0;           // 0 Householder columns, 1 CholeskyQR2 + reconstruction, 2 CholeskyQR2 from 8192 rows
     int pn_cluster = 1, pn_cpt = 2, pn_grid = 0, pn_rows = 128, la_panel_ctas = 48;
+    int tournament = 0;      // > 1: tournament pivoting on the sample over this many column groups (reading R-TP)
     int pn_blocked = 1;      // grid panel on 32-column sub-panels + in-panel DMMA updates: 0 never, 1 when
                              // a CTA's rows do not fit shared memory, 2 always
     int upd_kernel = 2;      // update GEMM: 0 CTA-wide TMA epilogue, 1 / 2 warp-specialised (BK 32 x 2 / 16 x 4 stages)
@@ -67,7 +69,8 @@ static const OptDesc kOpts[] = {{"schedule", -1, 2},     {"panel", 0, 2},     {"
                                 {"sq_grid", 0, 4096},    {"sq_nsm", -1, 1 << 20}, {"sq_hstride", 1, 8},
                                 {"sq_poll", 0, 2},       {"debug_sync", 0, 1}, {"trace", 0, 1},
                                 {"trace_panel", 1, 1 << 30}, {"nccl_timeout_ms", 1, (int64_t)1 << 40},
-                                {"upd_kernel", 0, 2}, {"pn_blocked", 0, 2}};
+                                {"upd_kernel", 0, 2}, {"pn_blocked", 0, 2},
+                                {"tournament", 0, 64}};
 static bool opt_set(Opts &o, const std::string &n, int64_t v) {
 #define OPT(field)                    \
     if (n == #field) {                \
@@ -76,7 +79,7 @@ static bool opt_set(Opts &o, const std::string &n, int64_t v) {
     }
     OPT(schedule) OPT(panel) OPT(pn_cluster) OPT(pn_cpt) OPT(pn_grid) OPT(pn_rows) OPT(la_panel_ctas)
     OPT(sq_cluster) OPT(sq_reg) OPT(sq_grid) OPT(sq_nsm) OPT(sq_hstride) OPT(sq_poll) OPT(debug_sync) OPT(trace)
-    OPT(trace_panel) OPT(nccl_timeout_ms) OPT(upd_kernel) OPT(pn_blocked)
+    OPT(trace_panel) OPT(nccl_timeout_ms) OPT(upd_kernel) OPT(pn_blocked) OPT(tournament)
 #undef OPT
     return false;
 }
@@ -117,6 +120,13 @@ struct rqrcp_ctx {
     double *colss = nullptr, *ptol2 = nullptr;  // R11-diagonal stop scale
     double *ybs = nullptr, *tns = nullptr, *wsub = nullptr, *w2sub = nullptr;  // blocked panel scratch
     int *subeff = nullptr;
+    // tournament pivoting scratch (tournament.cuh)
+    int64_t *tp_cand = nullptr, *tp_perm = nullptr, *tp_idx = nullptr, *tp_piv = nullptr, *tp_sd = nullptr,
+            *tp_ss = nullptr;
+    int *tp_cnt = nullptr, *tp_ints = nullptr;
+    double *tp_w = nullptr, *tp_w2 = nullptr;  // W / W2 of the Q-hat^T application (S5's W2 may still be in use)
+    double *tp_u = nullptr, *tp_tau = nullptr, *tp_vhat = nullptr, *tp_r11 = nullptr, *tp_vt = nullptr, *tp_y = nullptr,
+           *tp_tn = nullptr;
     int *stopc = nullptr;      // panel kernels: the R11-diagonal stop column (-1: none)
     SqHdr *slot_hdr = nullptr;
     int *slot_col = nullptr;
@@ -194,7 +204,8 @@ static const char *g_static_err = "no context";
     } while (0)
 
 static constexpr int kDynSmemMax = 200 * 1024;
-static constexpr int kPanelSub = 32;  // blocked grid panel: sub-panel width (columns factored per kernel)
+static constexpr int kPanelSub = 32;
+static constexpr int kTpMaxGroups = 64;  // tournament pivoting: column groups  // blocked grid panel: sub-panel width (columns factored per kernel)
 static constexpr int64_t kCqrMinRows = 8192;
 
 static int grid_for(int64_t total, int threads, int num_sms) {
@@ -565,6 +576,9 @@ static int free_all(rqrcp_ctx *ctx) {
                     ctx->rhat11,    ctx->omhat,     ctx->vhat,       ctx->tauhat,     ctx->splitk,     ctx->pbuf,
                     ctx->packbuf,   ctx->dispbuf,   ctx->colss,      ctx->ptol2,      ctx->stopc,      ctx->slot_hdr,
                     ctx->ybs,       ctx->tns,       ctx->wsub,       ctx->w2sub,      ctx->subeff,
+                    ctx->tp_cand,   ctx->tp_perm,   ctx->tp_idx,     ctx->tp_piv,     ctx->tp_sd,      ctx->tp_ss,
+                    ctx->tp_cnt,    ctx->tp_ints,   ctx->tp_u,       ctx->tp_tau,     ctx->tp_vhat,    ctx->tp_r11,
+                    ctx->tp_vt,     ctx->tp_y,      ctx->tp_tn,      ctx->tp_w,       ctx->tp_w2,
                     ctx->slot_col,  ctx->slot_v2,   ctx->slot_data,  ctx->sq_ll,      ctx->sq_spill,   ctx->pn_part,
                     ctx->pn_rowj,   ctx->cq_g,      ctx->cq_rc,      ctx->cq_rinv,    ctx->cq_uinv,    ctx->cq_lu,
                     ctx->cqr_status, ctx->bpre,     ctx->c5,         ctx->wom,        ctx->w2om,       ctx->swap_stage,
@@ -669,6 +683,23 @@ static int create_impl(rqrcp_ctx **out, const rqrcp_config *cfg, int nranks, int
     CKC(dalloc(&ctx->wsub, kPanelSub * bp));
     CKC(dalloc(&ctx->w2sub, kPanelSub * bp));
     CKC(cudaMalloc((void **)&ctx->subeff, sizeof(int)));
+    CKC(cudaMalloc((void **)&ctx->tp_cand, sizeof(int64_t) * kTpMaxGroups * bp));
+    CKC(cudaMalloc((void **)&ctx->tp_perm, sizeof(int64_t) * std::max<int64_t>(nn, 2 * bp)));
+    CKC(cudaMalloc((void **)&ctx->tp_idx, sizeof(int64_t) * std::max<int64_t>(nn, 2 * bp)));
+    CKC(cudaMalloc((void **)&ctx->tp_piv, sizeof(int64_t) * bp));
+    CKC(cudaMalloc((void **)&ctx->tp_sd, sizeof(int64_t) * 4 * bp));
+    CKC(cudaMalloc((void **)&ctx->tp_ss, sizeof(int64_t) * 4 * bp));
+    CKC(cudaMalloc((void **)&ctx->tp_cnt, sizeof(int) * kTpMaxGroups));
+    CKC(cudaMalloc((void **)&ctx->tp_ints, sizeof(int) * 8));
+    CKC(dalloc(&ctx->tp_u, lp * 2 * bp));
+    CKC(dalloc(&ctx->tp_w, bp * nn));
+    CKC(dalloc(&ctx->tp_w2, bp * nn));
+    CKC(dalloc(&ctx->tp_tau, bp));
+    CKC(dalloc(&ctx->tp_vhat, lp * bp));
+    CKC(dalloc(&ctx->tp_r11, bp * bp));
+    CKC(dalloc(&ctx->tp_vt, bp * lp));
+    CKC(dalloc(&ctx->tp_y, bp * bp));
+    CKC(dalloc(&ctx->tp_tn, bp * bp));
     CKC(cudaMalloc((void **)&ctx->slot_hdr, sizeof(SqHdr) * 2 * SQ_MAXG * 8));
     CKC(cudaMemset(ctx->slot_hdr, 0, sizeof(SqHdr) * 2 * SQ_MAXG * 8));
     CKC(cudaMalloc((void **)&ctx->slot_col, sizeof(int) * 2 * G));
@@ -1034,26 +1065,17 @@ struct Run {
     bool more_after(int64_t i, int bb) const { return (i + bb < k) || keep_last; }
 
     // ---- S2 -------------------------------------------------------------
-    int sample_qrcp(int64_t i) {
-        const int bb = (int)std::min<int64_t>(b, k - i);
-        const int bbpad = (int)rup(bb, 8);
-        const int64_t np = n - i;
-        const bool rule5 = ctx->update_rule == 2 && more_after(i, bb) && np - bb > 0;
-        if (rule5)  // Eq. (5) needs B2 = the pre-QRCP sample (P:236-246)
-            CK(cudaMemcpyAsync(ctx->bpre, ctx->bs[cur], sizeof(double) * (size_t)lpad * (size_t)np,
-                               cudaMemcpyDeviceToDevice, st));
-        ph_begin(ctx, PH_SQRCP);
+    SqArgs sq_args(double *B, int64_t nn, int bb) {
         SqArgs a{};
-        a.B = ctx->bs[cur];
+        a.B = B;
         a.ldb = lpad;
         a.l = l;
         a.lpad = lpad;
-        a.nn = np;
+        a.nn = nn;
         a.bb = bb;
         a.stop_tol2 = ctx->stop_tol2;
         a.slot_hdr = ctx->slot_hdr;
         a.slot_col = ctx->slot_col;
-        a.tag0 = (++ctx->launch_seq) << 8;
         a.slot_v2 = ctx->slot_v2;
         a.slot_data = ctx->slot_data;
         a.ll = ctx->sq_ll;
@@ -1061,7 +1083,7 @@ struct Run {
         a.tauhat = ctx->tauhat;
         a.vhat = ctx->vhat;
         a.rhat11 = ctx->rhat11;
-        a.bbpad = bbpad;
+        a.bbpad = (int)rup(bb, 8);
         a.perm = ctx->perm;
         a.bb_eff = bb_eff;
         a.done = done;
@@ -1071,43 +1093,69 @@ struct Run {
         a.swap_dst = ctx->swap_dst;
         a.swap_src = ctx->swap_src;
         a.swap_np = ctx->swap_np;
-        a.trace = (panels + 1 == ctx->opt.trace_panel) ? ctx->trace : nullptr;
+        a.trace = nullptr;
         a.spill = ctx->sq_spill;
+        return a;
+    }
+    // one sample QRCP launch (bb steps of Alg. 1 on the nn columns of a.B),
+    // the kernel chosen from the table by (l, nn)
+    int launch_sq(SqArgs a) {
+        const int64_t np = a.nn;
+        const int bb = a.bb;
+        a.tag0 = (++ctx->launch_seq) << 8;
         const SqKind kind = sq_kind(ctx, l, np);
         const SqKernels kt = sq_kernels(l);
         if (kind == SQK_CLUSTER) {
             const int cs = (int)std::max<int64_t>(1, (np + SQC_THREADS - 1) / SQC_THREADS);
-            CKT(cluster_launch(ctx, kt.cluster, cs, SQC_THREADS, (size_t)bb * l * sizeof(double), a));
-        } else if (kind == SQK_REG) {
+            return cluster_launch(ctx, kt.cluster, cs, SQC_THREADS, (size_t)bb * l * sizeof(double), a);
+        }
+        if (kind == SQK_REG) {
             const int grid = 1 + (int)((np + SQR_THREADS - 1) / SQR_THREADS);
             const size_t smem = (size_t)std::max(kt.reg_ls * SQR_THREADS, bb * l) * sizeof(double);
             a.hstride = 8;
             void *args[] = {&a};
-            CKT(coop_launch(ctx, (const void *)kt.reg, grid, SQR_THREADS, args, smem));
+            return coop_launch(ctx, (const void *)kt.reg, grid, SQR_THREADS, args, smem);
+        }
+        a.hstride = ctx->opt.sq_hstride;
+        a.poll_mode = ctx->opt.sq_poll;
+        int gcap = std::min(G, SQ_MAXG);
+        if (ctx->opt.sq_grid > 0) gcap = std::max(1, std::min(gcap, ctx->opt.sq_grid));
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(gcap, (np + 7) / 8));
+        const int64_t cpb = (np + grid - 1) / grid;
+        int tpc = 32;
+        while (tpc > 1 && cpb * tpc > SQ_THREADS) tpc >>= 1;
+        a.tpc = tpc;
+        const int cpw = 32 / tpc;
+        auto pad_ncs = [&](int64_t x) -> int64_t {
+            if (cpw >= 16 || x <= 0) return std::max<int64_t>(x, 1);
+            return x + (((cpw - x) % 16) + 16) % 16;
+        };
+        const int64_t state = cpb * (2 * (int64_t)sizeof(double) + 2 * (int64_t)sizeof(int));
+        int64_t nsm = cpb;
+        if (ctx->opt.sq_nsm >= 0) nsm = std::max<int64_t>(0, std::min<int64_t>(nsm, ctx->opt.sq_nsm));
+        while (nsm > 0 && (int64_t)l * pad_ncs(nsm) * 8 + state > kDynSmemMax) --nsm;
+        a.nsm = (int)nsm;
+        a.ncs = (int)pad_ncs(nsm);
+        const size_t smem = sq_smem_bytes(a.ncs, cpb, l);
+        void *args[] = {&a};
+        return coop_launch(ctx, (const void *)sample_qrcp_kernel, grid, SQ_THREADS, args, smem);
+    }
+
+    int sample_qrcp(int64_t i) {
+        const int bb = (int)std::min<int64_t>(b, k - i);
+        const int bbpad = (int)rup(bb, 8);
+        const int64_t np = n - i;
+        const bool rule5 = ctx->update_rule == 2 && more_after(i, bb) && np - bb > 0;
+        if (rule5)  // Eq. (5) needs B2 = the pre-QRCP sample (P:236-246)
+            CK(cudaMemcpyAsync(ctx->bpre, ctx->bs[cur], sizeof(double) * (size_t)lpad * (size_t)np,
+                               cudaMemcpyDeviceToDevice, st));
+        ph_begin(ctx, PH_SQRCP);
+        if (ctx->opt.tournament > 1) {
+            CKT(tournament(i, bb, np));
         } else {
-            a.hstride = ctx->opt.sq_hstride;
-            a.poll_mode = ctx->opt.sq_poll;
-            int gcap = std::min(G, SQ_MAXG);
-            if (ctx->opt.sq_grid > 0) gcap = std::max(1, std::min(gcap, ctx->opt.sq_grid));
-            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(gcap, (np + 7) / 8));
-            const int64_t cpb = (np + grid - 1) / grid;
-            int tpc = 32;
-            while (tpc > 1 && cpb * tpc > SQ_THREADS) tpc >>= 1;
-            a.tpc = tpc;
-            const int cpw = 32 / tpc;
-            auto pad_ncs = [&](int64_t x) -> int64_t {
-                if (cpw >= 16 || x <= 0) return std::max<int64_t>(x, 1);
-                return x + (((cpw - x) % 16) + 16) % 16;
-            };
-            const int64_t state = cpb * (2 * (int64_t)sizeof(double) + 2 * (int64_t)sizeof(int));
-            int64_t nsm = cpb;
-            if (ctx->opt.sq_nsm >= 0) nsm = std::max<int64_t>(0, std::min<int64_t>(nsm, ctx->opt.sq_nsm));
-            while (nsm > 0 && (int64_t)l * pad_ncs(nsm) * 8 + state > kDynSmemMax) --nsm;
-            a.nsm = (int)nsm;
-            a.ncs = (int)pad_ncs(nsm);
-            const size_t smem = sq_smem_bytes(a.ncs, cpb, l);
-            void *args[] = {&a};
-            CKT(coop_launch(ctx, (const void *)sample_qrcp_kernel, grid, SQ_THREADS, args, smem));
+            SqArgs a = sq_args(ctx->bs[cur], np, bb);
+            a.trace = (panels + 1 == ctx->opt.trace_panel) ? ctx->trace : nullptr;
+            CKT(launch_sq(a));
         }
         ph_end(ctx);
         // trace: R-hat in pivoted order
@@ -1118,6 +1166,108 @@ struct Run {
                                                                                ctx->rhat11, bbpad, l, np, bb_eff, out);
             CKL();
         }
+        return 0;
+    }
+
+    // Tournament pivoting on the sample (reading R-TP; tournament.cuh)
+    int tournament(int64_t i, int bb, int64_t np) {
+        const int Gt = ctx->opt.tournament;
+        const int bbpad = (int)rup(bb, 8);
+        double *B = ctx->bs[cur];
+        int *ti = ctx->tp_ints;  // [0] bb_eff [1] done [2] rank of a scratch QRCP
+        // local selections: group g's columns gathered into the scratch sample
+        std::vector<int64_t> maxc(Gt, 0);
+        for (int g = 0; g < Gt; ++g) {
+            const int64_t lq0 = dist_count(i, b, Gt, g);
+            const int64_t ng = dist_count(n, b, Gt, g) - lq0;
+            int *cnt = ctx->tp_cnt + g;
+            int64_t *cand = ctx->tp_cand + (int64_t)g * bbpad;
+            if (ng <= 0) {
+                CK(cudaMemsetAsync(cnt, 0, sizeof(int), st));
+                continue;
+            }
+            const int bg = (int)std::min<int64_t>(bb, ng);
+            maxc[g] = bg;
+            tp_gather_group_kernel<<<grid_for(ng * lpad, 256, G), 256, 0, st>>>(B, lpad, lpad, i, b, Gt, g, lq0, ng,
+                                                                              ctx->c5, ctx->tp_idx);
+            CKL();
+            CK(cudaMemsetAsync(ti, 0, sizeof(int) * 3, st));
+            SqArgs a = sq_args(ctx->c5, ng, bg);
+            a.perm = ctx->tp_perm;
+            a.piv = ctx->tp_piv;
+            a.tauhat = ctx->tp_tau;
+            a.vhat = ctx->tp_vhat;
+            a.rhat11 = ctx->tp_r11;
+            a.bb_eff = ti;
+            a.done = ti + 1;
+            a.rank = ti + 2;
+            a.swap_dst = ctx->tp_sd;
+            a.swap_src = ctx->tp_ss;
+            a.swap_np = ti + 3;
+            CKT(launch_sq(a));
+            tp_collect_kernel<<<1, 128, 0, st>>>(ctx->tp_perm, ti, ctx->tp_idx, cand, cnt);
+            CKL();
+        }
+        // merges up the tree; the last one (into group 0) is the root.  The
+        // root's reflector buffer is cleared first: columns beyond its pivot
+        // count are multiplied by zero rows of W2 below and must be finite.
+        CK(cudaMemsetAsync(ctx->vhat, 0, sizeof(double) * (size_t)lpad * bbpad, st));
+        for (int span = 1; span < Gt; span *= 2)
+            for (int g = 0; g + span < Gt; g += 2 * span) {
+                const int h = g + span;
+                const bool root = (2 * span >= Gt);
+                const int nu = (int)(maxc[g] + maxc[h]);
+                const int bu = std::min(bb, std::max(nu, 1));
+                const int ncols = std::max(nu, 1);
+                tp_union_kernel<<<grid_for((int64_t)ncols * lpad, 256, G), 256, 0, st>>>(
+                    B, lpad, lpad, ctx->tp_cand + (int64_t)g * bbpad, ctx->tp_cnt + g, ctx->tp_cand + (int64_t)h * bbpad,
+                    ctx->tp_cnt + h, ncols, ctx->tp_u, ctx->tp_idx);
+                CKL();
+                CK(cudaMemsetAsync(ti, 0, sizeof(int) * 3, st));
+                SqArgs a = sq_args(ctx->tp_u, ncols, bu);
+                a.perm = ctx->tp_perm;
+                a.piv = ctx->tp_piv;
+                a.bb_eff = ti;
+                a.done = ti + 1;
+                a.rank = ti + 2;
+                a.swap_dst = ctx->tp_sd;
+                a.swap_src = ctx->tp_ss;
+                a.swap_np = ti + 3;
+                if (!root) {  // the root's reflectors / R-hat11 go to the panel's buffers
+                    a.tauhat = ctx->tp_tau;
+                    a.vhat = ctx->tp_vhat;
+                    a.rhat11 = ctx->tp_r11;
+                }
+                a.bbpad = bbpad;
+                CKT(launch_sq(a));
+                tp_collect_kernel<<<1, 128, 0, st>>>(ctx->tp_perm, ti, ctx->tp_idx, ctx->tp_cand + (int64_t)g * bbpad,
+                                                     ctx->tp_cnt + g);
+                CKL();
+                maxc[g] = std::min<int64_t>(bb, nu);
+            }
+        // R-hat = Q-hat^T B for every sample column: W = V-hat^T B, W2 = -T-hat^T W,
+        // B += V-hat W2 (V-hat, tau-hat: the root's reflectors = the QR of the
+        // chosen columns in pivot order)
+        tp_transpose_kernel<<<grid_for((int64_t)lpad * bbpad, 256, G), 256, 0, st>>>(ctx->vhat, lpad, bbpad, ctx->tp_vt);
+        CKL();
+        CKT(gemm_skinny(ctx, bbpad, bbpad, lpad, ctx->vhat, lpad, ctx->vhat, lpad, ctx->tp_y, bbpad));
+        {
+            int nb = 8;
+            while (nb < bbpad) nb *= 2;
+            const size_t smem = ((size_t)nb * nb + (size_t)(nb / 2) * (nb / 2)) * sizeof(double);
+            tri_kernel<<<1, TRI_THREADS, smem, st>>>(ctx->tp_y, ctx->tauhat, nullptr, nullptr, 0, bb, bbpad, nb,
+                                                     ctx->tp_cnt, ctx->tp_tn, nullptr, 0, nullptr);
+            CKL();
+        }
+        CKT(gemm_skinny(ctx, bbpad, np, lpad, ctx->vhat, lpad, B, lpad, ctx->tp_w, bbpad));
+        CKT(gemm_skinny(ctx, bbpad, np, bbpad, ctx->tp_tn, bbpad, ctx->tp_w, bbpad, ctx->tp_w2, bbpad));
+        CKT(update_any(ctx, lpad, np, bbpad, ctx->tp_w2, bbpad, ctx->tp_vt, bbpad, B, lpad));
+        // perm, moves and the panel state, as the S2 kernels leave them
+        tp_iota_kernel<<<grid_for(np, 256, G), 256, 0, st>>>(ctx->perm, np);
+        CKL();
+        tp_finish_kernel<<<1, 32, 0, st>>>(ctx->tp_cand, ctx->tp_cnt, bb, status, done, bb_eff, rankd, ctx->perm,
+                                           ctx->swap_dst, ctx->swap_src, ctx->swap_np);
+        CKL();
         return 0;
     }
 

@@ -108,3 +108,12 @@ def test_multirank_rank_deficient():
     g = run_group(A, 60, 16, 8, 1, 2)
     assert g["rank"] == o["rank"] == 25
     assert np.array_equal(g["jpvt"], o["jpvt"])
+
+
+def test_p_invariance_tournament():
+    """Tournament pivoting (replicated over the ranks' copies of the sample)
+    keeps the bitwise P-invariance."""
+    A = inputs.make("graded", 900, 1100, 17).numpy()
+    s = run_single(A, 256, 64, 10, 17, opts=dict(tournament=4))
+    g = run_group(A, 256, 64, 10, 17, 2, opts=dict(tournament=4))
+    assert_bitwise(g, s)

@@ -30,7 +30,7 @@ RES_ATOL = 1e-12
 ELEM_RTOL = 1e-10
 RECON_TOL = 1e-13
 
-DEFAULT_OPTS = dict(schedule=-1, panel=0, upd_kernel=2, pn_blocked=1, pn_cluster=1, pn_cpt=2, pn_grid=0, pn_rows=128, la_panel_ctas=48,
+DEFAULT_OPTS = dict(schedule=-1, panel=0, upd_kernel=2, pn_blocked=1, tournament=0, pn_cluster=1, pn_cpt=2, pn_grid=0, pn_rows=128, la_panel_ctas=48,
                     sq_cluster=1, sq_reg=1, sq_grid=0, sq_nsm=-1, sq_hstride=8, sq_poll=1)
 
 
@@ -686,3 +686,48 @@ def test_lowrank_outputs(ctx, name, kind, m, n, k, b, p, seed):
     assert np.linalg.norm(Xh - Xref) <= 1e-8 * np.linalg.norm(Xref)
     r22 = np.linalg.norm(F[k:, k:])
     assert abs(np.linalg.norm(A - C @ Xh) - r22) <= 1e-10 * np.linalg.norm(A)
+
+
+# ---- tournament pivoting on the sample (reading R-TP): the GPU
+#      variant (sample QRCP kernels on column groups + merges) vs the oracle's
+TP_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "lowrank", "b128", "odd", "wide")]
+
+
+@pytest.mark.parametrize("groups", [2, 3, 8])
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", TP_CASES, ids=[c[0] for c in TP_CASES])
+def test_tournament_parity(ctx, groups, name, kind, m, n, k, b, p, seed):
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    o = oracle.rqrcp(A, k, b, p, seed=seed, tournament=groups)
+    with options(ctx, tournament=groups):
+        g = gpu_factor(ctx, A, k, b, p, seed)
+    compare(A, g, o, k)
+
+
+def test_tournament_trace_and_C2(ctx):
+    """C2 at full size with 8 groups, with the per-panel trace (R-hat after the
+    tournament, B_next after Eq. (4)) against the oracle's callback."""
+    c = inputs.CONFIGS["C2"]
+    A = inputs.config_matrix("C2").numpy()
+    m, n, k, b, p = c["m"], c["n"], c["k"], c["b"], c["p"]
+    tr = ctx.make_trace(n, b, p, 0, k // b)
+    Ad = to_dev(A)
+    with options(ctx, tournament=8):
+        jpvt, tau, rank = ctx.factor(Ad, k, b, p, seed=c["seed"], trace=tr)
+    torch.cuda.synchronize()
+    panels = []
+    o = oracle.rqrcp(A, k, b, p, seed=c["seed"], tournament=8,
+                     callback=lambda i, bb, l_, mp, np_, Rh, Bn, Oc, On, Af: panels.append((i, bb, Rh, Bn)))
+    assert np.array_equal(jpvt.cpu().numpy(), o["jpvt"])
+    check_trace_panels(tr, panels, o["jpvt"])
+    g = dict(A=Ad.cpu().numpy(), jpvt=jpvt.cpu().numpy(), tau=tau.cpu().numpy(), rank=rank)
+    compare(A, g, o, k)
+
+
+def test_tournament_rank_deficient(ctx):
+    rng = np.random.default_rng(42)
+    A = rng.standard_normal((120, 25)) @ rng.standard_normal((25, 100))
+    o = oracle.rqrcp(A, 60, 16, 8, seed=1, tournament=4)
+    with options(ctx, tournament=4):
+        g = gpu_factor(ctx, A, 60, 16, 8, 1)
+    assert g["rank"] == o["rank"] == 25
+    assert np.array_equal(g["jpvt"][:25], o["jpvt"][:25])
