@@ -648,3 +648,135 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
 }
 
 }  // namespace rq
+
+namespace rq {
+
+// ---------------------------------------------------------------------------
+// C = X^T Y (skinny M: S1 sketch, S5 W = V^T A22), warp-specialised like
+// gemm_upd_ws_kernel: a producer warp streams the (tile, K-slice) stages by
+// TMA into a full / empty mbarrier ring, the consumer warps never meet at a
+// CTA-wide barrier, and each writes its own fragments at a tile's end
+// (EPI_STORE: C; EPI_PARTIAL: the split-K slice).  Same tiles, same K slices
+// and the same per-element DMMA order as gemm_tma_kernel: the same bits.
+// ---------------------------------------------------------------------------
+template <int MT, int NT, int WM, int WN, int BK, int ST>
+constexpr size_t ws_gemm_smem() {
+    return 128 + (size_t)ST * BK * (8 * MT * WM + 8 * NT * WN) * sizeof(double) + 2 * ST * sizeof(uint64_t);
+}
+
+template <int MT, int NT, int WM, int WN, int BK, int ST, int EPI>
+__global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
+    gemm_ws_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY, TmaGemmArgs g) {
+    constexpr int BM = 8 * MT * WM;
+    constexpr int BN = 8 * NT * WN;
+    constexpr int KB = BK / 8;
+    constexpr int XS = KB * BM * 8;
+    constexpr int YS = KB * BN * 8;
+    constexpr int NCW = WM * WN;
+    constexpr unsigned STAGE_BYTES = (unsigned)((XS + YS) * sizeof(double));
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const unsigned pad = (128u - (smem_u32(smem_raw) & 127u)) & 127u;
+    double *xs = reinterpret_cast<double *>(smem_raw + pad);
+    double *ys = xs + ST * XS;
+    uint64_t *full = reinterpret_cast<uint64_t *>(ys + ST * YS);
+    uint64_t *empty = full + ST;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t tilesN = (g.N + BN - 1) / BN, tilesM = (g.M + BM - 1) / BM;
+    const int64_t per = tilesN * tilesM;
+    const int64_t ntiles = per * g.splits;
+    if (tid == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    // tile t -> (split, m-tile, n-tile), n fastest (as gemm_tma_kernel)
+    auto tile_geom = [&](int64_t t, int &split, int64_t &m0, int64_t &n0, int64_t &kbeg, int &nk) {
+        split = (int)(t / per);
+        const int64_t r = t % per;
+        m0 = (r / tilesN) * BM;
+        n0 = (r % tilesN) * BN;
+        kbeg = (int64_t)split * g.k_per_split;
+        const int64_t kend = min(g.K, kbeg + g.k_per_split);
+        nk = (kend > kbeg) ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+    };
+    if (warp == NCW) {  // producer
+        if (lane != 0) return;
+        int64_t sp = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            int split, nk;
+            int64_t m0, n0, kbeg;
+            tile_geom(t, split, m0, n0, kbeg, nk);
+            for (int kc = 0; kc < nk; ++kc, ++sp) {
+                const int slot = (int)(sp % ST);
+                if (sp >= ST) mbar_wait(&empty[slot], (unsigned)(((sp / ST) - 1) & 1));
+                mbar_expect_tx(&full[slot], STAGE_BYTES);
+                const int64_t k0 = kbeg + (int64_t)kc * BK;
+#pragma unroll
+                for (int kb = 0; kb < KB; ++kb) {
+                    tma_load_2d(xs + slot * XS + kb * BM * 8, &tmX, (int)(g.xk0 + k0 + kb * 8), (int)(g.xm0 + m0), &full[slot]);
+                    tma_load_2d(ys + slot * YS + kb * BN * 8, &tmY, (int)(g.yk0 + k0 + kb * 8), (int)(g.yn0 + n0), &full[slot]);
+                }
+            }
+        }
+        return;
+    }
+    const int wm = warp / WN, wn = warp % WN;
+    const int fr = lane >> 2, fk = (lane & 3) * 2;
+    int64_t sc = 0;
+    double acc[MT][NT][2];
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int split, nk;
+        int64_t m0, n0, kbeg;
+        tile_geom(t, split, m0, n0, kbeg, nk);
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int kc = 0; kc < nk; ++kc, ++sc) {
+            const int slot = (int)(sc % ST);
+            mbar_wait(&full[slot], (unsigned)((sc / ST) & 1));
+            const double *xd = xs + slot * XS;
+            const double *yd = ys + slot * YS;
+#pragma unroll
+            for (int kb = 0; kb < KB; ++kb) {
+                double2 a[MT], b[NT];
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+                    a[i] = *reinterpret_cast<const double2 *>(xd + (kb * BM + wm * 8 * MT + i * 8 + fr) * 8 + fk);
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+                    b[j] = *reinterpret_cast<const double2 *>(yd + (kb * BN + wn * 8 * NT + j * 8 + fr) * 8 + fk);
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i].y, b[j].y);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+        }
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+            const int64_t gm = m0 + wm * 8 * MT + i * 8 + fr;
+            if (gm >= g.M) continue;
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int64_t gn = n0 + wn * 8 * NT + j * 8 + fk + h;
+                    if (gn >= g.N) continue;
+                    if (EPI == EPI_STORE) g.C[gm + gn * g.ldc] = acc[i][j][h];
+                    else g.C[(int64_t)split * g.split_stride + gm + gn * g.M] = acc[i][j][h];
+                }
+        }
+    }
+}
+
+}  // namespace rq

@@ -51,6 +51,7 @@ struct Opts {
     int schedule = -1;       // -1 auto, 0 serial, 1 bulk || next sample QRCP, 2 bulk || next panel (look-ahead)
     int panel = 0;           // 0 Householder columns, 1 CholeskyQR2 + reconstruction, 2 CholeskyQR2 from 8192 rows
     int pn_cluster = 1, pn_cpt = 2, pn_grid = 0, pn_rows = 128, la_panel_ctas = 48;
+    int gemm_ws = 1;         // skinny TMA GEMMs (sketch, W): 1 warp-specialised, 0 CTA-barrier ring
     int tournament = 0;      // > 1: tournament pivoting on the sample over this many column groups (reading R-TP)
     int pn_blocked = 1;      // grid panel on 32-column sub-panels + in-panel DMMA updates: 0 never, 1 when
                              // a CTA's rows do not fit shared memory, 2 always
@@ -70,7 +71,7 @@ static const OptDesc kOpts[] = {{"schedule", -1, 2},     {"panel", 0, 2},     {"
                                 {"sq_poll", 0, 2},       {"debug_sync", 0, 1}, {"trace", 0, 1},
                                 {"trace_panel", 1, 1 << 30}, {"nccl_timeout_ms", 1, (int64_t)1 << 40},
                                 {"upd_kernel", 0, 2}, {"pn_blocked", 0, 2},
-                                {"tournament", 0, 64}};
+                                {"tournament", 0, 64}, {"gemm_ws", 0, 1}};
 static bool opt_set(Opts &o, const std::string &n, int64_t v) {
 #define OPT(field)                    \
     if (n == #field) {                \
@@ -79,7 +80,7 @@ static bool opt_set(Opts &o, const std::string &n, int64_t v) {
     }
     OPT(schedule) OPT(panel) OPT(pn_cluster) OPT(pn_cpt) OPT(pn_grid) OPT(pn_rows) OPT(la_panel_ctas)
     OPT(sq_cluster) OPT(sq_reg) OPT(sq_grid) OPT(sq_nsm) OPT(sq_hstride) OPT(sq_poll) OPT(debug_sync) OPT(trace)
-    OPT(trace_panel) OPT(nccl_timeout_ms) OPT(upd_kernel) OPT(pn_blocked) OPT(tournament)
+    OPT(trace_panel) OPT(nccl_timeout_ms) OPT(upd_kernel) OPT(pn_blocked) OPT(tournament) OPT(gemm_ws)
 #undef OPT
     return false;
 }
@@ -352,11 +353,22 @@ static int launch_tma_cfg(rqrcp_ctx *ctx, const double *X, int64_t xdim0, int64_
     if ((g.xk0 | g.yk0) & 1) return 0;
     CUtensorMap tx, ty;
     if (!make_tmap(&tx, X, xdim0, xdim1, ldx, BM) || !make_tmap(&ty, Y, ydim0, ydim1, ldy, BN)) return 0;
+    const int64_t tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM) * g.splits;
+    const int grid = (int)std::min<int64_t>(tiles, ctx->grid_cap > 0 ? ctx->grid_cap : ctx->num_sms);
+    if (!DYN && (EPI == EPI_STORE || EPI == EPI_PARTIAL) && ctx->opt.gemm_ws) {
+        // warp-specialised variant (producer warp, no CTA-wide barrier): same bits
+        constexpr int WST = (4 * BK * (BM + BN) * 8 <= 200 * 1024) ? 4 : 3;
+        const size_t smem = ws_gemm_smem<MT, NT, WM, WN, BK, WST>();
+        auto kern = gemm_ws_kernel<MT, NT, WM, WN, BK, WST, EPI>;
+        CK(smem_attr((const void *)kern, (int)smem, ctx->device));
+        kern<<<grid, (WM * WN + 1) * 32, smem, ctx->stream>>>(tx, ty, g);
+        CKL();
+        *done = true;
+        return 0;
+    }
     const size_t smem = tma_gemm_smem<MT, NT, WM, WN, BK, ST>();
     auto kern = gemm_tma_kernel<MT, NT, WM, WN, BK, ST, EPI, DYN>;
     CK(smem_attr((const void *)kern, (int)smem, ctx->device));
-    const int64_t tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM) * g.splits;
-    const int grid = (int)std::min<int64_t>(tiles, ctx->grid_cap > 0 ? ctx->grid_cap : ctx->num_sms);
     kern<<<grid, WM * WN * 32, smem, ctx->stream>>>(tx, ty, g);
     CKL();
     *done = true;

@@ -30,7 +30,7 @@ RES_ATOL = 1e-12
 ELEM_RTOL = 1e-10
 RECON_TOL = 1e-13
 
-DEFAULT_OPTS = dict(schedule=-1, panel=0, upd_kernel=2, pn_blocked=1, tournament=0, pn_cluster=1, pn_cpt=2, pn_grid=0, pn_rows=128, la_panel_ctas=48,
+DEFAULT_OPTS = dict(schedule=-1, panel=0, upd_kernel=2, pn_blocked=1, tournament=0, gemm_ws=1, pn_cluster=1, pn_cpt=2, pn_grid=0, pn_rows=128, la_panel_ctas=48,
                     sq_cluster=1, sq_reg=1, sq_grid=0, sq_nsm=-1, sq_hstride=8, sq_poll=1)
 
 
@@ -525,6 +525,18 @@ def test_update_kernels_bitwise(ctx, uk, name, kind, m, n, k, b, p, seed):
     A = inputs.make(kind, m, n, seed, rank=64).numpy()
     ref = gpu_factor(ctx, A, k, b, p, seed)
     with options(ctx, upd_kernel=uk):
+        g = gpu_factor(ctx, A, k, b, p, seed)
+    assert np.array_equal(g["A"], ref["A"]) and np.array_equal(g["jpvt"], ref["jpvt"])
+
+
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", [c for c in SCHED_CASES if c[0] in ("tall", "b128", "grid74")],
+                         ids=["tall", "b128", "grid74"])
+def test_skinny_gemm_kernels_bitwise(ctx, name, kind, m, n, k, b, p, seed):
+    """The sketch / W = V^T A22 GEMM: warp-specialised vs CTA-barrier ring
+    kernels -- same tiles, same K slices, same bits."""
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    ref = gpu_factor(ctx, A, k, b, p, seed)
+    with options(ctx, gemm_ws=0):
         g = gpu_factor(ctx, A, k, b, p, seed)
     assert np.array_equal(g["A"], ref["A"]) and np.array_equal(g["jpvt"], ref["jpvt"])
 
