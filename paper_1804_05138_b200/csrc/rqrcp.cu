@@ -90,7 +90,9 @@ struct rqrcp_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // concurrent small kernels (tri_kernel)
     cudaStream_t upd = nullptr;   // the bulk trailing update (lowest priority)
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_r12 = nullptr, ev_upd = nullptr, ev_pack = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_r12 = nullptr, ev_upd = nullptr, ev_pack = nullptr,
+                ev_h2d = nullptr;
+    cudaStream_t cps = nullptr;   // host <-> device copies of the end-to-end path
     int grid_cap = 0;  // > 0: persistent GEMM grids use at most this many CTAs
     int *tctr = nullptr;  // per-panel tile counters of the dynamically scheduled bulk update
     bool own_stream = false;
@@ -606,8 +608,9 @@ static int free_all(rqrcp_ctx *ctx) {
 static void destroy_events(rqrcp_ctx *ctx) {
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
-    for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_join, ctx->ev_r12, ctx->ev_upd, ctx->ev_pack})
+    for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_join, ctx->ev_r12, ctx->ev_upd, ctx->ev_pack, ctx->ev_h2d})
         if (e) cudaEventDestroy(e);
+    if (ctx->cps) cudaStreamDestroy(ctx->cps);
     if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->upd) cudaStreamDestroy(ctx->upd);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -816,8 +819,9 @@ static int create_impl(rqrcp_ctx **out, const rqrcp_config *cfg, int nranks, int
     CKC(cudaStreamCreateWithPriority(&ctx->upd, cudaStreamNonBlocking, prio_lo));
     CKC(cudaMallocHost((void **)&ctx->hstatus, sizeof(int) * 8));
     CKC(cudaMalloc((void **)&ctx->tctr, sizeof(int) * 8192));
-    for (cudaEvent_t *e : {&ctx->ev_r12, &ctx->ev_upd, &ctx->ev_fork, &ctx->ev_join, &ctx->ev_pack})
+    for (cudaEvent_t *e : {&ctx->ev_r12, &ctx->ev_upd, &ctx->ev_fork, &ctx->ev_join, &ctx->ev_pack, &ctx->ev_h2d})
         CKC(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    CKC(cudaStreamCreateWithFlags(&ctx->cps, cudaStreamNonBlocking));
     for (auto &e : ctx->ev) CKC(cudaEventCreate(&e));
     if (nranks > 1) {
         CKC(dalloc(&ctx->gsend, lp * (nn + bp)));
@@ -1072,6 +1076,12 @@ struct Run {
     } bulk;
     int *status, *bb_eff, *done, *rankd;
     cudaStream_t st;
+    // end-to-end path (rqrcp_factor_host): A streamed in by column chunks that
+    // feed the sketch, finished panels streamed out while later panels run
+    const double *h_in = nullptr;
+    double *h_out = nullptr;
+    int64_t h_ld = 0;
+    cudaStream_t cps = nullptr;  // copy stream
 
     int64_t ldv_for(int64_t mp) const { return P > 1 ? rup(mp, 8) : ctx->ldo; }
     bool more_after(int64_t i, int bb) const { return (i + bb < k) || keep_last; }
@@ -1800,9 +1810,26 @@ struct Run {
         ph_begin(ctx, PH_SKETCH);
         bool tdone = false;
         double *bdst = (P == 1) ? ctx->bs[cur] : ctx->gsend;
-        CKT(tma_skinny(ctx, lpad, n_loc, m, ctx->omt, m, lpad, ctx->ldo, 0, 0, A, m, n_loc, lda, 0, 0, bdst, lpad, &tdone,
-                       512, n));
-        if (!tdone) CKT(gemm_skinny(ctx, lpad, n_loc, m, ctx->omt, ctx->ldo, A, lda, bdst, lpad, n));
+        if (h_in) {
+            // column chunks: H2D on the copy stream, each chunk's sketch on the
+            // main stream as soon as it has landed (same K slices: same bits)
+            const int64_t CH = 2048;
+            for (int64_t c0 = 0; c0 < n_loc; c0 += CH) {
+                const int64_t nc = std::min(CH, n_loc - c0);
+                CK(cudaMemcpy2DAsync(A + c0 * lda, sizeof(double) * lda, h_in + c0 * h_ld, sizeof(double) * h_ld,
+                                     sizeof(double) * m, nc, cudaMemcpyHostToDevice, cps));
+                CK(cudaEventRecord(ctx->ev_h2d, cps));
+                CK(cudaStreamWaitEvent(st, ctx->ev_h2d, 0));
+                CKT(tma_skinny(ctx, lpad, nc, m, ctx->omt, m, lpad, ctx->ldo, 0, 0, A, m, n_loc, lda, 0, c0,
+                               bdst + c0 * lpad, lpad, &tdone, 512, n));
+                if (!tdone)
+                    CKT(gemm_skinny(ctx, lpad, nc, m, ctx->omt, ctx->ldo, A + c0 * lda, lda, bdst + c0 * lpad, lpad, n));
+            }
+        } else {
+            CKT(tma_skinny(ctx, lpad, n_loc, m, ctx->omt, m, lpad, ctx->ldo, 0, 0, A, m, n_loc, lda, 0, 0, bdst, lpad,
+                           &tdone, 512, n));
+            if (!tdone) CKT(gemm_skinny(ctx, lpad, n_loc, m, ctx->omt, ctx->ldo, A, lda, bdst, lpad, n));
+        }
         ph_end(ctx);
         if (P > 1) CKT(gather_sample(n_loc, 0, n, ctx->bs[cur]));
         sumsq_partial_kernel<<<4 * G, 256, 0, st>>>(ctx->bs[cur], lpad, n, lpad, ctx->sumsq_part);
@@ -1821,10 +1848,27 @@ struct Run {
         CKT(sample_qrcp(0));
         for (int64_t i = 0; i < k; i += b) {
             CKT(panel(i));
+            if (h_out) {  // the panel's columns are final: stream them out behind the next panels
+                const int64_t bb = std::min<int64_t>(b, k - i);
+                CK(cudaEventRecord(ctx->ev_h2d, st));
+                CK(cudaStreamWaitEvent(cps, ctx->ev_h2d, 0));
+                CK(cudaMemcpy2DAsync(h_out + i * h_ld, sizeof(double) * h_ld, A + i * lda, sizeof(double) * lda,
+                                     sizeof(double) * m, bb, cudaMemcpyDeviceToHost, cps));
+            }
             CKT(trailing_and_sample(i));
             ++panels;
         }
         CKT(join_bulk());
+        if (h_out && k < n) {  // the trailing columns (R12 rows, R22) are final now
+            CK(cudaEventRecord(ctx->ev_h2d, st));
+            CK(cudaStreamWaitEvent(cps, ctx->ev_h2d, 0));
+            CK(cudaMemcpy2DAsync(h_out + k * h_ld, sizeof(double) * h_ld, A + k * lda, sizeof(double) * lda,
+                                 sizeof(double) * m, n - k, cudaMemcpyDeviceToHost, cps));
+        }
+        if (h_out) {
+            CK(cudaEventRecord(ctx->ev_h2d, cps));
+            CK(cudaStreamWaitEvent(st, ctx->ev_h2d, 0));
+        }
         return 0;
     }
 };
@@ -1859,7 +1903,8 @@ static void print_traces(rqrcp_ctx *ctx);
 
 static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n, int64_t k, int b, int p,
                        uint64_t seed, int64_t *jpvt, double *tau, int64_t *rank_out, const double *omega_in,
-                       double *omega_out, rqrcp_trace *trace, bool keep_last = false, int *final_sample = nullptr) {
+                       double *omega_out, rqrcp_trace *trace, bool keep_last = false, int *final_sample = nullptr,
+                       const double *h_in = nullptr, double *h_out = nullptr, int64_t h_ld = 0) {
     if (!ctx) return -1;
     if (!A) return -2;
     if (lda < std::max<int64_t>(1, m)) return -3;
@@ -1912,6 +1957,10 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     R.bb_eff = ctx->iscal + 1;
     R.done = ctx->iscal + 2;
     R.rankd = ctx->iscal + 3;
+    R.h_in = h_in;
+    R.h_out = h_out;
+    R.h_ld = h_ld;
+    R.cps = ctx->cps;
     // schedule: the bulk rows of each trailing update overlap the next sample
     // QRCP (measured best at C2-C4: 4.40 / 50.7 / 1088 ms against 5.23 / 54.8 /
     // 1191 ms with the panel look-ahead, whose panel kernel slows down when it
@@ -2225,15 +2274,14 @@ extern "C" int rqrcp_factor_host(rqrcp_ctx *ctx, const double *A_host, int64_t l
         CK(cudaMalloc((void **)&ctx->tau_dev, sizeof(double) * std::min(ctx->max_m, ctx->max_n)));
         ctx->a_dev_elems = need;
     }
-    CK(cudaMemcpy2DAsync(ctx->a_dev, sizeof(double) * m, A_host, sizeof(double) * lda, sizeof(double) * m, n,
-                         cudaMemcpyHostToDevice, ctx->stream));
+    // A streams in by column chunks that feed the sketch, and the finished
+    // panels stream out while later panels run (copy stream); A_out_host may
+    // equal A_host: every input chunk has landed before the first output copy
     int64_t rk = 0;
     int rc = factor_impl(ctx, ctx->a_dev, m, m, n, k, b, p, seed, ctx->jpvt_dev, ctx->tau_dev, &rk, nullptr, nullptr,
-                         nullptr);
+                         nullptr, false, nullptr, A_host, A_out_host, lda);
     *rank_out = rk;
     if (rc != 0 && rc != RQRCP_W_RANK_DEFICIENT) return rc;
-    CK(cudaMemcpy2DAsync(A_out_host, sizeof(double) * lda, ctx->a_dev, sizeof(double) * m, sizeof(double) * m, n,
-                         cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(jpvt_host, ctx->jpvt_dev, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(tau_host, ctx->tau_dev, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));

@@ -424,6 +424,21 @@ def test_factor_host_equals_device(ctx):
     assert np.array_equal(jp.numpy(), g["jpvt"])
 
 
+def test_factor_host_streams_chunks(ctx):
+    """The end-to-end path streams A in by 2048-column chunks (each chunk's
+    sketch as it lands) and the finished panels out during the factorization:
+    bitwise the device-path result, also in place (A_out = A_in)."""
+    A = inputs.iid(9, 400, 4700).numpy()
+    g = gpu_factor(ctx, A, 128, 32, 8, 6)
+    Ah = inputs.fortran(torch.as_tensor(A)).pin_memory()
+    Ao = inputs.fortran(torch.zeros_like(torch.as_tensor(A))).pin_memory()
+    jp, ta, rank = ctx.factor_host(Ah, 128, 32, 8, seed=6, out=Ao)
+    assert rank == 128
+    assert np.array_equal(Ao.numpy(), g["A"]) and np.array_equal(jp.numpy(), g["jpvt"])
+    jp2, ta2, rank2 = ctx.factor_host(Ah, 128, 32, 8, seed=6)  # in place
+    assert np.array_equal(Ah.numpy(), g["A"])
+
+
 # ---- launch-shape variants of the sample QRCP (threads per column, spill) ----
 # sq_grid caps the cooperative grid (fewer CTAs -> more columns per CTA, fewer
 # threads per column) and sq_nsm caps the columns a CTA keeps in shared memory
