@@ -63,11 +63,10 @@ struct PanelArgs {
 // 32-column sub-panels of the blocked panel, so all 8 warps have columns)
 template <int CB>
 __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
-    constexpr int PN_CB = CB;
+    constexpr int NU = (CB == 4) ? 1 : PN_MAXB / 32;  // 32-column groups of the reduce (bb <= 32 for CB 4)
     extern __shared__ __align__(16) double pn_dyn[];
     __shared__ double w[PN_MAXB], rjs[PN_MAXB];
     __shared__ double wred[PN_WARPS][PN_MAXB];
-    __shared__ double xs[PN_MAXROWS];
     __shared__ double s_scal, s_tau, s_beta;
     __shared__ int s_stop;
     if (a.skip && *a.skip == 0) return;
@@ -104,33 +103,47 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
         const int par = j & 1;
         const int rj = (int)(j - r_lo);  // local index of row j (may be out of range)
         const int rs = max(0, rj + 1);
-        // ---- partial Gram row over own rows r > j (PN_CB columns per warp at
-        //      a time: all loads in flight, interleaved butterfly sums) -------
-        for (int c0 = warp * PN_CB; c0 < bb; c0 += PN_WARPS * PN_CB) {
-            double acc[PN_CB];
+        // ---- partial Gram row over own rows r > j: thread per row, 32 columns
+        //      per pass in registers, then a butterfly reduce-scatter inside the
+        //      warp (lane l ends with column 32 q + l) and the 8 warp sums in
+        //      warp order (one fixed order) ------------------------------------
+        for (int q = 0; q * 32 < bb; ++q) {
+            double acc[32];
 #pragma unroll
-            for (int u = 0; u < PN_CB; ++u) acc[u] = 0.0;
-            for (int r = rs + lane; r < nsm; r += 32) {
-                const double xr = Ps[r + (int64_t)j * lds];
+            for (int u = 0; u < 32; ++u) acc[u] = 0.0;
+            const int cb = min(32, bb - 32 * q);
+            for (int r = rs + tid; r < nrows; r += PN_THREADS) {
+                const double xr = Pv(r, j);
+                if (r < nsm) {
+                    const double *pr = Ps + r + (int64_t)(32 * q) * lds;
 #pragma unroll
-                for (int u = 0; u < PN_CB; ++u)
-                    if (c0 + u < bb) acc[u] += Ps[r + (int64_t)(c0 + u) * lds] * xr;
+                    for (int u = 0; u < 32; ++u)
+                        if (u < cb) acc[u] += pr[(int64_t)u * lds] * xr;
+                } else {
+                    const double *pr = Pg + r + (int64_t)(32 * q) * lda;
+#pragma unroll
+                    for (int u = 0; u < 32; ++u)
+                        if (u < cb) acc[u] += pr[(int64_t)u * lda] * xr;
+                }
             }
-            for (int r = max(rs, nsm) + lane; r < nrows; r += 32) {
-                const double xr = Pg[r + (int64_t)j * lda];
 #pragma unroll
-                for (int u = 0; u < PN_CB; ++u)
-                    if (c0 + u < bb) acc[u] += Pg[r + (int64_t)(c0 + u) * lda] * xr;
+            for (int o = 16; o >= 1; o >>= 1) {
+                const bool up = (lane & o) != 0;
+#pragma unroll
+                for (int u = 0; u < o; ++u) {
+                    const double send = up ? acc[u] : acc[u + o];
+                    const double keep = up ? acc[u + o] : acc[u];
+                    acc[u] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
             }
+            wred[warp][32 * q + lane] = acc[0];
+        }
+        __syncthreads();
+        for (int c = tid; c < bb; c += PN_THREADS) {
+            double v = 0.0;
 #pragma unroll
-            for (int u = 0; u < PN_CB; ++u) acc[u] = warp_sum(acc[u]);
-            if (lane < PN_CB && c0 + lane < bb) {
-                double v = acc[0];
-#pragma unroll
-                for (int u = 1; u < PN_CB; ++u)
-                    if (lane == u) v = acc[u];
-                a.part[((int64_t)par * G + g) * a.bbpad + c0 + lane] = v;
-            }
+            for (int ww = 0; ww < PN_WARPS; ++ww) v += wred[ww][c];
+            a.part[((int64_t)par * G + g) * a.bbpad + c] = v;
         }
         if (rj >= 0 && rj < nrows)
             for (int c = tid; c < bb; c += PN_THREADS) a.rowj[par * a.bbpad + c] = Pv(rj, c);
@@ -145,15 +158,15 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
             // one L2 round trip instead of one per batch of four rows
             const double *pp = a.part + (int64_t)par * G * a.bbpad;
             const int nu = (bb + 31) >> 5;
-            double acc[PN_MAXB / 32];
+            double acc[NU];
 #pragma unroll
-            for (int u = 0; u < PN_MAXB / 32; ++u) acc[u] = 0.0;
-            double v[PN_RMAX][PN_MAXB / 32];
+            for (int u = 0; u < NU; ++u) acc[u] = 0.0;
+            double v[PN_RMAX][NU];
 #pragma unroll
             for (int h = 0; h < PN_RMAX; ++h) {
                 const int gg = warp + h * PN_WARPS;
 #pragma unroll
-                for (int u = 0; u < PN_MAXB / 32; ++u) {
+                for (int u = 0; u < NU; ++u) {
                     const int c = lane + 32 * u;
                     v[h][u] = (u < nu && gg < G && c < bb) ? ld_cg(pp + (int64_t)gg * a.bbpad + c) : 0.0;
                 }
@@ -161,9 +174,9 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
 #pragma unroll
             for (int h = 0; h < PN_RMAX; ++h)
 #pragma unroll
-                for (int u = 0; u < PN_MAXB / 32; ++u) acc[u] += v[h][u];
+                for (int u = 0; u < NU; ++u) acc[u] += v[h][u];
 #pragma unroll
-            for (int u = 0; u < PN_MAXB / 32; ++u) {
+            for (int u = 0; u < NU; ++u) {
                 const int c = lane + 32 * u;
                 if (c < bb) wred[warp][c] = acc[u];
             }
@@ -208,36 +221,25 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
             for (int c = tid; c < j; c += PN_THREADS) a.ybuf[c + (int64_t)j * ldy] = rjs[c] + scal * w[c];
         // w_c = tau * (a_jc + scal g_c) for c > j
         for (int c = j + 1 + tid; c < bb; c += PN_THREADS) w[c] = tau * (rjs[c] + scal * w[c]);
-        for (int r = tid; r < nrows; r += PN_THREADS) xs[r] = Pv(r, j);
         __syncthreads();
         stamp(4);
-        // ---- update own rows ---------------------------------------------
+        // ---- update own rows: thread per row (the row's x_r read first; no
+        //      other thread touches the row) -----------------------------------
         if (tau != 0.0) {
-            for (int c = j + 1 + warp; c < bb; c += PN_WARPS) {
-                const double wc = w[c];
-                for (int r = lane; r < nsm; r += 32) {
-                    if (r > rj) Ps[r + (int64_t)c * lds] -= wc * (scal * xs[r]);
-                    else if (r == rj) Ps[r + (int64_t)c * lds] -= wc;
-                }
-            }
-            // L2-resident rows: lane per row, PN_CB columns per batch (loads in flight)
-            for (int r = nsm + lane; r < nrows; r += 32) {
-                const double vr = (r > rj) ? scal * xs[r] : 1.0;
-                if (r < rj) continue;
-                for (int c0 = j + 1 + warp * PN_CB; c0 < bb; c0 += PN_WARPS * PN_CB) {
-                    double x[PN_CB];
-#pragma unroll
-                    for (int u = 0; u < PN_CB; ++u) x[u] = (c0 + u < bb) ? Pg[r + (int64_t)(c0 + u) * lda] : 0.0;
-#pragma unroll
-                    for (int u = 0; u < PN_CB; ++u)
-                        if (c0 + u < bb) Pg[r + (int64_t)(c0 + u) * lda] = x[u] - w[c0 + u] * vr;
-                }
-            }
-            for (int r = tid; r < nrows; r += PN_THREADS) {
-                const double v = (r > rj) ? scal * xs[r] : s_beta;
-                if (r >= rj) {
-                    if (r < nsm) Ps[r + (int64_t)j * lds] = v;
-                    else Pg[r + (int64_t)j * lda] = v;
+            const double beta = s_beta;
+            for (int r = max(rj, 0) + tid; r < nrows; r += PN_THREADS) {
+                const double xr = Pv(r, j);
+                const double vr = (r > rj) ? scal * xr : 1.0;
+                if (r < nsm) {
+                    double *pr = Ps + r;
+#pragma unroll 8
+                    for (int c = j + 1; c < bb; ++c) pr[(int64_t)c * lds] -= w[c] * vr;
+                    pr[(int64_t)j * lds] = (r > rj) ? vr : beta;
+                } else {
+                    double *pr = Pg + r;
+#pragma unroll 8
+                    for (int c = j + 1; c < bb; ++c) pr[(int64_t)c * lda] -= w[c] * vr;
+                    pr[(int64_t)j * lda] = (r > rj) ? vr : beta;
                 }
             }
         }

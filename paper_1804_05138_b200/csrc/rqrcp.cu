@@ -814,7 +814,7 @@ static int create_impl(rqrcp_ctx **out, const rqrcp_config *cfg, int nranks, int
         }
         cudaGetLastError();
     }
-    CKC(smem_attr((const void *)tri_kernel, (128 * 128 + 64 * 64) * 8, dev));
+    CKC(smem_attr((const void *)tri_kernel, (int)tri_smem_bytes(128), dev));
     CKC(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     CKC(cudaStreamCreateWithPriority(&ctx->upd, cudaStreamNonBlocking, prio_lo));
     CKC(cudaMallocHost((void **)&ctx->hstatus, sizeof(int) * 8));
@@ -1276,7 +1276,7 @@ struct Run {
         {
             int nb = 8;
             while (nb < bbpad) nb *= 2;
-            const size_t smem = ((size_t)nb * nb + (size_t)(nb / 2) * (nb / 2)) * sizeof(double);
+            const size_t smem = tri_smem_bytes(nb);
             tri_kernel<<<1, TRI_THREADS, smem, st>>>(ctx->tp_y, ctx->tauhat, nullptr, nullptr, 0, bb, bbpad, nb,
                                                      ctx->tp_cnt, ctx->tp_tn, nullptr, 0, nullptr);
             CKL();
@@ -1468,7 +1468,7 @@ struct Run {
             const bool rule5 = ctx->update_rule == 2 && more_after(i, bb) && n - i - bb > 0;
             int nb = 8;
             while (nb < bbpad) nb *= 2;
-            const size_t smem = ((size_t)nb * nb + (size_t)(nb / 2) * (nb / 2)) * sizeof(double);
+            const size_t smem = tri_smem_bytes(nb);
             CK(cudaEventRecord(ctx->ev_fork, st));
             CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
             const int do_om = (more_after(i, bb) && n - i - bb > 0 && !rule5) ? 1 : 0;
@@ -1578,7 +1578,7 @@ struct Run {
             CKL();
             if (c1 < bb) {
                 // T_s, then the in-panel update of columns c1..bb (rows c0..m')
-                tri_kernel<<<1, TRI_THREADS, ((size_t)w * w + (size_t)(w / 2) * (w / 2)) * sizeof(double), st>>>(
+                tri_kernel<<<1, TRI_THREADS, tri_smem_bytes(w), st>>>(
                     ctx->ybs, tau + i + c0, nullptr, nullptr, 0, ws, w, w, ctx->subeff, ctx->tns, nullptr, 0, nullptr);
                 CKL();
                 const int64_t nr = bb - c1, K = mp - c0;
@@ -2171,7 +2171,7 @@ extern "C" int rqrcp_form_q1(rqrcp_ctx *ctx, const double *A, int64_t lda, int64
         CKL();
         int nb = 8;
         while (nb < bbpad) nb *= 2;
-        const size_t tsm = ((size_t)nb * nb + (size_t)(nb / 2) * (nb / 2)) * sizeof(double);
+        const size_t tsm = tri_smem_bytes(nb);
         tri_kernel<<<1, TRI_THREADS, tsm, st>>>(ctx->ybuf, tau + i, nullptr, nullptr, 0, bb, bbpad, nb, bbd, ctx->tneg,
                                                 ctx->omhat, 0, nullptr);
         CKL();

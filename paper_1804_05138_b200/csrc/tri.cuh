@@ -50,32 +50,48 @@ RQ_DEV void tri_mul_fu(const double *A, int lda, const double *B, int ldb, doubl
     }
 }
 
-// nb = power of two multiple of 8, >= bb
+// Shared memory of tri_kernel: the nb x nb working triangle with an odd
+// leading dimension (nb + 1: row- and column-wise walks are both free of bank
+// conflicts), whose strictly lower part holds the second operand transposed
+// (Y, or R-hat11), then (nb/2)^2 doubles of scratch and nb diagonal entries.
+inline size_t tri_smem_bytes(int nb) {
+    return ((size_t)nb * (nb + 1) + (size_t)(nb / 2) * (nb / 2) + (size_t)nb) * sizeof(double);
+}
+
+// nb = power of two multiple of 8, >= bb.  Every operand is staged in shared
+// memory once (coalesced); no serial chain waits on global memory.
 __global__ void __launch_bounds__(TRI_THREADS) tri_kernel(const double *ybuf /* bbpad x bbpad */, const double *tau,
                                                           const double *rhat11 /* bbpad x bbpad */,
                                                           const double *R11 /* &A[i+i lda] */, int64_t lda, int bb,
                                                           int bbpad, int nb, const int *bb_eff, double *tneg,
                                                           double *omhat, int do_omhat, const int *t_ready) {
     extern __shared__ __align__(16) double tsm[];
-    double *M = tsm;             // nb x nb
-    double *tmp = tsm + nb * nb; // (nb/2) x (nb/2)
-    const int ld = nb;
+    const int ld = nb + 1;
+    double *M = tsm;                       // nb x nb, ld nb + 1: upper = result, strict lower = operand^T
+    double *tmp = tsm + (size_t)nb * ld;   // (nb/2) x (nb/2)
+    double *dg = tmp + (nb / 2) * (nb / 2); // nb: diagonal of the staged operand
     const int bbe = *bb_eff;
     const int tid = threadIdx.x;
     if (blockIdx.x == 0) {
         // ---------------- T ----------------
         if (t_ready && *t_ready == 0) return;  // written by the CholeskyQR2 reconstruction
-        for (int e = tid; e < nb * nb; e += blockDim.x) M[e] = 0.0;
+        // upper: 0; strict lower M(r, c) (r > c) = Y(c, r) = v_c^T v_r (c < r < bbe)
+        for (int e = tid; e < nb * nb; e += blockDim.x) {
+            const int c = e % nb, r = e / nb;  // consecutive threads: consecutive c (coalesced ybuf column r)
+            M[r + c * ld] = (r > c && r < bbe) ? ybuf[c + (int64_t)r * bbpad] : 0.0;
+        }
+        for (int j = tid; j < nb; j += blockDim.x) dg[j] = (j < bbe) ? tau[j] : 0.0;
         __syncthreads();
         // base: each thread owns one 8x8 diagonal block, column recurrence
+        // T(r, j) = -tau_j sum_{r <= c < j} T(r, c) Y(c, j)
         if (tid < nb / 8) {
             const int k0 = tid * 8;
             for (int j = k0; j < k0 + 8; ++j) {
                 if (j >= bbe) continue;  // tau = 0 beyond the effective width: zero column
-                const double tj = tau[j];
+                const double tj = dg[j];
                 for (int r = k0; r < j; ++r) {
                     double acc = 0.0;
-                    for (int c = r; c < j; ++c) acc += M[r + c * ld] * ybuf[c + (int64_t)j * bbpad];
+                    for (int c = r; c < j; ++c) acc += M[r + c * ld] * M[j + c * ld];
                     M[r + j * ld] = -tj * acc;
                 }
                 M[j + j * ld] = tj;
@@ -84,15 +100,11 @@ __global__ void __launch_bounds__(TRI_THREADS) tri_kernel(const double *ybuf /* 
         __syncthreads();
         for (int s = 8; s < nb; s *= 2) {
             for (int k = 0; k < nb; k += 2 * s) {
-                // tmp = Y12 * T2 ; T12 = -T1 * tmp
+                // tmp = Y12 * T2 ; T12 = -T1 * tmp  (Y12(r, q) = M(k + s + q, k + r))
                 for (int e = tid; e < s * s; e += blockDim.x) {
                     const int r = e % s, c = e / s;
                     double acc = 0.0;
-                    for (int q = 0; q <= c; ++q) {
-                        const int gr = k + r, gq = k + s + q;
-                        const double y = (gr < bbe && gq < bbe) ? ybuf[gr + (int64_t)gq * bbpad] : 0.0;
-                        acc += y * M[(k + s + q) + (k + s + c) * ld];
-                    }
+                    for (int q = 0; q <= c; ++q) acc += M[(k + s + q) + (k + r) * ld] * M[(k + s + q) + (k + s + c) * ld];
                     tmp[r + c * (nb / 2)] = acc;
                 }
                 __syncthreads();
@@ -109,18 +121,26 @@ __global__ void __launch_bounds__(TRI_THREADS) tri_kernel(const double *ybuf /* 
         }
         for (int e = tid; e < bbpad * bbpad; e += blockDim.x) {
             const int r = e % bbpad, c = e / bbpad;
-            tneg[e] = (r < nb && c < nb) ? -M[r + c * ld] : 0.0;
+            tneg[e] = (r <= c && c < nb) ? -M[r + c * ld] : 0.0;
         }
     } else {
         // ---------------- Omega-hat11 = R-hat11 R11^{-1} ----------------
         if (!do_omhat || bbe != bb) return;
+        // upper: R11 (identity padding); strict lower M(r, c) (r > c) = R-hat11(c, r); dg = diag(R-hat11)
         for (int e = tid; e < nb * nb; e += blockDim.x) {
             const int r = e % nb, c = e / nb;
             double v = 0.0;
-            if (r < bb && c < bb) v = (r <= c) ? R11[r + (int64_t)c * lda] : 0.0;
-            else if (r == c) v = 1.0;  // identity padding
-            M[e] = v;
+            if (r <= c) {
+                if (r < bb && c < bb) v = R11[r + (int64_t)c * lda];
+                else if (r == c) v = 1.0;
+            }
+            M[r + c * ld] = v;
         }
+        for (int e = tid; e < nb * nb; e += blockDim.x) {
+            const int c = e % nb, r = e / nb;  // R-hat11(c, r), c < r: coalesced column r
+            if (r > c) M[r + c * ld] = (r < bb) ? rhat11[c + (int64_t)r * bbpad] : 0.0;
+        }
+        for (int j = tid; j < nb; j += blockDim.x) dg[j] = (j < bb) ? rhat11[j + (int64_t)j * bbpad] : 0.0;
         __syncthreads();
         // base: invert 8x8 diagonal blocks in place (thread per block column-by-column)
         if (tid < nb / 8) {
@@ -137,7 +157,7 @@ __global__ void __launch_bounds__(TRI_THREADS) tri_kernel(const double *ybuf /* 
                 }
             }
             for (int c = 0; c < 8; ++c)
-                for (int r = 0; r < 8; ++r) M[(k0 + r) + (k0 + c) * ld] = (r <= c) ? inv[r][c] : 0.0;
+                for (int r = 0; r <= c; ++r) M[(k0 + r) + (k0 + c) * ld] = inv[r][c];
         }
         __syncthreads();
         for (int s = 8; s < nb; s *= 2) {
@@ -153,8 +173,10 @@ __global__ void __launch_bounds__(TRI_THREADS) tri_kernel(const double *ybuf /* 
         for (int e = tid; e < bbpad * bbpad; e += blockDim.x) {
             const int r = e % bbpad, c = e / bbpad;
             double acc = 0.0;
-            if (r <= c && c < bb)
-                for (int q = r; q <= c; ++q) acc += rhat11[r + (int64_t)q * bbpad] * M[q + c * ld];
+            if (r <= c && c < bb) {
+                acc = dg[r] * M[r + c * ld];
+                for (int q = r + 1; q <= c; ++q) acc += M[q + r * ld] * M[q + c * ld];
+            }
             omhat[c + r * bbpad] = acc;  // stored transposed: the K-contiguous X of C = X^T R12
         }
     }
