@@ -181,7 +181,12 @@ int rqrcp_factor_ex(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n
  *                 reading R-TP) instead of Alg. 1 on the whole sample; 0 / 1: Alg. 1
  *   upd_kernel    trailing-update GEMM: 0 CTA-wide TMA epilogue, 1 / 2 warp-specialised
  *                 (per-warp TMA epilogue; 32 x 2 / 16 x 4 k-stages)
- *   sq_cluster, sq_reg, sq_grid, sq_nsm, sq_hstride, sq_poll   sample QRCP kernel choice / shape
+ *   sq_cluster, sq_grid, sq_nsm, sq_hstride   sample QRCP kernel choice / shape
+ *   sq_reg        register-resident grid sample QRCP: 1 the 256-thread kernel when the sample
+ *                 fits, else the 512-thread kernel with the top rows in global memory (l = 144);
+ *                 2 always the 512-thread kernel when it exists for l; 0 neither
+ *   sq_poll       grid sample QRCP exchange: 3 tagged 16-byte units (no fences), 0 acquire
+ *                 polls, 1 relaxed polls + one fence, 2 as 1 with backoff
  *   debug_sync    synchronise after every launch
  *   nccl_timeout_ms   multi-GPU: abort the communicator when a call exceeds it */
 int rqrcp_set_option(rqrcp_ctx *ctx, const char *name, int64_t value);

@@ -69,6 +69,23 @@ RQ_DEV void st_cg_v2(double2 *p, double2 v) {
     asm volatile("st.global.cg.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
+// Tagged 16-byte units for fence-free exchanges between CTAs: a 64-bit
+// value travels as two 32-bit halves, each beside the step tag, in one
+// single-copy-atomic 16-byte store; a reader polls until both tags match.
+// unit = {lo32 | tag << 32, hi32 | tag << 32}
+RQ_DEV void ll_store(uint4 *p, unsigned long long w, unsigned tag) {
+    const unsigned long long t = (unsigned long long)tag << 32;
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};\n" ::"l"(p), "l"((w & 0xffffffffull) | t),
+                 "l"((w >> 32) | t)
+                 : "memory");
+}
+RQ_DEV bool ll_load(const uint4 *p, unsigned tag, unsigned long long &w) {
+    unsigned long long a, b;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+    w = (a & 0xffffffffull) | (b << 32);
+    return (unsigned)(a >> 32) == tag && (unsigned)(b >> 32) == tag;
+}
+
 // L2 load for data written by other CTAs (after a grid barrier); not
 // volatile, so the compiler may batch several in flight.
 RQ_DEV double ld_cg(const double *p) { return __ldcg(p); }

@@ -32,6 +32,7 @@
 #include "sample_qrcp.cuh"
 #include "sample_qrcp_cl.cuh"
 #include "sample_qrcp_reg.cuh"
+#include "sample_qrcp_reg2.cuh"
 #include "tri.cuh"
 #include "cqr.cuh"
 #include "dist.cuh"
@@ -56,7 +57,7 @@ struct Opts {
     int pn_blocked = 1;      // grid panel on 32-column sub-panels + in-panel DMMA updates: 0 never, 1 when
                              // a CTA's rows do not fit shared memory, 2 always
     int upd_kernel = 2;      // update GEMM: 0 CTA-wide TMA epilogue, 1 / 2 warp-specialised (BK 32 x 2 / 16 x 4 stages)
-    int sq_cluster = 1, sq_reg = 1, sq_grid = 0, sq_nsm = -1, sq_hstride = 8, sq_poll = 1;
+    int sq_cluster = 1, sq_reg = 1, sq_grid = 0, sq_nsm = -1, sq_hstride = 8, sq_poll = 3;
     int debug_sync = 0, trace = 0, trace_panel = 1;
     int64_t nccl_timeout_ms = 600000;
 };
@@ -66,9 +67,9 @@ struct OptDesc {
 };
 static const OptDesc kOpts[] = {{"schedule", -1, 2},     {"panel", 0, 2},     {"pn_cluster", 0, 1},
                                 {"pn_cpt", 1, 2},        {"pn_grid", 0, 4096}, {"pn_rows", 1, 1 << 20},
-                                {"la_panel_ctas", 1, 4096}, {"sq_cluster", 0, 1}, {"sq_reg", 0, 1},
+                                {"la_panel_ctas", 1, 4096}, {"sq_cluster", 0, 1}, {"sq_reg", 0, 2},
                                 {"sq_grid", 0, 4096},    {"sq_nsm", -1, 1 << 20}, {"sq_hstride", 1, 8},
-                                {"sq_poll", 0, 2},       {"debug_sync", 0, 1}, {"trace", 0, 1},
+                                {"sq_poll", 0, 3},       {"debug_sync", 0, 1}, {"trace", 0, 1},
                                 {"trace_panel", 1, 1 << 30}, {"nccl_timeout_ms", 1, (int64_t)1 << 40},
                                 {"upd_kernel", 0, 2}, {"pn_blocked", 0, 2},
                                 {"tournament", 0, 64}, {"gemm_ws", 0, 1}};
@@ -137,6 +138,7 @@ struct rqrcp_ctx {
     double *slot_v2 = nullptr, *slot_data = nullptr;
     uint4 *sq_ll = nullptr;
     double *sq_spill = nullptr;
+    int64_t spill_cap = 0;  // doubles in sq_spill
     double *pn_part = nullptr, *pn_rowj = nullptr;
     double *cq_g = nullptr, *cq_rc = nullptr, *cq_rinv = nullptr, *cq_uinv = nullptr, *cq_lu = nullptr;
     int *cqr_status = nullptr;
@@ -720,9 +722,10 @@ static int create_impl(rqrcp_ctx **out, const rqrcp_config *cfg, int nranks, int
     CKC(cudaMalloc((void **)&ctx->slot_col, sizeof(int) * 2 * G));
     CKC(dalloc(&ctx->slot_v2, 2 * G));
     CKC(dalloc(&ctx->slot_data, 2 * G * lp));
-    CKC(cudaMalloc((void **)&ctx->sq_ll, sizeof(uint4) * 2 * SQ_MAXG * (SQ_MAXL + 2)));
-    CKC(cudaMemset(ctx->sq_ll, 0, sizeof(uint4) * 2 * SQ_MAXG * (SQ_MAXL + 2)));
+    CKC(cudaMalloc((void **)&ctx->sq_ll, sizeof(uint4) * 2 * SQ_MAXG * SQS_UNITS));
+    CKC(cudaMemset(ctx->sq_ll, 0, sizeof(uint4) * 2 * SQ_MAXG * SQS_UNITS));
     CKC(dalloc(&ctx->sq_spill, lp * nn));
+    ctx->spill_cap = lp * nn;
     CKC(dalloc(&ctx->bpre, lp * nn));
     CKC(dalloc(&ctx->c5, lp * nn));
     CKC(dalloc(&ctx->wom, bp * lp));
@@ -754,6 +757,7 @@ static int create_impl(rqrcp_ctx **out, const rqrcp_config *cfg, int nranks, int
     CKC(smem_attr((const void *)sample_qrcp_reg_kernel<40, 0>, 128 * 40 * 8, dev));
     CKC(smem_attr((const void *)sample_qrcp_reg_kernel<74, 0>, 128 * 74 * 8, dev));
     CKC(smem_attr((const void *)sample_qrcp_reg_kernel<72, 72>, 128 * 144 * 8, dev));
+    CKC(smem_attr((const void *)sample_qrcp_reg2_kernel<60, 32, 52>, 52 * SQR2_THREADS * 8, dev));
     for (const void *k : {(const void *)sample_qrcp_cluster_kernel<40>, (const void *)sample_qrcp_cluster_kernel<74>,
                           (const void *)sample_qrcp_cluster_kernel<80>}) {
         CKC(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -1019,27 +1023,37 @@ struct SqKernels {
     void (*cluster)(SqArgs);
     void (*reg)(SqArgs);
     int reg_ls;  // rows of the register-grid kernel kept in shared memory
+    void (*reg2)(SqArgs);  // 512-thread register grid with the top rows in global memory
+    int reg2_lt, reg2_ls;
 };
 static SqKernels sq_kernels(int l) {
-    if (l == 40) return {sample_qrcp_cluster_kernel<40>, sample_qrcp_reg_kernel<40, 0>, 0};
-    if (l == 74) return {sample_qrcp_cluster_kernel<74>, sample_qrcp_reg_kernel<74, 0>, 0};
-    if (l == 80) return {sample_qrcp_cluster_kernel<80>, nullptr, 0};
-    if (l == 144) return {nullptr, sample_qrcp_reg_kernel<72, 72>, 72};
-    return {nullptr, nullptr, 0};
+    if (l == 40) return {sample_qrcp_cluster_kernel<40>, sample_qrcp_reg_kernel<40, 0>, 0, nullptr, 0, 0};
+    if (l == 74) return {sample_qrcp_cluster_kernel<74>, sample_qrcp_reg_kernel<74, 0>, 0, nullptr, 0, 0};
+    if (l == 80) return {sample_qrcp_cluster_kernel<80>, nullptr, 0, nullptr, 0, 0};
+    if (l == 144)
+        return {nullptr, sample_qrcp_reg_kernel<72, 72>, 72, sample_qrcp_reg2_kernel<60, 32, 52>, 60, 52};
+    return {nullptr, nullptr, 0, nullptr, 0, 0};
 }
-enum SqKind { SQK_CLUSTER = 0, SQK_REG = 1, SQK_GRID = 2 };
+enum SqKind { SQK_CLUSTER = 0, SQK_REG = 1, SQK_GRID = 2, SQK_REG2 = 3 };
+static int sq_reg2_grid(int64_t np) { return 1 + (int)((np + SQR2_THREADS - 1) / SQR2_THREADS); }
 static SqKind sq_kind(const rqrcp_ctx *ctx, int l, int64_t np) {
     const SqKernels k = sq_kernels(l);
     const int64_t need = (np + SQC_THREADS - 1) / SQC_THREADS;
     if (ctx->opt.sq_cluster && k.cluster && need <= ctx->sqc_max) return SQK_CLUSTER;
     const int grid = 1 + (int)((np + SQR_THREADS - 1) / SQR_THREADS);
-    if (ctx->opt.sq_reg && k.reg && grid <= std::min(ctx->num_sms, SQ_MAXG)) return SQK_REG;
+    const int cap = std::min(ctx->num_sms, SQ_MAXG);
+    if (ctx->opt.sq_reg == 1 && k.reg && grid <= cap) return SQK_REG;
+    // wider samples: the 512-thread register grid (top rows in the spill scratch)
+    if (ctx->opt.sq_reg && k.reg2 && sq_reg2_grid(np) <= cap &&
+        (int64_t)sq_reg2_grid(np) * k.reg2_lt * SQR2_THREADS <= ctx->spill_cap)
+        return SQK_REG2;
     return SQK_GRID;
 }
 static int sq_ctas(const rqrcp_ctx *ctx, int l, int64_t np) {
     switch (sq_kind(ctx, l, np)) {
         case SQK_CLUSTER: return (int)std::max<int64_t>(1, (np + SQC_THREADS - 1) / SQC_THREADS);
         case SQK_REG: return 1 + (int)((np + SQR_THREADS - 1) / SQR_THREADS);
+        case SQK_REG2: return sq_reg2_grid(np);
         default: return std::min(ctx->num_sms, SQ_MAXG);
     }
 }
@@ -1130,6 +1144,12 @@ struct Run {
         if (kind == SQK_CLUSTER) {
             const int cs = (int)std::max<int64_t>(1, (np + SQC_THREADS - 1) / SQC_THREADS);
             return cluster_launch(ctx, kt.cluster, cs, SQC_THREADS, (size_t)bb * l * sizeof(double), a);
+        }
+        if (kind == SQK_REG2) {
+            const int grid = sq_reg2_grid(np);
+            const size_t smem = (size_t)std::max(kt.reg2_ls * SQR2_THREADS, bb * l) * sizeof(double);
+            void *args[] = {&a};
+            return coop_launch(ctx, (const void *)kt.reg2, grid, SQR2_THREADS, args, smem);
         }
         if (kind == SQK_REG) {
             const int grid = 1 + (int)((np + SQR_THREADS - 1) / SQR_THREADS);

@@ -49,6 +49,7 @@ constexpr int SQ_MAXL = 160;  // l = b + p <= 160 rows
 constexpr int SQ_RPL = 5;     // rows per lane of a warp-held column (SQ_MAXL / 32)
 constexpr int SQ_MAXB = 128;  // panel width
 constexpr int SQ_MAXG = 256;  // CTAs (headers scanned by one warp, 8 per lane)
+constexpr int SQS_UNITS = SQ_MAXL + 3;  // tagged slot (poll_mode 3): v, pos | col << 32, v2, column
 constexpr int SQ_SPB = 16;    // loads in flight per thread for L2-resident (spilled) columns
 
 struct __align__(16) SqHdr {  // one candidate header (16 bytes, one vector store)
@@ -67,7 +68,7 @@ struct SqArgs {
     int nsm;              // columns per CTA held in shared memory
     int ncs;              // row stride of the shared-memory tile (>= nsm)
     double *spill;        // global scratch for the other columns (transposed, per CTA)
-    uint4 *ll;            // [2][G][SQ_MAXL + 2] tagged 16-byte units (sample_qrcp_reg.cuh)
+    uint4 *ll;            // [2][G][SQ_MAXL + 3] tagged 16-byte units (sample_qrcp_reg.cuh; poll_mode 3 here)
     const double *stop_tol2;
     SqHdr *slot_hdr;      // [2][G] x hstride
     int *slot_col;        // [2][G] physical column of the candidate (written before the header)
@@ -88,7 +89,8 @@ struct SqArgs {
     double *gaps;         // [bb] or nullptr
     unsigned tag0;        // launch sequence * 256 (distinct per launch)
     int hstride;          // header stride in headers (8: one header per 128-byte line)
-    int poll_mode;        // 0: acquire polls; 1: relaxed polls + one acquire fence; 2: 1 + nanosleep backoff
+    int poll_mode;        // 0: acquire polls; 1: relaxed polls + one acquire fence; 2: 1 + nanosleep backoff;
+                          // 3: tagged 16-byte units (ll), no release / acquire fence on either side
     unsigned long long *trace;  // debug: [G][64 steps][4 phases] clock64 stamps, or nullptr
 };
 
@@ -259,18 +261,31 @@ __global__ void __launch_bounds__(SQ_THREADS, 1) sample_qrcp_kernel(SqArgs a) {
             v2 = __shfl_sync(0xffffffffu, v2, 0);
             p = __shfl_sync(0xffffffffu, p, 0);
             c = __shfl_sync(0xffffffffu, c, 0);
-            if (c >= 0) {
-                double *dst = a.slot_data + (int64_t)(parity * G + g) * lpad;
-                const int cl = c - (int)c_lo;
-                for (int t = lane; t < l; t += 32) __stcg(dst + t, *elem(t, cl));
-            }
-            if (lane == 0) {
-                a.slot_col[parity * G + g] = c;
-                if (want_v2) a.slot_v2[parity * G + g] = v2;
-            }
-            __syncwarp();
-            if (lane == 0) {
-                st_release_hdr(a.slot_hdr + (int64_t)(parity * G + g) * a.hstride, v, p, a.tag0 + (unsigned)step);
+            if (a.poll_mode == 3) {  // tagged units: no fence waits for this CTA's outstanding stores
+                uint4 *dst = a.ll + (int64_t)(parity * G + g) * SQS_UNITS;
+                const unsigned tg = a.tag0 + (unsigned)step;
+                if (c >= 0) {
+                    const int cl = c - (int)c_lo;
+                    for (int t = lane; t < l; t += 32)
+                        ll_store(dst + 3 + t, (unsigned long long)__double_as_longlong(*elem(t, cl)), tg);
+                }
+                if (lane == 0) ll_store(dst, (unsigned long long)__double_as_longlong(v), tg);
+                if (lane == 1) ll_store(dst + 1, (unsigned long long)(unsigned)p | ((unsigned long long)(unsigned)c << 32), tg);
+                if (lane == 2 && want_v2) ll_store(dst + 2, (unsigned long long)__double_as_longlong(v2), tg);
+            } else {
+                if (c >= 0) {
+                    double *dst = a.slot_data + (int64_t)(parity * G + g) * lpad;
+                    const int cl = c - (int)c_lo;
+                    for (int t = lane; t < l; t += 32) __stcg(dst + t, *elem(t, cl));
+                }
+                if (lane == 0) {
+                    a.slot_col[parity * G + g] = c;
+                    if (want_v2) a.slot_v2[parity * G + g] = v2;
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    st_release_hdr(a.slot_hdr + (int64_t)(parity * G + g) * a.hstride, v, p, a.tag0 + (unsigned)step);
+                }
             }
         }
     };
@@ -290,64 +305,150 @@ __global__ void __launch_bounds__(SQ_THREADS, 1) sample_qrcp_kernel(SqArgs a) {
             constexpr int HPL = SQ_MAXG / 32;  // headers per lane
             double v = -1.0;
             int p = INT_MAX, sl = -1;
-            bool ready[HPL];
-            double hv[HPL];
-            int hp[HPL];
+            bool stop;
+            double xv[SQ_RPL];
+            int wc = -1;
+            if (a.poll_mode == 3) {
+                // tagged units: poll the G headers, then the winner's column
+                const uint4 *slots = a.ll + (int64_t)(par * G) * SQS_UNITS;
+                bool ready[HPL];
+                unsigned long long h0[HPL], h1[HPL];
 #pragma unroll
-            for (int u = 0; u < HPL; ++u) { ready[u] = (lane + 32 * u >= G); hv[u] = -1.0; hp[u] = INT_MAX; }
-            // poll until every header of step j is visible (acquire loads)
-            const int pm = a.poll_mode;
-            while (true) {
-                bool all = true;
+                for (int u = 0; u < HPL; ++u) { ready[u] = (lane + 32 * u >= G); h0[u] = 0; h1[u] = 0; }
+                while (true) {
+                    bool all = true;
+#pragma unroll
+                    for (int u = 0; u < HPL; ++u) {
+                        if (!ready[u]) {
+                            const uint4 *hq = slots + (int64_t)(lane + 32 * u) * SQS_UNITS;
+                            const bool r0_ = ll_load(hq, want, h0[u]);
+                            const bool r1_ = ll_load(hq + 1, want, h1[u]);
+                            ready[u] = r0_ && r1_;
+                        }
+                        all = all && ready[u];
+                    }
+                    if (__all_sync(0xffffffffu, all)) break;
+                }
+                double hvs[HPL];
 #pragma unroll
                 for (int u = 0; u < HPL; ++u) {
-                    if (!ready[u]) {
-                        unsigned tg;
-                        const SqHdr *hp_ = a.slot_hdr + (int64_t)(par * G + lane + 32 * u) * a.hstride;
-                        if (pm == 0) ld_acquire_hdr(hp_, hv[u], hp[u], tg);
-                        else ld_relaxed_hdr(hp_, hv[u], hp[u], tg);
-                        ready[u] = (tg == want);
+                    const int q = lane + 32 * u;
+                    hvs[u] = __longlong_as_double((long long)h0[u]);
+                    const int hp_ = (int)(unsigned)(h1[u] & 0xffffffffull);
+                    if (q < G && hp_ != INT_MAX && sq_better(hvs[u], hp_, v, p)) {
+                        v = hvs[u]; p = hp_; sl = q; wc = (int)(unsigned)(h1[u] >> 32);
                     }
-                    all = all && ready[u];
                 }
-                if (__all_sync(0xffffffffu, all)) break;
-                if (pm == 2) __nanosleep(64);
-            }
-            if (pm != 0) asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
 #pragma unroll
-            for (int u = 0; u < HPL; ++u) {
-                const int q = lane + 32 * u;
-                if (q < G && hp[u] != INT_MAX && sq_better(hv[u], hp[u], v, p)) {
-                    v = hv[u]; p = hp[u]; sl = q;
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                    const int op = __shfl_xor_sync(0xffffffffu, p, o);
+                    const int osl = __shfl_xor_sync(0xffffffffu, sl, o);
+                    const int owc = __shfl_xor_sync(0xffffffffu, wc, o);
+                    if (osl >= 0 && (sl < 0 || sq_better(ov, op, v, p))) { v = ov; p = op; sl = osl; wc = owc; }
                 }
-            }
+                stop = (sl < 0) || !(v > stop2);
+                {
+                    const uint4 *src = slots + (int64_t)(sl >= 0 ? sl : 0) * SQS_UNITS + 3;
+                    bool ok[SQ_RPL];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-                const int op = __shfl_xor_sync(0xffffffffu, p, o);
-                const int osl = __shfl_xor_sync(0xffffffffu, sl, o);
-                if (osl >= 0 && (sl < 0 || sq_better(ov, op, v, p))) { v = ov; p = op; sl = osl; }
-            }
-            const bool stop = (sl < 0) || !(v > stop2);
-            double xv[SQ_RPL];
-            const double *src = a.slot_data + (int64_t)(par * G + (sl >= 0 ? sl : 0)) * lpad;
+                    for (int qq = 0; qq < SQ_RPL; ++qq) { ok[qq] = stop || lane + 32 * qq >= l; xv[qq] = 0.0; }
+                    while (true) {
+                        bool all = true;
 #pragma unroll
-            for (int qq = 0; qq < SQ_RPL; ++qq) {
-                const int t = lane + 32 * qq;
-                xv[qq] = (!stop && t < l) ? __ldcg(src + t) : 0.0;
-            }
-            const int wc = (sl >= 0) ? __ldcg(a.slot_col + par * G + sl) : -1;
-            if (lane == 0) {
-                s_stop = stop;
-                s_wpos = p;
-                s_wcol = wc;
-                if (g == 0 && want_v2 && !stop) {
-                    double v2 = -1.0;
-                    for (int q = 0; q < G; ++q) {
-                        const double hv = __ldcg(&a.slot_hdr[(int64_t)(par * G + q) * a.hstride].v);
-                        v2 = fmax(v2, (q == sl) ? __ldcg(a.slot_v2 + par * G + q) : hv);
+                        for (int qq = 0; qq < SQ_RPL; ++qq) {
+                            if (!ok[qq]) {
+                                unsigned long long w;
+                                ok[qq] = ll_load(src + lane + 32 * qq, want, w);
+                                xv[qq] = __longlong_as_double((long long)w);
+                            }
+                            all = all && ok[qq];
+                        }
+                        if (__all_sync(0xffffffffu, all)) break;
                     }
-                    a.gaps[j] = (v2 < 0.0 || v == 0.0) ? 1.0 : (v - v2) / v;
+                }
+                if (g == 0 && want_v2 && !stop) {  // gap of the step (diagnostic): runner-up over all slots
+                    double m2 = -1.0;
+#pragma unroll
+                    for (int u = 0; u < HPL; ++u) {
+                        const int q = lane + 32 * u;
+                        if (q >= G) continue;
+                        double val = hvs[u];
+                        if (q == sl) {
+                            unsigned long long w;
+                            while (!ll_load(slots + (int64_t)q * SQS_UNITS + 2, want, w)) {}
+                            val = __longlong_as_double((long long)w);
+                        }
+                        m2 = fmax(m2, val);
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+                    if (lane == 0) a.gaps[j] = (m2 < 0.0 || v == 0.0) ? 1.0 : (v - m2) / v;
+                }
+                if (lane == 0) {
+                    s_stop = stop;
+                    s_wpos = p;
+                    s_wcol = wc;
+                }
+            } else {
+                bool ready[HPL];
+                double hv[HPL];
+                int hp[HPL];
+#pragma unroll
+                for (int u = 0; u < HPL; ++u) { ready[u] = (lane + 32 * u >= G); hv[u] = -1.0; hp[u] = INT_MAX; }
+                // poll until every header of step j is visible (acquire loads)
+                const int pm = a.poll_mode;
+                while (true) {
+                    bool all = true;
+#pragma unroll
+                    for (int u = 0; u < HPL; ++u) {
+                        if (!ready[u]) {
+                            unsigned tg;
+                            const SqHdr *hp_ = a.slot_hdr + (int64_t)(par * G + lane + 32 * u) * a.hstride;
+                            if (pm == 0) ld_acquire_hdr(hp_, hv[u], hp[u], tg);
+                            else ld_relaxed_hdr(hp_, hv[u], hp[u], tg);
+                            ready[u] = (tg == want);
+                        }
+                        all = all && ready[u];
+                    }
+                    if (__all_sync(0xffffffffu, all)) break;
+                    if (pm == 2) __nanosleep(64);
+                }
+                if (pm != 0) asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+#pragma unroll
+                for (int u = 0; u < HPL; ++u) {
+                    const int q = lane + 32 * u;
+                    if (q < G && hp[u] != INT_MAX && sq_better(hv[u], hp[u], v, p)) {
+                        v = hv[u]; p = hp[u]; sl = q;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                    const int op = __shfl_xor_sync(0xffffffffu, p, o);
+                    const int osl = __shfl_xor_sync(0xffffffffu, sl, o);
+                    if (osl >= 0 && (sl < 0 || sq_better(ov, op, v, p))) { v = ov; p = op; sl = osl; }
+                }
+                stop = (sl < 0) || !(v > stop2);
+                const double *src = a.slot_data + (int64_t)(par * G + (sl >= 0 ? sl : 0)) * lpad;
+#pragma unroll
+                for (int qq = 0; qq < SQ_RPL; ++qq) {
+                    const int t = lane + 32 * qq;
+                    xv[qq] = (!stop && t < l) ? __ldcg(src + t) : 0.0;
+                }
+                wc = (sl >= 0) ? __ldcg(a.slot_col + par * G + sl) : -1;
+                if (lane == 0) {
+                    s_stop = stop;
+                    s_wpos = p;
+                    s_wcol = wc;
+                    if (g == 0 && want_v2 && !stop) {
+                        double v2 = -1.0;
+                        for (int q = 0; q < G; ++q) {
+                            const double hv = __ldcg(&a.slot_hdr[(int64_t)(par * G + q) * a.hstride].v);
+                            v2 = fmax(v2, (q == sl) ? __ldcg(a.slot_v2 + par * G + q) : hv);
+                        }
+                        a.gaps[j] = (v2 < 0.0 || v == 0.0) ? 1.0 : (v - v2) / v;
+                    }
                 }
             }
             if (!stop) {

@@ -1,44 +1,41 @@
-// sample_qrcp_reg.cuh -- S2 sample QRCP (Alg. 1, on the l x n'
-// sample, Alg. 2 line P:147) over a cooperative GRID with ONE COLUMN PER
-// THREAD: rows 0..LR-1 of the column in registers, rows LR..LR+LS-1 in
-// shared memory ([row][thread], conflict-free); n' <= grid x 256.  Same
-// arithmetic and outputs as sample_qrcp.cuh / sample_qrcp_cl.cuh (dlarfg
-// reading R-G7, squared-norm downdates with the R-G6 recompute, lowest
-// position on ties R-G5, stop rule R-G12); the per-step exchange is the grid
-// kernel's, without fences: every CTA publishes its best candidate (header
-// and column) in a global slot in which each 32-bit half of every word
-// travels with the step's tag in one 64-bit store (two per 16-byte unit, the
-// "low-latency" flag protocol), and warp 0 of every CTA polls the G headers
-// with relaxed loads until the tags match, picks the winner, polls its
-// column the same way and forms the reflector redundantly.  A 64-bit aligned
-// store is single-copy atomic, so a matching tag proves its half is current;
-// no release/acquire fence (each costs an L2 round trip per step) is needed.  CTA 0 holds no columns: it stages the
-// reflectors and R-hat rows in shared memory and writes the outputs at the
-// end (so its shared memory is free for them).  Used for samples larger than one
-// cluster can hold in registers (C3: 16384 columns; C4: 32768 columns of
-// 144 rows).
+// sample_qrcp_reg2.cuh -- S2 sample QRCP (Alg. 1, on the l x n'
+// sample, Alg. 2 line P:147) for samples too wide for sample_qrcp_reg.cuh
+// (C5: 65536 columns of 144 rows = 75.5 MB, more than the 148 SMs' registers
+// and shared memory together).  Same exchange, arithmetic contract and
+// outputs as sample_qrcp_reg_kernel (dlarfg R-G7, squared-norm downdates with
+// the R-G6 recompute, lowest position on ties R-G5, stop rule R-G12; tagged
+// 16-byte slot units, no fences), with two differences:
+//   * TH = 512 threads per CTA, one column per thread (so the grid of
+//     1 + n'/512 CTAs fits one CTA per SM for n' <= 75264);
+//   * each column is split in three row ranges: rows [0, LT) in a global
+//     scratch (transposed [row][thread] per CTA: coalesced), rows
+//     [LT, LT + LR) in registers, rows [LT + LR, L) in shared memory.
+// Step j only touches rows >= j, so the global rows -- the TOP rows -- drop
+// out of the traffic after step LT: summed over a 128-step panel the L2
+// traffic is sum_{j < LT} (LT - j) rows instead of LT rows per step.
+// (The spill kernel, sample_qrcp.cuh, keeps whole columns in L2 and streams
+// all their rows twice per step: 31 us per pivot at C5.)
 #pragma once
 #include <climits>
 #include "common.cuh"
 #include "sample_qrcp.cuh"
+#include "sample_qrcp_reg.cuh"
 
 namespace rq {
 
-#ifndef SQR_TRACE_DETAIL
-#define SQR_TRACE_DETAIL 0
-#endif
-constexpr int SQR_THREADS = 256;
-constexpr int SQR_CH = 16;  // rows per skipped chunk of the register rows (as SQC_CH)
-constexpr int SQR_UNITS = SQ_MAXL + 2;  // 16-byte units per slot: header (2) + column
+constexpr int SQR2_THREADS = 512;
 
-template <int LR, int LS>
-__global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs a) {
-    constexpr int L = LR + LS;
-    extern __shared__ __align__(16) double sq_dyn[];  // max(LS x 256, bb x L) doubles
+template <int LT, int LR, int LS>
+__global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArgs a) {
+    constexpr int TH = SQR2_THREADS;
+    constexpr int NW = TH / 32;
+    constexpr int L = LT + LR + LS;
+    constexpr int R0 = LT, S0 = LT + LR;  // first register row, first shared-memory row
+    extern __shared__ __align__(16) double sq_dyn[];  // max(LS x TH, bb x L) doubles
     __shared__ __align__(16) double xs[L + 1];
     __shared__ double xraw[L];
-    __shared__ double wv[SQ_WARPS];
-    __shared__ int wpos[SQ_WARPS], wcol[SQ_WARPS];
+    __shared__ double wv[NW];
+    __shared__ int wpos[NW], wcol[NW];
     __shared__ double s_tau, s_beta, s_alpha;
     __shared__ int s_wpos, s_wcol, s_stop, s_np;
     __shared__ int64_t low[SQ_MAXB];
@@ -47,20 +44,21 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
     __shared__ int hi_n;
     __shared__ int s_piv[SQ_MAXB];
     __shared__ double s_tauh[SQ_MAXB];
-    __shared__ unsigned long long s_trace[64 * 4];  // RQRCP_TRACE phase stamps
+    __shared__ unsigned long long s_trace[64 * 4];
 
     const int G = gridDim.x, g = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int l = a.l;
     const int64_t nn = a.nn;
-    // CTA 0 records the outputs (no columns); CTAs 1.. hold cpb <= 256 columns each
+    // CTA 0 records the outputs (no columns); CTAs 1.. hold cpb <= TH columns each
     const int64_t cpb = (nn + G - 2) / (G - 1);
     const int64_t c_lo = (g == 0) ? 0 : min(nn, (int64_t)(g - 1) * cpb);
     const int64_t c_hi = (g == 0) ? 0 : min(nn, c_lo + cpb);
     const bool have = tid < (int)(c_hi - c_lo);
     const int64_t pc = c_lo + tid;
-    double *xsm = sq_dyn;   // CTAs >= 1: [LS][256]
-    double *comp = sq_dyn;  // CTA 0: [bb][L]
+    double *xsm = sq_dyn;                                // CTAs >= 1: [LS][TH]
+    double *comp = sq_dyn;                               // CTA 0: [bb][L]
+    double *xt = a.spill + (int64_t)g * LT * TH + tid;   // this thread's top rows, stride TH
     if (*a.status != 0 || *a.done) {
         if (g == 0 && tid == 0) { *a.bb_eff = 0; *a.swap_np = 0; }
         return;
@@ -68,38 +66,26 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
     const double stop2 = *a.stop_tol2;
 
     double x[LR];
-    // the column's entries are contiguous: 16-byte loads when aligned
-    const bool vec = ((a.ldb & 1) == 0) && ((reinterpret_cast<uintptr_t>(a.B) & 15) == 0) && !(LR & 1) && !(LS & 1);
-    if (have && vec) {
-        const double2 *src = reinterpret_cast<const double2 *>(a.B + pc * a.ldb);
-#pragma unroll
-        for (int t = 0; t < LR; t += 2) {
-            const double2 v = src[t / 2];
-            x[t] = v.x;
-            x[t + 1] = v.y;
-        }
+    {
+        const double *src = a.B + pc * a.ldb;
 #pragma unroll 4
-        for (int t = 0; t < LS; t += 2) {
-            const double2 v = src[(LR + t) / 2];
-            xsm[t * SQR_THREADS + tid] = v.x;
-            xsm[(t + 1) * SQR_THREADS + tid] = v.y;
-        }
-    } else {
+        for (int t = 0; t < LT; ++t) xt[t * TH] = have ? src[t] : 0.0;
 #pragma unroll
-        for (int t = 0; t < LR; ++t) x[t] = have ? a.B[t + pc * a.ldb] : 0.0;
+        for (int t = 0; t < LR; ++t) x[t] = have ? src[R0 + t] : 0.0;
 #pragma unroll 4
-        for (int t = 0; t < LS; ++t) xsm[t * SQR_THREADS + tid] = have ? a.B[(LR + t) + pc * a.ldb] : 0.0;
+        for (int t = 0; t < LS; ++t) xsm[t * TH + tid] = have ? src[S0 + t] : 0.0;
     }
     double r = 0.0;
+    for (int t = 0; t < LT; ++t) r += xt[t * TH] * xt[t * TH];
 #pragma unroll
     for (int t = 0; t < LR; ++t) r += x[t] * x[t];
-    for (int t = 0; t < LS; ++t) r += xsm[t * SQR_THREADS + tid] * xsm[t * SQR_THREADS + tid];
+    for (int t = 0; t < LS; ++t) r += xsm[t * TH + tid] * xsm[t * TH + tid];
     double r0 = r;
     int lpos = (int)pc;
     bool act = have;
     if (have) a.perm[pc] = pc;
     if (g == 0) {
-        for (int q = tid; q < a.bb; q += SQR_THREADS) low[q] = q;
+        for (int q = tid; q < a.bb; q += TH) low[q] = q;
         if (tid == 0) hi_n = 0;
     }
 
@@ -118,12 +104,13 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
         __syncthreads();
         double bv = wv[0];
         int bp = wpos[0], bc = wcol[0];
-        for (int w = 1; w < SQ_WARPS; ++w)
+        for (int w = 1; w < NW; ++w)
             if (sq_better(wv[w], wpos[w], bv, bp)) { bv = wv[w]; bp = wpos[w]; bc = wcol[w]; }
-        // the owner stages its register rows in xraw (free until the next poll)
+        // the owner stages its top and register rows in xraw (free until the next poll)
         if (act && (int)pc == bc) {
+            for (int t = 0; t < LT; ++t) xraw[t] = xt[t * TH];
 #pragma unroll
-            for (int t = 0; t < LR; ++t) xraw[t] = x[t];
+            for (int t = 0; t < LR; ++t) xraw[R0 + t] = x[t];
         }
         __syncthreads();
         if (warp == 0) {
@@ -132,7 +119,7 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
             if (bc >= 0) {
                 const int oc = bc - (int)c_lo;
                 for (int t = lane; t < l; t += 32) {
-                    const double xv = (t < LR) ? xraw[t] : xsm[(t - LR) * SQR_THREADS + oc];
+                    const double xv = (t < S0) ? xraw[t] : xsm[(t - S0) * TH + oc];
                     ll_store(dst + 2 + t, (unsigned long long)__double_as_longlong(xv), tg);
                 }
             }
@@ -142,12 +129,10 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
     };
 
     if (a.trace)
-        for (int e = tid; e < 64 * 4; e += SQR_THREADS) s_trace[e] = 0ull;
+        for (int e = tid; e < 64 * 4; e += TH) s_trace[e] = 0ull;
     publish(0);
 
     int j = 0;
-    // phase stamps (RQRCP_TRACE): kept in shared memory, written at the end so
-    // the trace adds no global traffic to the steps it measures
     auto stamp = [&](int ph) {
         if (a.trace && tid == 0 && j < 64) s_trace[j * 4 + ph] = clock64();
     };
@@ -179,9 +164,6 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
                 }
                 if (__all_sync(0xffffffffu, all)) break;
             }
-#if SQR_TRACE_DETAIL
-            stamp(1);
-#endif
 #pragma unroll
             for (int u = 0; u < HPL; ++u) {
                 const int q = lane + 32 * u;
@@ -219,9 +201,6 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
                     }
                     if (__all_sync(0xffffffffu, all)) break;
                 }
-#if SQR_TRACE_DETAIL
-                stamp(2);
-#endif
             }
             if (lane == 0) { s_stop = stop; s_wpos = p; s_wcol = wc; }
             if (!stop) {
@@ -255,19 +234,15 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
             }
         }
         __syncthreads();
-#if SQR_TRACE_DETAIL
-        stamp(3);
-#else
         stamp(1);
-#endif
         if (s_stop) break;
         const int wp = s_wpos, wcl = s_wcol;
         const double tau = s_tau;
         if (g == 0) {
-            for (int t = tid; t < L; t += SQR_THREADS) comp[j * L + t] = (t < j) ? xraw[t] : (t == j ? s_beta : xs[t]);
+            for (int t = tid; t < L; t += TH) comp[j * L + t] = (t < j) ? xraw[t] : (t == j ? s_beta : xs[t]);
             if (tid == 0) { s_piv[j] = wp; s_tauh[j] = tau; }
         }
-        if (g == 0 && warp == SQ_WARPS - 1) {
+        if (g == 0 && warp == NW - 1) {
             const int64_t q = low[j];
             __syncwarp();
             if (lane == 0) low[j] = wcl;
@@ -292,110 +267,155 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
         // ---- 2. apply H_j to this thread's column, downdate the norm ---------
         if (act && (int)pc == wcl) act = false;
         if (act) {
-            // w = v^T x over rows >= j (xs is zero above row j); SQR_CH-row chunks
-            // entirely above row j are skipped (uniform branches); four
-            // independent accumulators
+            // w = v^T x over rows >= j (xs is zero above row j): top rows (global,
+            // only while j < LT; all loads of a batch in flight), register rows
+            // (SQR_CH chunks entirely above row j skipped), shared-memory rows
             double d[4] = {0.0, 0.0, 0.0, 0.0};
+            if (j < LT) {  // batches of 8 loads in flight (one L2 round trip each)
+                int t = j;
+                for (; t + 7 < LT; t += 8) {
+                    double y[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) y[u] = xt[(t + u) * TH];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) d[u & 3] += xs[t + u] * y[u];
+                }
+                for (; t < LT; ++t) d[0] += xs[t] * xt[t * TH];
+            }
 #pragma unroll
             for (int c0 = 0; c0 < LR; c0 += SQR_CH) {
-                if (j < c0 + SQR_CH) {
+                if (j < R0 + c0 + SQR_CH) {
 #pragma unroll
                     for (int t = c0; t < c0 + SQR_CH && t + 1 < LR; t += 2) {
-                        const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
+                        const double2 v2 = *reinterpret_cast<const double2 *>(&xs[R0 + t]);
                         d[(t >> 1) & 3] += v2.x * x[t] + v2.y * x[t + 1];
                     }
-                    if ((LR & 1) && c0 + SQR_CH >= LR) d[0] += xs[LR - 1] * x[LR - 1];
+                    if ((LR & 1) && c0 + SQR_CH >= LR) d[0] += xs[R0 + LR - 1] * x[LR - 1];
                 }
             }
             if (LS > 0) {
-                int t = (j > LR ? j : LR);
-                const double *xc = xsm + tid - LR * SQR_THREADS;
+                int t = (j > S0 ? j : S0);
+                const double *xc = xsm + tid - S0 * TH;
+                if (t & 1) { d[1] += xs[t] * xc[t * TH]; ++t; }  // (S0 is even)
                 for (; t + 3 < L; t += 4) {
-                    d[0] += xs[t] * xc[t * SQR_THREADS];
-                    d[1] += xs[t + 1] * xc[(t + 1) * SQR_THREADS];
-                    d[2] += xs[t + 2] * xc[(t + 2) * SQR_THREADS];
-                    d[3] += xs[t + 3] * xc[(t + 3) * SQR_THREADS];
+                    const double2 v01 = *reinterpret_cast<const double2 *>(&xs[t]);
+                    const double2 v23 = *reinterpret_cast<const double2 *>(&xs[t + 2]);
+                    d[0] += v01.x * xc[t * TH];
+                    d[1] += v01.y * xc[(t + 1) * TH];
+                    d[2] += v23.x * xc[(t + 2) * TH];
+                    d[3] += v23.y * xc[(t + 3) * TH];
                 }
-                for (; t < L; ++t) d[0] += xs[t] * xc[t * SQR_THREADS];
+                for (; t < L; ++t) d[0] += xs[t] * xc[t * TH];
             }
             const double tw = tau * ((d[0] + d[1]) + (d[2] + d[3]));
-            // x -= tw v; bj = x(j) picked in the chunk that holds row j
+            // x -= tw v; bj = x(j) from the range that holds row j
             double bj = 0.0;
+            if (j < LT) {
+                int t = j;
+                for (; t + 7 < LT; t += 8) {
+                    double y[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) y[u] = xt[(t + u) * TH];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const double nv = y[u] - tw * xs[t + u];
+                        xt[(t + u) * TH] = nv;
+                        if (t + u == j) bj = nv;
+                    }
+                }
+                for (; t < LT; ++t) {
+                    const double nv = xt[t * TH] - tw * xs[t];
+                    xt[t * TH] = nv;
+                    if (t == j) bj = nv;
+                }
+            }
 #pragma unroll
             for (int c0 = 0; c0 < LR; c0 += SQR_CH) {
-                if (j < c0 + SQR_CH) {
+                if (j < R0 + c0 + SQR_CH) {
 #pragma unroll
                     for (int t = c0; t < c0 + SQR_CH && t + 1 < LR; t += 2) {
-                        const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
+                        const double2 v2 = *reinterpret_cast<const double2 *>(&xs[R0 + t]);
                         x[t] -= tw * v2.x;
                         x[t + 1] -= tw * v2.y;
                     }
-                    if ((LR & 1) && c0 + SQR_CH >= LR) x[LR - 1] -= tw * xs[LR - 1];
-                    if (j >= c0) {
+                    if ((LR & 1) && c0 + SQR_CH >= LR) x[LR - 1] -= tw * xs[R0 + LR - 1];
+                    if (j >= R0 + c0) {
 #pragma unroll
-                        for (int t = c0; t < c0 + SQR_CH && t < LR; ++t) bj = (t == j) ? x[t] : bj;
+                        for (int t = c0; t < c0 + SQR_CH && t < LR; ++t) bj = (R0 + t == j) ? x[t] : bj;
                     }
                 }
             }
-#pragma unroll 4
-            for (int t = (j > LR ? j : LR); t < L; ++t) {
-                double *p = &xsm[(t - LR) * SQR_THREADS + tid];
-                const double nv = *p - tw * xs[t];
-                *p = nv;
-                if (t == j) bj = nv;
+            {
+                int t = (j > S0 ? j : S0);
+                if (t & 1) {
+                    double *q = &xsm[(t - S0) * TH + tid];
+                    const double nv = *q - tw * xs[t];
+                    *q = nv;
+                    if (t == j) bj = nv;
+                    ++t;
+                }
+#pragma unroll 2
+                for (; t + 1 < L; t += 2) {
+                    const double2 v01 = *reinterpret_cast<const double2 *>(&xs[t]);
+                    double *q = &xsm[(t - S0) * TH + tid];
+                    const double n0 = q[0] - tw * v01.x;
+                    const double n1 = q[TH] - tw * v01.y;
+                    q[0] = n0;
+                    q[TH] = n1;
+                    if (t == j) bj = n0;
+                    if (t + 1 == j) bj = n1;
+                }
+                for (; t < L; ++t) {
+                    double *q = &xsm[(t - S0) * TH + tid];
+                    const double nv = *q - tw * xs[t];
+                    *q = nv;
+                    if (t == j) bj = nv;
+                }
             }
             double rn = r - bj * bj;
             if (rn < 1e-6 * r0) {  // recompute from the updated rows (R-G6)
                 double s0 = 0.0;
+                for (int t = j + 1; t < LT; ++t) s0 += xt[t * TH] * xt[t * TH];
 #pragma unroll
                 for (int t = 0; t < LR; ++t)
-                    if (t > j) s0 += x[t] * x[t];
-                for (int t = (j + 1 > LR ? j + 1 : LR); t < L; ++t)
-                    s0 += xsm[(t - LR) * SQR_THREADS + tid] * xsm[(t - LR) * SQR_THREADS + tid];
+                    if (R0 + t > j) s0 += x[t] * x[t];
+                for (int t = (j + 1 > S0 ? j + 1 : S0); t < L; ++t) s0 += xsm[(t - S0) * TH + tid] * xsm[(t - S0) * TH + tid];
                 rn = s0;
             }
             r = rn;
             if (lpos == j) lpos = wp;
         }
-#if !SQR_TRACE_DETAIL
         stamp(2);
-#endif
         if (j + 1 < a.bb) publish(j + 1);
-#if !SQR_TRACE_DETAIL
         stamp(3);
-#endif
     }
     __syncthreads();
 
     // ---- results --------------------------------------------------------------
     if (a.trace)
-        for (int e = tid; e < 64 * 4; e += SQR_THREADS)
+        for (int e = tid; e < 64 * 4; e += TH)
             a.trace[(size_t)g * 256 + e] = (e / 4 < min(j + 1, 64)) ? s_trace[e] : 0ull;
-    if (have && vec) {
-        double2 *dst = reinterpret_cast<double2 *>(a.B + pc * a.ldb);
+    if (have) {
+        double *dst = a.B + pc * a.ldb;
+        for (int t = 0; t < LT; ++t) dst[t] = xt[t * TH];
 #pragma unroll
-        for (int t = 0; t < LR; t += 2) dst[t / 2] = make_double2(x[t], x[t + 1]);
-        for (int t = 0; t < LS; t += 2)
-            dst[(LR + t) / 2] = make_double2(xsm[t * SQR_THREADS + tid], xsm[(t + 1) * SQR_THREADS + tid]);
-    } else if (have) {
-#pragma unroll
-        for (int t = 0; t < LR; ++t) a.B[t + pc * a.ldb] = x[t];
-        for (int t = 0; t < LS; ++t) a.B[(LR + t) + pc * a.ldb] = xsm[t * SQR_THREADS + tid];
+        for (int t = 0; t < LR; ++t) dst[R0 + t] = x[t];
+        for (int t = 0; t < LS; ++t) dst[S0 + t] = xsm[t * TH + tid];
     }
     if (g == 0) {
-        for (int e = tid; e < j * a.lpad; e += SQR_THREADS) {
+        for (int e = tid; e < j * a.lpad; e += TH) {
             const int t = e % a.lpad, c = e / a.lpad;
             a.vhat[e] = (t < c || t >= L) ? 0.0 : (t == c ? 1.0 : comp[c * L + t]);
         }
-        for (int e = tid; e < j * a.bbpad; e += SQR_THREADS) {
+        for (int e = tid; e < j * a.bbpad; e += TH) {
             const int t = e % a.bbpad, c = e / a.bbpad;
             a.rhat11[e] = (t <= c) ? comp[c * L + t] : 0.0;
         }
-        for (int c = tid; c < j; c += SQR_THREADS) { a.piv[c] = s_piv[c]; a.tauhat[c] = s_tauh[c]; }
+        for (int c = tid; c < j; c += TH) { a.piv[c] = s_piv[c]; a.tauhat[c] = s_tauh[c]; }
         if (tid == 0) s_np = 0;
         __syncthreads();
         const int nlow = a.bb;
-        for (int e = tid; e < nlow + hi_n; e += SQR_THREADS) {
+        for (int e = tid; e < nlow + hi_n; e += TH) {
             int64_t xq, src;
             if (e < nlow) { xq = e; src = low[e]; }
             else { xq = hi_pos[e - nlow]; src = hi_phys[e - nlow]; }

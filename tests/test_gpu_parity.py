@@ -31,7 +31,7 @@ ELEM_RTOL = 1e-10
 RECON_TOL = 1e-13
 
 DEFAULT_OPTS = dict(schedule=-1, panel=0, upd_kernel=2, pn_blocked=1, tournament=0, gemm_ws=1, pn_cluster=1, pn_cpt=2, pn_grid=0, pn_rows=128, la_panel_ctas=48,
-                    sq_cluster=1, sq_reg=1, sq_grid=0, sq_nsm=-1, sq_hstride=8, sq_poll=1)
+                    sq_cluster=1, sq_reg=1, sq_grid=0, sq_nsm=-1, sq_hstride=8, sq_poll=3)
 
 
 @pytest.fixture(scope="module")
@@ -457,6 +457,21 @@ def test_sample_qrcp_launch_variants(ctx, grid, nsm, name, kind, m, n, k, b, p, 
     compare(A, g, o, k)
 
 
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", SQ_CASES[:3], ids=[c[0] for c in SQ_CASES[:3]])
+def test_sample_qrcp_exchange_modes_bitwise(ctx, name, kind, m, n, k, b, p, seed):
+    """Grid sample QRCP: the tagged-unit exchange (sq_poll 3, no fences) and
+    the release / acquire header exchange (0, 1) move the same candidates and
+    columns: same bits."""
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    outs = []
+    for pm in (0, 1, 3):
+        with options(ctx, sq_grid=7, sq_cluster=0, sq_reg=0, sq_nsm=5, sq_poll=pm):
+            outs.append(gpu_factor(ctx, A, k, b, p, seed))
+    for o in outs[:2]:
+        for key in ("A", "jpvt", "tau"):
+            assert np.array_equal(o[key], outs[2][key])
+
+
 # ---- the register-resident grid sample QRCP (sample_qrcp_reg.cuh) ----------
 REG_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "lowrank", "kfull", "b128")] + [
     ("reg_wide74", "iid", 800, 1900, 192, 64, 10, 21),
@@ -470,6 +485,24 @@ def test_sample_qrcp_register_grid(ctx, name, kind, m, n, k, b, p, seed):
     A = inputs.make(kind, m, n, seed, rank=64).numpy()
     o = oracle.rqrcp(A, k, b, p, seed=seed)
     with options(ctx, sq_cluster=0):
+        g = gpu_factor(ctx, A, k, b, p, seed)
+    compare(A, g, o, k)
+
+
+# the 512-thread register grid with the top 60 rows in global memory
+# (sample_qrcp_reg2.cuh, l = 144: the C5 sample); sq_reg = 2 selects it at
+# oracle-feasible widths, including samples narrower than one CTA per SM
+REG2_CASES = [("reg2_wide144", "graded", 900, 2100, 256, 128, 16, 22),
+              ("reg2_lowrank144", "lowrank", 700, 1300, 300, 128, 16, 23),
+              ("reg2_iid_ragged", "iid", 650, 4997, 384, 128, 16, 24),
+              ("reg2_kfull", "iid", 400, 600, 400, 128, 16, 25)]
+
+
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", REG2_CASES, ids=[c[0] for c in REG2_CASES])
+def test_sample_qrcp_register_grid_top_rows_global(ctx, name, kind, m, n, k, b, p, seed):
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    o = oracle.rqrcp(A, k, b, p, seed=seed)
+    with options(ctx, sq_cluster=0, sq_reg=2):
         g = gpu_factor(ctx, A, k, b, p, seed)
     compare(A, g, o, k)
 
