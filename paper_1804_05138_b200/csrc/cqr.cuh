@@ -17,11 +17,13 @@
 // With this sign choice R_jj = -sign(alpha_j) |R_jj| as LAPACK dlarfg's
 // beta (reading R-G7).
 //
-// The bb x bb factorizations run in one CTA with the matrix entries held in
-// registers (a fixed set per thread) and one __syncthreads per column: the
-// owners of row (and column) j+1 publish it to shared memory during step j.
-// The triangular inverses are block-recursive doublings in shared memory, and
-// the m' x bb products with them run on the FP64 tensor cores (DMMA).
+// The bb x bb factorizations run in one CTA on a shared-memory copy of the
+// matrix (leading dimension nb + 1: row and column walks both free of bank
+// conflicts), right-looking, one __syncthreads per column, two threads per
+// row of the trailing block.  The triangular inverses are block-recursive
+// doublings in shared memory, and every m' x bb or bb x bb product with them
+// (Q1 = P R1^{-1}, V2 = -Qbottom U^{-1}, T = (U S) L^{-T}) runs on the FP64
+// tensor cores (DMMA, cqr_rowmul_kernel).
 //
 // Guard: CholeskyQR2 is accurate when kappa(P) is well below u^{-1/2}.  The
 // first Cholesky must succeed with a diagonal ratio <= CQR_MAX_DIAG_RATIO and
@@ -43,19 +45,20 @@ RQ_DEV void cqr_stamp(int ph) {
 constexpr double CQR_MAX_DIAG_RATIO = 1e5;
 constexpr double CQR_MAX_ORTH_ERR = 1e-4;
 constexpr int CQR_MAXB = 128;
-constexpr int CQR_EPT_U = (CQR_MAXB * (CQR_MAXB + 1) / 2 + CQR_THREADS - 1) / CQR_THREADS;  // 33
-constexpr int CQR_EPT_F = (CQR_MAXB * CQR_MAXB + CQR_THREADS - 1) / CQR_THREADS;            // 64
+// shared memory of the one-CTA kernels: nb x (nb + 1) matrix + (nb/2)^2 scratch
+inline size_t cqr_smem_bytes(int nb) { return ((size_t)nb * (nb + 1) + (size_t)(nb / 2) * (nb / 2)) * sizeof(double); }
 
 // ---------------------------------------------------------------------------
 // In-place inverse of an upper-triangular nb x nb matrix in shared memory
-// (nb = 8 * 2^k, ld nb; identity padding beyond the live size) by
-// block-recursive doubling: invert the 8x8 diagonal blocks, then
+// (nb = 8 * 2^k, leading dimension ld; identity padding beyond the live size)
+// by block-recursive doubling: invert the 8x8 diagonal blocks, then
 // B <- -A^{-1} B D^{-1} for the off-diagonal block of every 2s x 2s block.
+// Only the upper triangle is written (a strictly lower part stays as it is).
 // tmp: nb^2/4 doubles (nb/(2s) blocks of s^2 per level).  All threads of the
 // CTA must call it.
 // ---------------------------------------------------------------------------
-RQ_DEV void tri_inv_upper_smem(double *M, int nb, double *tmp) {
-    const int ld = nb, tid = threadIdx.x;
+RQ_DEV void tri_inv_upper_smem(double *M, int nb, double *tmp, int ld) {
+    const int tid = threadIdx.x;
     // base: 8x8 diagonal blocks, one warp each (lane = column of the block,
     // back substitution down the rows; 8 lanes active)
     {
@@ -74,7 +77,8 @@ RQ_DEV void tri_inv_upper_smem(double *M, int nb, double *tmp) {
                 }
                 __syncwarp(0xffu);
 #pragma unroll
-                for (int r = 0; r < 8; ++r) M[(k0 + r) + (k0 + c) * ld] = x[r];
+                for (int r = 0; r < 8; ++r)
+                    if (r <= c) M[(k0 + r) + (k0 + c) * ld] = x[r];
             }
         }
     }
@@ -175,25 +179,22 @@ RQ_DEV void upper_index(int e, int &a, int &c) {
 // ---------------------------------------------------------------------------
 // Cholesky of the bb x bb Gram matrix (pass 1: G1 = P^T P; pass 2: G2 =
 // Q1^T Q1 with the orthogonality check), the accumulated R factor and the
-// inverse of this pass's R.  One CTA.  The upper triangle is held in
-// registers (element e = tid + 256 i of the packed triangle); step j applies
-// M(a,c) -= M(j,a) M(j,c) / M(j,j) to the elements with a > j, using row j
-// from shared memory, and the owners of row j+1 publish it for step j+1.
-// Outputs (ld bbpad, zero padding): Rc = R (pass 1) or R Rc (pass 2); Rinv.
-// smem: nb^2 + (nb/2)^2 doubles, nb = 8 * 2^k >= bb.
+// inverse of this pass's R.  One CTA, the upper triangle in shared memory:
+// step j applies M(a,c) -= M(j,a) M(j,c) / M(j,j) to j < a <= c (two threads
+// per row a, alternate columns), so M ends as D U with R = D^{1/2} U.
+// Outputs (ld bbpad, zero padding): Rc = R (pass 1) or R Rc (pass 2; the old
+// Rc staged nb/4 columns at a time); Rinv = R^{-1}.
 // ---------------------------------------------------------------------------
-template <int EPT>
 __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_chol_kernel(const double *G /* bbpad x bbpad */, int bb, int bbpad,
                                                                int nb, int pass, const int *bb_eff, int *status,
                                                                double *Rc, double *Rinv, const double *tol2) {
     extern __shared__ __align__(16) double cq_sm[];
-    double *M = cq_sm;              // nb x nb (R, then R^{-1})
-    double *tmp = cq_sm + nb * nb;  // (nb/2)^2
-    __shared__ double rowb[2][CQR_MAXB];
-    __shared__ double s_d[CQR_MAXB];
-    __shared__ double s_idl[2];
-    __shared__ int s_fail;
+    const int ld = nb + 1;
+    double *M = cq_sm;                   // nb x nb, ld nb + 1
+    double *tmp = cq_sm + (size_t)nb * ld;  // (nb/2)^2
+    __shared__ double s_sq[CQR_MAXB];
     __shared__ double s_red[CQR_THREADS / 32];
+    __shared__ int s_bad;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (pass == 1) {
         if (tid == 0) *status = (*bb_eff == bb) ? 0 : 1;
@@ -201,22 +202,16 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_chol_kernel(const double *
     }
     if (*status != 0) return;
     cqr_stamp(0);
-    const int ne = bb * (bb + 1) / 2;
-    double v[EPT];
-    int ea[EPT], ec[EPT];  // element (a, c), a <= c; a = -1: no element
     double mx = 0.0;
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-        const int e = tid + CQR_THREADS * i;
-        int a = 0, c = 0;
-        if (e < ne) upper_index(e, a, c);
-        ea[i] = (e < ne) ? a : -1;
-        ec[i] = c;
-        v[i] = (e < ne) ? G[a + (int64_t)c * bbpad] : 0.0;
-        if (e < ne) mx = fmax(mx, fabs(v[i] - (a == c ? 1.0 : 0.0)));
-        if (e < ne && a == 0) rowb[0][c] = v[i];
+    for (int e = tid; e < nb * nb; e += CQR_THREADS) {
+        const int r = e % nb, c = e / nb;
+        double v = (r == c) ? 1.0 : 0.0;
+        if (r < bb && c < bb) {
+            v = (r <= c) ? G[r + (int64_t)c * bbpad] : 0.0;
+            if (r <= c) mx = fmax(mx, fabs(v - (r == c ? 1.0 : 0.0)));
+        }
+        M[r + c * ld] = v;
     }
-    for (int j = tid; j < CQR_MAXB; j += CQR_THREADS) s_d[j] = 0.0;
     if (pass == 2) {  // max |G2 - I| over the upper triangle
         for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         if (lane == 0) s_red[warp] = mx;
@@ -231,111 +226,135 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_chol_kernel(const double *
         }
     }
     cqr_stamp(1);
-    // step j: M(a,c) -= M(j,a) M(j,c) / M(j,j) for a > j; the owners of row
-    // j+1 publish it, the owner of (j+1, j+1) also 1/M(j+1,j+1) (or a failure)
-    if (tid == 0) {
-        const double d0 = rowb[0][0];
-        s_d[0] = d0;
-        s_idl[0] = fast_rcp(d0);
-        s_fail = !(d0 > 0.0);
-    }
-    __syncthreads();
-    // (a failed pivot only poisons the remaining entries; checked after the loop)
+    // trailing block as a 16 x 16 thread grid: thread (ta, tc) owns rows
+    // j+1+ta+16p and columns j+1+tc+16q (p, q < 8): all loads of a step in flight
+    const int ta = tid & 15, tc = tid >> 4;
     for (int j = 0; j < bb; ++j) {
-        const double *rj = rowb[j & 1];
-        double *rn = rowb[(j + 1) & 1];
-        const double idl = s_idl[j & 1];
-        // all loads first (the stores below may alias them for the compiler),
-        // then the updates, then the publication of row j+1
-        double ra[EPT], rc[EPT];
+        const double idl = fast_rcp(M[j + j * ld]);
+        const int n0 = j + 1;
+        double ma[8], rq[8];
 #pragma unroll
-        for (int i = 0; i < EPT; ++i) {
-            ra[i] = rj[ea[i] > 0 ? ea[i] : 0];
-            rc[i] = rj[ec[i]];
+        for (int u = 0; u < 8; ++u) {
+            const int a = n0 + ta + 16 * u, c = n0 + tc + 16 * u;
+            ma[u] = (a < bb) ? M[j + a * ld] * idl : 0.0;
+            rq[u] = (c < bb) ? M[j + c * ld] : 0.0;
         }
 #pragma unroll
-        for (int i = 0; i < EPT; ++i) v[i] -= (ea[i] > j) ? ra[i] * rc[i] * idl : 0.0;
+        for (int pp = 0; pp < 8; ++pp) {
+            const int a = n0 + ta + 16 * pp;
+            if (a >= bb) break;
 #pragma unroll
-        for (int i = 0; i < EPT; ++i)
-            if (ea[i] == j + 1) rn[ec[i]] = v[i];
-#pragma unroll
-        for (int i = 0; i < EPT; ++i)
-            if (ea[i] == j + 1 && ec[i] == j + 1) {  // next pivot (one thread)
-                s_d[j + 1] = v[i];
-                s_idl[(j + 1) & 1] = fast_rcp(v[i]);
-                if (!(v[i] > 0.0)) s_fail = 1;
+            for (int qq = 0; qq < 8; ++qq) {
+                const int c = n0 + tc + 16 * qq;
+                if (c >= bb) break;
+                if (c >= a) M[a + c * ld] -= ma[pp] * rq[qq];
             }
+        }
         __syncthreads();
     }
-    __syncthreads();
     cqr_stamp(2);
-    // a failed (non-positive / NaN) pivot leaves s_fail set and s_d short
-    {
-        double dmax = 0.0, dmin = 1e308;
-        bool ok = !s_fail;
-        // a diagonal below the R11-diagonal stop threshold (reading R-G12b)
-        // declines: the column-by-column kernel then stops at that column
+    // checks: every pivot positive, none below the R11-diagonal stop threshold
+    // (reading R-G12b: the column-by-column kernel then stops at it), and the
+    // diagonal ratio of R (pass 1)
+    if (warp == 0) {
         const double t2 = (pass == 1 && tol2) ? *tol2 : -1.0;
-        for (int j = 0; j < bb; ++j) {
-            const double dj = s_d[j];
-            ok = ok && (dj > 0.0) && !(dj < t2);
-            dmax = fmax(dmax, dj);
-            dmin = fmin(dmin, dj);
+        bool ok = true;
+        double dmax = 0.0, dmin = 1e308;
+        for (int q = lane; q < bb; q += 32) {
+            const double d = M[q + q * ld];
+            ok = ok && (d > 0.0) && !(d < t2);
+            dmax = fmax(dmax, d);
+            dmin = fmin(dmin, d);
         }
-        // diag(R) = sqrt(d): ratio check on R (pass 1)
-        if (!ok || (pass == 1 && !(dmax <= CQR_MAX_DIAG_RATIO * CQR_MAX_DIAG_RATIO * dmin))) {
-            if (tid == 0) *status = 1;
-            return;
+        for (int o = 16; o > 0; o >>= 1) {
+            dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+            dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
         }
+        ok = __all_sync(0xffffffffu, ok);
+        if (lane == 0)
+            s_bad = !ok || (pass == 1 && !(dmax <= CQR_MAX_DIAG_RATIO * CQR_MAX_DIAG_RATIO * dmin));
     }
-    // R(a, c) = M(a, c) / sqrt(d_a) into smem (upper; identity padding)
-    for (int e = tid; e < nb * nb; e += CQR_THREADS) {
-        const int r = e % nb, c = e / nb;
-        M[e] = (r >= bb || c >= bb) ? (r == c ? 1.0 : 0.0) : 0.0;
+    for (int q = tid; q < bb; q += CQR_THREADS) s_sq[q] = sqrt(M[q + q * ld]);
+    __syncthreads();
+    if (s_bad) {
+        if (tid == 0) *status = 1;
+        return;
+    }
+    // R(a, c) = M(a, c) / sqrt(d_a), R(a, a) = sqrt(d_a)
+    for (int e = tid; e < bb * bb; e += CQR_THREADS) {
+        const int r = e % bb, c = e / bb;
+        if (r < c) M[r + c * ld] /= s_sq[r];
+        else if (r == c) M[r + c * ld] = s_sq[r];
     }
     __syncthreads();
+    if (pass == 1) {
+        for (int e = tid; e < bbpad * bbpad; e += CQR_THREADS) {
+            const int r = e % bbpad, c = e / bbpad;
+            Rc[e] = (r <= c && c < bb) ? M[r + c * ld] : 0.0;
+        }
+    } else {
+        // Rc <- R Rc: nb/4 columns of the old Rc at a time in tmp (written back
+        // only after their own chunk has been staged)
+        const int cw = nb / 4;
+        for (int c0 = 0; c0 < bb; c0 += cw) {
+            const int w = min(cw, bb - c0);
+            for (int e = tid; e < nb * w; e += CQR_THREADS) {
+                const int q = e % nb, cc = e / nb;
+                tmp[e] = (q < bb) ? Rc[q + (int64_t)(c0 + cc) * bbpad] : 0.0;
+            }
+            __syncthreads();
+            // a thread takes row r = tid mod nb of four chunk columns at once
+            // (e = e0 + tid + 256 u: nb divides 256, so r is the same for all four):
+            // four independent chains
+            for (int e0 = 0; e0 < nb * w; e0 += 4 * CQR_THREADS) {
+                int cc[4];
+                double acc[4];
+                const int r = (e0 + tid) % nb;
+                int cmax = -1;
 #pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-        const int a = ea[i], c = ec[i];
-        if (a >= 0) M[a + c * nb] = (a == c) ? sqrt(s_d[a]) : v[i] / sqrt(s_d[a]);
-    }
-    __syncthreads();
-    // Rc = R (pass 1) or R Rc_old (pass 2; staged in Rinv)
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + tid + u * CQR_THREADS;
+                    cc[u] = (e < nb * w) ? e / nb : -1;
+                    acc[u] = 0.0;
+                    if (cc[u] >= 0) cmax = max(cmax, c0 + cc[u]);
+                }
+                for (int q = r; q <= cmax; ++q) {
+                    const double mv = M[r + q * ld];
 #pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-        const int a = ea[i], c = ec[i];
-        if (a < 0) continue;
-        double acc;
-        if (pass == 1) acc = M[a + c * nb];
-        else {
-            acc = 0.0;
-            for (int q = a; q <= c; ++q) acc += M[a + q * nb] * Rc[q + (int64_t)c * bbpad];
+                    for (int u = 0; u < 4; ++u)
+                        if (cc[u] >= 0 && q <= c0 + cc[u]) acc[u] += mv * tmp[q + cc[u] * nb];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int c = c0 + cc[u];
+                    if (cc[u] >= 0 && r <= c && r < bb) Rc[r + (int64_t)c * bbpad] = acc[u];
+                }
+            }
+            __syncthreads();
         }
-        Rinv[a + (int64_t)c * bbpad] = acc;
     }
-    __syncthreads();
-    for (int c = warp; c < bbpad; c += CQR_THREADS / 32)
-        for (int r = lane; r < bbpad; r += 32)
-            Rc[r + (int64_t)c * bbpad] = (r < bb && c < bb && r <= c) ? Rinv[r + (int64_t)c * bbpad] : 0.0;
     cqr_stamp(3);
-    tri_inv_upper_smem(M, nb, tmp);
+    tri_inv_upper_smem(M, nb, tmp, ld);
     __syncthreads();
     cqr_stamp(4);
-    for (int c = warp; c < bbpad; c += CQR_THREADS / 32)
-        for (int r = lane; r < bbpad; r += 32) Rinv[r + (int64_t)c * bbpad] = (r < bb && c < bb) ? M[r + c * nb] : 0.0;
+    for (int e = tid; e < bbpad * bbpad; e += CQR_THREADS) {
+        const int r = e % bbpad, c = e / bbpad;
+        Rinv[e] = (r <= c && c < bb) ? M[r + c * ld] : 0.0;
+    }
 }
 
 // ---------------------------------------------------------------------------
 // Y(r, :) = s X(r, :) R for rows r in [r0, rows), R bbpad x bbpad (entries
 // with row or column >= bb are zero), on the FP64 tensor cores: each warp
-// owns 16 rows and all bbpad columns (mma.sync m8n8k4, A fragments from X in
+// takes 8-row tiles (grid-strided) with all bbpad columns (mma.sync m8n8k4, A fragments from X in
 // global memory, B fragments from R in shared memory with a row stride = 4 mod
 // 16 doubles: conflict-free).  In place allowed (a warp reads all its rows'
 // entries before it writes).  Columns bb..bbpad-1 of Y are written as 0.
 // mode 1 (V2 of the reconstruction): also A(r, c) = Y(r, c) (the panel below
 // the top block) and Vt(c, r) = Y(r, c).  No-op when *status != 0.
 // ---------------------------------------------------------------------------
-constexpr int RM_ROWS = 16;  // rows per warp (2 m8 tiles)
+constexpr int RM_ROWS = 8;   // rows per warp (one m8 tile: no register spills)
+constexpr int RM_MT = RM_ROWS / 8;
 __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_rowmul_kernel(const double *X, int64_t ldx, int64_t r0, int64_t rows,
                                                                  int bb, int bbpad, const double *R, double s,
                                                                  double *Y, int64_t ldy, const int *status, int mode,
@@ -349,55 +368,57 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_rowmul_kernel(const double
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t rbase = r0 + ((int64_t)blockIdx.x * (CQR_THREADS / 32) + warp) * RM_ROWS;
-    if (rbase >= rows) return;
     const int fr = lane >> 2, fk = lane & 3;
-    double acc[2][16][2];
+    const int64_t tstride = (int64_t)gridDim.x * (CQR_THREADS / 32) * RM_ROWS;
+    for (int64_t rbase = r0 + ((int64_t)blockIdx.x * (CQR_THREADS / 32) + warp) * RM_ROWS; rbase < rows;
+         rbase += tstride) {
+        double acc[RM_MT][16][2];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < RM_MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 16; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-    const int NT = bbpad / 8;
-    // all A fragments of this warp's rows first (one round trip), then the MMAs
-    double af[2][CQR_MAXB / 4];
+            for (int nt = 0; nt < 16; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+        const int NT = bbpad / 8;
+        // all A fragments of this warp's rows first (one round trip), then the MMAs
+        double af[RM_MT][CQR_MAXB / 4];
 #pragma unroll
-    for (int kk = 0; kk < CQR_MAXB / 4; ++kk) {
-        const int k = kk * 4 + fk;
+        for (int kk = 0; kk < CQR_MAXB / 4; ++kk) {
+            const int k = kk * 4 + fk;
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-            const int64_t r = rbase + mt * 8 + fr;
-            af[mt][kk] = (kk * 4 < bbpad && r < rows && k < bb) ? X[r + (int64_t)k * ldx] : 0.0;
-        }
-    }
-#pragma unroll
-    for (int kk = 0; kk < CQR_MAXB / 4; ++kk) {
-        if (kk * 4 >= bbpad) break;
-        const int k = kk * 4 + fk;
-#pragma unroll
-        for (int nt = 0; nt < 16; ++nt) {
-            if (nt < NT) {
-                const double b = rm_sm[k + (nt * 8 + fr) * ldr];
-#pragma unroll
-                for (int mt = 0; mt < 2; ++mt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt][kk], b);
+            for (int mt = 0; mt < RM_MT; ++mt) {
+                const int64_t r = rbase + mt * 8 + fr;
+                af[mt][kk] = (kk * 4 < bbpad && r < rows && k < bb) ? X[r + (int64_t)k * ldx] : 0.0;
             }
         }
-    }
-    __syncwarp();
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-        const int64_t r = rbase + mt * 8 + fr;
-        if (r >= rows) continue;
+        for (int kk = 0; kk < CQR_MAXB / 4; ++kk) {
+            if (kk * 4 >= bbpad) break;
+            const int k = kk * 4 + fk;
 #pragma unroll
-        for (int nt = 0; nt < 16; ++nt) {
-            if (nt >= NT) continue;
+            for (int nt = 0; nt < 16; ++nt) {
+                if (nt < NT) {
+                    const double b = rm_sm[k + (nt * 8 + fr) * ldr];
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const int c = nt * 8 + 2 * fk + hh;
-                const double y = (c < bb) ? s * acc[mt][nt][hh] : 0.0;
-                Y[r + (int64_t)c * ldy] = y;
-                if (mode == 1) {
-                    if (c < bb) A[r + (int64_t)c * lda] = y;
-                    vt[c + r * bbpad] = y;
+                    for (int mt = 0; mt < RM_MT; ++mt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt][kk], b);
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int mt = 0; mt < RM_MT; ++mt) {
+            const int64_t r = rbase + mt * 8 + fr;
+            if (r >= rows) continue;
+#pragma unroll
+            for (int nt = 0; nt < 16; ++nt) {
+                if (nt >= NT) continue;
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int c = nt * 8 + 2 * fk + hh;
+                    const double y = (c < bb) ? s * acc[mt][nt][hh] : 0.0;
+                    Y[r + (int64_t)c * ldy] = y;
+                    if (mode == 1) {
+                        if (c < bb) A[r + (int64_t)c * lda] = y;
+                        vt[c + r * bbpad] = y;
+                    }
                 }
             }
         }
@@ -407,158 +428,84 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_rowmul_kernel(const double
 // ---------------------------------------------------------------------------
 // Householder reconstruction of the top bb x bb block (one CTA):
 //   X = -Q(0:bb, 0:bb); for j: S_j = sign(X_jj) (1 if 0); pivot X_jj + S_j;
-//   L(:, j) = X(j+1:, j) / pivot; Schur update  ->  S - Qtop = L U.
-// The entries live in registers (element e = tid + 256 i, row-major index
-// (e / bb, e mod bb)); row and column j+1 are published during step j.
-//   T = (U S) L^{-T}, tau_j = T_jj, R = S Rc, U^{-1} (for V2 = -Qbottom U^{-1}).
+//   L(:, j) = X(j+1:, j) / pivot; Schur update  ->  S - Qtop = L U
+// (right-looking in shared memory, two threads per row of the trailing block,
+// one __syncthreads per column).  Then tau_j = T_jj = U_jj S_j, R = S Rc, and
+// for the host's DMMA products: U S (us), U^{-1} (Uinv; V2 = -Qbottom U^{-1})
+// and L^{-T} (linvt; T = (U S) L^{-T}).
 // Writes: the top block of the panel in A (L strictly below, R on/above), the
-// top bb rows of Vfull (after reading Q's) and Vt, tau, tneg = -T, Uinv; sets
+// top bb rows of Vfull (after reading Q's) and Vt, tau, us, Uinv, linvt; sets
 // *status = 1 (and writes none of the outputs) on a non-finite pivot.
-// smem: nb^2 + (nb/2)^2 doubles.
 // ---------------------------------------------------------------------------
-template <int EPT>
 __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_recon_kernel(double *vfull /* holds Q; ld ldq */, int64_t ldq, int bb,
                                                                 int bbpad, int nb, const double *Rc, int *status,
-                                                                double *A, int64_t lda, double *tau, double *tneg,
-                                                                double *Uinv, double *vt) {
+                                                                double *A, int64_t lda, double *tau, double *us,
+                                                                double *Uinv, double *linvt, double *vt) {
     extern __shared__ __align__(16) double rc_sm[];
-    double *M = rc_sm;             // nb x nb
-    double *tmp = rc_sm + nb * nb; // (nb/2)^2
-    __shared__ double rowb[2][CQR_MAXB], colb[2][CQR_MAXB];
+    const int ld = nb + 1;
+    double *M = rc_sm;                       // nb x nb, ld nb + 1
+    double *tmp = rc_sm + (size_t)nb * ld;   // (nb/2)^2
     __shared__ double sgn[CQR_MAXB], s_piv[CQR_MAXB];
-    __shared__ double s_ip[2];
     __shared__ int s_fail;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x;
+    const int ta = tid & 15, tc = tid >> 4;  // 16 x 16 thread grid over the trailing block
     if (*status != 0) return;
-    const int ne = bb * bb;
-    double v[EPT];
-    int erc[EPT];  // r | c << 16 (r = 0xffff: no element)
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-        const int e = tid + CQR_THREADS * i;
-        const int r = (e < ne) ? e / bb : -1, c = (e < ne) ? e % bb : 0;
-        erc[i] = (r & 0xffff) | (c << 16);
-        v[i] = (e < ne) ? -vfull[r + (int64_t)c * ldq] : 0.0;
-        if (r == 0) rowb[0][c] = v[i];
-        if (e < ne && c == 0) colb[0][r] = v[i];
+    cqr_stamp(0);
+    for (int e = tid; e < nb * nb; e += CQR_THREADS) {
+        const int r = e % nb, c = e / nb;
+        M[r + c * ld] = (r < bb && c < bb) ? -vfull[r + (int64_t)c * ldq] : (r == c ? 1.0 : 0.0);
     }
-    __syncthreads();
-    // step j: X(r,c) -= X(r,j) X(j,c) / piv_j for r, c > j; the owners of row
-    // and column j+1 publish them, the owner of (j+1, j+1) the next pivot
-    // (with its sign S_{j+1}) and its reciprocal
-    if (tid == 0) {
-        const double a0 = rowb[0][0];
-        const double sj = (a0 < 0.0) ? -1.0 : 1.0;
-        sgn[0] = sj;
-        s_piv[0] = a0 + sj;
-        s_ip[0] = fast_rcp(a0 + sj);
-        s_fail = !isfinite(a0);
-    }
+    if (tid == 0) s_fail = 0;
     __syncthreads();
     for (int j = 0; j < bb; ++j) {
-        const double *rj = rowb[j & 1], *cj = colb[j & 1];
-        double *rn = rowb[(j + 1) & 1], *cn = colb[(j + 1) & 1];
-        const double ip = s_ip[j & 1];
-        // all loads first, then the updates, then the publication
-        double xr[EPT], xc[EPT];
+        const double xjj = M[j + j * ld];
+        const double sj = (xjj < 0.0) ? -1.0 : 1.0;
+        const double piv = xjj + sj;
+        const double ip = fast_rcp(piv);
+        if (tid == 0) {
+            sgn[j] = sj;
+            s_piv[j] = piv;
+            if (!isfinite(xjj)) s_fail = 1;
+        }
+        const int n0 = j + 1;
+        double xr[8], xc[8];
 #pragma unroll
-        for (int i = 0; i < EPT; ++i) {
-            xr[i] = cj[(erc[i] & 0xffff) & 127];
-            xc[i] = rj[erc[i] >> 16];
+        for (int u = 0; u < 8; ++u) {
+            const int r = n0 + ta + 16 * u, c = n0 + tc + 16 * u;
+            xr[u] = (r < bb) ? M[r + j * ld] * ip : 0.0;
+            xc[u] = (c < bb) ? M[j + c * ld] : 0.0;
         }
 #pragma unroll
-        for (int i = 0; i < EPT; ++i) {
-            const int r = erc[i] & 0xffff, c = erc[i] >> 16;  // r = 0xffff: no element
-            const bool act = (r > j) && (c > j) && (r != 0xffff);
-            v[i] -= act ? xr[i] * ip * xc[i] : 0.0;
-        }
+        for (int pp = 0; pp < 8; ++pp) {
+            const int r = n0 + ta + 16 * pp;
+            if (r >= bb) break;
 #pragma unroll
-        for (int i = 0; i < EPT; ++i) {
-            const int r = erc[i] & 0xffff, c = erc[i] >> 16;
-            const bool act = (r > j) && (c > j) && (r != 0xffff);
-            if (act && r == j + 1) rn[c] = v[i];
-            if (act && c == j + 1) cn[r] = v[i];
-        }
-#pragma unroll
-        for (int i = 0; i < EPT; ++i)
-            if ((erc[i] & 0xffff) == j + 1 && (erc[i] >> 16) == j + 1) {  // next pivot (one thread)
-                const double sn = (v[i] < 0.0) ? -1.0 : 1.0;
-                sgn[j + 1] = sn;
-                s_piv[j + 1] = v[i] + sn;
-                s_ip[(j + 1) & 1] = fast_rcp(v[i] + sn);
-                if (!isfinite(v[i])) s_fail = 1;
+            for (int qq = 0; qq < 8; ++qq) {
+                const int c = n0 + tc + 16 * qq;
+                if (c >= bb) break;
+                M[r + c * ld] -= xr[pp] * xc[qq];
             }
+        }
         __syncthreads();
     }
-    const bool bad = s_fail;
-    __syncthreads();
-    if (bad) {
+    cqr_stamp(1);
+    if (s_fail) {
         if (tid == 0) *status = 1;
         return;
     }
-    // final entries: L(r, c) = X(r, c) / piv_c (r > c); U(r, c) = X(r, c) (r < c), U(c, c) = piv_c
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-        const int r = erc[i] & 0xffff, c = erc[i] >> 16;
-        if (r == 0xffff) continue;
-        if (r > c) v[i] /= s_piv[c];
-        else if (r == c) v[i] = s_piv[c];
-    }
-    // U -> smem -> U^{-1} -> Uinv (global)
-    for (int e = tid; e < nb * nb; e += CQR_THREADS) {
-        const int r = e % nb, c = e / nb;
-        M[e] = (r >= bb || c >= bb) ? (r == c ? 1.0 : 0.0) : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-        const int r = erc[i] & 0xffff, c = erc[i] >> 16;
-        if (r != 0xffff && r <= c) M[r + c * nb] = v[i];
-    }
-    __syncthreads();
-    tri_inv_upper_smem(M, nb, tmp);
-    __syncthreads();
-    for (int c = warp; c < bbpad; c += CQR_THREADS / 32)
-        for (int r = lane; r < bbpad; r += 32) Uinv[r + (int64_t)c * bbpad] = (r < bb && c < bb) ? M[r + c * nb] : 0.0;
-    __syncthreads();
-    // L^T (unit upper) -> smem -> L^{-T}
-    for (int e = tid; e < nb * nb; e += CQR_THREADS) {
-        const int r = e % nb, c = e / nb;
-        M[e] = (r == c) ? 1.0 : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-        const int r = erc[i] & 0xffff, c = erc[i] >> 16;
-        if (r != 0xffff && r > c) M[c + r * nb] = v[i];
-    }
-    __syncthreads();
-    tri_inv_upper_smem(M, nb, tmp);
-    __syncthreads();
-    // T(r, c) = sum_{r <= q <= c} U(r, q) S_q Linv^T(q, c): U from registers via tmp? -> use vt scratch:
-    // stage U (upper) row-major in Vt's top block rows (they are rewritten below)
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-        const int r = erc[i] & 0xffff, c = erc[i] >> 16;
-        if (r != 0xffff && r <= c) vt[c + (int64_t)r * bbpad] = v[i] * sgn[c];
-    }
-    __syncthreads();
-    for (int e = tid; e < bbpad * bbpad; e += CQR_THREADS) {
-        const int r = e / bbpad, c = e % bbpad;
-        double acc = 0.0;
-        if (r < bb && c < bb && r <= c)
-            for (int q = r; q <= c; ++q) acc += vt[q + (int64_t)r * bbpad] * M[q + c * nb];
-        tneg[r + (int64_t)c * bbpad] = -acc;
-        if (r == c && r < bb) tau[r] = acc;
+    // L(r, c) = X(r, c) / piv_c (r > c); U(c, c) = piv_c; U(r, c) = X(r, c) (r < c)
+    for (int e = tid; e < bb * bb; e += CQR_THREADS) {
+        const int r = e % bb, c = e / bb;
+        if (r > c) M[r + c * ld] /= s_piv[c];
+        else if (r == c) M[r + c * ld] = s_piv[c];
     }
     __syncthreads();
     // panel top block: L strictly below, R = S Rc on/above; Vt / Vfull top rows
-#pragma unroll
-    for (int i = 0; i < EPT; ++i) {
-        const int r = erc[i] & 0xffff, c = erc[i] >> 16;
-        if (r == 0xffff) continue;
-        A[r + (int64_t)c * lda] = (r > c) ? v[i] : sgn[r] * Rc[r + (int64_t)c * bbpad];
-        const double vv = (r > c) ? v[i] : (r == c ? 1.0 : 0.0);
+    for (int e = tid; e < bb * bb; e += CQR_THREADS) {
+        const int r = e % bb, c = e / bb;
+        const double x = M[r + c * ld];
+        A[r + (int64_t)c * lda] = (r > c) ? x : sgn[r] * Rc[r + (int64_t)c * bbpad];
+        const double vv = (r > c) ? x : (r == c ? 1.0 : 0.0);
         vt[c + (int64_t)r * bbpad] = vv;
         vfull[r + (int64_t)c * ldq] = vv;
     }
@@ -567,6 +514,34 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_recon_kernel(double *vfull
         vt[c + (int64_t)r * bbpad] = 0.0;
         vfull[r + (int64_t)c * ldq] = 0.0;
     }
+    for (int c = tid; c < bb; c += CQR_THREADS) tau[c] = s_piv[c] * sgn[c];
+    for (int e = tid; e < bbpad * bbpad; e += CQR_THREADS) {
+        const int r = e % bbpad, c = e / bbpad;
+        us[e] = (r <= c && c < bb) ? M[r + c * ld] * sgn[c] : 0.0;
+    }
+    __syncthreads();
+    // U^{-1} (upper, in place; L below untouched)
+    tri_inv_upper_smem(M, nb, tmp, ld);
+    __syncthreads();
+    for (int e = tid; e < bbpad * bbpad; e += CQR_THREADS) {
+        const int r = e % bbpad, c = e / bbpad;
+        Uinv[e] = (r <= c && c < bb) ? M[r + c * ld] : 0.0;
+    }
+    __syncthreads();
+    // upper := L^T (unit upper) from the strict lower part, then L^{-T}
+    for (int e = tid; e < nb * nb; e += CQR_THREADS) {
+        const int r = e % nb, c = e / nb;
+        if (r < c) M[r + c * ld] = (c < bb) ? M[c + r * ld] : 0.0;
+        else if (r == c) M[r + c * ld] = 1.0;
+    }
+    __syncthreads();
+    tri_inv_upper_smem(M, nb, tmp, ld);
+    __syncthreads();
+    for (int e = tid; e < bbpad * bbpad; e += CQR_THREADS) {
+        const int r = e % bbpad, c = e / bbpad;
+        linvt[e] = (r <= c && c < bb) ? M[r + c * ld] : 0.0;
+    }
+    cqr_stamp(2);
 }
 
 }  // namespace rq

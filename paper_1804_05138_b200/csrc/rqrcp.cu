@@ -765,10 +765,8 @@ static int create_impl(rqrcp_ctx **out, const rqrcp_config *cfg, int nranks, int
     CKC(smem_attr((const void *)sample_qrcp_cluster_kernel<40>, 128 * 40 * 8, dev));
     CKC(smem_attr((const void *)sample_qrcp_cluster_kernel<74>, 128 * 74 * 8, dev));
     CKC(smem_attr((const void *)sample_qrcp_cluster_kernel<80>, 128 * 80 * 8, dev));
-    CKC(smem_attr((const void *)cqr_chol_kernel<9>, (128 * 128 + 64 * 64) * 8, dev));
-    CKC(smem_attr((const void *)cqr_chol_kernel<CQR_EPT_U>, (128 * 128 + 64 * 64) * 8, dev));
-    CKC(smem_attr((const void *)cqr_recon_kernel<16>, (128 * 128 + 64 * 64) * 8, dev));
-    CKC(smem_attr((const void *)cqr_recon_kernel<CQR_EPT_F>, (128 * 128 + 64 * 64) * 8, dev));
+    CKC(smem_attr((const void *)cqr_chol_kernel, (int)cqr_smem_bytes(128), dev));
+    CKC(smem_attr((const void *)cqr_recon_kernel, (int)cqr_smem_bytes(128), dev));
     CKC(smem_attr((const void *)cqr_rowmul_kernel, 128 * 132 * 8, dev));
     {
         ctx->sqc_max = 0;
@@ -1630,44 +1628,45 @@ struct Run {
         }
         int nb = 8;
         while (nb < bbpad) nb *= 2;
-        const size_t csm = ((size_t)nb * nb + (size_t)(nb / 2) * (nb / 2)) * sizeof(double);
+        const size_t csm = cqr_smem_bytes(nb);
         const size_t rsm = (size_t)bbpad * (bbpad + 4) * sizeof(double);
-        const int rows_per_cta = RM_ROWS * (CQR_THREADS / 32);
-        const int rgrid = (int)std::max<int64_t>(1, (mp + rows_per_cta - 1) / rows_per_cta);
+        // DMMA row products: grid-strided 8-row tiles, at most one CTA per SM
+        auto rgrid = [&](int64_t rows) {
+            return (int)std::max<int64_t>(1, std::min<int64_t>(G, (rows + 8 * (CQR_THREADS / 32) - 1) / (8 * (CQR_THREADS / 32))));
+        };
         bool dn = false;
         // G1 = P^T P
         CKT(tma_skinny(ctx, bb, bb, mp, ctx->pbuf, m, bb, ldp, i, 0, ctx->pbuf, m, bb, ldp, i, 0, ctx->cq_g, bbpad, &dn, 128));
         if (!dn) CKT(gemm_skinny(ctx, bb, bb, mp, Pp, ldp, Pp, ldp, ctx->cq_g, bbpad));
-        if (bb <= 64) cqr_chol_kernel<9><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 1, bb_eff, ctx->cqr_status,
-                                                                   ctx->cq_rc, ctx->cq_rinv, ctx->ptol2);
-        else cqr_chol_kernel<CQR_EPT_U><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 1, bb_eff, ctx->cqr_status,
-                                                                    ctx->cq_rc, ctx->cq_rinv, ctx->ptol2);
+        cqr_chol_kernel<<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 1, bb_eff, ctx->cqr_status, ctx->cq_rc,
+                                                    ctx->cq_rinv, ctx->ptol2);
         CKL();
-        cqr_rowmul_kernel<<<rgrid, CQR_THREADS, rsm, st>>>(Pp, ldp, 0, mp, bb, bbpad, ctx->cq_rinv, 1.0, vfull, ldv,
-                                                           ctx->cqr_status, 0, nullptr, 0, nullptr);
+        // Q1 = P R1^{-1}
+        cqr_rowmul_kernel<<<rgrid(mp), CQR_THREADS, rsm, st>>>(Pp, ldp, 0, mp, bb, bbpad, ctx->cq_rinv, 1.0, vfull, ldv,
+                                                               ctx->cqr_status, 0, nullptr, 0, nullptr);
         CKL();
+        // G2 = Q1^T Q1, R2, Rc = R2 R1
         CKT(tma_skinny(ctx, bb, bb, mp, vfull, mp, bbpad, ldv, 0, 0, vfull, mp, bbpad, ldv, 0, 0, ctx->cq_g, bbpad, &dn, 128));
         if (!dn) CKT(gemm_skinny(ctx, bb, bb, mp, vfull, ldv, vfull, ldv, ctx->cq_g, bbpad));
-        if (bb <= 64) cqr_chol_kernel<9><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 2, bb_eff, ctx->cqr_status,
-                                                                   ctx->cq_rc, ctx->cq_rinv, nullptr);
-        else cqr_chol_kernel<CQR_EPT_U><<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 2, bb_eff, ctx->cqr_status,
-                                                                    ctx->cq_rc, ctx->cq_rinv, nullptr);
+        cqr_chol_kernel<<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 2, bb_eff, ctx->cqr_status, ctx->cq_rc,
+                                                    ctx->cq_rinv, nullptr);
         CKL();
-        cqr_rowmul_kernel<<<rgrid, CQR_THREADS, rsm, st>>>(vfull, ldv, 0, mp, bb, bbpad, ctx->cq_rinv, 1.0, vfull, ldv,
-                                                           ctx->cqr_status, 0, nullptr, 0, nullptr);
+        // Q = Q1 R2^{-1} (in place)
+        cqr_rowmul_kernel<<<rgrid(mp), CQR_THREADS, rsm, st>>>(vfull, ldv, 0, mp, bb, bbpad, ctx->cq_rinv, 1.0, vfull, ldv,
+                                                               ctx->cqr_status, 0, nullptr, 0, nullptr);
         CKL();
-        if (bb <= 64)
-            cqr_recon_kernel<16><<<1, CQR_THREADS, csm, st>>>(vfull, ldv, bb, bbpad, nb, ctx->cq_rc, ctx->cqr_status, Pp,
-                                                              ldp, tau + i, ctx->tneg, ctx->cq_uinv, vt);
-        else
-            cqr_recon_kernel<CQR_EPT_F><<<1, CQR_THREADS, csm, st>>>(vfull, ldv, bb, bbpad, nb, ctx->cq_rc,
-                                                                     ctx->cqr_status, Pp, ldp, tau + i, ctx->tneg,
-                                                                     ctx->cq_uinv, vt);
+        // reconstruction of the top block: L, U S, U^{-1}, L^{-T} (L^{-T} into cq_g: G2 is consumed)
+        cqr_recon_kernel<<<1, CQR_THREADS, csm, st>>>(vfull, ldv, bb, bbpad, nb, ctx->cq_rc, ctx->cqr_status, Pp, ldp,
+                                                     tau + i, ctx->cq_lu, ctx->cq_uinv, ctx->cq_g, vt);
         CKL();
+        // -T = -(U S) L^{-T}
+        cqr_rowmul_kernel<<<1, CQR_THREADS, rsm, st>>>(ctx->cq_lu, bbpad, 0, bbpad, bb, bbpad, ctx->cq_g, -1.0, ctx->tneg,
+                                                       bbpad, ctx->cqr_status, 0, nullptr, 0, nullptr);
+        CKL();
+        // V2 = -Qbottom U^{-1} (into Vfull, the panel and Vt)
         if (mp > bb) {
-            const int vgrid = (int)std::max<int64_t>(1, (mp - bb + rows_per_cta - 1) / rows_per_cta);
-            cqr_rowmul_kernel<<<vgrid, CQR_THREADS, rsm, st>>>(vfull, ldv, bb, mp, bb, bbpad, ctx->cq_uinv, -1.0, vfull,
-                                                               ldv, ctx->cqr_status, 1, Pp, ldp, vt);
+            cqr_rowmul_kernel<<<rgrid(mp - bb), CQR_THREADS, rsm, st>>>(vfull, ldv, bb, mp, bb, bbpad, ctx->cq_uinv, -1.0,
+                                                                        vfull, ldv, ctx->cqr_status, 1, Pp, ldp, vt);
             CKL();
         }
         return 0;
