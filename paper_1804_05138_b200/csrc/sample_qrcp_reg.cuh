@@ -310,11 +310,15 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
             if (LS > 0) {
                 int t = (j > LR ? j : LR);
                 const double *xc = xsm + tid - LR * SQR_THREADS;
+                if ((t & 1) && t < L) { d[1] += xs[t] * xc[t * SQR_THREADS]; ++t; }  // (LR is even)
+                // pairs of the reflector from one 16-byte broadcast load
                 for (; t + 3 < L; t += 4) {
-                    d[0] += xs[t] * xc[t * SQR_THREADS];
-                    d[1] += xs[t + 1] * xc[(t + 1) * SQR_THREADS];
-                    d[2] += xs[t + 2] * xc[(t + 2) * SQR_THREADS];
-                    d[3] += xs[t + 3] * xc[(t + 3) * SQR_THREADS];
+                    const double2 v01 = *reinterpret_cast<const double2 *>(&xs[t]);
+                    const double2 v23 = *reinterpret_cast<const double2 *>(&xs[t + 2]);
+                    d[0] += v01.x * xc[t * SQR_THREADS];
+                    d[1] += v01.y * xc[(t + 1) * SQR_THREADS];
+                    d[2] += v23.x * xc[(t + 2) * SQR_THREADS];
+                    d[3] += v23.y * xc[(t + 3) * SQR_THREADS];
                 }
                 for (; t < L; ++t) d[0] += xs[t] * xc[t * SQR_THREADS];
             }
@@ -337,12 +341,32 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
                     }
                 }
             }
-#pragma unroll 4
-            for (int t = (j > LR ? j : LR); t < L; ++t) {
-                double *p = &xsm[(t - LR) * SQR_THREADS + tid];
-                const double nv = *p - tw * xs[t];
-                *p = nv;
-                if (t == j) bj = nv;
+            {
+                int t = (j > LR ? j : LR);
+                if ((t & 1) && t < L) {
+                    double *q = &xsm[(t - LR) * SQR_THREADS + tid];
+                    const double nv = *q - tw * xs[t];
+                    *q = nv;
+                    if (t == j) bj = nv;
+                    ++t;
+                }
+#pragma unroll 2
+                for (; t + 1 < L; t += 2) {
+                    const double2 v01 = *reinterpret_cast<const double2 *>(&xs[t]);
+                    double *q = &xsm[(t - LR) * SQR_THREADS + tid];
+                    const double n0 = q[0] - tw * v01.x;
+                    const double n1 = q[SQR_THREADS] - tw * v01.y;
+                    q[0] = n0;
+                    q[SQR_THREADS] = n1;
+                    if (t == j) bj = n0;
+                    if (t + 1 == j) bj = n1;
+                }
+                for (; t < L; ++t) {
+                    double *q = &xsm[(t - LR) * SQR_THREADS + tid];
+                    const double nv = *q - tw * xs[t];
+                    *q = nv;
+                    if (t == j) bj = nv;
+                }
             }
             double rn = r - bj * bj;
             if (rn < 1e-6 * r0) {  // recompute from the updated rows (R-G6)
