@@ -129,11 +129,10 @@ __global__ void __launch_bounds__(TRI_THREADS) tri_kernel(const double *ybuf /* 
         // upper: R11 (identity padding); strict lower M(r, c) (r > c) = R-hat11(c, r); dg = diag(R-hat11)
         for (int e = tid; e < nb * nb; e += blockDim.x) {
             const int r = e % nb, c = e / nb;
+            if (r > c) continue;  // the strict lower part is the next loop's
             double v = 0.0;
-            if (r <= c) {
-                if (r < bb && c < bb) v = R11[r + (int64_t)c * lda];
-                else if (r == c) v = 1.0;
-            }
+            if (r < bb && c < bb) v = R11[r + (int64_t)c * lda];
+            else if (r == c) v = 1.0;
             M[r + c * ld] = v;
         }
         for (int e = tid; e < nb * nb; e += blockDim.x) {
