@@ -423,7 +423,7 @@ static int tma_skinny(rqrcp_ctx *ctx, int64_t M, int64_t N, int64_t K, const dou
     if (M <= 64) return TS(4, 4, 2, 4);
     if (M <= 80) return TS(5, 4, 2, 4);
     if (M <= 128) return TS(4, 4, 4, 2);
-    if (M <= 144) return TS(6, 4, 3, 2);
+    if (M <= 144) return TS(9, 2, 2, 4);  // 8 consumer warps (2 per sub-partition)
 #undef TS
     return 0;
 }
