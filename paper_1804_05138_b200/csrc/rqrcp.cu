@@ -1700,7 +1700,11 @@ struct Run {
                            &dn, 512, npp));
             if (!dn) CKT(gemm_skinny(ctx, bbpad, npl, mp, vfull, ldv, A22, lda, ctx->w, bbpad, npp));
             CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
-            CKT(gemm_skinny(ctx, bbpad, npl, bbpad, ctx->tneg, bbpad, ctx->w, bbpad, ctx->w2, bbpad, npp));
+            // W2 = -T^T W (K = bbpad: no split; the persistent TMA kernel when the
+            // operands allow it -- decided by pointers and sizes only, never by P)
+            CKT(tma_skinny(ctx, bbpad, npl, bbpad, ctx->tneg, bbpad, bbpad, bbpad, 0, 0, ctx->w, bbpad, npl, bbpad, 0,
+                           0, ctx->w2, bbpad, &dn, 512, npp));
+            if (!dn) CKT(gemm_skinny(ctx, bbpad, npl, bbpad, ctx->tneg, bbpad, ctx->w, bbpad, ctx->w2, bbpad, npp));
             if (s == 0) {
                 CKT(update_any(ctx, mp, npl, bbpad, ctx->w2, bbpad, vt, bbpad, A22, lda));
             } else {
