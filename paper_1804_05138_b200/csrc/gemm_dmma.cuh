@@ -180,8 +180,18 @@ __global__ void splitk_reduce_kernel(const double *P, int64_t M, int64_t N, int 
                                      int64_t ldc) {
     const int64_t total = M * N;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        // slices added in order q = 0, 1, ... (fixed: deterministic); loads in
+        // batches of 8 so a many-slice reduce is not one L2 latency per slice
         double s = 0.0;
-        for (int q = 0; q < splits; ++q) s += P[q * stride + e];
+        int q = 0;
+        for (; q + 8 <= splits; q += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = P[(int64_t)(q + u) * stride + e];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += v[u];
+        }
+        for (; q < splits; ++q) s += P[(int64_t)q * stride + e];
         const int64_t m = e % M, n = e / M;
         C[m + n * ldc] = s;
     }

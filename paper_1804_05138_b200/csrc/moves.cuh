@@ -120,8 +120,19 @@ __global__ void colsumsq_kernel(const double *P, int64_t ldp, int64_t rows, int 
     if (*bb_eff == 0) return;
     const int c = blockIdx.x;
     const double *x = P + (int64_t)c * ldp;
-    double s = 0.0;
-    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) s += x[r] * x[r];
+    // eight independent partial sums (eight loads in flight per thread), then a fixed tree
+    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    const int64_t step = (int64_t)blockDim.x;
+    int64_t r = threadIdx.x;
+    for (; r + 7 * step < rows; r += 8 * step) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = x[r + u * step];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] += v[u] * v[u];
+    }
+    for (int u = 0; r < rows; r += step, ++u) a[u] += x[r] * x[r];
+    double s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     s = warp_sum(s);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
     __syncthreads();
