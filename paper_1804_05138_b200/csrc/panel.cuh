@@ -114,16 +114,15 @@ __global__ void __launch_bounds__(PN_THREADS) panel_qr_kernel(PanelArgs a) {
             const int cb = min(32, bb - 32 * q);
             for (int r = rs + tid; r < nrows; r += PN_THREADS) {
                 const double xr = Pv(r, j);
-                if (r < nsm) {
-                    const double *pr = Ps + r + (int64_t)(32 * q) * lds;
+                // one running pointer (no 32 precomputed 64-bit addresses: the
+                // kernel sits at the register limit)
+                const bool sm = r < nsm;
+                const int64_t ld = sm ? lds : lda;
+                const double *pr = sm ? Ps + r + (int64_t)(32 * q) * lds : Pg + r + (int64_t)(32 * q) * lda;
 #pragma unroll
-                    for (int u = 0; u < 32; ++u)
-                        if (u < cb) acc[u] += pr[(int64_t)u * lds] * xr;
-                } else {
-                    const double *pr = Pg + r + (int64_t)(32 * q) * lda;
-#pragma unroll
-                    for (int u = 0; u < 32; ++u)
-                        if (u < cb) acc[u] += pr[(int64_t)u * lda] * xr;
+                for (int u = 0; u < 32; ++u) {
+                    if (u < cb) acc[u] += *pr * xr;
+                    pr += ld;
                 }
             }
 #pragma unroll
