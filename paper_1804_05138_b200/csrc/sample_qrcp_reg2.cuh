@@ -9,7 +9,9 @@
 //     1 + n'/512 CTAs fits one CTA per SM for n' <= 75264);
 //   * each column is split in three row ranges: rows [0, LT) in a global
 //     scratch (transposed [row][thread] per CTA: coalesced), rows
-//     [LT, LT + LR) in registers, rows [LT + LR, L) in shared memory.
+//     [LT, LT + LR) in registers, rows [LT + LR, L) in shared memory
+//     (the global rows are read with ld.global.cg: they stream past L1, which
+//     keeps the few spilled registers of this 128-register kernel).
 // Step j only touches rows >= j, so the global rows -- the TOP rows -- drop
 // out of the traffic after step LT: summed over a 128-step panel the L2
 // traffic is sum_{j < LT} (LT - j) rows instead of LT rows per step.
@@ -76,7 +78,7 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
         for (int t = 0; t < LS; ++t) xsm[t * TH + tid] = have ? src[S0 + t] : 0.0;
     }
     double r = 0.0;
-    for (int t = 0; t < LT; ++t) r += xt[t * TH] * xt[t * TH];
+    for (int t = 0; t < LT; ++t) r += xt[t * TH] * xt[t * TH];  // (just written: from L1)
 #pragma unroll
     for (int t = 0; t < LR; ++t) r += x[t] * x[t];
     for (int t = 0; t < LS; ++t) r += xsm[t * TH + tid] * xsm[t * TH + tid];
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
             if (sq_better(wv[w], wpos[w], bv, bp)) { bv = wv[w]; bp = wpos[w]; bc = wcol[w]; }
         // the owner stages its top and register rows in xraw (free until the next poll)
         if (act && (int)pc == bc) {
-            for (int t = 0; t < LT; ++t) xraw[t] = xt[t * TH];
+            for (int t = 0; t < LT; ++t) xraw[t] = __ldcg(&xt[t * TH]);
 #pragma unroll
             for (int t = 0; t < LR; ++t) xraw[R0 + t] = x[t];
         }
@@ -276,11 +278,11 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
                 for (; t + 7 < LT; t += 8) {
                     double y[8];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) y[u] = xt[(t + u) * TH];
+                    for (int u = 0; u < 8; ++u) y[u] = __ldcg(&xt[(t + u) * TH]);
 #pragma unroll
                     for (int u = 0; u < 8; ++u) d[u & 3] += xs[t + u] * y[u];
                 }
-                for (; t < LT; ++t) d[0] += xs[t] * xt[t * TH];
+                for (; t < LT; ++t) d[0] += xs[t] * __ldcg(&xt[t * TH]);
             }
 #pragma unroll
             for (int c0 = 0; c0 < LR; c0 += SQR_CH) {
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
                 for (; t + 7 < LT; t += 8) {
                     double y[8];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) y[u] = xt[(t + u) * TH];
+                    for (int u = 0; u < 8; ++u) y[u] = __ldcg(&xt[(t + u) * TH]);
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         const double nv = y[u] - tw * xs[t + u];
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
                     }
                 }
                 for (; t < LT; ++t) {
-                    const double nv = xt[t * TH] - tw * xs[t];
+                    const double nv = __ldcg(&xt[t * TH]) - tw * xs[t];
                     xt[t * TH] = nv;
                     if (t == j) bj = nv;
                 }
@@ -375,7 +377,7 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
             double rn = r - bj * bj;
             if (rn < 1e-6 * r0) {  // recompute from the updated rows (R-G6)
                 double s0 = 0.0;
-                for (int t = j + 1; t < LT; ++t) s0 += xt[t * TH] * xt[t * TH];
+                for (int t = j + 1; t < LT; ++t) s0 += __ldcg(&xt[t * TH]) * __ldcg(&xt[t * TH]);
 #pragma unroll
                 for (int t = 0; t < LR; ++t)
                     if (R0 + t > j) s0 += x[t] * x[t];
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
             a.trace[(size_t)g * 256 + e] = (e / 4 < min(j + 1, 64)) ? s_trace[e] : 0ull;
     if (have) {
         double *dst = a.B + pc * a.ldb;
-        for (int t = 0; t < LT; ++t) dst[t] = xt[t * TH];
+        for (int t = 0; t < LT; ++t) dst[t] = __ldcg(&xt[t * TH]);
 #pragma unroll
         for (int t = 0; t < LR; ++t) dst[R0 + t] = x[t];
         for (int t = 0; t < LS; ++t) dst[S0 + t] = xsm[t * TH + tid];
