@@ -1756,7 +1756,14 @@ struct Run {
             } else if (npl > 0) {
                 // C = Omega-hat11 R12 (DMMA; omhat holds Omega-hat11^T), then the
                 // gather B_next = [R-hat12 - C; R-hat22] (Eq. (4))
-                CKT(gemm_skinny(ctx, bbpad, npl, bb, ctx->omhat, bbpad, A + i + lj0 * lda, lda, ctx->c5, lpad, npp));
+                {
+                    bool dn4 = false;  // persistent TMA kernel (rows i.. of A as the K operand), else cp.async
+                    CKT(tma_skinny(ctx, bbpad, npl, bb, ctx->omhat, bbpad, bbpad, bbpad, 0, 0, A, m, n_loc, lda, i, lj0,
+                                   ctx->c5, lpad, &dn4, 512, npp));
+                    if (!dn4)
+                        CKT(gemm_skinny(ctx, bbpad, npl, bb, ctx->omhat, bbpad, A + i + lj0 * lda, lda, ctx->c5, lpad,
+                                        npp));
+                }
                 sample_update4_kernel<<<grid_for((int64_t)lpad * npl, 256, G), 256, 0, st>>>(
                     ctx->bs[cur], lpad, ctx->perm, ctx->c5, lpad, bb, l, lpad, npl, bb_eff, udst, lpad, i, lj0, b, P, me);
                 CKL();
