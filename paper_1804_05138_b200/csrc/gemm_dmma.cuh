@@ -179,6 +179,31 @@ __global__ void __launch_bounds__(WM *WN * 32) gemm_tn_kernel(GemmArgs g) {
 __global__ void splitk_reduce_kernel(const double *P, int64_t M, int64_t N, int splits, int64_t stride, double *C,
                                      int64_t ldc) {
     const int64_t total = M * N;
+    // pairs of consecutive elements (same column: M even) by 16-byte loads / stores
+    const bool vec = ((M | ldc | stride) & 1) == 0 && ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(C)) & 15) == 0;
+    if (vec) {
+        for (int64_t e = 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); e < total;
+             e += 2 * (int64_t)gridDim.x * blockDim.x) {
+            // slices added in order q = 0, 1, ... (fixed: deterministic)
+            double s0 = 0.0, s1 = 0.0;
+            int q = 0;
+            for (; q + 4 <= splits; q += 4) {
+                double2 v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const double2 *>(P + (int64_t)(q + u) * stride + e);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) { s0 += v[u].x; s1 += v[u].y; }
+            }
+            for (; q < splits; ++q) {
+                const double2 v = *reinterpret_cast<const double2 *>(P + (int64_t)q * stride + e);
+                s0 += v.x;
+                s1 += v.y;
+            }
+            const int64_t m = e % M, n = e / M;
+            *reinterpret_cast<double2 *>(C + m + n * ldc) = make_double2(s0, s1);
+        }
+        return;
+    }
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         // slices added in order q = 0, 1, ... (fixed: deterministic); loads in
         // batches of 8 so a many-slice reduce is not one L2 latency per slice

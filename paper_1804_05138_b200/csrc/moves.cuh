@@ -131,7 +131,7 @@ __global__ void colsumsq_kernel(const double *P, int64_t ldp, int64_t rows, int 
 #pragma unroll
         for (int u = 0; u < 8; ++u) a[u] += v[u] * v[u];
     }
-    for (int u = 0; r < rows; r += step, ++u) a[u] += x[r] * x[r];
+    for (; r < rows; r += step) a[0] += x[r] * x[r];  // (constant index: a[] stays in registers)
     double s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     s = warp_sum(s);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
