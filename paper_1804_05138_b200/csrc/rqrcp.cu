@@ -1992,17 +1992,15 @@ static int factor_impl(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_
     R.h_ld = h_ld;
     R.cps = ctx->cps;
     // schedule: the bulk rows of each trailing update overlap the next sample
-    // QRCP (measured best at C2-C4: 4.40 / 50.7 / 1088 ms against 5.23 / 54.8 /
-    // 1191 ms with the panel look-ahead, whose panel kernel slows down when it
-    // shares the GPU with the update, and 1087 ms serial at C4)
+    // QRCP when that sample QRCP is one cluster (C2: 4.34 vs 4.78 ms serial);
+    // the register grids fill the GPU and the update kernels run at their best
+    // alone: serial (C3 43.9 vs 46.6 ms, C4 / C5 likewise).  The panel
+    // look-ahead (schedule 2) loses everywhere: its panel kernel slows down
+    // when it shares the GPU with the update.
     int sched = ctx->opt.schedule;
     if (sched < 0) {
-        // schedule 1 when the sample QRCP leaves room for the bulk update (one
-        // cluster, or the register grid with the tile-claiming K <= 64 update);
-        // at b = 128 / l = 144 the register grid fills the GPU: serial
-        // (measured C4 1004.7 vs 1009.3 ms, C5 2245 vs 2239 ms)
         const SqKind kind = sq_kind(ctx, R.l, n);
-        sched = (kind == SQK_CLUSTER || (kind == SQK_REG && rup(b, 8) <= 64)) ? 1 : 0;
+        sched = (kind == SQK_CLUSTER) ? 1 : 0;
     }
     R.sched = sched;
     const int ev_t0 = ctx->nev;
