@@ -188,6 +188,11 @@ int rqrcp_factor_ex(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n
  *   sq_poll       grid sample QRCP exchange: 3 tagged 16-byte units (no fences), 0 acquire
  *                 polls, 1 relaxed polls + one fence, 2 as 1 with backoff
  *   debug_sync    synchronise after every launch
+ *   host_out      rqrcp_factor_host output: 0 (default) the whole factored A; 1 the factors
+ *                 only -- columns 0..k-1 full height (V below, R11 on / above the diagonal) and
+ *                 rows 0..k-1 of columns k..n-1 (R12); the R22 block of A_out_host is left
+ *                 as it was (the partial factorization's outputs are Pi, V + tau, R11, R12:
+ *                 P:79-83)
  *   nccl_timeout_ms   multi-GPU: abort the communicator when a call exceeds it */
 int rqrcp_set_option(rqrcp_ctx *ctx, const char *name, int64_t value);
 

@@ -59,6 +59,8 @@ struct Opts {
     int upd_kernel = 2;      // update GEMM: 0 CTA-wide TMA epilogue, 1 / 2 warp-specialised (BK 32 x 2 / 16 x 4 stages)
     int sq_cluster = 1, sq_reg = 1, sq_grid = 0, sq_nsm = -1, sq_hstride = 8, sq_poll = 3;
     int debug_sync = 0, trace = 0, trace_panel = 1;
+    int host_out = 0;        // rqrcp_factor_host output: 0 the whole factored A, 1 the factors only (columns
+                             // 0..k-1 full height = V and R11, rows 0..k-1 of columns k..n-1 = R12; R22 not copied)
     int64_t nccl_timeout_ms = 600000;
 };
 struct OptDesc {
@@ -72,7 +74,7 @@ static const OptDesc kOpts[] = {{"schedule", -1, 2},     {"panel", 0, 2},     {"
                                 {"sq_poll", 0, 3},       {"debug_sync", 0, 1}, {"trace", 0, 1},
                                 {"trace_panel", 1, 1 << 30}, {"nccl_timeout_ms", 1, (int64_t)1 << 40},
                                 {"upd_kernel", 0, 2}, {"pn_blocked", 0, 2},
-                                {"tournament", 0, 64}, {"gemm_ws", 0, 1}};
+                                {"tournament", 0, 64}, {"gemm_ws", 0, 1}, {"host_out", 0, 1}};
 static bool opt_set(Opts &o, const std::string &n, int64_t v) {
 #define OPT(field)                    \
     if (n == #field) {                \
@@ -81,7 +83,7 @@ static bool opt_set(Opts &o, const std::string &n, int64_t v) {
     }
     OPT(schedule) OPT(panel) OPT(pn_cluster) OPT(pn_cpt) OPT(pn_grid) OPT(pn_rows) OPT(la_panel_ctas)
     OPT(sq_cluster) OPT(sq_reg) OPT(sq_grid) OPT(sq_nsm) OPT(sq_hstride) OPT(sq_poll) OPT(debug_sync) OPT(trace)
-    OPT(trace_panel) OPT(nccl_timeout_ms) OPT(upd_kernel) OPT(pn_blocked) OPT(tournament) OPT(gemm_ws)
+    OPT(trace_panel) OPT(nccl_timeout_ms) OPT(upd_kernel) OPT(pn_blocked) OPT(tournament) OPT(gemm_ws) OPT(host_out)
 #undef OPT
     return false;
 }
@@ -1892,8 +1894,11 @@ struct Run {
         if (h_out && k < n) {  // the trailing columns (R12 rows, R22) are final now
             CK(cudaEventRecord(ctx->ev_h2d, st));
             CK(cudaStreamWaitEvent(cps, ctx->ev_h2d, 0));
+            // host_out 1: only the R12 rows (later panels' swaps move whole trailing
+            // columns, so they are final only here); R22 stays on the device
+            const int64_t rows = ctx->opt.host_out ? k : m;
             CK(cudaMemcpy2DAsync(h_out + k * h_ld, sizeof(double) * h_ld, A + k * lda, sizeof(double) * lda,
-                                 sizeof(double) * m, n - k, cudaMemcpyDeviceToHost, cps));
+                                 sizeof(double) * rows, n - k, cudaMemcpyDeviceToHost, cps));
         }
         if (h_out) {
             CK(cudaEventRecord(ctx->ev_h2d, cps));

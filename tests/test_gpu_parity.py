@@ -439,6 +439,29 @@ def test_factor_host_streams_chunks(ctx):
     assert np.array_equal(Ah.numpy(), g["A"])
 
 
+def test_factor_host_factors_only(ctx):
+    """Option host_out = 1: the host receives the partial factorization's
+    outputs only -- columns 0..k-1 full height (V, R11) and rows
+    0..k-1 of the trailing columns (R12), bitwise the device result; the R22
+    block of the output buffer is left untouched."""
+    A = inputs.iid(10, 500, 3000).numpy()
+    k = 96
+    g = gpu_factor(ctx, A, k, 32, 8, 7)
+    Ah = inputs.fortran(torch.as_tensor(A)).pin_memory()
+    Ao = inputs.fortran(torch.full(A.shape, 7.25, dtype=torch.float64)).pin_memory()
+    ctx.set_option("host_out", 1)
+    try:
+        jp, ta, rank = ctx.factor_host(Ah, k, 32, 8, seed=7, out=Ao)
+    finally:
+        ctx.set_option("host_out", 0)
+    o = Ao.numpy()
+    assert rank == k
+    assert np.array_equal(o[:, :k], g["A"][:, :k])
+    assert np.array_equal(o[:k, k:], g["A"][:k, k:])
+    assert np.all(o[k:, k:] == 7.25)
+    assert np.array_equal(jp.numpy(), g["jpvt"]) and np.array_equal(ta.numpy(), g["tau"][:k])
+
+
 # ---- launch-shape variants of the sample QRCP (threads per column, spill) ----
 # sq_grid caps the cooperative grid (fewer CTAs -> more columns per CTA, fewer
 # threads per column) and sq_nsm caps the columns a CTA keeps in shared memory
