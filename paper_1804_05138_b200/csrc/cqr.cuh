@@ -370,25 +370,30 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_rowmul_kernel(const double
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int fr = lane >> 2, fk = lane & 3;
     const int64_t tstride = (int64_t)gridDim.x * (CQR_THREADS / 32) * RM_ROWS;
-    for (int64_t rbase = r0 + ((int64_t)blockIdx.x * (CQR_THREADS / 32) + warp) * RM_ROWS; rbase < rows;
-         rbase += tstride) {
-        double acc[RM_MT][16][2];
-#pragma unroll
-        for (int mt = 0; mt < RM_MT; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < 16; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-        const int NT = bbpad / 8;
-        // all A fragments of this warp's rows first (one round trip), then the MMAs
-        double af[RM_MT][CQR_MAXB / 4];
+    const int NT = bbpad / 8;
+    // the A fragments of a warp's rows (one round trip), prefetched one tile
+    // ahead so the loads of tile t + 1 are in flight during tile t's MMAs
+    double af[RM_MT][CQR_MAXB / 4], an[RM_MT][CQR_MAXB / 4];
+    auto load_frag = [&](double (&f)[RM_MT][CQR_MAXB / 4], int64_t rb) {
 #pragma unroll
         for (int kk = 0; kk < CQR_MAXB / 4; ++kk) {
             const int k = kk * 4 + fk;
 #pragma unroll
             for (int mt = 0; mt < RM_MT; ++mt) {
-                const int64_t r = rbase + mt * 8 + fr;
-                af[mt][kk] = (kk * 4 < bbpad && r < rows && k < bb) ? X[r + (int64_t)k * ldx] : 0.0;
+                const int64_t r = rb + mt * 8 + fr;
+                f[mt][kk] = (kk * 4 < bbpad && r < rows && k < bb) ? X[r + (int64_t)k * ldx] : 0.0;
             }
         }
+    };
+    int64_t rbase = r0 + ((int64_t)blockIdx.x * (CQR_THREADS / 32) + warp) * RM_ROWS;
+    if (rbase < rows) load_frag(af, rbase);
+    for (; rbase < rows; rbase += tstride) {
+        if (rbase + tstride < rows) load_frag(an, rbase + tstride);
+        double acc[RM_MT][16][2];
+#pragma unroll
+        for (int mt = 0; mt < RM_MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 16; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
 #pragma unroll
         for (int kk = 0; kk < CQR_MAXB / 4; ++kk) {
             if (kk * 4 >= bbpad) break;
@@ -422,6 +427,10 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_rowmul_kernel(const double
                 }
             }
         }
+#pragma unroll
+        for (int mt = 0; mt < RM_MT; ++mt)
+#pragma unroll
+            for (int kk = 0; kk < CQR_MAXB / 4; ++kk) af[mt][kk] = an[mt][kk];
     }
 }
 

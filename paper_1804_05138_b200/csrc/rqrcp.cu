@@ -40,6 +40,7 @@
 #include "tournament.cuh"
 #include "srqr.cuh"
 #include "lowrank.cuh"
+#include "cqr_rg.cuh"
 
 using namespace rq;
 
@@ -50,7 +51,7 @@ enum Phase { PH_OMEGA, PH_SKETCH, PH_SQRCP, PH_SWAP, PH_PANEL, PH_TRAIL, PH_SUPD
 // Launch-path options (rqrcp_set_option; environment RQRCP_<NAME> at create).
 struct Opts {
     int schedule = -1;       // -1 auto, 0 serial, 1 bulk || next sample QRCP, 2 bulk || next panel (look-ahead)
-    int panel = 0;           // 0 Householder columns, 1 CholeskyQR2 + reconstruction, 2 CholeskyQR2 from 8192 rows
+    int panel = 2;           // 0 Householder columns, 1 CholeskyQR2 + reconstruction, 2 CholeskyQR2 from 8192 rows (measured: C3-C5)
     int pn_cluster = 1, pn_cpt = 2, pn_grid = 0, pn_rows = 128, la_panel_ctas = 48;
     int gemm_ws = 1;         // skinny TMA GEMMs (sketch, W): 1 warp-specialised, 0 CTA-barrier ring
     int tournament = 0;      // > 1: tournament pivoting on the sample over this many column groups (reading R-TP)
@@ -59,6 +60,7 @@ struct Opts {
     int upd_kernel = 2;      // update GEMM: 0 CTA-wide TMA epilogue, 1 / 2 warp-specialised (BK 32 x 2 / 16 x 4 stages)
     int sq_cluster = 1, sq_reg = 1, sq_grid = 0, sq_nsm = -1, sq_hstride = 8, sq_poll = 3;
     int debug_sync = 0, trace = 0, trace_panel = 1;
+    int cqr_rg = 1;          // CholeskyQR2 panel: 1 register-grid one-CTA factorizations (cqr_rg.cuh), 0 shared-memory
     int host_out = 0;        // rqrcp_factor_host output: 0 the whole factored A, 1 the factors only (columns
                              // 0..k-1 full height = V and R11, rows 0..k-1 of columns k..n-1 = R12; R22 not copied)
     int64_t nccl_timeout_ms = 600000;
@@ -74,7 +76,7 @@ static const OptDesc kOpts[] = {{"schedule", -1, 2},     {"panel", 0, 2},     {"
                                 {"sq_poll", 0, 3},       {"debug_sync", 0, 1}, {"trace", 0, 1},
                                 {"trace_panel", 1, 1 << 30}, {"nccl_timeout_ms", 1, (int64_t)1 << 40},
                                 {"upd_kernel", 0, 2}, {"pn_blocked", 0, 2},
-                                {"tournament", 0, 64}, {"gemm_ws", 0, 1}, {"host_out", 0, 1}};
+                                {"tournament", 0, 64}, {"gemm_ws", 0, 1}, {"host_out", 0, 1}, {"cqr_rg", 0, 1}};
 static bool opt_set(Opts &o, const std::string &n, int64_t v) {
 #define OPT(field)                    \
     if (n == #field) {                \
@@ -83,7 +85,7 @@ static bool opt_set(Opts &o, const std::string &n, int64_t v) {
     }
     OPT(schedule) OPT(panel) OPT(pn_cluster) OPT(pn_cpt) OPT(pn_grid) OPT(pn_rows) OPT(la_panel_ctas)
     OPT(sq_cluster) OPT(sq_reg) OPT(sq_grid) OPT(sq_nsm) OPT(sq_hstride) OPT(sq_poll) OPT(debug_sync) OPT(trace)
-    OPT(trace_panel) OPT(nccl_timeout_ms) OPT(upd_kernel) OPT(pn_blocked) OPT(tournament) OPT(gemm_ws) OPT(host_out)
+    OPT(trace_panel) OPT(nccl_timeout_ms) OPT(upd_kernel) OPT(pn_blocked) OPT(tournament) OPT(gemm_ws) OPT(host_out) OPT(cqr_rg)
 #undef OPT
     return false;
 }
@@ -142,7 +144,8 @@ struct rqrcp_ctx {
     double *sq_spill = nullptr;
     int64_t spill_cap = 0;  // doubles in sq_spill
     double *pn_part = nullptr, *pn_rowj = nullptr;
-    double *cq_g = nullptr, *cq_rc = nullptr, *cq_rinv = nullptr, *cq_uinv = nullptr, *cq_lu = nullptr;
+    double *cq_g = nullptr, *cq_rc = nullptr, *cq_rinv = nullptr, *cq_uinv = nullptr, *cq_lu = nullptr,
+           *cq_c = nullptr;
     int *cqr_status = nullptr;
     bool cqr_enabled = true;
     double *swap_stage = nullptr;
@@ -598,7 +601,7 @@ static int free_all(rqrcp_ctx *ctx) {
                     ctx->tp_cnt,    ctx->tp_ints,   ctx->tp_u,       ctx->tp_tau,     ctx->tp_vhat,    ctx->tp_r11,
                     ctx->tp_vt,     ctx->tp_y,      ctx->tp_tn,      ctx->tp_w,       ctx->tp_w2,
                     ctx->slot_col,  ctx->slot_v2,   ctx->slot_data,  ctx->sq_ll,      ctx->sq_spill,   ctx->pn_part,
-                    ctx->pn_rowj,   ctx->cq_g,      ctx->cq_rc,      ctx->cq_rinv,    ctx->cq_uinv,    ctx->cq_lu,
+                    ctx->pn_rowj,   ctx->cq_g,      ctx->cq_rc,      ctx->cq_rinv,    ctx->cq_uinv,    ctx->cq_lu,    ctx->cq_c,
                     ctx->cqr_status, ctx->bpre,     ctx->c5,         ctx->wom,        ctx->w2om,       ctx->swap_stage,
                     ctx->swap_dst,  ctx->swap_src,  ctx->swap_jstage, ctx->swap_np,   ctx->perm,       ctx->piv,
                     ctx->sumsq_part, ctx->iscal,    ctx->stop_tol2,  ctx->bars,       ctx->trace,      ctx->ptrace,
@@ -734,7 +737,8 @@ static int create_impl(rqrcp_ctx **out, const rqrcp_config *cfg, int nranks, int
     CKC(dalloc(&ctx->w2om, bp * lp));
     CKC(dalloc(&ctx->pn_part, 2 * G * bp));
     CKC(dalloc(&ctx->pn_rowj, 2 * bp));
-    for (double **q : {&ctx->cq_g, &ctx->cq_rc, &ctx->cq_rinv, &ctx->cq_uinv, &ctx->cq_lu}) CKC(dalloc(q, bp * bp));
+    for (double **q : {&ctx->cq_g, &ctx->cq_rc, &ctx->cq_rinv, &ctx->cq_uinv, &ctx->cq_lu, &ctx->cq_c})
+        CKC(dalloc(q, bp * bp));
     CKC(cudaMalloc((void **)&ctx->cqr_status, sizeof(int)));
     CKC(cudaMemset(ctx->cqr_status, 0xff, sizeof(int)));
     CKC(dalloc(&ctx->swap_stage, 2 * bp * mm));
@@ -769,6 +773,10 @@ static int create_impl(rqrcp_ctx **out, const rqrcp_config *cfg, int nranks, int
     CKC(smem_attr((const void *)sample_qrcp_cluster_kernel<80>, 128 * 80 * 8, dev));
     CKC(smem_attr((const void *)cqr_chol_kernel, (int)cqr_smem_bytes(128), dev));
     CKC(smem_attr((const void *)cqr_recon_kernel, (int)cqr_smem_bytes(128), dev));
+    CKC(smem_attr((const void *)cqr_chol_rg_kernel<128>, (int)cqr_rg_smem_bytes(128), dev));
+    CKC(smem_attr((const void *)cqr_chol_rg_kernel<64>, (int)cqr_rg_smem_bytes(64), dev));
+    CKC(smem_attr((const void *)cqr_recon_rg_kernel<128>, (int)cqr_rg_smem_bytes(128), dev));
+    CKC(smem_attr((const void *)cqr_recon_rg_kernel<64>, (int)cqr_rg_smem_bytes(64), dev));
     CKC(smem_attr((const void *)cqr_rowmul_kernel, 128 * 132 * 8, dev));
     {
         ctx->sqc_max = 0;
@@ -1640,9 +1648,30 @@ struct Run {
         // G1 = P^T P
         CKT(tma_skinny(ctx, bb, bb, mp, ctx->pbuf, m, bb, ldp, i, 0, ctx->pbuf, m, bb, ldp, i, 0, ctx->cq_g, bbpad, &dn, 128));
         if (!dn) CKT(gemm_skinny(ctx, bb, bb, mp, Pp, ldp, Pp, ldp, ctx->cq_g, bbpad));
-        cqr_chol_kernel<<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 1, bb_eff, ctx->cqr_status, ctx->cq_rc,
-                                                    ctx->cq_rinv, ctx->ptol2);
-        CKL();
+        const bool rg = ctx->opt.cqr_rg != 0;
+        const int nbr = std::max(16, nb);
+        auto chol = [&](int pass, const double *tol) -> int {
+            if (!rg) {
+                cqr_chol_kernel<<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, pass, bb_eff, ctx->cqr_status,
+                                                            ctx->cq_rc, ctx->cq_rinv, tol);
+                CKL();
+                return 0;
+            }
+            const size_t sm = cqr_rg_smem_bytes(nbr);
+            switch (nbr) {
+#define RGC(NBV)                                                                                                  \
+    case NBV:                                                                                                     \
+        cqr_chol_rg_kernel<NBV><<<1, RG_THREADS, sm, st>>>(ctx->cq_g, bb, bbpad, pass, bb_eff, ctx->cqr_status, \
+                                                            ctx->cq_rc, ctx->cq_rinv, tol);                       \
+        break;
+                RGC(16) RGC(32) RGC(64) RGC(128)
+#undef RGC
+                default: ctx->err = "cqr: unsupported panel width"; return RQRCP_E_UNSUPPORTED;
+            }
+            CKL();
+            return 0;
+        };
+        CKT(chol(1, ctx->ptol2));
         // Q1 = P R1^{-1}
         cqr_rowmul_kernel<<<rgrid(mp), CQR_THREADS, rsm, st>>>(Pp, ldp, 0, mp, bb, bbpad, ctx->cq_rinv, 1.0, vfull, ldv,
                                                                ctx->cqr_status, 0, nullptr, 0, nullptr);
@@ -1650,24 +1679,46 @@ struct Run {
         // G2 = Q1^T Q1, R2, Rc = R2 R1
         CKT(tma_skinny(ctx, bb, bb, mp, vfull, mp, bbpad, ldv, 0, 0, vfull, mp, bbpad, ldv, 0, 0, ctx->cq_g, bbpad, &dn, 128));
         if (!dn) CKT(gemm_skinny(ctx, bb, bb, mp, vfull, ldv, vfull, ldv, ctx->cq_g, bbpad));
-        cqr_chol_kernel<<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, 2, bb_eff, ctx->cqr_status, ctx->cq_rc,
-                                                    ctx->cq_rinv, nullptr);
-        CKL();
-        // Q = Q1 R2^{-1} (in place)
-        cqr_rowmul_kernel<<<rgrid(mp), CQR_THREADS, rsm, st>>>(vfull, ldv, 0, mp, bb, bbpad, ctx->cq_rinv, 1.0, vfull, ldv,
-                                                               ctx->cqr_status, 0, nullptr, 0, nullptr);
+        CKT(chol(2, nullptr));
+        // Q = Q1 R2^{-1}: only its top bb rows are formed (in place); the rows below
+        // go straight to V2 = -Qbottom U^{-1} = -Q1bottom (R2^{-1} U^{-1}) below
+        // (rg path: one pass over the panel fewer)
+        cqr_rowmul_kernel<<<rg ? 1 : rgrid(mp), CQR_THREADS, rsm, st>>>(vfull, ldv, 0, rg ? std::min<int64_t>(mp, bb) : mp,
+                                                                         bb, bbpad, ctx->cq_rinv, 1.0, vfull, ldv,
+                                                                         ctx->cqr_status, 0, nullptr, 0, nullptr);
         CKL();
         // reconstruction of the top block: L, U S, U^{-1}, L^{-T} (L^{-T} into cq_g: G2 is consumed)
-        cqr_recon_kernel<<<1, CQR_THREADS, csm, st>>>(vfull, ldv, bb, bbpad, nb, ctx->cq_rc, ctx->cqr_status, Pp, ldp,
-                                                     tau + i, ctx->cq_lu, ctx->cq_uinv, ctx->cq_g, vt);
+        if (!rg) {
+            cqr_recon_kernel<<<1, CQR_THREADS, csm, st>>>(vfull, ldv, bb, bbpad, nb, ctx->cq_rc, ctx->cqr_status, Pp, ldp,
+                                                         tau + i, ctx->cq_lu, ctx->cq_uinv, ctx->cq_g, vt);
+        } else {
+            switch (nbr) {
+#define RGR(NBV)                                                                                                      \
+    case NBV:                                                                                                         \
+        cqr_recon_rg_kernel<NBV><<<1, RG_THREADS, cqr_rg_smem_bytes(NBV), st>>>(vfull, ldv, bb, bbpad, ctx->cq_rc, ctx->cqr_status, Pp, ldp, \
+                                                           tau + i, ctx->cq_lu, ctx->cq_uinv, ctx->cq_g, vt);         \
+        break;
+                RGR(16) RGR(32) RGR(64) RGR(128)
+#undef RGR
+                default: ctx->err = "cqr: unsupported panel width"; return RQRCP_E_UNSUPPORTED;
+            }
+        }
         CKL();
         // -T = -(U S) L^{-T}
         cqr_rowmul_kernel<<<1, CQR_THREADS, rsm, st>>>(ctx->cq_lu, bbpad, 0, bbpad, bb, bbpad, ctx->cq_g, -1.0, ctx->tneg,
                                                        bbpad, ctx->cqr_status, 0, nullptr, 0, nullptr);
         CKL();
-        // V2 = -Qbottom U^{-1} (into Vfull, the panel and Vt)
+        // V2 = -Qbottom U^{-1} (into Vfull, the panel and Vt); rg path: C = R2^{-1} U^{-1}
+        // (bb x bb, one CTA) then V2 = -Q1bottom C
         if (mp > bb) {
-            cqr_rowmul_kernel<<<rgrid(mp - bb), CQR_THREADS, rsm, st>>>(vfull, ldv, bb, mp, bb, bbpad, ctx->cq_uinv, -1.0,
+            const double *cm = ctx->cq_uinv;
+            if (rg) {
+                cqr_rowmul_kernel<<<2, CQR_THREADS, rsm, st>>>(ctx->cq_rinv, bbpad, 0, bbpad, bb, bbpad, ctx->cq_uinv, 1.0,
+                                                              ctx->cq_c, bbpad, ctx->cqr_status, 0, nullptr, 0, nullptr);
+                CKL();
+                cm = ctx->cq_c;
+            }
+            cqr_rowmul_kernel<<<rgrid(mp - bb), CQR_THREADS, rsm, st>>>(vfull, ldv, bb, mp, bb, bbpad, cm, -1.0,
                                                                         vfull, ldv, ctx->cqr_status, 1, Pp, ldp, vt);
             CKL();
         }

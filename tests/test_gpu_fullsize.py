@@ -12,6 +12,8 @@ oracle:
   and R rows do not depend on k): identical first k' pivots, R rows 0..k'-1
   element-wise matched by column id (later swaps only permute columns),
   tau / V of the first k' columns, and the per-panel trace of those panels;
+* C3 again with the column-by-column Householder panel (option panel = 0;
+  the default from 8192 rows is CholeskyQR2 + reconstruction);
 * at any size, probes: with R = [R11 R12; 0 R22] from the factored matrix,
   ||A Pi x - Q (R x)|| / (||A||_F ||x||) <= 1e-13 and ||Q^T Q x - x|| / ||x||
   <= 1e-13 for Gaussian x (SURVEY.md §8(c) C4/C5 plan).
@@ -46,7 +48,7 @@ def _apply_q(F, tau, X, transpose=False):
     return Y
 
 
-def _run(name, prefix_panels=None, nprobe=4):
+def _run(name, prefix_panels=None, nprobe=4, opts=None):
     import paper_1804_05138_b200 as rq
     c = inputs.CONFIGS[name]
     m, n, k, b, p, seed = c["m"], c["n"], c["k"], c["b"], c["p"], c["seed"]
@@ -56,6 +58,8 @@ def _run(name, prefix_panels=None, nprobe=4):
     Ad = inputs.config_matrix(name, device="cuda")
     A = Ad.cpu().numpy()  # host copy of the input (not from the CUDA path)
     ctx = rq.RQRCP(max_m=m, max_n=n, max_b=b, max_p=p)
+    for kk, vv in (opts or {}).items():
+        ctx.set_option(kk, vv)
     tr = ctx.make_trace(n, b, p, 0, npan)
     jpvt, tau, rank = ctx.factor(Ad, k, b, p, seed=seed, trace=tr)
     torch.cuda.synchronize()
@@ -115,6 +119,14 @@ def _run(name, prefix_panels=None, nprobe=4):
 def test_C3_full_size():
     r = _run("C3")
     assert 0.0 < r < 1e-3  # low rank (1024 = k) plus 1e-6 noise: residual at the noise level
+
+
+def test_C3_full_size_householder_panel():
+    """The default panel at C3-C5 is CholeskyQR2 + reconstruction (panel = 2:
+    from 8192 rows); the column-by-column Householder grid panel gets the same
+    full-size check."""
+    r = _run("C3", opts={"panel": 0})
+    assert 0.0 < r < 1e-3
 
 
 def test_C4_full_size():

@@ -30,8 +30,8 @@ RES_ATOL = 1e-12
 ELEM_RTOL = 1e-10
 RECON_TOL = 1e-13
 
-DEFAULT_OPTS = dict(schedule=-1, panel=0, upd_kernel=2, pn_blocked=1, tournament=0, gemm_ws=1, pn_cluster=1, pn_cpt=2, pn_grid=0, pn_rows=128, la_panel_ctas=48,
-                    sq_cluster=1, sq_reg=1, sq_grid=0, sq_nsm=-1, sq_hstride=8, sq_poll=3)
+DEFAULT_OPTS = dict(schedule=-1, panel=2, upd_kernel=2, pn_blocked=1, tournament=0, gemm_ws=1, pn_cluster=1, pn_cpt=2, pn_grid=0, pn_rows=128, la_panel_ctas=48,
+                    sq_cluster=1, sq_reg=1, sq_grid=0, sq_nsm=-1, sq_hstride=8, sq_poll=3, cqr_rg=1, host_out=0)
 
 
 @pytest.fixture(scope="module")
@@ -697,15 +697,18 @@ def test_srqr_verify_errors(ctx):
 CQR_CASES = [c for c in CASES if c[0] in ("C1", "ragged", "tall", "wide", "lowrank", "b128", "odd")]
 
 
+@pytest.mark.parametrize("rg", [1, 0], ids=["regs", "smem"])
 @pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", CQR_CASES, ids=[c[0] for c in CQR_CASES])
-def test_cqr_panel_parity(ctx, name, kind, m, n, k, b, p, seed):
+def test_cqr_panel_parity(ctx, name, kind, m, n, k, b, p, seed, rg):
     """panel=1: every well-conditioned panel goes through CholeskyQR2 +
     reconstruction (checked through the panels_householder counter); the
     result meets the same acceptance.  R, V, tau come from a different
-    algorithm here, so they are compared to 1e-10 like everything else."""
+    algorithm here, so they are compared to 1e-10 like everything else.
+    rg: the one-CTA factorizations in registers (cqr_rg.cuh) or in shared
+    memory (cqr.cuh)."""
     A = inputs.make(kind, m, n, seed, rank=64).numpy()
     o = oracle.rqrcp(A, k, b, p, seed=seed)
-    with options(ctx, panel=1):
+    with options(ctx, panel=1, cqr_rg=rg):
         g = gpu_factor(ctx, A, k, b, p, seed)
         t = ctx.timings()
     compare(A, g, o, k)
