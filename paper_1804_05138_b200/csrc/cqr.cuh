@@ -362,15 +362,22 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_rowmul_kernel(const double
     extern __shared__ __align__(16) double rm_sm[];  // bbpad x (bbpad + pad)
     if (*status != 0) return;
     const int ldr = bbpad + 4;  // bbpad is a multiple of 8: ldr = 4 or 12 mod 16
-    for (int e = threadIdx.x; e < bbpad * bbpad; e += blockDim.x) {
-        const int k = e % bbpad, c = e / bbpad;
-        rm_sm[k + c * ldr] = R[k + (int64_t)c * bbpad];
+    // R staged by 16-byte cp.async copies, all in flight at once (a plain copy
+    // loop waits one L2 round trip per iteration: tens of microseconds per
+    // launch); R and its padded image are 16-byte aligned (bbpad, ldr even)
+    for (int e = threadIdx.x; e < bbpad * bbpad / 2; e += blockDim.x) {
+        const int k = (2 * e) % bbpad, c = (2 * e) / bbpad;
+        cp_async16(&rm_sm[k + c * ldr], &R[k + (int64_t)c * bbpad], 16);
     }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int fr = lane >> 2, fk = lane & 3;
     const int64_t tstride = (int64_t)gridDim.x * (CQR_THREADS / 32) * RM_ROWS;
     const int NT = bbpad / 8;
+    // column slices (gridDim.y > 1, small products): this CTA's 8-column tiles
+    const int nts = (NT + (int)gridDim.y - 1) / (int)gridDim.y;
+    const int nt0 = (int)blockIdx.y * nts, nt1 = min(NT, nt0 + nts);
     // the A fragments of a warp's rows (one round trip), prefetched one tile
     // ahead so the loads of tile t + 1 are in flight during tile t's MMAs
     double af[RM_MT][CQR_MAXB / 4], an[RM_MT][CQR_MAXB / 4];
@@ -400,7 +407,7 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_rowmul_kernel(const double
             const int k = kk * 4 + fk;
 #pragma unroll
             for (int nt = 0; nt < 16; ++nt) {
-                if (nt < NT) {
+                if (nt >= nt0 && nt < nt1) {
                     const double b = rm_sm[k + (nt * 8 + fr) * ldr];
 #pragma unroll
                     for (int mt = 0; mt < RM_MT; ++mt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt][kk], b);
@@ -414,7 +421,7 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_rowmul_kernel(const double
             if (r >= rows) continue;
 #pragma unroll
             for (int nt = 0; nt < 16; ++nt) {
-                if (nt >= NT) continue;
+                if (nt < nt0 || nt >= nt1) continue;
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
                     const int c = nt * 8 + 2 * fk + hh;

@@ -42,7 +42,7 @@ RQ_DEV int upk(int r, int c) { return c * (c + 1) / 2 + r; }  // packed upper, c
 template <int NB>
 __global__ void __launch_bounds__(RG_THREADS, 1) cqr_chol_rg_kernel(const double *G, int bb, int bbpad, int pass,
                                                                   const int *bb_eff, int *status, double *Rc,
-                                                                  double *Rinv, const double *tol2) {
+                                                                  double *Rinv, double *tol2, int tol_from_gram) {
     constexpr int E = NB / 16;
     static_assert(NB % 16 == 0 && E >= 1 && E <= 8, "NB in 16..128");
     extern __shared__ __align__(16) double rg_sm[];  // pass 2: R2 packed | old Rc packed
@@ -52,7 +52,18 @@ __global__ void __launch_bounds__(RG_THREADS, 1) cqr_chol_rg_kernel(const double
     __shared__ int s_bad;
     const int tid = threadIdx.x, ta = tid & 15, tc = tid >> 4, warp = tid >> 5, lane = tid & 31;
     if (pass == 1) {
-        if (tid == 0) *status = (*bb_eff == bb) ? 0 : 1;
+        if (tid == 0) {
+            *status = (*bb_eff == bb) ? 0 : 1;
+            if (tol_from_gram) {
+                // the R11-diagonal stop scale (reading R-G12b) from the Gram diagonal:
+                // ||panel||_F^2 = trace(P^T P), ascending columns (replaces colsumsq +
+                // panel_tol_kernel; also read by the column-by-column fallback)
+                double sg = 0.0;
+                for (int c = 0; c < bb; ++c) sg += G[c + (int64_t)c * bbpad];
+                const double eps = 0x1p-52;
+                *tol2 = (*bb_eff == 0) ? 0.0 : (1e3 * eps) * (1e3 * eps) * sg;
+            }
+        }
         __syncthreads();
     }
     if (*status != 0) return;

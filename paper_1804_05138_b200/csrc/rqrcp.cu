@@ -1393,14 +1393,16 @@ struct Run {
         ph_begin(ctx, PH_PANEL);
         double *Pp = ctx->pbuf + i;
         if (me == owner) {
-            {
+            ctx->cqr_enabled = (panel_mode == 1) || (panel_mode == 2 && mp >= kCqrMinRows);
+            // the stop scale: from the CholeskyQR2 Gram diagonal (register-grid path), else
+            // one pass of column sums of squares
+            if (!(ctx->cqr_enabled && ctx->opt.cqr_rg)) {
                 colsumsq_kernel<<<bb, 256, 0, st>>>(Pp, ldp, mp, bb, bb_eff, ctx->colss);
                 CKL();
                 panel_tol_kernel<<<1, 32, 0, st>>>(ctx->colss, bb, bb_eff, ctx->ptol2);
                 CKL();
-                CK(cudaMemsetAsync(ctx->stopc, 0xff, sizeof(int), st));
             }
-            ctx->cqr_enabled = (panel_mode == 1) || (panel_mode == 2 && mp >= kCqrMinRows);
+            CK(cudaMemsetAsync(ctx->stopc, 0xff, sizeof(int), st));
             CKT(panel_cqr(i, mp, bb, bbpad, Pp, ldp, vfull, ldv, vt));
             PanelArgs a{};
             a.skip = ctx->cqr_status;
@@ -1644,13 +1646,17 @@ struct Run {
         auto rgrid = [&](int64_t rows) {
             return (int)std::max<int64_t>(1, std::min<int64_t>(G, (rows + 8 * (CQR_THREADS / 32) - 1) / (8 * (CQR_THREADS / 32))));
         };
+        // small (bb-row) products: 8-row warp tiles x 4 column slices
+        auto sgrid = [&](int64_t rows) {
+            return dim3((unsigned)std::max<int64_t>(1, (rows + 8 * (CQR_THREADS / 32) - 1) / (8 * (CQR_THREADS / 32))), 4);
+        };
         bool dn = false;
         // G1 = P^T P
         CKT(tma_skinny(ctx, bb, bb, mp, ctx->pbuf, m, bb, ldp, i, 0, ctx->pbuf, m, bb, ldp, i, 0, ctx->cq_g, bbpad, &dn, 128));
         if (!dn) CKT(gemm_skinny(ctx, bb, bb, mp, Pp, ldp, Pp, ldp, ctx->cq_g, bbpad));
         const bool rg = ctx->opt.cqr_rg != 0;
         const int nbr = std::max(16, nb);
-        auto chol = [&](int pass, const double *tol) -> int {
+        auto chol = [&](int pass, double *tol) -> int {
             if (!rg) {
                 cqr_chol_kernel<<<1, CQR_THREADS, csm, st>>>(ctx->cq_g, bb, bbpad, nb, pass, bb_eff, ctx->cqr_status,
                                                             ctx->cq_rc, ctx->cq_rinv, tol);
@@ -1662,7 +1668,7 @@ struct Run {
 #define RGC(NBV)                                                                                                  \
     case NBV:                                                                                                     \
         cqr_chol_rg_kernel<NBV><<<1, RG_THREADS, sm, st>>>(ctx->cq_g, bb, bbpad, pass, bb_eff, ctx->cqr_status, \
-                                                            ctx->cq_rc, ctx->cq_rinv, tol);                       \
+                                                            ctx->cq_rc, ctx->cq_rinv, tol, pass == 1 ? 1 : 0);    \
         break;
                 RGC(16) RGC(32) RGC(64) RGC(128)
 #undef RGC
@@ -1683,7 +1689,8 @@ struct Run {
         // Q = Q1 R2^{-1}: only its top bb rows are formed (in place); the rows below
         // go straight to V2 = -Qbottom U^{-1} = -Q1bottom (R2^{-1} U^{-1}) below
         // (rg path: one pass over the panel fewer)
-        cqr_rowmul_kernel<<<rg ? 1 : rgrid(mp), CQR_THREADS, rsm, st>>>(vfull, ldv, 0, rg ? std::min<int64_t>(mp, bb) : mp,
+        cqr_rowmul_kernel<<<rg ? sgrid(std::min<int64_t>(mp, bb)) : dim3(rgrid(mp)), CQR_THREADS, rsm, st>>>(
+                                                                         vfull, ldv, 0, rg ? std::min<int64_t>(mp, bb) : mp,
                                                                          bb, bbpad, ctx->cq_rinv, 1.0, vfull, ldv,
                                                                          ctx->cqr_status, 0, nullptr, 0, nullptr);
         CKL();
@@ -1705,7 +1712,7 @@ struct Run {
         }
         CKL();
         // -T = -(U S) L^{-T}
-        cqr_rowmul_kernel<<<1, CQR_THREADS, rsm, st>>>(ctx->cq_lu, bbpad, 0, bbpad, bb, bbpad, ctx->cq_g, -1.0, ctx->tneg,
+        cqr_rowmul_kernel<<<sgrid(bbpad), CQR_THREADS, rsm, st>>>(ctx->cq_lu, bbpad, 0, bbpad, bb, bbpad, ctx->cq_g, -1.0, ctx->tneg,
                                                        bbpad, ctx->cqr_status, 0, nullptr, 0, nullptr);
         CKL();
         // V2 = -Qbottom U^{-1} (into Vfull, the panel and Vt); rg path: C = R2^{-1} U^{-1}
@@ -1713,7 +1720,7 @@ struct Run {
         if (mp > bb) {
             const double *cm = ctx->cq_uinv;
             if (rg) {
-                cqr_rowmul_kernel<<<2, CQR_THREADS, rsm, st>>>(ctx->cq_rinv, bbpad, 0, bbpad, bb, bbpad, ctx->cq_uinv, 1.0,
+                cqr_rowmul_kernel<<<sgrid(bbpad), CQR_THREADS, rsm, st>>>(ctx->cq_rinv, bbpad, 0, bbpad, bb, bbpad, ctx->cq_uinv, 1.0,
                                                               ctx->cq_c, bbpad, ctx->cqr_status, 0, nullptr, 0, nullptr);
                 CKL();
                 cm = ctx->cq_c;

@@ -64,7 +64,7 @@ static void run(int bb) {
                 CK(cudaMemcpyToSymbol(g_cqr_dbg, v == 1 ? &dbg : &nul, sizeof(dbg)));
                 cudaEventRecord(e0);
                 if (v == 0) cqr_chol_kernel<<<1, CQR_THREADS, sm>>>(pass == 1 ? dG : dG2, bb, bbpad, nb, pass, be, st, dRc[v], dR[v], nullptr);
-                else cqr_chol_rg_kernel<NB><<<1, RG_THREADS, smr>>>(pass == 1 ? dG : dG2, bb, bbpad, pass, be, st, dRc[v], dR[v], nullptr);
+                else cqr_chol_rg_kernel<NB><<<1, RG_THREADS, smr>>>(pass == 1 ? dG : dG2, bb, bbpad, pass, be, st, dRc[v], dR[v], nullptr, 0);
                 cudaEventRecord(e1);
                 CK(cudaEventSynchronize(e1));
                 CK(cudaGetLastError());
