@@ -274,7 +274,8 @@ __global__ void __launch_bounds__(RG_THREADS, 1) cqr_chol_rg_kernel(const double
 // same outputs as cqr_recon_kernel (cqr.cuh).
 // ---------------------------------------------------------------------------
 template <int NB>
-__global__ void __launch_bounds__(RG_THREADS, 1) cqr_recon_rg_kernel(double *vfull /* holds Q; ld ldq */, int64_t ldq,
+__global__ void __launch_bounds__(RG_THREADS, 1) cqr_recon_rg_kernel(const double *qtop /* Q(0:bb, 0:bb), ld ldqt */,
+                                                                   int64_t ldqt, double *vfull /* ld ldq */, int64_t ldq,
                                                                    int bb, int bbpad, const double *Rc, int *status,
                                                                    double *A, int64_t lda, double *tau, double *us,
                                                                    double *Uinv, double *linvt, double *vt) {
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(RG_THREADS, 1) cqr_recon_rg_kernel(double *vfu
 #pragma unroll
         for (int q = 0; q < E; ++q) {
             const int a = ta + 16 * p, c = tc + 16 * q;
-            x[p][q] = (a < bb && c < bb) ? -vfull[a + (int64_t)c * ldq] : (a == c ? 1.0 : 0.0);
+            x[p][q] = (a < bb && c < bb) ? -qtop[a + (int64_t)c * ldqt] : (a == c ? 1.0 : 0.0);
         }
     if (tid == 0) s_fail = 0;
     cqr_stamp(1);
@@ -379,27 +380,33 @@ __global__ void __launch_bounds__(RG_THREADS, 1) cqr_recon_rg_kernel(double *vfu
         if (tid == 0) *status = 1;
         return;
     }
+    // Two CTAs (gridDim.x == 2) run the same LU; CTA 0 then writes the
+    // factorization outputs and inverts L, CTA 1 inverts U (half the sweep's
+    // work each).  One CTA does all of it.
+    const bool do_low = (blockIdx.x == 0), do_up = (blockIdx.x == gridDim.x - 1);
     // ---- outputs of the factorization (before the in-place inversions) ------
 #pragma unroll
     for (int p = 0; p < E; ++p)
 #pragma unroll
         for (int q = 0; q < E; ++q) {
             const int a = ta + 16 * p, c = tc + 16 * q;
-            if (a < bb && c < bbpad) {
+            if (do_low && a < bb && c < bbpad) {
                 const double xv = x[p][q];
                 const double lvv = (a > c && c < bb) ? xv : (a == c ? 1.0 : 0.0);
                 if (c < bb) A[a + (int64_t)c * lda] = (a > c) ? xv : sgn[a] * Rc[a + (int64_t)c * bbpad];
                 rc_img[c + a * LS] = lvv;  // vt(c, a)
                 vfull[a + (int64_t)c * ldq] = lvv;
             }
-            if (a < bbpad && c < bbpad) {
+            if (do_low && a < bbpad && c < bbpad) {
                 const double u = (a < c) ? x[p][q] : piv[c < bb ? c : 0];
                 us[a + (int64_t)c * bbpad] = (a <= c && c < bb) ? u * sgn[c] : 0.0;
             }
             if (a == c && a < bb) x[p][q] = piv[a];  // U(j, j) = the Schur pivot
         }
-    for (int c = tid; c < bb; c += RG_THREADS) tau[c] = piv[c] * sgn[c];
+    if (do_low)
+        for (int c = tid; c < bb; c += RG_THREADS) tau[c] = piv[c] * sgn[c];
     __syncthreads();
+    if (do_low)
     for (int e = tid; e < bb * bbpad; e += RG_THREADS) {  // vt: bbpad x bb (rows of Vt = columns of V)
         const int r = e % bbpad, c = e / bbpad;
         vt[r + (int64_t)c * bbpad] = rc_img[r + c * LS];
@@ -450,12 +457,12 @@ __global__ void __launch_bounds__(RG_THREADS, 1) cqr_recon_rg_kernel(double *vfu
 #pragma unroll
                 for (int q = 0; q < E; ++q) {
                     const int c = tc + 16 * q;
-                    if (p >= jb && q <= jb) {  // lower part: a > j, c <= j
+                    if (do_low && p >= jb && q <= jb) {  // lower part: a > j, c <= j
                         const bool arow = (p > jb) || (a > j);
                         const bool ccol = (q < jb) || (c <= j);
                         if (arow && ccol) x[p][q] = fma(cv[p], rv[q], (q == jb && c == j) ? 0.0 : x[p][q]);
                     }
-                    if (p <= jb && q >= jb) {  // upper part: a <= j, c > j; column j finalised
+                    if (do_up && p <= jb && q >= jb) {  // upper part: a <= j, c > j; column j finalised
                         const bool arow = (p < jb) || (a <= j);
                         if (arow) {
                             if (q > jb) x[p][q] = fma(cv[p], rv[q], (p == jb && a == j) ? 0.0 : x[p][q]);
@@ -476,11 +483,12 @@ __global__ void __launch_bounds__(RG_THREADS, 1) cqr_recon_rg_kernel(double *vfu
 #pragma unroll
         for (int q = 0; q < E; ++q) {
             const int a = ta + 16 * p, c = tc + 16 * q;
-            if (a < bbpad && c < bbpad) Uinv[a + (int64_t)c * bbpad] = (a <= c && c < bb) ? x[p][q] : 0.0;
+            if (do_up && a < bbpad && c < bbpad) Uinv[a + (int64_t)c * bbpad] = (a <= c && c < bb) ? x[p][q] : 0.0;
             // L^{-T}(c, a) = Y(a, c) from the strict lower element (a, c)
             rc_img[c + a * LS] = (a > c) ? ((a < bb) ? x[p][q] : 0.0) : ((a == c && a < bb) ? 1.0 : 0.0);
         }
     __syncthreads();
+    if (do_low)
     for (int e = tid; e < bbpad * bbpad; e += RG_THREADS) {
         const int r = e % bbpad, c = e / bbpad;
         linvt[e] = rc_img[r + c * LS];

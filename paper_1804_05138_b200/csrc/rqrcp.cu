@@ -145,7 +145,7 @@ struct rqrcp_ctx {
     int64_t spill_cap = 0;  // doubles in sq_spill
     double *pn_part = nullptr, *pn_rowj = nullptr;
     double *cq_g = nullptr, *cq_rc = nullptr, *cq_rinv = nullptr, *cq_uinv = nullptr, *cq_lu = nullptr,
-           *cq_c = nullptr;
+           *cq_c = nullptr, *cq_q = nullptr;
     int *cqr_status = nullptr;
     bool cqr_enabled = true;
     double *swap_stage = nullptr;
@@ -601,7 +601,7 @@ static int free_all(rqrcp_ctx *ctx) {
                     ctx->tp_cnt,    ctx->tp_ints,   ctx->tp_u,       ctx->tp_tau,     ctx->tp_vhat,    ctx->tp_r11,
                     ctx->tp_vt,     ctx->tp_y,      ctx->tp_tn,      ctx->tp_w,       ctx->tp_w2,
                     ctx->slot_col,  ctx->slot_v2,   ctx->slot_data,  ctx->sq_ll,      ctx->sq_spill,   ctx->pn_part,
-                    ctx->pn_rowj,   ctx->cq_g,      ctx->cq_rc,      ctx->cq_rinv,    ctx->cq_uinv,    ctx->cq_lu,    ctx->cq_c,
+                    ctx->pn_rowj,   ctx->cq_g,      ctx->cq_rc,      ctx->cq_rinv,    ctx->cq_uinv,    ctx->cq_lu,    ctx->cq_c,    ctx->cq_q,
                     ctx->cqr_status, ctx->bpre,     ctx->c5,         ctx->wom,        ctx->w2om,       ctx->swap_stage,
                     ctx->swap_dst,  ctx->swap_src,  ctx->swap_jstage, ctx->swap_np,   ctx->perm,       ctx->piv,
                     ctx->sumsq_part, ctx->iscal,    ctx->stop_tol2,  ctx->bars,       ctx->trace,      ctx->ptrace,
@@ -737,7 +737,7 @@ static int create_impl(rqrcp_ctx **out, const rqrcp_config *cfg, int nranks, int
     CKC(dalloc(&ctx->w2om, bp * lp));
     CKC(dalloc(&ctx->pn_part, 2 * G * bp));
     CKC(dalloc(&ctx->pn_rowj, 2 * bp));
-    for (double **q : {&ctx->cq_g, &ctx->cq_rc, &ctx->cq_rinv, &ctx->cq_uinv, &ctx->cq_lu, &ctx->cq_c})
+    for (double **q : {&ctx->cq_g, &ctx->cq_rc, &ctx->cq_rinv, &ctx->cq_uinv, &ctx->cq_lu, &ctx->cq_c, &ctx->cq_q})
         CKC(dalloc(q, bp * bp));
     CKC(cudaMalloc((void **)&ctx->cqr_status, sizeof(int)));
     CKC(cudaMemset(ctx->cqr_status, 0xff, sizeof(int)));
@@ -1689,9 +1689,12 @@ struct Run {
         // Q = Q1 R2^{-1}: only its top bb rows are formed (in place); the rows below
         // go straight to V2 = -Qbottom U^{-1} = -Q1bottom (R2^{-1} U^{-1}) below
         // (rg path: one pass over the panel fewer)
+        // (rg path: Q_top into its own bbpad x bbpad buffer, read by both CTAs of the
+        // reconstruction while CTA 0 writes the top rows of V)
         cqr_rowmul_kernel<<<rg ? sgrid(std::min<int64_t>(mp, bb)) : dim3(rgrid(mp)), CQR_THREADS, rsm, st>>>(
                                                                          vfull, ldv, 0, rg ? std::min<int64_t>(mp, bb) : mp,
-                                                                         bb, bbpad, ctx->cq_rinv, 1.0, vfull, ldv,
+                                                                         bb, bbpad, ctx->cq_rinv, 1.0, rg ? ctx->cq_q : vfull,
+                                                                         rg ? (int64_t)bbpad : ldv,
                                                                          ctx->cqr_status, 0, nullptr, 0, nullptr);
         CKL();
         // reconstruction of the top block: L, U S, U^{-1}, L^{-T} (L^{-T} into cq_g: G2 is consumed)
@@ -1702,7 +1705,7 @@ struct Run {
             switch (nbr) {
 #define RGR(NBV)                                                                                                      \
     case NBV:                                                                                                         \
-        cqr_recon_rg_kernel<NBV><<<1, RG_THREADS, cqr_rg_smem_bytes(NBV), st>>>(vfull, ldv, bb, bbpad, ctx->cq_rc, ctx->cqr_status, Pp, ldp, \
+        cqr_recon_rg_kernel<NBV><<<2, RG_THREADS, cqr_rg_smem_bytes(NBV), st>>>(ctx->cq_q, bbpad, vfull, ldv, bb, bbpad, ctx->cq_rc, ctx->cqr_status, Pp, ldp, \
                                                            tau + i, ctx->cq_lu, ctx->cq_uinv, ctx->cq_g, vt);         \
         break;
                 RGR(16) RGR(32) RGR(64) RGR(128)

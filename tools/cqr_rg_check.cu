@@ -39,6 +39,8 @@ static void run(int bb) {
     int *st, *be;
     unsigned long long *dbg, *nul = nullptr;
     CK(cudaMalloc(&dbg, 8 * 16));
+    double *dQ2c;
+    CK(cudaMalloc(&dQ2c, sizeof(double) * bbpad * bbpad));
     CK(cudaMalloc(&dG, B)); CK(cudaMalloc(&dG2, B)); CK(cudaMalloc(&dQ, B)); CK(cudaMalloc(&dQ2, B));
     for (int v = 0; v < 2; ++v) {
         CK(cudaMalloc(&dRc[v], B)); CK(cudaMalloc(&dR[v], B)); CK(cudaMalloc(&dA[v], B)); CK(cudaMalloc(&dtau[v], 8 * bbpad));
@@ -75,10 +77,11 @@ static void run(int bb) {
                 if (v == 1) CK(cudaMemcpy(hc[pass - 1], dbg, 8 * 8, cudaMemcpyDeviceToHost));
             }
             CK(cudaMemcpy(dQ, Q.data(), B, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dQ2c, Q.data(), B, cudaMemcpyHostToDevice));
             CK(cudaMemset(st, 0, 4));
             cudaEventRecord(e0);
             if (v == 0) cqr_recon_kernel<<<1, CQR_THREADS, sm>>>(dQ, bbpad, bb, bbpad, nb, dRc[v], st, dA[v], bbpad, dtau[v], dus[v], dui[v], dli[v], dvt[v]);
-            else cqr_recon_rg_kernel<NB><<<1, RG_THREADS, smr>>>(dQ, bbpad, bb, bbpad, dRc[v], st, dA[v], bbpad, dtau[v], dus[v], dui[v], dli[v], dvt[v]);
+            else cqr_recon_rg_kernel<NB><<<2, RG_THREADS, smr>>>(dQ2c, bbpad, dQ, bbpad, bb, bbpad, dRc[v], st, dA[v], bbpad, dtau[v], dus[v], dui[v], dli[v], dvt[v]);
             cudaEventRecord(e1);
             CK(cudaEventSynchronize(e1));
             CK(cudaGetLastError());
