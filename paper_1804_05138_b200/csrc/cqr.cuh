@@ -422,16 +422,18 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_rowmul_kernel(const double
 #pragma unroll
             for (int nt = 0; nt < 16; ++nt) {
                 if (nt < nt0 || nt >= nt1) continue;
+                double yv[2];
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
                     const int c = nt * 8 + 2 * fk + hh;
                     const double y = (c < bb) ? s * acc[mt][nt][hh] : 0.0;
+                    yv[hh] = y;
                     Y[r + (int64_t)c * ldy] = y;
-                    if (mode == 1) {
-                        if (c < bb) A[r + (int64_t)c * lda] = y;
-                        vt[c + r * bbpad] = y;
-                    }
+                    if (mode == 1 && c < bb) A[r + (int64_t)c * lda] = y;
                 }
+                // Vt(c, r), Vt(c + 1, r): one 16-byte store (c even, bbpad even)
+                if (mode == 1)
+                    *reinterpret_cast<double2 *>(&vt[nt * 8 + 2 * fk + r * bbpad]) = make_double2(yv[0], yv[1]);
             }
         }
 #pragma unroll

@@ -31,6 +31,30 @@
 
 namespace rq {
 
+// dst[r] = src[r] (or 0 when !own) for r < m over the grid's x dimension;
+// 16-byte accesses when both columns are 16-byte aligned (the leading
+// dimensions are even on every path the bench takes).
+RQ_DEV void copy_col(double *dst, const double *src, int64_t m, bool own = true) {
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, ts = (int64_t)gridDim.x * blockDim.x;
+    if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+        const int64_t m2 = m >> 1;
+        double2 *d2 = reinterpret_cast<double2 *>(dst);
+        const double2 *s2 = reinterpret_cast<const double2 *>(src);
+        int64_t r = t0;
+        for (; r + 3 * ts < m2; r += 4 * ts) {  // four 16-byte loads in flight per thread
+            double2 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = own ? s2[r + u * ts] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) d2[r + u * ts] = v[u];
+        }
+        for (; r < m2; r += ts) d2[r] = own ? s2[r] : make_double2(0.0, 0.0);
+        if ((m & 1) && t0 == 0) dst[m - 1] = own ? src[m - 1] : 0.0;
+    } else {
+        for (int64_t r = t0; r < m; r += ts) dst[r] = own ? src[r] : 0.0;
+    }
+}
+
 // Pbuf(:, q) = A(:, local(i + perm[q])) for the slots this rank owns (zeros
 // otherwise); W2g(:, q) = W2(:, local - lj0w) likewise when w2 != nullptr (the
 // look-ahead's narrow update; lj0w = first local trailing column of the
@@ -44,10 +68,7 @@ __global__ void pack_pivots_kernel(const double *A, int64_t lda, int64_t m, int6
     const int64_t jg = i + perm[q];
     const bool own = dist_owner(jg, b, P) == me;
     const int64_t lj = own ? dist_local(jg, b, P) : 0;
-    const double *src = A + lj * lda;
-    double *dst = pbuf + (int64_t)q * ldp;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x)
-        dst[r] = own ? src[r] : 0.0;
+    copy_col(pbuf + (int64_t)q * ldp, A + lj * lda, m, own);
     if (w2 && blockIdx.x == 0)
         for (int r = threadIdx.x; r < w2rows; r += blockDim.x)
             w2g[r + (int64_t)q * w2rows] = own ? w2[r + (lj - lj0w) * ldw2] : 0.0;
@@ -60,10 +81,7 @@ __global__ void pack_slots_kernel(const double *A, int64_t lda, int64_t m, int64
     if (*bb_eff == 0) return;
     const int q = blockIdx.y;
     if (q >= bb) return;
-    const double *src = A + (ljs + q) * lda;
-    double *dst = dispbuf + (int64_t)q * ldd;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x)
-        dst[r] = src[r];
+    copy_col(dispbuf + (int64_t)q * ldd, A + (ljs + q) * lda, m);
 }
 
 // A(:, local(i + dst)) = S(:, src) for the moves with dst >= bb whose
@@ -80,10 +98,7 @@ __global__ void place_displaced_kernel(double *A, int64_t lda, int64_t m, int64_
     if (d < bb) return;
     const int64_t jg = i + d;
     if (dist_owner(jg, b, P) != me) return;
-    double *dst = A + dist_local(jg, b, P) * lda;
-    const double *src = S + s * lds;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x)
-        dst[r] = src[r];
+    copy_col(A + dist_local(jg, b, P) * lda, S + s * lds, m);
 }
 
 // A(:, ljs + q) = Pbuf(:, q) (owner; all m rows)
@@ -92,10 +107,7 @@ __global__ void copy_back_kernel(double *A, int64_t lda, int64_t m, int64_t ljs,
     if (*bb_eff == 0) return;
     const int q = blockIdx.y;
     if (q >= bb) return;
-    double *dst = A + (ljs + q) * lda;
-    const double *src = pbuf + (int64_t)q * ldp;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x)
-        dst[r] = src[r];
+    copy_col(A + (ljs + q) * lda, pbuf + (int64_t)q * ldp, m);
 }
 
 // replicated jpvt (+ i): the same moves; also the trace's per-panel pivots

@@ -1367,7 +1367,7 @@ struct Run {
         // (1) pack the pivot columns (full height) into this rank's buffer
         double *pk = (P > 1) ? ctx->packbuf : ctx->pbuf;
         {
-            dim3 grid((unsigned)std::min<int64_t>(64, (m + 255) / 256), (unsigned)bb);
+            dim3 grid((unsigned)std::min<int64_t>(64, (m + 2047) / 2048), (unsigned)bb);
             pack_pivots_kernel<<<grid, 256, 0, st>>>(A, lda, m, i, ctx->perm, bb, bb_eff, b, P, me, pk, ldp,
                                                     narrow ? ctx->w2 : nullptr, bulk.bbpad, bulk.bbpad, bulk.lj0,
                                                     ctx->w2g);
@@ -1512,7 +1512,7 @@ struct Run {
         //     displaced columns move and the panel is written back
         ph_begin(ctx, PH_SWAP);
         CKT(join_bulk());
-        const dim3 g1((unsigned)std::min<int64_t>(64, (m + 255) / 256), (unsigned)(2 * bb));
+        const dim3 g1((unsigned)std::min<int64_t>(64, (m + 2047) / 2048), (unsigned)(2 * bb));
         if (P > 1) {
             if (me == owner) {
                 pack_slots_kernel<<<dim3(g1.x, bb), 256, 0, st>>>(A, lda, m, ljs, bb, bb_eff, ctx->dispbuf, ldp);
