@@ -444,6 +444,80 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_rowmul_kernel(const double
 }
 
 // ---------------------------------------------------------------------------
+// The m'-row products of the panel (Q1 = P R1^{-1}, V2 = -Q1bottom C): same
+// arithmetic and epilogue as cqr_rowmul_kernel (for every output element the
+// same ascending-k DMMA chain, so the same bits), with 512 threads: 16 warps,
+// two per 8-row tile, each owning half of the 8-column tiles -- four warps per
+// SM sub-partition instead of two, so one warp's fragment loads and epilogue
+// stores overlap the others' DMMAs.  No prefetch (128 registers per thread).
+// ---------------------------------------------------------------------------
+constexpr int RM2_THREADS = 512;
+__global__ void __launch_bounds__(RM2_THREADS, 1) cqr_rowmul2_kernel(const double *X, int64_t ldx, int64_t r0, int64_t rows,
+                                                                   int bb, int bbpad, const double *R, double s,
+                                                                   double *Y, int64_t ldy, const int *status, int mode,
+                                                                   double *A, int64_t lda, double *vt) {
+    constexpr int NH = 2, NTW = 16 / NH;
+    extern __shared__ __align__(16) double rm_sm[];  // bbpad x (bbpad + pad)
+    if (*status != 0) return;
+    const int ldr = bbpad + 4;
+    for (int e = threadIdx.x; e < bbpad * bbpad / 2; e += blockDim.x) {
+        const int k = (2 * e) % bbpad, c = (2 * e) / bbpad;
+        cp_async16(&rm_sm[k + c * ldr], &R[k + (int64_t)c * bbpad], 16);
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int fr = lane >> 2, fk = lane & 3;
+    const int rt = warp / NH, h = warp % NH;
+    constexpr int RPC = (RM2_THREADS / 32 / NH) * 8;  // rows per CTA round
+    const int NT = bbpad / 8;
+    const int ntb = h * NTW;  // this warp's first 8-column tile
+    for (int64_t rbase = r0 + (int64_t)blockIdx.x * RPC + rt * 8; rbase < rows; rbase += (int64_t)gridDim.x * RPC) {
+        const int64_t r = rbase + fr;
+        double af[CQR_MAXB / 4];
+#pragma unroll
+        for (int kk = 0; kk < CQR_MAXB / 4; ++kk) {
+            const int k = kk * 4 + fk;
+            af[kk] = (kk * 4 < bbpad && r < rows && k < bb) ? X[r + (int64_t)k * ldx] : 0.0;
+        }
+        double acc[NTW][2];
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < CQR_MAXB / 4; ++kk) {
+            if (kk * 4 >= bbpad) break;
+            const int k = kk * 4 + fk;
+#pragma unroll
+            for (int j = 0; j < NTW; ++j) {
+                if (ntb + j < NT) {
+                    const double b = rm_sm[k + ((ntb + j) * 8 + fr) * ldr];
+                    dmma(acc[j][0], acc[j][1], af[kk], b);
+                }
+            }
+        }
+        __syncwarp();
+        if (r < rows) {
+#pragma unroll
+            for (int j = 0; j < NTW; ++j) {
+                const int nt = ntb + j;
+                if (nt >= NT) continue;
+                double yv[2];
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int c = nt * 8 + 2 * fk + hh;
+                    const double y = (c < bb) ? s * acc[j][hh] : 0.0;
+                    yv[hh] = y;
+                    Y[r + (int64_t)c * ldy] = y;
+                    if (mode == 1 && c < bb) A[r + (int64_t)c * lda] = y;
+                }
+                if (mode == 1)
+                    *reinterpret_cast<double2 *>(&vt[nt * 8 + 2 * fk + r * bbpad]) = make_double2(yv[0], yv[1]);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Householder reconstruction of the top bb x bb block (one CTA):
 //   X = -Q(0:bb, 0:bb); for j: S_j = sign(X_jj) (1 if 0); pivot X_jj + S_j;
 //   L(:, j) = X(j+1:, j) / pivot; Schur update  ->  S - Qtop = L U

@@ -778,6 +778,7 @@ static int create_impl(rqrcp_ctx **out, const rqrcp_config *cfg, int nranks, int
     CKC(smem_attr((const void *)cqr_recon_rg_kernel<128>, (int)cqr_rg_smem_bytes(128), dev));
     CKC(smem_attr((const void *)cqr_recon_rg_kernel<64>, (int)cqr_rg_smem_bytes(64), dev));
     CKC(smem_attr((const void *)cqr_rowmul_kernel, 128 * 132 * 8, dev));
+    CKC(smem_attr((const void *)cqr_rowmul2_kernel, 128 * 132 * 8, dev));
     {
         ctx->sqc_max = 0;
         for (int cs = SQC_MAXG; cs >= 1 && !ctx->sqc_max; --cs) {
@@ -1679,7 +1680,10 @@ struct Run {
         };
         CKT(chol(1, ctx->ptol2));
         // Q1 = P R1^{-1}
-        cqr_rowmul_kernel<<<rgrid(mp), CQR_THREADS, rsm, st>>>(Pp, ldp, 0, mp, bb, bbpad, ctx->cq_rinv, 1.0, vfull, ldv,
+        // (rg path: the 512-thread variant, bitwise the same products)
+        auto bigmul = rg ? cqr_rowmul2_kernel : cqr_rowmul_kernel;
+        const int bthreads = rg ? RM2_THREADS : CQR_THREADS;
+        bigmul<<<rgrid(mp), bthreads, rsm, st>>>(Pp, ldp, 0, mp, bb, bbpad, ctx->cq_rinv, 1.0, vfull, ldv,
                                                                ctx->cqr_status, 0, nullptr, 0, nullptr);
         CKL();
         // G2 = Q1^T Q1, R2, Rc = R2 R1
@@ -1728,7 +1732,7 @@ struct Run {
                 CKL();
                 cm = ctx->cq_c;
             }
-            cqr_rowmul_kernel<<<rgrid(mp - bb), CQR_THREADS, rsm, st>>>(vfull, ldv, bb, mp, bb, bbpad, cm, -1.0,
+            bigmul<<<rgrid(mp - bb), bthreads, rsm, st>>>(vfull, ldv, bb, mp, bb, bbpad, cm, -1.0,
                                                                         vfull, ldv, ctx->cqr_status, 1, Pp, ldp, vt);
             CKL();
         }
