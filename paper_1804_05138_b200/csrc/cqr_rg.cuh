@@ -278,7 +278,8 @@ __global__ void __launch_bounds__(RG_THREADS, 1) cqr_recon_rg_kernel(const doubl
                                                                    int64_t ldqt, double *vfull /* ld ldq */, int64_t ldq,
                                                                    int bb, int bbpad, const double *Rc, int *status,
                                                                    double *A, int64_t lda, double *tau, double *us,
-                                                                   double *Uinv, double *linvt, double *vt) {
+                                                                   double *Uinv, double *linvt, double *vt,
+                                                                   const double *r2inv, double *cmat) {
     constexpr int E = NB / 16;
     static_assert(NB % 16 == 0 && E >= 1 && E <= 8, "NB in 16..128");
     extern __shared__ __align__(16) double rc_img[];  // NB x (NB + 1): transposed outputs, copied out coalesced
@@ -492,6 +493,57 @@ __global__ void __launch_bounds__(RG_THREADS, 1) cqr_recon_rg_kernel(const doubl
     for (int e = tid; e < bbpad * bbpad; e += RG_THREADS) {
         const int r = e % bbpad, c = e / bbpad;
         linvt[e] = rc_img[r + c * LS];
+    }
+    // CTA 1 (the U^{-1} one) also forms C = R2^{-1} U^{-1} for V2 = -Q1bottom C:
+    // both upper triangular, packed in shared memory, register-grid product with
+    // the 16-row t blocks pruned to p <= tb <= q (as the Cholesky's Rc product)
+    if (do_up && cmat) {
+        __syncthreads();  // (one CTA: the L^{-T} copy above still reads the image)
+        double *S2 = rc_img, *S1 = rc_img + NB * (NB + 1) / 2;
+#pragma unroll
+        for (int p = 0; p < E; ++p)
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                const int a = ta + 16 * p, c = tc + 16 * q;
+                if (a <= c) {
+                    S2[upk(a, c)] = (c < bb) ? r2inv[a + (int64_t)c * bbpad] : 0.0;
+                    S1[upk(a, c)] = (c < bb) ? x[p][q] : 0.0;
+                }
+            }
+        __syncthreads();
+        double acc[E][E];
+#pragma unroll
+        for (int p = 0; p < E; ++p)
+#pragma unroll
+            for (int q = 0; q < E; ++q) acc[p][q] = 0.0;
+#pragma unroll
+        for (int tb = 0; tb < E; ++tb) {
+            for (int s = 0; s < 16; ++s) {
+                const int t = 16 * tb + s;
+                double r2[E], r1[E];
+#pragma unroll
+                for (int p = 0; p <= tb; ++p) {
+                    const int a = ta + 16 * p;
+                    r2[p] = (a <= t) ? S2[upk(a, t)] : 0.0;
+                }
+#pragma unroll
+                for (int q = tb; q < E; ++q) {
+                    const int c = tc + 16 * q;
+                    r1[q] = (t <= c) ? S1[upk(t, c)] : 0.0;
+                }
+#pragma unroll
+                for (int p = 0; p <= tb; ++p)
+#pragma unroll
+                    for (int q = tb; q < E; ++q) acc[p][q] = fma(r2[p], r1[q], acc[p][q]);
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < E; ++p)
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                const int a = ta + 16 * p, c = tc + 16 * q;
+                if (a < bbpad && c < bbpad) cmat[a + (int64_t)c * bbpad] = (a <= c && c < bb) ? acc[p][q] : 0.0;
+            }
     }
     cqr_stamp(5);
 }

@@ -1710,7 +1710,8 @@ struct Run {
 #define RGR(NBV)                                                                                                      \
     case NBV:                                                                                                         \
         cqr_recon_rg_kernel<NBV><<<2, RG_THREADS, cqr_rg_smem_bytes(NBV), st>>>(ctx->cq_q, bbpad, vfull, ldv, bb, bbpad, ctx->cq_rc, ctx->cqr_status, Pp, ldp, \
-                                                           tau + i, ctx->cq_lu, ctx->cq_uinv, ctx->cq_g, vt);         \
+                                                           tau + i, ctx->cq_lu, ctx->cq_uinv, ctx->cq_g, vt,          \
+                                                           ctx->cq_rinv, ctx->cq_c);                                  \
         break;
                 RGR(16) RGR(32) RGR(64) RGR(128)
 #undef RGR
@@ -1718,20 +1719,24 @@ struct Run {
             }
         }
         CKL();
-        // -T = -(U S) L^{-T}
-        cqr_rowmul_kernel<<<sgrid(bbpad), CQR_THREADS, rsm, st>>>(ctx->cq_lu, bbpad, 0, bbpad, bb, bbpad, ctx->cq_g, -1.0, ctx->tneg,
-                                                       bbpad, ctx->cqr_status, 0, nullptr, 0, nullptr);
+        // -T = -(U S) L^{-T}: first needed by W2 = -T^T W after W = V^T A22, so on one
+        // GPU it runs on the side stream (ahead of tri_kernel there, which skips T when
+        // this path succeeded; the main stream joins before W2).  P > 1: the owner
+        // broadcasts T right after the panel, so it stays on the main stream.
+        cudaStream_t tst = st;
+        if (P == 1) {
+            CK(cudaEventRecord(ctx->ev_fork, st));
+            CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+            tst = ctx->side;
+        }
+        cqr_rowmul_kernel<<<sgrid(bbpad), CQR_THREADS, rsm, tst>>>(ctx->cq_lu, bbpad, 0, bbpad, bb, bbpad, ctx->cq_g, -1.0,
+                                                                ctx->tneg, bbpad, ctx->cqr_status, 0, nullptr, 0, nullptr);
         CKL();
         // V2 = -Qbottom U^{-1} (into Vfull, the panel and Vt); rg path: C = R2^{-1} U^{-1}
         // (bb x bb, one CTA) then V2 = -Q1bottom C
         if (mp > bb) {
             const double *cm = ctx->cq_uinv;
-            if (rg) {
-                cqr_rowmul_kernel<<<sgrid(bbpad), CQR_THREADS, rsm, st>>>(ctx->cq_rinv, bbpad, 0, bbpad, bb, bbpad, ctx->cq_uinv, 1.0,
-                                                              ctx->cq_c, bbpad, ctx->cqr_status, 0, nullptr, 0, nullptr);
-                CKL();
-                cm = ctx->cq_c;
-            }
+            if (rg) cm = ctx->cq_c;  // formed by the reconstruction's second CTA
             bigmul<<<rgrid(mp - bb), bthreads, rsm, st>>>(vfull, ldv, bb, mp, bb, bbpad, cm, -1.0,
                                                                         vfull, ldv, ctx->cqr_status, 1, Pp, ldp, vt);
             CKL();

@@ -81,7 +81,7 @@ static void run(int bb) {
             CK(cudaMemset(st, 0, 4));
             cudaEventRecord(e0);
             if (v == 0) cqr_recon_kernel<<<1, CQR_THREADS, sm>>>(dQ, bbpad, bb, bbpad, nb, dRc[v], st, dA[v], bbpad, dtau[v], dus[v], dui[v], dli[v], dvt[v]);
-            else cqr_recon_rg_kernel<NB><<<2, RG_THREADS, smr>>>(dQ2c, bbpad, dQ, bbpad, bb, bbpad, dRc[v], st, dA[v], bbpad, dtau[v], dus[v], dui[v], dli[v], dvt[v]);
+            else cqr_recon_rg_kernel<NB><<<2, RG_THREADS, smr>>>(dQ2c, bbpad, dQ, bbpad, bb, bbpad, dRc[v], st, dA[v], bbpad, dtau[v], dus[v], dui[v], dli[v], dvt[v], nullptr, nullptr);
             cudaEventRecord(e1);
             CK(cudaEventSynchronize(e1));
             CK(cudaGetLastError());
