@@ -347,7 +347,6 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
                     double *q = &xsm[(t - LR) * SQR_THREADS + tid];
                     const double nv = *q - tw * xs[t];
                     *q = nv;
-                    if (t == j) bj = nv;
                     ++t;
                 }
 #pragma unroll 2
@@ -358,15 +357,14 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
                     const double n1 = q[SQR_THREADS] - tw * v01.y;
                     q[0] = n0;
                     q[SQR_THREADS] = n1;
-                    if (t == j) bj = n0;
-                    if (t + 1 == j) bj = n1;
                 }
                 for (; t < L; ++t) {
                     double *q = &xsm[(t - LR) * SQR_THREADS + tid];
                     const double nv = *q - tw * xs[t];
                     *q = nv;
-                    if (t == j) bj = nv;
                 }
+                // the updated x(j), read back once instead of selected in the loop
+                if (j >= LR) bj = xsm[(j - LR) * SQR_THREADS + tid];
             }
             double rn = r - bj * bj;
             if (rn < 1e-6 * r0) {  // recompute from the updated rows (R-G6)

@@ -353,7 +353,6 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
                     double *q = &xsm[(t - S0) * TH + tid];
                     const double nv = *q - tw * xs[t];
                     *q = nv;
-                    if (t == j) bj = nv;
                     ++t;
                 }
 #pragma unroll 2
@@ -364,15 +363,14 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
                     const double n1 = q[TH] - tw * v01.y;
                     q[0] = n0;
                     q[TH] = n1;
-                    if (t == j) bj = n0;
-                    if (t + 1 == j) bj = n1;
                 }
                 for (; t < L; ++t) {
                     double *q = &xsm[(t - S0) * TH + tid];
                     const double nv = *q - tw * xs[t];
                     *q = nv;
-                    if (t == j) bj = nv;
                 }
+                // the updated x(j), read back once instead of selected in the loop
+                if (j >= S0) bj = xsm[(j - S0) * TH + tid];
             }
             double rn = r - bj * bj;
             if (rn < 1e-6 * r0) {  // recompute from the updated rows (R-G6)
