@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
     constexpr int L = LR + LS;
     extern __shared__ __align__(16) double sq_dyn[];  // max(LS x 256, bb x L) doubles
     __shared__ __align__(16) double xs[L + 1];
-    __shared__ double xraw[L];
+    __shared__ __align__(16) double xraw[L + (L & 1)];
     __shared__ double wv[SQ_WARPS];
     __shared__ int wpos[SQ_WARPS], wcol[SQ_WARPS];
     __shared__ double s_tau, s_beta, s_alpha;
@@ -123,7 +123,9 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
         // the owner stages its register rows in xraw (free until the next poll)
         if (act && (int)pc == bc) {
 #pragma unroll
-            for (int t = 0; t < LR; ++t) xraw[t] = x[t];
+            for (int t = 0; t + 1 < LR; t += 2)  // 16-byte stores (xraw is 16-byte aligned)
+                *reinterpret_cast<double2 *>(&xraw[t]) = make_double2(x[t], x[t + 1]);
+            if (LR & 1) xraw[LR - 1] = x[LR - 1];
         }
         __syncthreads();
         if (warp == 0) {

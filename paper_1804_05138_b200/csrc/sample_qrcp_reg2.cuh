@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
     constexpr int R0 = LT, S0 = LT + LR;  // first register row, first shared-memory row
     extern __shared__ __align__(16) double sq_dyn[];  // max(LS x TH, bb x L) doubles
     __shared__ __align__(16) double xs[L + 1];
-    __shared__ double xraw[L];
+    __shared__ __align__(16) double xraw[L + (L & 1)];
     __shared__ double wv[NW];
     __shared__ int wpos[NW], wcol[NW];
     __shared__ double s_tau, s_beta, s_alpha;
@@ -111,8 +111,15 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
         // the owner stages its top and register rows in xraw (free until the next poll)
         if (act && (int)pc == bc) {
             for (int t = 0; t < LT; ++t) xraw[t] = __ldcg(&xt[t * TH]);
+            if ((R0 & 1) == 0) {  // 16-byte stores (xraw is 16-byte aligned)
 #pragma unroll
-            for (int t = 0; t < LR; ++t) xraw[R0 + t] = x[t];
+                for (int t = 0; t + 1 < LR; t += 2)
+                    *reinterpret_cast<double2 *>(&xraw[R0 + t]) = make_double2(x[t], x[t + 1]);
+                if (LR & 1) xraw[R0 + LR - 1] = x[LR - 1];
+            } else {
+#pragma unroll
+                for (int t = 0; t < LR; ++t) xraw[R0 + t] = x[t];
+            }
         }
         __syncthreads();
         if (warp == 0) {
