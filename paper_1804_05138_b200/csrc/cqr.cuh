@@ -450,6 +450,8 @@ __global__ void __launch_bounds__(CQR_THREADS, 1) cqr_rowmul_kernel(const double
 // two per 8-row tile, each owning half of the 8-column tiles -- four warps per
 // SM sub-partition instead of two, so one warp's fragment loads and epilogue
 // stores overlap the others' DMMAs.  No prefetch (128 registers per thread).
+// In place (V2) is safe: a CTA barrier separates each round's loads from its
+// stores (the warp pair of a row tile reads all columns, writes half each).
 // ---------------------------------------------------------------------------
 constexpr int RM2_THREADS = 512;
 __global__ void __launch_bounds__(RM2_THREADS, 1) cqr_rowmul2_kernel(const double *X, int64_t ldx, int64_t r0, int64_t rows,
@@ -472,7 +474,11 @@ __global__ void __launch_bounds__(RM2_THREADS, 1) cqr_rowmul2_kernel(const doubl
     constexpr int RPC = (RM2_THREADS / 32 / NH) * 8;  // rows per CTA round
     const int NT = bbpad / 8;
     const int ntb = h * NTW;  // this warp's first 8-column tile
-    for (int64_t rbase = r0 + (int64_t)blockIdx.x * RPC + rt * 8; rbase < rows; rbase += (int64_t)gridDim.x * RPC) {
+    // rounds are uniform over the CTA: the two warps of a row tile read ALL
+    // columns of their rows, so (in place: V2 overwrites its input) every
+    // fragment load of a round precedes the round's stores (CTA barrier)
+    for (int64_t base = r0 + (int64_t)blockIdx.x * RPC; base < rows; base += (int64_t)gridDim.x * RPC) {
+        const int64_t rbase = base + rt * 8;
         const int64_t r = rbase + fr;
         double af[CQR_MAXB / 4];
 #pragma unroll
@@ -480,6 +486,7 @@ __global__ void __launch_bounds__(RM2_THREADS, 1) cqr_rowmul2_kernel(const doubl
             const int k = kk * 4 + fk;
             af[kk] = (kk * 4 < bbpad && r < rows && k < bb) ? X[r + (int64_t)k * ldx] : 0.0;
         }
+        __syncthreads();
         double acc[NTW][2];
 #pragma unroll
         for (int j = 0; j < NTW; ++j) acc[j][0] = acc[j][1] = 0.0;

@@ -60,6 +60,7 @@ struct Opts {
     int upd_kernel = 2;      // update GEMM: 0 CTA-wide TMA epilogue, 1 / 2 warp-specialised (BK 32 x 2 / 16 x 4 stages)
     int sq_cluster = 1, sq_reg = 1, sq_grid = 0, sq_nsm = -1, sq_hstride = 8, sq_poll = 3;
     int debug_sync = 0, trace = 0, trace_panel = 1;
+    int sq_wide = 1;         // register-grid sample QRCP on every SM for wide samples (0: the fewest CTAs; 2: always)
     int cqr_rg = 1;          // CholeskyQR2 panel: 1 register-grid one-CTA factorizations (cqr_rg.cuh), 0 shared-memory
     int host_out = 0;        // rqrcp_factor_host output: 0 the whole factored A, 1 the factors only (columns
                              // 0..k-1 full height = V and R11, rows 0..k-1 of columns k..n-1 = R12; R22 not copied)
@@ -76,7 +77,7 @@ static const OptDesc kOpts[] = {{"schedule", -1, 2},     {"panel", 0, 2},     {"
                                 {"sq_poll", 0, 3},       {"debug_sync", 0, 1}, {"trace", 0, 1},
                                 {"trace_panel", 1, 1 << 30}, {"nccl_timeout_ms", 1, (int64_t)1 << 40},
                                 {"upd_kernel", 0, 2}, {"pn_blocked", 0, 2},
-                                {"tournament", 0, 64}, {"gemm_ws", 0, 1}, {"host_out", 0, 1}, {"cqr_rg", 0, 1}};
+                                {"tournament", 0, 64}, {"gemm_ws", 0, 1}, {"host_out", 0, 1}, {"cqr_rg", 0, 1}, {"sq_wide", 0, 2}};
 static bool opt_set(Opts &o, const std::string &n, int64_t v) {
 #define OPT(field)                    \
     if (n == #field) {                \
@@ -85,7 +86,7 @@ static bool opt_set(Opts &o, const std::string &n, int64_t v) {
     }
     OPT(schedule) OPT(panel) OPT(pn_cluster) OPT(pn_cpt) OPT(pn_grid) OPT(pn_rows) OPT(la_panel_ctas)
     OPT(sq_cluster) OPT(sq_reg) OPT(sq_grid) OPT(sq_nsm) OPT(sq_hstride) OPT(sq_poll) OPT(debug_sync) OPT(trace)
-    OPT(trace_panel) OPT(nccl_timeout_ms) OPT(upd_kernel) OPT(pn_blocked) OPT(tournament) OPT(gemm_ws) OPT(host_out) OPT(cqr_rg)
+    OPT(trace_panel) OPT(nccl_timeout_ms) OPT(upd_kernel) OPT(pn_blocked) OPT(tournament) OPT(gemm_ws) OPT(host_out) OPT(cqr_rg) OPT(sq_wide)
 #undef OPT
     return false;
 }
@@ -1045,6 +1046,16 @@ static SqKernels sq_kernels(int l) {
 }
 enum SqKind { SQK_CLUSTER = 0, SQK_REG = 1, SQK_GRID = 2, SQK_REG2 = 3 };
 static int sq_reg2_grid(int64_t np) { return 1 + (int)((np + SQR2_THREADS - 1) / SQR2_THREADS); }
+// Launch grid of the register-grid kernels: the fewest CTAs that hold the
+// sample (one column per thread) -- or, for wide samples that fit, every SM
+// (fewer columns per CTA: less per-step apply work on each SM; the exchange
+// polls one header per CTA either way).  Decided from (np, SM count) only.
+static int sq_reg_launch_grid(const rqrcp_ctx *ctx, int64_t np, int threads) {
+    const int base = 1 + (int)((np + threads - 1) / threads);
+    const int cap = std::min(ctx->num_sms, SQ_MAXG);
+    if (ctx->opt.sq_wide && base <= cap && (np >= (int64_t)64 * cap || ctx->opt.sq_wide == 2)) return cap;
+    return base;
+}
 static SqKind sq_kind(const rqrcp_ctx *ctx, int l, int64_t np) {
     const SqKernels k = sq_kernels(l);
     const int64_t need = (np + SQC_THREADS - 1) / SQC_THREADS;
@@ -1054,15 +1065,15 @@ static SqKind sq_kind(const rqrcp_ctx *ctx, int l, int64_t np) {
     if (ctx->opt.sq_reg == 1 && k.reg && grid <= cap) return SQK_REG;
     // wider samples: the 512-thread register grid (top rows in the spill scratch)
     if (ctx->opt.sq_reg && k.reg2 && sq_reg2_grid(np) <= cap &&
-        (int64_t)sq_reg2_grid(np) * k.reg2_lt * SQR2_THREADS <= ctx->spill_cap)
+        (int64_t)sq_reg_launch_grid(ctx, np, SQR2_THREADS) * k.reg2_lt * SQR2_THREADS <= ctx->spill_cap)
         return SQK_REG2;
     return SQK_GRID;
 }
 static int sq_ctas(const rqrcp_ctx *ctx, int l, int64_t np) {
     switch (sq_kind(ctx, l, np)) {
         case SQK_CLUSTER: return (int)std::max<int64_t>(1, (np + SQC_THREADS - 1) / SQC_THREADS);
-        case SQK_REG: return 1 + (int)((np + SQR_THREADS - 1) / SQR_THREADS);
-        case SQK_REG2: return sq_reg2_grid(np);
+        case SQK_REG: return sq_reg_launch_grid(ctx, np, SQR_THREADS);
+        case SQK_REG2: return sq_reg_launch_grid(ctx, np, SQR2_THREADS);
         default: return std::min(ctx->num_sms, SQ_MAXG);
     }
 }
@@ -1155,13 +1166,13 @@ struct Run {
             return cluster_launch(ctx, kt.cluster, cs, SQC_THREADS, (size_t)bb * l * sizeof(double), a);
         }
         if (kind == SQK_REG2) {
-            const int grid = sq_reg2_grid(np);
+            const int grid = sq_reg_launch_grid(ctx, np, SQR2_THREADS);
             const size_t smem = (size_t)std::max(kt.reg2_ls * SQR2_THREADS, bb * l) * sizeof(double);
             void *args[] = {&a};
             return coop_launch(ctx, (const void *)kt.reg2, grid, SQR2_THREADS, args, smem);
         }
         if (kind == SQK_REG) {
-            const int grid = 1 + (int)((np + SQR_THREADS - 1) / SQR_THREADS);
+            const int grid = sq_reg_launch_grid(ctx, np, SQR_THREADS);
             const size_t smem = (size_t)std::max(kt.reg_ls * SQR_THREADS, bb * l) * sizeof(double);
             a.hstride = 8;
             void *args[] = {&a};

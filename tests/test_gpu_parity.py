@@ -31,7 +31,7 @@ ELEM_RTOL = 1e-10
 RECON_TOL = 1e-13
 
 DEFAULT_OPTS = dict(schedule=-1, panel=2, upd_kernel=2, pn_blocked=1, tournament=0, gemm_ws=1, pn_cluster=1, pn_cpt=2, pn_grid=0, pn_rows=128, la_panel_ctas=48,
-                    sq_cluster=1, sq_reg=1, sq_grid=0, sq_nsm=-1, sq_hstride=8, sq_poll=3, cqr_rg=1, host_out=0)
+                    sq_cluster=1, sq_reg=1, sq_grid=0, sq_nsm=-1, sq_hstride=8, sq_poll=3, cqr_rg=1, host_out=0, sq_wide=1)
 
 
 @pytest.fixture(scope="module")
@@ -512,6 +512,26 @@ def test_sample_qrcp_register_grid(ctx, name, kind, m, n, k, b, p, seed):
     compare(A, g, o, k)
 
 
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", REG_CASES[:3] + REG_CASES[-3:],
+                         ids=[c[0] for c in REG_CASES[:3] + REG_CASES[-3:]])
+def test_sample_qrcp_register_grid_all_sms_bitwise(ctx, name, kind, m, n, k, b, p, seed):
+    """sq_wide = 2 spreads the sample over every SM (fewer columns per CTA, the
+    launch bench.py takes for wide samples); the per-column arithmetic and the
+    tie rule do not depend on the partition: bitwise the fewest-CTA launch."""
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    with options(ctx, sq_cluster=0, sq_wide=0):
+        g0 = gpu_factor(ctx, A, k, b, p, seed)
+    with options(ctx, sq_cluster=0, sq_wide=2):
+        g2 = gpu_factor(ctx, A, k, b, p, seed)
+    with options(ctx, sq_cluster=0, sq_reg=2, sq_wide=2):
+        g3 = gpu_factor(ctx, A, k, b, p, seed)
+    with options(ctx, sq_cluster=0, sq_reg=2, sq_wide=0):
+        g4 = gpu_factor(ctx, A, k, b, p, seed)
+    for key in ("A", "jpvt", "tau"):
+        assert np.array_equal(g0[key], g2[key]), key
+        assert np.array_equal(g3[key], g4[key]), key
+
+
 # the 512-thread register grid with the top 60 rows in global memory
 # (sample_qrcp_reg2.cuh, l = 144: the C5 sample); sq_reg = 2 selects it at
 # oracle-feasible widths, including samples narrower than one CTA per SM
@@ -713,6 +733,45 @@ def test_cqr_panel_parity(ctx, name, kind, m, n, k, b, p, seed, rg):
         t = ctx.timings()
     compare(A, g, o, k)
     assert t["panels_householder"] < t["panels"]
+
+
+def test_cqr_tall_in_place_products_deterministic():
+    """Tall panels through the CholeskyQR2 path (the default from 8192 rows): the
+    512-thread row product writes V2 over its own input (two warps per row tile),
+    which needs every fragment load of a round before the round's stores -- a race
+    there shows as run-to-run differences and a broken reconstruction.  Three runs
+    bitwise equal, and A Pi = Q R to 1e-13 (probe)."""
+    import paper_1804_05138_b200 as rq
+    m, n, k, b, p = 40000, 640, 384, 128, 16
+    A = inputs.make("graded", m, n, 31).numpy()
+    c = rq.RQRCP(max_m=m, max_n=n, max_b=b, max_p=p)
+    outs = []
+    for _ in range(3):
+        Ad = to_dev(A)
+        jpvt, tau, rank = c.factor(Ad, k, b, p, seed=31)
+        torch.cuda.synchronize()
+        outs.append((Ad.cpu().numpy(), jpvt.cpu().numpy(), tau.cpu().numpy()))
+    t = c.timings()
+    c.close()
+    assert t["panels_householder"] < t["panels"]  # the CholeskyQR2 path ran
+    for o in outs[1:]:
+        assert all(np.array_equal(x, y) for x, y in zip(outs[0], o))
+    F, jp, ta = outs[0]
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((n, 2))
+    R = np.triu(F[:k, :])
+    RX = np.zeros((m, 2))
+    RX[:k] = R @ X
+    RX[k:] = (F[:, k:] @ X[k:])[k:]
+    Xp = np.zeros_like(X)
+    Xp[jp] = X
+    Y = RX.copy()
+    for j in range(k - 1, -1, -1):
+        v = F[j:, j].copy()
+        v[0] = 1.0
+        Y[j:] -= ta[j] * np.outer(v, v @ Y[j:])
+    err = np.linalg.norm(A @ Xp - Y) / (np.linalg.norm(A) * np.linalg.norm(X))
+    assert err <= 1e-13, err
 
 
 def test_cqr_guard_falls_back(ctx):
