@@ -187,6 +187,10 @@ int rqrcp_factor_ex(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n
  *                 2 always the 512-thread kernel when it exists for l; 0 neither
  *   sq_poll       grid sample QRCP exchange: 3 tagged 16-byte units (no fences), 0 acquire
  *                 polls, 1 relaxed polls + one fence, 2 as 1 with backoff
+ *   sq_wide       register-grid sample QRCP launch: 1 (default) every SM for wide samples
+ *                 (n' >= 64 x SMs), 2 always every SM, 0 the fewest CTAs that hold the sample
+ *   cqr_rg        CholeskyQR2 panel one-CTA factorizations: 1 (default) register grid, 0 shared
+ *                 memory
  *   debug_sync    synchronise after every launch
  *   host_out      rqrcp_factor_host output: 0 (default) the whole factored A; 1 the factors
  *                 only -- columns 0..k-1 full height (V below, R11 on / above the diagonal) and
