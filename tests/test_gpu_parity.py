@@ -774,6 +774,23 @@ def test_cqr_tall_in_place_products_deterministic():
     assert err <= 1e-13, err
 
 
+def test_cqr_default_crosses_row_threshold():
+    """Default panel option 2: CholeskyQR2 while the panel has >= 8192 rows, the
+    column-by-column kernels below -- one factorization crossing the threshold
+    (m = 8300, b = 128: panel 0 via CholeskyQR2, panels 1.. via Householder)
+    matches the oracle like any other case."""
+    import paper_1804_05138_b200 as rq
+    m, n, k, b, p, seed = 8300, 600, 384, 128, 16, 41
+    A = inputs.make("iid", m, n, seed).numpy()
+    o = oracle.rqrcp(A, k, b, p, seed=seed)
+    c = rq.RQRCP(max_m=m, max_n=n, max_b=b, max_p=p)
+    g = gpu_factor(c, A, k, b, p, seed)
+    t = c.timings()
+    c.close()
+    compare(A, g, o, k)
+    assert 0 < t["panels_householder"] < t["panels"]
+
+
 def test_cqr_guard_falls_back(ctx):
     """A rank-stopped panel fails the CholeskyQR2 guard and is factored by the
     column-by-column kernel; the result matches the oracle's."""
