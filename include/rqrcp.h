@@ -189,6 +189,9 @@ int rqrcp_factor_ex(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n
  *                 polls, 1 relaxed polls + one fence, 2 as 1 with backoff
  *   sq_wide       register-grid sample QRCP launch: 1 (default) every SM for wide samples
  *                 (n' >= 64 x SMs), 2 always every SM, 0 the fewest CTAs that hold the sample
+ *   sq_smtop      register-grid sample QRCP row layout (l = 144): 1 (default) the shared-memory
+ *                 rows above the register rows (step j touches rows >= j only, so they drop out
+ *                 of the per-step shared-memory traffic), 0 below them
  *   cqr_rg        CholeskyQR2 panel one-CTA factorizations: 1 (default) register grid, 0 shared
  *                 memory
  *   debug_sync    synchronise after every launch

@@ -61,6 +61,8 @@ struct Opts {
     int sq_cluster = 1, sq_reg = 1, sq_grid = 0, sq_nsm = -1, sq_hstride = 8, sq_poll = 3;
     int debug_sync = 0, trace = 0, trace_panel = 1;
     int sq_wide = 1;         // register-grid sample QRCP on every SM for wide samples (0: the fewest CTAs; 2: always)
+    int sq_smtop = 1;        // register-grid sample QRCP: shared-memory rows above the register rows (they drop out
+                             // of the per-step traffic as the panel advances); 0: below
     int cqr_rg = 1;          // CholeskyQR2 panel: 1 register-grid one-CTA factorizations (cqr_rg.cuh), 0 shared-memory
     int host_out = 0;        // rqrcp_factor_host output: 0 the whole factored A, 1 the factors only (columns
                              // 0..k-1 full height = V and R11, rows 0..k-1 of columns k..n-1 = R12; R22 not copied)
@@ -77,7 +79,8 @@ static const OptDesc kOpts[] = {{"schedule", -1, 2},     {"panel", 0, 2},     {"
                                 {"sq_poll", 0, 3},       {"debug_sync", 0, 1}, {"trace", 0, 1},
                                 {"trace_panel", 1, 1 << 30}, {"nccl_timeout_ms", 1, (int64_t)1 << 40},
                                 {"upd_kernel", 0, 2}, {"pn_blocked", 0, 2},
-                                {"tournament", 0, 64}, {"gemm_ws", 0, 1}, {"host_out", 0, 1}, {"cqr_rg", 0, 1}, {"sq_wide", 0, 2}};
+                                {"tournament", 0, 64}, {"gemm_ws", 0, 1}, {"host_out", 0, 1}, {"cqr_rg", 0, 1}, {"sq_wide", 0, 2},
+                                {"sq_smtop", 0, 1}};
 static bool opt_set(Opts &o, const std::string &n, int64_t v) {
 #define OPT(field)                    \
     if (n == #field) {                \
@@ -86,7 +89,7 @@ static bool opt_set(Opts &o, const std::string &n, int64_t v) {
     }
     OPT(schedule) OPT(panel) OPT(pn_cluster) OPT(pn_cpt) OPT(pn_grid) OPT(pn_rows) OPT(la_panel_ctas)
     OPT(sq_cluster) OPT(sq_reg) OPT(sq_grid) OPT(sq_nsm) OPT(sq_hstride) OPT(sq_poll) OPT(debug_sync) OPT(trace)
-    OPT(trace_panel) OPT(nccl_timeout_ms) OPT(upd_kernel) OPT(pn_blocked) OPT(tournament) OPT(gemm_ws) OPT(host_out) OPT(cqr_rg) OPT(sq_wide)
+    OPT(trace_panel) OPT(nccl_timeout_ms) OPT(upd_kernel) OPT(pn_blocked) OPT(tournament) OPT(gemm_ws) OPT(host_out) OPT(cqr_rg) OPT(sq_wide) OPT(sq_smtop)
 #undef OPT
     return false;
 }
@@ -764,7 +767,9 @@ static int create_impl(rqrcp_ctx **out, const rqrcp_config *cfg, int nranks, int
     CKC(smem_attr((const void *)sample_qrcp_reg_kernel<40, 0>, 128 * 40 * 8, dev));
     CKC(smem_attr((const void *)sample_qrcp_reg_kernel<74, 0>, 128 * 74 * 8, dev));
     CKC(smem_attr((const void *)sample_qrcp_reg_kernel<72, 72>, 128 * 144 * 8, dev));
+    CKC(smem_attr((const void *)sample_qrcp_reg_kernel<72, 72, true>, 128 * 144 * 8, dev));
     CKC(smem_attr((const void *)sample_qrcp_reg2_kernel<60, 32, 52>, 52 * SQR2_THREADS * 8, dev));
+    CKC(smem_attr((const void *)sample_qrcp_reg2_kernel<60, 32, 52, true>, 52 * SQR2_THREADS * 8, dev));
     for (const void *k : {(const void *)sample_qrcp_cluster_kernel<40>, (const void *)sample_qrcp_cluster_kernel<74>,
                           (const void *)sample_qrcp_cluster_kernel<80>}) {
         CKC(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -1036,12 +1041,16 @@ struct SqKernels {
     void (*reg2)(SqArgs);  // 512-thread register grid with the top rows in global memory
     int reg2_lt, reg2_ls;
 };
-static SqKernels sq_kernels(int l) {
+static SqKernels sq_kernels(int l, bool smtop = true) {
     if (l == 40) return {sample_qrcp_cluster_kernel<40>, sample_qrcp_reg_kernel<40, 0>, 0, nullptr, 0, 0};
     if (l == 74) return {sample_qrcp_cluster_kernel<74>, sample_qrcp_reg_kernel<74, 0>, 0, nullptr, 0, 0};
     if (l == 80) return {sample_qrcp_cluster_kernel<80>, nullptr, 0, nullptr, 0, 0};
-    if (l == 144)
+    if (l == 144) {
+        if (smtop)
+            return {nullptr, sample_qrcp_reg_kernel<72, 72, true>, 72, sample_qrcp_reg2_kernel<60, 32, 52, true>, 60,
+                    52};
         return {nullptr, sample_qrcp_reg_kernel<72, 72>, 72, sample_qrcp_reg2_kernel<60, 32, 52>, 60, 52};
+    }
     return {nullptr, nullptr, 0, nullptr, 0, 0};
 }
 enum SqKind { SQK_CLUSTER = 0, SQK_REG = 1, SQK_GRID = 2, SQK_REG2 = 3 };
@@ -1160,7 +1169,7 @@ struct Run {
         const int bb = a.bb;
         a.tag0 = (++ctx->launch_seq) << 8;
         const SqKind kind = sq_kind(ctx, l, np);
-        const SqKernels kt = sq_kernels(l);
+        const SqKernels kt = sq_kernels(l, ctx->opt.sq_smtop != 0);
         if (kind == SQK_CLUSTER) {
             const int cs = (int)std::max<int64_t>(1, (np + SQC_THREADS - 1) / SQC_THREADS);
             return cluster_launch(ctx, kt.cluster, cs, SQC_THREADS, (size_t)bb * l * sizeof(double), a);

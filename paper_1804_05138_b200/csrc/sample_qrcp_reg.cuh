@@ -31,9 +31,17 @@ constexpr int SQR_THREADS = 256;
 constexpr int SQR_CH = 16;  // rows per skipped chunk of the register rows (as SQC_CH)
 constexpr int SQR_UNITS = SQ_MAXL + 2;  // 16-byte units per slot: header (2) + column
 
-template <int LR, int LS>
+// SMT (shared-memory top): rows [0, LS) in shared memory, rows [LS, L) in
+// registers.  Step j touches rows >= j only, so with the shared-memory rows on
+// top they drop out of the per-step shared-memory traffic as the panel
+// advances (l = 144, bb = 128: 2628 instead of 7676 row-steps per panel);
+// the register rows cost no shared-memory bandwidth wherever they sit.
+template <int LR, int LS, bool SMT = false>
 __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs a) {
     constexpr int L = LR + LS;
+    constexpr int R0 = SMT ? LS : 0;   // first register row
+    constexpr int S0 = SMT ? 0 : LR;   // first shared-memory row
+    constexpr int SE = S0 + LS;        // end of the shared-memory rows
     extern __shared__ __align__(16) double sq_dyn[];  // max(LS x 256, bb x L) doubles
     __shared__ __align__(16) double xs[L + 1];
     __shared__ __align__(16) double xraw[L + (L & 1)];
@@ -74,26 +82,29 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
         const double2 *src = reinterpret_cast<const double2 *>(a.B + pc * a.ldb);
 #pragma unroll
         for (int t = 0; t < LR; t += 2) {
-            const double2 v = src[t / 2];
+            const double2 v = src[(R0 + t) / 2];
             x[t] = v.x;
             x[t + 1] = v.y;
         }
 #pragma unroll 4
         for (int t = 0; t < LS; t += 2) {
-            const double2 v = src[(LR + t) / 2];
+            const double2 v = src[(S0 + t) / 2];
             xsm[t * SQR_THREADS + tid] = v.x;
             xsm[(t + 1) * SQR_THREADS + tid] = v.y;
         }
     } else {
 #pragma unroll
-        for (int t = 0; t < LR; ++t) x[t] = have ? a.B[t + pc * a.ldb] : 0.0;
+        for (int t = 0; t < LR; ++t) x[t] = have ? a.B[(R0 + t) + pc * a.ldb] : 0.0;
 #pragma unroll 4
-        for (int t = 0; t < LS; ++t) xsm[t * SQR_THREADS + tid] = have ? a.B[(LR + t) + pc * a.ldb] : 0.0;
+        for (int t = 0; t < LS; ++t) xsm[t * SQR_THREADS + tid] = have ? a.B[(S0 + t) + pc * a.ldb] : 0.0;
     }
     double r = 0.0;
+    if (SMT)  // ascending rows
+        for (int t = 0; t < LS; ++t) r += xsm[t * SQR_THREADS + tid] * xsm[t * SQR_THREADS + tid];
 #pragma unroll
     for (int t = 0; t < LR; ++t) r += x[t] * x[t];
-    for (int t = 0; t < LS; ++t) r += xsm[t * SQR_THREADS + tid] * xsm[t * SQR_THREADS + tid];
+    if (!SMT)
+        for (int t = 0; t < LS; ++t) r += xsm[t * SQR_THREADS + tid] * xsm[t * SQR_THREADS + tid];
     double r0 = r;
     int lpos = (int)pc;
     bool act = have;
@@ -123,9 +134,9 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
         // the owner stages its register rows in xraw (free until the next poll)
         if (act && (int)pc == bc) {
 #pragma unroll
-            for (int t = 0; t + 1 < LR; t += 2)  // 16-byte stores (xraw is 16-byte aligned)
-                *reinterpret_cast<double2 *>(&xraw[t]) = make_double2(x[t], x[t + 1]);
-            if (LR & 1) xraw[LR - 1] = x[LR - 1];
+            for (int t = 0; t + 1 < LR; t += 2)  // 16-byte stores (xraw is 16-byte aligned; R0 even)
+                *reinterpret_cast<double2 *>(&xraw[R0 + t]) = make_double2(x[t], x[t + 1]);
+            if (LR & 1) xraw[R0 + LR - 1] = x[LR - 1];
         }
         __syncthreads();
         if (warp == 0) {
@@ -134,7 +145,7 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
             if (bc >= 0) {
                 const int oc = bc - (int)c_lo;
                 for (int t = lane; t < l; t += 32) {
-                    const double xv = (t < LR) ? xraw[t] : xsm[(t - LR) * SQR_THREADS + oc];
+                    const double xv = (t >= S0 && t < SE) ? xsm[(t - S0) * SQR_THREADS + oc] : xraw[t];
                     ll_store(dst + 2 + t, (unsigned long long)__double_as_longlong(xv), tg);
                 }
             }
@@ -298,23 +309,13 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
             // entirely above row j are skipped (uniform branches); four
             // independent accumulators
             double d[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-            for (int c0 = 0; c0 < LR; c0 += SQR_CH) {
-                if (j < c0 + SQR_CH) {
-#pragma unroll
-                    for (int t = c0; t < c0 + SQR_CH && t + 1 < LR; t += 2) {
-                        const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
-                        d[(t >> 1) & 3] += v2.x * x[t] + v2.y * x[t + 1];
-                    }
-                    if ((LR & 1) && c0 + SQR_CH >= LR) d[0] += xs[LR - 1] * x[LR - 1];
-                }
-            }
-            if (LS > 0) {
-                int t = (j > LR ? j : LR);
-                const double *xc = xsm + tid - LR * SQR_THREADS;
-                if ((t & 1) && t < L) { d[1] += xs[t] * xc[t * SQR_THREADS]; ++t; }  // (LR is even)
+            // the shared-memory rows [max(j, S0), SE)
+            auto smem_dot = [&]() {
+                int t = (j > S0 ? j : S0);
+                const double *xc = xsm + tid - S0 * SQR_THREADS;
+                if ((t & 1) && t < SE) { d[1] += xs[t] * xc[t * SQR_THREADS]; ++t; }  // (S0 is even)
                 // pairs of the reflector from one 16-byte broadcast load
-                for (; t + 3 < L; t += 4) {
+                for (; t + 3 < SE; t += 4) {
                     const double2 v01 = *reinterpret_cast<const double2 *>(&xs[t]);
                     const double2 v23 = *reinterpret_cast<const double2 *>(&xs[t + 2]);
                     d[0] += v01.x * xc[t * SQR_THREADS];
@@ -322,60 +323,77 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
                     d[2] += v23.x * xc[(t + 2) * SQR_THREADS];
                     d[3] += v23.y * xc[(t + 3) * SQR_THREADS];
                 }
-                for (; t < L; ++t) d[0] += xs[t] * xc[t * SQR_THREADS];
+                for (; t < SE; ++t) d[0] += xs[t] * xc[t * SQR_THREADS];
+            };
+            if (SMT && LS > 0) smem_dot();
+#pragma unroll
+            for (int c0 = 0; c0 < LR; c0 += SQR_CH) {
+                if (j < R0 + c0 + SQR_CH) {
+#pragma unroll
+                    for (int t = c0; t < c0 + SQR_CH && t + 1 < LR; t += 2) {
+                        const double2 v2 = *reinterpret_cast<const double2 *>(&xs[R0 + t]);
+                        d[(t >> 1) & 3] += v2.x * x[t] + v2.y * x[t + 1];
+                    }
+                    if ((LR & 1) && c0 + SQR_CH >= LR) d[0] += xs[R0 + LR - 1] * x[LR - 1];
+                }
             }
+            if (!SMT && LS > 0) smem_dot();
             const double tw = tau * ((d[0] + d[1]) + (d[2] + d[3]));
             // x -= tw v; bj = x(j) picked in the chunk that holds row j
             double bj = 0.0;
 #pragma unroll
             for (int c0 = 0; c0 < LR; c0 += SQR_CH) {
-                if (j < c0 + SQR_CH) {
+                if (j < R0 + c0 + SQR_CH) {
 #pragma unroll
                     for (int t = c0; t < c0 + SQR_CH && t + 1 < LR; t += 2) {
-                        const double2 v2 = *reinterpret_cast<const double2 *>(&xs[t]);
+                        const double2 v2 = *reinterpret_cast<const double2 *>(&xs[R0 + t]);
                         x[t] -= tw * v2.x;
                         x[t + 1] -= tw * v2.y;
                     }
-                    if ((LR & 1) && c0 + SQR_CH >= LR) x[LR - 1] -= tw * xs[LR - 1];
-                    if (j >= c0) {
+                    if ((LR & 1) && c0 + SQR_CH >= LR) x[LR - 1] -= tw * xs[R0 + LR - 1];
+                    if (j >= R0 + c0) {
 #pragma unroll
-                        for (int t = c0; t < c0 + SQR_CH && t < LR; ++t) bj = (t == j) ? x[t] : bj;
+                        for (int t = c0; t < c0 + SQR_CH && t < LR; ++t) bj = (R0 + t == j) ? x[t] : bj;
                     }
                 }
             }
-            {
-                int t = (j > LR ? j : LR);
-                if ((t & 1) && t < L) {
-                    double *q = &xsm[(t - LR) * SQR_THREADS + tid];
+            if (LS > 0) {
+                int t = (j > S0 ? j : S0);
+                if ((t & 1) && t < SE) {
+                    double *q = &xsm[(t - S0) * SQR_THREADS + tid];
                     const double nv = *q - tw * xs[t];
                     *q = nv;
                     ++t;
                 }
 #pragma unroll 2
-                for (; t + 1 < L; t += 2) {
+                for (; t + 1 < SE; t += 2) {
                     const double2 v01 = *reinterpret_cast<const double2 *>(&xs[t]);
-                    double *q = &xsm[(t - LR) * SQR_THREADS + tid];
+                    double *q = &xsm[(t - S0) * SQR_THREADS + tid];
                     const double n0 = q[0] - tw * v01.x;
                     const double n1 = q[SQR_THREADS] - tw * v01.y;
                     q[0] = n0;
                     q[SQR_THREADS] = n1;
                 }
-                for (; t < L; ++t) {
-                    double *q = &xsm[(t - LR) * SQR_THREADS + tid];
+                for (; t < SE; ++t) {
+                    double *q = &xsm[(t - S0) * SQR_THREADS + tid];
                     const double nv = *q - tw * xs[t];
                     *q = nv;
                 }
                 // the updated x(j), read back once instead of selected in the loop
-                if (j >= LR) bj = xsm[(j - LR) * SQR_THREADS + tid];
+                if (j >= S0 && j < SE) bj = xsm[(j - S0) * SQR_THREADS + tid];
             }
             double rn = r - bj * bj;
             if (rn < 1e-6 * r0) {  // recompute from the updated rows (R-G6)
                 double s0 = 0.0;
+                auto smem_ss = [&]() {
+                    for (int t = (j + 1 > S0 ? j + 1 : S0); t < SE; ++t)
+                        s0 += xsm[(t - S0) * SQR_THREADS + tid] * xsm[(t - S0) * SQR_THREADS + tid];
+                };
+                if (SMT) smem_ss();
 #pragma unroll
                 for (int t = 0; t < LR; ++t)
-                    if (t > j) s0 += x[t] * x[t];
-                for (int t = (j + 1 > LR ? j + 1 : LR); t < L; ++t)
-                    s0 += xsm[(t - LR) * SQR_THREADS + tid] * xsm[(t - LR) * SQR_THREADS + tid];
+                    if (R0 + t > j) s0 += x[t] * x[t];
+                if (!SMT) smem_ss();
                 rn = s0;
             }
             r = rn;
@@ -398,13 +416,13 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
     if (have && vec) {
         double2 *dst = reinterpret_cast<double2 *>(a.B + pc * a.ldb);
 #pragma unroll
-        for (int t = 0; t < LR; t += 2) dst[t / 2] = make_double2(x[t], x[t + 1]);
+        for (int t = 0; t < LR; t += 2) dst[(R0 + t) / 2] = make_double2(x[t], x[t + 1]);
         for (int t = 0; t < LS; t += 2)
-            dst[(LR + t) / 2] = make_double2(xsm[t * SQR_THREADS + tid], xsm[(t + 1) * SQR_THREADS + tid]);
+            dst[(S0 + t) / 2] = make_double2(xsm[t * SQR_THREADS + tid], xsm[(t + 1) * SQR_THREADS + tid]);
     } else if (have) {
 #pragma unroll
-        for (int t = 0; t < LR; ++t) a.B[t + pc * a.ldb] = x[t];
-        for (int t = 0; t < LS; ++t) a.B[(LR + t) + pc * a.ldb] = xsm[t * SQR_THREADS + tid];
+        for (int t = 0; t < LR; ++t) a.B[(R0 + t) + pc * a.ldb] = x[t];
+        for (int t = 0; t < LS; ++t) a.B[(S0 + t) + pc * a.ldb] = xsm[t * SQR_THREADS + tid];
     }
     if (g == 0) {
         for (int e = tid; e < j * a.lpad; e += SQR_THREADS) {

@@ -27,12 +27,18 @@ namespace rq {
 
 constexpr int SQR2_THREADS = 512;
 
-template <int LT, int LR, int LS>
+// SMT: the shared-memory rows directly below the global ones (rows
+// [LT, LT + LS)) and the register rows at the bottom, so the shared-memory
+// rows also drop out of the per-step traffic as the panel advances (as
+// sample_qrcp_reg_kernel's SMT layout).
+template <int LT, int LR, int LS, bool SMT = false>
 __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArgs a) {
     constexpr int TH = SQR2_THREADS;
     constexpr int NW = TH / 32;
     constexpr int L = LT + LR + LS;
-    constexpr int R0 = LT, S0 = LT + LR;  // first register row, first shared-memory row
+    constexpr int R0 = SMT ? LT + LS : LT;  // first register row
+    constexpr int S0 = SMT ? LT : LT + LR;  // first shared-memory row
+    constexpr int SE = S0 + LS;             // end of the shared-memory rows
     extern __shared__ __align__(16) double sq_dyn[];  // max(LS x TH, bb x L) doubles
     __shared__ __align__(16) double xs[L + 1];
     __shared__ __align__(16) double xraw[L + (L & 1)];
@@ -79,9 +85,12 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
     }
     double r = 0.0;
     for (int t = 0; t < LT; ++t) r += xt[t * TH] * xt[t * TH];  // (just written: from L1)
+    if (SMT)  // ascending rows
+        for (int t = 0; t < LS; ++t) r += xsm[t * TH + tid] * xsm[t * TH + tid];
 #pragma unroll
     for (int t = 0; t < LR; ++t) r += x[t] * x[t];
-    for (int t = 0; t < LS; ++t) r += xsm[t * TH + tid] * xsm[t * TH + tid];
+    if (!SMT)
+        for (int t = 0; t < LS; ++t) r += xsm[t * TH + tid] * xsm[t * TH + tid];
     double r0 = r;
     int lpos = (int)pc;
     bool act = have;
@@ -128,7 +137,7 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
             if (bc >= 0) {
                 const int oc = bc - (int)c_lo;
                 for (int t = lane; t < l; t += 32) {
-                    const double xv = (t < S0) ? xraw[t] : xsm[(t - S0) * TH + oc];
+                    const double xv = (t >= S0 && t < SE) ? xsm[(t - S0) * TH + oc] : xraw[t];
                     ll_store(dst + 2 + t, (unsigned long long)__double_as_longlong(xv), tg);
                 }
             }
@@ -291,6 +300,21 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
                 }
                 for (; t < LT; ++t) d[0] += xs[t] * __ldcg(&xt[t * TH]);
             }
+            auto smem_dot = [&]() {
+                int t = (j > S0 ? j : S0);
+                const double *xc = xsm + tid - S0 * TH;
+                if ((t & 1) && t < SE) { d[1] += xs[t] * xc[t * TH]; ++t; }  // (S0 is even)
+                for (; t + 3 < SE; t += 4) {
+                    const double2 v01 = *reinterpret_cast<const double2 *>(&xs[t]);
+                    const double2 v23 = *reinterpret_cast<const double2 *>(&xs[t + 2]);
+                    d[0] += v01.x * xc[t * TH];
+                    d[1] += v01.y * xc[(t + 1) * TH];
+                    d[2] += v23.x * xc[(t + 2) * TH];
+                    d[3] += v23.y * xc[(t + 3) * TH];
+                }
+                for (; t < SE; ++t) d[0] += xs[t] * xc[t * TH];
+            };
+            if (SMT && LS > 0) smem_dot();
 #pragma unroll
             for (int c0 = 0; c0 < LR; c0 += SQR_CH) {
                 if (j < R0 + c0 + SQR_CH) {
@@ -302,20 +326,7 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
                     if ((LR & 1) && c0 + SQR_CH >= LR) d[0] += xs[R0 + LR - 1] * x[LR - 1];
                 }
             }
-            if (LS > 0) {
-                int t = (j > S0 ? j : S0);
-                const double *xc = xsm + tid - S0 * TH;
-                if (t & 1) { d[1] += xs[t] * xc[t * TH]; ++t; }  // (S0 is even)
-                for (; t + 3 < L; t += 4) {
-                    const double2 v01 = *reinterpret_cast<const double2 *>(&xs[t]);
-                    const double2 v23 = *reinterpret_cast<const double2 *>(&xs[t + 2]);
-                    d[0] += v01.x * xc[t * TH];
-                    d[1] += v01.y * xc[(t + 1) * TH];
-                    d[2] += v23.x * xc[(t + 2) * TH];
-                    d[3] += v23.y * xc[(t + 3) * TH];
-                }
-                for (; t < L; ++t) d[0] += xs[t] * xc[t * TH];
-            }
+            if (!SMT && LS > 0) smem_dot();
             const double tw = tau * ((d[0] + d[1]) + (d[2] + d[3]));
             // x -= tw v; bj = x(j) from the range that holds row j
             double bj = 0.0;
@@ -354,16 +365,16 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
                     }
                 }
             }
-            {
+            if (LS > 0) {
                 int t = (j > S0 ? j : S0);
-                if (t & 1) {
+                if ((t & 1) && t < SE) {
                     double *q = &xsm[(t - S0) * TH + tid];
                     const double nv = *q - tw * xs[t];
                     *q = nv;
                     ++t;
                 }
 #pragma unroll 2
-                for (; t + 1 < L; t += 2) {
+                for (; t + 1 < SE; t += 2) {
                     const double2 v01 = *reinterpret_cast<const double2 *>(&xs[t]);
                     double *q = &xsm[(t - S0) * TH + tid];
                     const double n0 = q[0] - tw * v01.x;
@@ -371,22 +382,27 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
                     q[0] = n0;
                     q[TH] = n1;
                 }
-                for (; t < L; ++t) {
+                for (; t < SE; ++t) {
                     double *q = &xsm[(t - S0) * TH + tid];
                     const double nv = *q - tw * xs[t];
                     *q = nv;
                 }
                 // the updated x(j), read back once instead of selected in the loop
-                if (j >= S0) bj = xsm[(j - S0) * TH + tid];
+                if (j >= S0 && j < SE) bj = xsm[(j - S0) * TH + tid];
             }
             double rn = r - bj * bj;
             if (rn < 1e-6 * r0) {  // recompute from the updated rows (R-G6)
                 double s0 = 0.0;
                 for (int t = j + 1; t < LT; ++t) s0 += __ldcg(&xt[t * TH]) * __ldcg(&xt[t * TH]);
+                auto smem_ss = [&]() {
+                    for (int t = (j + 1 > S0 ? j + 1 : S0); t < SE; ++t)
+                        s0 += xsm[(t - S0) * TH + tid] * xsm[(t - S0) * TH + tid];
+                };
+                if (SMT) smem_ss();
 #pragma unroll
                 for (int t = 0; t < LR; ++t)
                     if (R0 + t > j) s0 += x[t] * x[t];
-                for (int t = (j + 1 > S0 ? j + 1 : S0); t < L; ++t) s0 += xsm[(t - S0) * TH + tid] * xsm[(t - S0) * TH + tid];
+                if (!SMT) smem_ss();
                 rn = s0;
             }
             r = rn;
