@@ -192,6 +192,10 @@ int rqrcp_factor_ex(rqrcp_ctx *ctx, double *A, int64_t lda, int64_t m, int64_t n
  *   sq_smtop      register-grid sample QRCP row layout (l = 144): 1 (default) the shared-memory
  *                 rows above the register rows (step j touches rows >= j only, so they drop out
  *                 of the per-step shared-memory traffic), 0 below them
+ *   sq_spec       register-grid sample QRCP exchange: 0 (default) fetch the winner's column after
+ *                 every header has arrived; 1 fetch the column of the best candidate seen so far
+ *                 while the last headers arrive (the same winner; measured slower: the per-poll
+ *                 warp reduction delays the last header more than the column round trip saves)
  *   cqr_rg        CholeskyQR2 panel one-CTA factorizations: 1 (default) register grid, 0 shared
  *                 memory
  *   debug_sync    synchronise after every launch

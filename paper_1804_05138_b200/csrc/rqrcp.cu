@@ -63,6 +63,8 @@ struct Opts {
     int sq_wide = 1;         // register-grid sample QRCP on every SM for wide samples (0: the fewest CTAs; 2: always)
     int sq_smtop = 1;        // register-grid sample QRCP: shared-memory rows above the register rows (they drop out
                              // of the per-step traffic as the panel advances); 0: below
+    int sq_spec = 0;         // register-grid sample QRCP: 1 fetch the best arrived candidate's column while the
+                             // last headers arrive (measured slower: C4 S2 51.0 vs 46.8 ms), 0 after every header
     int cqr_rg = 1;          // CholeskyQR2 panel: 1 register-grid one-CTA factorizations (cqr_rg.cuh), 0 shared-memory
     int host_out = 0;        // rqrcp_factor_host output: 0 the whole factored A, 1 the factors only (columns
                              // 0..k-1 full height = V and R11, rows 0..k-1 of columns k..n-1 = R12; R22 not copied)
@@ -80,7 +82,7 @@ static const OptDesc kOpts[] = {{"schedule", -1, 2},     {"panel", 0, 2},     {"
                                 {"trace_panel", 1, 1 << 30}, {"nccl_timeout_ms", 1, (int64_t)1 << 40},
                                 {"upd_kernel", 0, 2}, {"pn_blocked", 0, 2},
                                 {"tournament", 0, 64}, {"gemm_ws", 0, 1}, {"host_out", 0, 1}, {"cqr_rg", 0, 1}, {"sq_wide", 0, 2},
-                                {"sq_smtop", 0, 1}};
+                                {"sq_smtop", 0, 1}, {"sq_spec", 0, 1}};
 static bool opt_set(Opts &o, const std::string &n, int64_t v) {
 #define OPT(field)                    \
     if (n == #field) {                \
@@ -89,7 +91,7 @@ static bool opt_set(Opts &o, const std::string &n, int64_t v) {
     }
     OPT(schedule) OPT(panel) OPT(pn_cluster) OPT(pn_cpt) OPT(pn_grid) OPT(pn_rows) OPT(la_panel_ctas)
     OPT(sq_cluster) OPT(sq_reg) OPT(sq_grid) OPT(sq_nsm) OPT(sq_hstride) OPT(sq_poll) OPT(debug_sync) OPT(trace)
-    OPT(trace_panel) OPT(nccl_timeout_ms) OPT(upd_kernel) OPT(pn_blocked) OPT(tournament) OPT(gemm_ws) OPT(host_out) OPT(cqr_rg) OPT(sq_wide) OPT(sq_smtop)
+    OPT(trace_panel) OPT(nccl_timeout_ms) OPT(upd_kernel) OPT(pn_blocked) OPT(tournament) OPT(gemm_ws) OPT(host_out) OPT(cqr_rg) OPT(sq_wide) OPT(sq_smtop) OPT(sq_spec)
 #undef OPT
     return false;
 }
@@ -1061,7 +1063,7 @@ static int sq_reg2_grid(int64_t np) { return 1 + (int)((np + SQR2_THREADS - 1) /
 // polls one header per CTA either way).  Decided from (np, SM count) only.
 static int sq_reg_launch_grid(const rqrcp_ctx *ctx, int64_t np, int threads) {
     const int base = 1 + (int)((np + threads - 1) / threads);
-    const int cap = std::min(ctx->num_sms, SQ_MAXG);
+    const int cap = std::min(ctx->num_sms, SQR_MAXG);
     if (ctx->opt.sq_wide && base <= cap && (np >= (int64_t)64 * cap || ctx->opt.sq_wide == 2)) return cap;
     return base;
 }
@@ -1070,7 +1072,7 @@ static SqKind sq_kind(const rqrcp_ctx *ctx, int l, int64_t np) {
     const int64_t need = (np + SQC_THREADS - 1) / SQC_THREADS;
     if (ctx->opt.sq_cluster && k.cluster && need <= ctx->sqc_max) return SQK_CLUSTER;
     const int grid = 1 + (int)((np + SQR_THREADS - 1) / SQR_THREADS);
-    const int cap = std::min(ctx->num_sms, SQ_MAXG);
+    const int cap = std::min(ctx->num_sms, SQR_MAXG);  // (register grids; the generic kernel takes SQ_MAXG)
     if (ctx->opt.sq_reg == 1 && k.reg && grid <= cap) return SQK_REG;
     // wider samples: the 512-thread register grid (top rows in the spill scratch)
     if (ctx->opt.sq_reg && k.reg2 && sq_reg2_grid(np) <= cap &&
@@ -1160,6 +1162,7 @@ struct Run {
         a.swap_np = ctx->swap_np;
         a.trace = nullptr;
         a.spill = ctx->sq_spill;
+        a.spec = ctx->opt.sq_spec;
         return a;
     }
     // one sample QRCP launch (bb steps of Alg. 1 on the nn columns of a.B),

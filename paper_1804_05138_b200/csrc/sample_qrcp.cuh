@@ -92,6 +92,8 @@ struct SqArgs {
     int poll_mode;        // 0: acquire polls; 1: relaxed polls + one acquire fence; 2: 1 + nanosleep backoff;
                           // 3: tagged 16-byte units (ll), no release / acquire fence on either side
     unsigned long long *trace;  // debug: [G][64 steps][4 phases] clock64 stamps, or nullptr
+    int spec;             // register grids: fetch the column of the best candidate seen so far while
+                          // the last headers are still arriving (0: only after every header)
 };
 
 RQ_DEV bool sq_better(double v, int pos, double bv, int bpos) { return (v > bv) || (v == bv && pos < bpos); }

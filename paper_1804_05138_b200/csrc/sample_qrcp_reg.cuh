@@ -30,12 +30,104 @@ namespace rq {
 constexpr int SQR_THREADS = 256;
 constexpr int SQR_CH = 16;  // rows per skipped chunk of the register rows (as SQC_CH)
 constexpr int SQR_UNITS = SQ_MAXL + 2;  // 16-byte units per slot: header (2) + column
+constexpr int SQR_MAXG = 160;  // register-grid CTAs (headers polled by one warp: 5 per lane)
 
 // SMT (shared-memory top): rows [0, LS) in shared memory, rows [LS, L) in
 // registers.  Step j touches rows >= j only, so with the shared-memory rows on
 // top they drop out of the per-step shared-memory traffic as the panel
 // advances (l = 144, bb = 128: 2628 instead of 7676 row-steps per panel);
 // the register rows cost no shared-memory bandwidth wherever they sit.
+// The per-step exchange of the register grids, run by warp 0 of every CTA:
+// poll the G candidate headers of step `want` (tagged units, no fences), pick
+// the winner (largest norm, lowest position on ties, R-G5), and fetch its
+// column.  With spec != 0 the column of the best candidate among the headers
+// that have arrived is fetched while the others are still being polled (the
+// same winner: sq_better is a total order).  Measured slower (C4 S2 51.0 vs
+// 46.8 ms): the warp reduction in every poll round delays the detection of
+// the last header by more than the column's L2 round trip it saves.  Five
+// headers per lane (G <= 160) instead of eight: C4 S2 50.6 -> 46.8 ms.
+struct SqWin {
+    double v;
+    int p, sl, wc;
+    bool stop;
+};
+RQ_DEV SqWin sq_exchange(const uint4 *slots, int G, unsigned want, int l, double stop2, int spec, int lane,
+                         double (&xv)[SQ_RPL]) {
+    constexpr int HPL = SQR_MAXG / 32;
+    bool ready[HPL];
+    unsigned long long h0[HPL], h1[HPL];
+#pragma unroll
+    for (int u = 0; u < HPL; ++u) { ready[u] = (lane + 32 * u >= G); h0[u] = 0; h1[u] = 0; }
+    bool ok[SQ_RPL];
+#pragma unroll
+    for (int qq = 0; qq < SQ_RPL; ++qq) { ok[qq] = true; xv[qq] = 0.0; }
+    int csl = -1;  // slot whose column is being fetched
+    SqWin w;
+    while (true) {
+        bool all = true;
+#pragma unroll
+        for (int u = 0; u < HPL; ++u) {
+            if (!ready[u]) {
+                const uint4 *hq = slots + (int64_t)(lane + 32 * u) * SQR_UNITS;
+                const bool r0_ = ll_load(hq, want, h0[u]);
+                const bool r1_ = ll_load(hq + 1, want, h1[u]);
+                ready[u] = r0_ && r1_;
+            }
+            all = all && ready[u];
+        }
+        const bool allh = __all_sync(0xffffffffu, all);
+        if (!allh && !spec) continue;
+        // best among the headers that have arrived
+        double v = -1.0;
+        int p = INT_MAX, sl = -1, wc = -1;
+#pragma unroll
+        for (int u = 0; u < HPL; ++u) {
+            const int q = lane + 32 * u;
+            const double hv = __longlong_as_double((long long)h0[u]);
+            const int hp = (int)(unsigned)(h1[u] & 0xffffffffull);
+            if (ready[u] && q < G && hp != INT_MAX && sq_better(hv, hp, v, p)) {
+                v = hv; p = hp; sl = q; wc = (int)(unsigned)(h1[u] >> 32);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int op = __shfl_xor_sync(0xffffffffu, p, o);
+            const int osl = __shfl_xor_sync(0xffffffffu, sl, o);
+            const int owc = __shfl_xor_sync(0xffffffffu, wc, o);
+            if (osl >= 0 && (sl < 0 || sq_better(ov, op, v, p))) { v = ov; p = op; sl = osl; wc = owc; }
+        }
+        const bool stop = allh && ((sl < 0) || !(v > stop2));
+        if (allh && stop) {
+            w = SqWin{v, p, sl, wc, true};
+            break;
+        }
+        if (sl >= 0 && sl != csl) {  // (re)start the column fetch
+            csl = sl;
+#pragma unroll
+            for (int qq = 0; qq < SQ_RPL; ++qq) ok[qq] = lane + 32 * qq >= l;
+        }
+        bool cdone = true;
+        if (csl >= 0) {
+            const uint4 *src = slots + (int64_t)csl * SQR_UNITS + 2;
+#pragma unroll
+            for (int qq = 0; qq < SQ_RPL; ++qq) {
+                if (!ok[qq]) {
+                    unsigned long long x;
+                    ok[qq] = ll_load(src + lane + 32 * qq, want, x);
+                    xv[qq] = __longlong_as_double((long long)x);
+                }
+                cdone = cdone && ok[qq];
+            }
+        }
+        if (allh && __all_sync(0xffffffffu, cdone)) {  // csl == sl here
+            w = SqWin{v, p, sl, wc, false};
+            break;
+        }
+    }
+    return w;
+}
+
 template <int LR, int LS, bool SMT = false>
 __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs a) {
     constexpr int L = LR + LS;
@@ -170,72 +262,14 @@ __global__ void __launch_bounds__(SQR_THREADS, 1) sample_qrcp_reg_kernel(SqArgs 
         // ---- 1. winner and its reflector (warp 0, redundantly per CTA) --------
         if (warp == 0) {
             const unsigned want = a.tag0 + (unsigned)j;
-            constexpr int HPL = SQ_MAXG / 32;
             const uint4 *slots = a.ll + (int64_t)(par * G) * SQR_UNITS;
-            double v = -1.0;
-            int p = INT_MAX, sl = -1, wc = -1;
-            bool ready[HPL];
-            unsigned long long h0[HPL], h1[HPL];
-#pragma unroll
-            for (int u = 0; u < HPL; ++u) { ready[u] = (lane + 32 * u >= G); h0[u] = 0; h1[u] = 0; }
-            while (true) {
-                bool all = true;
-#pragma unroll
-                for (int u = 0; u < HPL; ++u) {
-                    if (!ready[u]) {
-                        const uint4 *hq = slots + (int64_t)(lane + 32 * u) * SQR_UNITS;
-                        const bool r0_ = ll_load(hq, want, h0[u]);
-                        const bool r1_ = ll_load(hq + 1, want, h1[u]);
-                        ready[u] = r0_ && r1_;
-                    }
-                    all = all && ready[u];
-                }
-                if (__all_sync(0xffffffffu, all)) break;
-            }
-#if SQR_TRACE_DETAIL
-            stamp(1);
-#endif
-#pragma unroll
-            for (int u = 0; u < HPL; ++u) {
-                const int q = lane + 32 * u;
-                const double hv = __longlong_as_double((long long)h0[u]);
-                const int hp = (int)(unsigned)(h1[u] & 0xffffffffull);
-                if (q < G && hp != INT_MAX && sq_better(hv, hp, v, p)) {
-                    v = hv; p = hp; sl = q; wc = (int)(unsigned)(h1[u] >> 32);
-                }
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-                const int op = __shfl_xor_sync(0xffffffffu, p, o);
-                const int osl = __shfl_xor_sync(0xffffffffu, sl, o);
-                const int owc = __shfl_xor_sync(0xffffffffu, wc, o);
-                if (osl >= 0 && (sl < 0 || sq_better(ov, op, v, p))) { v = ov; p = op; sl = osl; wc = owc; }
-            }
-            const bool stop = (sl < 0) || !(v > stop2);
             double xv[SQ_RPL];
-            {
-                const uint4 *src = slots + (int64_t)(sl >= 0 ? sl : 0) * SQR_UNITS + 2;
-                bool ok[SQ_RPL];
-#pragma unroll
-                for (int qq = 0; qq < SQ_RPL; ++qq) { ok[qq] = stop || lane + 32 * qq >= l; xv[qq] = 0.0; }
-                while (true) {
-                    bool all = true;
-#pragma unroll
-                    for (int qq = 0; qq < SQ_RPL; ++qq) {
-                        if (!ok[qq]) {
-                            unsigned long long w;
-                            ok[qq] = ll_load(src + lane + 32 * qq, want, w);
-                            xv[qq] = __longlong_as_double((long long)w);
-                        }
-                        all = all && ok[qq];
-                    }
-                    if (__all_sync(0xffffffffu, all)) break;
-                }
+            const SqWin win = sq_exchange(slots, G, want, l, stop2, a.spec, lane, xv);
+            const bool stop = win.stop;
+            const int p = win.p, wc = win.wc;
 #if SQR_TRACE_DETAIL
-                stamp(2);
+            stamp(2);
 #endif
-            }
             if (lane == 0) { s_stop = stop; s_wpos = p; s_wcol = wc; }
             if (!stop) {
                 double sx = 0.0;

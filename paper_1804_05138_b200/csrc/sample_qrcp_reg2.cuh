@@ -160,66 +160,11 @@ __global__ void __launch_bounds__(SQR2_THREADS, 1) sample_qrcp_reg2_kernel(SqArg
         // ---- 1. winner and its reflector (warp 0, redundantly per CTA) --------
         if (warp == 0) {
             const unsigned want = a.tag0 + (unsigned)j;
-            constexpr int HPL = SQ_MAXG / 32;
             const uint4 *slots = a.ll + (int64_t)(par * G) * SQR_UNITS;
-            double v = -1.0;
-            int p = INT_MAX, sl = -1, wc = -1;
-            bool ready[HPL];
-            unsigned long long h0[HPL], h1[HPL];
-#pragma unroll
-            for (int u = 0; u < HPL; ++u) { ready[u] = (lane + 32 * u >= G); h0[u] = 0; h1[u] = 0; }
-            while (true) {
-                bool all = true;
-#pragma unroll
-                for (int u = 0; u < HPL; ++u) {
-                    if (!ready[u]) {
-                        const uint4 *hq = slots + (int64_t)(lane + 32 * u) * SQR_UNITS;
-                        const bool r0_ = ll_load(hq, want, h0[u]);
-                        const bool r1_ = ll_load(hq + 1, want, h1[u]);
-                        ready[u] = r0_ && r1_;
-                    }
-                    all = all && ready[u];
-                }
-                if (__all_sync(0xffffffffu, all)) break;
-            }
-#pragma unroll
-            for (int u = 0; u < HPL; ++u) {
-                const int q = lane + 32 * u;
-                const double hv = __longlong_as_double((long long)h0[u]);
-                const int hp = (int)(unsigned)(h1[u] & 0xffffffffull);
-                if (q < G && hp != INT_MAX && sq_better(hv, hp, v, p)) {
-                    v = hv; p = hp; sl = q; wc = (int)(unsigned)(h1[u] >> 32);
-                }
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-                const int op = __shfl_xor_sync(0xffffffffu, p, o);
-                const int osl = __shfl_xor_sync(0xffffffffu, sl, o);
-                const int owc = __shfl_xor_sync(0xffffffffu, wc, o);
-                if (osl >= 0 && (sl < 0 || sq_better(ov, op, v, p))) { v = ov; p = op; sl = osl; wc = owc; }
-            }
-            const bool stop = (sl < 0) || !(v > stop2);
             double xv[SQ_RPL];
-            {
-                const uint4 *src = slots + (int64_t)(sl >= 0 ? sl : 0) * SQR_UNITS + 2;
-                bool ok[SQ_RPL];
-#pragma unroll
-                for (int qq = 0; qq < SQ_RPL; ++qq) { ok[qq] = stop || lane + 32 * qq >= l; xv[qq] = 0.0; }
-                while (true) {
-                    bool all = true;
-#pragma unroll
-                    for (int qq = 0; qq < SQ_RPL; ++qq) {
-                        if (!ok[qq]) {
-                            unsigned long long w;
-                            ok[qq] = ll_load(src + lane + 32 * qq, want, w);
-                            xv[qq] = __longlong_as_double((long long)w);
-                        }
-                        all = all && ok[qq];
-                    }
-                    if (__all_sync(0xffffffffu, all)) break;
-                }
-            }
+            const SqWin win = sq_exchange(slots, G, want, l, stop2, a.spec, lane, xv);
+            const bool stop = win.stop;
+            const int p = win.p, wc = win.wc;
             if (lane == 0) { s_stop = stop; s_wpos = p; s_wcol = wc; }
             if (!stop) {
                 double sx = 0.0;

@@ -31,7 +31,7 @@ ELEM_RTOL = 1e-10
 RECON_TOL = 1e-13
 
 DEFAULT_OPTS = dict(schedule=-1, panel=2, upd_kernel=2, pn_blocked=1, tournament=0, gemm_ws=1, pn_cluster=1, pn_cpt=2, pn_grid=0, pn_rows=128, la_panel_ctas=48,
-                    sq_cluster=1, sq_reg=1, sq_grid=0, sq_nsm=-1, sq_hstride=8, sq_poll=3, cqr_rg=1, host_out=0, sq_wide=1, sq_smtop=1)
+                    sq_cluster=1, sq_reg=1, sq_grid=0, sq_nsm=-1, sq_hstride=8, sq_poll=3, cqr_rg=1, host_out=0, sq_wide=1, sq_smtop=1, sq_spec=0)
 
 
 @pytest.fixture(scope="module")
@@ -547,6 +547,21 @@ def test_sample_qrcp_register_grid_row_layouts(ctx, name, kind, m, n, k, b, p, s
         compare(A, g, o, k)
         gs.append(g)
     assert np.array_equal(gs[0]["jpvt"], gs[1]["jpvt"])
+
+
+@pytest.mark.parametrize("name,kind,m,n,k,b,p,seed", REG_CASES[:2] + REG_CASES[-2:],
+                         ids=[c[0] for c in REG_CASES[:2] + REG_CASES[-2:]])
+@pytest.mark.parametrize("sq_reg", [1, 2])
+def test_sample_qrcp_register_grid_speculative_exchange_bitwise(ctx, name, kind, m, n, k, b, p, seed, sq_reg):
+    """The speculative column fetch of the register grids' exchange (sq_spec = 1)
+    picks the same winner and reflector as fetching after every header: bitwise."""
+    A = inputs.make(kind, m, n, seed, rank=64).numpy()
+    gs = []
+    for spec in (0, 1):
+        with options(ctx, sq_cluster=0, sq_reg=sq_reg, sq_wide=2, sq_spec=spec):
+            gs.append(gpu_factor(ctx, A, k, b, p, seed))
+    for key in ("A", "jpvt", "tau"):
+        assert np.array_equal(gs[0][key], gs[1][key]), key
 
 
 # the 512-thread register grid with the top 60 rows in global memory
