@@ -7,7 +7,7 @@ oracle:
   the per-panel trace of all 16 panels (R-hat after S2, the Eq. (4) sample
   after S6) against the oracle's panel callback;
 * C4 (32768^2, k = 8192) and C5 (65536^2, k = 4096): the PREFIX oracle to
-  k' = 4 panels (C4) / 2 panels (C5) (the prefix property, pinned for the
+  k' = 512 = 4 panels at both (the prefix property, pinned for the
   oracle in test_oracle_pins.py::test_prefix_property: the first k' pivots
   and R rows do not depend on k): identical first k' pivots, R rows 0..k'-1
   element-wise matched by column id (later swaps only permute columns),
@@ -135,5 +135,5 @@ def test_C4_full_size():
 
 
 def test_C5_full_size():
-    r = _run("C5", prefix_panels=int(os.environ.get("RQRCP_TEST_C5_PANELS", "2")), nprobe=2)
+    r = _run("C5", prefix_panels=int(os.environ.get("RQRCP_TEST_C5_PANELS", "4")), nprobe=2)
     assert 0.0 < r < 1.0
